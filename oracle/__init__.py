@@ -1,0 +1,350 @@
+"""Plain CPU oracle for the SpMV hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package. The
+product path (``paper_1711_05487_b200``) never imports it and shares no code
+with it (no kernels, headers, helpers, tables or constants).
+
+Heavy loops live in ``oracle.c`` (fp64, no FMA, serial); the small pure
+functions (selection rule, analytic bounds, amortisation, harmonic mean) are
+written out here in Python. Every function cites the passage it follows:
+``P:n`` = reference PAPER.md line n, ``S:n`` = SPEC.md line n, ``SURVEY 8(x)``
+= the reading this build takes.
+
+Pins (tests/test_oracle_*.py, ``-m "not gpu"``) -- no function is
+"parity unpinned":
+  spmv            dense brute-force matvec, identity/diagonal exact, A e_j =
+                  column j exact, stencil A*1 closed forms, dyadic exactness
+                  vs Fraction arithmetic, scipy csr @ x, Neumaier self-check
+  power_iter      monotone nu_k (k>=1) for symmetric A, nu <= lambda_max closed
+                  form, nu -> lambda_max vs numpy eigvalsh on a small grid
+  shard_bounds    SPEC S:254-255 examples, linear-scan definition, coverage
+  tile_rows       linear-scan definition, ownership cover
+  merge_splits    binary-search split vs the sequential merge, path invariants
+  long_chunks     coverage / exact tiling of long rows
+  d16 encode/dec  SPEC S:134-136 widths, round trip, stencil gap closed forms
+  features        SPEC S:415 sd example, stencil closed forms
+  select          hand-evaluated rule table on the configs' closed-form features
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `make oracle` (or __graft_entry__.build())")
+        L = ctypes.CDLL(path)
+        vp = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        L.oracle_spmv.argtypes = [i64, vp, vp, vp, vp, vp]
+        L.oracle_spmv_rows.argtypes = [vp, vp, vp, vp, vp, i64, vp]
+        L.oracle_absrow_rows.argtypes = [vp, vp, vp, vp, vp, i64, vp]
+        L.oracle_spmv_neumaier.argtypes = [i64, vp, vp, vp, vp, vp]
+        L.oracle_spmv_omp.argtypes = [i64, vp, vp, vp, vp, vp, ctypes.c_int]
+        L.oracle_spmv_omp.restype = ctypes.c_int
+        L.oracle_power_iter.argtypes = [i64, vp, vp, vp, vp, ctypes.c_int, vp, vp, ctypes.c_int]
+        L.oracle_power_iter.restype = ctypes.c_int
+        L.oracle_shard_bounds.argtypes = [i64, vp, i64, i64, vp]
+        L.oracle_validate.argtypes = [i64, i64, vp, vp, _i64p]
+        L.oracle_validate.restype = ctypes.c_int
+        L.oracle_features.argtypes = [i64, vp, vp, i64, i64, vp]
+        L.oracle_tile_rows.argtypes = [i64, vp, i64, i64, vp]
+        L.oracle_merge_splits.argtypes = [i64, vp, i64, i64, i64, vp, vp]
+        L.oracle_long_chunks.argtypes = [i64, vp, i64, i64, vp, vp, vp]
+        L.oracle_long_chunks.restype = i64
+        L.oracle_d16_encode.argtypes = [i64, vp, vp, vp, vp, _i64p]
+        L.oracle_d16_encode.restype = ctypes.c_int
+        L.oracle_d16_decode.argtypes = [i64, vp, vp, vp, vp]
+        L.oracle_tile_anchor.argtypes = [vp, i64, i64, i64, vp]
+        _LIB = L
+    return _LIB
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _rp64(rowptr):
+    return np.ascontiguousarray(rowptr, dtype=np.int64)
+
+
+def _c32(colind):
+    return np.ascontiguousarray(colind, dtype=np.int32)
+
+
+def _f64(v):
+    return np.ascontiguousarray(v, dtype=np.float64)
+
+
+# --------------------------------------------------------------------------
+# SpMV (Fig. 2, accumulation reading SURVEY 8(c3) #1)
+# --------------------------------------------------------------------------
+def spmv(rowptr, colind, vals, x):
+    rp = _rp64(rowptr)
+    n = rp.size - 1
+    y = np.empty(n, np.float64)
+    ci, v, xx = _c32(colind), _f64(vals), _f64(x)
+    _lib().oracle_spmv(n, _p(rp), _p(ci), _p(v), _p(xx), _p(y))
+    return y
+
+
+def spmv_omp(rowptr, colind, vals, x, nthreads=0):
+    """Row-parallel form (P:708-711 static nnz-balanced partition); bitwise == spmv."""
+    rp = _rp64(rowptr)
+    n = rp.size - 1
+    y = np.empty(n, np.float64)
+    ci, v, xx = _c32(colind), _f64(vals), _f64(x)
+    used = _lib().oracle_spmv_omp(n, _p(rp), _p(ci), _p(v), _p(xx), _p(y), int(nthreads))
+    return y, used
+
+
+def spmv_rows(rowptr, colind, vals, x, rows):
+    rp, ci, v, xx = _rp64(rowptr), _c32(colind), _f64(vals), _f64(x)
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty(r.size, np.float64)
+    _lib().oracle_spmv_rows(_p(rp), _p(ci), _p(v), _p(xx), _p(r), r.size, _p(out))
+    return out
+
+
+def absrow(rowptr, colind, vals, x, rows=None):
+    """s_i = sum_j |a_ij x_j|, the right side of BJ.north_star's per-row bound."""
+    rp, ci, v, xx = _rp64(rowptr), _c32(colind), _f64(vals), _f64(x)
+    if rows is None:
+        m = rp.size - 1
+        out = np.empty(m, np.float64)
+        _lib().oracle_absrow_rows(_p(rp), _p(ci), _p(v), _p(xx), None, m, _p(out))
+    else:
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        out = np.empty(r.size, np.float64)
+        _lib().oracle_absrow_rows(_p(rp), _p(ci), _p(v), _p(xx), _p(r), r.size, _p(out))
+    return out
+
+
+def spmv_neumaier(rowptr, colind, vals, x):
+    rp = _rp64(rowptr)
+    n = rp.size - 1
+    y = np.empty(n, np.float64)
+    ci, v, xx = _c32(colind), _f64(vals), _f64(x)
+    _lib().oracle_spmv_neumaier(n, _p(rp), _p(ci), _p(v), _p(xx), _p(y))
+    return y
+
+
+def power_iter(rowptr, colind, vals, x0, K, nthreads=1):
+    """Iterated mode x <- Ax/||Ax|| (BJ.configs[5]). Returns (rc, x_K, nu[K])."""
+    rp = _rp64(rowptr)
+    n = rp.size - 1
+    ci, v, x = _c32(colind), _f64(vals), _f64(x0)
+    xo = np.empty(n, np.float64)
+    nu = np.zeros(K, np.float64)
+    rc = _lib().oracle_power_iter(n, _p(rp), _p(ci), _p(v), _p(x), int(K), _p(xo), _p(nu), int(nthreads))
+    return rc, xo, nu
+
+
+# --------------------------------------------------------------------------
+# Plan structures; bit-exact definitions
+# --------------------------------------------------------------------------
+def shard_bounds(rowptr, G):
+    rp = _rp64(rowptr)
+    b = np.empty(G + 1, np.int64)
+    _lib().oracle_shard_bounds(rp.size - 1, _p(rp), int(rp[-1]), int(G), _p(b))
+    return b
+
+
+VALIDATE_CODES = {0: "ok", 1: "rowptr[0] != 0", 2: "rowptr[n] != nnz", 3: "rowptr decreasing",
+                  4: "colind out of range", 5: "colind not strictly increasing in row"}
+
+
+def validate(n, nnz, rowptr, colind):
+    rp, ci = _rp64(rowptr), _c32(colind)
+    where = ctypes.c_int64(-1)
+    code = _lib().oracle_validate(int(n), int(nnz), _p(rp), _p(ci), ctypes.byref(where))
+    return code, where.value
+
+
+class _Feat(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in
+                ("n", "nnz", "nnz_min", "nnz_max", "n_empty", "n_long", "nnz_long", "n_short", "max_short")] + \
+               [(k, ctypes.c_uint64) for k in ("s1", "s2", "s1_short", "s2_short")] + \
+               [(k, ctypes.c_int64) for k in ("maxgap", "misses")] + \
+               [(k, ctypes.c_double) for k in ("nnz_avg", "nnz_sd", "avg_short", "sd_short")]
+
+
+def features(rowptr, colind, L_split=4096, line_elems=16):
+    """Theta(N) Table I features + counts for selection."""
+    rp, ci = _rp64(rowptr), _c32(colind)
+    f = _Feat()
+    _lib().oracle_features(rp.size - 1, _p(rp), _p(ci), int(L_split), int(line_elems), ctypes.byref(f))
+    return {k: getattr(f, k) for k, _ in _Feat._fields_}
+
+
+def tile_count(nnz, C):
+    return max(1, -(-int(nnz) // int(C)))
+
+
+def tile_rows(rowptr, C):
+    rp = _rp64(rowptr)
+    T = tile_count(rp[-1], C)
+    R = np.empty(T + 1, np.int64)
+    _lib().oracle_tile_rows(rp.size - 1, _p(rp), int(C), T, _p(R))
+    return R
+
+
+def merge_splits(rowptr, items):
+    rp = _rp64(rowptr)
+    n, nnz = rp.size - 1, int(rp[-1])
+    T = max(1, -(-(n + nnz) // int(items)))
+    si = np.empty(T + 1, np.int64)
+    sj = np.empty(T + 1, np.int64)
+    _lib().oracle_merge_splits(n, _p(rp), nnz, int(items), T, _p(si), _p(sj))
+    return si, sj
+
+
+def long_chunks(rowptr, L_split, C):
+    rp = _rp64(rowptr)
+    n = rp.size - 1
+    q = _lib().oracle_long_chunks(n, _p(rp), int(L_split), int(C), None, None, None)
+    crow, cb, ce = (np.empty(q, np.int64) for _ in range(3))
+    if q:
+        _lib().oracle_long_chunks(n, _p(rp), int(L_split), int(C), _p(crow), _p(cb), _p(ce))
+    return crow, cb, ce
+
+
+def d16_encode(rowptr, colind):
+    """Returns (width, maxgap, dcol u16[nnz] | None, head i32[n] | None)."""
+    rp, ci = _rp64(rowptr), _c32(colind)
+    n, nnz = rp.size - 1, int(rp[-1])
+    dcol = np.zeros(max(nnz, 1), np.uint16)
+    head = np.zeros(max(n, 1), np.int32)
+    mg = ctypes.c_int64(0)
+    w = _lib().oracle_d16_encode(n, _p(rp), _p(ci), _p(dcol), _p(head), ctypes.byref(mg))
+    if w == 0:
+        return 0, mg.value, None, None
+    return w, mg.value, dcol[:nnz], head[:n]
+
+
+def d16_decode(rowptr, dcol, head):
+    rp = _rp64(rowptr)
+    n, nnz = rp.size - 1, int(rp[-1])
+    out = np.empty(max(nnz, 1), np.int32)
+    _lib().oracle_d16_decode(n, _p(rp), _p(np.ascontiguousarray(dcol, np.uint16)),
+                             _p(np.ascontiguousarray(head, np.int32)), _p(out))
+    return out[:nnz]
+
+
+def tile_anchor(colind, C):
+    ci = _c32(colind)
+    T = tile_count(ci.size, C)
+    out = np.empty(T, np.int32)
+    _lib().oracle_tile_anchor(_p(ci), ci.size, int(C), T, _p(out))
+    return out
+
+
+# --------------------------------------------------------------------------
+# Analytic bounds (Sec. III-B) and methodology helpers
+# --------------------------------------------------------------------------
+def p_mb(nnz, n, bmax, rowptr_bytes=4, colind_bytes=4):
+    """P_MB = 2 NNZ / ((S_CSR + S_x + S_y)/B_max), S_CSR = 8NNZ + 4NNZ + 4(N+1)."""
+    s = 8 * nnz + colind_bytes * nnz + rowptr_bytes * (n + 1) + 16 * n
+    return 2.0 * nnz / (s / bmax)
+
+
+def p_peak(nnz, n, bmax):
+    """P_peak = 2 NNZ / ((S_values + S_x + S_y)/B_max)."""
+    return 2.0 * nnz / ((8 * nnz + 16 * n) / bmax)
+
+
+def algorithmic_bytes(n, nnz, rowptr_bytes):
+    """BJ.metric bytes: values + colind + rowptr + x + y, uncompressed CSR."""
+    return 8 * nnz + 4 * nnz + rowptr_bytes * (n + 1) + 8 * n + 8 * n
+
+
+def n_iters_min(t_pre, t_base, t_sel):
+    """N_iters,min = t_pre / (t_spmv - t'_spmv) (SPEC example S:627)."""
+    d = t_base - t_sel
+    return math.inf if d <= 0 else t_pre / d
+
+
+def harmonic_mean(rates):
+    """Paper methodology: runs summarised by the harmonic mean."""
+    return len(rates) / sum(1.0 / r for r in rates)
+
+
+# --------------------------------------------------------------------------
+# Selection (Table II). A pure function of the
+# features and device properties. Rule constants are readings.
+# --------------------------------------------------------------------------
+VARIANT_VECTOR, VARIANT_STREAM, VARIANT_MERGE, VARIANT_SPLIT = 1, 2, 3, 4
+CLASS_MB, CLASS_ML, CLASS_IMB, CLASS_CMP = 1, 2, 4, 8
+
+
+@dataclass
+class Selection:
+    variant: int
+    vs: int
+    d16: bool
+    xwin: bool
+    classes: int
+
+
+def _pow2ceil(v):
+    p = 1
+    while p < v:
+        p *= 2
+    return p
+
+
+def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty_frac=0.25):
+    """Feature-guided selection. f = features(..) dict.
+
+    IMB: skew (sd_s/avg_s > skew_sd or empty/N > empty_frac) ->
+    merge_path; else long rows (n_long > 0 and nnz_max > K_long*nnz_avg) ->
+    long_row_split. Regular rows -> cta_stream for avg_s <= 32, else
+    csr_vector (CMP analogue: lane group sized to the row, VS =
+    clamp(pow2ceil(avg_s), 2, 32)). MB: working set > L2/2 and
+    maxgap <= 65535 -> D16 colind (only with cta_stream). ML:
+    misses/nnz > 0.75 and x larger than L2/16 -> x persistence window when it
+    fits the access-policy window.
+    """
+    n, nnz = f["n"], f["nnz"]
+    avg_s = f["avg_short"]
+    sd_s = f["sd_short"]
+    ws = algorithmic_bytes(n, nnz, rowptr_bytes)
+    classes = 0
+    skew = n > 0 and ((avg_s > 0 and sd_s / avg_s > skew_sd) or f["n_empty"] > empty_frac * n)
+    longr = f["n_long"] > 0 and f["nnz_max"] > K_long * f["nnz_avg"]
+    if skew or longr:
+        classes |= CLASS_IMB
+    vs = min(32, max(2, _pow2ceil(int(math.ceil(avg_s))) if avg_s > 0 else 2))
+    if skew:
+        variant = VARIANT_MERGE
+    elif longr:
+        variant = VARIANT_SPLIT
+    elif avg_s <= 32:
+        variant = VARIANT_STREAM
+    else:
+        variant = VARIANT_VECTOR
+    if avg_s <= 4:
+        classes |= CLASS_CMP
+    mb = ws > l2_bytes // 2
+    if mb and not (classes & CLASS_IMB):
+        classes |= CLASS_MB
+    d16 = bool((classes & CLASS_MB) and variant == VARIANT_STREAM and f["maxgap"] <= 65535)
+    ml = nnz > 0 and f["misses"] > 0.75 * nnz and 8 * n > l2_bytes // 16
+    if ml:
+        classes |= CLASS_ML
+    xwin = bool(ml and 8 * n <= window_max)
+    return Selection(variant, vs, d16, xwin, classes)

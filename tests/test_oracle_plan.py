@@ -1,0 +1,273 @@
+"""Pins for the oracle's plan structures, features, selection and formulas (CPU)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synthgen as sg
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def rp_of(lens):
+    rp = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    return rp
+
+
+def random_rowptrs(count=60, seed=7):
+    g = np.random.default_rng(seed)
+    out = []
+    for t in range(count):
+        n = int(g.integers(1, 300))
+        kind = t % 4
+        if kind == 0:
+            lens = g.integers(0, 20, n)
+        elif kind == 1:
+            lens = g.choice([0, 0, 0, 1, 50], n)
+        elif kind == 2:
+            lens = np.minimum((g.pareto(1.1, n) * 4).astype(np.int64), 3000)
+        else:
+            lens = np.zeros(n, np.int64)
+        out.append(rp_of(lens))
+    return out
+
+
+# ---- partition -------------------------
+@pytest.mark.parametrize("ex", GOLD["partition"])
+def test_partition_spec_examples(ex):
+    assert oracle.shard_bounds(rp_of(ex["lengths"]), ex["G"]).tolist() == ex["bounds"]
+
+
+def test_partition_vs_linear_scan():
+    for rp in random_rowptrs():
+        n, nnz = rp.size - 1, int(rp[-1])
+        for G in (1, 2, 3, 8, 17):
+            b = oracle.shard_bounds(rp, G)
+            exp = [0] + [next((r for r in range(n + 1) if rp[r] >= -(-g * nnz // G)), n) for g in range(1, G)] + [n]
+            assert b.tolist() == exp
+            assert np.all(np.diff(b) >= 0)
+
+
+def test_tile_rows_vs_linear_scan_and_ownership():
+    for rp in random_rowptrs():
+        n, nnz = rp.size - 1, int(rp[-1])
+        for C in (1, 4, 16, 64):
+            R = oracle.tile_rows(rp, C)
+            T = oracle.tile_count(nnz, C)
+            assert R.size == T + 1 and R[0] == 0 and R[-1] == n
+            for k in range(1, T):
+                assert R[k] == next((r for r in range(n + 1) if rp[r] >= k * C), n)
+            # each row owned by exactly one tile, and its start lies in its tile window
+            for k in range(T - 1):
+                for r in range(R[k], R[k + 1]):
+                    assert k * C <= rp[r] < (k + 1) * C
+
+
+# ---- merge path ------------------------------------------------
+def split_binary_search(rp, d):
+    """The survey's binary-search split rule (a different algorithm from the oracle's merge)."""
+    n, nnz = rp.size - 1, int(rp[-1])
+    lo, hi = max(0, d - nnz), min(d, n)
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if rp[mid + 1] <= d - mid - 1:
+            lo = mid + 1
+        else:
+            hi = mid
+    return lo, d - lo
+
+
+def test_merge_splits_vs_binary_search_and_invariants():
+    for rp in random_rowptrs():
+        n, nnz = rp.size - 1, int(rp[-1])
+        for items in (1, 3, 7, 64):
+            si, sj = oracle.merge_splits(rp, items)
+            T = si.size - 1
+            assert si[0] == 0 and sj[0] == 0 and si[-1] == n and sj[-1] == nnz
+            for k in range(T + 1):
+                d = min(k * items, n + nnz)
+                assert (si[k], sj[k]) == split_binary_search(rp, d)
+                i, j = si[k], sj[k]
+                if i > 0 and j < nnz:
+                    assert rp[i] <= j  # A[i-1] <= B[j] (ties to A)
+                if i < n and j > 0:
+                    assert j - 1 < rp[i + 1]  # B[j-1] < A[i]
+
+
+# ---- long-row chunks -----------------------------------
+@pytest.mark.parametrize("ex", GOLD["decompose"])
+def test_decompose_examples_long_rows(ex):
+    crow, cb, ce = oracle.long_chunks(rp_of(ex["lengths"]), ex["threshold"], 4)
+    assert sorted(set(crow.tolist())) == ex["long_rows"]
+
+
+def test_long_chunks_cover_long_rows_exactly():
+    for rp in random_rowptrs():
+        lens = np.diff(rp)
+        for L, C in ((10, 4), (0, 1), (30, 64)):
+            crow, cb, ce = oracle.long_chunks(rp, L, C)
+            covered = []
+            for r, b, e in zip(crow, cb, ce):
+                assert rp[r] <= b < e <= rp[r + 1] and e - b <= C
+                covered.extend(range(b, e))
+            exp = [j for i in np.nonzero(lens > L)[0] for j in range(rp[i], rp[i + 1])]
+            assert covered == exp  # disjoint, ordered, complete (decomposition conservation S:149)
+
+
+# ---- D16 delta colind -------------------------
+def test_delta_width_spec_examples():
+    for ex in GOLD["delta_width"]:
+        if ex["rows"] == "banded bandwidth 3":
+            m = sg.small_suite(0)[-1][1]  # banded
+            w, mg, _, _ = oracle.d16_encode(m.rowptr, m.colind)
+            assert mg <= 2
+        else:
+            rows = ex["rows"]
+            rp = rp_of([len(r) for r in rows])
+            w, mg, _, _ = oracle.d16_encode(rp, np.concatenate([np.array(r, np.int32) for r in rows]))
+        assert w == ex["width"]
+
+
+@pytest.mark.parametrize("name,m", sg.small_suite(5))
+def test_d16_round_trip(name, m):
+    w, mg, dcol, head = oracle.d16_encode(m.rowptr, m.colind)
+    if w == 0:
+        assert mg > 65535
+        return
+    assert np.array_equal(oracle.d16_decode(m.rowptr, dcol, head), m.colind)
+    rp = m.rowptr.astype(np.int64)
+    empty = np.diff(rp) == 0
+    assert np.all(head[empty] == m.n)  # sentinel
+    assert np.all(dcol[rp[:-1][~empty]] == 0)  # placeholder delta at heads
+
+
+@pytest.mark.parametrize("n", [3, 5, 24])
+def test_stencil_maxgap_closed_forms(n):
+    m7 = sg.stencil(n, 7)
+    m27 = sg.stencil(n, 27)
+    assert oracle.d16_encode(m7.rowptr, m7.colind)[1] == n * n
+    assert oracle.d16_encode(m27.rowptr, m27.colind)[1] == n * n - n - 1
+    w, _, dcol, head = oracle.d16_encode(m7.rowptr, m7.colind)
+    assert np.array_equal(oracle.d16_decode(m7.rowptr, dcol, head), m7.colind)
+
+
+def test_config_widths():
+    # C2 (128^3): maxgap 128^2 = 16384 -> 16-bit; C5 (384^3): 384^2-384-1 = 147071 -> none
+    assert 128 * 128 <= 65535 < 384 * 384 - 384 - 1
+    m = sg.config(1)
+    assert oracle.d16_encode(m.rowptr, m.colind)[0] == 16
+
+
+def test_tile_anchor():
+    ci = np.arange(100, dtype=np.int32) * 3
+    assert oracle.tile_anchor(ci, 16).tolist() == (np.arange(0, 100, 16) * 3).tolist()
+
+
+# ---- features (Table I) -------------------------------------------
+def test_features_spec_example():
+    g = GOLD["features_sd"]
+    rp = rp_of(g["lengths"])
+    f = oracle.features(rp, np.array([0, 0, 1, 0, 1, 2], np.int32))
+    assert (f["nnz_min"], f["nnz_max"], f["nnz_avg"]) == (g["nnz_min"], g["nnz_max"], g["nnz_avg"])
+    assert abs(f["nnz_sd"] - math.sqrt(g["nnz_sd_sq_num"] / g["nnz_sd_sq_den"])) < 1e-15
+    r = GOLD["features_row"]
+    f = oracle.features(rp_of([4]), np.array(r["colind"], np.int32), line_elems=r["line_elems"])
+    assert f["misses"] == r["misses"] and f["maxgap"] == r["maxgap"]
+
+
+@pytest.mark.parametrize("n", [2, 3, 10])
+def test_features_stencil_closed_forms(n):
+    f = oracle.features(sg.stencil(n, 7).rowptr, sg.stencil(n, 7).colind)
+    N = n ** 3
+    assert f["nnz"] == 7 * N - 6 * n * n and f["nnz_min"] == 4 and f["nnz_max"] == (7 if n >= 3 else 4)
+    assert f["nnz_avg"] == f["nnz"] / N
+    # sd from the closed-form length histogram: lengths 7 - #boundary faces
+    i = np.arange(N)
+    lens = 7 - sum(((c == 0).astype(int) + (c == n - 1)) for c in (i % n, (i // n) % n, i // (n * n)))
+    assert abs(f["nnz_sd"] - lens.std()) < 1e-12
+    f27 = oracle.features(sg.stencil(n, 27).rowptr, sg.stencil(n, 27).colind)
+    assert f27["nnz"] == (3 * n - 2) ** 3 and f27["nnz_min"] == 8 and f27["nnz_max"] == (27 if n >= 3 else 8)
+
+
+def test_features_configs_small():
+    f1 = oracle.features(sg.config(1).rowptr, sg.config(1).colind)
+    assert f1["nnz_min"] == f1["nnz_max"] == 9 and f1["nnz_sd"] == 0.0
+    m4 = sg.config(4, small=True)
+    f4 = oracle.features(m4.rowptr, m4.colind)
+    assert f4["nnz_min"] == 15 and f4["nnz_max"] == 4500 and f4["n_long"] == 10 and f4["nnz_long"] == 45000
+
+
+# ---- validation ------------------------------------------
+@pytest.mark.parametrize("rp,ci,n,nnz,code,where", [
+    ([0, 1, 2], [0, 1], 2, 2, 0, -1),
+    ([1, 1, 2], [0, 1], 2, 2, 1, 0),
+    ([0, 1, 3], [0, 1], 2, 2, 2, 2),
+    ([0, 2, 1, 2], [0, 1], 3, 2, 3, 1),
+    ([0, 1, 2], [0, 2], 2, 2, 4, 1),
+    ([0, 1, 2], [-1, 0], 2, 2, 4, 0),
+    ([0, 2, 4], [0, 1, 1, 1], 2, 4, 5, 3),
+    ([0, 2, 4], [1, 0, 0, 1], 2, 4, 5, 1),
+    ([0, 0, 0], [], 2, 0, 0, -1),
+])
+def test_validate_hand_cases(rp, ci, n, nnz, code, where):
+    assert oracle.validate(n, nnz, np.array(rp), np.array(ci, np.int32)) == (code, where)
+
+
+# ---- selection (Table II) ---------------------------
+L2 = 126 * 2 ** 20
+WIN = 128 * 2 ** 20
+
+
+def test_select_rule_table_on_closed_form_features():
+    def feat(n, nnz, avg_s, sd_s, n_empty=0, n_long=0, nnz_max=0, maxgap=0, misses=0):
+        return dict(n=n, nnz=nnz, avg_short=avg_s, sd_short=sd_s, n_empty=n_empty, n_long=n_long,
+                    nnz_max=nnz_max, nnz_avg=nnz / n, maxgap=maxgap, misses=misses)
+    S = oracle
+    # C2: 7-pt 128^3 (closed forms above): regular, 217 MB > L2/2, maxgap 16384
+    s = S.select(feat(2097152, 14581760, 6.953125, 0.2148, maxgap=16384, misses=8323072), L2, WIN, 4)
+    assert (s.variant, s.d16, s.xwin) == (S.VARIANT_STREAM, True, False) and s.classes & S.CLASS_MB
+    # C5: 27-pt 384^3: regular, maxgap 147071 -> no D16
+    s = S.select(feat(56623104, 1520875000, 26.86, 0.5, maxgap=147071, misses=10 ** 8), L2, WIN, 8)
+    assert (s.variant, s.d16) == (S.VARIANT_STREAM, False)
+    # C1: 1.28 MB working set -> no MB, no D16
+    s = S.select(feat(10000, 90000, 9.0, 0.0, maxgap=9000, misses=80000), L2, WIN, 4)
+    assert (s.variant, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_STREAM, False, 0)
+    # C3-like: half the rows empty -> merge path, IMB
+    s = S.select(feat(4194304, 65244537, 12.8, 78.5, n_empty=2185429, n_long=1794, nnz_max=97958,
+                      maxgap=4165791, misses=56437921), L2, WIN, 4)
+    assert s.variant == S.VARIANT_MERGE and s.classes & S.CLASS_IMB and s.xwin and s.classes & S.CLASS_ML
+    # C4-like: long rows, regular short part -> split
+    s = S.select(feat(1000000, 34998500, 15.0, 0.0, n_long=100, nnz_max=200000, maxgap=900000,
+                      misses=34000000), L2, WIN, 4)
+    assert (s.variant, s.vs) == (S.VARIANT_SPLIT, 16) and s.classes & S.CLASS_IMB
+    # medium regular rows -> csr_vector with VS = pow2ceil(avg)
+    s = S.select(feat(100000, 4000000, 40.0, 2.0, maxgap=10), L2, WIN, 4)
+    assert (s.variant, s.vs) == (S.VARIANT_VECTOR, 32)
+
+
+# ---- formulas ----------------------------------------------------------------
+def test_bounds_spec_numbers():
+    b = GOLD["bounds"]
+    assert abs(oracle.p_mb(b["nnz"], b["n"], b["bmax"]) / b["p_mb"] - 1) < b["p_mb_rel_tol"]
+    assert oracle.p_peak(b["nnz"], b["n"], b["bmax"]) >= oracle.p_mb(b["nnz"], b["n"], b["bmax"])
+    # NNZ -> inf limit of P_peak / P_MB is 1.5
+    assert abs(oracle.p_peak(10 ** 12, 10, 1.0) / oracle.p_mb(10 ** 12, 10, 1.0) - 1.5) < 1e-9
+
+
+def test_amortization_and_harmonic_mean():
+    a = GOLD["amortization"]
+    assert round(oracle.n_iters_min(a["t_pre"], a["t_base"], a["t_sel"]), 9) == a["n_iters_min"]
+    assert oracle.n_iters_min(1.0, 0.005, 0.010) == math.inf
+    for h in GOLD["harmonic_mean"]:
+        assert abs(oracle.harmonic_mean(h["rates"]) - h["hm"]) < 1e-15
+
+
+def test_algorithmic_bytes_configs():
+    # C2 216,924,164 B; C4 439,982,004 B; C5 19,609,454,504 B
+    assert oracle.algorithmic_bytes(2097152, 14581760, 4) == 216924164
+    assert oracle.algorithmic_bytes(1000000, 34998500, 4) == 439982004
+    assert oracle.algorithmic_bytes(56623104, 1520875000, 8) == 19609454504
