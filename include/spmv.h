@@ -1,0 +1,227 @@
+/* spmv.h -- C ABI of the B200-native adaptive fp64 CSR SpMV library (libspmv.so).
+ *
+ * The method is Elafrou, Goumas, Koziris, arXiv 1711.05487 ("the paper";
+ * P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n). The library
+ * computes y = A*x for A in CSR (Sec. II, Fig. 2) after a cheap
+ * inspector that extracts Theta(N) features (Table I), builds
+ * nnz-balanced partitions (Sec. IV-A), optionally delta-encodes
+ * the column indices (MB class, Sec. III-E) and selects one of the
+ * optimisations of Table II re-designed for sm_100a.
+ *
+ * No C++ types, exceptions or torch types cross this boundary. Every call
+ * returns a status (or NULL) and never throws. Failing calls set a
+ * thread-local status/message readable with spmv_last_status()/_error().
+ *
+ * Conventions
+ *  - Ownership: plan-creation calls read the caller's arrays synchronously and
+ *    copy what they need; the caller keeps ownership and may free them on
+ *    return. Array pointers may be host (pageable or pinned) or device
+ *    memory of the plan's device; the library detects which.
+ *  - Failure leaves no plan: on error *out is NULL and nothing leaks.
+ *  - A plan is not reentrant (one call at a time per plan); distinct plans
+ *    are independent. All floating-point data is IEEE fp64.
+ *  - CSR invariants: rowptr[0] = 0, rowptr[n_rows] = nnz,
+ *    nondecreasing; 0 <= colind < n_cols and strictly increasing inside a
+ *    row (no duplicates). Empty rows are legal and give y_i = 0.0.
+ */
+#ifndef SPMV_H_
+#define SPMV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct spmv_plan_s* spmv_plan;
+
+typedef enum {
+  SPMV_OK = 0,
+  SPMV_E_ARG = -1,          /* null pointer, negative size, bad option, ngpus out of range */
+  SPMV_E_CSR = -2,          /* CSR invariant violated; spmv_last_error() names it and where */
+  SPMV_E_CUDA = -3,         /* CUDA runtime error (message carries cudaGetErrorString) */
+  SPMV_E_NCCL = -4,         /* reserved for the fused NVLink exchange */
+  SPMV_E_NOMEM = -5,        /* device or host allocation failed */
+  SPMV_E_UNSUPPORTED = -6,  /* n >= 2^31 (int32 colind) or nnz >= 2^31 with 32-bit rowptr */
+  SPMV_E_ZERO_NORM = -7     /* iterated mode hit ||y|| == 0 */
+} spmv_status;
+
+/* Kernel variants (Table II re-designed for sm_100a). */
+typedef enum {
+  SPMV_VARIANT_AUTO = 0,    /* feature-guided selection (P:492-521 reading) */
+  SPMV_VARIANT_VECTOR = 1,  /* csr_vector<VS>: VS lanes per row (CMP: unroll+vectorise) */
+  SPMV_VARIANT_STREAM = 2,  /* cta_stream: TMA-staged fixed nnz tiles (MB: vectorised streaming) */
+  SPMV_VARIANT_MERGE = 3,   /* merge_path: rows+nnz balanced (IMB "auto" schedule) */
+  SPMV_VARIANT_SPLIT = 4    /* long_row_split: short rows + chunked long rows (IMB decomposition, Fig. 7) */
+} spmv_variant;
+
+/* Bottleneck classes (Sec. III-A) recorded by the selection. */
+enum { SPMV_CLASS_MB = 1, SPMV_CLASS_ML = 2, SPMV_CLASS_IMB = 4, SPMV_CLASS_CMP = 8 };
+
+typedef struct spmv_options {
+  int32_t struct_size;     /* = sizeof(spmv_options); set by spmv_options_default */
+  int32_t force_variant;   /* spmv_variant; 0 = feature-guided selection */
+  int32_t force_vs;        /* lanes per row for VECTOR/STREAM/SPLIT reductions: 0 = auto, else 1,2,4,8,16,32 */
+  int32_t d16;             /* delta colind: -1 auto, 0 off, 1 on when encodable (STREAM only) */
+  int32_t xwin;            /* L2 persistence window on x (ML analogue of P:599-606): -1 auto, 0 off, 1 on */
+  int32_t validate;        /* 1 = check CSR invariants on the device (default), 0 = trust the input */
+  int64_t l_split;         /* long-row threshold in nnz (0 = 4096) */
+  int64_t k_long;          /* long rows trigger SPLIT when nnz_max > k_long * nnz_avg (0 = 100) */
+  int64_t tile_nnz;        /* STREAM tile size C in nonzeros (0 = 2048; multiple of 256) */
+  int64_t merge_items;     /* MERGE items (rows + nnz) per CTA (0 = 2048; multiple of 256) */
+  int64_t long_chunk;      /* SPLIT chunk size in nonzeros (0 = 8192; multiple of 256) */
+  int32_t emulate_devices; /* ngpus > 1: 1 = place every shard on the current device (tests) */
+  int32_t reserved[7];
+} spmv_options;
+
+/* Theta(N) features (Table I) + counts used by the selection.
+ * Integers are exact; nnz_sd = sqrt((double)(N*S2 - S1^2)) / N (128-bit difference). */
+typedef struct spmv_features {
+  int64_t n, nnz, nnz_min, nnz_max, n_empty, n_long, nnz_long, n_short, max_short;
+  uint64_t s1, s2, s1_short, s2_short;
+  int64_t maxgap;          /* max in-row column gap over non-head nonzeros (0 if none) */
+  int64_t misses;          /* non-head nonzeros with gap > 16 (Table I misses_i, 128-B line) */
+  double nnz_avg, nnz_sd, avg_short, sd_short;
+} spmv_features;
+
+typedef struct spmv_device_props {
+  int32_t sm_count;
+  int32_t cc_major, cc_minor;
+  int32_t pad_;
+  int64_t l2_bytes;              /* cudaDeviceProp::l2CacheSize */
+  int64_t persisting_l2_max;     /* cudaDeviceProp::persistingL2CacheMaxSize */
+  int64_t access_window_max;     /* cudaDeviceProp::accessPolicyMaxWindowSize */
+  int64_t global_mem_bytes;
+} spmv_device_props;
+
+typedef struct spmv_selection {
+  int32_t variant;   /* spmv_variant (never AUTO) */
+  int32_t vs;        /* lanes per row */
+  int32_t d16;       /* 1 when the delta-encoded colind stream is used */
+  int32_t xwin;      /* 1 when the x persistence window is set */
+  int32_t classes;   /* SPMV_CLASS_* bitmask */
+  int32_t pad_;
+} spmv_selection;
+
+typedef struct spmv_plan_info {
+  int64_t n_rows, n_cols, nnz;
+  int32_t rowptr_bytes, ngpus;
+  spmv_selection sel;
+  spmv_features feat;
+  int32_t d16_width;          /* 0, 8 or 16 (matrix-global, "never both") */
+  int32_t pad_;
+  int64_t tile_nnz, n_tiles;  /* STREAM tiling */
+  int64_t merge_items, n_merge_tiles;
+  int64_t l_split, long_chunk, n_long_chunks;
+  double upload_ms, inspect_ms, select_ms, encode_ms; /* plan-time breakdown */
+  int64_t device_bytes;       /* device memory held by the plan (all shards) */
+  int64_t shard_bounds[9];    /* b_0..b_G for G <= 8 (rows) */
+} spmv_plan_info;
+
+/* ---- plan lifecycle ---------------------------------------------------- */
+
+/* Fill *opt with defaults (auto selection, validation on). */
+void spmv_options_default(spmv_options* opt);
+
+/* Core call named by BJ.north_star. Square n x n matrix, int64 rowptr.
+ * ngpus >= 1 shards rows nnz-balanced over devices 0..ngpus-1 of this
+ * process (SURVEY 8(c2) bound rule) with x replicated.
+ * Returns NULL on failure (see spmv_last_status / spmv_last_error). */
+spmv_plan spmv_plan_create(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* colind,
+                           const double* values, int ngpus);
+
+/* Extended creation: rectangular row blocks (n_rows x n_cols, e.g. one rank's
+ * shard of a square matrix; colind are global column ids), rowptr of 4 or 8
+ * bytes per entry, options (nullable). *out = NULL on failure. */
+spmv_status spmv_plan_create_ex(spmv_plan* out, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                const void* rowptr, int rowptr_bytes, const int32_t* colind,
+                                const double* values, int ngpus, const spmv_options* opt);
+
+/* NULL-safe; frees device memory and streams of every shard. */
+void spmv_plan_destroy(spmv_plan p);
+
+/* ---- execution ----------------------------------------------------------- */
+
+/* y = A x (overwrite, Fig. 2 read as accumulation).
+ * x: n_cols doubles, y: n_rows doubles, host or device. Synchronous. */
+int spmv_execute(spmv_plan p, const double* x, double* y);
+
+/* Same, enqueued on the plan's stream of shard 0 without a host sync.
+ * Single-shard plans only; x and y must be device pointers of that device. */
+int spmv_execute_async(spmv_plan p, const double* x, double* y);
+
+/* As spmv_execute_async, restricted to one stage for per-kernel timing:
+ * stage 0 = the whole SpMV, 1 = the main kernel(s) only, 2 = the carry
+ * fix-up epilogue only (y is complete only after stages 1 and 2). */
+int spmv_execute_stage(spmv_plan p, const double* x, double* y, int stage);
+
+/* Iterated mode (BJ.configs[5]): x_0 = x0; for k < iters: y = A x_k,
+ * nu_k = ||y||_2, x_{k+1} = y / nu_k. Writes x_iters to x_out (host or
+ * device), nu_{iters-1} to *last_norm (nullable) and nu_0..nu_{iters-1} to
+ * nu_out (nullable, host). Square plans only. Synchronous. */
+spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters, double* last_norm,
+                         double* nu_out);
+
+/* Building blocks of the distributed iterated mode (one process per GPU;
+ * the exchange runs in the caller's NCCL process group). Single-shard
+ * plans, device pointers, enqueued on the plan stream:
+ *   spmv_norm_partials: partials[0..spmv_norm_partial_count()) = sums of
+ *     y_i^2 over fixed contiguous row chunks of y (n_rows entries).
+ *   spmv_normalize: nu = sqrt(sum_{q ascending} partials[q]) over `count`
+ *     partials (all ranks' partials in rank order), x_out[i] = y[i] / nu,
+ *     *nu_dev = nu. Every rank computes the identical nu. */
+int32_t spmv_norm_partial_count(void);
+int spmv_norm_partials(spmv_plan p, const double* y, double* partials);
+int spmv_normalize(spmv_plan p, const double* y, const double* partials, int count, double* x_out,
+                   double* nu_dev);
+
+/* ---- inspection ---------------------------------------------------------- */
+
+spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info);
+
+/* Plan-resident buffers and stream of shard g (the timed path: no copies
+ * when spmv_execute* receives these pointers). */
+double* spmv_plan_x_device(spmv_plan p, int g);
+double* spmv_plan_y_device(spmv_plan p, int g);
+void* spmv_plan_stream(spmv_plan p, int g);  /* a cudaStream_t */
+
+/* Copy a plan structure of shard g to host memory for bit-exact checks.
+ * Returns the number of elements (call with dst = NULL to size), or < 0. */
+enum {
+  SPMV_ARR_TILE_ROWS = 1,    /* int64[n_tiles+1]: R_k = lower_bound(rowptr, k*C) */
+  SPMV_ARR_MERGE_ROWS = 2,   /* int64[n_merge_tiles+1]: merge-path split i_k */
+  SPMV_ARR_MERGE_NNZ = 3,    /* int64[n_merge_tiles+1]: merge-path split j_k */
+  SPMV_ARR_CHUNK_ROW = 4,    /* int64[n_long_chunks] */
+  SPMV_ARR_CHUNK_BEGIN = 5,  /* int64[n_long_chunks] */
+  SPMV_ARR_CHUNK_END = 6,    /* int64[n_long_chunks] */
+  SPMV_ARR_DCOL = 7,         /* uint16[nnz] delta colind */
+  SPMV_ARR_HEAD = 8,         /* int32[n_rows] */
+  SPMV_ARR_ANCHOR = 9,       /* int32[n_tiles] */
+  SPMV_ARR_DECODED = 10,     /* int32[nnz] colind re-decoded on the device from dcol/head/anchor */
+  SPMV_ARR_SHARD_BOUNDS = 11 /* int64[ngpus+1] */
+};
+int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst);
+
+/* nnz-balanced contiguous row partition:
+ * b_0 = 0, b_G = n, b_g = min{ r : rowptr[r] >= ceil(g*nnz/G) }. Host
+ * arrays. Returns SPMV_OK or SPMV_E_ARG. */
+spmv_status spmv_shard_bounds(int64_t n, const void* rowptr, int rowptr_bytes, int G, int64_t* bounds);
+
+/* The feature-guided selection as a pure function (callable without a GPU). */
+spmv_status spmv_select(const spmv_features* f, const spmv_device_props* d, int rowptr_bytes,
+                        const spmv_options* opt, spmv_selection* out);
+
+/* Properties of device `dev` used by the selection (needs a GPU). */
+spmv_status spmv_device_query(int dev, spmv_device_props* out);
+
+/* ---- errors --------------------------------------------------------------- */
+spmv_status spmv_last_status(void);
+const char* spmv_last_error(void);
+
+/* Kernels launched by this library since load (all shards, all calls). */
+int64_t spmv_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMV_H_ */

@@ -1,0 +1,267 @@
+"""ctypes binding of include/spmv.h (same names as the C ABI, minus the prefix).
+
+Accepts numpy arrays (host) or torch tensors (host or CUDA) and passes their
+raw pointers; the library detects host vs device memory itself.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_PATH = os.path.join(_HERE, "libspmv.so")
+if not os.path.exists(_PATH):
+    raise ImportError(f"{_PATH} is missing: build it with `make spmv` or __graft_entry__.build() "
+                      "(there is no CPU fallback)")
+lib = ctypes.CDLL(_PATH)
+
+VARIANTS = {"auto": 0, "vector": 1, "stream": 2, "merge": 3, "split": 4}
+VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
+CLASSES = {"MB": 1, "ML": 2, "IMB": 4, "CMP": 8}
+ARR = {"tile_rows": 1, "merge_rows": 2, "merge_nnz": 3, "chunk_row": 4, "chunk_begin": 5, "chunk_end": 6,
+       "dcol": 7, "head": 8, "anchor": 9, "decoded": 10, "shard_bounds": 11}
+_ARR_DTYPE = {1: np.int64, 2: np.int64, 3: np.int64, 4: np.int64, 5: np.int64, 6: np.int64, 7: np.uint16,
+              8: np.int32, 9: np.int32, 10: np.int32, 11: np.int64}
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_int32), ("force_variant", ctypes.c_int32), ("force_vs", ctypes.c_int32),
+                ("d16", ctypes.c_int32), ("xwin", ctypes.c_int32), ("validate", ctypes.c_int32),
+                ("l_split", ctypes.c_int64), ("k_long", ctypes.c_int64), ("tile_nnz", ctypes.c_int64),
+                ("merge_items", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
+                ("emulate_devices", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+    @classmethod
+    def make(cls, **kw):
+        o = cls()
+        lib.spmv_options_default(ctypes.byref(o))
+        for k, v in kw.items():
+            if k == "force_variant" and isinstance(v, str):
+                v = VARIANTS[v]
+            setattr(o, k, v)
+        return o
+
+
+class Features(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in
+                ("n", "nnz", "nnz_min", "nnz_max", "n_empty", "n_long", "nnz_long", "n_short", "max_short")] + \
+               [(k, ctypes.c_uint64) for k in ("s1", "s2", "s1_short", "s2_short")] + \
+               [(k, ctypes.c_int64) for k in ("maxgap", "misses")] + \
+               [(k, ctypes.c_double) for k in ("nnz_avg", "nnz_sd", "avg_short", "sd_short")]
+
+
+class DeviceProps(ctypes.Structure):
+    _fields_ = [("sm_count", ctypes.c_int32), ("cc_major", ctypes.c_int32), ("cc_minor", ctypes.c_int32),
+                ("pad_", ctypes.c_int32), ("l2_bytes", ctypes.c_int64), ("persisting_l2_max", ctypes.c_int64),
+                ("access_window_max", ctypes.c_int64), ("global_mem_bytes", ctypes.c_int64)]
+
+
+class Selection(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int32), ("vs", ctypes.c_int32), ("d16", ctypes.c_int32),
+                ("xwin", ctypes.c_int32), ("classes", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("rowptr_bytes", ctypes.c_int32), ("ngpus", ctypes.c_int32), ("sel", Selection),
+                ("feat", Features), ("d16_width", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("tile_nnz", ctypes.c_int64), ("n_tiles", ctypes.c_int64), ("merge_items", ctypes.c_int64),
+                ("n_merge_tiles", ctypes.c_int64), ("l_split", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
+                ("n_long_chunks", ctypes.c_int64), ("upload_ms", ctypes.c_double), ("inspect_ms", ctypes.c_double),
+                ("select_ms", ctypes.c_double), ("encode_ms", ctypes.c_double), ("device_bytes", ctypes.c_int64),
+                ("shard_bounds", ctypes.c_int64 * 9)]
+
+
+_vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+lib.spmv_options_default.argtypes = [ctypes.POINTER(Options)]
+lib.spmv_plan_create.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int]
+lib.spmv_plan_create.restype = _vp
+lib.spmv_plan_create_ex.argtypes = [ctypes.POINTER(_vp), _i64, _i64, _i64, _vp, ctypes.c_int, _vp, _vp, ctypes.c_int,
+                                    ctypes.POINTER(Options)]
+lib.spmv_plan_destroy.argtypes = [_vp]
+lib.spmv_execute.argtypes = [_vp, _vp, _vp]
+lib.spmv_execute_async.argtypes = [_vp, _vp, _vp]
+lib.spmv_execute_stage.argtypes = [_vp, _vp, _vp, ctypes.c_int]
+lib.spmv_iterate.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.POINTER(_d), _vp]
+lib.spmv_norm_partial_count.restype = _i32
+lib.spmv_norm_partials.argtypes = [_vp, _vp, _vp]
+lib.spmv_normalize.argtypes = [_vp, _vp, _vp, ctypes.c_int, _vp, _vp]
+lib.spmv_plan_query.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
+lib.spmv_plan_x_device.argtypes = [_vp, ctypes.c_int]
+lib.spmv_plan_x_device.restype = _vp
+lib.spmv_plan_y_device.argtypes = [_vp, ctypes.c_int]
+lib.spmv_plan_y_device.restype = _vp
+lib.spmv_plan_stream.argtypes = [_vp, ctypes.c_int]
+lib.spmv_plan_stream.restype = _vp
+lib.spmv_plan_export.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp]
+lib.spmv_plan_export.restype = _i64
+lib.spmv_shard_bounds.argtypes = [_i64, _vp, ctypes.c_int, ctypes.c_int, _vp]
+lib.spmv_select.argtypes = [ctypes.POINTER(Features), ctypes.POINTER(DeviceProps), ctypes.c_int,
+                            ctypes.POINTER(Options), ctypes.POINTER(Selection)]
+lib.spmv_device_query.argtypes = [ctypes.c_int, ctypes.POINTER(DeviceProps)]
+lib.spmv_last_error.restype = ctypes.c_char_p
+lib.spmv_kernel_launches.restype = _i64
+
+
+class SpmvError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"spmv status {status}: {msg}")
+        self.status = status
+        self.msg = msg
+
+
+def _check(rc):
+    if rc != 0:
+        raise SpmvError(int(rc), lib.spmv_last_error().decode())
+    return rc
+
+
+def _ptr(a):
+    """Raw pointer of a numpy array or torch tensor (contiguity is the caller's job)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"], "array must be contiguous"
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        assert a.is_contiguous(), "tensor must be contiguous"
+        return a.data_ptr()
+    if isinstance(a, int):
+        return a
+    raise TypeError(type(a))
+
+
+def _elem_bytes(a):
+    if isinstance(a, np.ndarray):
+        return a.dtype.itemsize
+    return a.element_size()
+
+
+def _numel(a):
+    return a.size if isinstance(a, np.ndarray) else a.numel()
+
+
+def kernel_launches() -> int:
+    return int(lib.spmv_kernel_launches())
+
+
+def norm_partial_count() -> int:
+    return int(lib.spmv_norm_partial_count())
+
+
+def shard_bounds(rowptr: np.ndarray, G: int) -> np.ndarray:
+    rp = np.ascontiguousarray(rowptr)
+    out = np.empty(G + 1, np.int64)
+    _check(lib.spmv_shard_bounds(rp.size - 1, rp.ctypes.data, rp.dtype.itemsize, G, out.ctypes.data))
+    return out
+
+
+def select(features: dict, props: dict, rowptr_bytes: int, **opts) -> dict:
+    f = Features(**{k: features[k] for k, _ in Features._fields_})
+    d = DeviceProps(**{k: props.get(k, 0) for k, _ in DeviceProps._fields_})
+    o = Options.make(**opts)
+    s = Selection()
+    _check(lib.spmv_select(ctypes.byref(f), ctypes.byref(d), rowptr_bytes, ctypes.byref(o), ctypes.byref(s)))
+    return {k: getattr(s, k) for k, _ in Selection._fields_ if k != "pad_"}
+
+
+def device_query(dev: int = 0) -> dict:
+    d = DeviceProps()
+    _check(lib.spmv_device_query(dev, ctypes.byref(d)))
+    return {k: getattr(d, k) for k, _ in DeviceProps._fields_ if k != "pad_"}
+
+
+class Plan:
+    """spmv_plan_create_ex + execute/iterate/query/export/destroy."""
+
+    def __init__(self, rowptr, colind, values, n_cols=None, ngpus=1, **opts):
+        n_rows = _numel(rowptr) - 1
+        nnz = _numel(colind)
+        self._h = _vp()
+        self.options = Options.make(**opts)
+        # keep references alive for the duration of the (synchronous) create
+        self._keep = (rowptr, colind, values)
+        _check(lib.spmv_plan_create_ex(ctypes.byref(self._h), n_rows, n_rows if n_cols is None else n_cols, nnz,
+                                       _ptr(rowptr), _elem_bytes(rowptr), _ptr(colind), _ptr(values), ngpus,
+                                       ctypes.byref(self.options)))
+        self._keep = None
+        self.n_rows = n_rows
+        self.n_cols = n_rows if n_cols is None else n_cols
+        self.nnz = nnz
+
+    @property
+    def handle(self):
+        return self._h.value
+
+    def destroy(self):
+        if self._h and self._h.value:
+            lib.spmv_plan_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def execute(self, x, y=None):
+        if y is None:
+            y = np.empty(self.n_rows, np.float64)
+        _check(lib.spmv_execute(self._h, _ptr(x), _ptr(y)))
+        return y
+
+    def execute_async(self, x, y):
+        _check(lib.spmv_execute_async(self._h, _ptr(x), _ptr(y)))
+
+    def execute_stage(self, x, y, stage):
+        _check(lib.spmv_execute_stage(self._h, _ptr(x), _ptr(y), int(stage)))
+
+    def iterate(self, x0, iters, x_out=None):
+        if x_out is None:
+            x_out = np.empty(self.n_cols, np.float64)
+        nu = np.zeros(iters, np.float64)
+        last = ctypes.c_double(0.0)
+        rc = lib.spmv_iterate(self._h, _ptr(x0), _ptr(x_out), int(iters), ctypes.byref(last), nu.ctypes.data)
+        if rc != 0:
+            raise SpmvError(int(rc), lib.spmv_last_error().decode())
+        return x_out, nu
+
+    def norm_partials(self, y, partials):
+        _check(lib.spmv_norm_partials(self._h, _ptr(y), _ptr(partials)))
+
+    def normalize(self, y, partials, count, x_out, nu_dev):
+        _check(lib.spmv_normalize(self._h, _ptr(y), _ptr(partials), int(count), _ptr(x_out), _ptr(nu_dev)))
+
+    def info(self) -> dict:
+        i = PlanInfo()
+        _check(lib.spmv_plan_query(self._h, ctypes.byref(i)))
+        d = {k: getattr(i, k) for k, _ in PlanInfo._fields_ if k not in ("sel", "feat", "pad_", "shard_bounds")}
+        d["sel"] = {k: getattr(i.sel, k) for k, _ in Selection._fields_ if k != "pad_"}
+        d["variant"] = VARIANT_NAMES[i.sel.variant]
+        d["classes"] = [k for k, v in CLASSES.items() if i.sel.classes & v]
+        d["feat"] = {k: getattr(i.feat, k) for k, _ in Features._fields_}
+        d["shard_bounds"] = list(i.shard_bounds)[: i.ngpus + 1]
+        return d
+
+    def export(self, which, g=0) -> np.ndarray:
+        w = ARR[which] if isinstance(which, str) else which
+        n = lib.spmv_plan_export(self._h, g, w, None)
+        if n < 0:
+            raise SpmvError(int(n), lib.spmv_last_error().decode())
+        out = np.empty(n, _ARR_DTYPE[w])
+        if n:
+            rc = lib.spmv_plan_export(self._h, g, w, out.ctypes.data)
+            if rc < 0:
+                raise SpmvError(int(rc), lib.spmv_last_error().decode())
+        return out
+
+    def x_device(self, g=0) -> int:
+        return lib.spmv_plan_x_device(self._h, g)
+
+    def y_device(self, g=0) -> int:
+        return lib.spmv_plan_y_device(self._h, g)
+
+    def stream(self, g=0) -> int:
+        return lib.spmv_plan_stream(self._h, g)

@@ -1,0 +1,901 @@
+// api.cu -- the C ABI of include/spmv.h: plan lifecycle (upload, inspector,
+// selection, structure build), execution, iterated mode, inspection.
+//
+// C++ exceptions are used internally and never cross the ABI: every entry
+// point catches and converts to a spmv_status + thread-local message.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "spmv.h"
+#include "internal.h"
+
+using namespace spmv;
+
+namespace {
+
+thread_local spmv_status g_status = SPMV_OK;
+thread_local std::string g_msg;
+std::atomic<int64_t> g_launches{0};
+
+struct Err : std::runtime_error {
+  spmv_status st;
+  Err(spmv_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+[[noreturn]] void fail(spmv_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Err(s, buf);
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    fail(SPMV_E_NOMEM, "%s: %s", what, cudaGetErrorString(e));
+  }
+  fail(SPMV_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+void count_launches(int n, const char* what) {
+  g_launches += n;
+  ck(cudaGetLastError(), what);
+}
+
+spmv_status set_ok() {
+  g_status = SPMV_OK;
+  return SPMV_OK;
+}
+spmv_status set_err(spmv_status s, const std::string& m) {
+  g_status = s;
+  g_msg = m;
+  return s;
+}
+
+double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+bool is_device_ptr(const void* p, int* dev) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    if (dev) *dev = a.device;
+    return true;
+  }
+  return false;
+}
+
+int64_t rp_at(const void* rp, int bytes, int64_t i) {
+  return bytes == 8 ? ((const int64_t*)rp)[i] : (int64_t)((const int32_t*)rp)[i];
+}
+
+}  // namespace
+
+struct Shard {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  int64_t row0 = 0, m = 0, n_cols = 0, nnz0 = 0, nnz = 0;
+  int rp_bytes = 4;
+  void* rowptr = nullptr;
+  int32_t* col = nullptr;
+  double* val = nullptr;
+  double* x = nullptr;
+  double* y = nullptr;
+  uint32_t* headbits = nullptr;
+  DevStats* stats = nullptr;
+  DevStats hs{};
+  int sm_count = 148;
+  // STREAM
+  int64_t C = 0, T = 0;
+  int32_t* tile_row = nullptr;
+  int32_t* carry_row = nullptr;
+  double* carry_val = nullptr;
+  bool need_fixup = false;
+  uint16_t* dcol = nullptr;
+  int32_t* head = nullptr;
+  int32_t* anchor = nullptr;
+  int stages = 4, stream_grid = 0;
+  // MERGE
+  int64_t items = 0, Tm = 0;
+  int32_t* mrow = nullptr;
+  int64_t* mnnz = nullptr;
+  int32_t* mcarry_row = nullptr;
+  double* mcarry_val = nullptr;
+  // SPLIT
+  int64_t n_long = 0, n_chunks = 0;
+  int32_t* long_rows = nullptr;
+  int64_t* chunk_start = nullptr;
+  int32_t* chunk_row = nullptr;
+  double* chunk_val = nullptr;
+  // iterated mode
+  double* allpart = nullptr;  // G * kNormPartials
+  double* nu = nullptr;
+  int nu_cap = 0;
+  cudaEvent_t ev_part = nullptr, ev_x = nullptr;
+  std::vector<void*> allocs;
+  int64_t bytes = 0;
+
+  template <typename T>
+  T* alloc(size_t count, size_t pad_bytes = 64) {
+    void* p = nullptr;
+    const size_t b = count * sizeof(T) + pad_bytes;
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+    ck(cudaMalloc(&p, b), "cudaMalloc");
+    allocs.push_back(p);
+    bytes += (int64_t)b;
+    return static_cast<T*>(p);
+  }
+  void release() {
+    cudaSetDevice(dev);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+    if (ev_part) cudaEventDestroy(ev_part);
+    if (ev_x) cudaEventDestroy(ev_x);
+    if (stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+  }
+  MatView view() const { return MatView{rp_bytes, rowptr, col, val, m, n_cols, nnz}; }
+};
+
+struct spmv_plan_s {
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  int rp_bytes = 4;
+  spmv_options opt{};
+  spmv_selection sel{};
+  spmv_features feat{};
+  spmv_device_props props{};
+  int d16_width = 0;
+  std::vector<Shard> shards;
+  std::vector<int64_t> bounds;
+  double upload_ms = 0, inspect_ms = 0, select_ms = 0, encode_ms = 0;
+  int64_t l_split = 4096, k_long = 100, C = 2048, items = 2048, chunk = 8192;
+
+  ~spmv_plan_s() {
+    for (auto& s : shards) s.release();
+  }
+  ExecArgs args(Shard& s, const double* x, double* y) const {
+    ExecArgs a{};
+    a.A = s.view();
+    a.x = x;
+    a.y = y;
+    a.vs = sel.vs;
+    a.sm_count = s.sm_count;
+    a.C = s.C;
+    a.T = s.T;
+    a.tile_row = s.tile_row;
+    a.carry_row = s.carry_row;
+    a.carry_val = s.carry_val;
+    a.need_fixup = s.need_fixup;
+    a.dcol = sel.d16 ? s.dcol : nullptr;
+    a.head = s.head;
+    a.anchor = s.anchor;
+    a.stages = s.stages;
+    a.stream_grid = s.stream_grid;
+    a.items = s.items;
+    a.Tm = s.Tm;
+    a.mrow = s.mrow;
+    a.mnnz = s.mnnz;
+    a.mcarry_row = s.mcarry_row;
+    a.mcarry_val = s.mcarry_val;
+    a.l_split = l_split;
+    a.chunk = chunk;
+    a.n_long = s.n_long;
+    a.n_chunks = s.n_chunks;
+    a.long_rows = s.long_rows;
+    a.chunk_start = s.chunk_start;
+    a.chunk_row = s.chunk_row;
+    a.chunk_val = s.chunk_val;
+    return a;
+  }
+  int launch(Shard& s, const double* x, double* y, int stage = 0) const {
+    ExecArgs a = args(s, x, y);
+    a.stage = stage;
+    switch (sel.variant) {
+      case SPMV_VARIANT_VECTOR: return launch_vector(a, false, s.stream);
+      case SPMV_VARIANT_STREAM: return launch_stream(a, s.stream);
+      case SPMV_VARIANT_MERGE: return launch_merge(a, s.stream);
+      default: return launch_split(a, s.stream);
+    }
+  }
+};
+
+// ----------------------------------------------------------------------------
+// selection (pure function, Table II)
+// ----------------------------------------------------------------------------
+namespace {
+int pow2ceil(int64_t v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_bytes, const spmv_options& o,
+                 spmv_selection& s) {
+  const int64_t k_long = o.k_long > 0 ? o.k_long : 100;
+  const double avg_s = f.avg_short, sd_s = f.sd_short;
+  const int64_t n = f.n, nnz = f.nnz;
+  const int64_t ws = 12 * nnz + (int64_t)rp_bytes * (n + 1) + 16 * n;
+  const bool skew = n > 0 && ((avg_s > 0 && sd_s / avg_s > 1.0) || (double)f.n_empty > 0.25 * (double)n);
+  const bool longr = f.n_long > 0 && (double)f.nnz_max > (double)k_long * f.nnz_avg;
+  int classes = 0;
+  if (skew || longr) classes |= SPMV_CLASS_IMB;
+  int vs = avg_s > 0 ? pow2ceil((int64_t)std::ceil(avg_s)) : 2;
+  vs = std::min(32, std::max(2, vs));
+  int variant = skew ? SPMV_VARIANT_MERGE : longr ? SPMV_VARIANT_SPLIT : avg_s <= 32 ? SPMV_VARIANT_STREAM
+                                                                                     : SPMV_VARIANT_VECTOR;
+  if (avg_s <= 4) classes |= SPMV_CLASS_CMP;
+  if (ws > d.l2_bytes / 2 && !(classes & SPMV_CLASS_IMB)) classes |= SPMV_CLASS_MB;
+  bool d16 = (classes & SPMV_CLASS_MB) && variant == SPMV_VARIANT_STREAM && f.maxgap <= 65535;
+  const bool ml = nnz > 0 && (double)f.misses > 0.75 * (double)nnz && 8 * n > d.l2_bytes / 16;
+  if (ml) classes |= SPMV_CLASS_ML;
+  bool xwin = ml && 8 * n <= d.access_window_max;
+  // explicit options override the feature-guided choice
+  if (o.force_variant > 0) variant = o.force_variant;
+  if (o.force_vs > 0) vs = o.force_vs;
+  if (o.d16 == 0) d16 = false;
+  if (o.d16 == 1) d16 = f.maxgap <= 65535;
+  if (variant != SPMV_VARIANT_STREAM) d16 = false;
+  if (o.xwin == 0) xwin = false;
+  if (o.xwin == 1) xwin = true;
+  s.variant = variant;
+  s.vs = vs;
+  s.d16 = d16 ? 1 : 0;
+  s.xwin = xwin ? 1 : 0;
+  s.classes = classes;
+  s.pad_ = 0;
+}
+
+void validate_options(const spmv_options& o) {
+  if (o.force_variant < 0 || o.force_variant > 4) fail(SPMV_E_ARG, "force_variant %d out of range", o.force_variant);
+  if (o.force_vs != 0 && o.force_vs != 1 && o.force_vs != 2 && o.force_vs != 4 && o.force_vs != 8 &&
+      o.force_vs != 16 && o.force_vs != 32)
+    fail(SPMV_E_ARG, "force_vs %d not in {0,1,2,4,8,16,32}", o.force_vs);
+  if (o.tile_nnz != 0 && (o.tile_nnz % 256 || o.tile_nnz < 256 || o.tile_nnz > 16384))
+    fail(SPMV_E_ARG, "tile_nnz %lld must be a multiple of 256 in [256, 16384]", (long long)o.tile_nnz);
+  if (o.merge_items != 0 && o.merge_items != 2048) fail(SPMV_E_ARG, "merge_items must be 2048");
+  if (o.long_chunk != 0 && (o.long_chunk % 256 || o.long_chunk < 256))
+    fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
+  if (o.l_split < 0 || o.k_long < 0) fail(SPMV_E_ARG, "negative l_split / k_long");
+}
+
+void features_from_stats(const std::vector<DevStats>& st, const std::vector<int64_t>& m, spmv_features& f) {
+  memset(&f, 0, sizeof f);
+  f.nnz_min = LLONG_MAX;
+  for (size_t g = 0; g < st.size(); ++g) {
+    const DevStats& s = st[g];
+    f.n += m[g];
+    f.s1 += s.s1;
+    f.s2 += s.s2;
+    f.s1_short += s.s1_short;
+    f.s2_short += s.s2_short;
+    if (m[g] > 0) f.nnz_min = std::min<int64_t>(f.nnz_min, s.nnz_min);
+    f.nnz_max = std::max<int64_t>(f.nnz_max, s.nnz_max);
+    f.n_empty += s.n_empty;
+    f.n_long += s.n_long;
+    f.nnz_long += s.nnz_long;
+    f.n_short += s.n_short;
+    f.max_short = std::max<int64_t>(f.max_short, s.max_short);
+    f.maxgap = std::max<int64_t>(f.maxgap, s.maxgap);
+    f.misses += s.misses;
+  }
+  if (f.n == 0) f.nnz_min = 0;
+  f.nnz = (int64_t)f.s1;
+  auto sd = [](uint64_t cnt, uint64_t s1, uint64_t s2) {
+    if (cnt == 0) return 0.0;
+    unsigned __int128 a = (unsigned __int128)cnt * s2, b = (unsigned __int128)s1 * s1;
+    return std::sqrt((double)(a - b)) / (double)cnt;
+  };
+  f.nnz_avg = f.n ? (double)f.s1 / (double)f.n : 0.0;
+  f.nnz_sd = sd((uint64_t)f.n, f.s1, f.s2);
+  f.avg_short = f.n_short ? (double)f.s1_short / (double)f.n_short : 0.0;
+  f.sd_short = sd((uint64_t)f.n_short, f.s1_short, f.s2_short);
+}
+
+void query_props(int dev, spmv_device_props& p) {
+  cudaDeviceProp d;
+  ck(cudaGetDeviceProperties(&d, dev), "cudaGetDeviceProperties");
+  p.sm_count = d.multiProcessorCount;
+  p.cc_major = d.major;
+  p.cc_minor = d.minor;
+  p.pad_ = 0;
+  p.l2_bytes = d.l2CacheSize;
+  p.persisting_l2_max = d.persistingL2CacheMaxSize;
+  p.access_window_max = d.accessPolicyMaxWindowSize;
+  p.global_mem_bytes = (int64_t)d.totalGlobalMem;
+}
+
+void shard_bounds_host(int64_t n, const void* rp, int bytes, int G, int64_t* b) {
+  const int64_t nnz = rp_at(rp, bytes, n);
+  b[0] = 0;
+  for (int g = 1; g < G; ++g) {
+    const int64_t key = (g * nnz + G - 1) / G;
+    int64_t lo = 0, hi = n + 1;
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (rp_at(rp, bytes, mid) < key) lo = mid + 1; else hi = mid;
+    }
+    b[g] = std::min(lo, n);
+  }
+  b[G] = n;
+}
+
+const char* csr_code_name(int code) {
+  switch (code) {
+    case 1: return "rowptr[0] != 0";
+    case 2: return "rowptr[n] != nnz";
+    case 3: return "rowptr decreasing";
+    case 4: return "colind out of range";
+    case 5: return "colind not strictly increasing in row";
+    default: return "?";
+  }
+}
+
+[[noreturn]] void fail_csr(int code, int64_t where) {
+  fail(SPMV_E_CSR, "invalid CSR: code %d (%s) at %s %lld", code, csr_code_name(code),
+       code <= 3 ? "row" : "nonzero", (long long)where);
+}
+
+// ---------------------------------------------------------------------------
+spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* rowptr, int rp_bytes,
+                      const int32_t* colind, const double* values, int ngpus, const spmv_options* optp) {
+  if (!rowptr || (nnz > 0 && (!colind || !values))) fail(SPMV_E_ARG, "null array pointer");
+  if (n_rows < 0 || n_cols < 0 || nnz < 0) fail(SPMV_E_ARG, "negative size");
+  if (rp_bytes != 4 && rp_bytes != 8) fail(SPMV_E_ARG, "rowptr_bytes must be 4 or 8");
+  if (n_rows >= INT32_MAX || n_cols > INT32_MAX)
+    fail(SPMV_E_UNSUPPORTED, "n >= 2^31 is not supported (int32 colind / row ids)");
+  if (rp_bytes == 4 && nnz > INT32_MAX) fail(SPMV_E_UNSUPPORTED, "nnz >= 2^31 needs a 64-bit rowptr");
+  spmv_options opt;
+  spmv_options_default(&opt);
+  if (optp) {
+    if (optp->struct_size != (int32_t)sizeof(spmv_options)) fail(SPMV_E_ARG, "spmv_options.struct_size mismatch");
+    opt = *optp;
+  }
+  validate_options(opt);
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (ngpus < 1 || ngpus > 8) fail(SPMV_E_ARG, "ngpus %d out of range [1, 8]", ngpus);
+  if (ngpus > ndev && !opt.emulate_devices) fail(SPMV_E_ARG, "ngpus %d > %d visible devices", ngpus, ndev);
+  int cur = 0;
+  ck(cudaGetDevice(&cur), "cudaGetDevice");
+
+  auto P = std::unique_ptr<spmv_plan_s>(new spmv_plan_s());
+  P->n_rows = n_rows;
+  P->n_cols = n_cols;
+  P->nnz = nnz;
+  P->rp_bytes = rp_bytes;
+  P->opt = opt;
+  P->l_split = opt.l_split > 0 ? opt.l_split : 4096;
+  P->k_long = opt.k_long > 0 ? opt.k_long : 100;
+  P->C = opt.tile_nnz > 0 ? opt.tile_nnz : 2048;
+  P->items = 2048;
+  P->chunk = opt.long_chunk > 0 ? opt.long_chunk : 8192;
+  query_props(cur, P->props);
+
+  // ---- a1: host-side rowptr end checks, shard bounds ----------------------------
+  double t_a = now_ms();
+  int rp_dev = -1;
+  const bool rp_on_dev = is_device_ptr(rowptr, &rp_dev);
+  std::vector<unsigned char> rp_host;
+  const void* rp_h = rowptr;
+  if (rp_on_dev && ngpus > 1) {
+    rp_host.resize((size_t)(n_rows + 1) * rp_bytes);
+    ck(cudaMemcpy(rp_host.data(), rowptr, rp_host.size(), cudaMemcpyDeviceToHost), "copy rowptr");
+    rp_h = rp_host.data();
+  }
+  int64_t rp0, rpn;
+  if (rp_on_dev && ngpus == 1) {
+    ck(cudaMemcpy(&rp0, rowptr, rp_bytes, cudaMemcpyDeviceToHost), "copy rowptr[0]");
+    ck(cudaMemcpy(&rpn, (const char*)rowptr + n_rows * rp_bytes, rp_bytes, cudaMemcpyDeviceToHost), "rowptr[n]");
+    if (rp_bytes == 4) { rp0 = (int32_t)rp0; rpn = (int32_t)rpn; }
+  } else {
+    rp0 = rp_at(rp_h, rp_bytes, 0);
+    rpn = rp_at(rp_h, rp_bytes, n_rows);
+  }
+  if (opt.validate || true) {
+    if (rp0 != 0) fail_csr(1, 0);
+    if (rpn != nnz) fail_csr(2, n_rows);
+  }
+  P->bounds.assign(ngpus + 1, 0);
+  if (ngpus == 1) { P->bounds[1] = n_rows; }
+  else shard_bounds_host(n_rows, rp_h, rp_bytes, ngpus, P->bounds.data());
+
+  // ---- a1: upload every shard ---------------------------------------------------
+  P->shards.resize(ngpus);
+  for (int g = 0; g < ngpus; ++g) {
+    Shard& s = P->shards[g];
+    s.dev = opt.emulate_devices ? cur : g;
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&s.ev_part, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&s.ev_x, cudaEventDisableTiming), "cudaEventCreate");
+    cudaDeviceProp dp;
+    ck(cudaGetDeviceProperties(&dp, s.dev), "cudaGetDeviceProperties");
+    s.sm_count = dp.multiProcessorCount;
+    s.row0 = P->bounds[g];
+    s.m = P->bounds[g + 1] - P->bounds[g];
+    s.n_cols = n_cols;
+    s.rp_bytes = rp_bytes;
+    s.nnz0 = ngpus == 1 ? 0 : rp_at(rp_h, rp_bytes, s.row0);
+    s.nnz = ngpus == 1 ? nnz : rp_at(rp_h, rp_bytes, s.row0 + s.m) - s.nnz0;
+    if (s.nnz < 0) fail_csr(3, s.row0);
+    s.rowptr = s.alloc<char>((size_t)(s.m + 1) * rp_bytes);
+    s.col = s.alloc<int32_t>((size_t)s.nnz);
+    s.val = s.alloc<double>((size_t)s.nnz);
+    ck(cudaMemcpyAsync(s.rowptr, (const char*)rowptr + s.row0 * rp_bytes, (size_t)(s.m + 1) * rp_bytes,
+                       cudaMemcpyDefault, s.stream), "upload rowptr");
+    if (s.nnz) {
+      ck(cudaMemcpyAsync(s.col, colind + s.nnz0, (size_t)s.nnz * 4, cudaMemcpyDefault, s.stream), "upload colind");
+      ck(cudaMemcpyAsync(s.val, values + s.nnz0, (size_t)s.nnz * 8, cudaMemcpyDefault, s.stream), "upload values");
+    }
+    launch_rebase(s.rowptr, rp_bytes, s.m + 1, s.nnz0, s.stream);
+    count_launches(s.nnz0 ? 1 : 0, "rebase");
+  }
+  for (auto& s : P->shards) ck(cudaStreamSynchronize(s.stream), "upload sync");
+  P->upload_ms = now_ms() - t_a;
+
+  // ---- a2: inspector (features, validation, max gap) ---------------------------------
+  double t_b = now_ms();
+  for (auto& s : P->shards) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    s.stats = s.alloc<DevStats>(1);
+    s.headbits = s.alloc<uint32_t>((size_t)(s.nnz + 31) / 32 + 1);
+    DevStats init{};
+    init.nnz_min = LLONG_MAX;
+    init.rp_err = LLONG_MAX;
+    init.col_err = LLONG_MAX;
+    ck(cudaMemcpyAsync(s.stats, &init, sizeof init, cudaMemcpyHostToDevice, s.stream), "stats init");
+    ck(cudaMemsetAsync(s.headbits, 0, ((size_t)(s.nnz + 31) / 32 + 1) * 4, s.stream), "memset");
+    launch_rowstats(s.view(), P->l_split, s.headbits, s.stats, s.stream);
+    count_launches(s.m ? 1 : 0, "rowstats");
+    ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
+  }
+  for (auto& s : P->shards) {
+    ck(cudaStreamSynchronize(s.stream), "rowstats");
+    if (s.hs.rp_err != LLONG_MAX) fail_csr(3, s.row0 + s.hs.rp_err);
+  }
+  for (auto& s : P->shards) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    launch_validate_gaps(s.view(), s.headbits, s.stats, s.stream);
+    count_launches(s.nnz ? 1 : 0, "validate_gaps");
+    ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
+  }
+  for (auto& s : P->shards) {
+    ck(cudaStreamSynchronize(s.stream), "validate");
+    if (opt.validate && s.hs.col_err != LLONG_MAX) {
+      const int code = (s.hs.col_err & 1) ? 5 : 4;
+      fail_csr(code, s.nnz0 + (s.hs.col_err >> 1));
+    }
+  }
+  P->inspect_ms = now_ms() - t_b;
+
+  // ---- a5: selection -------------------------------------------------------------
+  double t_c = now_ms();
+  std::vector<DevStats> st;
+  std::vector<int64_t> ms;
+  for (auto& s : P->shards) { st.push_back(s.hs); ms.push_back(s.m); }
+  features_from_stats(st, ms, P->feat);
+  select_impl(P->feat, P->props, rp_bytes, opt, P->sel);
+  if (P->sel.d16) P->d16_width = P->feat.maxgap <= 255 ? 8 : 16;
+  P->select_ms = now_ms() - t_c;
+
+  // ---- a3/a4: structures for the selected variant ---------------------------------
+  double t_d = now_ms();
+  for (auto& s : P->shards) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    const MatView A = s.view();
+    if (P->sel.variant == SPMV_VARIANT_STREAM) {
+      s.C = P->C;
+      s.T = std::max<int64_t>(1, (s.nnz + s.C - 1) / s.C);
+      s.tile_row = s.alloc<int32_t>((size_t)s.T + 1);
+      s.carry_row = s.alloc<int32_t>((size_t)s.T);
+      s.carry_val = s.alloc<double>((size_t)s.T);
+      launch_tile_rows(A, s.C, s.T, s.tile_row, s.stats, s.stream);
+      count_launches(1, "tile_rows");
+      if (P->sel.d16) {
+        s.dcol = s.alloc<uint16_t>((size_t)s.nnz);
+        s.head = s.alloc<int32_t>((size_t)s.m);
+        s.anchor = s.alloc<int32_t>((size_t)s.T);
+        launch_d16_encode(A, s.headbits, s.C, s.T, s.dcol, s.head, s.anchor, s.stream);
+        count_launches(3, "d16_encode");
+      }
+      ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
+      ck(cudaStreamSynchronize(s.stream), "tiles");
+      s.need_fixup = s.hs.n_incoming > 0;
+      s.stages = 4;
+      ExecArgs a = P->args(s, nullptr, nullptr);
+      s.stream_grid = stream_prepare(a);
+      if (s.stream_grid < 0) { cudaGetLastError(); s.stages = 2; a = P->args(s, nullptr, nullptr); s.stream_grid = stream_prepare(a); }
+      if (s.stream_grid < 0) fail(SPMV_E_CUDA, "cta_stream: cannot fit tile_nnz=%lld in shared memory", (long long)s.C);
+    } else if (P->sel.variant == SPMV_VARIANT_MERGE) {
+      s.items = P->items;
+      s.Tm = std::max<int64_t>(1, (s.m + s.nnz + s.items - 1) / s.items);
+      s.mrow = s.alloc<int32_t>((size_t)s.Tm + 1);
+      s.mnnz = s.alloc<int64_t>((size_t)s.Tm + 1);
+      s.mcarry_row = s.alloc<int32_t>((size_t)s.Tm);
+      s.mcarry_val = s.alloc<double>((size_t)s.Tm);
+      launch_merge_splits(A, s.items, s.Tm, s.mrow, s.mnnz, s.stream);
+      count_launches(1, "merge_splits");
+    } else if (P->sel.variant == SPMV_VARIANT_SPLIT) {
+      s.n_long = s.hs.n_long;
+      if (s.n_long > 0) {
+        const int nb = 1024;
+        s.long_rows = s.alloc<int32_t>((size_t)s.n_long);
+        s.chunk_start = s.alloc<int64_t>((size_t)s.n_long + 1);
+        int32_t* scratch = s.alloc<int32_t>((size_t)nb * 4 + 8);
+        launch_long_rows(A, P->l_split, P->chunk, s.long_rows, s.n_long, s.chunk_start, scratch, nb, s.stream);
+        count_launches(4, "long_rows");
+        ck(cudaMemcpyAsync(&s.n_chunks, s.chunk_start + s.n_long, 8, cudaMemcpyDeviceToHost, s.stream), "chunks");
+        ck(cudaStreamSynchronize(s.stream), "long_rows");
+        s.chunk_row = s.alloc<int32_t>((size_t)s.n_chunks);
+        s.chunk_val = s.alloc<double>((size_t)s.n_chunks);
+      }
+    }
+    s.x = s.alloc<double>((size_t)n_cols);
+    s.y = s.alloc<double>((size_t)s.m);
+    s.allpart = s.alloc<double>((size_t)kNormPartials * ngpus);
+  }
+  for (auto& s : P->shards) {
+    ck(cudaStreamSynchronize(s.stream), "structures");
+    if (s.headbits) {  // only needed by the inspector
+      cudaFree(s.headbits);
+      auto it = std::find(s.allocs.begin(), s.allocs.end(), (void*)s.headbits);
+      if (it != s.allocs.end()) s.allocs.erase(it);
+      s.bytes -= (int64_t)(((size_t)(s.nnz + 31) / 32 + 1) * 4 + 64);
+      s.headbits = nullptr;
+    }
+    // ML analogue: keep x resident in L2 via an access-policy window
+    if (P->sel.xwin) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      const size_t xb = (size_t)n_cols * 8;
+      const size_t win = std::min<size_t>(xb, (size_t)P->props.access_window_max);
+      const size_t persist = std::min<size_t>(win, (size_t)P->props.persisting_l2_max);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist);
+      cudaStreamAttrValue v;
+      memset(&v, 0, sizeof v);
+      v.accessPolicyWindow.base_ptr = s.x;
+      v.accessPolicyWindow.num_bytes = win;
+      v.accessPolicyWindow.hitRatio = win ? std::min(1.0f, (float)persist / (float)win) : 0.f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      ck(cudaStreamSetAttribute(s.stream, cudaStreamAttributeAccessPolicyWindow, &v), "access policy window");
+    }
+  }
+  P->encode_ms = now_ms() - t_d;
+  ck(cudaSetDevice(cur), "cudaSetDevice");
+  return P.release();
+}
+
+template <typename F>
+spmv_status guard(F&& f) {
+  try {
+    f();
+    return set_ok();
+  } catch (const Err& e) {
+    return set_err(e.st, e.what());
+  } catch (const std::bad_alloc&) {
+    return set_err(SPMV_E_NOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return set_err(SPMV_E_CUDA, e.what());
+  }
+}
+
+// run the plan on x (device pointer valid on every shard's device or the
+// shards' replicas) into y (per-shard outputs)
+void execute_impl(spmv_plan p, const double* x, double* y, bool sync) {
+  if (!p || !x || !y) fail(SPMV_E_ARG, "null argument");
+  int xdev = -1, ydev = -1;
+  const bool xd = is_device_ptr(x, &xdev), yd = is_device_ptr(y, &ydev);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& s : p->shards) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    const double* xs = x;
+    if (!(xd && xdev == s.dev)) {
+      if (x != s.x)
+        ck(cudaMemcpyAsync(s.x, x, (size_t)p->n_cols * 8, cudaMemcpyDefault, s.stream), "copy x");
+      xs = s.x;
+    }
+    double* ys = y + s.row0;
+    const bool direct = yd && ydev == s.dev;
+    if (!direct) ys = s.y;
+    count_launches(p->launch(s, xs, ys), "spmv");
+    if (!direct) ck(cudaMemcpyAsync(y + s.row0, s.y, (size_t)s.m * 8, cudaMemcpyDefault, s.stream), "copy y");
+  }
+  if (sync)
+    for (auto& s : p->shards) ck(cudaStreamSynchronize(s.stream), "spmv sync");
+  cudaSetDevice(cur);
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+void spmv_options_default(spmv_options* o) {
+  if (!o) return;
+  memset(o, 0, sizeof *o);
+  o->struct_size = (int32_t)sizeof(spmv_options);
+  o->d16 = -1;
+  o->xwin = -1;
+  o->validate = 1;
+}
+
+spmv_plan spmv_plan_create(int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* colind,
+                           const double* values, int ngpus) {
+  spmv_plan out = nullptr;
+  spmv_plan_create_ex(&out, n, n, nnz, rowptr, 8, colind, values, ngpus, nullptr);
+  return out;
+}
+
+spmv_status spmv_plan_create_ex(spmv_plan* out, int64_t n_rows, int64_t n_cols, int64_t nnz, const void* rowptr,
+                                int rowptr_bytes, const int32_t* colind, const double* values, int ngpus,
+                                const spmv_options* opt) {
+  if (!out) return set_err(SPMV_E_ARG, "out is NULL");
+  *out = nullptr;
+  return guard([&] { *out = create_impl(n_rows, n_cols, nnz, rowptr, rowptr_bytes, colind, values, ngpus, opt); });
+}
+
+void spmv_plan_destroy(spmv_plan p) { delete p; }
+
+int spmv_execute(spmv_plan p, const double* x, double* y) {
+  return guard([&] { execute_impl(p, x, y, true); });
+}
+
+int spmv_execute_async(spmv_plan p, const double* x, double* y) { return spmv_execute_stage(p, x, y, 0); }
+
+int spmv_execute_stage(spmv_plan p, const double* x, double* y, int stage) {
+  return guard([&] {
+    if (!p || !x || !y || stage < 0 || stage > 2) fail(SPMV_E_ARG, "bad argument");
+    if (p->shards.size() != 1) fail(SPMV_E_ARG, "spmv_execute_async/_stage need a single-shard plan");
+    Shard& s = p->shards[0];
+    count_launches(p->launch(s, x, y, stage), "spmv");
+  });
+}
+
+int32_t spmv_norm_partial_count(void) { return kNormPartials; }
+
+int spmv_norm_partials(spmv_plan p, const double* y, double* partials) {
+  return guard([&] {
+    if (!p || !y || !partials || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    count_launches(launch_norm_partials(y, s.m, partials, s.stream), "norm_partials");
+  });
+}
+
+int spmv_normalize(spmv_plan p, const double* y, const double* partials, int count, double* x_out, double* nu_dev) {
+  return guard([&] {
+    if (!p || !y || !partials || !x_out || count < 1 || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    count_launches(launch_normalize(y, s.m, partials, count, x_out, nu_dev, s.stream), "normalize");
+  });
+}
+
+spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters, double* last_norm,
+                         double* nu_out) {
+  return guard([&] {
+    if (!p || !x0 || !x_out || iters < 1) fail(SPMV_E_ARG, "bad argument");
+    if (p->n_rows != p->n_cols) fail(SPMV_E_ARG, "iterated mode needs a square matrix");
+    const int G = (int)p->shards.size();
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& s : p->shards) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      if (s.nu_cap < iters) {
+        s.nu = s.alloc<double>((size_t)iters);
+        s.nu_cap = iters;
+      }
+      ck(cudaMemcpyAsync(s.x, x0, (size_t)p->n_cols * 8, cudaMemcpyDefault, s.stream), "copy x0");
+    }
+    for (int k = 0; k < iters; ++k) {
+      for (int g = 0; g < G; ++g) {
+        Shard& s = p->shards[g];
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        count_launches(p->launch(s, s.x, s.y), "spmv");
+        count_launches(launch_norm_partials(s.y, s.m, s.allpart + (size_t)g * kNormPartials, s.stream), "norm");
+        ck(cudaEventRecord(s.ev_part, s.stream), "event");
+      }
+      for (int g = 0; g < G; ++g) {
+        Shard& s = p->shards[g];
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        for (int h = 0; h < G; ++h) {
+          if (h == g) continue;
+          Shard& t = p->shards[h];
+          ck(cudaStreamWaitEvent(s.stream, t.ev_part, 0), "wait");
+          ck(cudaMemcpyPeerAsync(s.allpart + (size_t)h * kNormPartials, s.dev, t.allpart + (size_t)h * kNormPartials,
+                                 t.dev, kNormPartials * 8, s.stream), "partials exchange");
+        }
+        count_launches(launch_normalize(s.y, s.m, s.allpart, G * kNormPartials, s.x + s.row0, s.nu + k, s.stream),
+                       "normalize");
+        ck(cudaEventRecord(s.ev_x, s.stream), "event");
+      }
+      if (G > 1) {
+        for (int g = 0; g < G; ++g) {
+          Shard& s = p->shards[g];
+          ck(cudaSetDevice(s.dev), "cudaSetDevice");
+          for (int h = 0; h < G; ++h) {
+            if (h == g) continue;
+            Shard& t = p->shards[h];
+            ck(cudaStreamWaitEvent(s.stream, t.ev_x, 0), "wait");
+            ck(cudaMemcpyPeerAsync(s.x + t.row0, s.dev, t.x + t.row0, t.dev, (size_t)t.m * 8, s.stream),
+               "x all-gather");
+          }
+        }
+      }
+    }
+    Shard& s0 = p->shards[0];
+    std::vector<double> nu(iters);
+    ck(cudaSetDevice(s0.dev), "cudaSetDevice");
+    for (auto& s : p->shards) ck(cudaStreamSynchronize(s.stream), "iterate");
+    ck(cudaMemcpy(nu.data(), s0.nu, (size_t)iters * 8, cudaMemcpyDeviceToHost), "nu");
+    ck(cudaMemcpy(x_out, s0.x, (size_t)p->n_cols * 8, cudaMemcpyDefault), "x_out");
+    cudaSetDevice(cur);
+    if (nu_out) memcpy(nu_out, nu.data(), (size_t)iters * 8);
+    if (last_norm) *last_norm = nu[iters - 1];
+    for (int k = 0; k < iters; ++k)
+      if (nu[k] == 0.0) fail(SPMV_E_ZERO_NORM, "iterated mode: ||y|| == 0 at iteration %d", k);
+  });
+}
+
+spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
+  return guard([&] {
+    if (!p || !info) fail(SPMV_E_ARG, "null argument");
+    memset(info, 0, sizeof *info);
+    info->n_rows = p->n_rows;
+    info->n_cols = p->n_cols;
+    info->nnz = p->nnz;
+    info->rowptr_bytes = p->rp_bytes;
+    info->ngpus = (int32_t)p->shards.size();
+    info->sel = p->sel;
+    info->feat = p->feat;
+    info->d16_width = p->d16_width;
+    const Shard& s0 = p->shards[0];
+    info->tile_nnz = s0.C;
+    info->n_tiles = s0.T;
+    info->merge_items = s0.items;
+    info->n_merge_tiles = s0.Tm;
+    info->l_split = p->l_split;
+    info->long_chunk = p->chunk;
+    int64_t nc = 0, bytes = 0;
+    for (auto& s : p->shards) { nc += s.n_chunks; bytes += s.bytes; }
+    info->n_long_chunks = nc;
+    info->upload_ms = p->upload_ms;
+    info->inspect_ms = p->inspect_ms;
+    info->select_ms = p->select_ms;
+    info->encode_ms = p->encode_ms;
+    info->device_bytes = bytes;
+    for (size_t g = 0; g < p->bounds.size() && g < 9; ++g) info->shard_bounds[g] = p->bounds[g];
+  });
+}
+
+double* spmv_plan_x_device(spmv_plan p, int g) {
+  return (p && g >= 0 && g < (int)p->shards.size()) ? p->shards[g].x : nullptr;
+}
+double* spmv_plan_y_device(spmv_plan p, int g) {
+  return (p && g >= 0 && g < (int)p->shards.size()) ? p->shards[g].y : nullptr;
+}
+void* spmv_plan_stream(spmv_plan p, int g) {
+  return (p && g >= 0 && g < (int)p->shards.size()) ? (void*)p->shards[g].stream : nullptr;
+}
+
+int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
+  int64_t count = -1;
+  spmv_status st = guard([&] {
+    if (!p || g < 0 || g >= (int)p->shards.size()) fail(SPMV_E_ARG, "bad plan / shard");
+    Shard& s = p->shards[g];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    auto widen32 = [&](const int32_t* src, int64_t n) {
+      count = n;
+      if (!dst || n == 0) return;
+      if (!src) fail(SPMV_E_ARG, "structure not built for the selected variant");
+      std::vector<int32_t> h((size_t)n);
+      ck(cudaMemcpy(h.data(), src, (size_t)n * 4, cudaMemcpyDeviceToHost), "export");
+      for (int64_t i = 0; i < n; ++i) ((int64_t*)dst)[i] = h[i];
+    };
+    auto raw = [&](const void* src, int64_t n, size_t es) {
+      count = n;
+      if (!dst || n == 0) return;
+      if (!src) fail(SPMV_E_ARG, "structure not built for the selected variant");
+      ck(cudaMemcpy(dst, src, (size_t)n * es, cudaMemcpyDeviceToHost), "export");
+    };
+    switch (which) {
+      case SPMV_ARR_TILE_ROWS: widen32(s.tile_row, s.tile_row ? s.T + 1 : 0); break;
+      case SPMV_ARR_MERGE_ROWS: widen32(s.mrow, s.mrow ? s.Tm + 1 : 0); break;
+      case SPMV_ARR_MERGE_NNZ: raw(s.mnnz, s.mnnz ? s.Tm + 1 : 0, 8); break;
+      case SPMV_ARR_CHUNK_ROW:
+      case SPMV_ARR_CHUNK_BEGIN:
+      case SPMV_ARR_CHUNK_END: {
+        count = s.n_chunks;
+        if (!dst || s.n_chunks == 0) break;
+        int64_t* tmp = nullptr;
+        ck(cudaMalloc(&tmp, (size_t)s.n_chunks * 24), "cudaMalloc");
+        ExecArgs a = p->args(s, nullptr, nullptr);
+        launch_chunk_export(a, tmp, s.stream);
+        g_launches += 1;
+        cudaError_t e = cudaStreamSynchronize(s.stream);
+        if (e == cudaSuccess) {
+          const int part = which - SPMV_ARR_CHUNK_ROW;
+          e = cudaMemcpy(dst, tmp + (size_t)part * s.n_chunks, (size_t)s.n_chunks * 8, cudaMemcpyDeviceToHost);
+        }
+        cudaFree(tmp);
+        ck(e, "chunk export");
+        break;
+      }
+      case SPMV_ARR_DCOL: raw(s.dcol, s.dcol ? s.nnz : 0, 2); break;
+      case SPMV_ARR_HEAD: raw(s.head, s.head ? s.m : 0, 4); break;
+      case SPMV_ARR_ANCHOR: raw(s.anchor, s.anchor ? s.T : 0, 4); break;
+      case SPMV_ARR_DECODED: {
+        count = s.dcol ? s.nnz : 0;
+        if (!dst || count == 0) break;
+        int32_t* tmp = nullptr;
+        ck(cudaMalloc(&tmp, (size_t)s.nnz * 4 + 64), "cudaMalloc");
+        launch_d16_decode_export(s.view(), s.dcol, s.head, s.anchor, s.tile_row, s.C, s.T, tmp, s.stream);
+        g_launches += 1;
+        cudaError_t e = cudaStreamSynchronize(s.stream);
+        if (e == cudaSuccess) e = cudaMemcpy(dst, tmp, (size_t)s.nnz * 4, cudaMemcpyDeviceToHost);
+        cudaFree(tmp);
+        ck(e, "decode export");
+        break;
+      }
+      case SPMV_ARR_SHARD_BOUNDS:
+        count = (int64_t)p->bounds.size();
+        if (dst) memcpy(dst, p->bounds.data(), p->bounds.size() * 8);
+        break;
+      default: fail(SPMV_E_ARG, "unknown array id %d", which);
+    }
+  });
+  return st == SPMV_OK ? count : (int64_t)st;
+}
+
+spmv_status spmv_shard_bounds(int64_t n, const void* rowptr, int rowptr_bytes, int G, int64_t* bounds) {
+  return guard([&] {
+    if (!rowptr || !bounds || n < 0 || G < 1 || (rowptr_bytes != 4 && rowptr_bytes != 8))
+      fail(SPMV_E_ARG, "bad argument");
+    shard_bounds_host(n, rowptr, rowptr_bytes, G, bounds);
+  });
+}
+
+spmv_status spmv_select(const spmv_features* f, const spmv_device_props* d, int rowptr_bytes, const spmv_options* opt,
+                        spmv_selection* out) {
+  return guard([&] {
+    if (!f || !d || !out) fail(SPMV_E_ARG, "null argument");
+    spmv_options o;
+    spmv_options_default(&o);
+    if (opt) o = *opt;
+    validate_options(o);
+    select_impl(*f, *d, rowptr_bytes, o, *out);
+  });
+}
+
+spmv_status spmv_device_query(int dev, spmv_device_props* out) {
+  return guard([&] {
+    if (!out) fail(SPMV_E_ARG, "null argument");
+    query_props(dev, *out);
+  });
+}
+
+spmv_status spmv_last_status(void) { return g_status; }
+const char* spmv_last_error(void) { return g_msg.c_str(); }
+int64_t spmv_kernel_launches(void) { return g_launches.load(); }
+
+}  // extern "C"

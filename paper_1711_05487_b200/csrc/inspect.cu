@@ -1,0 +1,318 @@
+// inspect.cu -- the plan-time inspector on the device.
+//
+//  K0 rowstats       Theta(N) features of Table I over rowptr, the
+//                    rowptr invariants and the row-head bitmap
+//  K1 validate_gaps  colind range / strict order, max in-row gap
+//                    (needed for the 16-bit delta width) and the
+//                    Table I misses count, one pass over colind
+//  K2 tile_rows      per-CTA nnz tiles: R_k = lower_bound(rowptr, k*C)
+//                    (nnz-balanced partition of P:708-711 at CTA granularity)
+//     merge_splits   merge-path diagonals (IMB "auto" analogue)
+//     long_rows      ordered long-row list + chunk prefix (decomposition)
+//  K3 d16_encode     delta colind + heads + tile anchors (MB)
+//
+// Every accumulator is an integer, so atomics give order-independent
+// (deterministic) results.
+#include <climits>
+#include "common.cuh"
+#include "internal.h"
+
+namespace spmv {
+
+template <typename RP>
+__global__ void __launch_bounds__(kNT) rowstats_kernel(const RP* __restrict__ rp, int64_t m, int64_t nnz,
+                                                       int64_t l_split, uint32_t* __restrict__ headbits,
+                                                       DevStats* st) {
+  unsigned long long s1 = 0, s2 = 0, s1s = 0, s2s = 0;
+  long long mn = LLONG_MAX, mx = 0, ne = 0, nl = 0, nnzl = 0, ns = 0, mxs = 0, err = LLONG_MAX;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const int64_t a = (int64_t)rp[i], b = (int64_t)rp[i + 1];
+    const long long len = b - a;
+    if (len < 0) { err = err < i ? err : i; continue; }
+    const unsigned long long ul = (unsigned long long)len;
+    s1 += ul; s2 += ul * ul;
+    mn = len < mn ? len : mn;
+    mx = len > mx ? len : mx;
+    ne += (len == 0);
+    if (len > l_split) { nl++; nnzl += len; }
+    else { ns++; s1s += ul; s2s += ul * ul; mxs = len > mxs ? len : mxs; }
+    if (len > 0 && a >= 0 && a < nnz) atomicOr(&headbits[a >> 5], 1u << (a & 31));
+  }
+  s1 = warp_sum(s1); s2 = warp_sum(s2); s1s = warp_sum(s1s); s2s = warp_sum(s2s);
+  ne = warp_sum(ne); nl = warp_sum(nl); nnzl = warp_sum(nnzl); ns = warp_sum(ns);
+  mn = warp_min(mn); mx = warp_max(mx); mxs = warp_max(mxs); err = warp_min(err);
+  if ((threadIdx.x & 31) == 0) {
+    if (s1) atomicAdd(&st->s1, s1);
+    if (s2) atomicAdd(&st->s2, s2);
+    if (s1s) atomicAdd(&st->s1_short, s1s);
+    if (s2s) atomicAdd(&st->s2_short, s2s);
+    if (ne) atomicAdd((unsigned long long*)&st->n_empty, (unsigned long long)ne);
+    if (nl) atomicAdd((unsigned long long*)&st->n_long, (unsigned long long)nl);
+    if (nnzl) atomicAdd((unsigned long long*)&st->nnz_long, (unsigned long long)nnzl);
+    if (ns) atomicAdd((unsigned long long*)&st->n_short, (unsigned long long)ns);
+    atomicMin(&st->nnz_min, mn);
+    atomicMax(&st->nnz_max, mx);
+    atomicMax(&st->max_short, mxs);
+    if (err != LLONG_MAX) atomicMin(&st->rp_err, err);
+  }
+}
+
+__global__ void __launch_bounds__(kNT) validate_gaps_kernel(const int32_t* __restrict__ col, int64_t nnz,
+                                                            int64_t n_cols, const uint32_t* __restrict__ headbits,
+                                                            DevStats* st) {
+  long long mg = 0, miss = 0, err = LLONG_MAX;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz; j += stride) {
+    const int64_t c = col[j];
+    if (c < 0 || c >= n_cols) { long long k = 2 * j; err = k < err ? k : err; continue; }
+    const bool head = (headbits[j >> 5] >> (j & 31)) & 1u;
+    if (!head && j > 0) {
+      const int64_t g = c - (int64_t)col[j - 1];
+      if (g <= 0) { long long k = 2 * j + 1; err = k < err ? k : err; continue; }
+      mg = g > mg ? g : mg;
+      miss += (g > 16);
+    }
+  }
+  mg = warp_max(mg); miss = warp_sum(miss); err = warp_min(err);
+  if ((threadIdx.x & 31) == 0) {
+    if (mg) atomicMax(&st->maxgap, mg);
+    if (miss) atomicAdd((unsigned long long*)&st->misses, (unsigned long long)miss);
+    if (err != LLONG_MAX) atomicMin(&st->col_err, err);
+  }
+}
+
+static int grid_for(int64_t work, int per_cta_min = kNT) {
+  int64_t g = (work + per_cta_min - 1) / per_cta_min;
+  if (g < 1) g = 1;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)g;
+}
+
+void launch_rowstats(const MatView& A, int64_t l_split, uint32_t* headbits, DevStats* st, cudaStream_t s) {
+  const int g = grid_for(A.m);
+  if (A.m == 0) return;
+  if (A.rp_bytes == 8)
+    rowstats_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.m, A.nnz, l_split, headbits, st);
+  else
+    rowstats_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.m, A.nnz, l_split, headbits, st);
+}
+
+void launch_validate_gaps(const MatView& A, const uint32_t* headbits, DevStats* st, cudaStream_t s) {
+  if (A.nnz == 0) return;
+  validate_gaps_kernel<<<grid_for(A.nnz), kNT, 0, s>>>(A.col, A.nnz, A.n_cols, headbits, st);
+}
+
+// ---- K2: tiles, merge splits -------------------------------------------------
+template <typename RP>
+__global__ void tile_rows_kernel(const RP* __restrict__ rp, int64_t m, int64_t C, int64_t T,
+                                 int32_t* __restrict__ tile_row, DevStats* st) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > T) return;
+  int64_t R;
+  if (k == 0) R = 0;
+  else if (k == T) R = m;
+  else { R = lower_bound_dev(rp, 0, m, k * C); R = R > m ? m : R; }
+  tile_row[k] = (int32_t)R;
+  // tile k (< T) has an incoming row iff rowptr[R_k] > k*C
+  if (k < T && (int64_t)rp[R] > k * C) atomicAdd((unsigned long long*)&st->n_incoming, 1ull);
+}
+
+void launch_tile_rows(const MatView& A, int64_t C, int64_t T, int32_t* tile_row, DevStats* st, cudaStream_t s) {
+  const int g = (int)((T + 1 + kNT - 1) / kNT);
+  if (A.rp_bytes == 8)
+    tile_rows_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.m, C, T, tile_row, st);
+  else
+    tile_rows_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.m, C, T, tile_row, st);
+}
+
+// split(d) = (i, d-i): binary search over [max(0,d-nnz), min(d,m)] advancing
+// while rowptr[mid+1] <= d-mid-1 (row end precedes the nonzero, ties to rows)
+template <typename RP>
+__global__ void merge_splits_kernel(const RP* __restrict__ rp, int64_t m, int64_t nnz, int64_t items, int64_t T,
+                                    int32_t* __restrict__ mrow, int64_t* __restrict__ mnnz) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > T) return;
+  int64_t d = k * items;
+  if (d > m + nnz) d = m + nnz;
+  int64_t lo = d - nnz > 0 ? d - nnz : 0, hi = d < m ? d : m;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)rp[mid + 1] <= d - mid - 1) lo = mid + 1; else hi = mid;
+  }
+  mrow[k] = (int32_t)lo;
+  mnnz[k] = d - lo;
+}
+
+void launch_merge_splits(const MatView& A, int64_t items, int64_t T, int32_t* mrow, int64_t* mnnz, cudaStream_t s) {
+  const int g = (int)((T + 1 + kNT - 1) / kNT);
+  if (A.rp_bytes == 8)
+    merge_splits_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.m, A.nnz, items, T, mrow, mnnz);
+  else
+    merge_splits_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.m, A.nnz, items, T, mrow, mnnz);
+}
+
+// ---- long rows: ordered compaction (count / scan / write) -------------------
+template <typename RP>
+__device__ __forceinline__ bool is_long(const RP* rp, int64_t i, int64_t l_split) {
+  return (int64_t)rp[i + 1] - (int64_t)rp[i] > l_split;
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(kNT) long_count_kernel(const RP* __restrict__ rp, int64_t m, int64_t l_split,
+                                                         int64_t rows_per_cta, int32_t* __restrict__ counts) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = r0 + rows_per_cta < m ? r0 + rows_per_cta : m;
+  int c = 0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kNT) c += is_long(rp, i, l_split);
+  c = warp_sum(c);
+  __shared__ int ws[kNT / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kNT / 32; ++w) t += ws[w];
+    counts[blockIdx.x] = t;
+  }
+}
+
+// single-CTA exclusive scan of n int64 values given by f(i), written to out[0..n]
+template <typename F>
+__device__ void cta_exclusive_scan(int64_t n, F f, int64_t* out) {
+  __shared__ int64_t wsum[kNT / 32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t base = 0; base < n; base += kNT) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < n ? f(i) : 0;
+    int64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    int64_t wpre = 0;
+    for (int q = 0; q < w; ++q) wpre += wsum[q];
+    if (i < n) out[i] = carry + wpre + inc - v;
+    __syncthreads();
+    if (threadIdx.x == kNT - 1) carry += wpre + inc;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+__global__ void __launch_bounds__(kNT) scan_counts_kernel(const int32_t* counts, int64_t nb, int64_t* offs) {
+  cta_exclusive_scan(nb, [&](int64_t i) { return (int64_t)counts[i]; }, offs);
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(kNT) long_write_kernel(const RP* __restrict__ rp, int64_t m, int64_t l_split,
+                                                         int64_t rows_per_cta, const int64_t* __restrict__ offs,
+                                                         int32_t* __restrict__ long_rows) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = r0 + rows_per_cta < m ? r0 + rows_per_cta : m;
+  __shared__ int wcnt[kNT / 32];
+  __shared__ int64_t base;
+  if (threadIdx.x == 0) base = offs[blockIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t b = r0; b < r1; b += kNT) {
+    const int64_t i = b + threadIdx.x;
+    const bool f = i < r1 && is_long(rp, i, l_split);
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wcnt[w] = __popc(bal);
+    __syncthreads();
+    int pre = 0;
+    for (int q = 0; q < w; ++q) pre += wcnt[q];
+    if (f) long_rows[base + pre + __popc(bal & ((1u << lane) - 1))] = (int32_t)i;
+    __syncthreads();
+    if (threadIdx.x == 0) { int t = 0; for (int q = 0; q < kNT / 32; ++q) t += wcnt[q]; base += t; }
+    __syncthreads();
+  }
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(kNT) chunk_prefix_kernel(const RP* __restrict__ rp, const int32_t* long_rows,
+                                                           int64_t n_long, int64_t chunk, int64_t* chunk_start) {
+  cta_exclusive_scan(n_long, [&](int64_t q) {
+    const int64_t r = long_rows[q];
+    const int64_t len = (int64_t)rp[r + 1] - (int64_t)rp[r];
+    return (len + chunk - 1) / chunk;
+  }, chunk_start);
+}
+
+void launch_long_rows(const MatView& A, int64_t l_split, int64_t chunk, int32_t* long_rows, int64_t n_long,
+                      int64_t* chunk_start, int32_t* scratch_counts, int nb, cudaStream_t s) {
+  // scratch_counts: nb int32 counts followed by (nb+1) int64 offsets (8-B aligned by the caller)
+  const int64_t rpc = (A.m + nb - 1) / nb;
+  int64_t* offs = reinterpret_cast<int64_t*>(scratch_counts + ((nb + 1) & ~1));
+  if (A.rp_bytes == 8) {
+    auto rp = (const int64_t*)A.rowptr;
+    long_count_kernel<<<nb, kNT, 0, s>>>(rp, A.m, l_split, rpc, scratch_counts);
+    scan_counts_kernel<<<1, kNT, 0, s>>>(scratch_counts, nb, offs);
+    long_write_kernel<<<nb, kNT, 0, s>>>(rp, A.m, l_split, rpc, offs, long_rows);
+    chunk_prefix_kernel<<<1, kNT, 0, s>>>(rp, long_rows, n_long, chunk, chunk_start);
+  } else {
+    auto rp = (const int32_t*)A.rowptr;
+    long_count_kernel<<<nb, kNT, 0, s>>>(rp, A.m, l_split, rpc, scratch_counts);
+    scan_counts_kernel<<<1, kNT, 0, s>>>(scratch_counts, nb, offs);
+    long_write_kernel<<<nb, kNT, 0, s>>>(rp, A.m, l_split, rpc, offs, long_rows);
+    chunk_prefix_kernel<<<1, kNT, 0, s>>>(rp, long_rows, n_long, chunk, chunk_start);
+  }
+}
+
+// ---- K3: delta colind ------------------------------------------------------------
+// dcol[j] = colind[j] - colind[j-1] for non-head j, 0 at row heads;
+// head[i] = colind[rowptr[i]] or n_cols for an empty row; anchor[k] = colind[k*C].
+__global__ void __launch_bounds__(kNT) d16_dcol_kernel(const int32_t* __restrict__ col, int64_t nnz,
+                                                       const uint32_t* __restrict__ headbits, uint16_t* dcol) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz; j += stride) {
+    const bool h = (headbits[j >> 5] >> (j & 31)) & 1u;
+    dcol[j] = h ? (uint16_t)0 : (uint16_t)(col[j] - col[j - 1]);
+  }
+}
+template <typename RP>
+__global__ void __launch_bounds__(kNT) d16_head_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ col,
+                                                       int64_t m, int64_t n_cols, int32_t* head) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const int64_t a = rp[i], b = rp[i + 1];
+    head[i] = b > a ? col[a] : (int32_t)n_cols;
+  }
+}
+__global__ void d16_anchor_kernel(const int32_t* __restrict__ col, int64_t nnz, int64_t C, int64_t T, int32_t* anchor) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < T) anchor[k] = k * C < nnz ? col[k * C] : 0;
+}
+
+void launch_d16_encode(const MatView& A, const uint32_t* headbits, int64_t C, int64_t T, uint16_t* dcol,
+                       int32_t* head, int32_t* anchor, cudaStream_t s) {
+  if (A.nnz) d16_dcol_kernel<<<grid_for(A.nnz), kNT, 0, s>>>(A.col, A.nnz, headbits, dcol);
+  if (A.m) {
+    if (A.rp_bytes == 8)
+      d16_head_kernel<int64_t><<<grid_for(A.m), kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, A.m, A.n_cols, head);
+    else
+      d16_head_kernel<int32_t><<<grid_for(A.m), kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, A.m, A.n_cols, head);
+  }
+  d16_anchor_kernel<<<(int)((T + kNT - 1) / kNT), kNT, 0, s>>>(A.col, A.nnz, C, T, anchor);
+}
+
+// rowptr slice of a shard: subtract the shard's first offset
+template <typename RP>
+__global__ void rebase_kernel(RP* rp, int64_t count, int64_t base) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) rp[i] = (RP)(rp[i] - base);
+}
+
+void launch_rebase(void* rowptr, int rp_bytes, int64_t count, int64_t base, cudaStream_t s) {
+  if (base == 0 || count == 0) return;
+  if (rp_bytes == 8) rebase_kernel<int64_t><<<grid_for(count), kNT, 0, s>>>((int64_t*)rowptr, count, base);
+  else rebase_kernel<int32_t><<<grid_for(count), kNT, 0, s>>>((int32_t*)rowptr, count, base);
+}
+
+}  // namespace spmv

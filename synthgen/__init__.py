@@ -46,6 +46,7 @@ def _lib():
         L.sg_vector.argtypes = [i64, i64, u64, ci, d, vp]
         L.sg_stencil_nnz_range.argtypes = [i64, ci, i64, i64]; L.sg_stencil_nnz_range.restype = i64
         L.sg_stencil_fill.argtypes = [i64, ci, d, d, ci, u64, i64, i64, i64, vp, ci, vp, vp]
+        L.sg_stencil_rowptr.argtypes = [i64, ci, i64, i64, vp, ci]
         L.sg_pick_rows.argtypes = [i64, i64, u64, vp]
         L.sg_randrows_nnz.argtypes = [i64, ci, i64, i64, i64]; L.sg_randrows_nnz.restype = i64
         L.sg_randrows_fill.argtypes = [i64, ci, i64, vp, i64, i64, u64, ci, u64, vp, ci, vp, vp]
@@ -121,6 +122,15 @@ def stencil(n, pts, diag=None, off=-1.0, rp64=False, val_mode=MODE_CONST, val_se
     L.sg_stencil_fill(n, pts, diag, off, val_mode, val_seed, rb, re, nz0, _p(rp), 8 if rp64 else 4, _p(ci), _p(va))
     x = vector(N, x_seed, x_mode, out=outs.get("x"))
     return CSR(N, rp, ci, va, x, name=f"stencil{pts}_{n}", meta={"rows": (rb, re), "nz0": nz0})
+
+
+def stencil_rowptr(n, pts, rp64=True, rows=None):
+    """Global rowptr of the pts-point stencil on n^3 (or of a row block, rebased)."""
+    N = n ** 3
+    rb, re = rows if rows is not None else (0, N)
+    rp = np.empty(re - rb + 1, np.int64 if rp64 else np.int32)
+    _lib().sg_stencil_rowptr(n, pts, rb, re, _p(rp), 8 if rp64 else 4)
+    return rp
 
 
 def randrows(n, k, diag=True, long_rows=None, k_long=0, col_seed=1, val_mode=MODE_U11, val_seed=2,

@@ -143,6 +143,15 @@ void sg_stencil_fill(int64_t n, int pts, double diag, double off, int val_mode, 
   }
 }
 
+// rowptr only, rows [rb, re), rebased to 0 (cheap: closed-form lengths).
+void sg_stencil_rowptr(int64_t n, int pts, int64_t rb, int64_t re, void* rowptr, int rp_bytes) {
+  const int64_t m = re - rb;
+  std::vector<int64_t> lens(m);
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < m; ++r) lens[r] = stencil_row_len(rb + r, n, pts);
+  prefix_rowptr(lens, rowptr, rp_bytes);
+}
+
 // Distinct sorted rows: `count` rows of [0,n) by rejection, stream (seed, t).
 void sg_pick_rows(int64_t n, int64_t count, uint64_t seed, int64_t* out) {
   std::vector<int64_t> got;

@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bar (BJ.north_star): |y_gpu[i] - y_ref[i]| <= 1e-12 * sum_j |a_ij x_j| for
+every row; bit-exact for integer work (plan structures, D16 round trip,
+features, validation codes) and for dyadic inputs where every summation
+order is exact.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synthgen as sg
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+spmv = pytest.importorskip("paper_1711_05487_b200")
+
+TOL = 1e-12
+
+
+def assert_bound(y, m, rows=None, tol=TOL):
+    if rows is None:
+        yr = oracle.spmv(m.rowptr, m.colind, m.vals, m.x)
+        s = oracle.absrow(m.rowptr, m.colind, m.vals, m.x)
+        yy = y
+    else:
+        yr = oracle.spmv_rows(m.rowptr, m.colind, m.vals, m.x, rows)
+        s = oracle.absrow(m.rowptr, m.colind, m.vals, m.x, rows)
+        yy = y[rows]
+    err = np.abs(yy - yr)
+    bad = np.nonzero(err > tol * s)[0]
+    assert bad.size == 0, f"{bad.size} rows over the bound, first {bad[:5]}, err {err[bad[:5]]}, s {s[bad[:5]]}"
+    # empty rows must be exactly zero (bound RHS is 0)
+    return err
+
+
+VARIANTS = [("vector", 1), ("vector", 2), ("vector", 8), ("vector", 32), ("stream", 1), ("stream", 4),
+            ("stream", 8), ("stream", 32), ("merge", 0), ("split", 4), ("split", 32)]
+
+SUITE = sg.small_suite(seed=21)
+
+
+@pytest.mark.parametrize("variant,vs", VARIANTS)
+@pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
+def test_small_suite_all_variants(name, m, variant, vs):
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant=variant, force_vs=vs, l_split=64,
+                  tile_nnz=256)
+    y = p.execute(m.x)
+    assert_bound(y, m)
+    assert p.info()["variant"] == variant
+
+
+@pytest.mark.parametrize("variant,vs", VARIANTS + [("stream_d16", 8)])
+@pytest.mark.parametrize("name,m", sg.small_suite(seed=4, val_mode=sg.MODE_DYADIC, x_mode=sg.MODE_DYADIC),
+                         ids=[n for n, _ in SUITE])
+def test_dyadic_bit_exact(name, m, variant, vs):
+    kw = dict(force_vs=vs, l_split=64, tile_nnz=512)
+    if variant == "stream_d16":
+        variant, kw["d16"] = "stream", 1
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant=variant, **kw)
+    y = p.execute(m.x)
+    assert np.array_equal(y, oracle.spmv(m.rowptr, m.colind, m.vals, m.x))
+
+
+@pytest.mark.parametrize("tile", [256, 1024, 2048, 4096])
+@pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
+def test_stream_d16_and_structures(name, m, tile):
+    w, mg, dcol, head = oracle.d16_encode(m.rowptr, m.colind)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", d16=1, tile_nnz=tile)
+    info = p.info()
+    assert np.array_equal(p.export("tile_rows"), oracle.tile_rows(m.rowptr, tile))
+    if w == 0:
+        assert info["sel"]["d16"] == 0
+    else:
+        assert info["sel"]["d16"] == 1 and info["d16_width"] == w
+        if m.nnz:
+            assert np.array_equal(p.export("dcol"), dcol)
+            assert np.array_equal(p.export("head"), head)
+            assert np.array_equal(p.export("anchor"), oracle.tile_anchor(m.colind, tile))
+            assert np.array_equal(p.export("decoded"), m.colind)  # round trip
+    assert_bound(p.execute(m.x), m)
+
+
+@pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
+def test_plan_structures_bit_exact(name, m):
+    pm = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="merge")
+    si, sj = oracle.merge_splits(m.rowptr, 2048)
+    assert np.array_equal(pm.export("merge_rows"), si) and np.array_equal(pm.export("merge_nnz"), sj)
+    for L, C in ((64, 256), (4096, 8192), (0, 256)):
+        ps = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="split", l_split=L,
+                       long_chunk=C)
+        crow, cb, ce = oracle.long_chunks(m.rowptr, L if L else 4096, C)
+        assert np.array_equal(ps.export("chunk_row"), crow)
+        assert np.array_equal(ps.export("chunk_begin"), cb)
+        assert np.array_equal(ps.export("chunk_end"), ce)
+        assert_bound(ps.execute(m.x), m)
+    # features: exact integers, identical doubles (same formula, IEEE sqrt)
+    f = oracle.features(m.rowptr, m.colind)
+    g = pm.info()["feat"]
+    for k, v in f.items():
+        assert g[k] == v, k
+
+
+@pytest.mark.parametrize("rp,ci,n,nnz", [
+    ([1, 1, 2], [0, 1], 2, 2),
+    ([0, 1, 3], [0, 1], 2, 2),
+    ([0, 2, 1, 2], [0, 1], 3, 2),
+    ([0, 1, 2], [0, 2], 2, 2),
+    ([0, 1, 2], [-1, 0], 2, 2),
+    ([0, 2, 4], [0, 1, 1, 1], 2, 4),
+    ([0, 2, 4], [1, 0, 0, 1], 2, 4),
+    ([0, 3, 6], [0, 1, 1, 0, 5, 1], 2, 6),
+])
+def test_validation_matches_oracle(rp, ci, n, nnz):
+    code, where = oracle.validate(n, nnz, np.array(rp), np.array(ci, np.int32))
+    assert code != 0
+    rp64 = np.array(rp, np.int64)
+    with pytest.raises(spmv.SpmvError) as e:
+        spmv.Plan(rp64[: n + 1] if rp64.size > n + 1 else rp64, np.array(ci[:max(nnz, 0)], np.int32),
+                  np.ones(len(ci)), n_cols=n)
+    assert e.value.status == -2
+    assert f"code {code} " in e.value.msg and e.value.msg.endswith(f" {where}"), e.value.msg
+
+
+def test_valid_edge_cases():
+    # all-empty matrix, single row, zero rows
+    for rp, ci, n in (([0, 0, 0, 0], [], 3), ([0, 1], [0], 1), ([0], [], 0)):
+        for v in ("vector", "stream", "merge", "split"):
+            p = spmv.Plan(np.array(rp, np.int64), np.array(ci, np.int32), np.ones(len(ci)), n_cols=max(n, 1),
+                          force_variant=v)
+            y = p.execute(np.full(max(n, 1), 3.0), np.full(n, 7.0) if n else np.zeros(0))
+            assert np.array_equal(y, oracle.spmv(np.array(rp), np.array(ci, np.int32), np.ones(len(ci)),
+                                                 np.full(max(n, 1), 3.0)))
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4])
+def test_configs_full_auto_selection(c):
+    m = sg.config(c)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals)
+    y = p.execute(m.x)
+    assert_bound(y, m)
+    info = p.info()
+    f = oracle.features(m.rowptr, m.colind)
+    props = spmv.device_query(0)
+    o = oracle.select(f, props["l2_bytes"], props["access_window_max"], m.rowptr.dtype.itemsize)
+    assert (info["sel"]["variant"], info["sel"]["vs"], bool(info["sel"]["d16"]), bool(info["sel"]["xwin"])) == \
+        (o.variant, o.vs, o.d16, o.xwin)
+
+
+@pytest.mark.parametrize("c", [2, 3, 4])
+@pytest.mark.parametrize("variant", ["vector", "stream", "merge", "split"])
+def test_configs_full_forced_variants(c, variant):
+    m = sg.config(c)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=variant)
+    assert_bound(p.execute(m.x), m)
+
+
+def test_stencil_ones_bit_exact():
+    # 7-pt A*1 counts missing neighbours exactly -> bit-equal
+    m = sg.config(2)
+    ones = np.ones(m.n)
+    ref = oracle.spmv(m.rowptr, m.colind, m.vals, ones)
+    for v in ("vector", "stream", "merge", "split"):
+        for d16 in (0, 1):
+            p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=v, d16=d16)
+            assert np.array_equal(p.execute(ones), ref)
+
+
+def test_device_and_host_buffers_agree():
+    m = sg.config(2)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals)
+    y_host = p.execute(m.x)
+    xd = torch.from_numpy(m.x).cuda()
+    yd = torch.empty(m.n, dtype=torch.float64, device="cuda")
+    p.execute(xd, yd)
+    assert np.array_equal(yd.cpu().numpy(), y_host)
+    # plan-resident buffers (the timed path)
+    p2 = spmv.Plan(torch.from_numpy(m.rowptr).cuda(), torch.from_numpy(m.colind).cuda(),
+                   torch.from_numpy(m.vals).cuda())
+    assert p2.info()["variant"] == p.info()["variant"]
+    p2.execute(xd, yd)
+    torch.cuda.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), y_host)
+
+
+def test_deterministic_repeat():
+    m = sg.config(3, small=True)
+    for v in ("vector", "stream", "merge", "split"):
+        p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=v)
+        y0 = p.execute(m.x)
+        for _ in range(3):
+            assert np.array_equal(p.execute(m.x), y0)
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("variant", ["vector", "stream", "merge", "split"])
+def test_emulated_shards(G, variant):
+    m = sg.config(4, small=True)
+    p1 = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=variant, force_vs=8)
+    pg = spmv.Plan(m.rowptr, m.colind, m.vals, ngpus=G, emulate_devices=1, force_variant=variant, force_vs=8)
+    assert pg.info()["shard_bounds"] == oracle.shard_bounds(m.rowptr, G).tolist()
+    yg = pg.execute(m.x)
+    assert_bound(yg, m)
+    if variant == "vector":  # fixed per-row order: bit-equal across shard counts
+        assert np.array_equal(yg, p1.execute(m.x))
+
+
+def test_iterated_mode_vs_oracle():
+    m = sg.config(5, small=True)
+    K = 100
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, K)
+    assert rc == 0
+    for G in (1, 3):
+        p = spmv.Plan(m.rowptr, m.colind, m.vals, ngpus=G, emulate_devices=1)
+        xg, nug = p.iterate(m.x, K)
+        # SURVEY 8(c3) #21 end-to-end tolerances
+        assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
+        assert abs(nug[-1] - nur[-1]) <= 1e-12 * nur[-1]
+        assert np.all(np.abs(nug - nur) <= 1e-12 * nur)
+        # stepwise: y_k from the GPU's own x_k obeys the per-row bound
+        for k in (1, 49):
+            xk, _ = p.iterate(m.x, k)
+            yk = p.execute(xk)
+            mk = sg.CSR(m.n, m.rowptr, m.colind, m.vals, xk)
+            assert_bound(yk, mk)
+        assert np.all(np.diff(nug[1:]) >= -1e-13 * nug[1:-1])  # monotone for symmetric A
+
+
+def test_iterated_zero_norm():
+    rp = np.zeros(11, np.int64)
+    p = spmv.Plan(rp, np.zeros(0, np.int32), np.zeros(0))
+    with pytest.raises(spmv.SpmvError) as e:
+        p.iterate(np.ones(10), 3)
+    assert e.value.status == -7
+
+
+@pytest.mark.slow
+def test_c5_full_sampled_rows_and_properties():
+    m = sg.config(5)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals)
+    info = p.info()
+    assert info["feat"]["nnz"] == 1520875000 and info["feat"]["maxgap"] == 384 * 384 - 384 - 1
+    y = p.execute(m.x)
+    g = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([g.integers(0, m.n, 200000), np.arange(5000), m.n - 1 - np.arange(5000),
+                                     np.arange(0, m.n, 147457)]))
+    assert_bound(y, m, rows)
+    # A*1 closed form on every row (exact in any order)
+    y1 = p.execute(np.ones(m.n))
+    assert set(np.unique(y1).tolist()) == {0.0, 9.0, 15.0, 19.0}
+    n = 384
+    i = np.arange(m.n, dtype=np.int64)
+    prod = np.ones(m.n)
+    for c in (i % n, (i // n) % n, i // (n * n)):
+        prod *= 3 - (c == 0).astype(float) - (c == n - 1)
+    assert np.array_equal(y1, 27.0 - prod)
