@@ -71,7 +71,8 @@ typedef struct spmv_options {
   int64_t merge_items;     /* MERGE items (rows + nnz) per CTA (0 = 2048; multiple of 256) */
   int64_t long_chunk;      /* SPLIT chunk size in nonzeros (0 = 8192; multiple of 256) */
   int32_t emulate_devices; /* ngpus > 1: 1 = place every shard on the current device (tests) */
-  int32_t reserved[7];
+  int32_t stages;          /* STREAM smem ring depth: 0 = auto (deepest of 4/3/2 fitting 2 CTAs/SM), else 2..8 */
+  int32_t reserved[6];
 } spmv_options;
 
 /* Theta(N) features (Table I) + counts used by the selection.

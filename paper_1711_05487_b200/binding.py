@@ -31,7 +31,7 @@ class Options(ctypes.Structure):
                 ("d16", ctypes.c_int32), ("xwin", ctypes.c_int32), ("validate", ctypes.c_int32),
                 ("l_split", ctypes.c_int64), ("k_long", ctypes.c_int64), ("tile_nnz", ctypes.c_int64),
                 ("merge_items", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
-                ("emulate_devices", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("emulate_devices", ctypes.c_int32), ("stages", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
 
     @classmethod
     def make(cls, **kw):

@@ -242,6 +242,14 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   vs = std::min(32, std::max(2, vs));
   int variant = skew ? SPMV_VARIANT_MERGE : longr ? SPMV_VARIANT_SPLIT : avg_s <= 32 ? SPMV_VARIANT_STREAM
                                                                                      : SPMV_VARIANT_VECTOR;
+  if (variant == SPMV_VARIANT_STREAM) {
+    // cta_stream: size the lane group so a tile's rows cover its 256 consumer
+    // lanes: VS = pow2ceil(avg_s * 256 / C), clamp [1, 32]
+    const int64_t C = o.tile_nnz > 0 ? o.tile_nnz : 2048;
+    const double want = avg_s * 256.0 / (double)C;
+    vs = want > 1.0 ? pow2ceil((int64_t)std::ceil(want)) : 1;
+    vs = std::min(32, vs);
+  }
   if (avg_s <= 4) classes |= SPMV_CLASS_CMP;
   if (ws > d.l2_bytes / 2 && !(classes & SPMV_CLASS_IMB)) classes |= SPMV_CLASS_MB;
   bool d16 = (classes & SPMV_CLASS_MB) && variant == SPMV_VARIANT_STREAM && f.maxgap <= 65535;
@@ -275,6 +283,7 @@ void validate_options(const spmv_options& o) {
   if (o.long_chunk != 0 && (o.long_chunk % 256 || o.long_chunk < 256))
     fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
   if (o.l_split < 0 || o.k_long < 0) fail(SPMV_E_ARG, "negative l_split / k_long");
+  if (o.stages < 0 || o.stages == 1 || o.stages > 8) fail(SPMV_E_ARG, "stages must be 0 (auto) or in [2, 8]");
 }
 
 void features_from_stats(const std::vector<DevStats>& st, const std::vector<int64_t>& m, spmv_features& f) {
@@ -520,7 +529,14 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
       ck(cudaStreamSynchronize(s.stream), "tiles");
       s.need_fixup = s.hs.n_incoming > 0;
-      s.stages = 4;
+      // ring depth: the deepest of 4/3/2 stages that still fits two CTAs per SM
+      if (opt.stages > 0) {
+        s.stages = opt.stages;
+      } else {
+        s.stages = 2;
+        for (int st = 4; st >= 2; --st)
+          if (2 * stream_smem_bytes(s.C, st, rp_bytes, P->sel.d16) + 2048 <= 228 * 1024) { s.stages = st; break; }
+      }
       ExecArgs a = P->args(s, nullptr, nullptr);
       s.stream_grid = stream_prepare(a);
       if (s.stream_grid < 0) { cudaGetLastError(); s.stages = 2; a = P->args(s, nullptr, nullptr); s.stream_grid = stream_prepare(a); }
@@ -849,7 +865,7 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
         if (!dst || count == 0) break;
         int32_t* tmp = nullptr;
         ck(cudaMalloc(&tmp, (size_t)s.nnz * 4 + 64), "cudaMalloc");
-        launch_d16_decode_export(s.view(), s.dcol, s.head, s.anchor, s.tile_row, s.C, s.T, tmp, s.stream);
+        launch_d16_decode_export(s.view(), s.dcol, s.head, s.anchor, s.tile_row, s.C, s.T, p->sel.vs, tmp, s.stream);
         g_launches += 1;
         cudaError_t e = cudaStreamSynchronize(s.stream);
         if (e == cudaSuccess) e = cudaMemcpy(dst, tmp, (size_t)s.nnz * 4, cudaMemcpyDeviceToHost);

@@ -37,7 +37,8 @@ void launch_long_rows(const MatView& A, int64_t l_split, int64_t chunk, int32_t*
 void launch_d16_encode(const MatView& A, const uint32_t* headbits, int64_t C, int64_t T, uint16_t* dcol,
                        int32_t* head, int32_t* anchor, cudaStream_t s);
 void launch_d16_decode_export(const MatView& A, const uint16_t* dcol, const int32_t* head, const int32_t* anchor,
-                              const int32_t* tile_row, int64_t C, int64_t T, int32_t* out, cudaStream_t s);
+                              const int32_t* tile_row, int64_t C, int64_t T, int vs, int32_t* out, cudaStream_t s);
+void launch_fixup(const int32_t* crow, const double* cval, int64_t T, double* y, int set, cudaStream_t s);
 
 // ---- SpMV variants ----------------------------------------------------------
 struct ExecArgs {

@@ -1,0 +1,401 @@
+// stream.cu -- cta_stream: the MB-class kernel (Table II "vectorization" +
+// delta colind) re-designed for sm_100a.
+//
+// Persistent, warp-specialised CTAs. Tile k covers the fixed nonzero range
+// [k*C, min((k+1)*C, nnz)) and owns rows [R_k, R_{k+1}).
+//  * producer warp (one elected lane): TMA bulk copies (cp.async.bulk +
+//    mbarrier complete_tx, L2 evict_first) of the tile's values, colind (or
+//    16-bit deltas), rowptr slice and (D16) row heads into an S-stage smem
+//    ring; it refills a stage once every consumer warp has released it
+//    through the stage's "empty" mbarrier. No __syncthreads anywhere.
+//  * 8 consumer warps: VS lanes per row, rows of the tile in parallel; every
+//    lane forms its products from smem with 4 gathers of x in flight (x read
+//    through L1/L2; neighbouring rows share x lines), subgroup butterfly sum.
+//    The row entering the tile from the previous one is written to carry[k]
+//    (ordered fix-up kernel), every owned row to y (its head part if it
+//    continues into later tiles).
+//  * D16: each lane owns a contiguous piece of the row; the absolute column is
+//    rebuilt as head[r] (or the tile anchor for the entering row) + a
+//    subgroup exclusive scan of the lanes' delta sums + a running sum.
+#include "common.cuh"
+#include "internal.h"
+
+namespace spmv {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = 32 * kConsumerWarps;
+constexpr int kStreamThreads = kConsumers + 32;
+
+struct TileMeta {
+  int32_t R0, R1;   // owned rows [R0, R1)
+  int32_t rp_off;   // element offset of row max(R0-1,0) in the staged rowptr slice; -1 = read global
+  int32_t hd_off;   // element offset of row R0 in the staged head slice; -1 = read global
+  int32_t anchor;   // D16: absolute column of nonzero k*C
+  int32_t pad_[3];
+};
+
+__host__ __device__ __forceinline__ size_t al128(size_t v) { return (v + 127) & ~(size_t)127; }
+
+struct StreamLayout {
+  size_t vals, idx, rp, hd, stage, full, empty, meta, total;
+  uint32_t rp_cap, hd_cap;  // bytes
+};
+
+__host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int rp_bytes, bool d16) {
+  StreamLayout L;
+  const size_t rows_cap = (size_t)C / 2 + 32;
+  L.rp_cap = (uint32_t)(((rows_cap + 2) * rp_bytes + 32 + 15) & ~(size_t)15);
+  L.hd_cap = d16 ? (uint32_t)(((rows_cap + 2) * 4 + 32 + 15) & ~(size_t)15) : 0u;
+  L.vals = 0;
+  L.idx = al128((size_t)C * 8);
+  L.rp = al128(L.idx + (size_t)C * (d16 ? 2 : 4));
+  L.hd = al128(L.rp + L.rp_cap);
+  L.stage = al128(L.hd + L.hd_cap);
+  size_t o = L.stage * stages;
+  L.full = o; o += 8 * (size_t)stages;
+  L.empty = o; o += 8 * (size_t)stages;
+  L.meta = al128(o); o = L.meta + sizeof(TileMeta) * (size_t)stages;
+  L.total = al128(o);
+  return L;
+}
+
+size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, bool d16) {
+  return stream_layout(C, stages, rp_bytes, d16).total;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <typename RP>
+struct StreamP {
+  const RP* rp;
+  const void* idx;  // int32 colind or uint16 dcol
+  const int32_t* head;
+  const int32_t* anchor;
+  const double* val;
+  const double* x;
+  double* y;
+  const int32_t* tile_row;
+  int32_t* carry_row;
+  double* carry_val;
+  int64_t nnz, C, T;
+  int stages;
+};
+
+// D16 columns of one row's lane piece: calls f(t, col) for t in the lane's
+// contiguous sub-range of [ls, le). Every lane of the VS-group must call it.
+template <int VS, typename F>
+__device__ __forceinline__ void d16_row_cols(const uint16_t* __restrict__ d_s, int ls, int le, int lane, int base,
+                                             F&& f) {
+  const int len = le - ls;
+  const int chunk = (len + VS - 1) / VS;
+  int a = ls + lane * chunk;
+  a = a < le ? a : le;
+  int b = a + chunk;
+  b = b < le ? b : le;
+  uint32_t ps = 0;
+  for (int t = a; t < b; ++t) ps += (t == ls) ? 0u : (uint32_t)d_s[t];
+  uint32_t inc = ps;
+#pragma unroll
+  for (int o = 1; o < VS; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o, VS);
+    if (lane >= o) inc += v;
+  }
+  int c = base + (int)(inc - ps);
+#pragma unroll 4
+  for (int t = a; t < b; ++t) {
+    c += (t == ls) ? 0 : (int)d_s[t];
+    f(t, c);
+  }
+}
+
+template <int VS, typename RP, bool D16>
+__global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP> p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), D16);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.empty);
+  TileMeta* meta = reinterpret_cast<TileMeta*>(smem + L.meta);
+  constexpr int IB = D16 ? 2 : 4;
+  constexpr int RPB = (int)sizeof(RP);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (threadIdx.x < 32) {
+    // ------------------------------ producer ------------------------------
+    if (threadIdx.x == 0) {
+      const uint64_t pol = policy_evict_first();
+      int i = 0;
+      for (int64_t k = blockIdx.x; k < p.T; k += gridDim.x, ++i) {
+        const int s = i % p.stages;
+        if (i >= p.stages) mbar_wait(&empty[s], (uint32_t)(((i / p.stages) - 1) & 1));
+        const int64_t R0 = ld_ro(p.tile_row + k), R1 = ld_ro(p.tile_row + k + 1);
+        const int64_t t0 = k * p.C;
+        const int64_t cnt = (p.nnz - t0) < p.C ? (p.nnz - t0) : p.C;
+        const uint32_t vb = (uint32_t)((cnt * 8 + 15) & ~15ll);
+        const uint32_t ib = (uint32_t)((cnt * IB + 15) & ~15ll);
+        const int64_t fr0 = R0 > 0 ? R0 - 1 : 0;
+        const int64_t b0 = (fr0 * RPB) & ~15ll, b1 = ((R1 + 1) * RPB + 15) & ~15ll;
+        const bool rp_ok = (b1 - b0) <= (int64_t)L.rp_cap;
+        uint32_t hb = 0;
+        int64_t h0 = 0;
+        bool hd_ok = false;
+        TileMeta mt;
+        mt.R0 = (int32_t)R0;
+        mt.R1 = (int32_t)R1;
+        mt.rp_off = rp_ok ? (int32_t)((fr0 * RPB - b0) / RPB) : -1;
+        mt.hd_off = -1;
+        mt.anchor = 0;
+        if (D16) {
+          h0 = (R0 * 4) & ~15ll;
+          const int64_t h1 = (R1 * 4 + 15) & ~15ll;
+          hd_ok = (h1 - h0) <= (int64_t)L.hd_cap;
+          hb = hd_ok ? (uint32_t)(h1 - h0) : 0u;
+          mt.hd_off = hd_ok ? (int32_t)((R0 * 4 - h0) / 4) : -1;
+          mt.anchor = ld_ro(p.anchor + k);
+        }
+        meta[s] = mt;
+        unsigned char* st = smem + L.stage * s;
+        mbar_arrive_expect_tx(&full[s], vb + ib + (rp_ok ? (uint32_t)(b1 - b0) : 0u) + hb);
+        if (vb) {
+          bulk_g2s(st + L.vals, p.val + t0, vb, &full[s], pol);
+          bulk_g2s(st + L.idx, static_cast<const unsigned char*>(p.idx) + t0 * IB, ib, &full[s], pol);
+        }
+        if (rp_ok) bulk_g2s(st + L.rp, reinterpret_cast<const unsigned char*>(p.rp) + b0, (uint32_t)(b1 - b0),
+                            &full[s], pol);
+        if (hb) bulk_g2s(st + L.hd, reinterpret_cast<const unsigned char*>(p.head) + h0, hb, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------- consumers --------------------------------
+  const int ct = threadIdx.x - 32;
+  const int cw = ct >> 5;
+  constexpr int GPW = 32 / VS;
+  constexpr int NG = kConsumers / VS;
+  const int lane = ct % VS;
+  const int gi = (ct & 31) / VS;
+  int i = 0;
+  for (int64_t k = blockIdx.x; k < p.T; k += gridDim.x, ++i) {
+    const int s = i % p.stages;
+    mbar_wait(&full[s], (uint32_t)((i / p.stages) & 1));
+    const TileMeta mt = meta[s];
+    const unsigned char* st = smem + L.stage * s;
+    const double* vals_s = reinterpret_cast<const double*>(st + L.vals);
+    const RP* rp_s = reinterpret_cast<const RP*>(st + L.rp);
+    const int64_t t0 = k * p.C;
+    const int64_t t1 = (t0 + p.C) < p.nnz ? (t0 + p.C) : p.nnz;
+    const int64_t R0 = mt.R0, R1 = mt.R1;
+    const int64_t fr0 = R0 > 0 ? R0 - 1 : 0;
+    auto rows = [&](int64_t r) -> int64_t {
+      return mt.rp_off >= 0 ? (int64_t)rp_s[r - fr0 + mt.rp_off] : (int64_t)ld_ro(p.rp + r);
+    };
+    const bool incoming = R0 > 0 && rows(R0) > t0;
+    const int64_t fr = R0 - (incoming ? 1 : 0);
+    const int nloc = (int)(R1 - R0) + (incoming ? 1 : 0);
+
+    for (int qb = cw * GPW; qb < nloc; qb += NG) {
+      const int q = qb + gi;
+      const bool active = q < nloc;
+      int ls = 0, le = 0;
+      int64_t r = 0;
+      if (active) {
+        r = fr + q;
+        const int64_t a = rows(r), b = rows(r + 1);
+        ls = (int)((a > t0 ? a : t0) - t0);
+        le = (int)((b < t1 ? b : t1) - t0);
+      }
+      double acc;
+      if (!D16) {
+        const int32_t* idx_s = reinterpret_cast<const int32_t*>(st + L.idx);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int l = ls + lane;
+        for (; l + 3 * VS < le; l += 4 * VS) {
+          const int c0 = idx_s[l], c1 = idx_s[l + VS], c2 = idx_s[l + 2 * VS], c3 = idx_s[l + 3 * VS];
+          const double x0 = ld_x(p.x + c0), x1 = ld_x(p.x + c1), x2 = ld_x(p.x + c2), x3 = ld_x(p.x + c3);
+          a0 = fma(vals_s[l], x0, a0);
+          a1 = fma(vals_s[l + VS], x1, a1);
+          a2 = fma(vals_s[l + 2 * VS], x2, a2);
+          a3 = fma(vals_s[l + 3 * VS], x3, a3);
+        }
+        for (; l < le; l += VS) a0 = fma(vals_s[l], ld_x(p.x + idx_s[l]), a0);
+        acc = (a0 + a1) + (a2 + a3);
+      } else {
+        const uint16_t* d_s = reinterpret_cast<const uint16_t*>(st + L.idx);
+        const int32_t* hd_s = reinterpret_cast<const int32_t*>(st + L.hd);
+        int base = mt.anchor;
+        if (active && (!incoming || q > 0))
+          base = mt.hd_off >= 0 ? hd_s[r - R0 + mt.hd_off] : ld_ro(p.head + r);
+        double a0 = 0.0;
+        d16_row_cols<VS>(d_s, ls, le, lane, base, [&](int t, int c) { a0 = fma(vals_s[t], ld_x(p.x + c), a0); });
+        acc = a0;
+      }
+      acc = group_sum<VS>(acc);
+      if (active && lane == 0) {
+        if (incoming && q == 0) {
+          p.carry_row[k] = (int32_t)r;
+          p.carry_val[k] = acc;
+        } else {
+          p.y[r] = acc;
+        }
+      }
+    }
+    if (!incoming && ct == 0) p.carry_row[k] = -1;
+    __syncwarp();
+    if ((ct & 31) == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+template <int VS, typename RP, bool D16>
+static int stream_prepare_t(const ExecArgs& a) {
+  const size_t smem = stream_smem_bytes(a.C, a.stages, sizeof(RP), D16);
+  if (cudaFuncSetAttribute(stream_kernel<VS, RP, D16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return -1;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_kernel<VS, RP, D16>, kStreamThreads, smem) !=
+          cudaSuccess ||
+      per_sm < 1)
+    return -1;
+  int64_t grid = (int64_t)a.sm_count * per_sm;
+  if (grid > a.T) grid = a.T;
+  return (int)grid;
+}
+
+template <int VS, typename RP, bool D16>
+static void stream_launch_t(const ExecArgs& a, cudaStream_t s) {
+  StreamP<RP> p;
+  p.rp = (const RP*)a.A.rowptr;
+  p.idx = D16 ? (const void*)a.dcol : (const void*)a.A.col;
+  p.head = a.head;
+  p.anchor = a.anchor;
+  p.val = a.A.val;
+  p.x = a.x;
+  p.y = a.y;
+  p.tile_row = a.tile_row;
+  p.carry_row = a.carry_row;
+  p.carry_val = a.carry_val;
+  p.nnz = a.A.nnz;
+  p.C = a.C;
+  p.T = a.T;
+  p.stages = a.stages;
+  const size_t smem = stream_smem_bytes(a.C, a.stages, sizeof(RP), D16);
+  stream_kernel<VS, RP, D16><<<a.stream_grid, kStreamThreads, smem, s>>>(p);
+}
+
+template <typename RP, bool D16, bool PREP>
+static int stream_vs(const ExecArgs& a, cudaStream_t s) {
+#define SPMV_VS_CASE(V)                                  \
+  case V:                                                \
+    if (PREP) return stream_prepare_t<V, RP, D16>(a);    \
+    stream_launch_t<V, RP, D16>(a, s);                   \
+    return 0;
+  switch (a.vs) {
+    SPMV_VS_CASE(1)
+    SPMV_VS_CASE(2)
+    SPMV_VS_CASE(4)
+    SPMV_VS_CASE(8)
+    SPMV_VS_CASE(16)
+    default:
+      if (PREP) return stream_prepare_t<32, RP, D16>(a);
+      stream_launch_t<32, RP, D16>(a, s);
+      return 0;
+  }
+#undef SPMV_VS_CASE
+}
+
+template <bool PREP>
+static int stream_dispatch(const ExecArgs& a, cudaStream_t s) {
+  const bool d16 = a.dcol != nullptr;
+  if (a.A.rp_bytes == 8) return d16 ? stream_vs<int64_t, true, PREP>(a, s) : stream_vs<int64_t, false, PREP>(a, s);
+  return d16 ? stream_vs<int32_t, true, PREP>(a, s) : stream_vs<int32_t, false, PREP>(a, s);
+}
+
+int stream_prepare(const ExecArgs& a) { return stream_dispatch<true>(a, nullptr); }
+
+int launch_stream(const ExecArgs& a, cudaStream_t s) {
+  int n = 0;
+  if (a.stage != 2) {
+    stream_dispatch<false>(a, s);
+    ++n;
+  }
+  if (a.need_fixup && a.stage != 1) {
+    launch_fixup(a.carry_row, a.carry_val, a.T, a.y, 0, s);
+    ++n;
+  }
+  return n;
+}
+
+// Export: re-decode the delta colind on the device with the STREAM kernel's
+// own per-row decoder (bit-exact round trip).
+template <int VS, typename RP>
+__global__ void __launch_bounds__(kNT) d16_decode_kernel(const RP* __restrict__ rp, const uint16_t* __restrict__ dcol,
+                                                         const int32_t* __restrict__ head,
+                                                         const int32_t* __restrict__ anchor,
+                                                         const int32_t* __restrict__ tile_row, int64_t nnz, int64_t C,
+                                                         int32_t* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint16_t* d_s = reinterpret_cast<uint16_t*>(smem);
+  const int64_t k = blockIdx.x;
+  const int64_t t0 = k * C, t1 = (t0 + C) < nnz ? (t0 + C) : nnz;
+  const int cnt = (int)(t1 - t0);
+  for (int l = threadIdx.x; l < cnt; l += kNT) d_s[l] = dcol[t0 + l];
+  __syncthreads();
+  const int64_t R0 = tile_row[k], R1 = tile_row[k + 1];
+  const bool incoming = R0 > 0 && (int64_t)rp[R0] > t0;
+  const int64_t fr = R0 - (incoming ? 1 : 0);
+  const int nloc = (int)(R1 - R0) + (incoming ? 1 : 0);
+  const int lane = threadIdx.x % VS, gi = (threadIdx.x & 31) / VS, w = threadIdx.x >> 5;
+  for (int qb = w * (32 / VS); qb < nloc; qb += kNT / VS) {
+    const int q = qb + gi;
+    const bool active = q < nloc;
+    int ls = 0, le = 0, base = anchor[k];
+    if (active) {
+      const int64_t r = fr + q;
+      const int64_t a = rp[r], b = rp[r + 1];
+      ls = (int)((a > t0 ? a : t0) - t0);
+      le = (int)((b < t1 ? b : t1) - t0);
+      if (!incoming || q > 0) base = head[r];
+    }
+    d16_row_cols<VS>(d_s, ls, le, lane, base, [&](int t, int c) { out[t0 + t] = c; });
+  }
+}
+
+template <int VS>
+static void d16_export_vs(const MatView& A, const uint16_t* dcol, const int32_t* head, const int32_t* anchor,
+                          const int32_t* tile_row, int64_t C, int64_t T, int32_t* out, cudaStream_t s) {
+  const size_t smem = (size_t)C * 2 + 16;
+  if (A.rp_bytes == 8) {
+    cudaFuncSetAttribute(d16_decode_kernel<VS, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    d16_decode_kernel<VS, int64_t><<<(int)T, kNT, smem, s>>>((const int64_t*)A.rowptr, dcol, head, anchor, tile_row,
+                                                             A.nnz, C, out);
+  } else {
+    cudaFuncSetAttribute(d16_decode_kernel<VS, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    d16_decode_kernel<VS, int32_t><<<(int)T, kNT, smem, s>>>((const int32_t*)A.rowptr, dcol, head, anchor, tile_row,
+                                                             A.nnz, C, out);
+  }
+}
+
+void launch_d16_decode_export(const MatView& A, const uint16_t* dcol, const int32_t* head, const int32_t* anchor,
+                              const int32_t* tile_row, int64_t C, int64_t T, int vs, int32_t* out, cudaStream_t s) {
+  if (A.nnz == 0) return;
+  switch (vs) {
+    case 1: d16_export_vs<1>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
+    case 2: d16_export_vs<2>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
+    case 4: d16_export_vs<4>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
+    case 8: d16_export_vs<8>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
+    case 16: d16_export_vs<16>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
+    default: d16_export_vs<32>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
+  }
+}
+
+}  // namespace spmv
