@@ -243,10 +243,10 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   int variant = skew ? SPMV_VARIANT_MERGE : longr ? SPMV_VARIANT_SPLIT : avg_s <= 32 ? SPMV_VARIANT_STREAM
                                                                                      : SPMV_VARIANT_VECTOR;
   if (variant == SPMV_VARIANT_STREAM) {
-    // cta_stream: size the lane group so a tile's rows cover its 256 consumer
-    // lanes: VS = pow2ceil(avg_s * 256 / C), clamp [1, 32]
-    const int64_t C = o.tile_nnz > 0 ? o.tile_nnz : 2048;
-    const double want = avg_s * 256.0 / (double)C;
+    // cta_stream: size the lane group so a tile's rows cover the 32 lanes of
+    // its consumer warp: VS = pow2ceil(avg_s * 32 / C), clamp [1, 32]
+    const int64_t C = o.tile_nnz > 0 ? o.tile_nnz : 512;
+    const double want = avg_s * 32.0 / (double)C;
     vs = want > 1.0 ? pow2ceil((int64_t)std::ceil(want)) : 1;
     vs = std::min(32, vs);
   }
@@ -277,13 +277,13 @@ void validate_options(const spmv_options& o) {
   if (o.force_vs != 0 && o.force_vs != 1 && o.force_vs != 2 && o.force_vs != 4 && o.force_vs != 8 &&
       o.force_vs != 16 && o.force_vs != 32)
     fail(SPMV_E_ARG, "force_vs %d not in {0,1,2,4,8,16,32}", o.force_vs);
-  if (o.tile_nnz != 0 && (o.tile_nnz % 256 || o.tile_nnz < 256 || o.tile_nnz > 16384))
-    fail(SPMV_E_ARG, "tile_nnz %lld must be a multiple of 256 in [256, 16384]", (long long)o.tile_nnz);
+  if (o.tile_nnz != 0 && (o.tile_nnz % 512 || o.tile_nnz < 512 || o.tile_nnz > 16384))
+    fail(SPMV_E_ARG, "tile_nnz %lld must be a multiple of 512 in [512, 16384]", (long long)o.tile_nnz);
   if (o.merge_items != 0 && o.merge_items != 2048) fail(SPMV_E_ARG, "merge_items must be 2048");
   if (o.long_chunk != 0 && (o.long_chunk % 256 || o.long_chunk < 256))
     fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
   if (o.l_split < 0 || o.k_long < 0) fail(SPMV_E_ARG, "negative l_split / k_long");
-  if (o.stages < 0 || o.stages == 1 || o.stages > 8) fail(SPMV_E_ARG, "stages must be 0 (auto) or in [2, 8]");
+  if (o.stages < 0 || o.stages == 1 || o.stages > 32) fail(SPMV_E_ARG, "stages must be 0 (auto) or in [2, 32]");
 }
 
 void features_from_stats(const std::vector<DevStats>& st, const std::vector<int64_t>& m, spmv_features& f) {
@@ -394,7 +394,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   P->opt = opt;
   P->l_split = opt.l_split > 0 ? opt.l_split : 4096;
   P->k_long = opt.k_long > 0 ? opt.k_long : 100;
-  P->C = opt.tile_nnz > 0 ? opt.tile_nnz : 2048;
+  P->C = opt.tile_nnz > 0 ? opt.tile_nnz : 512;
   P->items = 2048;
   P->chunk = opt.long_chunk > 0 ? opt.long_chunk : 8192;
   query_props(cur, P->props);
@@ -529,12 +529,13 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
       ck(cudaStreamSynchronize(s.stream), "tiles");
       s.need_fixup = s.hs.n_incoming > 0;
-      // ring depth: the deepest of 4/3/2 stages that still fits two CTAs per SM
+      // ring depth: the deepest of 16..2 stages that still fits two CTAs per SM
+      // (8 consumer warps each own a tile in compute; the rest stream in)
       if (opt.stages > 0) {
         s.stages = opt.stages;
       } else {
         s.stages = 2;
-        for (int st = 4; st >= 2; --st)
+        for (int st = 16; st >= 2; --st)
           if (2 * stream_smem_bytes(s.C, st, rp_bytes, P->sel.d16) + 2048 <= 228 * 1024) { s.stages = st; break; }
       }
       ExecArgs a = P->args(s, nullptr, nullptr);

@@ -1,30 +1,35 @@
 // stream.cu -- cta_stream: the MB-class kernel (Table II "vectorization" +
 // delta colind) re-designed for sm_100a.
 //
-// Persistent, warp-specialised CTAs. Tile k covers the fixed nonzero range
-// [k*C, min((k+1)*C, nnz)) and owns rows [R_k, R_{k+1}).
-//  * producer warp (one elected lane): TMA bulk copies (cp.async.bulk +
-//    mbarrier complete_tx, L2 evict_first) of the tile's values, colind (or
-//    16-bit deltas), rowptr slice and (D16) row heads into an S-stage smem
-//    ring; it refills a stage once every consumer warp has released it
-//    through the stage's "empty" mbarrier. No __syncthreads anywhere.
-//  * 8 consumer warps: VS lanes per row, rows of the tile in parallel; every
-//    lane forms its products from smem with 4 gathers of x in flight (x read
-//    through L1/L2; neighbouring rows share x lines), subgroup butterfly sum.
-//    The row entering the tile from the previous one is written to carry[k]
-//    (ordered fix-up kernel), every owned row to y (its head part if it
-//    continues into later tiles).
-//  * D16: each lane owns a contiguous piece of the row; the absolute column is
-//    rebuilt as head[r] (or the tile anchor for the entering row) + a
-//    subgroup exclusive scan of the lanes' delta sums + a running sum.
+// Persistent, warp-specialised CTAs, one consumer WARP per tile. Tile k
+// covers the fixed nonzero range [k*C, min((k+1)*C, nnz)) and owns rows
+// [R_k, R_{k+1}).
+//  * producer warp (one lane): TMA bulk copies (cp.async.bulk + mbarrier
+//    complete_tx, L2 evict_first) of the tile's values, colind (or 16-bit
+//    deltas), rowptr slice and (D16) row heads into an S-stage smem ring.
+//    Tile i of the CTA goes to stage i % S and consumer warp i % W; the
+//    producer refills a stage when its warp releases it (empty mbarrier).
+//    No __syncthreads after set-up: W tiles are in compute per CTA while the
+//    next S - W tiles stream in.
+//  * consumer warp, int32 colind: (1) products: each lane reads 4 consecutive
+//    colind / values with 128-bit smem loads and keeps C/32 x gathers in
+//    flight (x through L1/L2; neighbouring rows share x lines), products
+//    overwrite the values in smem; (2) rows: VS lanes per row sum the
+//    products, butterfly within the group.
+//  * consumer warp, D16: VS lanes per row, each lane owns a contiguous piece
+//    of the row; absolute columns are head[r] (or the tile anchor for the row
+//    entering the tile) + a subgroup exclusive scan of the lanes' delta sums
+//    + a running sum; gathers and FMAs follow the decode.
+//  The row entering the tile from the previous one goes to carry[k] (ordered
+//  fix-up kernel); every owned row is written to y (its head part if it
+//  continues into later tiles).
 #include "common.cuh"
 #include "internal.h"
 
 namespace spmv {
 
 constexpr int kConsumerWarps = 8;
-constexpr int kConsumers = 32 * kConsumerWarps;
-constexpr int kStreamThreads = kConsumers + 32;
+constexpr int kStreamThreads = 32 * (kConsumerWarps + 1);
 
 struct TileMeta {
   int32_t R0, R1;   // owned rows [R0, R1)
@@ -41,9 +46,11 @@ struct StreamLayout {
   uint32_t rp_cap, hd_cap;  // bytes
 };
 
+// rows staged per tile: C/4 + 32 (average row length >= ~4; sparser tiles
+// read rowptr from global memory, still correct)
 __host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int rp_bytes, bool d16) {
   StreamLayout L;
-  const size_t rows_cap = (size_t)C / 2 + 32;
+  const size_t rows_cap = (size_t)C / 4 + 32;
   L.rp_cap = (uint32_t)(((rows_cap + 2) * rp_bytes + 32 + 15) & ~(size_t)15);
   L.hd_cap = d16 ? (uint32_t)(((rows_cap + 2) * 4 + 32 + 15) & ~(size_t)15) : 0u;
   L.vals = 0;
@@ -119,11 +126,12 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
   TileMeta* meta = reinterpret_cast<TileMeta*>(smem + L.meta);
   constexpr int IB = D16 ? 2 : 4;
   constexpr int RPB = (int)sizeof(RP);
+  const int S = p.stages;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], 1);
     }
     fence_mbar_init();
   }
@@ -135,8 +143,8 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
       const uint64_t pol = policy_evict_first();
       int i = 0;
       for (int64_t k = blockIdx.x; k < p.T; k += gridDim.x, ++i) {
-        const int s = i % p.stages;
-        if (i >= p.stages) mbar_wait(&empty[s], (uint32_t)(((i / p.stages) - 1) & 1));
+        const int s = i % S;
+        if (i >= S) mbar_wait(&empty[s], (uint32_t)(((i / S) - 1) & 1));
         const int64_t R0 = ld_ro(p.tile_row + k), R1 = ld_ro(p.tile_row + k + 1);
         const int64_t t0 = k * p.C;
         const int64_t cnt = (p.nnz - t0) < p.C ? (p.nnz - t0) : p.C;
@@ -147,7 +155,6 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
         const bool rp_ok = (b1 - b0) <= (int64_t)L.rp_cap;
         uint32_t hb = 0;
         int64_t h0 = 0;
-        bool hd_ok = false;
         TileMeta mt;
         mt.R0 = (int32_t)R0;
         mt.R1 = (int32_t)R1;
@@ -157,7 +164,7 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
         if (D16) {
           h0 = (R0 * 4) & ~15ll;
           const int64_t h1 = (R1 * 4 + 15) & ~15ll;
-          hd_ok = (h1 - h0) <= (int64_t)L.hd_cap;
+          const bool hd_ok = (h1 - h0) <= (int64_t)L.hd_cap;
           hb = hd_ok ? (uint32_t)(h1 - h0) : 0u;
           mt.hd_off = hd_ok ? (int32_t)((R0 * 4 - h0) / 4) : -1;
           mt.anchor = ld_ro(p.anchor + k);
@@ -178,22 +185,23 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
   }
 
   // ------------------------------- consumers --------------------------------
-  const int ct = threadIdx.x - 32;
-  const int cw = ct >> 5;
+  const int w = (threadIdx.x >> 5) - 1;
+  const int lane32 = threadIdx.x & 31;
   constexpr int GPW = 32 / VS;
-  constexpr int NG = kConsumers / VS;
-  const int lane = ct % VS;
-  const int gi = (ct & 31) / VS;
-  int i = 0;
-  for (int64_t k = blockIdx.x; k < p.T; k += gridDim.x, ++i) {
-    const int s = i % p.stages;
-    mbar_wait(&full[s], (uint32_t)((i / p.stages) & 1));
+  const int lane = lane32 % VS;
+  const int gi = lane32 / VS;
+  for (int i = w;; i += kConsumerWarps) {
+    const int64_t k = blockIdx.x + (int64_t)i * gridDim.x;
+    if (k >= p.T) break;
+    const int s = i % S;
+    mbar_wait(&full[s], (uint32_t)((i / S) & 1));
     const TileMeta mt = meta[s];
-    const unsigned char* st = smem + L.stage * s;
-    const double* vals_s = reinterpret_cast<const double*>(st + L.vals);
+    unsigned char* st = smem + L.stage * s;
+    double* vals_s = reinterpret_cast<double*>(st + L.vals);
     const RP* rp_s = reinterpret_cast<const RP*>(st + L.rp);
     const int64_t t0 = k * p.C;
     const int64_t t1 = (t0 + p.C) < p.nnz ? (t0 + p.C) : p.nnz;
+    const int cnt = (int)(t1 - t0);
     const int64_t R0 = mt.R0, R1 = mt.R1;
     const int64_t fr0 = R0 > 0 ? R0 - 1 : 0;
     auto rows = [&](int64_t r) -> int64_t {
@@ -203,7 +211,43 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
     const int64_t fr = R0 - (incoming ? 1 : 0);
     const int nloc = (int)(R1 - R0) + (incoming ? 1 : 0);
 
-    for (int qb = cw * GPW; qb < nloc; qb += NG) {
+    if (!D16) {
+      // (1) products in place: lane owns elements 128*u + 4*lane32 + {0..3}
+      const int32_t* idx_s = reinterpret_cast<const int32_t*>(st + L.idx);
+      for (int ub = 0; ub < cnt; ub += 512) {
+        int c[16];
+        double xv[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = ub + 128 * u + 4 * lane32;
+          const int4 c4 = *reinterpret_cast<const int4*>(idx_s + e);
+          c[4 * u + 0] = e + 0 < cnt ? c4.x : 0;
+          c[4 * u + 1] = e + 1 < cnt ? c4.y : 0;
+          c[4 * u + 2] = e + 2 < cnt ? c4.z : 0;
+          c[4 * u + 3] = e + 3 < cnt ? c4.w : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) xv[q] = ld_x(p.x + c[q]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = ub + 128 * u + 4 * lane32;
+          if (e < cnt) {
+            double2* v2 = reinterpret_cast<double2*>(vals_s + e);
+            double2 a = v2[0], b = v2[1];
+            a.x *= xv[4 * u + 0];
+            a.y *= xv[4 * u + 1];
+            b.x *= xv[4 * u + 2];
+            b.y *= xv[4 * u + 3];
+            v2[0] = a;
+            v2[1] = b;
+          }
+        }
+      }
+      __syncwarp();
+    }
+
+    // (2) per-row sums, VS lanes per row
+    for (int qb = 0; qb < nloc; qb += GPW) {
       const int q = qb + gi;
       const bool active = q < nloc;
       int ls = 0, le = 0;
@@ -216,19 +260,14 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
       }
       double acc;
       if (!D16) {
-        const int32_t* idx_s = reinterpret_cast<const int32_t*>(st + L.idx);
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        double a0 = 0.0, a1 = 0.0;
         int l = ls + lane;
-        for (; l + 3 * VS < le; l += 4 * VS) {
-          const int c0 = idx_s[l], c1 = idx_s[l + VS], c2 = idx_s[l + 2 * VS], c3 = idx_s[l + 3 * VS];
-          const double x0 = ld_x(p.x + c0), x1 = ld_x(p.x + c1), x2 = ld_x(p.x + c2), x3 = ld_x(p.x + c3);
-          a0 = fma(vals_s[l], x0, a0);
-          a1 = fma(vals_s[l + VS], x1, a1);
-          a2 = fma(vals_s[l + 2 * VS], x2, a2);
-          a3 = fma(vals_s[l + 3 * VS], x3, a3);
+        for (; l + VS < le; l += 2 * VS) {
+          a0 += vals_s[l];
+          a1 += vals_s[l + VS];
         }
-        for (; l < le; l += VS) a0 = fma(vals_s[l], ld_x(p.x + idx_s[l]), a0);
-        acc = (a0 + a1) + (a2 + a3);
+        if (l < le) a0 += vals_s[l];
+        acc = a0 + a1;
       } else {
         const uint16_t* d_s = reinterpret_cast<const uint16_t*>(st + L.idx);
         const int32_t* hd_s = reinterpret_cast<const int32_t*>(st + L.hd);
@@ -249,9 +288,9 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
         }
       }
     }
-    if (!incoming && ct == 0) p.carry_row[k] = -1;
+    if (!incoming && lane32 == 0) p.carry_row[k] = -1;
     __syncwarp();
-    if ((ct & 31) == 0) mbar_arrive(&empty[s]);
+    if (lane32 == 0) mbar_arrive(&empty[s]);
   }
 }
 
@@ -294,10 +333,10 @@ static void stream_launch_t(const ExecArgs& a, cudaStream_t s) {
 
 template <typename RP, bool D16, bool PREP>
 static int stream_vs(const ExecArgs& a, cudaStream_t s) {
-#define SPMV_VS_CASE(V)                                  \
-  case V:                                                \
-    if (PREP) return stream_prepare_t<V, RP, D16>(a);    \
-    stream_launch_t<V, RP, D16>(a, s);                   \
+#define SPMV_VS_CASE(V)                               \
+  case V:                                             \
+    if (PREP) return stream_prepare_t<V, RP, D16>(a); \
+    stream_launch_t<V, RP, D16>(a, s);                \
     return 0;
   switch (a.vs) {
     SPMV_VS_CASE(1)

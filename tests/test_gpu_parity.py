@@ -45,7 +45,7 @@ SUITE = sg.small_suite(seed=21)
 @pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
 def test_small_suite_all_variants(name, m, variant, vs):
     p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant=variant, force_vs=vs, l_split=64,
-                  tile_nnz=256)
+                  tile_nnz=512)
     y = p.execute(m.x)
     assert_bound(y, m)
     assert p.info()["variant"] == variant
@@ -63,11 +63,13 @@ def test_dyadic_bit_exact(name, m, variant, vs):
     assert np.array_equal(y, oracle.spmv(m.rowptr, m.colind, m.vals, m.x))
 
 
-@pytest.mark.parametrize("tile", [256, 1024, 2048, 4096])
+@pytest.mark.parametrize("tile", [512, 1024, 4096])
+@pytest.mark.parametrize("vs", [1, 4])
 @pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
-def test_stream_d16_and_structures(name, m, tile):
+def test_stream_d16_and_structures(name, m, tile, vs):
     w, mg, dcol, head = oracle.d16_encode(m.rowptr, m.colind)
-    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", d16=1, tile_nnz=tile)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", d16=1, tile_nnz=tile,
+                  force_vs=vs)
     info = p.info()
     assert np.array_equal(p.export("tile_rows"), oracle.tile_rows(m.rowptr, tile))
     if w == 0:

@@ -1,0 +1,10 @@
+import json, sys
+for f in sys.argv[1:]:
+    d = json.load(open(f))
+    print(f)
+    for r in d['results']:
+        if 'ms' in r:
+            print('  %-7s vs=%2d d16=%d tile=%5d  %8.3f ms  %7.1f GB/s' % (r['variant'], r['vs'], r['d16'], r['tile'], r['ms'], r['gbs']))
+        else:
+            print('  ERR', r)
+    print(d['summary'])
