@@ -283,7 +283,8 @@ void validate_options(const spmv_options& o) {
   if (o.long_chunk != 0 && (o.long_chunk % 256 || o.long_chunk < 256))
     fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
   if (o.l_split < 0 || o.k_long < 0) fail(SPMV_E_ARG, "negative l_split / k_long");
-  if (o.stages < 0 || o.stages == 1 || o.stages > 32) fail(SPMV_E_ARG, "stages must be 0 (auto) or in [2, 32]");
+  if (o.stages < 0 || o.stages > 32 || o.stages % kStreamConsumerWarps)
+    fail(SPMV_E_ARG, "stages must be 0 (auto) or a multiple of %d up to 32", kStreamConsumerWarps);
 }
 
 void features_from_stats(const std::vector<DevStats>& st, const std::vector<int64_t>& m, spmv_features& f) {
@@ -535,12 +536,18 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
         s.stages = opt.stages;
       } else {
         s.stages = 2;
-        for (int st = 16; st >= 2; --st)
-          if (2 * stream_smem_bytes(s.C, st, rp_bytes, P->sel.d16) + 2048 <= 228 * 1024) { s.stages = st; break; }
+        // two stages per consumer warp when 2+ CTAs fit per SM, else one
+        const int W = kStreamConsumerWarps;
+        s.stages = 2 * stream_smem_bytes(s.C, 2 * W, rp_bytes, P->sel.d16) + 2048 <= 228 * 1024 ? 2 * W : W;
       }
       ExecArgs a = P->args(s, nullptr, nullptr);
       s.stream_grid = stream_prepare(a);
-      if (s.stream_grid < 0) { cudaGetLastError(); s.stages = 2; a = P->args(s, nullptr, nullptr); s.stream_grid = stream_prepare(a); }
+      if (s.stream_grid < 0 && s.stages > kStreamConsumerWarps) {
+        cudaGetLastError();
+        s.stages = kStreamConsumerWarps;
+        a = P->args(s, nullptr, nullptr);
+        s.stream_grid = stream_prepare(a);
+      }
       if (s.stream_grid < 0) fail(SPMV_E_CUDA, "cta_stream: cannot fit tile_nnz=%lld in shared memory", (long long)s.C);
     } else if (P->sel.variant == SPMV_VARIANT_MERGE) {
       s.items = P->items;

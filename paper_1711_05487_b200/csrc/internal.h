@@ -7,6 +7,7 @@ namespace spmv {
 
 constexpr int kNT = 256;  // threads per CTA for every SpMV kernel
 constexpr int kNormPartials = 512;  // fixed row chunking of the norm reduction
+constexpr int kStreamConsumerWarps = 4;  // cta_stream consumer warps per CTA (stages: multiple of this)
 
 // Device-side inspector accumulators (integers only => order-independent).
 struct DevStats {

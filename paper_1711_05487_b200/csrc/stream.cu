@@ -28,7 +28,10 @@
 
 namespace spmv {
 
-constexpr int kConsumerWarps = 8;
+// W consumer warps; the ring depth S is a multiple of W, so every stage is
+// owned by one warp and its mbarrier phases are consumed strictly in order
+// (a parity wait can never run two phases ahead).
+constexpr int kConsumerWarps = kStreamConsumerWarps;
 constexpr int kStreamThreads = 32 * (kConsumerWarps + 1);
 
 struct TileMeta {
