@@ -307,7 +307,7 @@ def _pow2ceil(v):
     return p
 
 
-def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty_frac=0.25, tile_nnz=512):
+def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty_frac=0.25):
     """Feature-guided selection. f = features(..) dict.
 
     IMB (P:608-627): skew (sd_s/avg_s > skew_sd or empty/N > empty_frac) ->
@@ -338,9 +338,8 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     else:
         variant = VARIANT_VECTOR
     if variant == VARIANT_STREAM:
-        # cta_stream lane group: a tile's rows cover its consumer warp's 32 lanes
-        want = avg_s * 32.0 / tile_nnz
-        vs = min(32, _pow2ceil(int(math.ceil(want))) if want > 1.0 else 1)
+        # cta_stream: one lane per row up to 32 nonzeros, else pow2ceil(avg_s/32)
+        vs = min(32, _pow2ceil(int(math.ceil(avg_s / 32.0)))) if avg_s > 32 else 1
     if avg_s <= 4:
         classes |= CLASS_CMP
     mb = ws > l2_bytes // 2

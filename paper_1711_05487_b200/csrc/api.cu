@@ -242,13 +242,11 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   vs = std::min(32, std::max(2, vs));
   int variant = skew ? SPMV_VARIANT_MERGE : longr ? SPMV_VARIANT_SPLIT : avg_s <= 32 ? SPMV_VARIANT_STREAM
                                                                                      : SPMV_VARIANT_VECTOR;
+  if (o.force_variant > 0) variant = o.force_variant;
   if (variant == SPMV_VARIANT_STREAM) {
-    // cta_stream: size the lane group so a tile's rows cover the 32 lanes of
-    // its consumer warp: VS = pow2ceil(avg_s * 32 / C), clamp [1, 32]
-    const int64_t C = o.tile_nnz > 0 ? o.tile_nnz : 512;
-    const double want = avg_s * 32.0 / (double)C;
-    vs = want > 1.0 ? pow2ceil((int64_t)std::ceil(want)) : 1;
-    vs = std::min(32, vs);
+    // cta_stream: one lane per row for rows up to 32 nonzeros (lanes walk
+    // consecutive rows in step), else VS = pow2ceil(avg_s / 32), clamp 32
+    vs = avg_s > 32 ? std::min(32, pow2ceil((int64_t)std::ceil(avg_s / 32.0))) : 1;
   }
   if (avg_s <= 4) classes |= SPMV_CLASS_CMP;
   if (ws > d.l2_bytes / 2 && !(classes & SPMV_CLASS_IMB)) classes |= SPMV_CLASS_MB;
@@ -257,7 +255,6 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   if (ml) classes |= SPMV_CLASS_ML;
   bool xwin = ml && 8 * n <= d.access_window_max;
   // explicit options override the feature-guided choice
-  if (o.force_variant > 0) variant = o.force_variant;
   if (o.force_vs > 0) vs = o.force_vs;
   if (o.d16 == 0) d16 = false;
   if (o.d16 == 1) d16 = f.maxgap <= 65535;
@@ -395,7 +392,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   P->opt = opt;
   P->l_split = opt.l_split > 0 ? opt.l_split : 4096;
   P->k_long = opt.k_long > 0 ? opt.k_long : 100;
-  P->C = opt.tile_nnz > 0 ? opt.tile_nnz : 512;
+  P->C = opt.tile_nnz > 0 ? opt.tile_nnz : 1024;
   P->items = 2048;
   P->chunk = opt.long_chunk > 0 ? opt.long_chunk : 8192;
   query_props(cur, P->props);
@@ -535,10 +532,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       if (opt.stages > 0) {
         s.stages = opt.stages;
       } else {
-        s.stages = 2;
-        // two stages per consumer warp when 2+ CTAs fit per SM, else one
+        // two stages per consumer warp (one in compute, one streaming in)
         const int W = kStreamConsumerWarps;
-        s.stages = 2 * stream_smem_bytes(s.C, 2 * W, rp_bytes, P->sel.d16) + 2048 <= 228 * 1024 ? 2 * W : W;
+        s.stages = stream_smem_bytes(s.C, 2 * W, rp_bytes, P->sel.d16) + 1024 <= 227 * 1024 ? 2 * W : W;
       }
       ExecArgs a = P->args(s, nullptr, nullptr);
       s.stream_grid = stream_prepare(a);

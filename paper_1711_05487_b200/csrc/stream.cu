@@ -214,42 +214,10 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
     const int64_t fr = R0 - (incoming ? 1 : 0);
     const int nloc = (int)(R1 - R0) + (incoming ? 1 : 0);
 
-    if (!D16) {
-      // (1) products in place: lane owns elements 128*u + 4*lane32 + {0..3}
-      const int32_t* idx_s = reinterpret_cast<const int32_t*>(st + L.idx);
-      for (int ub = 0; ub < cnt; ub += 512) {
-        int c[16];
-        double xv[16];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = ub + 128 * u + 4 * lane32;
-          const int4 c4 = *reinterpret_cast<const int4*>(idx_s + e);
-          c[4 * u + 0] = e + 0 < cnt ? c4.x : 0;
-          c[4 * u + 1] = e + 1 < cnt ? c4.y : 0;
-          c[4 * u + 2] = e + 2 < cnt ? c4.z : 0;
-          c[4 * u + 3] = e + 3 < cnt ? c4.w : 0;
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) xv[q] = ld_x(p.x + c[q]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = ub + 128 * u + 4 * lane32;
-          if (e < cnt) {
-            double2* v2 = reinterpret_cast<double2*>(vals_s + e);
-            double2 a = v2[0], b = v2[1];
-            a.x *= xv[4 * u + 0];
-            a.y *= xv[4 * u + 1];
-            b.x *= xv[4 * u + 2];
-            b.y *= xv[4 * u + 3];
-            v2[0] = a;
-            v2[1] = b;
-          }
-        }
-      }
-      __syncwarp();
-    }
-
-    // (2) per-row sums, VS lanes per row
+    (void)cnt;
+    // per-row products and sums, VS lanes per row (VS = 1 for short rows:
+    // lanes walk consecutive rows in step, so a banded matrix gathers x from
+    // 2-3 cache lines per warp instruction)
     for (int qb = 0; qb < nloc; qb += GPW) {
       const int q = qb + gi;
       const bool active = q < nloc;
@@ -263,14 +231,19 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
       }
       double acc;
       if (!D16) {
-        double a0 = 0.0, a1 = 0.0;
+        const int32_t* idx_s = reinterpret_cast<const int32_t*>(st + L.idx);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int l = ls + lane;
-        for (; l + VS < le; l += 2 * VS) {
-          a0 += vals_s[l];
-          a1 += vals_s[l + VS];
+        for (; l + 3 * VS < le; l += 4 * VS) {
+          const int c0 = idx_s[l], c1 = idx_s[l + VS], c2 = idx_s[l + 2 * VS], c3 = idx_s[l + 3 * VS];
+          const double x0 = ld_x(p.x + c0), x1 = ld_x(p.x + c1), x2 = ld_x(p.x + c2), x3 = ld_x(p.x + c3);
+          a0 = fma(vals_s[l], x0, a0);
+          a1 = fma(vals_s[l + VS], x1, a1);
+          a2 = fma(vals_s[l + 2 * VS], x2, a2);
+          a3 = fma(vals_s[l + 3 * VS], x3, a3);
         }
-        if (l < le) a0 += vals_s[l];
-        acc = a0 + a1;
+        for (; l < le; l += VS) a0 = fma(vals_s[l], ld_x(p.x + idx_s[l]), a0);
+        acc = (a0 + a1) + (a2 + a3);
       } else {
         const uint16_t* d_s = reinterpret_cast<const uint16_t*>(st + L.idx);
         const int32_t* hd_s = reinterpret_cast<const int32_t*>(st + L.hd);
