@@ -244,9 +244,9 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
                                                                                      : SPMV_VARIANT_VECTOR;
   if (o.force_variant > 0) variant = o.force_variant;
   if (variant == SPMV_VARIANT_STREAM) {
-    // cta_stream: one lane per row for rows up to 32 nonzeros (lanes walk
-    // consecutive rows in step), else VS = pow2ceil(avg_s / 32), clamp 32
-    vs = avg_s > 32 ? std::min(32, pow2ceil((int64_t)std::ceil(avg_s / 32.0))) : 1;
+    // cta_stream: the smallest lane group giving each lane <= 8 nonzeros of a
+    // row (one batch of 8 gathers): VS = pow2ceil(avg_s / 8), clamp [1, 32]
+    vs = avg_s > 8 ? std::min(32, pow2ceil((int64_t)std::ceil(avg_s / 8.0))) : 1;
   }
   if (avg_s <= 4) classes |= SPMV_CLASS_CMP;
   if (ws > d.l2_bytes / 2 && !(classes & SPMV_CLASS_IMB)) classes |= SPMV_CLASS_MB;
@@ -392,7 +392,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   P->opt = opt;
   P->l_split = opt.l_split > 0 ? opt.l_split : 4096;
   P->k_long = opt.k_long > 0 ? opt.k_long : 100;
-  P->C = opt.tile_nnz > 0 ? opt.tile_nnz : 1024;
+  P->C = opt.tile_nnz > 0 ? opt.tile_nnz : 512;
   P->items = 2048;
   P->chunk = opt.long_chunk > 0 ? opt.long_chunk : 8192;
   query_props(cur, P->props);

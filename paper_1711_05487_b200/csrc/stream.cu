@@ -231,19 +231,27 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP
       }
       double acc;
       if (!D16) {
+        // batches of 8 predicated elements per lane: 8 independent gathers in flight
         const int32_t* idx_s = reinterpret_cast<const int32_t*>(st + L.idx);
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int l = ls + lane;
-        for (; l + 3 * VS < le; l += 4 * VS) {
-          const int c0 = idx_s[l], c1 = idx_s[l + VS], c2 = idx_s[l + 2 * VS], c3 = idx_s[l + 3 * VS];
-          const double x0 = ld_x(p.x + c0), x1 = ld_x(p.x + c1), x2 = ld_x(p.x + c2), x3 = ld_x(p.x + c3);
-          a0 = fma(vals_s[l], x0, a0);
-          a1 = fma(vals_s[l + VS], x1, a1);
-          a2 = fma(vals_s[l + 2 * VS], x2, a2);
-          a3 = fma(vals_s[l + 3 * VS], x3, a3);
+        double a0 = 0.0, a1 = 0.0;
+        for (int l0 = ls + lane; l0 < le; l0 += 8 * VS) {
+          int c[8];
+          double v[8], xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int l = l0 + u * VS;
+            c[u] = l < le ? idx_s[l] : -1;
+            v[u] = l < le ? vals_s[l] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_x(p.x + c[u]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; u += 2) {
+            a0 = fma(v[u], xv[u], a0);
+            a1 = fma(v[u + 1], xv[u + 1], a1);
+          }
         }
-        for (; l < le; l += VS) a0 = fma(vals_s[l], ld_x(p.x + idx_s[l]), a0);
-        acc = (a0 + a1) + (a2 + a3);
+        acc = a0 + a1;
       } else {
         const uint16_t* d_s = reinterpret_cast<const uint16_t*>(st + L.idx);
         const int32_t* hd_s = reinterpret_cast<const int32_t*>(st + L.hd);

@@ -4,7 +4,8 @@ for f in sys.argv[1:]:
     print(f)
     for r in d['results']:
         if 'ms' in r:
-            print('  %-7s vs=%2d d16=%d tile=%5d  %8.3f ms  %7.1f GB/s' % (r['variant'], r['vs'], r['d16'], r['tile'], r['ms'], r['gbs']))
+            o = r['opts']
+            print('  %-7s vs=%2d d16=%d tile=%5d st=%2s  %8.3f ms  %7.1f GB/s' % (r['variant'], r['vs'], r['d16'], r['tile'], o.get('stages', '-'), r['ms'], r['gbs']))
         else:
             print('  ERR', r)
     print(d['summary'])

@@ -71,12 +71,15 @@ def main():
     auto = res[0]
     print(json.dumps({"auto": auto}), flush=True)
     grid = []
-    vss = (4, 8, 16, 32) if not a.quick else (8, 32)
-    tiles = (1024, 2048, 4096) if not a.quick else (2048,)
+    vss = (1, 2, 4, 8, 16, 32) if not a.quick else (4, 8)
     for vs in vss:
         grid.append(dict(force_variant="vector", force_vs=vs))
-    for vs, t, d in itertools.product(vss, tiles, (0, 1)):
-        grid.append(dict(force_variant="stream", force_vs=vs, tile_nnz=t, d16=d))
+    svs = (1, 2, 4, 8) if not a.quick else (1, 4)
+    tiles = (512, 1024, 2048) if not a.quick else (512, 1024)
+    stages = (4, 8, 12) if not a.quick else (8,)
+    d16s = (0, 1) if a.config in (1, 2) else (0,)
+    for vs, t, sg_, d in itertools.product(svs, tiles, stages, d16s):
+        grid.append(dict(force_variant="stream", force_vs=vs, tile_nnz=t, stages=sg_, d16=d))
     grid.append(dict(force_variant="merge"))
     for vs in vss:
         grid.append(dict(force_variant="split", force_vs=vs))
