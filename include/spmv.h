@@ -67,11 +67,11 @@ typedef struct spmv_options {
   int32_t validate;        /* 1 = check CSR invariants on the device (default), 0 = trust the input */
   int64_t l_split;         /* long-row threshold in nnz (0 = 4096) */
   int64_t k_long;          /* long rows trigger SPLIT when nnz_max > k_long * nnz_avg (0 = 100) */
-  int64_t tile_nnz;        /* STREAM tile size C in nonzeros (0 = 512; multiple of 512, <= 16384) */
+  int64_t tile_nnz;        /* STREAM tile size C in nonzeros (0 = 512; multiple of 128, <= 16384) */
   int64_t merge_items;     /* MERGE items (rows + nnz) per CTA (0 = 2048; multiple of 256) */
   int64_t long_chunk;      /* SPLIT chunk size in nonzeros (0 = 8192; multiple of 256) */
   int32_t emulate_devices; /* ngpus > 1: 1 = place every shard on the current device (tests) */
-  int32_t stages;          /* STREAM smem ring depth: 0 = auto (deepest <= 16 fitting 2 CTAs/SM), else 2..32 */
+  int32_t stages;          /* STREAM smem ring depth: 0 = auto (one stage per consumer warp), else a multiple of 4 <= 32 */
   int32_t reserved[6];
 } spmv_options;
 

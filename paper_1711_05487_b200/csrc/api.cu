@@ -274,8 +274,8 @@ void validate_options(const spmv_options& o) {
   if (o.force_vs != 0 && o.force_vs != 1 && o.force_vs != 2 && o.force_vs != 4 && o.force_vs != 8 &&
       o.force_vs != 16 && o.force_vs != 32)
     fail(SPMV_E_ARG, "force_vs %d not in {0,1,2,4,8,16,32}", o.force_vs);
-  if (o.tile_nnz != 0 && (o.tile_nnz % 512 || o.tile_nnz < 512 || o.tile_nnz > 16384))
-    fail(SPMV_E_ARG, "tile_nnz %lld must be a multiple of 512 in [512, 16384]", (long long)o.tile_nnz);
+  if (o.tile_nnz != 0 && (o.tile_nnz % 128 || o.tile_nnz < 128 || o.tile_nnz > 16384))
+    fail(SPMV_E_ARG, "tile_nnz %lld must be a multiple of 128 in [128, 16384]", (long long)o.tile_nnz);
   if (o.merge_items != 0 && o.merge_items != 2048) fail(SPMV_E_ARG, "merge_items must be 2048");
   if (o.long_chunk != 0 && (o.long_chunk % 256 || o.long_chunk < 256))
     fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
@@ -532,9 +532,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       if (opt.stages > 0) {
         s.stages = opt.stages;
       } else {
-        // two stages per consumer warp (one in compute, one streaming in)
-        const int W = kStreamConsumerWarps;
-        s.stages = stream_smem_bytes(s.C, 2 * W, rp_bytes, P->sel.d16) + 1024 <= 227 * 1024 ? 2 * W : W;
+        // one stage per consumer warp: measured on B200 (tools/sweep.py, C2/C5),
+        // more resident warps beat a deeper ring (the x gathers are latency-bound)
+        s.stages = kStreamConsumerWarps;
       }
       ExecArgs a = P->args(s, nullptr, nullptr);
       s.stream_grid = stream_prepare(a);

@@ -49,11 +49,11 @@ struct StreamLayout {
   uint32_t rp_cap, hd_cap;  // bytes
 };
 
-// rows staged per tile: C/4 + 32 (average row length >= ~4; sparser tiles
+// rows staged per tile: C/8 + 16 (average row length >= ~7; sparser tiles
 // read rowptr from global memory, still correct)
 __host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int rp_bytes, bool d16) {
   StreamLayout L;
-  const size_t rows_cap = (size_t)C / 4 + 32;
+  const size_t rows_cap = (size_t)C / 8 + 16;
   L.rp_cap = (uint32_t)(((rows_cap + 2) * rp_bytes + 32 + 15) & ~(size_t)15);
   L.hd_cap = d16 ? (uint32_t)(((rows_cap + 2) * 4 + 32 + 15) & ~(size_t)15) : 0u;
   L.vals = 0;
@@ -121,7 +121,7 @@ __device__ __forceinline__ void d16_row_cols(const uint16_t* __restrict__ d_s, i
 }
 
 template <int VS, typename RP, bool D16>
-__global__ void __launch_bounds__(kStreamThreads) stream_kernel(const StreamP<RP> p) {
+__global__ void __launch_bounds__(kStreamThreads, 8) stream_kernel(const StreamP<RP> p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), D16);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);

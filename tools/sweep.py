@@ -74,9 +74,9 @@ def main():
     vss = (1, 2, 4, 8, 16, 32) if not a.quick else (4, 8)
     for vs in vss:
         grid.append(dict(force_variant="vector", force_vs=vs))
-    svs = (1, 2, 4, 8) if not a.quick else (1, 4)
-    tiles = (512, 1024, 2048) if not a.quick else (512, 1024)
-    stages = (4, 8, 12) if not a.quick else (8,)
+    svs = (1, 2, 4) if not a.quick else (1, 4)
+    tiles = (256, 384, 512, 768, 1024) if not a.quick else (384, 512)
+    stages = (4, 8) if not a.quick else (4,)
     d16s = (0, 1) if a.config in (1, 2) else (0,)
     for vs, t, sg_, d in itertools.product(svs, tiles, stages, d16s):
         grid.append(dict(force_variant="stream", force_vs=vs, tile_nnz=t, stages=sg_, d16=d))
