@@ -338,8 +338,8 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     else:
         variant = VARIANT_VECTOR
     if variant == VARIANT_STREAM:
-        # cta_stream: smallest lane group giving each lane <= 8 nonzeros of a row
-        vs = min(32, _pow2ceil(int(math.ceil(avg_s / 8.0)))) if avg_s > 8 else 1
+        # cta_stream: one lane per row up to 32 nonzeros, else pow2ceil(avg_s/32)
+        vs = min(32, _pow2ceil(int(math.ceil(avg_s / 32.0)))) if avg_s > 32 else 1
     if avg_s <= 4:
         classes |= CLASS_CMP
     mb = ws > l2_bytes // 2

@@ -244,9 +244,10 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
                                                                                      : SPMV_VARIANT_VECTOR;
   if (o.force_variant > 0) variant = o.force_variant;
   if (variant == SPMV_VARIANT_STREAM) {
-    // cta_stream: the smallest lane group giving each lane <= 8 nonzeros of a
-    // row (one batch of 8 gathers): VS = pow2ceil(avg_s / 8), clamp [1, 32]
-    vs = avg_s > 8 ? std::min(32, pow2ceil((int64_t)std::ceil(avg_s / 8.0))) : 1;
+    // cta_stream: one lane per row for rows up to 32 nonzeros (lanes walk
+    // consecutive rows in step: coalesced x gathers on banded matrices), else
+    // VS = pow2ceil(avg_s / 32), clamp 32 (sweep on B200: VS=1 best on C2, C5)
+    vs = avg_s > 32 ? std::min(32, pow2ceil((int64_t)std::ceil(avg_s / 32.0))) : 1;
   }
   if (avg_s <= 4) classes |= SPMV_CLASS_CMP;
   if (ws > d.l2_bytes / 2 && !(classes & SPMV_CLASS_IMB)) classes |= SPMV_CLASS_MB;
@@ -510,6 +511,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const MatView A = s.view();
     if (P->sel.variant == SPMV_VARIANT_STREAM) {
+      // tile size: ~28 rows of average length per consumer warp (B200 sweep:
+      // 512 best for 7-nnz rows, 768 for 27-nnz rows)
+      if (opt.tile_nnz == 0) P->C = P->feat.avg_short > 16 ? 768 : 512;
       s.C = P->C;
       s.T = std::max<int64_t>(1, (s.nnz + s.C - 1) / s.C);
       s.tile_row = s.alloc<int32_t>((size_t)s.T + 1);

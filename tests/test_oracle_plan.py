@@ -232,7 +232,7 @@ def test_select_rule_table_on_closed_form_features():
     assert (s.variant, s.d16, s.xwin, s.vs) == (S.VARIANT_STREAM, True, False, 1) and s.classes & S.CLASS_MB
     # C5: 27-pt 384^3: regular, maxgap 147071 -> no D16
     s = S.select(feat(56623104, 1520875000, 26.86, 0.5, maxgap=147071, misses=10 ** 8), L2, WIN, 8)
-    assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, False, 4)  # pow2ceil(26.86 / 8) = 4
+    assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, False, 1)  # rows <= 32 nnz: one lane per row
     # C1: 1.28 MB working set -> no MB, no D16
     s = S.select(feat(10000, 90000, 9.0, 0.0, maxgap=9000, misses=80000), L2, WIN, 4)
     assert (s.variant, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_STREAM, False, 0)
