@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--iters", type=int, default=10, help="iterated-mode iterations to time (0 = skip)")
     return ap.parse_args()
 
 
@@ -130,7 +131,7 @@ def build_block(cfg, rank, world, pkg=None):
         s = sg.seeds(cfg)
         m = sg.stencil(n, pts, rp64=rp64, x_seed=s["x"], rows=(rb, re))
         del full_rp
-        return dict(rowptr=m.rowptr, colind=m.colind, vals=m.vals, x=m.x, N=N, nnz=nnz, rows=(rb, re),
+        return dict(rowptr=m.rowptr, colind=m.colind, vals=m.vals, x=m.x, N=N, nnz=nnz, rows=(rb, re), bounds=b,
                     rp_bytes=8 if rp64 else 4, gen_s=time.time() - t)
     m = sg.config(cfg)
     rp = m.rowptr.astype(np.int64)
@@ -138,7 +139,8 @@ def build_block(cfg, rank, world, pkg=None):
     rb, re = int(b[rank]), int(b[rank + 1])
     lrp = (rp[rb:re + 1] - rp[rb]).astype(m.rowptr.dtype)
     return dict(rowptr=np.ascontiguousarray(lrp), colind=m.colind[rp[rb]:rp[re]], vals=m.vals[rp[rb]:rp[re]],
-                x=m.x, N=m.n, nnz=m.nnz, rows=(rb, re), rp_bytes=m.rowptr.dtype.itemsize, gen_s=time.time() - t)
+                x=m.x, N=m.n, nnz=m.nnz, rows=(rb, re), bounds=b, rp_bytes=m.rowptr.dtype.itemsize,
+                gen_s=time.time() - t)
 
 
 def algo_bytes(n_rows, n_cols, nnz, rp_bytes):
@@ -304,6 +306,30 @@ def run_native(a):
                "h2d_bytes_per_step": 8 * blk["N"] * world, "d2h_bytes_per_step": 8 * blk["N"],
                "ms_per_step": ms_e2e}
 
+    # iterated mode x <- Ax/||Ax|| (BJ.configs[5]): per iteration SpMV + norm
+    # partials + NCCL all-gather of partials + normalize + all-gather(v) of x
+    iterated = None
+    if a.iters > 0:
+        from paper_1711_05487_b200 import parallel
+        P = spmv.norm_partial_count()
+        xf = torch.from_numpy(blk["x"]).cuda()
+        yl = torch.empty(n_rows, dtype=torch.float64, device="cuda")
+        pl = torch.empty(P, dtype=torch.float64, device="cuda")
+        pa = torch.empty(world * P, dtype=torch.float64, device="cuda")
+        nu = torch.empty(a.iters + 2, dtype=torch.float64, device="cuda")
+        steps = parallel.native_steps(plan)
+        b = [int(v) for v in blk["bounds"]]
+        dd = dist if world > 1 else parallel.NoDist
+        with torch.cuda.stream(stream):
+            parallel.iterate(dd, steps, b, rank, world, xf, yl, pl, pa, nu, 2)
+            ms_it = max_over_ranks(timed(lambda: parallel.iterate(dd, steps, b, rank, world, xf, yl, pl, pa, nu, 1),
+                                         a.iters)) / a.iters
+            exch = lambda: parallel.exchange_only(dd, b, rank, world, xf, pl, pa)  # noqa: E731
+            ms_ex = max_over_ranks(timed(exch, a.iters)) / a.iters
+        iterated = {"iters_timed": a.iters, "ms_per_iter": ms_it, "spmv_ms": ms_step, "exchange_ms": ms_ex,
+                    "gflops_per_iter": 2.0 * blk["nnz"] / (ms_it * 1e-3) / 1e9,
+                    "exchange": "NCCL all-gather(partials) + per-rank broadcast of x blocks" if world > 1 else "none (1 GPU)"}
+
     nnz = blk["nnz"]
     N = blk["N"]
     gflops = 2.0 * nnz / (ms_step * 1e-3) / 1e9
@@ -349,6 +375,7 @@ def run_native(a):
                          "kernel_ms": ms_main, "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "iterated": iterated,
             "gpu_launches": launches,
             "clocks": clocks,
         }

@@ -1,0 +1,82 @@
+"""World-size-2 gloo tests (CPU) of the one-process-per-GPU orchestration in
+paper_1711_05487_b200/parallel.py: shard bounds, the rank-ordered norm
+combine and the all-gather(v) of x blocks. The local steps are CPU stubs built
+on the oracle (tests may use it; the product never does)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synthgen as sg
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, K, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1711_05487_b200 as pkg
+        from paper_1711_05487_b200 import parallel
+        m = sg.config(5, small=True)
+        rp = m.rowptr.astype(np.int64)
+        b = pkg.shard_bounds(rp, world)
+        b0, b1 = int(b[rank]), int(b[rank + 1])
+        lrp = rp[b0:b1 + 1] - rp[b0]
+        lci, lva = m.colind[rp[b0]:rp[b1]], m.vals[rp[b0]:rp[b1]]
+        P = 512
+        steps = parallel.ShardSteps(
+            spmv=lambda x, y: y.copy_(torch.from_numpy(oracle.spmv(lrp, lci, lva, x.numpy()))),
+            partials=lambda y, p: p.copy_(torch.tensor(
+                [float(np.sum(y.numpy()[q * y.numel() // P:(q + 1) * y.numel() // P] ** 2)) for q in range(P)],
+                dtype=torch.float64)),
+            normalize=lambda y, pa, cnt, xb, nu: (nu.fill_(float(np.sqrt(np.sum(pa.numpy()[:cnt])))),
+                                                  xb.copy_(y / nu[0])),
+        )
+        x = torch.from_numpy(m.x.copy())
+        y = torch.empty(b1 - b0, dtype=torch.float64)
+        pl = torch.empty(P, dtype=torch.float64)
+        pa = torch.empty(world * P, dtype=torch.float64)
+        nu = torch.empty(K, dtype=torch.float64)
+        parallel.iterate(dist, steps, b, rank, world, x, y, pl, pa, nu, K)
+        out_q.put((rank, b.tolist(), x.numpy().copy(), nu.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_sharded_power_iteration_gloo(world):
+    K = 30
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, K, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m = sg.config(5, small=True)
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, K)
+    assert rc == 0
+    res.sort()
+    for rank, b, x, nu in res:
+        assert b == oracle.shard_bounds(m.rowptr, world).tolist()
+        assert np.max(np.abs(x - xr)) <= 1e-10 * np.max(np.abs(xr))
+        assert np.all(np.abs(nu - nur) <= 1e-12 * nur)
+    # every rank ends with the identical replica and identical nu (rank-ordered combine)
+    for rank, b, x, nu in res[1:]:
+        assert np.array_equal(x, res[0][2]) and np.array_equal(nu, res[0][3])
