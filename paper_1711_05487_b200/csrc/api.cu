@@ -119,7 +119,14 @@ struct Shard {
   int64_t* mnnz = nullptr;
   int32_t* mcarry_row = nullptr;
   double* mcarry_val = nullptr;
-  // SPLIT
+  // SPLIT: compacted short-row CSR (view sv), medium row list, long chunks
+  void* rp_s = nullptr;
+  int32_t* col_s = nullptr;
+  double* val_s = nullptr;
+  MatView sv{};
+  bool has_short = false;
+  int32_t* mid_rows = nullptr;
+  int64_t n_mid = 0;
   int64_t n_long = 0, n_chunks = 0;
   int32_t* long_rows = nullptr;
   int64_t* chunk_start = nullptr;
@@ -204,6 +211,9 @@ struct spmv_plan_s {
     a.chunk_start = s.chunk_start;
     a.chunk_row = s.chunk_row;
     a.chunk_val = s.chunk_val;
+    a.S = s.has_short ? s.sv : a.A;
+    a.mid_rows = s.mid_rows;
+    a.n_mid = s.n_mid;
     return a;
   }
   int launch(Shard& s, const double* x, double* y, int stage = 0) const {
@@ -507,48 +517,50 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
 
   // ---- a3/a4: structures for the selected variant ---------------------------------
   double t_d = now_ms();
+  // cta_stream structures over the view V (the whole shard, or the compacted
+  // short-row CSR of long_row_split)
+  auto build_stream = [&](Shard& s, const MatView& V, bool d16, int vs) {
+    // tile size: ~28 rows of average length per consumer warp (B200 sweep:
+    // 512 best for 7-nnz rows, 768 for 27-nnz rows)
+    const double avg = V.m ? (double)V.nnz / (double)V.m : 0.0;
+    s.C = opt.tile_nnz > 0 ? opt.tile_nnz : (avg > 16 ? 768 : 512);
+    P->C = s.C;
+    s.T = std::max<int64_t>(1, (V.nnz + s.C - 1) / s.C);
+    s.tile_row = s.alloc<int32_t>((size_t)s.T + 1);
+    s.carry_row = s.alloc<int32_t>((size_t)s.T);
+    s.carry_val = s.alloc<double>((size_t)s.T);
+    launch_tile_rows(V, s.C, s.T, s.tile_row, s.stats, s.stream);
+    count_launches(1, "tile_rows");
+    if (d16) {
+      s.dcol = s.alloc<uint16_t>((size_t)V.nnz);
+      s.head = s.alloc<int32_t>((size_t)V.m);
+      s.anchor = s.alloc<int32_t>((size_t)s.T);
+      launch_d16_encode(V, s.headbits, s.C, s.T, s.dcol, s.head, s.anchor, s.stream);
+      count_launches(3, "d16_encode");
+    }
+    ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
+    ck(cudaStreamSynchronize(s.stream), "tiles");
+    s.need_fixup = s.hs.n_incoming > 0;
+    // one stage per consumer warp: measured on B200 (tools/sweep.py, C2/C5),
+    // more resident warps beat a deeper ring (the x gathers are latency-bound)
+    s.stages = opt.stages > 0 ? opt.stages : kStreamConsumerWarps;
+    ExecArgs a = P->args(s, nullptr, nullptr);
+    a.A = V;
+    a.vs = vs;
+    s.stream_grid = stream_prepare(a);
+    if (s.stream_grid < 0 && s.stages > kStreamConsumerWarps) {
+      cudaGetLastError();
+      s.stages = kStreamConsumerWarps;
+      a.stages = s.stages;
+      s.stream_grid = stream_prepare(a);
+    }
+    if (s.stream_grid < 0) fail(SPMV_E_CUDA, "cta_stream: cannot fit tile_nnz=%lld in shared memory", (long long)s.C);
+  };
   for (auto& s : P->shards) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const MatView A = s.view();
     if (P->sel.variant == SPMV_VARIANT_STREAM) {
-      // tile size: ~28 rows of average length per consumer warp (B200 sweep:
-      // 512 best for 7-nnz rows, 768 for 27-nnz rows)
-      if (opt.tile_nnz == 0) P->C = P->feat.avg_short > 16 ? 768 : 512;
-      s.C = P->C;
-      s.T = std::max<int64_t>(1, (s.nnz + s.C - 1) / s.C);
-      s.tile_row = s.alloc<int32_t>((size_t)s.T + 1);
-      s.carry_row = s.alloc<int32_t>((size_t)s.T);
-      s.carry_val = s.alloc<double>((size_t)s.T);
-      launch_tile_rows(A, s.C, s.T, s.tile_row, s.stats, s.stream);
-      count_launches(1, "tile_rows");
-      if (P->sel.d16) {
-        s.dcol = s.alloc<uint16_t>((size_t)s.nnz);
-        s.head = s.alloc<int32_t>((size_t)s.m);
-        s.anchor = s.alloc<int32_t>((size_t)s.T);
-        launch_d16_encode(A, s.headbits, s.C, s.T, s.dcol, s.head, s.anchor, s.stream);
-        count_launches(3, "d16_encode");
-      }
-      ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
-      ck(cudaStreamSynchronize(s.stream), "tiles");
-      s.need_fixup = s.hs.n_incoming > 0;
-      // ring depth: the deepest of 16..2 stages that still fits two CTAs per SM
-      // (8 consumer warps each own a tile in compute; the rest stream in)
-      if (opt.stages > 0) {
-        s.stages = opt.stages;
-      } else {
-        // one stage per consumer warp: measured on B200 (tools/sweep.py, C2/C5),
-        // more resident warps beat a deeper ring (the x gathers are latency-bound)
-        s.stages = kStreamConsumerWarps;
-      }
-      ExecArgs a = P->args(s, nullptr, nullptr);
-      s.stream_grid = stream_prepare(a);
-      if (s.stream_grid < 0 && s.stages > kStreamConsumerWarps) {
-        cudaGetLastError();
-        s.stages = kStreamConsumerWarps;
-        a = P->args(s, nullptr, nullptr);
-        s.stream_grid = stream_prepare(a);
-      }
-      if (s.stream_grid < 0) fail(SPMV_E_CUDA, "cta_stream: cannot fit tile_nnz=%lld in shared memory", (long long)s.C);
+      build_stream(s, A, P->sel.d16, P->sel.vs);
     } else if (P->sel.variant == SPMV_VARIANT_MERGE) {
       s.items = P->items;
       s.Tm = std::max<int64_t>(1, (s.m + s.nnz + s.items - 1) / s.items);
@@ -559,6 +571,38 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       launch_merge_splits(A, s.items, s.Tm, s.mrow, s.mnnz, s.stream);
       count_launches(1, "merge_splits");
     } else if (P->sel.variant == SPMV_VARIANT_SPLIT) {
+      // decomposition by row length (Fig. 6 read through S:120-125):
+      // short rows (len <= T_s) -> compacted CSR run by cta_stream,
+      // medium rows (T_s < len <= L_split) -> ordered list, one warp per row,
+      // long rows (len > L_split) -> chunk table
+      const int64_t ts = std::min<int64_t>(kShortRowMax, P->l_split);
+      int64_t* scan = s.alloc<int64_t>((size_t)scan_blocks(s.m) + 2);
+      s.rp_s = s.alloc<char>((size_t)(s.m + 1) * rp_bytes);
+      launch_filtered_csr(A, 0, ts, s.rp_s, nullptr, nullptr, scan, s.stream);
+      count_launches(3, "short rowptr");
+      int64_t nnz_s = 0;
+      ck(cudaMemcpyAsync(&nnz_s, (char*)s.rp_s + s.m * rp_bytes, rp_bytes, cudaMemcpyDeviceToHost, s.stream),
+         "short nnz");
+      ck(cudaStreamSynchronize(s.stream), "short nnz");
+      s.col_s = s.alloc<int32_t>((size_t)nnz_s);
+      s.val_s = s.alloc<double>((size_t)nnz_s);
+      launch_filtered_csr(A, 0, ts, s.rp_s, s.col_s, s.val_s, scan, s.stream);
+      count_launches(4, "short csr");
+      s.sv = MatView{rp_bytes, s.rp_s, s.col_s, s.val_s, s.m, s.n_cols, nnz_s};
+      s.has_short = true;
+      build_stream(s, s.sv, false, 1);
+      if (P->l_split > ts) {
+        launch_row_list(A, ts + 1, P->l_split, nullptr, scan, s.stream);  // count only
+        count_launches(2, "medium count");
+        const int64_t nb = scan_blocks(s.m);
+        ck(cudaMemcpyAsync(&s.n_mid, scan + nb, 8, cudaMemcpyDeviceToHost, s.stream), "medium count");
+        ck(cudaStreamSynchronize(s.stream), "medium count");
+        if (s.n_mid > 0) {
+          s.mid_rows = s.alloc<int32_t>((size_t)s.n_mid);
+          launch_row_list(A, ts + 1, P->l_split, s.mid_rows, scan, s.stream);
+          count_launches(3, "medium rows");
+        }
+      }
       s.n_long = s.hs.n_long;
       if (s.n_long > 0) {
         const int nb = 1024;

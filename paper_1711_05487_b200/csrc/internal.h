@@ -72,7 +72,17 @@ struct ExecArgs {
   const int64_t* chunk_start;
   int32_t* chunk_row;
   double* chunk_val;
+  MatView S;                 // SPLIT: compacted short-row CSR (other rows empty)
+  const int32_t* mid_rows;   // SPLIT: medium rows, one warp each
+  int64_t n_mid;
 };
+
+constexpr int64_t kShortRowMax = 32;  // SPLIT: rows up to this length go to cta_stream (one lane per row)
+int64_t scan_blocks(int64_t m);
+void launch_filtered_csr(const MatView& A, int64_t lo, int64_t hi, void* out_rp, int32_t* out_col, double* out_val,
+                         int64_t* scratch, cudaStream_t s);
+void launch_row_list(const MatView& A, int64_t lo, int64_t hi, int32_t* out, int64_t* scratch, cudaStream_t s);
+void launch_rowlist(const ExecArgs& a, const int32_t* rows, int64_t nrows, cudaStream_t s);
 
 int launch_vector(const ExecArgs& a, bool skip_long, cudaStream_t s);  // returns #launches
 int launch_stream(const ExecArgs& a, cudaStream_t s);

@@ -182,7 +182,19 @@ __global__ void __launch_bounds__(kNT) long_chunk_kernel(const RP* __restrict__ 
 }
 
 int launch_split(const ExecArgs& a, cudaStream_t s) {
-  int n = a.stage != 2 ? launch_vector(a, true, s) : 0;
+  // 1. short rows: cta_stream over the compacted short-row CSR (writes every
+  //    row of y; emptied medium/long rows get 0), one lane per row
+  ExecArgs b = a;
+  b.A = a.S;
+  b.vs = 1;
+  b.dcol = nullptr;
+  int n = launch_stream(b, s);
+  // 2. medium rows: one warp per listed row (overwrites their y)
+  if (a.stage != 2 && a.n_mid > 0) {
+    launch_rowlist(a, a.mid_rows, a.n_mid, s);
+    ++n;
+  }
+  // 3. long rows: chunk partials, then the ordered per-row reduction (sets y)
   if (a.n_chunks > 0) {
     if (a.stage != 2) {
       ++n;
