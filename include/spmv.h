@@ -72,7 +72,8 @@ typedef struct spmv_options {
   int64_t long_chunk;      /* SPLIT chunk size in nonzeros (0 = 8192; multiple of 256) */
   int32_t emulate_devices; /* ngpus > 1: 1 = place every shard on the current device (tests) */
   int32_t stages;          /* STREAM smem ring depth: 0 = auto (one stage per consumer warp), else a multiple of 4 <= 32 */
-  int32_t reserved[6];
+  int32_t seg;             /* STREAM / SPLIT short part, segmented consumer mode: -1 auto, 0 off, 1 on */
+  int32_t reserved[5];
 } spmv_options;
 
 /* Theta(N) features (Table I) + counts used by the selection.
@@ -101,7 +102,7 @@ typedef struct spmv_selection {
   int32_t d16;       /* 1 when the delta-encoded colind stream is used */
   int32_t xwin;      /* 1 when the x persistence window is set */
   int32_t classes;   /* SPMV_CLASS_* bitmask */
-  int32_t pad_;
+  int32_t seg;       /* 1: cta_stream runs in segmented mode (random gathers: products first, balanced row walk) */
 } spmv_selection;
 
 typedef struct spmv_plan_info {

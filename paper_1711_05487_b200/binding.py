@@ -31,7 +31,8 @@ class Options(ctypes.Structure):
                 ("d16", ctypes.c_int32), ("xwin", ctypes.c_int32), ("validate", ctypes.c_int32),
                 ("l_split", ctypes.c_int64), ("k_long", ctypes.c_int64), ("tile_nnz", ctypes.c_int64),
                 ("merge_items", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
-                ("emulate_devices", ctypes.c_int32), ("stages", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+                ("emulate_devices", ctypes.c_int32), ("stages", ctypes.c_int32), ("seg", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
 
     @classmethod
     def make(cls, **kw):
@@ -60,7 +61,7 @@ class DeviceProps(ctypes.Structure):
 
 class Selection(ctypes.Structure):
     _fields_ = [("variant", ctypes.c_int32), ("vs", ctypes.c_int32), ("d16", ctypes.c_int32),
-                ("xwin", ctypes.c_int32), ("classes", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+                ("xwin", ctypes.c_int32), ("classes", ctypes.c_int32), ("seg", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):

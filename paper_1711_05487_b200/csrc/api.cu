@@ -197,6 +197,7 @@ struct spmv_plan_s {
     a.anchor = s.anchor;
     a.stages = s.stages;
     a.stream_grid = s.stream_grid;
+    a.seg = sel.seg != 0;
     a.items = s.items;
     a.Tm = s.Tm;
     a.mrow = s.mrow;
@@ -272,12 +273,20 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   if (variant != SPMV_VARIANT_STREAM) d16 = false;
   if (o.xwin == 0) xwin = false;
   if (o.xwin == 1) xwin = true;
+  // cta_stream consumer mode: segmented (products first, balanced row walk)
+  // for random-gather tiles: the long_row_split short part, or a STREAM
+  // matrix whose in-row gaps mostly exceed a cache line
+  bool seg = variant == SPMV_VARIANT_SPLIT ||
+             (variant == SPMV_VARIANT_STREAM && nnz > 0 && (double)f.misses > 0.75 * (double)nnz);
+  if (o.seg == 0) seg = false;
+  if (o.seg == 1) seg = variant == SPMV_VARIANT_SPLIT || variant == SPMV_VARIANT_STREAM;
+  if (d16) seg = false;
   s.variant = variant;
   s.vs = vs;
   s.d16 = d16 ? 1 : 0;
   s.xwin = xwin ? 1 : 0;
   s.classes = classes;
-  s.pad_ = 0;
+  s.seg = seg ? 1 : 0;
 }
 
 void validate_options(const spmv_options& o) {
@@ -575,7 +584,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       // short rows (len <= T_s) -> compacted CSR run by cta_stream,
       // medium rows (T_s < len <= L_split) -> ordered list, one warp per row,
       // long rows (len > L_split) -> chunk table
-      const int64_t ts = std::min<int64_t>(kShortRowMax, P->l_split);
+      // segmented cta_stream is balanced for any row length up to L_split, so
+      // the short bin takes every non-long row (no medium bin); the row-step
+      // mode keeps short rows only (one lane per row)
+      const int64_t ts = P->sel.seg ? P->l_split : std::min<int64_t>(kShortRowMax, P->l_split);
       int64_t* scan = s.alloc<int64_t>((size_t)scan_blocks(s.m) + 2);
       s.rp_s = s.alloc<char>((size_t)(s.m + 1) * rp_bytes);
       launch_filtered_csr(A, 0, ts, s.rp_s, nullptr, nullptr, scan, s.stream);
@@ -706,6 +718,7 @@ void spmv_options_default(spmv_options* o) {
   o->struct_size = (int32_t)sizeof(spmv_options);
   o->d16 = -1;
   o->xwin = -1;
+  o->seg = -1;
   o->validate = 1;
 }
 

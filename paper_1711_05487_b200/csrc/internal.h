@@ -60,6 +60,7 @@ struct ExecArgs {
   const int32_t* anchor;
   int stages;
   int stream_grid;
+  bool seg;  // cta_stream segmented mode (random-gather tiles)
   // MERGE
   int64_t items, Tm;
   const int32_t* mrow;
@@ -88,7 +89,7 @@ int launch_vector(const ExecArgs& a, bool skip_long, cudaStream_t s);  // return
 int launch_stream(const ExecArgs& a, cudaStream_t s);
 int launch_merge(const ExecArgs& a, cudaStream_t s);
 int launch_split(const ExecArgs& a, cudaStream_t s);
-size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, bool d16);
+size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, bool d16, bool seg);
 int stream_prepare(const ExecArgs& a);  // smem attribute + persistent grid (<0 on error)
 void launch_chunk_export(const ExecArgs& a, int64_t* out, cudaStream_t s);  // [row|begin|end] x n_chunks
 void launch_rebase(void* rowptr, int rp_bytes, int64_t count, int64_t base, cudaStream_t s);

@@ -45,15 +45,16 @@ struct TileMeta {
 __host__ __device__ __forceinline__ size_t al128(size_t v) { return (v + 127) & ~(size_t)127; }
 
 struct StreamLayout {
-  size_t vals, idx, rp, hd, stage, full, empty, meta, total;
+  size_t vals, idx, rp, hd, stage, full, empty, meta, prod, total;
   uint32_t rp_cap, hd_cap;  // bytes
 };
 
-// rows staged per tile: C/8 + 16 (average row length >= ~7; sparser tiles
-// read rowptr from global memory, still correct)
-__host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int rp_bytes, bool d16) {
+// rows staged per tile: C/8 + 16 (row-step; average row length >= ~7) or
+// C/4 + 32 (segmented); sparser tiles read rowptr from global memory (correct,
+// slower). SEG adds one C-double product buffer per consumer warp.
+__host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int rp_bytes, bool d16, bool seg) {
   StreamLayout L;
-  const size_t rows_cap = (size_t)C / 8 + 16;
+  const size_t rows_cap = seg ? (size_t)C / 4 + 32 : (size_t)C / 8 + 16;
   L.rp_cap = (uint32_t)(((rows_cap + 2) * rp_bytes + 32 + 15) & ~(size_t)15);
   L.hd_cap = d16 ? (uint32_t)(((rows_cap + 2) * 4 + 32 + 15) & ~(size_t)15) : 0u;
   L.vals = 0;
@@ -65,12 +66,14 @@ __host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int
   L.full = o; o += 8 * (size_t)stages;
   L.empty = o; o += 8 * (size_t)stages;
   L.meta = al128(o); o = L.meta + sizeof(TileMeta) * (size_t)stages;
+  L.prod = al128(o);
+  o = L.prod + (seg ? (size_t)kConsumerWarps * C * 8 : 0);
   L.total = al128(o);
   return L;
 }
 
-size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, bool d16) {
-  return stream_layout(C, stages, rp_bytes, d16).total;
+size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, bool d16, bool seg) {
+  return stream_layout(C, stages, rp_bytes, d16, seg).total;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -120,10 +123,100 @@ __device__ __forceinline__ void d16_row_cols(const uint16_t* __restrict__ d_s, i
   }
 }
 
-template <int VS, typename RP, bool D16>
-__global__ void __launch_bounds__(kStreamThreads, 8) stream_kernel(const StreamP<RP> p) {
+// SEG (segmented) consumer mode for random-gather (ML-class) tiles: products
+// first, lane l owning elements l + 32u (16 independent gathers in flight),
+// stored XOR-swizzled so the contiguous 16-element reads of the row pass are
+// bank-conflict free; then lane l walks elements [16l, 16l+16) and the row
+// ends inside them (a merge of row ends and nonzeros), rows cut by lane edges
+// are combined by a segmented shuffle scan in lane order. A row is written by
+// the tile where it ENDS; the row crossing the tile end is the tile's carry
+// (the ordered fix-up adds it). Balanced for any row-length mix.
+__device__ __forceinline__ int seg_swz(int e) { return e ^ ((e >> 4) & 15); }
+
+template <typename RP, typename Rows>
+__device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __restrict__ vals_s,
+                                         const int32_t* __restrict__ idx_s, double* __restrict__ prod,
+                                         const Rows& rows, int64_t fr, int nloc, int64_t t0, int cnt, int64_t k,
+                                         int lane) {
+  for (int ub = 0; ub < cnt; ub += 512) {
+    int c[16];
+    double xv[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = ub + lane + 32 * u;
+      c[u] = e < cnt ? idx_s[e] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) xv[u] = c[u] >= 0 ? ld_x(p.x + c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = ub + lane + 32 * u;
+      if (e < cnt) prod[seg_swz(e)] = vals_s[e] * xv[u];
+    }
+  }
+  __syncwarp();
+  const int E = (int)(p.C >> 5);
+  const int a = lane * E < cnt ? lane * E : cnt;
+  const int b = a + E < cnt ? a + E : cnt;
+  // unclamped local end of local row q (rows crossing the tile end have e > cnt)
+  auto rend = [&](int q) -> int64_t { return rows(fr + q + 1) - t0; };
+  int q = 0;
+  if (lane > 0) {  // first row with end > a
+    int lo = 0, hi = nloc;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (rend(mid) > a) hi = mid; else lo = mid + 1;
+    }
+    q = lo;
+  }
+  double acc = 0.0, first_val = 0.0;
+  int first = -1;
+  int64_t e_q = q < nloc ? rend(q) : INT64_MAX;
+  for (int t = a; t < b; ++t) {
+    while (e_q <= t) {
+      if (first < 0) { first = q; first_val = acc; }
+      else p.y[fr + q] = acc;
+      acc = 0.0;
+      ++q;
+      e_q = q < nloc ? rend(q) : INT64_MAX;
+    }
+    acc += prod[seg_swz(t)];
+  }
+  while (e_q <= b) {
+    if (first < 0) { first = q; first_val = acc; }
+    else p.y[fr + q] = acc;
+    acc = 0.0;
+    ++q;
+    e_q = q < nloc ? rend(q) : INT64_MAX;
+  }
+  // carry-out of this lane: the row in progress at b (if any)
+  int key = (q < nloc && b > a) ? q : -1 - lane;
+  double S = acc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int k2 = __shfl_up_sync(0xffffffffu, key, o);
+    const double S2 = __shfl_up_sync(0xffffffffu, S, o);
+    if (lane >= o && k2 == key) S += S2;
+  }
+  const int pk = __shfl_up_sync(0xffffffffu, key, 1);
+  const double pS = __shfl_up_sync(0xffffffffu, S, 1);
+  if (first >= 0) p.y[fr + first] = (lane > 0 && pk == first) ? pS + first_val : first_val;
+  const int key31 = __shfl_sync(0xffffffffu, key, 31);
+  const double S31 = __shfl_sync(0xffffffffu, S, 31);
+  if (lane == 0) {
+    if (key31 >= 0) {
+      p.carry_row[k] = (int32_t)(fr + key31);
+      p.carry_val[k] = S31;
+    } else {
+      p.carry_row[k] = -1;
+    }
+  }
+}
+
+template <int VS, typename RP, bool D16, bool SEG>
+__global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(const StreamP<RP> p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), D16);
+  const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), D16, SEG);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.empty);
   TileMeta* meta = reinterpret_cast<TileMeta*>(smem + L.meta);
@@ -214,7 +307,13 @@ __global__ void __launch_bounds__(kStreamThreads, 8) stream_kernel(const StreamP
     const int64_t fr = R0 - (incoming ? 1 : 0);
     const int nloc = (int)(R1 - R0) + (incoming ? 1 : 0);
 
-    (void)cnt;
+    if constexpr (SEG) {
+      seg_tile(p, vals_s, reinterpret_cast<const int32_t*>(st + L.idx),
+               reinterpret_cast<double*>(smem + L.prod) + (size_t)w * p.C, rows, fr, nloc, t0, cnt, k, lane32);
+      __syncwarp();
+      if (lane32 == 0) mbar_arrive(&empty[s]);
+      continue;
+    }
     // per-row products and sums, VS lanes per row (VS = 1 for short rows:
     // lanes walk consecutive rows in step, so a banded matrix gathers x from
     // 2-3 cache lines per warp instruction)
@@ -278,15 +377,15 @@ __global__ void __launch_bounds__(kStreamThreads, 8) stream_kernel(const StreamP
   }
 }
 
-template <int VS, typename RP, bool D16>
+template <int VS, typename RP, bool D16, bool SEG = false>
 static int stream_prepare_t(const ExecArgs& a) {
-  const size_t smem = stream_smem_bytes(a.C, a.stages, sizeof(RP), D16);
-  if (cudaFuncSetAttribute(stream_kernel<VS, RP, D16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
+  const size_t smem = stream_smem_bytes(a.C, a.stages, sizeof(RP), D16, SEG);
+  if (cudaFuncSetAttribute(stream_kernel<VS, RP, D16, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
     return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_kernel<VS, RP, D16>, kStreamThreads, smem) !=
-          cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_kernel<VS, RP, D16, SEG>, kStreamThreads,
+                                                    smem) != cudaSuccess ||
       per_sm < 1)
     return -1;
   int64_t grid = (int64_t)a.sm_count * per_sm;
@@ -294,7 +393,7 @@ static int stream_prepare_t(const ExecArgs& a) {
   return (int)grid;
 }
 
-template <int VS, typename RP, bool D16>
+template <int VS, typename RP, bool D16, bool SEG = false>
 static void stream_launch_t(const ExecArgs& a, cudaStream_t s) {
   StreamP<RP> p;
   p.rp = (const RP*)a.A.rowptr;
@@ -311,8 +410,8 @@ static void stream_launch_t(const ExecArgs& a, cudaStream_t s) {
   p.C = a.C;
   p.T = a.T;
   p.stages = a.stages;
-  const size_t smem = stream_smem_bytes(a.C, a.stages, sizeof(RP), D16);
-  stream_kernel<VS, RP, D16><<<a.stream_grid, kStreamThreads, smem, s>>>(p);
+  const size_t smem = stream_smem_bytes(a.C, a.stages, sizeof(RP), D16, SEG);
+  stream_kernel<VS, RP, D16, SEG><<<a.stream_grid, kStreamThreads, smem, s>>>(p);
 }
 
 template <typename RP, bool D16, bool PREP>
@@ -339,6 +438,16 @@ static int stream_vs(const ExecArgs& a, cudaStream_t s) {
 template <bool PREP>
 static int stream_dispatch(const ExecArgs& a, cudaStream_t s) {
   const bool d16 = a.dcol != nullptr;
+  if (a.seg && !d16) {  // segmented mode: one instantiation per rowptr width
+    if (a.A.rp_bytes == 8) {
+      if (PREP) return stream_prepare_t<1, int64_t, false, true>(a);
+      stream_launch_t<1, int64_t, false, true>(a, s);
+    } else {
+      if (PREP) return stream_prepare_t<1, int32_t, false, true>(a);
+      stream_launch_t<1, int32_t, false, true>(a, s);
+    }
+    return 0;
+  }
   if (a.A.rp_bytes == 8) return d16 ? stream_vs<int64_t, true, PREP>(a, s) : stream_vs<int64_t, false, PREP>(a, s);
   return d16 ? stream_vs<int32_t, true, PREP>(a, s) : stream_vs<int32_t, false, PREP>(a, s);
 }

@@ -36,19 +36,41 @@ def assert_bound(y, m, rows=None, tol=TOL):
 
 
 VARIANTS = [("vector", 1), ("vector", 2), ("vector", 8), ("vector", 32), ("stream", 1), ("stream", 4),
-            ("stream", 8), ("stream", 32), ("merge", 0), ("split", 4), ("split", 32)]
+            ("stream", 8), ("stream", 32), ("stream_seg", 1), ("merge", 0), ("split", 4), ("split_rowstep", 32)]
 
 SUITE = sg.small_suite(seed=21)
+
+
+def variant_kw(variant):
+    """test variant name -> (force_variant, extra options)"""
+    if variant == "stream_seg":
+        return "stream", {"seg": 1}
+    if variant == "stream_d16":
+        return "stream", {"d16": 1}
+    if variant == "split_rowstep":
+        return "split", {"seg": 0}
+    return variant, {}
 
 
 @pytest.mark.parametrize("variant,vs", VARIANTS)
 @pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
 def test_small_suite_all_variants(name, m, variant, vs):
-    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant=variant, force_vs=vs, l_split=64,
-                  tile_nnz=512)
+    fv, extra = variant_kw(variant)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant=fv, force_vs=vs, l_split=64,
+                  tile_nnz=512, **extra)
     y = p.execute(m.x)
     assert_bound(y, m)
-    assert p.info()["variant"] == variant
+    assert p.info()["variant"] == fv
+
+
+@pytest.mark.parametrize("tile", [128, 384, 1024])
+@pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
+def test_seg_mode_tiles(name, m, tile):
+    for fv in ("stream", "split"):
+        p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant=fv, seg=1, tile_nnz=tile,
+                      l_split=256)
+        assert p.info()["sel"]["seg"] == 1
+        assert_bound(p.execute(m.x), m)
 
 
 @pytest.mark.parametrize("variant,vs", VARIANTS + [("stream_d16", 8)])
@@ -56,8 +78,8 @@ def test_small_suite_all_variants(name, m, variant, vs):
                          ids=[n for n, _ in SUITE])
 def test_dyadic_bit_exact(name, m, variant, vs):
     kw = dict(force_vs=vs, l_split=64, tile_nnz=512)
-    if variant == "stream_d16":
-        variant, kw["d16"] = "stream", 1
+    variant, extra = variant_kw(variant)
+    kw.update(extra)
     p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant=variant, **kw)
     y = p.execute(m.x)
     assert np.array_equal(y, oracle.spmv(m.rowptr, m.colind, m.vals, m.x))

@@ -71,7 +71,7 @@ def main():
     auto = res[0]
     print(json.dumps({"auto": auto}), flush=True)
     grid = []
-    vss = (1, 2, 4, 8, 16, 32) if not a.quick else (4, 8)
+    vss = (1, 2, 4, 8, 16, 32) if not a.quick else (4, 8, 32)  # VS=32 = warp-per-row baseline
     for vs in vss:
         grid.append(dict(force_variant="vector", force_vs=vs))
     svs = (1, 2, 4) if not a.quick else (1, 4)
@@ -80,9 +80,12 @@ def main():
     d16s = (0, 1) if a.config in (1, 2) else (0,)
     for vs, t, sg_, d in itertools.product(svs, tiles, stages, d16s):
         grid.append(dict(force_variant="stream", force_vs=vs, tile_nnz=t, stages=sg_, d16=d))
+    for t in tiles:
+        grid.append(dict(force_variant="stream", seg=1, tile_nnz=t))
     grid.append(dict(force_variant="merge"))
-    for vs in vss:
-        grid.append(dict(force_variant="split", force_vs=vs))
+    for sg_ in (0, 1):
+        for t in tiles:
+            grid.append(dict(force_variant="split", seg=sg_, tile_nnz=t))
     for g in grid:
         try:
             r = run(**g)
