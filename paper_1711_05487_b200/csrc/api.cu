@@ -103,30 +103,17 @@ struct Shard {
   DevStats* stats = nullptr;
   DevStats hs{};
   int sm_count = 148;
-  // STREAM
-  int64_t C = 0, T = 0;
-  int32_t* tile_row = nullptr;
-  int32_t* carry_row = nullptr;
-  double* carry_val = nullptr;
-  bool need_fixup = false;
-  uint16_t* dcol = nullptr;
-  int32_t* head = nullptr;
-  int32_t* anchor = nullptr;
-  int stages = 4, stream_grid = 0;
+  // STREAM: sp[0] over the whole shard; SPLIT: sp[0] short bin, sp[1] medium bin
+  StreamPlan sp[2];
+  int n_sp = 0;
+  bool zero_y = false;
   // MERGE
   int64_t items = 0, Tm = 0;
   int32_t* mrow = nullptr;
   int64_t* mnnz = nullptr;
   int32_t* mcarry_row = nullptr;
   double* mcarry_val = nullptr;
-  // SPLIT: compacted short-row CSR (view sv), medium row list, long chunks
-  void* rp_s = nullptr;
-  int32_t* col_s = nullptr;
-  double* val_s = nullptr;
-  MatView sv{};
-  bool has_short = false;
-  int32_t* mid_rows = nullptr;
-  int64_t n_mid = 0;
+  // SPLIT long rows
   int64_t n_long = 0, n_chunks = 0;
   int32_t* long_rows = nullptr;
   int64_t* chunk_start = nullptr;
@@ -186,18 +173,10 @@ struct spmv_plan_s {
     a.y = y;
     a.vs = sel.vs;
     a.sm_count = s.sm_count;
-    a.C = s.C;
-    a.T = s.T;
-    a.tile_row = s.tile_row;
-    a.carry_row = s.carry_row;
-    a.carry_val = s.carry_val;
-    a.need_fixup = s.need_fixup;
-    a.dcol = sel.d16 ? s.dcol : nullptr;
-    a.head = s.head;
-    a.anchor = s.anchor;
-    a.stages = s.stages;
-    a.stream_grid = s.stream_grid;
-    a.seg = sel.seg != 0;
+    a.sp[0] = s.sp[0];
+    a.sp[1] = s.sp[1];
+    a.n_sp = s.n_sp;
+    a.zero_y = s.zero_y;
     a.items = s.items;
     a.Tm = s.Tm;
     a.mrow = s.mrow;
@@ -212,9 +191,6 @@ struct spmv_plan_s {
     a.chunk_start = s.chunk_start;
     a.chunk_row = s.chunk_row;
     a.chunk_val = s.chunk_val;
-    a.S = s.has_short ? s.sv : a.A;
-    a.mid_rows = s.mid_rows;
-    a.n_mid = s.n_mid;
     return a;
   }
   int launch(Shard& s, const double* x, double* y, int stage = 0) const {
@@ -276,8 +252,7 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   // cta_stream consumer mode: segmented (products first, balanced row walk)
   // for random-gather tiles: the long_row_split short part, or a STREAM
   // matrix whose in-row gaps mostly exceed a cache line
-  bool seg = variant == SPMV_VARIANT_SPLIT ||
-             (variant == SPMV_VARIANT_STREAM && nnz > 0 && (double)f.misses > 0.75 * (double)nnz);
+  bool seg = variant == SPMV_VARIANT_STREAM && nnz > 0 && (double)f.misses > 0.75 * (double)nnz;
   if (o.seg == 0) seg = false;
   if (o.seg == 1) seg = variant == SPMV_VARIANT_SPLIT || variant == SPMV_VARIANT_STREAM;
   if (d16) seg = false;
@@ -526,50 +501,97 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
 
   // ---- a3/a4: structures for the selected variant ---------------------------------
   double t_d = now_ms();
-  // cta_stream structures over the view V (the whole shard, or the compacted
-  // short-row CSR of long_row_split)
-  auto build_stream = [&](Shard& s, const MatView& V, bool d16, int vs) {
-    // tile size: ~28 rows of average length per consumer warp (B200 sweep:
-    // 512 best for 7-nnz rows, 768 for 27-nnz rows)
+  // cta_stream structures over the CSR view V (the whole shard, or one
+  // compacted length bin of long_row_split mapped back through rowmap)
+  auto build_stream = [&](Shard& s, StreamPlan& sp, const MatView& V, const int32_t* rowmap, bool d16, int vs,
+                          bool seg) {
+    sp.V = V;
+    sp.rowmap = rowmap;
+    sp.vs = vs;
+    sp.seg = seg;
     const double avg = V.m ? (double)V.nnz / (double)V.m : 0.0;
-    s.C = opt.tile_nnz > 0 ? opt.tile_nnz : (avg > 16 ? 768 : 512);
-    P->C = s.C;
-    s.T = std::max<int64_t>(1, (V.nnz + s.C - 1) / s.C);
-    s.tile_row = s.alloc<int32_t>((size_t)s.T + 1);
-    s.carry_row = s.alloc<int32_t>((size_t)s.T);
-    s.carry_val = s.alloc<double>((size_t)s.T);
-    launch_tile_rows(V, s.C, s.T, s.tile_row, s.stats, s.stream);
+    // tile size: one pass of the consumer warp over ~32 rows (row-step mode,
+    // B200 sweeps: 768 for 27-nnz rows, 384 for 15-nnz rows); 512 for rows of
+    // <= 12 nonzeros and for the segmented mode; VS > 1 groups: 32/VS rows
+    int64_t C = 512;
+    if (!seg && avg > 12) {
+      const double rows_per_pass = 32.0 / vs;
+      C = (int64_t)(rows_per_pass * avg / 128.0) * 128;
+      C = std::min<int64_t>(4096, std::max<int64_t>(384, C));
+    }
+    sp.C = opt.tile_nnz > 0 ? opt.tile_nnz : C;
+    P->C = sp.C;
+    sp.T = std::max<int64_t>(1, (V.nnz + sp.C - 1) / sp.C);
+    // staged rowptr entries: 1.5x the expected rows per tile (+32)
+    const double rpt = avg > 0 ? (double)sp.C / avg : (double)sp.C;
+    sp.rows_cap = (int)std::min<double>((double)sp.C + 32, 1.5 * rpt + 32);
+    sp.tile_row = s.alloc<int32_t>((size_t)sp.T + 1);
+    sp.carry_row = s.alloc<int32_t>((size_t)sp.T);
+    sp.carry_val = s.alloc<double>((size_t)sp.T);
+    DevStats zero{};
+    ck(cudaMemcpyAsync(&s.stats->n_incoming, &zero.n_incoming, 8, cudaMemcpyHostToDevice, s.stream), "stats");
+    launch_tile_rows(V, sp.C, sp.T, sp.tile_row, s.stats, s.stream);
     count_launches(1, "tile_rows");
     if (d16) {
-      s.dcol = s.alloc<uint16_t>((size_t)V.nnz);
-      s.head = s.alloc<int32_t>((size_t)V.m);
-      s.anchor = s.alloc<int32_t>((size_t)s.T);
-      launch_d16_encode(V, s.headbits, s.C, s.T, s.dcol, s.head, s.anchor, s.stream);
+      uint16_t* dcol = s.alloc<uint16_t>((size_t)V.nnz);
+      int32_t* head = s.alloc<int32_t>((size_t)V.m);
+      int32_t* anchor = s.alloc<int32_t>((size_t)sp.T);
+      launch_d16_encode(V, s.headbits, sp.C, sp.T, dcol, head, anchor, s.stream);
       count_launches(3, "d16_encode");
+      sp.dcol = dcol;
+      sp.head = head;
+      sp.anchor = anchor;
     }
     ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
     ck(cudaStreamSynchronize(s.stream), "tiles");
-    s.need_fixup = s.hs.n_incoming > 0;
+    sp.need_fixup = s.hs.n_incoming > 0;
     // one stage per consumer warp: measured on B200 (tools/sweep.py, C2/C5),
     // more resident warps beat a deeper ring (the x gathers are latency-bound)
-    s.stages = opt.stages > 0 ? opt.stages : kStreamConsumerWarps;
-    ExecArgs a = P->args(s, nullptr, nullptr);
-    a.A = V;
-    a.vs = vs;
-    s.stream_grid = stream_prepare(a);
-    if (s.stream_grid < 0 && s.stages > kStreamConsumerWarps) {
+    sp.stages = opt.stages > 0 ? opt.stages : kStreamConsumerWarps;
+    sp.grid = stream_prepare(sp, s.sm_count);
+    if (sp.grid < 0 && sp.stages > kStreamConsumerWarps) {
       cudaGetLastError();
-      s.stages = kStreamConsumerWarps;
-      a.stages = s.stages;
-      s.stream_grid = stream_prepare(a);
+      sp.stages = kStreamConsumerWarps;
+      sp.grid = stream_prepare(sp, s.sm_count);
     }
-    if (s.stream_grid < 0) fail(SPMV_E_CUDA, "cta_stream: cannot fit tile_nnz=%lld in shared memory", (long long)s.C);
+    if (sp.grid < 0) fail(SPMV_E_CUDA, "cta_stream: cannot fit tile_nnz=%lld in shared memory", (long long)sp.C);
+  };
+  // compacted bin of the rows with lo <= len <= hi (non-empty), for cta_stream
+  auto build_bin = [&](Shard& s, StreamPlan& sp, const MatView& A, int64_t lo, int64_t hi, int vs, bool seg,
+                       int64_t* scan) -> bool {
+    const int64_t nb = scan_blocks(s.m);
+    int64_t nrows = 0;
+    launch_row_list(A, lo, hi, nullptr, scan, s.stream);  // count
+    count_launches(2, "bin count");
+    ck(cudaMemcpyAsync(&nrows, scan + nb, 8, cudaMemcpyDeviceToHost, s.stream), "bin count");
+    ck(cudaStreamSynchronize(s.stream), "bin count");
+    if (nrows == 0) return false;
+    int32_t* rows = s.alloc<int32_t>((size_t)nrows);
+    launch_row_list(A, lo, hi, rows, scan, s.stream);
+    count_launches(3, "bin rows");
+    void* frp = s.alloc<char>((size_t)(s.m + 1) * rp_bytes);
+    launch_filtered_csr(A, lo, hi, frp, nullptr, nullptr, scan, s.stream);
+    count_launches(3, "bin rowptr");
+    int64_t bnnz = 0;
+    ck(cudaMemcpyAsync(&bnnz, (char*)frp + s.m * rp_bytes, rp_bytes, cudaMemcpyDeviceToHost, s.stream), "bin nnz");
+    ck(cudaStreamSynchronize(s.stream), "bin nnz");
+    if (rp_bytes == 4) bnnz = (int32_t)bnnz;
+    int32_t* bcol = s.alloc<int32_t>((size_t)bnnz);
+    double* bval = s.alloc<double>((size_t)bnnz);
+    launch_filtered_csr(A, lo, hi, frp, bcol, bval, scan, s.stream);
+    count_launches(4, "bin csr");
+    void* brp = s.alloc<char>((size_t)(nrows + 1) * rp_bytes);
+    launch_gather_rowptr(frp, rp_bytes, rows, nrows, s.m, brp, s.stream);
+    count_launches(1, "bin gather");
+    build_stream(s, sp, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, rows, false, vs, seg);
+    return true;
   };
   for (auto& s : P->shards) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const MatView A = s.view();
     if (P->sel.variant == SPMV_VARIANT_STREAM) {
-      build_stream(s, A, P->sel.d16, P->sel.vs);
+      build_stream(s, s.sp[0], A, nullptr, P->sel.d16, P->sel.vs, P->sel.seg != 0);
+      s.n_sp = 1;
     } else if (P->sel.variant == SPMV_VARIANT_MERGE) {
       s.items = P->items;
       s.Tm = std::max<int64_t>(1, (s.m + s.nnz + s.items - 1) / s.items);
@@ -580,41 +602,19 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       launch_merge_splits(A, s.items, s.Tm, s.mrow, s.mnnz, s.stream);
       count_launches(1, "merge_splits");
     } else if (P->sel.variant == SPMV_VARIANT_SPLIT) {
-      // decomposition by row length (Fig. 6 read through S:120-125):
-      // short rows (len <= T_s) -> compacted CSR run by cta_stream,
-      // medium rows (T_s < len <= L_split) -> ordered list, one warp per row,
-      // long rows (len > L_split) -> chunk table
-      // segmented cta_stream is balanced for any row length up to L_split, so
-      // the short bin takes every non-long row (no medium bin); the row-step
-      // mode keeps short rows only (one lane per row)
-      const int64_t ts = P->sel.seg ? P->l_split : std::min<int64_t>(kShortRowMax, P->l_split);
+      // decomposition by row length (P:608-621; Fig. 6 read through S:120-125):
+      // short rows (1 <= len <= T_s) and medium rows (T_s < len <= L_split)
+      // become compacted CSR bins run by cta_stream (one lane per short row,
+      // a 32-lane group per medium row; segmented mode: one bin up to
+      // L_split); long rows (len > L_split) become the chunk table; empty rows
+      // are covered by clearing y first
+      const bool seg = P->sel.seg != 0;
+      const int64_t ts = seg ? P->l_split : std::min<int64_t>(kShortRowMax, P->l_split);
       int64_t* scan = s.alloc<int64_t>((size_t)scan_blocks(s.m) + 2);
-      s.rp_s = s.alloc<char>((size_t)(s.m + 1) * rp_bytes);
-      launch_filtered_csr(A, 0, ts, s.rp_s, nullptr, nullptr, scan, s.stream);
-      count_launches(3, "short rowptr");
-      int64_t nnz_s = 0;
-      ck(cudaMemcpyAsync(&nnz_s, (char*)s.rp_s + s.m * rp_bytes, rp_bytes, cudaMemcpyDeviceToHost, s.stream),
-         "short nnz");
-      ck(cudaStreamSynchronize(s.stream), "short nnz");
-      s.col_s = s.alloc<int32_t>((size_t)nnz_s);
-      s.val_s = s.alloc<double>((size_t)nnz_s);
-      launch_filtered_csr(A, 0, ts, s.rp_s, s.col_s, s.val_s, scan, s.stream);
-      count_launches(4, "short csr");
-      s.sv = MatView{rp_bytes, s.rp_s, s.col_s, s.val_s, s.m, s.n_cols, nnz_s};
-      s.has_short = true;
-      build_stream(s, s.sv, false, 1);
-      if (P->l_split > ts) {
-        launch_row_list(A, ts + 1, P->l_split, nullptr, scan, s.stream);  // count only
-        count_launches(2, "medium count");
-        const int64_t nb = scan_blocks(s.m);
-        ck(cudaMemcpyAsync(&s.n_mid, scan + nb, 8, cudaMemcpyDeviceToHost, s.stream), "medium count");
-        ck(cudaStreamSynchronize(s.stream), "medium count");
-        if (s.n_mid > 0) {
-          s.mid_rows = s.alloc<int32_t>((size_t)s.n_mid);
-          launch_row_list(A, ts + 1, P->l_split, s.mid_rows, scan, s.stream);
-          count_launches(3, "medium rows");
-        }
-      }
+      s.n_sp = 0;
+      if (build_bin(s, s.sp[s.n_sp], A, 1, ts, 1, seg, scan)) ++s.n_sp;
+      if (P->l_split > ts && build_bin(s, s.sp[s.n_sp], A, ts + 1, P->l_split, 32, false, scan)) ++s.n_sp;
+      s.zero_y = true;
       s.n_long = s.hs.n_long;
       if (s.n_long > 0) {
         const int nb = 1024;
@@ -851,8 +851,8 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     info->feat = p->feat;
     info->d16_width = p->d16_width;
     const Shard& s0 = p->shards[0];
-    info->tile_nnz = s0.C;
-    info->n_tiles = s0.T;
+    info->tile_nnz = s0.sp[0].C;
+    info->n_tiles = s0.sp[0].T;
     info->merge_items = s0.items;
     info->n_merge_tiles = s0.Tm;
     info->l_split = p->l_split;
@@ -900,7 +900,7 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
       ck(cudaMemcpy(dst, src, (size_t)n * es, cudaMemcpyDeviceToHost), "export");
     };
     switch (which) {
-      case SPMV_ARR_TILE_ROWS: widen32(s.tile_row, s.tile_row ? s.T + 1 : 0); break;
+      case SPMV_ARR_TILE_ROWS: widen32(s.sp[0].tile_row, s.sp[0].tile_row ? s.sp[0].T + 1 : 0); break;
       case SPMV_ARR_MERGE_ROWS: widen32(s.mrow, s.mrow ? s.Tm + 1 : 0); break;
       case SPMV_ARR_MERGE_NNZ: raw(s.mnnz, s.mnnz ? s.Tm + 1 : 0, 8); break;
       case SPMV_ARR_CHUNK_ROW:
@@ -922,15 +922,15 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
         ck(e, "chunk export");
         break;
       }
-      case SPMV_ARR_DCOL: raw(s.dcol, s.dcol ? s.nnz : 0, 2); break;
-      case SPMV_ARR_HEAD: raw(s.head, s.head ? s.m : 0, 4); break;
-      case SPMV_ARR_ANCHOR: raw(s.anchor, s.anchor ? s.T : 0, 4); break;
+      case SPMV_ARR_DCOL: raw(s.sp[0].dcol, s.sp[0].dcol ? s.nnz : 0, 2); break;
+      case SPMV_ARR_HEAD: raw(s.sp[0].head, s.sp[0].head ? s.m : 0, 4); break;
+      case SPMV_ARR_ANCHOR: raw(s.sp[0].anchor, s.sp[0].anchor ? s.sp[0].T : 0, 4); break;
       case SPMV_ARR_DECODED: {
-        count = s.dcol ? s.nnz : 0;
+        count = s.sp[0].dcol ? s.nnz : 0;
         if (!dst || count == 0) break;
         int32_t* tmp = nullptr;
         ck(cudaMalloc(&tmp, (size_t)s.nnz * 4 + 64), "cudaMalloc");
-        launch_d16_decode_export(s.view(), s.dcol, s.head, s.anchor, s.tile_row, s.C, s.T, p->sel.vs, tmp, s.stream);
+        launch_d16_decode_export(s.sp[0], tmp, s.stream);
         g_launches += 1;
         cudaError_t e = cudaStreamSynchronize(s.stream);
         if (e == cudaSuccess) e = cudaMemcpy(dst, tmp, (size_t)s.nnz * 4, cudaMemcpyDeviceToHost);

@@ -235,6 +235,25 @@ void launch_row_list(const MatView& A, int64_t lo, int64_t hi, int32_t* out, int
   else row_list_t<int32_t>(A, lo, hi, out, scratch, s);
 }
 
+// ---- compacted rowptr of a bin ---------------------------------------------------
+template <typename RP>
+__global__ void gather_rowptr_kernel(const RP* __restrict__ frp, const int32_t* __restrict__ rows, int64_t n,
+                                     int64_t m, RP* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q <= n; q += stride)
+    out[q] = q < n ? frp[rows[q]] : frp[m];
+}
+
+void launch_gather_rowptr(const void* frp, int rp_bytes, const int32_t* rows, int64_t n, int64_t m, void* out,
+                          cudaStream_t s) {
+  int64_t g = (n + 1 + kNT - 1) / kNT;
+  if (g > 148 * 16) g = 148 * 16;
+  if (rp_bytes == 8)
+    gather_rowptr_kernel<int64_t><<<(int)g, kNT, 0, s>>>((const int64_t*)frp, rows, n, m, (int64_t*)out);
+  else
+    gather_rowptr_kernel<int32_t><<<(int)g, kNT, 0, s>>>((const int32_t*)frp, rows, n, m, (int32_t*)out);
+}
+
 // ---- medium rows: one VS-lane group per listed row ----------------------------
 template <int VS, typename RP>
 __global__ void __launch_bounds__(kNT) rowlist_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ col,

@@ -1,4 +1,4 @@
-// internal.h -- host-side declarations shared by api.cu and kernels.cu.
+// internal.h -- host-side declarations shared by api.cu and the kernel files.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -8,6 +8,7 @@ namespace spmv {
 constexpr int kNT = 256;  // threads per CTA for every SpMV kernel
 constexpr int kNormPartials = 512;  // fixed row chunking of the norm reduction
 constexpr int kStreamConsumerWarps = 4;  // cta_stream consumer warps per CTA (stages: multiple of this)
+constexpr int64_t kShortRowMax = 32;  // SPLIT: rows up to this length form the one-lane-per-row bin
 
 // Device-side inspector accumulators (integers only => order-independent).
 struct DevStats {
@@ -27,6 +28,23 @@ struct MatView {
   int64_t m, n_cols, nnz;
 };
 
+// One cta_stream pass over the CSR view V (the whole shard, or one compacted
+// length bin of long_row_split whose row q is row rowmap[q] of y).
+struct StreamPlan {
+  MatView V{};
+  const int32_t* rowmap = nullptr;  // nullptr = identity
+  int64_t C = 0, T = 0;
+  int32_t* tile_row = nullptr;
+  int32_t* carry_row = nullptr;
+  double* carry_val = nullptr;
+  bool need_fixup = false;
+  const uint16_t* dcol = nullptr;  // D16 stream (nullptr = int32 colind)
+  const int32_t* head = nullptr;
+  const int32_t* anchor = nullptr;
+  int stages = 0, grid = 0, vs = 1, rows_cap = 0;
+  bool seg = false;  // segmented consumer mode (random-gather tiles)
+};
+
 // ---- inspector ------------------------------------------------------------
 void launch_rowstats(const MatView& A, int64_t l_split, uint32_t* headbits, DevStats* st, cudaStream_t s);
 void launch_validate_gaps(const MatView& A, const uint32_t* headbits, DevStats* st, cudaStream_t s);
@@ -37,9 +55,21 @@ void launch_long_rows(const MatView& A, int64_t l_split, int64_t chunk, int32_t*
                       int64_t* chunk_start, int32_t* scratch_counts, int nblocks_scratch, cudaStream_t s);
 void launch_d16_encode(const MatView& A, const uint32_t* headbits, int64_t C, int64_t T, uint16_t* dcol,
                        int32_t* head, int32_t* anchor, cudaStream_t s);
-void launch_d16_decode_export(const MatView& A, const uint16_t* dcol, const int32_t* head, const int32_t* anchor,
-                              const int32_t* tile_row, int64_t C, int64_t T, int vs, int32_t* out, cudaStream_t s);
+void launch_d16_decode_export(const StreamPlan& sp, int32_t* out, cudaStream_t s);
 void launch_fixup(const int32_t* crow, const double* cval, int64_t T, double* y, int set, cudaStream_t s);
+void launch_rebase(void* rowptr, int rp_bytes, int64_t count, int64_t base, cudaStream_t s);
+
+// ---- length bins (bins.cu) ----------------------------------------------------
+int64_t scan_blocks(int64_t m);
+// rowptr (and colind/values when out_col != null) of the rows with lo <= len <= hi,
+// every other row empty (same row count)
+void launch_filtered_csr(const MatView& A, int64_t lo, int64_t hi, void* out_rp, int32_t* out_col, double* out_val,
+                         int64_t* scratch, cudaStream_t s);
+// ordered list of the rows with lo <= len <= hi (count in scratch[scan_blocks(m)]; out may be null)
+void launch_row_list(const MatView& A, int64_t lo, int64_t hi, int32_t* out, int64_t* scratch, cudaStream_t s);
+// compacted rowptr: out[q] = frp[rows[q]] (q < n), out[n] = frp[m]
+void launch_gather_rowptr(const void* frp, int rp_bytes, const int32_t* rows, int64_t n, int64_t m, void* out,
+                          cudaStream_t s);
 
 // ---- SpMV variants ----------------------------------------------------------
 struct ExecArgs {
@@ -49,50 +79,32 @@ struct ExecArgs {
   int vs;
   int sm_count;
   int stage;  // 0 = whole SpMV, 1 = main kernel(s) only, 2 = epilogue (fix-up) only
-  // STREAM
-  int64_t C, T;
-  const int32_t* tile_row;
-  int32_t* carry_row;
-  double* carry_val;
-  bool need_fixup;
-  const uint16_t* dcol;
-  const int32_t* head;
-  const int32_t* anchor;
-  int stages;
-  int stream_grid;
-  bool seg;  // cta_stream segmented mode (random-gather tiles)
+  // STREAM (sp[0]) / SPLIT bins (sp[0] short, sp[1] medium)
+  StreamPlan sp[2];
+  int n_sp;
+  bool zero_y;  // SPLIT over compacted bins: y = 0 before the bin kernels
   // MERGE
   int64_t items, Tm;
   const int32_t* mrow;
   const int64_t* mnnz;
   int32_t* mcarry_row;
   double* mcarry_val;
-  // SPLIT
+  // SPLIT long rows
   int64_t l_split, chunk, n_long, n_chunks;
   const int32_t* long_rows;
   const int64_t* chunk_start;
   int32_t* chunk_row;
   double* chunk_val;
-  MatView S;                 // SPLIT: compacted short-row CSR (other rows empty)
-  const int32_t* mid_rows;   // SPLIT: medium rows, one warp each
-  int64_t n_mid;
 };
 
-constexpr int64_t kShortRowMax = 32;  // SPLIT: rows up to this length go to cta_stream (one lane per row)
-int64_t scan_blocks(int64_t m);
-void launch_filtered_csr(const MatView& A, int64_t lo, int64_t hi, void* out_rp, int32_t* out_col, double* out_val,
-                         int64_t* scratch, cudaStream_t s);
-void launch_row_list(const MatView& A, int64_t lo, int64_t hi, int32_t* out, int64_t* scratch, cudaStream_t s);
-void launch_rowlist(const ExecArgs& a, const int32_t* rows, int64_t nrows, cudaStream_t s);
-
 int launch_vector(const ExecArgs& a, bool skip_long, cudaStream_t s);  // returns #launches
+int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int stage, cudaStream_t s);
 int launch_stream(const ExecArgs& a, cudaStream_t s);
 int launch_merge(const ExecArgs& a, cudaStream_t s);
 int launch_split(const ExecArgs& a, cudaStream_t s);
-size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, bool d16, bool seg);
-int stream_prepare(const ExecArgs& a);  // smem attribute + persistent grid (<0 on error)
+size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, int rows_cap, bool d16, bool seg);
+int stream_prepare(const StreamPlan& sp, int sm_count);  // smem attribute + persistent grid (<0 on error)
 void launch_chunk_export(const ExecArgs& a, int64_t* out, cudaStream_t s);  // [row|begin|end] x n_chunks
-void launch_rebase(void* rowptr, int rp_bytes, int64_t count, int64_t base, cudaStream_t s);
 
 // ---- iterated mode -------------------------------------------------------------
 int launch_norm_partials(const double* y, int64_t m, double* partials, cudaStream_t s);

@@ -1,36 +1,32 @@
 // stream.cu -- cta_stream: the MB-class kernel (Table II "vectorization" +
-// delta colind) re-designed for sm_100a.
+// delta colind) re-designed for sm_100a; also the engine of the
+// long_row_split bins.
 //
-// Persistent, warp-specialised CTAs, one consumer WARP per tile. Tile k
-// covers the fixed nonzero range [k*C, min((k+1)*C, nnz)) and owns rows
-// [R_k, R_{k+1}).
+// Persistent, warp-specialised CTAs: 1 producer warp + W = 4 consumer warps,
+// one consumer WARP per tile. Tile k covers the fixed nonzero range
+// [k*C, min((k+1)*C, nnz)) and owns rows [R_k, R_{k+1}).
 //  * producer warp (one lane): TMA bulk copies (cp.async.bulk + mbarrier
 //    complete_tx, L2 evict_first) of the tile's values, colind (or 16-bit
-//    deltas), rowptr slice and (D16) row heads into an S-stage smem ring.
-//    Tile i of the CTA goes to stage i % S and consumer warp i % W; the
-//    producer refills a stage when its warp releases it (empty mbarrier).
-//    No __syncthreads after set-up: W tiles are in compute per CTA while the
-//    next S - W tiles stream in.
-//  * consumer warp, int32 colind: (1) products: each lane reads 4 consecutive
-//    colind / values with 128-bit smem loads and keeps C/32 x gathers in
-//    flight (x through L1/L2; neighbouring rows share x lines), products
-//    overwrite the values in smem; (2) rows: VS lanes per row sum the
-//    products, butterfly within the group.
-//  * consumer warp, D16: VS lanes per row, each lane owns a contiguous piece
-//    of the row; absolute columns are head[r] (or the tile anchor for the row
-//    entering the tile) + a subgroup exclusive scan of the lanes' delta sums
-//    + a running sum; gathers and FMAs follow the decode.
-//  The row entering the tile from the previous one goes to carry[k] (ordered
-//  fix-up kernel); every owned row is written to y (its head part if it
-//  continues into later tiles).
+//    deltas), rowptr slice and (D16) row heads into the consumer warp's smem
+//    stage. Tile i of the CTA goes to stage i % S and warp i % W; S is a
+//    multiple of W, so a stage's mbarrier phases are consumed in order. One
+//    stage per warp by default: on B200 more resident warps beat a deeper
+//    ring (the x gathers are latency-bound). No __syncthreads after set-up.
+//  * row-step mode (default): VS lanes per row, lanes of a warp walk
+//    consecutive rows in step (VS = 1 for rows up to 32 nonzeros), so a
+//    banded matrix gathers x from 2-3 cache lines per warp instruction; each
+//    lane keeps 8 predicated gathers in flight. D16 rows are decoded per lane
+//    piece (head or tile anchor + subgroup scan + running sum).
+//  * segmented mode (option): products first, then a warp-balanced walk of
+//    row ends over 16-element lane ranges (any row-length mix).
+//  Rows are written to y[rowmap[r]] (identity without a map). In row-step
+//  mode the row entering a tile is the tile's carry; in segmented mode the
+//  row leaving it is; the ordered fix-up kernel adds carries in tile order.
 #include "common.cuh"
 #include "internal.h"
 
 namespace spmv {
 
-// W consumer warps; the ring depth S is a multiple of W, so every stage is
-// owned by one warp and its mbarrier phases are consumed strictly in order
-// (a parity wait can never run two phases ahead).
 constexpr int kConsumerWarps = kStreamConsumerWarps;
 constexpr int kStreamThreads = 32 * (kConsumerWarps + 1);
 
@@ -49,14 +45,13 @@ struct StreamLayout {
   uint32_t rp_cap, hd_cap;  // bytes
 };
 
-// rows staged per tile: C/8 + 16 (row-step; average row length >= ~7) or
-// C/4 + 32 (segmented); sparser tiles read rowptr from global memory (correct,
-// slower). SEG adds one C-double product buffer per consumer warp.
-__host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int rp_bytes, bool d16, bool seg) {
+// rows_cap: rowptr entries staged per tile (plan-time, from the view's
+// average row length); tiles with more rows read rowptr from global memory.
+__host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int rp_bytes, int rows_cap, bool d16,
+                                                      bool seg) {
   StreamLayout L;
-  const size_t rows_cap = seg ? (size_t)C / 4 + 32 : (size_t)C / 8 + 16;
-  L.rp_cap = (uint32_t)(((rows_cap + 2) * rp_bytes + 32 + 15) & ~(size_t)15);
-  L.hd_cap = d16 ? (uint32_t)(((rows_cap + 2) * 4 + 32 + 15) & ~(size_t)15) : 0u;
+  L.rp_cap = (uint32_t)(((size_t)(rows_cap + 2) * rp_bytes + 32 + 15) & ~(size_t)15);
+  L.hd_cap = d16 ? (uint32_t)(((size_t)(rows_cap + 2) * 4 + 32 + 15) & ~(size_t)15) : 0u;
   L.vals = 0;
   L.idx = al128((size_t)C * 8);
   L.rp = al128(L.idx + (size_t)C * (d16 ? 2 : 4));
@@ -72,8 +67,8 @@ __host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int
   return L;
 }
 
-size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, bool d16, bool seg) {
-  return stream_layout(C, stages, rp_bytes, d16, seg).total;
+size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, int rows_cap, bool d16, bool seg) {
+  return stream_layout(C, stages, rp_bytes, rows_cap, d16, seg).total;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -89,12 +84,18 @@ struct StreamP {
   const double* val;
   const double* x;
   double* y;
+  const int32_t* rowmap;
   const int32_t* tile_row;
   int32_t* carry_row;
   double* carry_val;
   int64_t nnz, C, T;
-  int stages;
+  int stages, rows_cap;
 };
+
+template <typename RP>
+__device__ __forceinline__ int64_t out_row(const StreamP<RP>& p, int64_t r) {
+  return p.rowmap ? (int64_t)ld_ro(p.rowmap + r) : r;
+}
 
 // D16 columns of one row's lane piece: calls f(t, col) for t in the lane's
 // contiguous sub-range of [ls, le). Every lane of the VS-group must call it.
@@ -123,14 +124,12 @@ __device__ __forceinline__ void d16_row_cols(const uint16_t* __restrict__ d_s, i
   }
 }
 
-// SEG (segmented) consumer mode for random-gather (ML-class) tiles: products
-// first, lane l owning elements l + 32u (16 independent gathers in flight),
-// stored XOR-swizzled so the contiguous 16-element reads of the row pass are
-// bank-conflict free; then lane l walks elements [16l, 16l+16) and the row
-// ends inside them (a merge of row ends and nonzeros), rows cut by lane edges
+// Segmented consumer mode: products first (lane l owns elements l + 32u, 16
+// independent gathers in flight), stored XOR-swizzled so the contiguous
+// 16-element reads of the row pass are bank-conflict free; lane l then walks
+// elements [16l, 16l+16) and the row ends inside them; rows cut by lane edges
 // are combined by a segmented shuffle scan in lane order. A row is written by
-// the tile where it ENDS; the row crossing the tile end is the tile's carry
-// (the ordered fix-up adds it). Balanced for any row-length mix.
+// the tile where it ENDS; the row crossing the tile end is the tile's carry.
 __device__ __forceinline__ int seg_swz(int e) { return e ^ ((e >> 4) & 15); }
 
 template <typename RP, typename Rows>
@@ -158,8 +157,7 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
   const int E = (int)(p.C >> 5);
   const int a = lane * E < cnt ? lane * E : cnt;
   const int b = a + E < cnt ? a + E : cnt;
-  // unclamped local end of local row q (rows crossing the tile end have e > cnt)
-  auto rend = [&](int q) -> int64_t { return rows(fr + q + 1) - t0; };
+  auto rend = [&](int q) -> int64_t { return rows(fr + q + 1) - t0; };  // unclamped
   int q = 0;
   if (lane > 0) {  // first row with end > a
     int lo = 0, hi = nloc;
@@ -175,7 +173,7 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
   for (int t = a; t < b; ++t) {
     while (e_q <= t) {
       if (first < 0) { first = q; first_val = acc; }
-      else p.y[fr + q] = acc;
+      else p.y[out_row(p, fr + q)] = acc;
       acc = 0.0;
       ++q;
       e_q = q < nloc ? rend(q) : INT64_MAX;
@@ -184,12 +182,11 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
   }
   while (e_q <= b) {
     if (first < 0) { first = q; first_val = acc; }
-    else p.y[fr + q] = acc;
+    else p.y[out_row(p, fr + q)] = acc;
     acc = 0.0;
     ++q;
     e_q = q < nloc ? rend(q) : INT64_MAX;
   }
-  // carry-out of this lane: the row in progress at b (if any)
   int key = (q < nloc && b > a) ? q : -1 - lane;
   double S = acc;
 #pragma unroll
@@ -200,12 +197,12 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
   }
   const int pk = __shfl_up_sync(0xffffffffu, key, 1);
   const double pS = __shfl_up_sync(0xffffffffu, S, 1);
-  if (first >= 0) p.y[fr + first] = (lane > 0 && pk == first) ? pS + first_val : first_val;
+  if (first >= 0) p.y[out_row(p, fr + first)] = (lane > 0 && pk == first) ? pS + first_val : first_val;
   const int key31 = __shfl_sync(0xffffffffu, key, 31);
   const double S31 = __shfl_sync(0xffffffffu, S, 31);
   if (lane == 0) {
     if (key31 >= 0) {
-      p.carry_row[k] = (int32_t)(fr + key31);
+      p.carry_row[k] = (int32_t)out_row(p, fr + key31);
       p.carry_val[k] = S31;
     } else {
       p.carry_row[k] = -1;
@@ -216,7 +213,7 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
 template <int VS, typename RP, bool D16, bool SEG>
 __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(const StreamP<RP> p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), D16, SEG);
+  const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), p.rows_cap, D16, SEG);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.empty);
   TileMeta* meta = reinterpret_cast<TileMeta*>(smem + L.meta);
@@ -293,7 +290,7 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(con
     mbar_wait(&full[s], (uint32_t)((i / S) & 1));
     const TileMeta mt = meta[s];
     unsigned char* st = smem + L.stage * s;
-    double* vals_s = reinterpret_cast<double*>(st + L.vals);
+    const double* vals_s = reinterpret_cast<const double*>(st + L.vals);
     const RP* rp_s = reinterpret_cast<const RP*>(st + L.rp);
     const int64_t t0 = k * p.C;
     const int64_t t1 = (t0 + p.C) < p.nnz ? (t0 + p.C) : p.nnz;
@@ -310,76 +307,94 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(con
     if constexpr (SEG) {
       seg_tile(p, vals_s, reinterpret_cast<const int32_t*>(st + L.idx),
                reinterpret_cast<double*>(smem + L.prod) + (size_t)w * p.C, rows, fr, nloc, t0, cnt, k, lane32);
-      __syncwarp();
-      if (lane32 == 0) mbar_arrive(&empty[s]);
-      continue;
-    }
-    // per-row products and sums, VS lanes per row (VS = 1 for short rows:
-    // lanes walk consecutive rows in step, so a banded matrix gathers x from
-    // 2-3 cache lines per warp instruction)
-    for (int qb = 0; qb < nloc; qb += GPW) {
-      const int q = qb + gi;
-      const bool active = q < nloc;
-      int ls = 0, le = 0;
-      int64_t r = 0;
-      if (active) {
-        r = fr + q;
-        const int64_t a = rows(r), b = rows(r + 1);
-        ls = (int)((a > t0 ? a : t0) - t0);
-        le = (int)((b < t1 ? b : t1) - t0);
-      }
-      double acc;
-      if (!D16) {
-        // batches of 8 predicated elements per lane: 8 independent gathers in flight
-        const int32_t* idx_s = reinterpret_cast<const int32_t*>(st + L.idx);
-        double a0 = 0.0, a1 = 0.0;
-        for (int l0 = ls + lane; l0 < le; l0 += 8 * VS) {
-          int c[8];
-          double v[8], xv[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int l = l0 + u * VS;
-            c[u] = l < le ? idx_s[l] : -1;
-            v[u] = l < le ? vals_s[l] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_x(p.x + c[u]) : 0.0;
-#pragma unroll
-          for (int u = 0; u < 8; u += 2) {
-            a0 = fma(v[u], xv[u], a0);
-            a1 = fma(v[u + 1], xv[u + 1], a1);
-          }
+    } else {
+      for (int qb = 0; qb < nloc; qb += GPW) {
+        const int q = qb + gi;
+        const bool active = q < nloc;
+        int ls = 0, le = 0;
+        int64_t r = 0;
+        if (active) {
+          r = fr + q;
+          const int64_t a = rows(r), b = rows(r + 1);
+          ls = (int)((a > t0 ? a : t0) - t0);
+          le = (int)((b < t1 ? b : t1) - t0);
         }
-        acc = a0 + a1;
-      } else {
-        const uint16_t* d_s = reinterpret_cast<const uint16_t*>(st + L.idx);
-        const int32_t* hd_s = reinterpret_cast<const int32_t*>(st + L.hd);
-        int base = mt.anchor;
-        if (active && (!incoming || q > 0))
-          base = mt.hd_off >= 0 ? hd_s[r - R0 + mt.hd_off] : ld_ro(p.head + r);
-        double a0 = 0.0;
-        d16_row_cols<VS>(d_s, ls, le, lane, base, [&](int t, int c) { a0 = fma(vals_s[t], ld_x(p.x + c), a0); });
-        acc = a0;
-      }
-      acc = group_sum<VS>(acc);
-      if (active && lane == 0) {
-        if (incoming && q == 0) {
-          p.carry_row[k] = (int32_t)r;
-          p.carry_val[k] = acc;
+        double acc;
+        if constexpr (!D16) {
+          // batches of 8 predicated elements per lane: 8 independent gathers in flight
+          const int32_t* idx_s = reinterpret_cast<const int32_t*>(st + L.idx);
+          double a0 = 0.0, a1 = 0.0;
+          for (int l0 = ls + lane; l0 < le; l0 += 8 * VS) {
+            int c[8];
+            double v[8], xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int l = l0 + u * VS;
+              c[u] = l < le ? idx_s[l] : -1;
+              v[u] = l < le ? vals_s[l] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_x(p.x + c[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+              a0 = fma(v[u], xv[u], a0);
+              a1 = fma(v[u + 1], xv[u + 1], a1);
+            }
+          }
+          acc = a0 + a1;
         } else {
-          p.y[r] = acc;
+          const uint16_t* d_s = reinterpret_cast<const uint16_t*>(st + L.idx);
+          const int32_t* hd_s = reinterpret_cast<const int32_t*>(st + L.hd);
+          int base = mt.anchor;
+          if (active && (!incoming || q > 0))
+            base = mt.hd_off >= 0 ? hd_s[r - R0 + mt.hd_off] : ld_ro(p.head + r);
+          double a0 = 0.0;
+          d16_row_cols<VS>(d_s, ls, le, lane, base,
+                           [&](int t, int c) { a0 = fma(vals_s[t], ld_x(p.x + c), a0); });
+          acc = a0;
+        }
+        acc = group_sum<VS>(acc);
+        if (active && lane == 0) {
+          if (incoming && q == 0) {
+            p.carry_row[k] = (int32_t)out_row(p, r);
+            p.carry_val[k] = acc;
+          } else {
+            p.y[out_row(p, r)] = acc;
+          }
         }
       }
+      if (!incoming && lane32 == 0) p.carry_row[k] = -1;
     }
-    if (!incoming && lane32 == 0) p.carry_row[k] = -1;
     __syncwarp();
     if (lane32 == 0) mbar_arrive(&empty[s]);
   }
 }
 
-template <int VS, typename RP, bool D16, bool SEG = false>
-static int stream_prepare_t(const ExecArgs& a) {
-  const size_t smem = stream_smem_bytes(a.C, a.stages, sizeof(RP), D16, SEG);
+template <typename RP>
+static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y) {
+  StreamP<RP> p;
+  p.rp = (const RP*)sp.V.rowptr;
+  p.idx = sp.dcol ? (const void*)sp.dcol : (const void*)sp.V.col;
+  p.head = sp.head;
+  p.anchor = sp.anchor;
+  p.val = sp.V.val;
+  p.x = x;
+  p.y = y;
+  p.rowmap = sp.rowmap;
+  p.tile_row = sp.tile_row;
+  p.carry_row = sp.carry_row;
+  p.carry_val = sp.carry_val;
+  p.nnz = sp.V.nnz;
+  p.C = sp.C;
+  p.T = sp.T;
+  p.stages = sp.stages;
+  p.rows_cap = sp.rows_cap;
+  return p;
+}
+
+template <int VS, typename RP, bool D16, bool SEG>
+static int stream_prepare_t(const StreamPlan& sp, int sm_count) {
+  const size_t smem = stream_smem_bytes(sp.C, sp.stages, sizeof(RP), sp.rows_cap, D16, SEG);
   if (cudaFuncSetAttribute(stream_kernel<VS, RP, D16, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return -1;
@@ -388,84 +403,65 @@ static int stream_prepare_t(const ExecArgs& a) {
                                                     smem) != cudaSuccess ||
       per_sm < 1)
     return -1;
-  int64_t grid = (int64_t)a.sm_count * per_sm;
-  if (grid > a.T) grid = a.T;
+  int64_t grid = (int64_t)sm_count * per_sm;
+  if (grid > sp.T) grid = sp.T;
   return (int)grid;
 }
 
-template <int VS, typename RP, bool D16, bool SEG = false>
-static void stream_launch_t(const ExecArgs& a, cudaStream_t s) {
-  StreamP<RP> p;
-  p.rp = (const RP*)a.A.rowptr;
-  p.idx = D16 ? (const void*)a.dcol : (const void*)a.A.col;
-  p.head = a.head;
-  p.anchor = a.anchor;
-  p.val = a.A.val;
-  p.x = a.x;
-  p.y = a.y;
-  p.tile_row = a.tile_row;
-  p.carry_row = a.carry_row;
-  p.carry_val = a.carry_val;
-  p.nnz = a.A.nnz;
-  p.C = a.C;
-  p.T = a.T;
-  p.stages = a.stages;
-  const size_t smem = stream_smem_bytes(a.C, a.stages, sizeof(RP), D16, SEG);
-  stream_kernel<VS, RP, D16, SEG><<<a.stream_grid, kStreamThreads, smem, s>>>(p);
+template <int VS, typename RP, bool D16, bool SEG>
+static void stream_launch_t(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
+  const size_t smem = stream_smem_bytes(sp.C, sp.stages, sizeof(RP), sp.rows_cap, D16, SEG);
+  stream_kernel<VS, RP, D16, SEG><<<sp.grid, kStreamThreads, smem, s>>>(make_params<RP>(sp, x, y));
+}
+
+template <int VS, typename RP, bool D16, bool SEG, bool PREP>
+static int stream_one(const StreamPlan& sp, int sm_count, const double* x, double* y, cudaStream_t s) {
+  if (PREP) return stream_prepare_t<VS, RP, D16, SEG>(sp, sm_count);
+  stream_launch_t<VS, RP, D16, SEG>(sp, x, y, s);
+  return 0;
 }
 
 template <typename RP, bool D16, bool PREP>
-static int stream_vs(const ExecArgs& a, cudaStream_t s) {
-#define SPMV_VS_CASE(V)                               \
-  case V:                                             \
-    if (PREP) return stream_prepare_t<V, RP, D16>(a); \
-    stream_launch_t<V, RP, D16>(a, s);                \
-    return 0;
-  switch (a.vs) {
-    SPMV_VS_CASE(1)
-    SPMV_VS_CASE(2)
-    SPMV_VS_CASE(4)
-    SPMV_VS_CASE(8)
-    SPMV_VS_CASE(16)
-    default:
-      if (PREP) return stream_prepare_t<32, RP, D16>(a);
-      stream_launch_t<32, RP, D16>(a, s);
-      return 0;
+static int stream_vs(const StreamPlan& sp, int smc, const double* x, double* y, cudaStream_t s) {
+  switch (sp.vs) {
+    case 1: return stream_one<1, RP, D16, false, PREP>(sp, smc, x, y, s);
+    case 2: return stream_one<2, RP, D16, false, PREP>(sp, smc, x, y, s);
+    case 4: return stream_one<4, RP, D16, false, PREP>(sp, smc, x, y, s);
+    case 8: return stream_one<8, RP, D16, false, PREP>(sp, smc, x, y, s);
+    case 16: return stream_one<16, RP, D16, false, PREP>(sp, smc, x, y, s);
+    default: return stream_one<32, RP, D16, false, PREP>(sp, smc, x, y, s);
   }
-#undef SPMV_VS_CASE
 }
 
 template <bool PREP>
-static int stream_dispatch(const ExecArgs& a, cudaStream_t s) {
-  const bool d16 = a.dcol != nullptr;
-  if (a.seg && !d16) {  // segmented mode: one instantiation per rowptr width
-    if (a.A.rp_bytes == 8) {
-      if (PREP) return stream_prepare_t<1, int64_t, false, true>(a);
-      stream_launch_t<1, int64_t, false, true>(a, s);
-    } else {
-      if (PREP) return stream_prepare_t<1, int32_t, false, true>(a);
-      stream_launch_t<1, int32_t, false, true>(a, s);
-    }
-    return 0;
-  }
-  if (a.A.rp_bytes == 8) return d16 ? stream_vs<int64_t, true, PREP>(a, s) : stream_vs<int64_t, false, PREP>(a, s);
-  return d16 ? stream_vs<int32_t, true, PREP>(a, s) : stream_vs<int32_t, false, PREP>(a, s);
+static int stream_dispatch(const StreamPlan& sp, int smc, const double* x, double* y, cudaStream_t s) {
+  const bool d16 = sp.dcol != nullptr;
+  const bool rp8 = sp.V.rp_bytes == 8;
+  if (sp.seg && !d16)
+    return rp8 ? stream_one<1, int64_t, false, true, PREP>(sp, smc, x, y, s)
+               : stream_one<1, int32_t, false, true, PREP>(sp, smc, x, y, s);
+  if (rp8) return d16 ? stream_vs<int64_t, true, PREP>(sp, smc, x, y, s) : stream_vs<int64_t, false, PREP>(sp, smc, x, y, s);
+  return d16 ? stream_vs<int32_t, true, PREP>(sp, smc, x, y, s) : stream_vs<int32_t, false, PREP>(sp, smc, x, y, s);
 }
 
-int stream_prepare(const ExecArgs& a) { return stream_dispatch<true>(a, nullptr); }
+int stream_prepare(const StreamPlan& sp, int sm_count) {
+  return stream_dispatch<true>(sp, sm_count, nullptr, nullptr, nullptr);
+}
 
-int launch_stream(const ExecArgs& a, cudaStream_t s) {
+int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int stage, cudaStream_t s) {
   int n = 0;
-  if (a.stage != 2) {
-    stream_dispatch<false>(a, s);
+  if (stage != 2) {
+    stream_dispatch<false>(sp, 0, x, y, s);
     ++n;
   }
-  if (a.need_fixup && a.stage != 1) {
-    launch_fixup(a.carry_row, a.carry_val, a.T, a.y, 0, s);
+  if (sp.need_fixup && stage != 1) {
+    launch_fixup(sp.carry_row, sp.carry_val, sp.T, y, 0, s);
     ++n;
   }
   return n;
 }
+
+int launch_stream(const ExecArgs& a, cudaStream_t s) { return launch_stream_plan(a.sp[0], a.x, a.y, a.stage, s); }
 
 // Export: re-decode the delta colind on the device with the STREAM kernel's
 // own per-row decoder (bit-exact round trip).
@@ -503,30 +499,28 @@ __global__ void __launch_bounds__(kNT) d16_decode_kernel(const RP* __restrict__ 
 }
 
 template <int VS>
-static void d16_export_vs(const MatView& A, const uint16_t* dcol, const int32_t* head, const int32_t* anchor,
-                          const int32_t* tile_row, int64_t C, int64_t T, int32_t* out, cudaStream_t s) {
-  const size_t smem = (size_t)C * 2 + 16;
-  if (A.rp_bytes == 8) {
+static void d16_export_vs(const StreamPlan& sp, int32_t* out, cudaStream_t s) {
+  const size_t smem = (size_t)sp.C * 2 + 16;
+  if (sp.V.rp_bytes == 8) {
     cudaFuncSetAttribute(d16_decode_kernel<VS, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    d16_decode_kernel<VS, int64_t><<<(int)T, kNT, smem, s>>>((const int64_t*)A.rowptr, dcol, head, anchor, tile_row,
-                                                             A.nnz, C, out);
+    d16_decode_kernel<VS, int64_t><<<(int)sp.T, kNT, smem, s>>>((const int64_t*)sp.V.rowptr, sp.dcol, sp.head,
+                                                                sp.anchor, sp.tile_row, sp.V.nnz, sp.C, out);
   } else {
     cudaFuncSetAttribute(d16_decode_kernel<VS, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    d16_decode_kernel<VS, int32_t><<<(int)T, kNT, smem, s>>>((const int32_t*)A.rowptr, dcol, head, anchor, tile_row,
-                                                             A.nnz, C, out);
+    d16_decode_kernel<VS, int32_t><<<(int)sp.T, kNT, smem, s>>>((const int32_t*)sp.V.rowptr, sp.dcol, sp.head,
+                                                                sp.anchor, sp.tile_row, sp.V.nnz, sp.C, out);
   }
 }
 
-void launch_d16_decode_export(const MatView& A, const uint16_t* dcol, const int32_t* head, const int32_t* anchor,
-                              const int32_t* tile_row, int64_t C, int64_t T, int vs, int32_t* out, cudaStream_t s) {
-  if (A.nnz == 0) return;
-  switch (vs) {
-    case 1: d16_export_vs<1>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
-    case 2: d16_export_vs<2>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
-    case 4: d16_export_vs<4>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
-    case 8: d16_export_vs<8>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
-    case 16: d16_export_vs<16>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
-    default: d16_export_vs<32>(A, dcol, head, anchor, tile_row, C, T, out, s); break;
+void launch_d16_decode_export(const StreamPlan& sp, int32_t* out, cudaStream_t s) {
+  if (sp.V.nnz == 0) return;
+  switch (sp.vs) {
+    case 1: d16_export_vs<1>(sp, out, s); break;
+    case 2: d16_export_vs<2>(sp, out, s); break;
+    case 4: d16_export_vs<4>(sp, out, s); break;
+    case 8: d16_export_vs<8>(sp, out, s); break;
+    case 16: d16_export_vs<16>(sp, out, s); break;
+    default: d16_export_vs<32>(sp, out, s); break;
   }
 }
 

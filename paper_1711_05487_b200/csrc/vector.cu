@@ -182,19 +182,13 @@ __global__ void __launch_bounds__(kNT) long_chunk_kernel(const RP* __restrict__ 
 }
 
 int launch_split(const ExecArgs& a, cudaStream_t s) {
-  // 1. short rows: cta_stream over the compacted short-row CSR (writes every
-  //    row of y; emptied medium/long rows get 0), one lane per row
-  ExecArgs b = a;
-  b.A = a.S;
-  b.vs = 1;
-  b.dcol = nullptr;
-  int n = launch_stream(b, s);
-  // 2. medium rows: one warp per listed row (overwrites their y)
-  if (a.stage != 2 && a.n_mid > 0) {
-    launch_rowlist(a, a.mid_rows, a.n_mid, s);
-    ++n;
-  }
-  // 3. long rows: chunk partials, then the ordered per-row reduction (sets y)
+  int n = 0;
+  // 0. rows in no bin (empty rows) must read 0: clear y once
+  if (a.zero_y && a.stage != 2 && a.A.m > 0) cudaMemsetAsync(a.y, 0, (size_t)a.A.m * 8, s);
+  // 1. short / medium bins: cta_stream over each compacted bin (rows mapped
+  //    back to y through the bin's row map); the bins own disjoint rows
+  for (int b = 0; b < a.n_sp; ++b) n += launch_stream_plan(a.sp[b], a.x, a.y, a.stage, s);
+  // 2. long rows: chunk partials, then the ordered per-row reduction (sets y)
   if (a.n_chunks > 0) {
     if (a.stage != 2) {
       ++n;
