@@ -8,7 +8,7 @@ NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall 
              --expt-relaxed-constexpr -Iinclude -Ipaper_1711_05487_b200/csrc
 PKG       := paper_1711_05487_b200
 CU_SRCS   := $(wildcard $(PKG)/csrc/*.cu)
-CU_HDRS   := $(wildcard $(PKG)/csrc/*.cuh) include/spmv.h
+CU_HDRS   := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/spmv.h
 
 all: synthgen oracle spmv
 
