@@ -548,6 +548,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     // one stage per consumer warp: measured on B200 (tools/sweep.py, C2/C5),
     // more resident warps beat a deeper ring (the x gathers are latency-bound)
     sp.stages = opt.stages > 0 ? opt.stages : kStreamConsumerWarps;
+    // shrink the staged-rowptr capacity until the ring fits (sparser tiles
+    // then read rowptr from global memory)
+    while (sp.rows_cap > 64 && stream_smem_bytes(sp.C, sp.stages, V.rp_bytes, sp.rows_cap, d16, seg) > 227 * 1024)
+      sp.rows_cap /= 2;
     sp.grid = stream_prepare(sp, s.sm_count);
     if (sp.grid < 0 && sp.stages > kStreamConsumerWarps) {
       cudaGetLastError();
