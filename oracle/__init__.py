@@ -310,9 +310,9 @@ def _pow2ceil(v):
 def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty_frac=0.25):
     """Feature-guided selection. f = features(..) dict.
 
-    IMB (P:608-627): skew (sd_s/avg_s > skew_sd or empty/N > empty_frac) ->
-    merge_path; else long rows (n_long > 0 and nnz_max > K_long*nnz_avg) ->
-    long_row_split. Regular rows -> cta_stream for avg_s <= 32, else
+    IMB: long rows (n_long > 0 and nnz_max > K_long*nnz_avg) ->
+    long_row_split; else skew (sd_s/avg_s > skew_sd or empty/N > empty_frac)
+    -> merge_path. Regular rows -> cta_stream for avg_s <= 32, else
     csr_vector (CMP analogue: lane group sized to the row, VS =
     clamp(pow2ceil(avg_s), 2, 32)). MB: working set > L2/2 and
     maxgap <= 65535 -> D16 colind (only with cta_stream). ML:
@@ -329,10 +329,10 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     if skew or longr:
         classes |= CLASS_IMB
     vs = min(32, max(2, _pow2ceil(int(math.ceil(avg_s))) if avg_s > 0 else 2))
-    if skew:
-        variant = VARIANT_MERGE
-    elif longr:
+    if longr:  # long rows first: the length-bin decomposition also absorbs skew
         variant = VARIANT_SPLIT
+    elif skew:
+        variant = VARIANT_MERGE
     elif avg_s <= 32:
         variant = VARIANT_STREAM
     else:

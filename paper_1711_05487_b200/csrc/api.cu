@@ -227,7 +227,9 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   if (skew || longr) classes |= SPMV_CLASS_IMB;
   int vs = avg_s > 0 ? pow2ceil((int64_t)std::ceil(avg_s)) : 2;
   vs = std::min(32, std::max(2, vs));
-  int variant = skew ? SPMV_VARIANT_MERGE : longr ? SPMV_VARIANT_SPLIT : avg_s <= 32 ? SPMV_VARIANT_STREAM
+  // long rows first: the length-bin decomposition also absorbs skew (B200
+  // sweep on C3: split 0.37 ms vs merge_path 0.99 ms)
+  int variant = longr ? SPMV_VARIANT_SPLIT : skew ? SPMV_VARIANT_MERGE : avg_s <= 32 ? SPMV_VARIANT_STREAM
                                                                                      : SPMV_VARIANT_VECTOR;
   if (o.force_variant > 0) variant = o.force_variant;
   if (variant == SPMV_VARIANT_STREAM) {
@@ -510,11 +512,11 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     sp.vs = vs;
     sp.seg = seg;
     const double avg = V.m ? (double)V.nnz / (double)V.m : 0.0;
-    // tile size: one pass of the consumer warp over ~32 rows (row-step mode,
-    // B200 sweeps: 768 for 27-nnz rows, 384 for 15-nnz rows); 512 for rows of
-    // <= 12 nonzeros and for the segmented mode; VS > 1 groups: 32/VS rows
+    // tile size: one pass of the consumer warp over its 32/VS rows (row-step
+    // mode; B200 sweeps: 768 for 27-nnz rows, 384 for 15-nnz and shorter
+    // rows), clamp [384, 4096]; 512 in the segmented mode
     int64_t C = 512;
-    if (!seg && avg > 12) {
+    if (!seg) {
       const double rows_per_pass = 32.0 / vs;
       C = (int64_t)(rows_per_pass * avg / 128.0) * 128;
       C = std::min<int64_t>(4096, std::max<int64_t>(384, C));

@@ -349,8 +349,38 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(con
           if (active && (!incoming || q > 0))
             base = mt.hd_off >= 0 ? hd_s[r - R0 + mt.hd_off] : ld_ro(p.head + r);
           double a0 = 0.0;
-          d16_row_cols<VS>(d_s, ls, le, lane, base,
-                           [&](int t, int c) { a0 = fma(vals_s[t], ld_x(p.x + c), a0); });
+          if constexpr (VS == 1) {
+            // one lane per row: running column sum, batches of 8 gathers
+            double a1 = 0.0;
+            int c = base;
+            for (int l0 = ls; l0 < le; l0 += 8) {
+              int cc[8];
+              double v[8], xv[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int l = l0 + u;
+                if (l < le) {
+                  c += (l == ls) ? 0 : (int)d_s[l];
+                  cc[u] = c;
+                  v[u] = vals_s[l];
+                } else {
+                  cc[u] = -1;
+                  v[u] = 0.0;
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) xv[u] = cc[u] >= 0 ? ld_x(p.x + cc[u]) : 0.0;
+#pragma unroll
+              for (int u = 0; u < 8; u += 2) {
+                a0 = fma(v[u], xv[u], a0);
+                a1 = fma(v[u + 1], xv[u + 1], a1);
+              }
+            }
+            a0 += a1;
+          } else {
+            d16_row_cols<VS>(d_s, ls, le, lane, base,
+                             [&](int t, int c) { a0 = fma(vals_s[t], ld_x(p.x + c), a0); });
+          }
           acc = a0;
         }
         acc = group_sum<VS>(acc);

@@ -236,10 +236,14 @@ def test_select_rule_table_on_closed_form_features():
     # C1: 1.28 MB working set -> no MB, no D16
     s = S.select(feat(10000, 90000, 9.0, 0.0, maxgap=9000, misses=80000), L2, WIN, 4)
     assert (s.variant, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_STREAM, False, 0)
-    # C3-like: half the rows empty -> merge path, IMB
+    # C3-like: half the rows empty and long rows -> long_row_split (long rows first), IMB
     s = S.select(feat(4194304, 65244537, 12.8, 78.5, n_empty=2185429, n_long=1794, nnz_max=97958,
                       maxgap=4165791, misses=56437921), L2, WIN, 4)
-    assert s.variant == S.VARIANT_MERGE and s.classes & S.CLASS_IMB and s.xwin and s.classes & S.CLASS_ML
+    assert s.variant == S.VARIANT_SPLIT and s.classes & S.CLASS_IMB and s.xwin and s.classes & S.CLASS_ML
+    # skew without long rows -> merge path
+    s = S.select(feat(4194304, 20000000, 4.8, 9.0, n_empty=2185429, n_long=0, nnz_max=3000,
+                      maxgap=4165791, misses=19000000), L2, WIN, 4)
+    assert s.variant == S.VARIANT_MERGE and s.classes & S.CLASS_IMB
     # C4-like: long rows, regular short part -> split
     s = S.select(feat(1000000, 34998500, 15.0, 0.0, n_long=100, nnz_max=200000, maxgap=900000,
                       misses=34000000), L2, WIN, 4)
