@@ -73,7 +73,7 @@ typedef struct spmv_options {
   int32_t emulate_devices; /* ngpus > 1: 1 = place every shard on the current device (tests) */
   int32_t stages;          /* STREAM smem ring depth: 0 = auto (one stage per consumer warp), else a multiple of 4 <= 32 */
   int32_t seg;             /* STREAM / SPLIT short part, segmented consumer mode: -1 auto, 0 off, 1 on */
-  int32_t reserved[5];
+  int32_t reserved[5];      /* reserved[0] = 1 disables row-aligned tiles (tests) */
 } spmv_options;
 
 /* Theta(N) features (Table I) + counts used by the selection.
@@ -118,6 +118,9 @@ typedef struct spmv_plan_info {
   double upload_ms, inspect_ms, select_ms, encode_ms; /* plan-time breakdown */
   int64_t device_bytes;       /* device memory held by the plan (all shards) */
   int64_t shard_bounds[9];    /* b_0..b_G for G <= 8 (rows) */
+  int64_t tile_stride;        /* STREAM tile stride in nonzeros (= tile_nnz, or tile_nnz - longest row) */
+  int32_t tiles_row_aligned;  /* 1: tile k = rows starting in [k*stride, (k+1)*stride); no carries */
+  int32_t pad2_;
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */

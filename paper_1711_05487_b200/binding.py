@@ -39,6 +39,9 @@ class Options(ctypes.Structure):
         o = cls()
         lib.spmv_options_default(ctypes.byref(o))
         for k, v in kw.items():
+            if k == "no_aligned":  # reserved[0]: disable row-aligned STREAM tiles
+                o.reserved[0] = int(v)
+                continue
             if k == "force_variant" and isinstance(v, str):
                 v = VARIANTS[v]
             setattr(o, k, v)
@@ -72,7 +75,8 @@ class PlanInfo(ctypes.Structure):
                 ("n_merge_tiles", ctypes.c_int64), ("l_split", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
                 ("n_long_chunks", ctypes.c_int64), ("upload_ms", ctypes.c_double), ("inspect_ms", ctypes.c_double),
                 ("select_ms", ctypes.c_double), ("encode_ms", ctypes.c_double), ("device_bytes", ctypes.c_int64),
-                ("shard_bounds", ctypes.c_int64 * 9)]
+                ("shard_bounds", ctypes.c_int64 * 9), ("tile_stride", ctypes.c_int64),
+                ("tiles_row_aligned", ctypes.c_int32), ("pad2_", ctypes.c_int32)]
 
 
 _vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
@@ -238,7 +242,7 @@ class Plan:
     def info(self) -> dict:
         i = PlanInfo()
         _check(lib.spmv_plan_query(self._h, ctypes.byref(i)))
-        d = {k: getattr(i, k) for k, _ in PlanInfo._fields_ if k not in ("sel", "feat", "pad_", "shard_bounds")}
+        d = {k: getattr(i, k) for k, _ in PlanInfo._fields_ if k not in ("sel", "feat", "pad_", "pad2_", "shard_bounds")}
         d["sel"] = {k: getattr(i.sel, k) for k, _ in Selection._fields_ if k != "pad_"}
         d["variant"] = VARIANT_NAMES[i.sel.variant]
         d["classes"] = [k for k, v in CLASSES.items() if i.sel.classes & v]

@@ -506,7 +506,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   // cta_stream structures over the CSR view V (the whole shard, or one
   // compacted length bin of long_row_split mapped back through rowmap)
   auto build_stream = [&](Shard& s, StreamPlan& sp, const MatView& V, const int32_t* rowmap, bool d16, int vs,
-                          bool seg) {
+                          bool seg, int64_t maxlen) {
     sp.V = V;
     sp.rowmap = rowmap;
     sp.vs = vs;
@@ -523,7 +523,12 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     }
     sp.C = opt.tile_nnz > 0 ? opt.tile_nnz : C;
     P->C = sp.C;
-    sp.T = std::max<int64_t>(1, (V.nnz + sp.C - 1) / sp.C);
+    // row-aligned tiles when the longest row fits twice in a tile: tile k =
+    // rows starting in [k*stride, (k+1)*stride), stride = C - maxlen, so no
+    // row crosses a tile (no carries, no fix-up kernel)
+    sp.aligned = !seg && maxlen >= 0 && 2 * maxlen <= sp.C && opt.reserved[0] == 0;
+    sp.stride = sp.aligned ? sp.C - maxlen : sp.C;
+    sp.T = std::max<int64_t>(1, (V.nnz + sp.stride - 1) / sp.stride);
     // staged rowptr entries: 1.5x the expected rows per tile (+32)
     const double rpt = avg > 0 ? (double)sp.C / avg : (double)sp.C;
     sp.rows_cap = (int)std::min<double>((double)sp.C + 32, 1.5 * rpt + 32);
@@ -532,13 +537,13 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     sp.carry_val = s.alloc<double>((size_t)sp.T);
     DevStats zero{};
     ck(cudaMemcpyAsync(&s.stats->n_incoming, &zero.n_incoming, 8, cudaMemcpyHostToDevice, s.stream), "stats");
-    launch_tile_rows(V, sp.C, sp.T, sp.tile_row, s.stats, s.stream);
+    launch_tile_rows(V, sp.stride, sp.T, sp.tile_row, s.stats, s.stream);
     count_launches(1, "tile_rows");
     if (d16) {
       uint16_t* dcol = s.alloc<uint16_t>((size_t)V.nnz);
       int32_t* head = s.alloc<int32_t>((size_t)V.m);
       int32_t* anchor = s.alloc<int32_t>((size_t)sp.T);
-      launch_d16_encode(V, s.headbits, sp.C, sp.T, dcol, head, anchor, s.stream);
+      launch_d16_encode(V, s.headbits, sp.stride, sp.T, dcol, head, anchor, s.stream);
       count_launches(3, "d16_encode");
       sp.dcol = dcol;
       sp.head = head;
@@ -546,7 +551,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     }
     ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
     ck(cudaStreamSynchronize(s.stream), "tiles");
-    sp.need_fixup = s.hs.n_incoming > 0;
+    sp.need_fixup = !sp.aligned && s.hs.n_incoming > 0;
     // one stage per consumer warp: measured on B200 (tools/sweep.py, C2/C5),
     // more resident warps beat a deeper ring (the x gathers are latency-bound)
     sp.stages = opt.stages > 0 ? opt.stages : kStreamConsumerWarps;
@@ -589,14 +594,15 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     void* brp = s.alloc<char>((size_t)(nrows + 1) * rp_bytes);
     launch_gather_rowptr(frp, rp_bytes, rows, nrows, s.m, brp, s.stream);
     count_launches(1, "bin gather");
-    build_stream(s, sp, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, rows, false, vs, seg);
+    build_stream(s, sp, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, rows, false, vs, seg,
+                 std::min<int64_t>(hi, P->feat.nnz_max));
     return true;
   };
   for (auto& s : P->shards) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const MatView A = s.view();
     if (P->sel.variant == SPMV_VARIANT_STREAM) {
-      build_stream(s, s.sp[0], A, nullptr, P->sel.d16, P->sel.vs, P->sel.seg != 0);
+      build_stream(s, s.sp[0], A, nullptr, P->sel.d16, P->sel.vs, P->sel.seg != 0, P->feat.nnz_max);
       s.n_sp = 1;
     } else if (P->sel.variant == SPMV_VARIANT_MERGE) {
       s.items = P->items;
@@ -859,6 +865,8 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     const Shard& s0 = p->shards[0];
     info->tile_nnz = s0.sp[0].C;
     info->n_tiles = s0.sp[0].T;
+    info->tile_stride = s0.sp[0].stride;
+    info->tiles_row_aligned = s0.sp[0].aligned ? 1 : 0;
     info->merge_items = s0.items;
     info->n_merge_tiles = s0.Tm;
     info->l_split = p->l_split;

@@ -43,6 +43,8 @@ struct StreamPlan {
   const int32_t* anchor = nullptr;
   int stages = 0, grid = 0, vs = 1, rows_cap = 0;
   bool seg = false;  // segmented consumer mode (random-gather tiles)
+  bool aligned = false;  // row-aligned tiles: tile k = rows starting in [k*stride, (k+1)*stride)
+  int64_t stride = 0;    // tile stride in nonzeros (C, or C - longest row when aligned)
 };
 
 // ---- inspector ------------------------------------------------------------

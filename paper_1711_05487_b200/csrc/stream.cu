@@ -31,11 +31,13 @@ constexpr int kConsumerWarps = kStreamConsumerWarps;
 constexpr int kStreamThreads = 32 * (kConsumerWarps + 1);
 
 struct TileMeta {
+  int64_t t0;       // first nonzero of the tile
+  int32_t cnt;      // nonzeros in the tile
+  int32_t voff, ioff;  // position of nonzero t0 in the staged values / index arrays
   int32_t R0, R1;   // owned rows [R0, R1)
   int32_t rp_off;   // element offset of row max(R0-1,0) in the staged rowptr slice; -1 = read global
   int32_t hd_off;   // element offset of row R0 in the staged head slice; -1 = read global
-  int32_t anchor;   // D16: absolute column of nonzero k*C
-  int32_t pad_[3];
+  int32_t anchor;   // D16: absolute column of nonzero k*C (nnz-aligned tiles)
 };
 
 __host__ __device__ __forceinline__ size_t al128(size_t v) { return (v + 127) & ~(size_t)127; }
@@ -53,8 +55,8 @@ __host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int
   L.rp_cap = (uint32_t)(((size_t)(rows_cap + 2) * rp_bytes + 32 + 15) & ~(size_t)15);
   L.hd_cap = d16 ? (uint32_t)(((size_t)(rows_cap + 2) * 4 + 32 + 15) & ~(size_t)15) : 0u;
   L.vals = 0;
-  L.idx = al128((size_t)C * 8);
-  L.rp = al128(L.idx + (size_t)C * (d16 ? 2 : 4));
+  L.idx = al128((size_t)(C + 2) * 8);  // + rounding slack of row-aligned tiles
+  L.rp = al128(L.idx + (size_t)(C + 8) * (d16 ? 2 : 4));
   L.hd = al128(L.rp + L.rp_cap);
   L.stage = al128(L.hd + L.hd_cap);
   size_t o = L.stage * stages;
@@ -90,6 +92,7 @@ struct StreamP {
   double* carry_val;
   int64_t nnz, C, T;
   int stages, rows_cap;
+  int aligned;  // 1: row-aligned tiles (no row crosses a tile, no carries)
 };
 
 template <typename RP>
@@ -211,7 +214,7 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
 }
 
 template <int VS, typename RP, bool D16, bool SEG>
-__global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(const StreamP<RP> p) {
+__global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : (D16 ? 6 : 8)) stream_kernel(const StreamP<RP> p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), p.rows_cap, D16, SEG);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
@@ -239,16 +242,31 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(con
         const int s = i % S;
         if (i >= S) mbar_wait(&empty[s], (uint32_t)(((i / S) - 1) & 1));
         const int64_t R0 = ld_ro(p.tile_row + k), R1 = ld_ro(p.tile_row + k + 1);
-        const int64_t t0 = k * p.C;
-        const int64_t cnt = (p.nnz - t0) < p.C ? (p.nnz - t0) : p.C;
-        const uint32_t vb = (uint32_t)((cnt * 8 + 15) & ~15ll);
-        const uint32_t ib = (uint32_t)((cnt * IB + 15) & ~15ll);
+        // nnz-aligned tile [k*C, ...) or row-aligned tile [rowptr[R0], rowptr[R1])
+        // (copies rounded out to 16 B; voff/ioff = offsets of t0 in the stage)
+        int64_t t0, cnt, v0, i0;
+        if (p.aligned) {
+          t0 = (int64_t)ld_ro(p.rp + R0);
+          cnt = (int64_t)ld_ro(p.rp + R1) - t0;
+          v0 = t0 & ~1ll;
+          i0 = t0 & ~(int64_t)(16 / IB - 1);
+        } else {
+          t0 = k * p.C;
+          cnt = (p.nnz - t0) < p.C ? (p.nnz - t0) : p.C;
+          v0 = i0 = t0;
+        }
+        const uint32_t vb = cnt > 0 ? (uint32_t)(((t0 + cnt - v0) * 8 + 15) & ~15ll) : 0u;
+        const uint32_t ib = cnt > 0 ? (uint32_t)(((t0 + cnt - i0) * IB + 15) & ~15ll) : 0u;
         const int64_t fr0 = R0 > 0 ? R0 - 1 : 0;
         const int64_t b0 = (fr0 * RPB) & ~15ll, b1 = ((R1 + 1) * RPB + 15) & ~15ll;
         const bool rp_ok = (b1 - b0) <= (int64_t)L.rp_cap;
         uint32_t hb = 0;
         int64_t h0 = 0;
         TileMeta mt;
+        mt.t0 = t0;
+        mt.cnt = (int32_t)cnt;
+        mt.voff = (int32_t)(t0 - v0);
+        mt.ioff = (int32_t)(t0 - i0);
         mt.R0 = (int32_t)R0;
         mt.R1 = (int32_t)R1;
         mt.rp_off = rp_ok ? (int32_t)((fr0 * RPB - b0) / RPB) : -1;
@@ -265,9 +283,9 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(con
         meta[s] = mt;
         unsigned char* st = smem + L.stage * s;
         mbar_arrive_expect_tx(&full[s], vb + ib + (rp_ok ? (uint32_t)(b1 - b0) : 0u) + hb);
-        if (vb) {
-          bulk_g2s(st + L.vals, p.val + t0, vb, &full[s], pol);
-          bulk_g2s(st + L.idx, static_cast<const unsigned char*>(p.idx) + t0 * IB, ib, &full[s], pol);
+        if (cnt > 0) {
+          bulk_g2s(st + L.vals, p.val + v0, vb, &full[s], pol);
+          bulk_g2s(st + L.idx, static_cast<const unsigned char*>(p.idx) + i0 * IB, ib, &full[s], pol);
         }
         if (rp_ok) bulk_g2s(st + L.rp, reinterpret_cast<const unsigned char*>(p.rp) + b0, (uint32_t)(b1 - b0),
                             &full[s], pol);
@@ -290,11 +308,12 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(con
     mbar_wait(&full[s], (uint32_t)((i / S) & 1));
     const TileMeta mt = meta[s];
     unsigned char* st = smem + L.stage * s;
-    const double* vals_s = reinterpret_cast<const double*>(st + L.vals);
+    const double* vals_s = reinterpret_cast<const double*>(st + L.vals) + mt.voff;
+    const unsigned char* idx_b = st + L.idx + (size_t)mt.ioff * IB;
     const RP* rp_s = reinterpret_cast<const RP*>(st + L.rp);
-    const int64_t t0 = k * p.C;
-    const int64_t t1 = (t0 + p.C) < p.nnz ? (t0 + p.C) : p.nnz;
-    const int cnt = (int)(t1 - t0);
+    const int64_t t0 = mt.t0;
+    const int cnt = mt.cnt;
+    const int64_t t1 = t0 + cnt;
     const int64_t R0 = mt.R0, R1 = mt.R1;
     const int64_t fr0 = R0 > 0 ? R0 - 1 : 0;
     auto rows = [&](int64_t r) -> int64_t {
@@ -305,7 +324,7 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(con
     const int nloc = (int)(R1 - R0) + (incoming ? 1 : 0);
 
     if constexpr (SEG) {
-      seg_tile(p, vals_s, reinterpret_cast<const int32_t*>(st + L.idx),
+      seg_tile(p, vals_s, reinterpret_cast<const int32_t*>(idx_b),
                reinterpret_cast<double*>(smem + L.prod) + (size_t)w * p.C, rows, fr, nloc, t0, cnt, k, lane32);
     } else {
       for (int qb = 0; qb < nloc; qb += GPW) {
@@ -322,7 +341,7 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(con
         double acc;
         if constexpr (!D16) {
           // batches of 8 predicated elements per lane: 8 independent gathers in flight
-          const int32_t* idx_s = reinterpret_cast<const int32_t*>(st + L.idx);
+          const int32_t* idx_s = reinterpret_cast<const int32_t*>(idx_b);
           double a0 = 0.0, a1 = 0.0;
           for (int l0 = ls + lane; l0 < le; l0 += 8 * VS) {
             int c[8];
@@ -343,7 +362,7 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : 8) stream_kernel(con
           }
           acc = a0 + a1;
         } else {
-          const uint16_t* d_s = reinterpret_cast<const uint16_t*>(st + L.idx);
+          const uint16_t* d_s = reinterpret_cast<const uint16_t*>(idx_b);
           const int32_t* hd_s = reinterpret_cast<const int32_t*>(st + L.hd);
           int base = mt.anchor;
           if (active && (!incoming || q > 0))
@@ -419,6 +438,7 @@ static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y)
   p.T = sp.T;
   p.stages = sp.stages;
   p.rows_cap = sp.rows_cap;
+  p.aligned = sp.aligned ? 1 : 0;
   return p;
 }
 
@@ -542,8 +562,10 @@ static void d16_export_vs(const StreamPlan& sp, int32_t* out, cudaStream_t s) {
   }
 }
 
-void launch_d16_decode_export(const StreamPlan& sp, int32_t* out, cudaStream_t s) {
-  if (sp.V.nnz == 0) return;
+void launch_d16_decode_export(const StreamPlan& sp_in, int32_t* out, cudaStream_t s) {
+  if (sp_in.V.nnz == 0) return;
+  StreamPlan sp = sp_in;
+  sp.C = sp.stride;  // the tile_row / anchor arrays are laid out at the stride
   switch (sp.vs) {
     case 1: d16_export_vs<1>(sp, out, s); break;
     case 2: d16_export_vs<2>(sp, out, s); break;

@@ -35,8 +35,13 @@ def assert_bound(y, m, rows=None, tol=TOL):
     return err
 
 
+def m_maxlen(m):
+    return int(np.diff(m.rowptr.astype(np.int64)).max(initial=0))
+
+
 VARIANTS = [("vector", 1), ("vector", 2), ("vector", 8), ("vector", 32), ("stream", 1), ("stream", 4),
-            ("stream", 8), ("stream", 32), ("stream_seg", 1), ("merge", 0), ("split", 4), ("split_rowstep", 32)]
+            ("stream", 8), ("stream", 32), ("stream_seg", 1), ("stream_nnz_tiles", 1), ("merge", 0), ("split", 4),
+    ("split_seg", 32)]
 
 SUITE = sg.small_suite(seed=21)
 
@@ -47,8 +52,10 @@ def variant_kw(variant):
         return "stream", {"seg": 1}
     if variant == "stream_d16":
         return "stream", {"d16": 1}
-    if variant == "split_rowstep":
-        return "split", {"seg": 0}
+    if variant == "split_seg":
+        return "split", {"seg": 1}
+    if variant == "stream_nnz_tiles":
+        return "stream", {"no_aligned": 1}
     return variant, {}
 
 
@@ -93,7 +100,9 @@ def test_stream_d16_and_structures(name, m, tile, vs):
     p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", d16=1, tile_nnz=tile,
                   force_vs=vs)
     info = p.info()
-    assert np.array_equal(p.export("tile_rows"), oracle.tile_rows(m.rowptr, tile))
+    stride = info["tile_stride"]  # tile_nnz, or tile_nnz - longest row for row-aligned tiles
+    assert stride == (tile - m_maxlen(m) if info["tiles_row_aligned"] else tile)
+    assert np.array_equal(p.export("tile_rows"), oracle.tile_rows(m.rowptr, stride))
     if w == 0:
         assert info["sel"]["d16"] == 0
     else:
@@ -101,7 +110,7 @@ def test_stream_d16_and_structures(name, m, tile, vs):
         if m.nnz:
             assert np.array_equal(p.export("dcol"), dcol)
             assert np.array_equal(p.export("head"), head)
-            assert np.array_equal(p.export("anchor"), oracle.tile_anchor(m.colind, tile))
+            assert np.array_equal(p.export("anchor"), oracle.tile_anchor(m.colind, stride))
             assert np.array_equal(p.export("decoded"), m.colind)  # round trip
     assert_bound(p.execute(m.x), m)
 
