@@ -539,6 +539,11 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     ck(cudaMemcpyAsync(&s.stats->n_incoming, &zero.n_incoming, 8, cudaMemcpyHostToDevice, s.stream), "stats");
     launch_tile_rows(V, sp.stride, sp.T, sp.tile_row, s.stats, s.stream);
     count_launches(1, "tile_rows");
+    if (sp.aligned) {
+      sp.tile_nz = s.alloc<int64_t>((size_t)sp.T + 1);
+      launch_tile_nz(V, sp.tile_row, sp.T, sp.tile_nz, s.stream);
+      count_launches(1, "tile_nz");
+    }
     if (d16) {
       uint16_t* dcol = s.alloc<uint16_t>((size_t)V.nnz);
       int32_t* head = s.alloc<int32_t>((size_t)V.m);

@@ -235,6 +235,20 @@ void launch_row_list(const MatView& A, int64_t lo, int64_t hi, int32_t* out, int
   else row_list_t<int32_t>(A, lo, hi, out, scratch, s);
 }
 
+// ---- first nonzero of each row-aligned STREAM tile ---------------------------------
+template <typename RP>
+__global__ void tile_nz_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ tile_row, int64_t T,
+                               int64_t* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k <= T) out[k] = (int64_t)rp[tile_row[k]];
+}
+
+void launch_tile_nz(const MatView& A, const int32_t* tile_row, int64_t T, int64_t* tile_nz, cudaStream_t s) {
+  const int g = (int)((T + 1 + kNT - 1) / kNT);
+  if (A.rp_bytes == 8) tile_nz_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)A.rowptr, tile_row, T, tile_nz);
+  else tile_nz_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, tile_row, T, tile_nz);
+}
+
 // ---- compacted rowptr of a bin ---------------------------------------------------
 template <typename RP>
 __global__ void gather_rowptr_kernel(const RP* __restrict__ frp, const int32_t* __restrict__ rows, int64_t n,

@@ -45,7 +45,9 @@ struct StreamPlan {
   bool seg = false;  // segmented consumer mode (random-gather tiles)
   bool aligned = false;  // row-aligned tiles: tile k = rows starting in [k*stride, (k+1)*stride)
   int64_t stride = 0;    // tile stride in nonzeros (C, or C - longest row when aligned)
+  int64_t* tile_nz = nullptr;  // aligned: tile_nz[k] = rowptr[tile_row[k]], k = 0..T
 };
+void launch_tile_nz(const MatView& A, const int32_t* tile_row, int64_t T, int64_t* tile_nz, cudaStream_t s);
 
 // ---- inspector ------------------------------------------------------------
 void launch_rowstats(const MatView& A, int64_t l_split, uint32_t* headbits, DevStats* st, cudaStream_t s);

@@ -88,6 +88,7 @@ struct StreamP {
   double* y;
   const int32_t* rowmap;
   const int32_t* tile_row;
+  const int64_t* tile_nz;  // row-aligned tiles: first nonzero of tile k (= rowptr[tile_row[k]])
   int32_t* carry_row;
   double* carry_val;
   int64_t nnz, C, T;
@@ -237,17 +238,33 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : (D16 ? 6 : 8)) strea
     // ------------------------------ producer ------------------------------
     if (threadIdx.x == 0) {
       const uint64_t pol = policy_evict_first();
+      // tile metadata is prefetched one tile ahead (independent loads issued
+      // before waiting on the stage), keeping global latency off the serial
+      // producer path
+      int64_t nR0 = 0, nR1 = 0, nT0 = 0, nT1 = 0;
+      auto fetch = [&](int64_t kk) {
+        if (kk < p.T) {
+          nR0 = ld_ro(p.tile_row + kk);
+          nR1 = ld_ro(p.tile_row + kk + 1);
+          if (p.aligned) {
+            nT0 = ld_ro(p.tile_nz + kk);
+            nT1 = ld_ro(p.tile_nz + kk + 1);
+          }
+        }
+      };
+      fetch(blockIdx.x);
       int i = 0;
       for (int64_t k = blockIdx.x; k < p.T; k += gridDim.x, ++i) {
         const int s = i % S;
+        const int64_t R0 = nR0, R1 = nR1, aT0 = nT0, aT1 = nT1;
+        fetch(k + gridDim.x);
         if (i >= S) mbar_wait(&empty[s], (uint32_t)(((i / S) - 1) & 1));
-        const int64_t R0 = ld_ro(p.tile_row + k), R1 = ld_ro(p.tile_row + k + 1);
         // nnz-aligned tile [k*C, ...) or row-aligned tile [rowptr[R0], rowptr[R1])
         // (copies rounded out to 16 B; voff/ioff = offsets of t0 in the stage)
         int64_t t0, cnt, v0, i0;
         if (p.aligned) {
-          t0 = (int64_t)ld_ro(p.rp + R0);
-          cnt = (int64_t)ld_ro(p.rp + R1) - t0;
+          t0 = aT0;
+          cnt = aT1 - aT0;
           v0 = t0 & ~1ll;
           i0 = t0 & ~(int64_t)(16 / IB - 1);
         } else {
@@ -431,6 +448,7 @@ static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y)
   p.y = y;
   p.rowmap = sp.rowmap;
   p.tile_row = sp.tile_row;
+  p.tile_nz = sp.tile_nz;
   p.carry_row = sp.carry_row;
   p.carry_val = sp.carry_val;
   p.nnz = sp.V.nnz;
