@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--vs", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--d16", type=int, default=-1)
+    ap.add_argument("--seg", type=int, default=-1)
+    ap.add_argument("--no-aligned", action="store_true", help="nnz-aligned STREAM tiles (carries + fix-up)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -239,6 +241,10 @@ def run_native(a):
         opts["tile_nnz"] = a.tile
     if a.d16 >= 0:
         opts["d16"] = a.d16
+    if a.seg >= 0:
+        opts["seg"] = a.seg
+    if a.no_aligned:
+        opts["no_aligned"] = 1
     t0 = time.time()
     plan = spmv.Plan(blk["rowptr"], blk["colind"], blk["vals"], n_cols=blk["N"], **opts)
     plan_s = time.time() - t0

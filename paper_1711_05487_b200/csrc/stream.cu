@@ -215,7 +215,7 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
 }
 
 template <int VS, typename RP, bool D16, bool SEG>
-__global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : (D16 ? 6 : 8)) stream_kernel(const StreamP<RP> p) {
+__global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : (D16 ? 7 : 8)) stream_kernel(const StreamP<RP> p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), p.rows_cap, D16, SEG);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
@@ -362,19 +362,20 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : (D16 ? 6 : 8)) strea
           double a0 = 0.0, a1 = 0.0;
           for (int l0 = ls + lane; l0 < le; l0 += 8 * VS) {
             int c[8];
-            double v[8], xv[8];
+            double xv[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const int l = l0 + u * VS;
               c[u] = l < le ? idx_s[l] : -1;
-              v[u] = l < le ? vals_s[l] : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_x(p.x + c[u]) : 0.0;
+            // values read from smem after the gathers are issued (fewer live registers)
 #pragma unroll
             for (int u = 0; u < 8; u += 2) {
-              a0 = fma(v[u], xv[u], a0);
-              a1 = fma(v[u + 1], xv[u + 1], a1);
+              const int l = l0 + u * VS;
+              a0 = fma(l < le ? vals_s[l] : 0.0, xv[u], a0);
+              a1 = fma(l + VS < le ? vals_s[l + VS] : 0.0, xv[u + 1], a1);
             }
           }
           acc = a0 + a1;
@@ -391,25 +392,24 @@ __global__ void __launch_bounds__(kStreamThreads, SEG ? 4 : (D16 ? 6 : 8)) strea
             int c = base;
             for (int l0 = ls; l0 < le; l0 += 8) {
               int cc[8];
-              double v[8], xv[8];
+              double xv[8];
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
                 const int l = l0 + u;
                 if (l < le) {
                   c += (l == ls) ? 0 : (int)d_s[l];
                   cc[u] = c;
-                  v[u] = vals_s[l];
                 } else {
                   cc[u] = -1;
-                  v[u] = 0.0;
                 }
               }
 #pragma unroll
               for (int u = 0; u < 8; ++u) xv[u] = cc[u] >= 0 ? ld_x(p.x + cc[u]) : 0.0;
 #pragma unroll
               for (int u = 0; u < 8; u += 2) {
-                a0 = fma(v[u], xv[u], a0);
-                a1 = fma(v[u + 1], xv[u + 1], a1);
+                const int l = l0 + u;
+                a0 = fma(l < le ? vals_s[l] : 0.0, xv[u], a0);
+                a1 = fma(l + 1 < le ? vals_s[l + 1] : 0.0, xv[u + 1], a1);
               }
             }
             a0 += a1;
