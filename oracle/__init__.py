@@ -314,8 +314,9 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     long_row_split; else skew (sd_s/avg_s > skew_sd or empty/N > empty_frac)
     -> merge_path. Regular rows -> cta_stream for avg_s <= 32, else
     csr_vector (CMP analogue: lane group sized to the row, VS =
-    clamp(pow2ceil(avg_s), 2, 32)). MB: working set > L2/2 and
-    maxgap <= 65535 -> D16 colind (only with cta_stream). ML:
+    clamp(pow2ceil(avg_s), 2, 32)). MB: working set > L2/2 (the
+    D16 colind it maps to is available but not auto-selected: slower on
+    B200, reading 9). ML:
     misses/nnz > 0.75 and x larger than L2/16 -> x persistence window when it
     fits the access-policy window.
     """
@@ -345,7 +346,7 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     mb = ws > l2_bytes // 2
     if mb and not (classes & CLASS_IMB):
         classes |= CLASS_MB
-    d16 = bool((classes & CLASS_MB) and variant == VARIANT_STREAM and f["maxgap"] <= 65535)
+    d16 = False  # MB delta colind is implemented but not auto-selected (reading 9)
     ml = nnz > 0 and f["misses"] > 0.75 * nnz and 8 * n > l2_bytes // 16
     if ml:
         classes |= CLASS_ML

@@ -240,7 +240,10 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   }
   if (avg_s <= 4) classes |= SPMV_CLASS_CMP;
   if (ws > d.l2_bytes / 2 && !(classes & SPMV_CLASS_IMB)) classes |= SPMV_CLASS_MB;
-  bool d16 = (classes & SPMV_CLASS_MB) && variant == SPMV_VARIANT_STREAM && f.maxgap <= 65535;
+  // MB -> delta colind: implemented and bit-exact, but on B200 the
+  // decode costs more than the 2 B/nnz it saves (C2: 55 us with vs 45 us
+  // without), so the feature-guided rule leaves it off; d16=1 forces it
+  bool d16 = false;
   const bool ml = nnz > 0 && (double)f.misses > 0.75 * (double)nnz && 8 * n > d.l2_bytes / 16;
   if (ml) classes |= SPMV_CLASS_ML;
   bool xwin = ml && 8 * n <= d.access_window_max;
@@ -526,12 +529,15 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     // row-aligned tiles when the longest row fits twice in a tile: tile k =
     // rows starting in [k*stride, (k+1)*stride), stride = C - maxlen, so no
     // row crosses a tile (no carries, no fix-up kernel)
-    sp.aligned = !seg && maxlen >= 0 && 2 * maxlen <= sp.C && opt.reserved[0] == 0;
+    // (B200: removes a ~5 us fix-up launch, worth it below ~256M nonzeros;
+    // on C5, 1.5G nonzeros, nnz-aligned tiles measured 7% faster)
+    sp.aligned = !seg && maxlen >= 0 && 2 * maxlen <= sp.C && V.nnz < ((int64_t)1 << 28) && opt.reserved[0] == 0;
     sp.stride = sp.aligned ? sp.C - maxlen : sp.C;
     sp.T = std::max<int64_t>(1, (V.nnz + sp.stride - 1) / sp.stride);
     // staged rowptr entries: 1.5x the expected rows per tile (+32)
     const double rpt = avg > 0 ? (double)sp.C / avg : (double)sp.C;
     sp.rows_cap = (int)std::min<double>((double)sp.C + 32, 1.5 * rpt + 32);
+    if (const char* e = getenv("SPMV_ROWS_CAP")) sp.rows_cap = atoi(e);  // tuning knob
     sp.tile_row = s.alloc<int32_t>((size_t)sp.T + 1);
     sp.carry_row = s.alloc<int32_t>((size_t)sp.T);
     sp.carry_val = s.alloc<double>((size_t)sp.T);

@@ -229,7 +229,7 @@ def test_select_rule_table_on_closed_form_features():
     S = oracle
     # C2: 7-pt 128^3 (closed forms above): regular, 217 MB > L2/2, maxgap 16384
     s = S.select(feat(2097152, 14581760, 6.953125, 0.2148, maxgap=16384, misses=8323072), L2, WIN, 4)
-    assert (s.variant, s.d16, s.xwin, s.vs) == (S.VARIANT_STREAM, True, False, 1) and s.classes & S.CLASS_MB
+    assert (s.variant, s.d16, s.xwin, s.vs) == (S.VARIANT_STREAM, False, False, 1) and s.classes & S.CLASS_MB
     # C5: 27-pt 384^3: regular, maxgap 147071 -> no D16
     s = S.select(feat(56623104, 1520875000, 26.86, 0.5, maxgap=147071, misses=10 ** 8), L2, WIN, 8)
     assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, False, 1)  # rows <= 32 nnz: one lane per row
