@@ -73,7 +73,8 @@ typedef struct spmv_options {
   int32_t emulate_devices; /* ngpus > 1: 1 = place every shard on the current device (tests) */
   int32_t stages;          /* STREAM smem ring depth: 0 = auto (one stage per consumer warp), else a multiple of 4 <= 32 */
   int32_t seg;             /* STREAM / SPLIT short part, segmented consumer mode: -1 auto, 0 off, 1 on */
-  int32_t reserved[5];      /* reserved[0] = 1 disables row-aligned tiles (tests) */
+  int32_t long_mode;       /* SPLIT long rows: 0 auto, 1 nonzero chunks, 2 column-tiled (x block in smem) */
+  int32_t reserved[4];     /* reserved[0] = 1 disables row-aligned tiles (tests) */
 } spmv_options;
 
 /* Theta(N) features (Table I) + counts used by the selection.

@@ -32,7 +32,7 @@ class Options(ctypes.Structure):
                 ("l_split", ctypes.c_int64), ("k_long", ctypes.c_int64), ("tile_nnz", ctypes.c_int64),
                 ("merge_items", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
                 ("emulate_devices", ctypes.c_int32), ("stages", ctypes.c_int32), ("seg", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("long_mode", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
     @classmethod
     def make(cls, **kw):

@@ -119,6 +119,10 @@ struct Shard {
   int64_t* chunk_start = nullptr;
   int32_t* chunk_row = nullptr;
   double* chunk_val = nullptr;
+  bool long_tiled = false;
+  int64_t nblk = 0;
+  int64_t* long_seg = nullptr;
+  double* long_partial = nullptr;
   // iterated mode
   double* allpart = nullptr;  // G * kNormPartials
   double* nu = nullptr;
@@ -191,6 +195,10 @@ struct spmv_plan_s {
     a.chunk_start = s.chunk_start;
     a.chunk_row = s.chunk_row;
     a.chunk_val = s.chunk_val;
+    a.long_tiled = s.long_tiled;
+    a.nblk = s.nblk;
+    a.long_seg = s.long_seg;
+    a.long_partial = s.long_partial;
     return a;
   }
   int launch(Shard& s, const double* x, double* y, int stage = 0) const {
@@ -280,6 +288,7 @@ void validate_options(const spmv_options& o) {
   if (o.long_chunk != 0 && (o.long_chunk % 256 || o.long_chunk < 256))
     fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
   if (o.l_split < 0 || o.k_long < 0) fail(SPMV_E_ARG, "negative l_split / k_long");
+  if (o.long_mode < 0 || o.long_mode > 2) fail(SPMV_E_ARG, "long_mode must be 0, 1 or 2");
   if (o.stages < 0 || o.stages > 32 || o.stages % kStreamConsumerWarps)
     fail(SPMV_E_ARG, "stages must be 0 (auto) or a multiple of %d up to 32", kStreamConsumerWarps);
 }
@@ -636,7 +645,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       int64_t* scan = s.alloc<int64_t>((size_t)scan_blocks(s.m) + 2);
       s.n_sp = 0;
       if (build_bin(s, s.sp[s.n_sp], A, 1, ts, 1, seg, scan)) ++s.n_sp;
-      if (P->l_split > ts && build_bin(s, s.sp[s.n_sp], A, ts + 1, P->l_split, 32, false, scan)) ++s.n_sp;
+      // medium bin lane group: 32, or force_vs when given
+      const int mvs = opt.force_vs > 0 ? opt.force_vs : 32;
+      if (P->l_split > ts && build_bin(s, s.sp[s.n_sp], A, ts + 1, P->l_split, mvs, false, scan)) ++s.n_sp;
       s.zero_y = true;
       s.n_long = s.hs.n_long;
       if (s.n_long > 0) {
@@ -650,6 +661,19 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
         ck(cudaStreamSynchronize(s.stream), "long_rows");
         s.chunk_row = s.alloc<int32_t>((size_t)s.n_chunks);
         s.chunk_val = s.alloc<double>((size_t)s.n_chunks);
+        // column-tiled long rows when a (row, x block) segment averages >= 64
+        // nonzeros (dense-ish long rows: x served from smem, not one L2 sector
+        // per nonzero); long_mode 1/2 forces chunks / tiled
+        const int64_t nblk = (s.n_cols + kLongXB - 1) / kLongXB;
+        const bool dense = s.hs.nnz_long >= 64 * s.n_long * nblk;
+        s.long_tiled = opt.long_mode == 2 || (opt.long_mode == 0 && dense);
+        if (s.long_tiled) {
+          s.nblk = nblk;
+          s.long_seg = s.alloc<int64_t>((size_t)s.n_long * (nblk + 1));
+          s.long_partial = s.alloc<double>((size_t)s.n_long * nblk);
+          launch_long_seg(A, s.long_rows, s.n_long, nblk, s.long_seg, s.stream);
+          count_launches(1, "long_seg");
+        }
       }
     }
     s.x = s.alloc<double>((size_t)n_cols);

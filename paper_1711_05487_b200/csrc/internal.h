@@ -93,13 +93,22 @@ struct ExecArgs {
   const int64_t* mnnz;
   int32_t* mcarry_row;
   double* mcarry_val;
-  // SPLIT long rows
+  // SPLIT long rows: nonzero chunks, or column-tiled (x block in smem)
   int64_t l_split, chunk, n_long, n_chunks;
   const int32_t* long_rows;
   const int64_t* chunk_start;
   int32_t* chunk_row;
   double* chunk_val;
+  bool long_tiled;
+  int64_t nblk;               // x blocks of kLongXB columns
+  const int64_t* long_seg;    // [n_long][nblk+1] segment starts
+  double* long_partial;       // [n_long][nblk]
 };
+
+constexpr int64_t kLongXB = 2048;  // columns per x block staged in smem by the column-tiled long-row kernel
+void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long, int64_t nblk, int64_t* seg,
+                     cudaStream_t s);
+int launch_long_tiled(const ExecArgs& a, cudaStream_t s);
 
 int launch_vector(const ExecArgs& a, bool skip_long, cudaStream_t s);  // returns #launches
 int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int stage, cudaStream_t s);

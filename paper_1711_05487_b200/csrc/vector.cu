@@ -188,7 +188,9 @@ int launch_split(const ExecArgs& a, cudaStream_t s) {
   // 1. short / medium bins: cta_stream over each compacted bin (rows mapped
   //    back to y through the bin's row map); the bins own disjoint rows
   for (int b = 0; b < a.n_sp; ++b) n += launch_stream_plan(a.sp[b], a.x, a.y, a.stage, s);
-  // 2. long rows: chunk partials, then the ordered per-row reduction (sets y)
+  // 2. long rows: column-tiled (x blocks in smem) or nonzero chunks, then the
+  //    ordered per-row reduction (sets y)
+  if (a.long_tiled) return n + launch_long_tiled(a, s);
   if (a.n_chunks > 0) {
     if (a.stage != 2) {
       ++n;

@@ -41,7 +41,7 @@ def m_maxlen(m):
 
 VARIANTS = [("vector", 1), ("vector", 2), ("vector", 8), ("vector", 32), ("stream", 1), ("stream", 4),
             ("stream", 8), ("stream", 32), ("stream_seg", 1), ("stream_nnz_tiles", 1), ("merge", 0), ("split", 4),
-    ("split_seg", 32)]
+    ("split_seg", 32), ("split_chunks", 16), ("split_tiled", 8)]
 
 SUITE = sg.small_suite(seed=21)
 
@@ -54,6 +54,10 @@ def variant_kw(variant):
         return "stream", {"d16": 1}
     if variant == "split_seg":
         return "split", {"seg": 1}
+    if variant == "split_chunks":
+        return "split", {"long_mode": 1}
+    if variant == "split_tiled":
+        return "split", {"long_mode": 2}
     if variant == "stream_nnz_tiles":
         return "stream", {"no_aligned": 1}
     return variant, {}
