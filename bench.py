@@ -51,11 +51,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--variant", default="auto", choices=["auto", "vector", "stream", "merge", "split"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "vector", "stream", "merge", "split", "nnzsplit"])
     ap.add_argument("--vs", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--d16", type=int, default=-1)
     ap.add_argument("--seg", type=int, default=-1)
+    ap.add_argument("--split-bins", type=int, default=-1, help="SPLIT non-long rows: 0 cta_stream bins, 1 nnz_split")
     ap.add_argument("--no-aligned", action="store_true", help="nnz-aligned STREAM tiles (carries + fix-up)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -245,6 +246,8 @@ def run_native(a):
         opts["seg"] = a.seg
     if a.no_aligned:
         opts["no_aligned"] = 1
+    if a.split_bins >= 0:
+        opts["split_bins"] = a.split_bins
     t0 = time.time()
     plan = spmv.Plan(blk["rowptr"], blk["colind"], blk["vals"], n_cols=blk["N"], **opts)
     plan_s = time.time() - t0

@@ -52,7 +52,9 @@ typedef enum {
   SPMV_VARIANT_VECTOR = 1,  /* csr_vector<VS>: VS lanes per row (CMP: unroll+vectorise) */
   SPMV_VARIANT_STREAM = 2,  /* cta_stream: TMA-staged fixed nnz tiles (MB: vectorised streaming) */
   SPMV_VARIANT_MERGE = 3,   /* merge_path: rows+nnz balanced (IMB "auto" schedule) */
-  SPMV_VARIANT_SPLIT = 4    /* long_row_split: short rows + chunked long rows (IMB decomposition, Fig. 7) */
+  SPMV_VARIANT_SPLIT = 4,   /* long_row_split: long rows by column-tiled CTAs + the other rows (IMB decomposition, Fig. 7) */
+  SPMV_VARIANT_NNZSPLIT = 5 /* nnz_split: equal-nonzero warp tiles over the non-empty rows, rows cut at tile edges
+                               (nnz-balanced partition P:708-711 + decomposition P:608-621 at warp granularity) */
 } spmv_variant;
 
 /* Bottleneck classes (Sec. III-A) recorded by the selection. */
@@ -74,7 +76,8 @@ typedef struct spmv_options {
   int32_t stages;          /* STREAM smem ring depth: 0 = auto (one stage per consumer warp), else a multiple of 4 <= 32 */
   int32_t seg;             /* STREAM / SPLIT short part, segmented consumer mode: -1 auto, 0 off, 1 on */
   int32_t long_mode;       /* SPLIT long rows: 0 auto, 1 nonzero chunks, 2 column-tiled (x block in smem) */
-  int32_t reserved[4];     /* reserved[0] = 1 disables row-aligned tiles (tests) */
+  int32_t split_bins;      /* SPLIT non-long rows: -1 auto (one nnz_split bin), 0 cta_stream length bins, 1 nnz_split bin */
+  int32_t reserved[3];     /* reserved[0] = 1 disables row-aligned tiles (tests) */
 } spmv_options;
 
 /* Theta(N) features (Table I) + counts used by the selection.
@@ -85,6 +88,7 @@ typedef struct spmv_features {
   int64_t maxgap;          /* max in-row column gap over non-head nonzeros (0 if none) */
   int64_t misses;          /* non-head nonzeros with gap > 16 (Table I misses_i, 128-B line) */
   double nnz_avg, nnz_sd, avg_short, sd_short;
+  int64_t n_cols;          /* columns (x length); the long-row density test uses it */
 } spmv_features;
 
 typedef struct spmv_device_props {
@@ -122,6 +126,8 @@ typedef struct spmv_plan_info {
   int64_t tile_stride;        /* STREAM tile stride in nonzeros (= tile_nnz, or tile_nnz - longest row) */
   int32_t tiles_row_aligned;  /* 1: tile k = rows starting in [k*stride, (k+1)*stride); no carries */
   int32_t pad2_;
+  int64_t n_nz_rows;          /* nnz_split: non-empty rows of the pass (mc) */
+  int64_t n_nz_tiles;         /* nnz_split: warp tiles of 256 nonzeros */
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */
@@ -204,7 +210,10 @@ enum {
   SPMV_ARR_HEAD = 8,         /* int32[n_rows] */
   SPMV_ARR_ANCHOR = 9,       /* int32[n_tiles] */
   SPMV_ARR_DECODED = 10,     /* int32[nnz] colind re-decoded on the device from dcol/head/anchor */
-  SPMV_ARR_SHARD_BOUNDS = 11 /* int64[ngpus+1] */
+  SPMV_ARR_SHARD_BOUNDS = 11, /* int64[ngpus+1] */
+  SPMV_ARR_NZ_ROWMAP = 12,    /* int64[mc+1]: nnz_split non-empty rows (y row ids), rowmap[mc] = n_rows */
+  SPMV_ARR_NZ_RPC = 13,       /* int64[mc+1]: their rowptr (rpc[q] = rowptr[rowmap[q]], rpc[mc] = nnz) */
+  SPMV_ARR_NZ_TILE_Q = 14     /* int64[n_nz_tiles+1]: tile_q[k] = last q with rpc[q] <= 256k; tile_q[T] = mc */
 };
 int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst);
 

@@ -22,6 +22,8 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``) -- no function is
   tile_rows       linear-scan definition, ownership cover
   merge_splits    binary-search split vs the sequential merge, path invariants
   long_chunks     coverage / exact tiling of long rows
+  nonempty_rows   numpy flatnonzero of the row lengths, coverage
+  nz_tiles        binary-search (searchsorted) re-derivation, ownership cover
   d16 encode/dec  SPEC S:134-136 widths, round trip, stencil gap closed forms
   features        SPEC S:415 sd example, stencil closed forms
   select          hand-evaluated rule table on the configs' closed-form features
@@ -65,6 +67,9 @@ def _lib():
         L.oracle_tile_rows.argtypes = [i64, vp, i64, i64, vp]
         L.oracle_merge_splits.argtypes = [i64, vp, i64, i64, i64, vp, vp]
         L.oracle_long_chunks.argtypes = [i64, vp, i64, i64, vp, vp, vp]
+        L.oracle_nonempty_rows.argtypes = [i64, vp, vp, vp]
+        L.oracle_nonempty_rows.restype = i64
+        L.oracle_nz_tiles.argtypes = [i64, vp, i64, i64, vp]
         L.oracle_long_chunks.restype = i64
         L.oracle_d16_encode.argtypes = [i64, vp, vp, vp, vp, _i64p]
         L.oracle_d16_encode.restype = ctypes.c_int
@@ -183,12 +188,15 @@ class _Feat(ctypes.Structure):
                [(k, ctypes.c_double) for k in ("nnz_avg", "nnz_sd", "avg_short", "sd_short")]
 
 
-def features(rowptr, colind, L_split=4096, line_elems=16):
-    """Theta(N) Table I features + counts for selection."""
+def features(rowptr, colind, L_split=4096, line_elems=16, n_cols=None):
+    """Theta(N) Table I features + counts for selection.
+    n_cols (default: square, = rows) is carried for the long-row density test."""
     rp, ci = _rp64(rowptr), _c32(colind)
     f = _Feat()
     _lib().oracle_features(rp.size - 1, _p(rp), _p(ci), int(L_split), int(line_elems), ctypes.byref(f))
-    return {k: getattr(f, k) for k, _ in _Feat._fields_}
+    d = {k: getattr(f, k) for k, _ in _Feat._fields_}
+    d["n_cols"] = int(rp.size - 1 if n_cols is None else n_cols)
+    return d
 
 
 def tile_count(nnz, C):
@@ -201,6 +209,30 @@ def tile_rows(rowptr, C):
     R = np.empty(T + 1, np.int64)
     _lib().oracle_tile_rows(rp.size - 1, _p(rp), int(C), T, _p(R))
     return R
+
+
+NZ_TILE = 256  # nnz_split warp tile (nonzeros)
+
+
+def nonempty_rows(rowptr):
+    """(rowmap[mc+1], rpc[mc+1]) of the non-empty rows (reading 19)."""
+    rp = _rp64(rowptr)
+    n = rp.size - 1
+    mc = _lib().oracle_nonempty_rows(n, _p(rp), None, None)
+    rowmap = np.empty(mc + 1, np.int64)
+    rpc = np.empty(mc + 1, np.int64)
+    _lib().oracle_nonempty_rows(n, _p(rp), _p(rowmap), _p(rpc))
+    return rowmap, rpc
+
+
+def nz_tiles(rpc, W=NZ_TILE):
+    """tile_q[k] = largest q with rpc[q] <= k*W (k < T = ceil(nnz/W)), tile_q[T] = mc."""
+    rpc = _rp64(rpc)
+    mc, nnz = rpc.size - 1, int(rpc[-1])
+    T = -(-nnz // int(W))
+    tq = np.empty(T + 1, np.int64)
+    _lib().oracle_nz_tiles(mc, _p(rpc), int(W), T, _p(tq))
+    return tq
 
 
 def merge_splits(rowptr, items):
@@ -287,7 +319,7 @@ def harmonic_mean(rates):
 # Selection (Table II). A pure function of the
 # features and device properties. Rule constants are readings.
 # --------------------------------------------------------------------------
-VARIANT_VECTOR, VARIANT_STREAM, VARIANT_MERGE, VARIANT_SPLIT = 1, 2, 3, 4
+VARIANT_VECTOR, VARIANT_STREAM, VARIANT_MERGE, VARIANT_SPLIT, VARIANT_NNZSPLIT = 1, 2, 3, 4, 5
 CLASS_MB, CLASS_ML, CLASS_IMB, CLASS_CMP = 1, 2, 4, 8
 
 
@@ -311,8 +343,9 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     """Feature-guided selection. f = features(..) dict.
 
     IMB: long rows (n_long > 0 and nnz_max > K_long*nnz_avg) ->
-    long_row_split; else skew (sd_s/avg_s > skew_sd or empty/N > empty_frac)
-    -> merge_path. Regular rows -> cta_stream for avg_s <= 32, else
+    long_row_split when they are dense enough for column-tiled x blocks
+    (nnz_long >= 64 * n_long * ceil(n_cols/2048)), else nnz_split; skew
+    (sd_s/avg_s > skew_sd or empty/N > empty_frac) -> nnz_split. Regular rows -> cta_stream for avg_s <= 32, else
     csr_vector (CMP analogue: lane group sized to the row, VS =
     clamp(pow2ceil(avg_s), 2, 32)). MB: working set > L2/2 (the
     D16 colind it maps to is available but not auto-selected: slower on
@@ -330,10 +363,12 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     if skew or longr:
         classes |= CLASS_IMB
     vs = min(32, max(2, _pow2ceil(int(math.ceil(avg_s))) if avg_s > 0 else 2))
-    if longr:  # long rows first: the length-bin decomposition also absorbs skew
-        variant = VARIANT_SPLIT
+    nblk = -(-int(f.get("n_cols", n)) // 2048)
+    dense_long = f["n_long"] > 0 and f["nnz_long"] >= 64 * f["n_long"] * nblk
+    if longr:  # long rows first: the decomposition also absorbs skew
+        variant = VARIANT_SPLIT if dense_long else VARIANT_NNZSPLIT
     elif skew:
-        variant = VARIANT_MERGE
+        variant = VARIANT_NNZSPLIT
     elif avg_s <= 32:
         variant = VARIANT_STREAM
     else:

@@ -235,6 +235,37 @@ void oracle_tile_rows(int64_t n, const int64_t* rowptr, int64_t C, int64_t T, in
 }
 
 /* ---------------------------------------------------------------------------
+ * nnz_split structures (reading 19; the nnz-balanced partition of
+ * P:708-711 cut at warp granularity, long rows shared by consecutive pieces
+ * as in the decomposition P:608-621). Written as plain sequential scans.
+ *   rows with rowptr[i+1] > rowptr[i], in increasing i: rowmap[q] = i,
+ *   rpc[q] = rowptr[i]; rowmap[mc] = n, rpc[mc] = nnz. Returns mc.
+ *   tile_q[k] = the largest q with rpc[q] <= k*W (k < T), tile_q[T] = mc.
+ * ------------------------------------------------------------------------- */
+int64_t oracle_nonempty_rows(int64_t n, const int64_t* rowptr, int64_t* rowmap, int64_t* rpc) {
+  int64_t q = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (rowptr[i + 1] > rowptr[i]) {
+      if (rowmap) rowmap[q] = i;
+      if (rpc) rpc[q] = rowptr[i];
+      ++q;
+    }
+  }
+  if (rowmap) rowmap[q] = n;
+  if (rpc) rpc[q] = rowptr[n];
+  return q;
+}
+
+void oracle_nz_tiles(int64_t mc, const int64_t* rpc, int64_t W, int64_t T, int64_t* tile_q) {
+  int64_t q = 0;
+  for (int64_t k = 0; k < T; ++k) {
+    while (q + 1 <= mc && rpc[q + 1] <= k * W) ++q;
+    tile_q[k] = q;
+  }
+  tile_q[T] = mc;
+}
+
+/* ---------------------------------------------------------------------------
  * Merge-path split (the GPU analogue of the IMB "auto" schedule,
  * P:621-627): merge list A[i] = rowptr[i+1] (i < n) with list B[j] = j
  * (j < nnz); ties go to A. split(d) = (i, d-i) with i the number of A items

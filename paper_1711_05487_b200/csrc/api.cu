@@ -123,6 +123,12 @@ struct Shard {
   int64_t nblk = 0;
   int64_t* long_seg = nullptr;
   double* long_partial = nullptr;
+  // NNZSPLIT (whole shard) / SPLIT short+medium rows as one nnz_split bin
+  NzPlan nz;
+  bool use_nz = false;
+  // SPLIT: side stream for the long rows (concurrent with the bins)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // iterated mode
   double* allpart = nullptr;  // G * kNormPartials
   double* nu = nullptr;
@@ -148,6 +154,10 @@ struct Shard {
     allocs.clear();
     if (ev_part) cudaEventDestroy(ev_part);
     if (ev_x) cudaEventDestroy(ev_x);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
+    side = nullptr;
     if (stream) cudaStreamDestroy(stream);
     stream = nullptr;
   }
@@ -176,6 +186,7 @@ struct spmv_plan_s {
     a.x = x;
     a.y = y;
     a.vs = sel.vs;
+    a.nnz_max = feat.nnz_max;
     a.sm_count = s.sm_count;
     a.sp[0] = s.sp[0];
     a.sp[1] = s.sp[1];
@@ -199,6 +210,11 @@ struct spmv_plan_s {
     a.nblk = s.nblk;
     a.long_seg = s.long_seg;
     a.long_partial = s.long_partial;
+    a.nz = s.nz;
+    a.use_nz = s.use_nz;
+    a.side = s.side;
+    a.ev_fork = s.ev_fork;
+    a.ev_join = s.ev_join;
     return a;
   }
   int launch(Shard& s, const double* x, double* y, int stage = 0) const {
@@ -208,6 +224,7 @@ struct spmv_plan_s {
       case SPMV_VARIANT_VECTOR: return launch_vector(a, false, s.stream);
       case SPMV_VARIANT_STREAM: return launch_stream(a, s.stream);
       case SPMV_VARIANT_MERGE: return launch_merge(a, s.stream);
+      case SPMV_VARIANT_NNZSPLIT: return launch_nzsplit(a, s.stream);
       default: return launch_split(a, s.stream);
     }
   }
@@ -235,10 +252,16 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   if (skew || longr) classes |= SPMV_CLASS_IMB;
   int vs = avg_s > 0 ? pow2ceil((int64_t)std::ceil(avg_s)) : 2;
   vs = std::min(32, std::max(2, vs));
-  // long rows first: the length-bin decomposition also absorbs skew (B200
-  // sweep on C3: split 0.37 ms vs merge_path 0.99 ms)
-  int variant = longr ? SPMV_VARIANT_SPLIT : skew ? SPMV_VARIANT_MERGE : avg_s <= 32 ? SPMV_VARIANT_STREAM
-                                                                                     : SPMV_VARIANT_VECTOR;
+  // IMB: long rows dense enough for column-tiled x blocks (a (row, 2048-col
+  // block) segment averages >= 64 nonzeros) -> long_row_split (long rows
+  // tiled, concurrently with one nnz_split bin of the other rows); any other
+  // long-row or skewed matrix -> nnz_split (rows cut at warp-tile edges)
+  const int64_t nblk = (f.n_cols + 2047) / 2048;
+  const bool dense_long = f.n_long > 0 && f.nnz_long >= 64 * f.n_long * nblk;
+  int variant = longr ? (dense_long ? SPMV_VARIANT_SPLIT : SPMV_VARIANT_NNZSPLIT)
+                : skew ? SPMV_VARIANT_NNZSPLIT
+                : avg_s <= 32 ? SPMV_VARIANT_STREAM
+                              : SPMV_VARIANT_VECTOR;
   if (o.force_variant > 0) variant = o.force_variant;
   if (variant == SPMV_VARIANT_STREAM) {
     // cta_stream: one lane per row for rows up to 32 nonzeros (lanes walk
@@ -278,7 +301,7 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
 }
 
 void validate_options(const spmv_options& o) {
-  if (o.force_variant < 0 || o.force_variant > 4) fail(SPMV_E_ARG, "force_variant %d out of range", o.force_variant);
+  if (o.force_variant < 0 || o.force_variant > 5) fail(SPMV_E_ARG, "force_variant %d out of range", o.force_variant);
   if (o.force_vs != 0 && o.force_vs != 1 && o.force_vs != 2 && o.force_vs != 4 && o.force_vs != 8 &&
       o.force_vs != 16 && o.force_vs != 32)
     fail(SPMV_E_ARG, "force_vs %d not in {0,1,2,4,8,16,32}", o.force_vs);
@@ -289,6 +312,7 @@ void validate_options(const spmv_options& o) {
     fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
   if (o.l_split < 0 || o.k_long < 0) fail(SPMV_E_ARG, "negative l_split / k_long");
   if (o.long_mode < 0 || o.long_mode > 2) fail(SPMV_E_ARG, "long_mode must be 0, 1 or 2");
+  if (o.split_bins < -1 || o.split_bins > 1) fail(SPMV_E_ARG, "split_bins must be -1, 0 or 1");
   if (o.stages < 0 || o.stages > 32 || o.stages % kStreamConsumerWarps)
     fail(SPMV_E_ARG, "stages must be 0 (auto) or a multiple of %d up to 32", kStreamConsumerWarps);
 }
@@ -509,6 +533,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   std::vector<int64_t> ms;
   for (auto& s : P->shards) { st.push_back(s.hs); ms.push_back(s.m); }
   features_from_stats(st, ms, P->feat);
+  P->feat.n_cols = n_cols;
   select_impl(P->feat, P->props, rp_bytes, opt, P->sel);
   if (P->sel.d16) P->d16_width = P->feat.maxgap <= 255 ? 8 : 16;
   P->select_ms = now_ms() - t_c;
@@ -548,8 +573,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     sp.rows_cap = (int)std::min<double>((double)sp.C + 32, 1.5 * rpt + 32);
     if (const char* e = getenv("SPMV_ROWS_CAP")) sp.rows_cap = atoi(e);  // tuning knob
     sp.tile_row = s.alloc<int32_t>((size_t)sp.T + 1);
-    sp.carry_row = s.alloc<int32_t>((size_t)sp.T);
-    sp.carry_val = s.alloc<double>((size_t)sp.T);
+    sp.carry_row = s.alloc<int32_t>((size_t)fixup_capacity(sp.T));
+    sp.carry_val = s.alloc<double>((size_t)fixup_capacity(sp.T));
+    sp.max_run = (std::max<int64_t>(maxlen, P->feat.nnz_max) + sp.stride - 1) / sp.stride + 1;
     DevStats zero{};
     ck(cudaMemcpyAsync(&s.stats->n_incoming, &zero.n_incoming, 8, cudaMemcpyHostToDevice, s.stream), "stats");
     launch_tile_rows(V, sp.stride, sp.T, sp.tile_row, s.stats, s.stream);
@@ -587,9 +613,29 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     }
     if (sp.grid < 0) fail(SPMV_E_CUDA, "cta_stream: cannot fit tile_nnz=%lld in shared memory", (long long)sp.C);
   };
-  // compacted bin of the rows with lo <= len <= hi (non-empty), for cta_stream
+  // nnz_split pass over the view V (colind/values) restricted to the
+  // non-empty rows rowmap[0..mc) with rowptr rpc; y rows [0, s.m)
+  auto build_nz = [&](Shard& s, NzPlan& z, const MatView& V, const void* rpc, int32_t* rowmap, int64_t mc) {
+    z.V = V;
+    z.rpc = rpc;
+    z.rowmap = rowmap;
+    z.mc = mc;
+    z.m_out = s.m;
+    z.zero_gaps = true;
+    z.T = (V.nnz + kNzTile - 1) / kNzTile;
+    z.tile_q = s.alloc<int32_t>((size_t)z.T + 1);
+    z.carry_row = s.alloc<int32_t>((size_t)fixup_capacity(z.T));
+    z.carry_val = s.alloc<double>((size_t)fixup_capacity(z.T));
+    z.max_run = P->feat.nnz_max / kNzTile + 2;
+    launch_nz_tiles(z, s.stream);
+    count_launches(2, "nz tiles");
+    z.grid = nz_prepare(z, s.sm_count);
+    if (z.grid < 0) fail(SPMV_E_CUDA, "nnz_split: occupancy query failed");
+  };
+  // compacted bin of the rows with lo <= len <= hi (non-empty): cta_stream
+  // plan sp, or (nz != null) one nnz_split pass
   auto build_bin = [&](Shard& s, StreamPlan& sp, const MatView& A, int64_t lo, int64_t hi, int vs, bool seg,
-                       int64_t* scan) -> bool {
+                       int64_t* scan, NzPlan* nz = nullptr) -> bool {
     const int64_t nb = scan_blocks(s.m);
     int64_t nrows = 0;
     launch_row_list(A, lo, hi, nullptr, scan, s.stream);  // count
@@ -597,7 +643,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     ck(cudaMemcpyAsync(&nrows, scan + nb, 8, cudaMemcpyDeviceToHost, s.stream), "bin count");
     ck(cudaStreamSynchronize(s.stream), "bin count");
     if (nrows == 0) return false;
-    int32_t* rows = s.alloc<int32_t>((size_t)nrows);
+    int32_t* rows = s.alloc<int32_t>((size_t)nrows + 1);
     launch_row_list(A, lo, hi, rows, scan, s.stream);
     count_launches(3, "bin rows");
     void* frp = s.alloc<char>((size_t)(s.m + 1) * rp_bytes);
@@ -614,6 +660,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     void* brp = s.alloc<char>((size_t)(nrows + 1) * rp_bytes);
     launch_gather_rowptr(frp, rp_bytes, rows, nrows, s.m, brp, s.stream);
     count_launches(1, "bin gather");
+    if (nz) {
+      build_nz(s, *nz, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, brp, rows, nrows);
+      return true;
+    }
     build_stream(s, sp, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, rows, false, vs, seg,
                  std::min<int64_t>(hi, P->feat.nnz_max));
     return true;
@@ -629,10 +679,32 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       s.Tm = std::max<int64_t>(1, (s.m + s.nnz + s.items - 1) / s.items);
       s.mrow = s.alloc<int32_t>((size_t)s.Tm + 1);
       s.mnnz = s.alloc<int64_t>((size_t)s.Tm + 1);
-      s.mcarry_row = s.alloc<int32_t>((size_t)s.Tm);
-      s.mcarry_val = s.alloc<double>((size_t)s.Tm);
+      s.mcarry_row = s.alloc<int32_t>((size_t)fixup_capacity(s.Tm));
+      s.mcarry_val = s.alloc<double>((size_t)fixup_capacity(s.Tm));
       launch_merge_splits(A, s.items, s.Tm, s.mrow, s.mnnz, s.stream);
       count_launches(1, "merge_splits");
+    } else if (P->sel.variant == SPMV_VARIANT_NNZSPLIT) {
+      // the non-empty rows of the whole shard (colind / values used in place)
+      int64_t* scan = s.alloc<int64_t>((size_t)scan_blocks(s.m) + 2);
+      const int64_t nb = scan_blocks(s.m);
+      int64_t mc = 0;
+      launch_row_list(A, 1, INT64_MAX, nullptr, scan, s.stream);
+      count_launches(2, "nz count");
+      ck(cudaMemcpyAsync(&mc, scan + nb, 8, cudaMemcpyDeviceToHost, s.stream), "nz count");
+      ck(cudaStreamSynchronize(s.stream), "nz count");
+      if (s.m == 0) mc = 0;
+      int32_t* rows = s.alloc<int32_t>((size_t)mc + 1);
+      void* rpc = s.alloc<char>((size_t)(mc + 1) * rp_bytes);
+      if (s.m > 0) {
+        launch_row_list(A, 1, INT64_MAX, rows, scan, s.stream);
+        count_launches(3, "nz rows");
+        launch_gather_rowptr(A.rowptr, rp_bytes, rows, mc, s.m, rpc, s.stream);
+        count_launches(1, "nz rowptr");
+      } else {
+        ck(cudaMemsetAsync(rpc, 0, rp_bytes, s.stream), "memset");
+      }
+      build_nz(s, s.nz, A, rpc, rows, mc);
+      s.use_nz = true;
     } else if (P->sel.variant == SPMV_VARIANT_SPLIT) {
       // decomposition by row length (Fig. 6 read through S:120-125):
       // short rows (1 <= len <= T_s) and medium rows (T_s < len <= L_split)
@@ -644,11 +716,22 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       const int64_t ts = seg ? P->l_split : std::min<int64_t>(kShortRowMax, P->l_split);
       int64_t* scan = s.alloc<int64_t>((size_t)scan_blocks(s.m) + 2);
       s.n_sp = 0;
-      if (build_bin(s, s.sp[s.n_sp], A, 1, ts, 1, seg, scan)) ++s.n_sp;
-      // medium bin lane group: 32, or force_vs when given
-      const int mvs = opt.force_vs > 0 ? opt.force_vs : 32;
-      if (P->l_split > ts && build_bin(s, s.sp[s.n_sp], A, ts + 1, P->l_split, mvs, false, scan)) ++s.n_sp;
-      s.zero_y = true;
+      if (opt.split_bins != 0) {
+        // all rows up to L_split as one nnz_split bin (zeroes empty and long rows;
+        // the long-row reduction runs after it)
+        s.use_nz = true;
+        if (!build_bin(s, s.sp[0], A, 1, P->l_split, 1, false, scan, &s.nz)) {
+          s.nz = NzPlan{};
+          s.nz.m_out = s.m;
+          s.nz.zero_gaps = true;
+        }
+      } else {
+        if (build_bin(s, s.sp[s.n_sp], A, 1, ts, 1, seg, scan)) ++s.n_sp;
+        // medium bin lane group: 32, or force_vs when given
+        const int mvs = opt.force_vs > 0 ? opt.force_vs : 32;
+        if (P->l_split > ts && build_bin(s, s.sp[s.n_sp], A, ts + 1, P->l_split, mvs, false, scan)) ++s.n_sp;
+        s.zero_y = true;
+      }
       s.n_long = s.hs.n_long;
       if (s.n_long > 0) {
         const int nb = 1024;
@@ -659,8 +742,8 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
         count_launches(4, "long_rows");
         ck(cudaMemcpyAsync(&s.n_chunks, s.chunk_start + s.n_long, 8, cudaMemcpyDeviceToHost, s.stream), "chunks");
         ck(cudaStreamSynchronize(s.stream), "long_rows");
-        s.chunk_row = s.alloc<int32_t>((size_t)s.n_chunks);
-        s.chunk_val = s.alloc<double>((size_t)s.n_chunks);
+        s.chunk_row = s.alloc<int32_t>((size_t)fixup_capacity(s.n_chunks));
+        s.chunk_val = s.alloc<double>((size_t)fixup_capacity(s.n_chunks));
         // column-tiled long rows when a (row, x block) segment averages >= 64
         // nonzeros (dense-ish long rows: x served from smem, not one L2 sector
         // per nonzero); long_mode 1/2 forces chunks / tiled
@@ -674,6 +757,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
           launch_long_seg(A, s.long_rows, s.n_long, nblk, s.long_seg, s.stream);
           count_launches(1, "long_seg");
         }
+        // the long rows run on a side stream, concurrently with the bins
+        ck(cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaEventCreateWithFlags(&s.ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&s.ev_join, cudaEventDisableTiming), "cudaEventCreate");
       }
     }
     s.x = s.alloc<double>((size_t)n_cols);
@@ -766,6 +853,7 @@ void spmv_options_default(spmv_options* o) {
   o->d16 = -1;
   o->xwin = -1;
   o->seg = -1;
+  o->split_bins = -1;
   o->validate = 1;
 }
 
@@ -904,6 +992,8 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     info->tiles_row_aligned = s0.sp[0].aligned ? 1 : 0;
     info->merge_items = s0.items;
     info->n_merge_tiles = s0.Tm;
+    info->n_nz_rows = s0.nz.mc;
+    info->n_nz_tiles = s0.nz.T;
     info->l_split = p->l_split;
     info->long_chunk = p->chunk;
     int64_t nc = 0, bytes = 0;
@@ -985,6 +1075,20 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
         if (e == cudaSuccess) e = cudaMemcpy(dst, tmp, (size_t)s.nnz * 4, cudaMemcpyDeviceToHost);
         cudaFree(tmp);
         ck(e, "decode export");
+        break;
+      }
+      case SPMV_ARR_NZ_ROWMAP: widen32(s.nz.rowmap, s.nz.rowmap ? s.nz.mc + 1 : 0); break;
+      case SPMV_ARR_NZ_TILE_Q: widen32(s.nz.tile_q, s.nz.tile_q ? s.nz.T + 1 : 0); break;
+      case SPMV_ARR_NZ_RPC: {
+        count = s.nz.rpc ? s.nz.mc + 1 : 0;
+        if (!dst || count == 0) break;
+        if (s.rp_bytes == 8) {
+          ck(cudaMemcpy(dst, s.nz.rpc, (size_t)count * 8, cudaMemcpyDeviceToHost), "export");
+        } else {
+          std::vector<int32_t> h((size_t)count);
+          ck(cudaMemcpy(h.data(), s.nz.rpc, (size_t)count * 4, cudaMemcpyDeviceToHost), "export");
+          for (int64_t i = 0; i < count; ++i) ((int64_t*)dst)[i] = h[i];
+        }
         break;
       }
       case SPMV_ARR_SHARD_BOUNDS:

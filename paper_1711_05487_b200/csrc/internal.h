@@ -46,8 +46,30 @@ struct StreamPlan {
   bool aligned = false;  // row-aligned tiles: tile k = rows starting in [k*stride, (k+1)*stride)
   int64_t stride = 0;    // tile stride in nonzeros (C, or C - longest row when aligned)
   int64_t* tile_nz = nullptr;  // aligned: tile_nz[k] = rowptr[tile_row[k]], k = 0..T
+  int64_t max_run = 1;         // longest run of equal carry rows (fix-up choice)
 };
 void launch_tile_nz(const MatView& A, const int32_t* tile_row, int64_t T, int64_t* tile_nz, cudaStream_t s);
+
+// One nnz_split pass (nzsplit.cu) over the CSR view V restricted to its
+// non-empty rows: rpc[mc+1] (rowptr of the non-empty rows, V's rowptr type),
+// rowmap[mc+1] (y row of each, rowmap[mc] = m_out), warp tiles of kNzTile
+// nonzeros with tile_q[k] = the non-empty row holding nonzero k*kNzTile.
+constexpr int64_t kNzTile = 256;
+struct NzPlan {
+  MatView V{};                      // colind / values / nnz (V.rowptr unused by the kernel)
+  const void* rpc = nullptr;
+  const int32_t* rowmap = nullptr;
+  int32_t* tile_q = nullptr;
+  int32_t* carry_row = nullptr;
+  double* carry_val = nullptr;
+  int64_t mc = 0, T = 0, m_out = 0;
+  int grid = 0;
+  int64_t max_run = 1;    // longest run of equal carry rows (fix-up choice)
+  bool zero_gaps = true;  // write y = 0 for the rows of [0, m_out) not in rowmap
+};
+void launch_nz_tiles(const NzPlan& z, cudaStream_t s);  // tile_q and rowmap[mc] = m_out
+int nz_prepare(const NzPlan& z, int sm_count);         // persistent grid (<0 on error)
+int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaStream_t s);
 
 // ---- inspector ------------------------------------------------------------
 void launch_rowstats(const MatView& A, int64_t l_split, uint32_t* headbits, DevStats* st, cudaStream_t s);
@@ -60,7 +82,10 @@ void launch_long_rows(const MatView& A, int64_t l_split, int64_t chunk, int32_t*
 void launch_d16_encode(const MatView& A, const uint32_t* headbits, int64_t C, int64_t T, uint16_t* dcol,
                        int32_t* head, int32_t* anchor, cudaStream_t s);
 void launch_d16_decode_export(const StreamPlan& sp, int32_t* out, cudaStream_t s);
-void launch_fixup(const int32_t* crow, const double* cval, int64_t T, double* y, int set, cudaStream_t s);
+// ordered carry fix-up (vector.cu); the carry arrays must hold fixup_capacity(T)
+// entries (levels of the hierarchical reduce-by-key live after the T carries)
+int64_t fixup_capacity(int64_t T);
+int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int64_t max_run, cudaStream_t s);
 void launch_rebase(void* rowptr, int rp_bytes, int64_t count, int64_t base, cudaStream_t s);
 
 // ---- length bins (bins.cu) ----------------------------------------------------
@@ -82,11 +107,18 @@ struct ExecArgs {
   double* y;
   int vs;
   int sm_count;
+  int64_t nnz_max;  // longest row (bounds the carry runs of the fix-ups)
   int stage;  // 0 = whole SpMV, 1 = main kernel(s) only, 2 = epilogue (fix-up) only
   // STREAM (sp[0]) / SPLIT bins (sp[0] short, sp[1] medium)
   StreamPlan sp[2];
   int n_sp;
   bool zero_y;  // SPLIT over compacted bins: y = 0 before the bin kernels
+  // NNZSPLIT (whole shard) / SPLIT short+medium rows as one nnz_split bin
+  NzPlan nz;
+  bool use_nz;
+  // SPLIT: long rows run on a side stream concurrently with the bins
+  cudaStream_t side;
+  cudaEvent_t ev_fork, ev_join;
   // MERGE
   int64_t items, Tm;
   const int32_t* mrow;
@@ -108,13 +140,14 @@ struct ExecArgs {
 constexpr int64_t kLongXB = 2048;  // columns per x block staged in smem by the column-tiled long-row kernel
 void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long, int64_t nblk, int64_t* seg,
                      cudaStream_t s);
-int launch_long_tiled(const ExecArgs& a, cudaStream_t s);
+void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s);
 
 int launch_vector(const ExecArgs& a, bool skip_long, cudaStream_t s);  // returns #launches
 int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int stage, cudaStream_t s);
 int launch_stream(const ExecArgs& a, cudaStream_t s);
 int launch_merge(const ExecArgs& a, cudaStream_t s);
 int launch_split(const ExecArgs& a, cudaStream_t s);
+int launch_nzsplit(const ExecArgs& a, cudaStream_t s);
 size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, int rows_cap, bool d16, bool seg);
 int stream_prepare(const StreamPlan& sp, int sm_count);  // smem attribute + persistent grid (<0 on error)
 void launch_chunk_export(const ExecArgs& a, int64_t* out, cudaStream_t s);  // [row|begin|end] x n_chunks

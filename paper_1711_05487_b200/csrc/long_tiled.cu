@@ -85,20 +85,15 @@ __global__ void __launch_bounds__(kNT) long_reduce_kernel(const double* __restri
   if (lane == 0) y[long_rows[q]] = a;
 }
 
-int launch_long_tiled(const ExecArgs& a, cudaStream_t s) {
-  int n = 0;
-  if (a.n_long == 0) return 0;
-  if (a.stage != 2) {
+// part 1: the column-tiled partials; part 2: the ordered per-row reduction
+void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s) {
+  if (a.n_long == 0) return;
+  if (part == 1)
     long_tiled_kernel<<<(int)a.nblk, kNT, 0, s>>>(a.A.col, a.A.val, a.x, a.n_long, a.A.n_cols, a.long_seg, a.nblk,
                                                   a.long_partial);
-    ++n;
-  }
-  if (a.stage != 1) {
+  else
     long_reduce_kernel<<<(int)((a.n_long * 32 + kNT - 1) / kNT), kNT, 0, s>>>(a.long_partial, a.n_long, a.nblk,
                                                                              a.long_rows, a.y);
-    ++n;
-  }
-  return n;
 }
 
 }  // namespace spmv

@@ -100,7 +100,7 @@ int launch_merge(const ExecArgs& a, cudaStream_t s) {
       merge_kernel<int32_t><<<(int)a.Tm, kNT, 0, s>>>((const int32_t*)a.A.rowptr, a.A.col, a.A.val, a.x, a.y, a.A.m,
                                                       a.mrow, a.mnnz, a.mcarry_row, a.mcarry_val);
   }
-  if (a.stage != 1) { launch_fixup(a.mcarry_row, a.mcarry_val, a.Tm, a.y, 0, s); ++n; }
+  if (a.stage != 1) n += launch_fixup(a.mcarry_row, a.mcarry_val, a.Tm, a.y, 0, a.nnz_max / 2048 + 2, s);
   return n;
 }
 

@@ -543,8 +543,7 @@ int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int sta
     ++n;
   }
   if (sp.need_fixup && stage != 1) {
-    launch_fixup(sp.carry_row, sp.carry_val, sp.T, y, 0, s);
-    ++n;
+    n += launch_fixup(sp.carry_row, sp.carry_val, sp.T, y, 0, sp.max_run, s);
   }
   return n;
 }

@@ -85,6 +85,26 @@ int launch_vector(const ExecArgs& a, bool skip_long, cudaStream_t s) {
 // consecutive entries k..k' with the same row r >= 0, in increasing k:
 // y[r] = (set ? 0 : y[r]) + (v_k + v_{k+1} + ... + v_k')
 // ============================================================================
+// ---- ordered carry fix-up ----------------------------------------------------
+// T carries (row, value) in tile order; a run of equal consecutive rows holds
+// the pieces of one row cut by tile edges. Each run is summed in order and
+// added to (set = 0) or stored in (set = 1) y[row]; rows < 0 are no carry.
+// Short runs (plan-time bound max_run <= 16): one thread per run start walks
+// it. Longer runs (long rows cut into many tiles): a hierarchical
+// reduce-by-key, 1024 carries per CTA (block segmented scan); runs cut by a
+// CTA edge are passed up as (head, tail) pieces to the next level, stored
+// after the T carries (fixup_capacity). Deterministic, no fp atomics.
+constexpr int64_t kFixItems = 1024;  // carries per CTA (256 threads x 4)
+
+int64_t fixup_capacity(int64_t T) {
+  int64_t tot = T, n = T;
+  while (n > kFixItems) {
+    n = 2 * ((n + kFixItems - 1) / kFixItems);
+    tot += n;
+  }
+  return tot > 1 ? tot : 1;
+}
+
 __global__ void __launch_bounds__(kNT) fixup_kernel(const int32_t* __restrict__ crow,
                                                     const double* __restrict__ cval, int64_t T,
                                                     double* __restrict__ y, int set) {
@@ -98,8 +118,138 @@ __global__ void __launch_bounds__(kNT) fixup_kernel(const int32_t* __restrict__ 
   y[r] = set ? s : y[r] + s;
 }
 
-void launch_fixup(const int32_t* crow, const double* cval, int64_t T, double* y, int set, cudaStream_t s) {
-  fixup_kernel<<<(int)((T + kNT - 1) / kNT), kNT, 0, s>>>(crow, cval, T, y, set);
+__global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restrict__ crow,
+                                                          const double* __restrict__ cval, int64_t n,
+                                                          double* __restrict__ y, int set,
+                                                          int32_t* __restrict__ orow, double* __restrict__ oval) {
+  __shared__ double wv[kNT / 32];
+  __shared__ int wf[kNT / 32];
+  __shared__ int64_t first_end;
+  const int64_t bs = (int64_t)blockIdx.x * kFixItems;
+  const int64_t be = (bs + kFixItems) < n ? (bs + kFixItems) : n;
+  const bool head_open = bs > 0 && crow[bs - 1] == crow[bs];
+  const bool tail_open = be < n && crow[be] == crow[be - 1];
+  if (threadIdx.x == 0) {
+    first_end = be - 1;
+    if (orow) {
+      orow[2 * blockIdx.x] = -1;
+      orow[2 * blockIdx.x + 1] = -1;
+      oval[2 * blockIdx.x] = 0.0;
+      oval[2 * blockIdx.x + 1] = 0.0;
+    }
+  }
+  __syncthreads();
+  const int64_t i0 = bs + 4 * (int64_t)threadIdx.x;
+  int32_t r[4];
+  double v[4], inc[4];
+  bool st[4], en[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t i = i0 + u;
+    const bool ok = i < be;
+    r[u] = ok ? crow[i] : INT32_MIN;
+    v[u] = ok ? cval[i] : 0.0;
+    st[u] = ok && (i == bs || crow[i - 1] != r[u]);
+    en[u] = ok && (i == be - 1 || crow[i + 1] != r[u]);
+    if (en[u] && i < be - 1) atomicMin((unsigned long long*)&first_end, (unsigned long long)i);
+  }
+  // thread-local segmented inclusive sums
+  double acc = 0.0;
+  bool any = false;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    acc = st[u] ? v[u] : acc + v[u];
+    any = any || st[u];
+    inc[u] = acc;
+  }
+  // block exclusive segmented scan of (acc, any) over threads
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double S = acc;
+  int f = any;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double su = __shfl_up_sync(0xffffffffu, S, o);
+    const int fu = __shfl_up_sync(0xffffffffu, f, o);
+    if (lane >= o) {
+      if (!f) S += su;
+      f |= fu;
+    }
+  }
+  if (lane == 31) {
+    wv[w] = S;
+    wf[w] = f;
+  }
+  __syncthreads();
+  double ex = __shfl_up_sync(0xffffffffu, S, 1);
+  int exf = __shfl_up_sync(0xffffffffu, f, 1);
+  if (lane == 0) {
+    ex = 0.0;
+    exf = 0;
+  }
+  // prefix from earlier warps (until a warp containing a run start)
+  if (!exf) {
+    double pre = 0.0;
+    for (int q = w - 1; q >= 0; --q) {
+      pre = wv[q] + pre;
+      if (wf[q]) break;
+    }
+    ex = pre + ex;
+  }
+  const int64_t e1 = first_end;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (!en[u] || r[u] < 0) continue;
+    const int64_t i = i0 + u;
+    // inclusive run sum at i: items of the run inside this thread + the prefix
+    // when the run started in an earlier thread
+    bool started_here = false;
+    for (int t = 0; t <= u; ++t) started_here = started_here || st[t];
+    const double sum = started_here ? inc[u] : ex + inc[u];
+    const bool in_first = i <= e1;  // the run holds item bs
+    if (i == be - 1 && tail_open) {
+      // continues into the next CTA; a run over the whole CTA fills both
+      // slots (sum, +0.0) so the next level sees it contiguous with its
+      // neighbours' pieces
+      const bool whole = in_first && head_open;
+      if (whole) {
+        orow[2 * blockIdx.x] = r[u];
+        oval[2 * blockIdx.x] = sum;
+      }
+      orow[2 * blockIdx.x + 1] = r[u];
+      oval[2 * blockIdx.x + 1] = whole ? 0.0 : sum;
+    } else if (in_first && head_open) {
+      orow[2 * blockIdx.x] = r[u];
+      oval[2 * blockIdx.x] = sum;
+    } else {
+      y[r[u]] = set ? sum : y[r[u]] + sum;
+    }
+  }
+}
+
+int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int64_t max_run, cudaStream_t s) {
+  if (T <= 0) return 0;
+  if (max_run <= 16) {
+    fixup_kernel<<<(int)((T + kNT - 1) / kNT), kNT, 0, s>>>(crow, cval, T, y, set);
+    return 1;
+  }
+  int launches = 0;
+  int64_t n = T;
+  int32_t* cr = crow;
+  double* cv = cval;
+  int64_t off = T;
+  for (;;) {
+    const int64_t nb = (n + kFixItems - 1) / kFixItems;
+    int32_t* orow = nb > 1 ? crow + off : nullptr;
+    double* oval = nb > 1 ? cval + off : nullptr;
+    fixup_level_kernel<<<(int)nb, kNT, 0, s>>>(cr, cv, n, y, set, orow, oval);
+    ++launches;
+    if (nb == 1) break;
+    cr = orow;
+    cv = oval;
+    n = 2 * nb;
+    off += n;
+  }
+  return launches;
 }
 
 // ============================================================================
@@ -183,29 +333,48 @@ __global__ void __launch_bounds__(kNT) long_chunk_kernel(const RP* __restrict__ 
 
 int launch_split(const ExecArgs& a, cudaStream_t s) {
   int n = 0;
-  // 0. rows in no bin (empty rows) must read 0: clear y once
-  if (a.zero_y && a.stage != 2 && a.A.m > 0) cudaMemsetAsync(a.y, 0, (size_t)a.A.m * 8, s);
-  // 1. short / medium bins: cta_stream over each compacted bin (rows mapped
-  //    back to y through the bin's row map); the bins own disjoint rows
-  for (int b = 0; b < a.n_sp; ++b) n += launch_stream_plan(a.sp[b], a.x, a.y, a.stage, s);
-  // 2. long rows: column-tiled (x blocks in smem) or nonzero chunks, then the
-  //    ordered per-row reduction (sets y)
-  if (a.long_tiled) return n + launch_long_tiled(a, s);
-  if (a.n_chunks > 0) {
-    if (a.stage != 2) {
-      ++n;
-      if (a.A.rp_bytes == 8)
-        long_chunk_kernel<int64_t><<<(int)a.n_chunks, kNT, 0, s>>>((const int64_t*)a.A.rowptr, a.A.col, a.A.val,
-                                                                   a.x, a.long_rows, a.chunk_start, a.n_long, a.chunk,
-                                                                   a.chunk_row, a.chunk_val);
-      else
-        long_chunk_kernel<int32_t><<<(int)a.n_chunks, kNT, 0, s>>>((const int32_t*)a.A.rowptr, a.A.col, a.A.val,
-                                                                   a.x, a.long_rows, a.chunk_start, a.n_long, a.chunk,
-                                                                   a.chunk_row, a.chunk_val);
-    }
-    if (a.stage != 1) { launch_fixup(a.chunk_row, a.chunk_val, a.n_chunks, a.y, 1, s); ++n; }
+  const bool longs = a.n_long > 0 && (a.long_tiled || a.n_chunks > 0);
+  // 0. legacy stream bins: rows in no bin (empty rows) must read 0
+  if (!a.use_nz && a.zero_y && a.stage != 2 && a.A.m > 0) cudaMemsetAsync(a.y, 0, (size_t)a.A.m * 8, s);
+  // 1. long rows (column-tiled x blocks or nonzero chunks) write per-chunk
+  //    partials only; they run on the side stream, concurrently with the
+  //    bins (gather-bound bins + stream-bound long rows overlap)
+  const bool conc = longs && a.side && a.stage != 2;
+  cudaStream_t ls = conc ? a.side : s;
+  if (conc) {
+    cudaEventRecord(a.ev_fork, s);
+    cudaStreamWaitEvent(a.side, a.ev_fork, 0);
+  }
+  if (longs && a.stage != 2) {
+    ++n;
+    if (a.long_tiled) launch_long_tiled(a, 1, ls);
+    else if (a.A.rp_bytes == 8)
+      long_chunk_kernel<int64_t><<<(int)a.n_chunks, kNT, 0, ls>>>((const int64_t*)a.A.rowptr, a.A.col, a.A.val,
+                                                                  a.x, a.long_rows, a.chunk_start, a.n_long, a.chunk,
+                                                                  a.chunk_row, a.chunk_val);
+    else
+      long_chunk_kernel<int32_t><<<(int)a.n_chunks, kNT, 0, ls>>>((const int32_t*)a.A.rowptr, a.A.col, a.A.val,
+                                                                  a.x, a.long_rows, a.chunk_start, a.n_long, a.chunk,
+                                                                  a.chunk_row, a.chunk_val);
+  }
+  if (conc) cudaEventRecord(a.ev_join, ls);
+  // 2. short / medium rows: one nnz_split bin, or cta_stream length bins
+  //    (rows mapped back to y through the bin's row map; disjoint rows)
+  if (a.use_nz) n += launch_nz_plan(a.nz, a.x, a.y, a.stage, s);
+  else
+    for (int b = 0; b < a.n_sp; ++b) n += launch_stream_plan(a.sp[b], a.x, a.y, a.stage, s);
+  if (conc) cudaStreamWaitEvent(s, a.ev_join, 0);
+  // 3. ordered per-row reduction of the long-row partials (sets y; after the
+  //    bins, whose gap zeroing may cover the long rows)
+  if (longs && a.stage != 1) {
+    ++n;
+    if (a.long_tiled) launch_long_tiled(a, 2, s);
+    else launch_fixup(a.chunk_row, a.chunk_val, a.n_chunks, a.y, 1, (a.nnz_max + a.chunk - 1) / a.chunk, s);
   }
   return n;
 }
+
+// NNZSPLIT: one nnz_split pass over the whole shard
+int launch_nzsplit(const ExecArgs& a, cudaStream_t s) { return launch_nz_plan(a.nz, a.x, a.y, a.stage, s); }
 
 }  // namespace spmv

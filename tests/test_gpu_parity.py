@@ -41,7 +41,8 @@ def m_maxlen(m):
 
 VARIANTS = [("vector", 1), ("vector", 2), ("vector", 8), ("vector", 32), ("stream", 1), ("stream", 4),
             ("stream", 8), ("stream", 32), ("stream_seg", 1), ("stream_nnz_tiles", 1), ("merge", 0), ("split", 4),
-    ("split_seg", 32), ("split_chunks", 16), ("split_tiled", 8)]
+    ("split_seg", 32), ("split_chunks", 16), ("split_tiled", 8), ("split_bins", 8), ("nnzsplit", 0)]
+ALL = ("vector", "stream", "merge", "split", "nnzsplit")
 
 SUITE = sg.small_suite(seed=21)
 
@@ -53,7 +54,9 @@ def variant_kw(variant):
     if variant == "stream_d16":
         return "stream", {"d16": 1}
     if variant == "split_seg":
-        return "split", {"seg": 1}
+        return "split", {"seg": 1, "split_bins": 0}
+    if variant == "split_bins":
+        return "split", {"split_bins": 0}
     if variant == "split_chunks":
         return "split", {"long_mode": 1}
     if variant == "split_tiled":
@@ -79,7 +82,7 @@ def test_small_suite_all_variants(name, m, variant, vs):
 def test_seg_mode_tiles(name, m, tile):
     for fv in ("stream", "split"):
         p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant=fv, seg=1, tile_nnz=tile,
-                      l_split=256)
+                      l_split=256, split_bins=0)
         assert p.info()["sel"]["seg"] == 1
         assert_bound(p.execute(m.x), m)
 
@@ -132,8 +135,15 @@ def test_plan_structures_bit_exact(name, m):
         assert np.array_equal(ps.export("chunk_begin"), cb)
         assert np.array_equal(ps.export("chunk_end"), ce)
         assert_bound(ps.execute(m.x), m)
+    # nnz_split structures (reading 19)
+    pz = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="nnzsplit")
+    rowmap, rpc = oracle.nonempty_rows(m.rowptr)
+    assert np.array_equal(pz.export("nz_rowmap"), rowmap)
+    assert np.array_equal(pz.export("nz_rpc"), rpc)
+    assert np.array_equal(pz.export("nz_tile_q"), oracle.nz_tiles(rpc) if m.nnz else np.array([0]))
+    assert pz.info()["n_nz_rows"] == rowmap.size - 1
     # features: exact integers, identical doubles (same formula, IEEE sqrt)
-    f = oracle.features(m.rowptr, m.colind)
+    f = oracle.features(m.rowptr, m.colind, n_cols=m.x.size)
     g = pm.info()["feat"]
     for k, v in f.items():
         assert g[k] == v, k
@@ -163,7 +173,7 @@ def test_validation_matches_oracle(rp, ci, n, nnz):
 def test_valid_edge_cases():
     # all-empty matrix, single row, zero rows
     for rp, ci, n in (([0, 0, 0, 0], [], 3), ([0, 1], [0], 1), ([0], [], 0)):
-        for v in ("vector", "stream", "merge", "split"):
+        for v in ALL:
             p = spmv.Plan(np.array(rp, np.int64), np.array(ci, np.int32), np.ones(len(ci)), n_cols=max(n, 1),
                           force_variant=v)
             y = p.execute(np.full(max(n, 1), 3.0), np.full(n, 7.0) if n else np.zeros(0))
@@ -186,10 +196,11 @@ def test_configs_full_auto_selection(c):
 
 
 @pytest.mark.parametrize("c", [2, 3, 4])
-@pytest.mark.parametrize("variant", ["vector", "stream", "merge", "split"])
+@pytest.mark.parametrize("variant", list(ALL) + ["split_bins"])
 def test_configs_full_forced_variants(c, variant):
+    variant, extra = variant_kw(variant)
     m = sg.config(c)
-    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=variant)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=variant, **extra)
     assert_bound(p.execute(m.x), m)
 
 
@@ -198,7 +209,7 @@ def test_stencil_ones_bit_exact():
     m = sg.config(2)
     ones = np.ones(m.n)
     ref = oracle.spmv(m.rowptr, m.colind, m.vals, ones)
-    for v in ("vector", "stream", "merge", "split"):
+    for v in ALL:
         for d16 in (0, 1):
             p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=v, d16=d16)
             assert np.array_equal(p.execute(ones), ref)
@@ -223,7 +234,7 @@ def test_device_and_host_buffers_agree():
 
 def test_deterministic_repeat():
     m = sg.config(3, small=True)
-    for v in ("vector", "stream", "merge", "split"):
+    for v in ALL:
         p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=v)
         y0 = p.execute(m.x)
         for _ in range(3):
@@ -231,7 +242,7 @@ def test_deterministic_repeat():
 
 
 @pytest.mark.parametrize("G", [2, 3, 8])
-@pytest.mark.parametrize("variant", ["vector", "stream", "merge", "split"])
+@pytest.mark.parametrize("variant", ALL)
 def test_emulated_shards(G, variant):
     m = sg.config(4, small=True)
     p1 = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=variant, force_vs=8)
@@ -292,3 +303,34 @@ def test_c5_full_sampled_rows_and_properties():
     for c in (i % n, (i // n) % n, i // (n * n)):
         prod *= 3 - (c == 0).astype(float) - (c == n - 1)
     assert np.array_equal(y1, 27.0 - prod)
+
+
+# nnz_split edge cases: rows ending exactly at warp-tile edges, a row spanning
+# many tiles, leading / trailing / interleaved empty rows, nnz < one tile,
+# nnz an exact multiple of the tile, int64 rowptr
+NZ_EDGE = [
+    ("tile_aligned_rows", [256] * 8),
+    ("row_ends_at_edge", [255, 1, 256, 0, 0, 512]),
+    ("one_row_many_tiles", [0, 0, 5000, 0]),
+    ("lead_trail_empty", [0] * 7 + [3, 0, 0, 300, 1] + [0] * 9),
+    ("tiny", [1, 0, 2]),
+    ("len1_mult", [1] * 512),
+    ("alternating", [0, 1] * 700 + [0, 257] * 3),
+    # runs of > 1024 carries: the hierarchical fix-up (two and three levels)
+    ("huge_rows", [3, 600000, 2, 0, 300000, 1]),
+    ("huge_adjacent", [270000, 270000, 1, 270000]),
+]
+
+
+@pytest.mark.parametrize("rp_dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("name,lens", NZ_EDGE, ids=[n for n, _ in NZ_EDGE])
+def test_nzsplit_edges(name, lens, rp_dtype):
+    g = np.random.default_rng(7)
+    lens = np.asarray(lens, np.int64)
+    m = sg.from_lengths(lens, max(int(lens.max()), lens.size), g, sg.MODE_U11, sg.MODE_U11)
+    rp = m.rowptr.astype(rp_dtype)
+    for fv, extra in (("nnzsplit", {}), ("split", {"l_split": 64})):
+        p = spmv.Plan(rp, m.colind, m.vals, n_cols=m.x.size, force_variant=fv, **extra)
+        y = p.execute(m.x, np.full(m.n, np.nan))
+        assert_bound(y, m)
+        assert np.all(y[lens == 0] == 0.0)

@@ -223,9 +223,9 @@ WIN = 128 * 2 ** 20
 
 
 def test_select_rule_table_on_closed_form_features():
-    def feat(n, nnz, avg_s, sd_s, n_empty=0, n_long=0, nnz_max=0, maxgap=0, misses=0):
+    def feat(n, nnz, avg_s, sd_s, n_empty=0, n_long=0, nnz_max=0, maxgap=0, misses=0, nnz_long=0):
         return dict(n=n, nnz=nnz, avg_short=avg_s, sd_short=sd_s, n_empty=n_empty, n_long=n_long,
-                    nnz_max=nnz_max, nnz_avg=nnz / n, maxgap=maxgap, misses=misses)
+                    nnz_max=nnz_max, nnz_avg=nnz / n, maxgap=maxgap, misses=misses, nnz_long=nnz_long, n_cols=n)
     S = oracle
     # C2: 7-pt 128^3 (closed forms above): regular, 217 MB > L2/2, maxgap 16384
     s = S.select(feat(2097152, 14581760, 6.953125, 0.2148, maxgap=16384, misses=8323072), L2, WIN, 4)
@@ -236,18 +236,24 @@ def test_select_rule_table_on_closed_form_features():
     # C1: 1.28 MB working set -> no MB, no D16
     s = S.select(feat(10000, 90000, 9.0, 0.0, maxgap=9000, misses=80000), L2, WIN, 4)
     assert (s.variant, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_STREAM, False, 0)
-    # C3-like: half the rows empty and long rows -> long_row_split (long rows first), IMB
+    # C3-like: half the rows empty, sparse long rows (11.4M nnz over 1794 rows of
+    # 4.2M columns: far below 64 per 2048-column block) -> nnz_split, IMB + ML
     s = S.select(feat(4194304, 65244537, 12.8, 78.5, n_empty=2185429, n_long=1794, nnz_max=97958,
-                      maxgap=4165791, misses=56437921), L2, WIN, 4)
-    assert s.variant == S.VARIANT_SPLIT and s.classes & S.CLASS_IMB and s.xwin and s.classes & S.CLASS_ML
-    # skew without long rows -> merge path
+                      maxgap=4165791, misses=56437921, nnz_long=11392466), L2, WIN, 4)
+    assert s.variant == S.VARIANT_NNZSPLIT and s.classes & S.CLASS_IMB and s.xwin and s.classes & S.CLASS_ML
+    # skew without long rows -> nnz_split
     s = S.select(feat(4194304, 20000000, 4.8, 9.0, n_empty=2185429, n_long=0, nnz_max=3000,
                       maxgap=4165791, misses=19000000), L2, WIN, 4)
-    assert s.variant == S.VARIANT_MERGE and s.classes & S.CLASS_IMB
-    # C4-like: long rows, regular short part -> split
+    assert s.variant == S.VARIANT_NNZSPLIT and s.classes & S.CLASS_IMB
+    # C4-like: 100 dense long rows (200,000 of 1M columns: ~410 per 2048-column
+    # block) -> long_row_split (column-tiled long rows + nnz_split bin)
     s = S.select(feat(1000000, 34998500, 15.0, 0.0, n_long=100, nnz_max=200000, maxgap=900000,
-                      misses=34000000), L2, WIN, 4)
+                      misses=34000000, nnz_long=20000000), L2, WIN, 4)
     assert (s.variant, s.vs) == (S.VARIANT_SPLIT, 16) and s.classes & S.CLASS_IMB
+    # the same long rows 10x sparser (41 per block) -> nnz_split
+    s = S.select(feat(1000000, 16998500, 15.0, 0.0, n_long=100, nnz_max=20000, maxgap=900000,
+                      misses=16000000, nnz_long=2000000), L2, WIN, 4)
+    assert s.variant == S.VARIANT_NNZSPLIT
     # medium regular rows -> csr_vector with VS = pow2ceil(avg)
     s = S.select(feat(100000, 4000000, 40.0, 2.0, maxgap=10), L2, WIN, 4)
     assert (s.variant, s.vs) == (S.VARIANT_VECTOR, 32)
@@ -275,3 +281,39 @@ def test_algorithmic_bytes_configs():
     assert oracle.algorithmic_bytes(2097152, 14581760, 4) == 216924164
     assert oracle.algorithmic_bytes(1000000, 34998500, 4) == 439982004
     assert oracle.algorithmic_bytes(56623104, 1520875000, 8) == 19609454504
+
+
+# ---- nnz_split structures (reading 19) ---------------------------------
+def test_nonempty_rows_and_nz_tiles_hand_example():
+    # lengths [0, 3, 0, 0, 1, 300, 0, 2]: non-empty rows 1, 4, 5, 7
+    lens = np.array([0, 3, 0, 0, 1, 300, 0, 2])
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    rowmap, rpc = oracle.nonempty_rows(rp)
+    assert rowmap.tolist() == [1, 4, 5, 7, 8] and rpc.tolist() == [0, 3, 4, 304, 306]
+    # nonzero 256 lies in row 5 (q = 2), so tile 1 starts inside it
+    assert oracle.nz_tiles(rpc).tolist() == [0, 2, 4]
+    assert oracle.nz_tiles(rpc, W=4).tolist()[:3] == [0, 2, 2]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_nz_structures_rederived(seed):
+    g = np.random.default_rng(seed)
+    n = int(g.integers(1, 3000))
+    lens = g.integers(0, 40, n) * (g.random(n) < 0.6)
+    lens[g.integers(0, n, 3)] = g.integers(0, 2000, 3)
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    rowmap, rpc = oracle.nonempty_rows(rp)
+    nz = np.flatnonzero(lens > 0)
+    assert np.array_equal(rowmap[:-1], nz) and rowmap[-1] == n
+    assert np.array_equal(rpc[:-1], rp[nz]) and rpc[-1] == rp[-1]
+    for W in (256, 7):
+        tq = oracle.nz_tiles(rpc, W)
+        T = -(-int(rp[-1]) // W)
+        assert tq.size == T + 1 and tq[-1] == rpc.size - 1
+        k = np.arange(T)
+        # searchsorted re-derivation: last q with rpc[q] <= k*W
+        assert np.array_equal(tq[:-1], np.searchsorted(rpc, k * W, side="right") - 1)
+        # ownership: nonzero k*W lies in row rowmap[tq[k]]
+        for kk in k[:: max(1, T // 50)]:
+            q = tq[kk]
+            assert rpc[q] <= kk * W < rpc[q + 1]
