@@ -123,6 +123,7 @@ struct Shard {
   int64_t nblk = 0;
   int64_t* long_seg = nullptr;
   double* long_partial = nullptr;
+  int long_grid = 0;
   // NNZSPLIT (whole shard) / SPLIT short+medium rows as one nnz_split bin
   NzPlan nz;
   bool use_nz = false;
@@ -210,6 +211,7 @@ struct spmv_plan_s {
     a.nblk = s.nblk;
     a.long_seg = s.long_seg;
     a.long_partial = s.long_partial;
+    a.long_grid = s.long_grid;
     a.nz = s.nz;
     a.use_nz = s.use_nz;
     a.side = s.side;
@@ -615,7 +617,8 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   };
   // nnz_split pass over the view V (colind/values) restricted to the
   // non-empty rows rowmap[0..mc) with rowptr rpc; y rows [0, s.m)
-  auto build_nz = [&](Shard& s, NzPlan& z, const MatView& V, const void* rpc, int32_t* rowmap, int64_t mc) {
+  auto build_nz = [&](Shard& s, NzPlan& z, const MatView& V, const void* rpc, int32_t* rowmap, int64_t mc,
+                      int64_t maxlen) {
     z.V = V;
     z.rpc = rpc;
     z.rowmap = rowmap;
@@ -626,7 +629,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     z.tile_q = s.alloc<int32_t>((size_t)z.T + 1);
     z.carry_row = s.alloc<int32_t>((size_t)fixup_capacity(z.T));
     z.carry_val = s.alloc<double>((size_t)fixup_capacity(z.T));
-    z.max_run = P->feat.nnz_max / kNzTile + 2;
+    z.max_run = maxlen / kNzTile + 2;
+    z.sched = s.alloc<unsigned long long>(2);
+    ck(cudaMemsetAsync(z.sched, 0, 16, s.stream), "memset");
     launch_nz_tiles(z, s.stream);
     count_launches(2, "nz tiles");
     z.grid = nz_prepare(z, s.sm_count);
@@ -661,7 +666,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     launch_gather_rowptr(frp, rp_bytes, rows, nrows, s.m, brp, s.stream);
     count_launches(1, "bin gather");
     if (nz) {
-      build_nz(s, *nz, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, brp, rows, nrows);
+      build_nz(s, *nz, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, brp, rows, nrows,
+               hi >= P->l_split ? P->feat.max_short : std::min<int64_t>(hi, P->feat.nnz_max));
+      nz->skip_rp = A.rowptr;
       return true;
     }
     build_stream(s, sp, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, rows, false, vs, seg,
@@ -703,7 +710,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       } else {
         ck(cudaMemsetAsync(rpc, 0, rp_bytes, s.stream), "memset");
       }
-      build_nz(s, s.nz, A, rpc, rows, mc);
+      build_nz(s, s.nz, A, rpc, rows, mc, P->feat.nnz_max);
       s.use_nz = true;
     } else if (P->sel.variant == SPMV_VARIANT_SPLIT) {
       // decomposition by row length (Fig. 6 read through S:120-125):
@@ -724,6 +731,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
           s.nz = NzPlan{};
           s.nz.m_out = s.m;
           s.nz.zero_gaps = true;
+          s.nz.skip_rp = A.rowptr;  // T == 0: launch_split clears y before the long rows
         }
       } else {
         if (build_bin(s, s.sp[s.n_sp], A, 1, ts, 1, seg, scan)) ++s.n_sp;
@@ -756,6 +764,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
           s.long_partial = s.alloc<double>((size_t)s.n_long * nblk);
           launch_long_seg(A, s.long_rows, s.n_long, nblk, s.long_seg, s.stream);
           count_launches(1, "long_seg");
+          int per_sm = 0;
+          if (const char* e = getenv("SPMV_LONG_CTAS")) per_sm = atoi(e);
+          s.long_grid = long_tiled_grid(nblk, s.sm_count, per_sm);
         }
         // the long rows run on a side stream, concurrently with the bins
         ck(cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking), "cudaStreamCreate");

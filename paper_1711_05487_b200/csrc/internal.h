@@ -65,10 +65,16 @@ struct NzPlan {
   int64_t mc = 0, T = 0, m_out = 0;
   int grid = 0;
   int64_t max_run = 1;    // longest run of equal carry rows (fix-up choice)
+  bool tma = false;       // streams by TMA bulk copies (else LDG.256 through L1)
+  unsigned long long* sched = nullptr;  // dynamic tile scheduling counters [2], zero between launches
+  bool dynamic = false;   // tickets (else static round-robin chunks)
+  int64_t chunk = 1;      // tiles per ticket / round-robin chunk
   bool zero_gaps = true;  // write y = 0 for the rows of [0, m_out) not in rowmap
+  const void* skip_rp = nullptr;  // SPLIT: zero only the gap rows empty in this rowptr (long rows are written
+                                  // concurrently by the long-row reduction)
 };
 void launch_nz_tiles(const NzPlan& z, cudaStream_t s);  // tile_q and rowmap[mc] = m_out
-int nz_prepare(const NzPlan& z, int sm_count);         // persistent grid (<0 on error)
+int nz_prepare(NzPlan& z, int sm_count);  // picks the stream mode, returns the persistent grid (<0 on error)
 int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaStream_t s);
 
 // ---- inspector ------------------------------------------------------------
@@ -135,12 +141,14 @@ struct ExecArgs {
   int64_t nblk;               // x blocks of kLongXB columns
   const int64_t* long_seg;    // [n_long][nblk+1] segment starts
   double* long_partial;       // [n_long][nblk]
+  int long_grid;              // persistent grid of the column-tiled kernel
 };
 
 constexpr int64_t kLongXB = 2048;  // columns per x block staged in smem by the column-tiled long-row kernel
 void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long, int64_t nblk, int64_t* seg,
                      cudaStream_t s);
 void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s);
+int long_tiled_grid(int64_t nblk, int sm_count, int per_sm);
 
 int launch_vector(const ExecArgs& a, bool skip_long, cudaStream_t s);  // returns #launches
 int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int stage, cudaStream_t s);

@@ -15,6 +15,8 @@
 
 namespace spmv {
 
+constexpr int kLongRG = 2;  // row groups per x block (CTAs per block)
+
 // seg[q*(nblk+1) + b] = first nonzero of long row q with column >= b*XB
 template <typename RP>
 __global__ void long_seg_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ col,
@@ -43,32 +45,71 @@ void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long,
     long_seg_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, long_rows, n_long, nblk, seg);
 }
 
+__device__ __forceinline__ void lt_ld256_s32(const int32_t* p, int (&c)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.s32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void lt_ld256_f64(const double* p, double* v) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+
+// CTA (b, g): x block b staged in smem, long rows q = g, g + RG, ... of it.
+// A warp streams a segment [s0, s1) in 8-aligned groups of 8 nonzeros per
+// lane (one 256-bit colind load + two 256-bit value loads, 16 nonzeros per
+// lane in flight), masking the group edges outside the segment.
 __global__ void __launch_bounds__(kNT) long_tiled_kernel(const int32_t* __restrict__ col,
                                                          const double* __restrict__ val, const double* __restrict__ x,
                                                          int64_t n_long, int64_t n_cols, const int64_t* __restrict__ seg,
-                                                         int64_t nblk, double* __restrict__ partial) {
+                                                         int64_t nblk, int rg, double* __restrict__ partial) {
   __shared__ double xs[kLongXB];
-  const int64_t b = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // persistent: work item (b, g) = it / rg, it % rg, round-robin over CTAs
+  for (int64_t it = blockIdx.x; it < nblk * rg; it += gridDim.x) {
+  const int64_t b = it / rg, g = it % rg;
   const int64_t c0 = b * kLongXB;
   const int cw = (int)((n_cols - c0) < kLongXB ? (n_cols - c0) : kLongXB);
+  __syncthreads();  // previous item's readers are done with xs
   for (int i = threadIdx.x; i < cw; i += kNT) xs[i] = ld_x(x + c0 + i);
   __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t q = w; q < n_long; q += kNT / 32) {
+  for (int64_t q = g + (int64_t)rg * w; q < n_long; q += (int64_t)rg * (kNT / 32)) {
     const int64_t s0 = ld_ro(seg + q * (nblk + 1) + b), s1 = ld_ro(seg + q * (nblk + 1) + b + 1);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int64_t j = s0 + lane;
-    for (; j + 96 < s1; j += 128) {
-      const int k0 = ld_stream(col + j) - (int)c0, k1 = ld_stream(col + j + 32) - (int)c0,
-                k2 = ld_stream(col + j + 64) - (int)c0, k3 = ld_stream(col + j + 96) - (int)c0;
-      a0 = fma(ld_stream(val + j), xs[k0], a0);
-      a1 = fma(ld_stream(val + j + 32), xs[k1], a1);
-      a2 = fma(ld_stream(val + j + 64), xs[k2], a2);
-      a3 = fma(ld_stream(val + j + 96), xs[k3], a3);
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t base = s0 & ~7ll; base < s1; base += 512) {
+      int c[2][8];
+      double v[2][8];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int64_t e = base + 256 * r + 8 * lane;
+        if (e < s1) {
+          lt_ld256_s32(col + e, c[r]);
+          lt_ld256_f64(val + e, v[r]);
+          lt_ld256_f64(val + e + 4, v[r] + 4);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            c[r][i] = (int)c0;
+            v[r][i] = 0.0;
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int64_t e = base + 256 * r + 8 * lane;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const bool in = e + i >= s0 && e + i < s1;
+          const double t = v[r][i] * xs[in ? c[r][i] - (int)c0 : 0];
+          if (i & 1) a1 += in ? t : 0.0;
+          else a0 += in ? t : 0.0;
+        }
+      }
     }
-    for (; j < s1; j += 32) a0 = fma(ld_stream(val + j), xs[ld_stream(col + j) - (int)c0], a0);
-    const double t = warp_sum((a0 + a1) + (a2 + a3));
+    const double t = warp_sum(a0 + a1);
     if (lane == 0) partial[q * nblk + b] = t;
+  }
   }
 }
 
@@ -86,11 +127,19 @@ __global__ void __launch_bounds__(kNT) long_reduce_kernel(const double* __restri
 }
 
 // part 1: the column-tiled partials; part 2: the ordered per-row reduction
+// persistent grid: per_sm CTAs per SM (<= 0: one CTA per work item)
+int long_tiled_grid(int64_t nblk, int sm_count, int per_sm) {
+  const int64_t items = nblk * kLongRG;
+  if (per_sm <= 0) return (int)items;
+  const int64_t g = (int64_t)sm_count * per_sm;
+  return (int)(g < items ? g : items);
+}
+
 void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s) {
   if (a.n_long == 0) return;
   if (part == 1)
-    long_tiled_kernel<<<(int)a.nblk, kNT, 0, s>>>(a.A.col, a.A.val, a.x, a.n_long, a.A.n_cols, a.long_seg, a.nblk,
-                                                  a.long_partial);
+    long_tiled_kernel<<<a.long_grid, kNT, 0, s>>>(a.A.col, a.A.val, a.x, a.n_long, a.A.n_cols, a.long_seg, a.nblk,
+                                                  kLongRG, a.long_partial);
   else
     long_reduce_kernel<<<(int)((a.n_long * 32 + kNT - 1) / kNT), kNT, 0, s>>>(a.long_partial, a.n_long, a.nblk,
                                                                              a.long_rows, a.y);

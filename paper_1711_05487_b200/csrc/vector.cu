@@ -334,12 +334,15 @@ __global__ void __launch_bounds__(kNT) long_chunk_kernel(const RP* __restrict__ 
 int launch_split(const ExecArgs& a, cudaStream_t s) {
   int n = 0;
   const bool longs = a.n_long > 0 && (a.long_tiled || a.n_chunks > 0);
-  // 0. legacy stream bins: rows in no bin (empty rows) must read 0
-  if (!a.use_nz && a.zero_y && a.stage != 2 && a.A.m > 0) cudaMemsetAsync(a.y, 0, (size_t)a.A.m * 8, s);
-  // 1. long rows (column-tiled x blocks or nonzero chunks) write per-chunk
-  //    partials only; they run on the side stream, concurrently with the
-  //    bins (gather-bound bins + stream-bound long rows overlap)
-  const bool conc = longs && a.side && a.stage != 2;
+  // 0. rows in no bin must read 0: legacy stream bins (empty rows), or an
+  //    nnz_split bin without nonzeros
+  if (a.stage != 2 && a.A.m > 0 && ((!a.use_nz && a.zero_y) || (a.use_nz && a.nz.T == 0)))
+    cudaMemsetAsync(a.y, 0, (size_t)a.A.m * 8, s);
+  // 1. long rows (column-tiled x blocks or nonzero chunks) and their ordered
+  //    per-row reduction run on the side stream, concurrently with the bins
+  //    (gather-bound bins + stream-bound long rows overlap); the bins never
+  //    write the long rows' y
+  const bool conc = longs && a.side;
   cudaStream_t ls = conc ? a.side : s;
   if (conc) {
     cudaEventRecord(a.ev_fork, s);
@@ -357,6 +360,14 @@ int launch_split(const ExecArgs& a, cudaStream_t s) {
                                                                   a.x, a.long_rows, a.chunk_start, a.n_long, a.chunk,
                                                                   a.chunk_row, a.chunk_val);
   }
+  if (longs && a.stage != 1) {
+    if (a.long_tiled) {
+      launch_long_tiled(a, 2, ls);
+      ++n;
+    } else {
+      n += launch_fixup(a.chunk_row, a.chunk_val, a.n_chunks, a.y, 1, (a.nnz_max + a.chunk - 1) / a.chunk, ls);
+    }
+  }
   if (conc) cudaEventRecord(a.ev_join, ls);
   // 2. short / medium rows: one nnz_split bin, or cta_stream length bins
   //    (rows mapped back to y through the bin's row map; disjoint rows)
@@ -364,13 +375,6 @@ int launch_split(const ExecArgs& a, cudaStream_t s) {
   else
     for (int b = 0; b < a.n_sp; ++b) n += launch_stream_plan(a.sp[b], a.x, a.y, a.stage, s);
   if (conc) cudaStreamWaitEvent(s, a.ev_join, 0);
-  // 3. ordered per-row reduction of the long-row partials (sets y; after the
-  //    bins, whose gap zeroing may cover the long rows)
-  if (longs && a.stage != 1) {
-    ++n;
-    if (a.long_tiled) launch_long_tiled(a, 2, s);
-    else launch_fixup(a.chunk_row, a.chunk_val, a.n_chunks, a.y, 1, (a.nnz_max + a.chunk - 1) / a.chunk, s);
-  }
   return n;
 }
 

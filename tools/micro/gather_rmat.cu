@@ -12,9 +12,13 @@ __device__ __forceinline__ int ld_na(const int* p) { int v; asm volatile("ld.glo
 __device__ __forceinline__ double ld_na(const double* p) { double v; asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p)); return v; }
 __device__ __forceinline__ double ld_cg(const double* p) { double v; asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p)); return v; }
 
+__device__ __forceinline__ double ld_nax(const double* p) { double v; asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p)); return v; }
+__device__ __forceinline__ double ld_el(const double* p) { double v; asm volatile("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p)); return v; }
+__device__ int g_hot;
 template <int MODE>
 __global__ void __launch_bounds__(256) kern(const int* __restrict__ idx, const double* __restrict__ val,
                                             const double* __restrict__ x, int64_t n, double* out) {
+  const int H = g_hot;
   extern __shared__ double dummy[];
   double acc = 0.0;
   // contiguous chunk per warp (like a row-block kernel): warp w owns [w*CH, (w+1)*CH)
@@ -29,7 +33,7 @@ __global__ void __launch_bounds__(256) kern(const int* __restrict__ idx, const d
 #pragma unroll
     for (int u = 0; u < 8; ++u) { c[u] = ld_na(idx + i + u * 32); v[u] = ld_na(val + i + u * 32); }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) xv[u] = MODE == 0 ? __ldg(x + c[u]) : ld_cg(x + c[u]);
+    for (int u = 0; u < 8; ++u) xv[u] = MODE == 0 ? __ldg(x + c[u]) : MODE == 1 ? ld_cg(x + c[u]) : MODE == 2 ? (c[u] < H ? __ldg(x + c[u]) : ld_nax(x + c[u])) : (c[u] < H ? ld_el(x + c[u]) : ld_nax(x + c[u]));
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc = fma(v[u], xv[u], acc);
   }
@@ -71,28 +75,39 @@ int main() {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   cudaFuncSetAttribute(kern<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(kern<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(kern<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(kern<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   for (int p = 0; p < 2; ++p) {
     cudaMemcpy(idx, p ? hp.data() : h.data(), E * 4, cudaMemcpyHostToDevice);
-    for (int mode = 0; mode < 2; ++mode)
-      for (int smemkb : {0, 24, 96, 180}) {
-        int occ = 8;
-        int grid = sms * occ;
-        size_t sm = (size_t)smemkb * 1024 / occ;
-        int carve = smemkb == 0 ? 0 : (smemkb * 100 + 227) / 228;
-        if (carve > 100) carve = 100;
-        cudaFuncSetAttribute(kern<0>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-        cudaFuncSetAttribute(kern<1>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-        auto run = [&]() {
-          if (mode == 0) kern<0><<<grid, 256, sm>>>(idx, val, x, E, out);
-          else kern<1><<<grid, 256, sm>>>(idx, val, x, E, out);
-        };
-        run(); run();
-        cudaEventRecord(a);
-        for (int r = 0; r < 10; ++r) run();
-        cudaEventRecord(b); cudaEventSynchronize(b);
-        float ms; cudaEventElapsedTime(&ms, a, b); ms /= 10;
-        printf("%s mode=%s smem/SM=%3d KB: %8.1f us  %7.1f Ggather/s\n", p ? "hot-perm" : "natural ",
-               mode == 0 ? "L1" : "L2", smemkb, ms * 1e3, E / (ms * 1e-3) / 1e9);
+    for (int mode = 0; mode < 4; ++mode)
+      for (int H : {4096, 16384, 65536, 262144}) {
+        if (mode < 2 && H != 4096) continue;
+        if (mode >= 2 && !p) continue;
+        cudaMemcpyToSymbol(g_hot, &H, 4);
+        for (int smemkb : {0, 96}) {
+          int occ = 8;
+          int grid = sms * occ;
+          size_t sm = (size_t)smemkb * 1024 / occ;
+          int carve = smemkb == 0 ? 0 : (smemkb * 100 + 227) / 228;
+          cudaFuncSetAttribute(kern<0>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+          cudaFuncSetAttribute(kern<1>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+          cudaFuncSetAttribute(kern<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+          cudaFuncSetAttribute(kern<3>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+          auto run = [&]() {
+            if (mode == 0) kern<0><<<grid, 256, sm>>>(idx, val, x, E, out);
+            else if (mode == 1) kern<1><<<grid, 256, sm>>>(idx, val, x, E, out);
+            else if (mode == 2) kern<2><<<grid, 256, sm>>>(idx, val, x, E, out);
+            else kern<3><<<grid, 256, sm>>>(idx, val, x, E, out);
+          };
+          run(); run();
+          cudaEventRecord(a);
+          for (int r = 0; r < 10; ++r) run();
+          cudaEventRecord(b); cudaEventSynchronize(b);
+          float ms; cudaEventElapsedTime(&ms, a, b); ms /= 10;
+          const char* mn[] = {"L1", "L2", "hot-ldg/cold-na", "hot-evl/cold-na"};
+          printf("%s mode=%-16s H=%6d smem/SM=%3d KB: %8.1f us  %7.1f Ggather/s\n", p ? "hot-perm" : "natural ",
+                 mn[mode], H, smemkb, ms * 1e3, E / (ms * 1e-3) / 1e9);
+        }
       }
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
