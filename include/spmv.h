@@ -77,7 +77,9 @@ typedef struct spmv_options {
   int32_t seg;             /* STREAM / SPLIT short part, segmented consumer mode: -1 auto, 0 off, 1 on */
   int32_t long_mode;       /* SPLIT long rows: 0 auto, 1 nonzero chunks, 2 column-tiled (x block in smem) */
   int32_t split_bins;      /* SPLIT non-long rows: -1 auto (one nnz_split bin), 0 cta_stream length bins, 1 nnz_split bin */
-  int32_t reserved[3];     /* reserved[0] = 1 disables row-aligned tiles (tests) */
+  int32_t hot_x;           /* NNZSPLIT hot-x table in smem: -1 auto (top columns cover >= 20 % of nnz), 0 off,
+                              K > 0 = force, at most K (<= 16384) columns */
+  int32_t reserved[2];     /* reserved[0] = 1 disables row-aligned tiles (tests) */
 } spmv_options;
 
 /* Theta(N) features (Table I) + counts used by the selection.
@@ -128,6 +130,8 @@ typedef struct spmv_plan_info {
   int32_t pad2_;
   int64_t n_nz_rows;          /* nnz_split: non-empty rows of the pass (mc) */
   int64_t n_nz_tiles;         /* nnz_split: warp tiles of 256 nonzeros */
+  int64_t n_hot;              /* nnz_split: hot columns served from shared memory (0 = off) */
+  double hot_cover;           /* fraction of nonzeros in the (candidate) hot columns */
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */
@@ -213,7 +217,8 @@ enum {
   SPMV_ARR_SHARD_BOUNDS = 11, /* int64[ngpus+1] */
   SPMV_ARR_NZ_ROWMAP = 12,    /* int64[mc+1]: nnz_split non-empty rows (y row ids), rowmap[mc] = n_rows */
   SPMV_ARR_NZ_RPC = 13,       /* int64[mc+1]: their rowptr (rpc[q] = rowptr[rowmap[q]], rpc[mc] = nnz) */
-  SPMV_ARR_NZ_TILE_Q = 14     /* int64[n_nz_tiles+1]: tile_q[k] = last q with rpc[q] <= 256k; tile_q[T] = mc */
+  SPMV_ARR_NZ_TILE_Q = 14,    /* int64[n_nz_tiles+1]: tile_q[k] = last q with rpc[q] <= 256k; tile_q[T] = mc */
+  SPMV_ARR_NZ_HOT_COLS = 15   /* int64[n_hot]: hot columns in column order (reading 20) */
 };
 int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst);
 

@@ -24,6 +24,7 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``) -- no function is
   long_chunks     coverage / exact tiling of long rows
   nonempty_rows   numpy flatnonzero of the row lengths, coverage
   nz_tiles        binary-search (searchsorted) re-derivation, ownership cover
+  hot_columns     hand example, maximality of the count threshold
   d16 encode/dec  SPEC S:134-136 widths, round trip, stencil gap closed forms
   features        SPEC S:415 sd example, stencil closed forms
   select          hand-evaluated rule table on the configs' closed-form features
@@ -233,6 +234,29 @@ def nz_tiles(rpc, W=NZ_TILE):
     tq = np.empty(T + 1, np.int64)
     _lib().oracle_nz_tiles(mc, _p(rpc), int(W), T, _p(tq))
     return tq
+
+
+HOT_BUCKETS = 4096
+
+
+def hot_columns(colind, n_cols, K, buckets=HOT_BUCKETS):
+    """nnz_split hot-x set (reading 20): column counts cnt, count
+    histogram H[min(cnt, buckets-1)]; t = the smallest count >= 1 such that the
+    columns with cnt >= t number <= K (the top bucket is taken whole); the hot
+    columns are those with cnt >= t in column order, the first min(#, K)
+    rounded down to even. Returns (hot columns, coverage = their nonzeros)."""
+    cnt = np.bincount(np.asarray(colind, np.int64), minlength=int(n_cols))
+    H = np.bincount(np.minimum(cnt, buckets - 1), minlength=buckets)
+    acc, t = 0, buckets - 1
+    for v in range(buckets - 1, 0, -1):
+        if v < buckets - 1 and acc + H[v] > K:
+            break
+        acc += int(H[v])
+        t = v
+    hot = np.flatnonzero(cnt >= t)
+    k2 = min(hot.size, K) & ~1
+    hot = hot[:k2]
+    return hot, int(cnt[hot].sum())
 
 
 def merge_splits(rowptr, items):

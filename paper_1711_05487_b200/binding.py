@@ -22,9 +22,10 @@ VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 CLASSES = {"MB": 1, "ML": 2, "IMB": 4, "CMP": 8}
 ARR = {"tile_rows": 1, "merge_rows": 2, "merge_nnz": 3, "chunk_row": 4, "chunk_begin": 5, "chunk_end": 6,
        "dcol": 7, "head": 8, "anchor": 9, "decoded": 10, "shard_bounds": 11, "nz_rowmap": 12, "nz_rpc": 13,
-       "nz_tile_q": 14}
+       "nz_tile_q": 14, "nz_hot_cols": 15}
 _ARR_DTYPE = {1: np.int64, 2: np.int64, 3: np.int64, 4: np.int64, 5: np.int64, 6: np.int64, 7: np.uint16,
-              8: np.int32, 9: np.int32, 10: np.int32, 11: np.int64, 12: np.int64, 13: np.int64, 14: np.int64}
+              8: np.int32, 9: np.int32, 10: np.int32, 11: np.int64, 12: np.int64, 13: np.int64, 14: np.int64,
+              15: np.int64}
 
 
 class Options(ctypes.Structure):
@@ -33,7 +34,8 @@ class Options(ctypes.Structure):
                 ("l_split", ctypes.c_int64), ("k_long", ctypes.c_int64), ("tile_nnz", ctypes.c_int64),
                 ("merge_items", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
                 ("emulate_devices", ctypes.c_int32), ("stages", ctypes.c_int32), ("seg", ctypes.c_int32),
-                ("long_mode", ctypes.c_int32), ("split_bins", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("long_mode", ctypes.c_int32), ("split_bins", ctypes.c_int32), ("hot_x", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
     @classmethod
     def make(cls, **kw):
@@ -79,7 +81,7 @@ class PlanInfo(ctypes.Structure):
                 ("select_ms", ctypes.c_double), ("encode_ms", ctypes.c_double), ("device_bytes", ctypes.c_int64),
                 ("shard_bounds", ctypes.c_int64 * 9), ("tile_stride", ctypes.c_int64),
                 ("tiles_row_aligned", ctypes.c_int32), ("pad2_", ctypes.c_int32), ("n_nz_rows", ctypes.c_int64),
-                ("n_nz_tiles", ctypes.c_int64)]
+                ("n_nz_tiles", ctypes.c_int64), ("n_hot", ctypes.c_int64), ("hot_cover", ctypes.c_double)]
 
 
 _vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double

@@ -124,6 +124,7 @@ struct Shard {
   int64_t* long_seg = nullptr;
   double* long_partial = nullptr;
   int long_grid = 0;
+  bool split_fused = true;
   // NNZSPLIT (whole shard) / SPLIT short+medium rows as one nnz_split bin
   NzPlan nz;
   bool use_nz = false;
@@ -177,6 +178,7 @@ struct spmv_plan_s {
   std::vector<int64_t> bounds;
   double upload_ms = 0, inspect_ms = 0, select_ms = 0, encode_ms = 0;
   int64_t l_split = 4096, k_long = 100, C = 2048, items = 2048, chunk = 8192;
+  double hot_cover = 0.0;  // nnz_split hot-x set: fraction of nonzeros in the hot columns
 
   ~spmv_plan_s() {
     for (auto& s : shards) s.release();
@@ -212,6 +214,7 @@ struct spmv_plan_s {
     a.long_seg = s.long_seg;
     a.long_partial = s.long_partial;
     a.long_grid = s.long_grid;
+    a.split_fused = s.split_fused;
     a.nz = s.nz;
     a.use_nz = s.use_nz;
     a.side = s.side;
@@ -314,6 +317,7 @@ void validate_options(const spmv_options& o) {
     fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
   if (o.l_split < 0 || o.k_long < 0) fail(SPMV_E_ARG, "negative l_split / k_long");
   if (o.long_mode < 0 || o.long_mode > 2) fail(SPMV_E_ARG, "long_mode must be 0, 1 or 2");
+  if (o.hot_x < -1) fail(SPMV_E_ARG, "hot_x must be -1 (auto), 0 (off) or a column count");
   if (o.split_bins < -1 || o.split_bins > 1) fail(SPMV_E_ARG, "split_bins must be -1, 0 or 1");
   if (o.stages < 0 || o.stages > 32 || o.stages % kStreamConsumerWarps)
     fail(SPMV_E_ARG, "stages must be 0 (auto) or a multiple of %d up to 32", kStreamConsumerWarps);
@@ -394,6 +398,15 @@ const char* csr_code_name(int code) {
 [[noreturn]] void fail_csr(int code, int64_t where) {
   fail(SPMV_E_CSR, "invalid CSR: code %d (%s) at %s %lld", code, csr_code_name(code),
        code <= 3 ? "row" : "nonzero", (long long)where);
+}
+
+// ordered-carry arrays: fixup_capacity(T) entries (hierarchical levels) plus
+// the zeroed level counter the fix-up's last CTA uses
+void alloc_carries(Shard& s, int64_t T, int32_t*& row, double*& val) {
+  const int64_t cap = fixup_capacity(T);
+  row = s.alloc<int32_t>((size_t)cap + 2);
+  val = s.alloc<double>((size_t)cap);
+  ck(cudaMemsetAsync(row + cap, 0, 8, s.stream), "memset");
 }
 
 // ---------------------------------------------------------------------------
@@ -575,8 +588,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     sp.rows_cap = (int)std::min<double>((double)sp.C + 32, 1.5 * rpt + 32);
     if (const char* e = getenv("SPMV_ROWS_CAP")) sp.rows_cap = atoi(e);  // tuning knob
     sp.tile_row = s.alloc<int32_t>((size_t)sp.T + 1);
-    sp.carry_row = s.alloc<int32_t>((size_t)fixup_capacity(sp.T));
-    sp.carry_val = s.alloc<double>((size_t)fixup_capacity(sp.T));
+    alloc_carries(s, sp.T, sp.carry_row, sp.carry_val);
     sp.max_run = (std::max<int64_t>(maxlen, P->feat.nnz_max) + sp.stride - 1) / sp.stride + 1;
     DevStats zero{};
     ck(cudaMemcpyAsync(&s.stats->n_incoming, &zero.n_incoming, 8, cudaMemcpyHostToDevice, s.stream), "stats");
@@ -603,6 +615,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     // one stage per consumer warp: measured on B200 (tools/sweep.py, C2/C5),
     // more resident warps beat a deeper ring (the x gathers are latency-bound)
     sp.stages = opt.stages > 0 ? opt.stages : kStreamConsumerWarps;
+    if (const char* e = getenv("SPMV_STREAM_L2PF")) sp.l2pf = atoi(e) != 0;
     // shrink the staged-rowptr capacity until the ring fits (sparser tiles
     // then read rowptr from global memory)
     while (sp.rows_cap > 64 && stream_smem_bytes(sp.C, sp.stages, V.rp_bytes, sp.rows_cap, d16, seg) > 227 * 1024)
@@ -625,17 +638,92 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     z.mc = mc;
     z.m_out = s.m;
     z.zero_gaps = true;
+    z.persistent = P->sel.variant != SPMV_VARIANT_SPLIT;  // SPLIT: shares the SMs with the long-row kernel
+    if (const char* e = getenv("SPMV_NZ_PERSIST")) z.persistent = atoi(e) != 0;
     z.T = (V.nnz + kNzTile - 1) / kNzTile;
     z.tile_q = s.alloc<int32_t>((size_t)z.T + 1);
-    z.carry_row = s.alloc<int32_t>((size_t)fixup_capacity(z.T));
-    z.carry_val = s.alloc<double>((size_t)fixup_capacity(z.T));
+    alloc_carries(s, z.T, z.carry_row, z.carry_val);
     z.max_run = maxlen / kNzTile + 2;
-    z.sched = s.alloc<unsigned long long>(2);
-    ck(cudaMemsetAsync(z.sched, 0, 16, s.stream), "memset");
     launch_nz_tiles(z, s.stream);
     count_launches(2, "nz tiles");
     z.grid = nz_prepare(z, s.sm_count);
     if (z.grid < 0) fail(SPMV_E_CUDA, "nnz_split: occupancy query failed");
+  };
+  // hot-x set of an nnz_split pass over the plan's own colind copy (ML class,
+  // P:599-606 re-designed): the most frequent columns (count >= t, first K in
+  // column order, K <= kHotMax) are re-encoded as ~slot when they cover >= 20 %
+  // of the nonzeros (auto) or when forced (opt.hot_x > 0 = max K)
+  auto build_hot = [&](Shard& s, NzPlan& z, const MatView& V, int32_t* col_own) {
+    if (opt.hot_x == 0 || V.nnz == 0 || V.n_cols == 0) return;
+    int Kmax = opt.hot_x > 0 ? std::min(opt.hot_x, kHotMax) : kHotMax;
+    Kmax &= ~1;  // the smem table is bulk-copied in 16-B units
+    if (Kmax < 2) return;
+    const int64_t nc = V.n_cols, nb = (nc + 1023) / 1024;
+    int32_t *cnt = nullptr, *H = nullptr, *bsum = nullptr, *slot = nullptr;
+    unsigned long long* cov = nullptr;
+    auto cleanup = [&] {
+      cudaFree(cnt); cudaFree(H); cudaFree(bsum); cudaFree(slot); cudaFree(cov);
+    };
+    try {
+      ck(cudaMalloc(&cnt, (size_t)nc * 4), "cudaMalloc");
+      ck(cudaMalloc(&H, (size_t)kHotBuckets * 4), "cudaMalloc");
+      ck(cudaMalloc(&bsum, (size_t)nb * 4 + 4), "cudaMalloc");
+      ck(cudaMalloc(&slot, (size_t)nc * 4), "cudaMalloc");
+      ck(cudaMalloc(&cov, 8), "cudaMalloc");
+      launch_col_counts(V.col, V.nnz, nc, cnt, H, s.stream);
+      count_launches(2, "col counts");
+      std::vector<int32_t> h(kHotBuckets);
+      ck(cudaMemcpyAsync(h.data(), H, (size_t)kHotBuckets * 4, cudaMemcpyDeviceToHost, s.stream), "hist");
+      ck(cudaStreamSynchronize(s.stream), "hist");
+      // smallest t >= 1 whose columns (count >= t) number <= Kmax; the top
+      // bucket (count >= kHotBuckets-1) is taken whole, truncated to Kmax in
+      // column order
+      int64_t acc = 0;
+      int t = kHotBuckets - 1;
+      for (int v = kHotBuckets - 1; v >= 1; --v) {
+        if (v < kHotBuckets - 1 && acc + h[v] > Kmax) break;
+        acc += h[v];
+        t = v;
+      }
+      launch_hot_flags(cnt, nc, t, bsum, s.stream);
+      std::vector<int32_t> bs((size_t)nb + 1, 0);
+      ck(cudaMemcpyAsync(bs.data(), bsum, (size_t)nb * 4, cudaMemcpyDeviceToHost, s.stream), "hot flags");
+      ck(cudaStreamSynchronize(s.stream), "hot flags");
+      int64_t tot = 0;
+      for (int64_t b = 0; b < nb; ++b) {
+        const int32_t c = bs[b];
+        bs[b] = (int32_t)std::min<int64_t>(tot, INT32_MAX);
+        tot += c;
+      }
+      const int K = (int)std::min<int64_t>(tot, Kmax) & ~1;
+      if (K < 2) { cleanup(); return; }
+      ck(cudaMemcpyAsync(bsum, bs.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, s.stream), "hot offsets");
+      int32_t* hot_cols = s.alloc<int32_t>((size_t)K);
+      launch_hot_write(cnt, nc, t, bsum, K, hot_cols, slot, s.stream);
+      count_launches(2, "hot set");
+      // coverage = nonzeros in the hot columns
+      std::vector<int32_t> hc((size_t)K);
+      std::vector<int32_t> cv((size_t)nc);
+      ck(cudaMemcpyAsync(hc.data(), hot_cols, (size_t)K * 4, cudaMemcpyDeviceToHost, s.stream), "hot cols");
+      ck(cudaMemcpyAsync(cv.data(), cnt, (size_t)nc * 4, cudaMemcpyDeviceToHost, s.stream), "counts");
+      ck(cudaStreamSynchronize(s.stream), "hot set");
+      int64_t covered = 0;
+      for (int k = 0; k < K; ++k) covered += cv[(size_t)hc[k]];
+      const bool on = opt.hot_x > 0 || (double)covered >= 0.2 * (double)V.nnz;
+      if (on) {
+        launch_hot_encode(col_own, V.nnz, slot, s.stream);  // the plan's own colind copy of V
+        count_launches(1, "hot encode");
+        z.n_hot = K;
+        z.hot_cols = hot_cols;
+        z.xhot = s.alloc<double>((size_t)K);
+        ck(cudaStreamSynchronize(s.stream), "hot encode");
+      }
+      P->hot_cover = (double)covered / (double)V.nnz;
+      cleanup();
+    } catch (...) {
+      cleanup();
+      throw;
+    }
   };
   // compacted bin of the rows with lo <= len <= hi (non-empty): cta_stream
   // plan sp, or (nz != null) one nnz_split pass
@@ -666,6 +754,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     launch_gather_rowptr(frp, rp_bytes, rows, nrows, s.m, brp, s.stream);
     count_launches(1, "bin gather");
     if (nz) {
+      // (hot-x only when forced: its one 1024-thread CTA per SM leaves no
+      // room for the concurrent long-row kernel; measured 554 vs 281 us on C3)
+      if (opt.hot_x > 0) build_hot(s, *nz, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, bcol);
       build_nz(s, *nz, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, brp, rows, nrows,
                hi >= P->l_split ? P->feat.max_short : std::min<int64_t>(hi, P->feat.nnz_max));
       nz->skip_rp = A.rowptr;
@@ -686,8 +777,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       s.Tm = std::max<int64_t>(1, (s.m + s.nnz + s.items - 1) / s.items);
       s.mrow = s.alloc<int32_t>((size_t)s.Tm + 1);
       s.mnnz = s.alloc<int64_t>((size_t)s.Tm + 1);
-      s.mcarry_row = s.alloc<int32_t>((size_t)fixup_capacity(s.Tm));
-      s.mcarry_val = s.alloc<double>((size_t)fixup_capacity(s.Tm));
+      alloc_carries(s, s.Tm, s.mcarry_row, s.mcarry_val);
       launch_merge_splits(A, s.items, s.Tm, s.mrow, s.mnnz, s.stream);
       count_launches(1, "merge_splits");
     } else if (P->sel.variant == SPMV_VARIANT_NNZSPLIT) {
@@ -710,6 +800,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       } else {
         ck(cudaMemsetAsync(rpc, 0, rp_bytes, s.stream), "memset");
       }
+      build_hot(s, s.nz, A, s.col);
       build_nz(s, s.nz, A, rpc, rows, mc, P->feat.nnz_max);
       s.use_nz = true;
     } else if (P->sel.variant == SPMV_VARIANT_SPLIT) {
@@ -750,8 +841,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
         count_launches(4, "long_rows");
         ck(cudaMemcpyAsync(&s.n_chunks, s.chunk_start + s.n_long, 8, cudaMemcpyDeviceToHost, s.stream), "chunks");
         ck(cudaStreamSynchronize(s.stream), "long_rows");
-        s.chunk_row = s.alloc<int32_t>((size_t)fixup_capacity(s.n_chunks));
-        s.chunk_val = s.alloc<double>((size_t)fixup_capacity(s.n_chunks));
+        alloc_carries(s, s.n_chunks, s.chunk_row, s.chunk_val);
         // column-tiled long rows when a (row, x block) segment averages >= 64
         // nonzeros (dense-ish long rows: x served from smem, not one L2 sector
         // per nonzero); long_mode 1/2 forces chunks / tiled
@@ -767,6 +857,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
           int per_sm = 0;
           if (const char* e = getenv("SPMV_LONG_CTAS")) per_sm = atoi(e);
           s.long_grid = long_tiled_grid(nblk, s.sm_count, per_sm);
+          if (const char* e = getenv("SPMV_SPLIT_FUSED")) s.split_fused = atoi(e) != 0;
         }
         // the long rows run on a side stream, concurrently with the bins
         ck(cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -865,6 +956,7 @@ void spmv_options_default(spmv_options* o) {
   o->xwin = -1;
   o->seg = -1;
   o->split_bins = -1;
+  o->hot_x = -1;
   o->validate = 1;
 }
 
@@ -1005,6 +1097,8 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     info->n_merge_tiles = s0.Tm;
     info->n_nz_rows = s0.nz.mc;
     info->n_nz_tiles = s0.nz.T;
+    info->n_hot = s0.nz.n_hot;
+    info->hot_cover = p->hot_cover;
     info->l_split = p->l_split;
     info->long_chunk = p->chunk;
     int64_t nc = 0, bytes = 0;
@@ -1090,6 +1184,7 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
       }
       case SPMV_ARR_NZ_ROWMAP: widen32(s.nz.rowmap, s.nz.rowmap ? s.nz.mc + 1 : 0); break;
       case SPMV_ARR_NZ_TILE_Q: widen32(s.nz.tile_q, s.nz.tile_q ? s.nz.T + 1 : 0); break;
+      case SPMV_ARR_NZ_HOT_COLS: widen32(s.nz.hot_cols, s.nz.n_hot); break;
       case SPMV_ARR_NZ_RPC: {
         count = s.nz.rpc ? s.nz.mc + 1 : 0;
         if (!dst || count == 0) break;

@@ -47,6 +47,7 @@ struct StreamPlan {
   int64_t stride = 0;    // tile stride in nonzeros (C, or C - longest row when aligned)
   int64_t* tile_nz = nullptr;  // aligned: tile_nz[k] = rowptr[tile_row[k]], k = 0..T
   int64_t max_run = 1;         // longest run of equal carry rows (fix-up choice)
+  bool l2pf = false;           // producer L2-prefetches each stage's next tile (measured slower: C2 53.7 vs 47.0 us)
 };
 void launch_tile_nz(const MatView& A, const int32_t* tile_row, int64_t T, int64_t* tile_nz, cudaStream_t s);
 
@@ -65,16 +66,27 @@ struct NzPlan {
   int64_t mc = 0, T = 0, m_out = 0;
   int grid = 0;
   int64_t max_run = 1;    // longest run of equal carry rows (fix-up choice)
-  bool tma = false;       // streams by TMA bulk copies (else LDG.256 through L1)
-  unsigned long long* sched = nullptr;  // dynamic tile scheduling counters [2], zero between launches
-  bool dynamic = false;   // tickets (else static round-robin chunks)
-  int64_t chunk = 1;      // tiles per ticket / round-robin chunk
+  // hot-x mode: colind of the n_hot most frequent columns re-encoded as ~slot;
+  // xhot[slot] = x[hot_cols[slot]] is refreshed per SpMV and staged in smem
+  int n_hot = 0;
+  const int32_t* hot_cols = nullptr;
+  double* xhot = nullptr;
   bool zero_gaps = true;  // write y = 0 for the rows of [0, m_out) not in rowmap
+  bool persistent = true;  // grid = resident CTAs (else one tile per warp: lets a concurrent kernel share the SMs)
   const void* skip_rp = nullptr;  // SPLIT: zero only the gap rows empty in this rowptr (long rows are written
                                   // concurrently by the long-row reduction)
 };
 void launch_nz_tiles(const NzPlan& z, cudaStream_t s);  // tile_q and rowmap[mc] = m_out
-int nz_prepare(NzPlan& z, int sm_count);  // picks the stream mode, returns the persistent grid (<0 on error)
+int nz_prepare(NzPlan& z, int sm_count);  // persistent grid (<0 on error)
+// hot-x set (plan time): column counts + a count histogram of kHotBuckets,
+// then the ordered compaction of the columns with count >= t (first K)
+constexpr int kHotBuckets = 4096;
+constexpr int kHotMax = 16384;  // hot columns staged in smem (128 KB)
+void launch_col_counts(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* cnt, int32_t* H, cudaStream_t s);
+void launch_hot_flags(const int32_t* cnt, int64_t n_cols, int32_t t, int32_t* bsum, cudaStream_t s);
+void launch_hot_write(const int32_t* cnt, int64_t n_cols, int32_t t, const int32_t* boff, int K, int32_t* hot_cols,
+                      int32_t* slot, cudaStream_t s);
+void launch_hot_encode(int32_t* col, int64_t nnz, const int32_t* slot, cudaStream_t s);
 int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaStream_t s);
 
 // ---- inspector ------------------------------------------------------------
@@ -142,6 +154,7 @@ struct ExecArgs {
   const int64_t* long_seg;    // [n_long][nblk+1] segment starts
   double* long_partial;       // [n_long][nblk]
   int long_grid;              // persistent grid of the column-tiled kernel
+  bool split_fused;           // SPLIT: nz bin + tiled long rows interleaved in one grid
 };
 
 constexpr int64_t kLongXB = 2048;  // columns per x block staged in smem by the column-tiled long-row kernel
@@ -156,6 +169,7 @@ int launch_stream(const ExecArgs& a, cudaStream_t s);
 int launch_merge(const ExecArgs& a, cudaStream_t s);
 int launch_split(const ExecArgs& a, cudaStream_t s);
 int launch_nzsplit(const ExecArgs& a, cudaStream_t s);
+int launch_split_fused(const ExecArgs& a, cudaStream_t s);  // nz bin + column-tiled long rows, one grid
 size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, int rows_cap, bool d16, bool seg);
 int stream_prepare(const StreamPlan& sp, int sm_count);  // smem attribute + persistent grid (<0 on error)
 void launch_chunk_export(const ExecArgs& a, int64_t* out, cudaStream_t s);  // [row|begin|end] x n_chunks

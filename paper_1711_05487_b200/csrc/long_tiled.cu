@@ -10,8 +10,7 @@
 // kernel sums each row's partials in block order (deterministic) into y.
 // Chosen when the long rows are dense enough that a block segment averages
 // >= 64 nonzeros; otherwise the nonzero-chunk kernel is used.
-#include "common.cuh"
-#include "internal.h"
+#include "tiles.cuh"
 
 namespace spmv {
 
@@ -45,72 +44,10 @@ void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long,
     long_seg_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, long_rows, n_long, nblk, seg);
 }
 
-__device__ __forceinline__ void lt_ld256_s32(const int32_t* p, int (&c)[8]) {
-  asm volatile("ld.global.nc.L1::no_allocate.v8.s32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7])
-               : "l"(p));
-}
-__device__ __forceinline__ void lt_ld256_f64(const double* p, double* v) {
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
-               : "l"(p));
-}
-
-// CTA (b, g): x block b staged in smem, long rows q = g, g + RG, ... of it.
-// A warp streams a segment [s0, s1) in 8-aligned groups of 8 nonzeros per
-// lane (one 256-bit colind load + two 256-bit value loads, 16 nonzeros per
-// lane in flight), masking the group edges outside the segment.
-__global__ void __launch_bounds__(kNT) long_tiled_kernel(const int32_t* __restrict__ col,
-                                                         const double* __restrict__ val, const double* __restrict__ x,
-                                                         int64_t n_long, int64_t n_cols, const int64_t* __restrict__ seg,
-                                                         int64_t nblk, int rg, double* __restrict__ partial) {
+// CTA item loop (persistent when the grid is smaller than the item count)
+__global__ void __launch_bounds__(kNT) long_tiled_kernel(const LongP p) {
   __shared__ double xs[kLongXB];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // persistent: work item (b, g) = it / rg, it % rg, round-robin over CTAs
-  for (int64_t it = blockIdx.x; it < nblk * rg; it += gridDim.x) {
-  const int64_t b = it / rg, g = it % rg;
-  const int64_t c0 = b * kLongXB;
-  const int cw = (int)((n_cols - c0) < kLongXB ? (n_cols - c0) : kLongXB);
-  __syncthreads();  // previous item's readers are done with xs
-  for (int i = threadIdx.x; i < cw; i += kNT) xs[i] = ld_x(x + c0 + i);
-  __syncthreads();
-  for (int64_t q = g + (int64_t)rg * w; q < n_long; q += (int64_t)rg * (kNT / 32)) {
-    const int64_t s0 = ld_ro(seg + q * (nblk + 1) + b), s1 = ld_ro(seg + q * (nblk + 1) + b + 1);
-    double a0 = 0.0, a1 = 0.0;
-    for (int64_t base = s0 & ~7ll; base < s1; base += 512) {
-      int c[2][8];
-      double v[2][8];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int64_t e = base + 256 * r + 8 * lane;
-        if (e < s1) {
-          lt_ld256_s32(col + e, c[r]);
-          lt_ld256_f64(val + e, v[r]);
-          lt_ld256_f64(val + e + 4, v[r] + 4);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            c[r][i] = (int)c0;
-            v[r][i] = 0.0;
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int64_t e = base + 256 * r + 8 * lane;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const bool in = e + i >= s0 && e + i < s1;
-          const double t = v[r][i] * xs[in ? c[r][i] - (int)c0 : 0];
-          if (i & 1) a1 += in ? t : 0.0;
-          else a0 += in ? t : 0.0;
-        }
-      }
-    }
-    const double t = warp_sum(a0 + a1);
-    if (lane == 0) partial[q * nblk + b] = t;
-  }
-  }
+  for (int64_t it = blockIdx.x; it < p.nblk * p.rg; it += gridDim.x) long_item<kNT>(p, it, xs);
 }
 
 // y[long_rows[q]] = sum_b partial[q][b] (lane-strided, butterfly: fixed order)
@@ -126,6 +63,22 @@ __global__ void __launch_bounds__(kNT) long_reduce_kernel(const double* __restri
   if (lane == 0) y[long_rows[q]] = a;
 }
 
+LongP long_params(const ExecArgs& a) {
+  LongP p;
+  p.col = a.A.col;
+  p.val = a.A.val;
+  p.x = a.x;
+  p.seg = a.long_seg;
+  p.partial = a.long_partial;
+  p.n_long = a.n_long;
+  p.n_cols = a.A.n_cols;
+  p.nblk = a.nblk;
+  p.rg = kLongRG;
+  return p;
+}
+
+int long_items(const ExecArgs& a) { return (int)(a.nblk * kLongRG); }
+
 // part 1: the column-tiled partials; part 2: the ordered per-row reduction
 // persistent grid: per_sm CTAs per SM (<= 0: one CTA per work item)
 int long_tiled_grid(int64_t nblk, int sm_count, int per_sm) {
@@ -138,8 +91,7 @@ int long_tiled_grid(int64_t nblk, int sm_count, int per_sm) {
 void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s) {
   if (a.n_long == 0) return;
   if (part == 1)
-    long_tiled_kernel<<<a.long_grid, kNT, 0, s>>>(a.A.col, a.A.val, a.x, a.n_long, a.A.n_cols, a.long_seg, a.nblk,
-                                                  kLongRG, a.long_partial);
+    long_tiled_kernel<<<a.long_grid, kNT, 0, s>>>(long_params(a));
   else
     long_reduce_kernel<<<(int)((a.n_long * 32 + kNT - 1) / kNT), kNT, 0, s>>>(a.long_partial, a.n_long, a.nblk,
                                                                              a.long_rows, a.y);

@@ -1,0 +1,95 @@
+// split.cu -- the fused long_row_split pass (IMB decomposition).
+//
+// The dense long rows run as column-tiled items (x block in smem, streams from
+// HBM) and the other rows as one nnz_split bin (random x gathers, bound by the
+// L1 miss path). Launched as two kernels, even on two streams, they hardly
+// overlap on B200: the first fills every SM and the block scheduler runs the
+// second behind it (measured C4: 57 + 80 us -> 140 us). Here ONE grid
+// interleaves both kinds of CTAs in blockIdx order -- long item i sits at
+// block floor(i * total / n_items) -- so every SM mixes HBM-bound long-row
+// CTAs with gather-bound short-row CTAs for the whole pass. The epilogue
+// (ordered carry fix-up of the bin + per-row reduction of the long-row
+// partials, disjoint rows) is one launch as well.
+#include "tiles.cuh"
+
+namespace spmv {
+
+constexpr int kSplitThreads = 256;
+
+template <typename RP>
+__global__ void __launch_bounds__(kSplitThreads, 4) split_fused_kernel(const NzP<RP> z, const LongP l, int64_t n_items,
+                                                                         int64_t n_groups) {
+  __shared__ double xs[kLongXB];
+  __shared__ __align__(16) uint32_t emask_s[kSplitThreads / 32][8];
+  const int64_t total = n_items + n_groups;
+  const int64_t b = blockIdx.x;
+  const int64_t Lb = (b + 1) * n_items / total;  // long items among blocks [0, b]
+  if (Lb > b * n_items / total) {
+    long_item<kSplitThreads>(l, Lb - 1, xs);
+    return;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k = (b - Lb) * (kSplitThreads / 32) + w;  // nz tile: group (b - Lb), warp w
+  if (k < z.T) nz_tile<RP, false>(z, k, lane, emask_s[w], nullptr);
+}
+
+// blocks [0, nfb): ordered carry fix-up of the bin (runs <= 16: one thread
+// per run start); blocks [nfb, ...): y[long_rows[q]] = sum_b partial[q][b]
+__global__ void __launch_bounds__(kNT) split_epilogue_kernel(const int32_t* __restrict__ crow,
+                                                             const double* __restrict__ cval, int64_t T, int nfb,
+                                                             const double* __restrict__ partial, int64_t n_long,
+                                                             int64_t nblk, const int32_t* __restrict__ long_rows,
+                                                             double* __restrict__ y) {
+  if ((int)blockIdx.x < nfb) {
+    const int64_t k = (int64_t)blockIdx.x * kNT + threadIdx.x;
+    if (k >= T) return;
+    const int32_t r = crow[k];
+    if (r < 0 || (k > 0 && crow[k - 1] == r)) return;
+    double s = cval[k];
+    for (int64_t q = k + 1; q < T && crow[q] == r; ++q) s += cval[q];
+    y[r] += s;
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t q = ((int64_t)(blockIdx.x - nfb) * kNT + threadIdx.x) >> 5;
+  if (q >= n_long) return;
+  double a = 0.0;
+  for (int64_t b = lane; b < nblk; b += 32) a += partial[q * nblk + b];
+  a = warp_sum(a);
+  if (lane == 0) y[long_rows[q]] = a;
+}
+
+NzP<int32_t> nz_params32(const NzPlan& z, const double* x, double* y);
+NzP<int64_t> nz_params64(const NzPlan& z, const double* x, double* y);
+LongP long_params(const ExecArgs& a);
+int long_items(const ExecArgs& a);
+
+int launch_split_fused(const ExecArgs& a, cudaStream_t s) {
+  int n = 0;
+  const NzPlan& z = a.nz;
+  if (a.stage != 2) {
+    const int64_t items = long_items(a), groups = (z.T + kSplitThreads / 32 - 1) / (kSplitThreads / 32);
+    const int grid = (int)(items + groups);
+    if (z.V.rp_bytes == 8)
+      split_fused_kernel<int64_t><<<grid, kSplitThreads, 0, s>>>(nz_params64(z, a.x, a.y), long_params(a), items, groups);
+    else
+      split_fused_kernel<int32_t><<<grid, kSplitThreads, 0, s>>>(nz_params32(z, a.x, a.y), long_params(a), items, groups);
+    ++n;
+  }
+  if (a.stage != 1) {
+    if (z.T > 1 && z.max_run > 16) {
+      n += launch_fixup(z.carry_row, z.carry_val, z.T, a.y, 0, z.max_run, s);
+      launch_long_tiled(a, 2, s);
+      ++n;
+    } else {
+      const int nfb = z.T > 1 ? (int)((z.T + kNT - 1) / kNT) : 0;
+      const int nrb = (int)((a.n_long * 32 + kNT - 1) / kNT);
+      split_epilogue_kernel<<<nfb + nrb, kNT, 0, s>>>(z.carry_row, z.carry_val, z.T, nfb, a.long_partial, a.n_long,
+                                                       a.nblk, a.long_rows, a.y);
+      ++n;
+    }
+  }
+  return n;
+}
+
+}  // namespace spmv

@@ -94,6 +94,7 @@ struct StreamP {
   int64_t nnz, C, T;
   int stages, rows_cap;
   int aligned;  // 1: row-aligned tiles (no row crosses a tile, no carries)
+  int l2pf;     // 1: the producer prefetches the stage's next tile into L2
 };
 
 template <typename RP>
@@ -259,11 +260,46 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? 7 : 8))
         }
       };
       fetch(blockIdx.x);
+      // L2 prefetch of the tile that will next reuse this stage (S tiles
+      // ahead): its DRAM latency then overlaps the consumer's current tile
+      // and the later TMA copy hits L2 (metadata fetched one tile earlier)
+      int64_t pR0 = 0, pR1 = 0, pT0 = 0, pT1 = 0;
+      auto pfetch = [&](int64_t kk) {
+        if (p.l2pf && kk < p.T) {
+          pR0 = ld_ro(p.tile_row + kk);
+          pR1 = ld_ro(p.tile_row + kk + 1);
+          if constexpr (AL) {
+            pT0 = ld_ro(p.tile_nz + kk);
+            pT1 = ld_ro(p.tile_nz + kk + 1);
+          }
+        }
+      };
+      pfetch(blockIdx.x + (int64_t)S * gridDim.x);
       int i = 0;
       for (int64_t k = blockIdx.x; k < p.T; k += gridDim.x, ++i) {
         const int s = i % S;
         const int64_t R0 = nR0, R1 = nR1, aT0 = nT0, aT1 = nT1;
         fetch(k + gridDim.x);
+        const int64_t k2 = k + (int64_t)S * gridDim.x;
+        if (p.l2pf && k2 < p.T) {
+          int64_t u0, u1;
+          if constexpr (AL) {
+            u0 = pT0;
+            u1 = pT1;
+          } else {
+            u0 = k2 * p.C;
+            u1 = (u0 + p.C) < p.nnz ? (u0 + p.C) : p.nnz;
+          }
+          if (u1 > u0) {
+            const int64_t a0 = u0 & ~15ll, a1 = (u1 + 15) & ~15ll;  // whole 128-B lines of values
+            bulk_prefetch_l2(p.val + a0, (uint32_t)((a1 - a0) * 8));
+            const int64_t b0 = (u0 * IB) & ~127ll, b1 = (u1 * IB + 127) & ~127ll;
+            bulk_prefetch_l2(static_cast<const unsigned char*>(p.idx) + b0, (uint32_t)(b1 - b0));
+          }
+          const int64_t r0 = ((pR0 > 0 ? pR0 - 1 : 0) * RPB) & ~127ll, r1 = ((pR1 + 1) * RPB + 127) & ~127ll;
+          bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(p.rp) + r0, (uint32_t)(r1 - r0));
+        }
+        pfetch(k2 + gridDim.x);
         if (i >= S) mbar_wait(&empty[s], (uint32_t)(((i / S) - 1) & 1));
         // nnz-aligned tile [k*C, ...) or row-aligned tile [rowptr[R0], rowptr[R1])
         // (copies rounded out to 16 B; voff/ioff = offsets of t0 in the stage)
@@ -474,6 +510,7 @@ static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y)
   p.stages = sp.stages;
   p.rows_cap = sp.rows_cap;
   p.aligned = sp.aligned ? 1 : 0;
+  p.l2pf = sp.l2pf ? 1 : 0;
   return p;
 }
 

@@ -1,0 +1,193 @@
+// tiles.cuh -- device bodies shared by the nnz_split kernel, the column-tiled
+// long-row kernel and the fused long_row_split kernel (one work unit each).
+#pragma once
+#include "common.cuh"
+#include "internal.h"
+
+namespace spmv {
+
+__device__ __forceinline__ void ld256_s32(const int32_t* p, int (&c)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.s32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld256_f64(const double* p, double* v) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+
+// ---- nnz_split warp tile (see nzsplit.cu) -----------------------------------
+template <typename RP>
+struct NzP {
+  const RP* rpc;
+  const int32_t* col;
+  const double* val;
+  const double* x;
+  double* y;
+  const int32_t* rowmap;
+  const int32_t* tile_q;
+  int32_t* carry_row;
+  double* carry_val;
+  const RP* orp;        // non-null: zero a gap row only if it is empty in this rowptr (SPLIT: long rows are not ours)
+  const double* xhot;   // hot-x mode: x of the hot columns, [n_hot]
+  int64_t nnz, T;
+  int n_hot;
+  int zero_gaps;
+};
+
+// warp tile k = nonzeros [k*256, (k+1)*256); em: the warp's 8-word smem row-end
+// mask; xh: the hot-x smem table (HOT)
+template <typename RP, bool HOT>
+__device__ __forceinline__ void nz_tile(const NzP<RP>& p, int64_t k, int lane, uint32_t* em, const double* xh) {
+  const int64_t t0 = k * kNzTile;
+  const int cnt = (int)((p.nnz - t0) < kNzTile ? (p.nnz - t0) : kNzTile);
+  const int e0 = lane * 8;
+  int c[8];
+  double v[8];
+  if (e0 + 8 <= cnt) {
+    ld256_s32(p.col + t0 + e0, c);
+    ld256_f64(p.val + t0 + e0, v);
+    ld256_f64(p.val + t0 + e0 + 4, v + 4);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool ok = e0 + i < cnt;
+      c[i] = ok ? ld_stream(p.col + t0 + e0 + i) : 0;
+      v[i] = ok ? ld_stream(p.val + t0 + e0 + i) : 0.0;
+    }
+  }
+  double xv[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if constexpr (HOT) xv[i] = c[i] < 0 ? xh[~c[i]] : ld_x(p.x + c[i]);
+    else xv[i] = ld_x(p.x + c[i]);
+  }
+
+  // rows ending in the tile: q in [q0, q1), end position rpc[q+1]-1
+  const int64_t q0 = ld_ro(p.tile_q + k), q1 = ld_ro(p.tile_q + k + 1);
+  const int n_end = (int)(q1 - q0);
+  if (lane < 8) em[lane] = 0u;
+  __syncwarp();
+  for (int j = lane; j < n_end; j += 32) {
+    const int64_t q = q0 + j;
+    const int e = (int)((int64_t)ld_ro(p.rpc + q + 1) - 1 - t0);
+    atomicOr(&em[e >> 5], 1u << (e & 31));
+    if (p.zero_gaps) {
+      const int32_t ra = ld_ro(p.rowmap + q), rb = ld_ro(p.rowmap + q + 1);
+      for (int32_t r = ra + 1; r < rb; ++r)
+        if (!p.orp || ld_ro(p.orp + r + 1) == ld_ro(p.orp + r)) p.y[r] = 0.0;
+    }
+  }
+  if (k == 0 && p.zero_gaps) {
+    const int32_t r0 = ld_ro(p.rowmap);
+    for (int32_t r = lane; r < r0; r += 32)
+      if (!p.orp || ld_ro(p.orp + r + 1) == ld_ro(p.orp + r)) p.y[r] = 0.0;
+  }
+  __syncwarp();
+  const uint4 m0 = *reinterpret_cast<const uint4*>(em);
+  const uint4 m1 = *reinterpret_cast<const uint4*>(em + 4);
+  const uint32_t words[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+  const int wi = lane >> 2, sh = (lane & 3) * 8;
+  uint32_t word = 0;
+  int before = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i < wi) before += __popc(words[i]);
+    if (i == wi) word = words[i];
+  }
+  before += __popc(word & ((1u << sh) - 1u));
+  const uint32_t my = (word >> sh) & 0xffu;
+
+  // lane-sequential sums; the first row end of the lane is completed after
+  // the cross-lane scan, later ones are complete inside the lane
+  const int64_t qf = q0 + before;
+  double acc = 0.0, head = 0.0;
+  int ne = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    acc = fma(v[i], xv[i], acc);
+    if ((my >> i) & 1u) {
+      if (ne == 0) head = acc;
+      else p.y[ld_ro(p.rowmap + qf + ne)] = acc;
+      ++ne;
+      acc = 0.0;
+    }
+  }
+  // segmented inclusive scan of the lane tails, reset at lanes with a row end
+  double S = acc;
+  int f = ne > 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double su = __shfl_up_sync(0xffffffffu, S, o);
+    const int fu = __shfl_up_sync(0xffffffffu, f, o);
+    if (lane >= o) {
+      if (!f) S += su;
+      f |= fu;
+    }
+  }
+  const double cin = __shfl_up_sync(0xffffffffu, S, 1);
+  if (ne > 0) p.y[ld_ro(p.rowmap + qf)] = (lane > 0 ? cin : 0.0) + head;
+  if (lane == 31) {
+    if (cnt == kNzTile && !(my & 0x80u)) {
+      p.carry_row[k] = ld_ro(p.rowmap + q1);
+      p.carry_val[k] = S;
+    } else {
+      p.carry_row[k] = -1;
+    }
+  }
+}
+
+// ---- column-tiled long rows (see long_tiled.cu) -----------------------------
+struct LongP {
+  const int32_t* col;
+  const double* val;
+  const double* x;
+  const int64_t* seg;   // [n_long][nblk+1]
+  double* partial;      // [n_long][nblk]
+  int64_t n_long, n_cols, nblk;
+  int rg;               // row groups per x block
+};
+
+// work item it = (x block b, row group g) = (it / rg, it % rg) for the whole
+// CTA of NT threads: x block b staged in xs (kLongXB doubles), then each warp
+// streams the segments of long rows q = g + rg*(w + NW*i), lane l taking
+// nonzeros l, l+32, ... (coalesced loads, 16 in flight per lane). Lane-strided
+// order matters for the smem gather: the 32 lanes of one load read 32
+// consecutive nonzeros of a sorted row, i.e. nearby columns (~2-way bank
+// conflicts), where lane-contiguous chunks scatter over the whole block
+// (measured ~8 wavefronts per gather on C4).
+template <int NT>
+__device__ __forceinline__ void long_item(const LongP& p, int64_t it, double* xs) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  const int64_t b = it / p.rg, g = it % p.rg;
+  const int64_t c0 = b * kLongXB;
+  const int cw = (int)((p.n_cols - c0) < kLongXB ? (p.n_cols - c0) : kLongXB);
+  __syncthreads();  // previous readers of xs are done
+  for (int i = threadIdx.x; i < cw; i += NT) xs[i] = ld_x(p.x + c0 + i);
+  __syncthreads();
+  for (int64_t q = g + (int64_t)p.rg * w; q < p.n_long; q += (int64_t)p.rg * NW) {
+    const int64_t s0 = ld_ro(p.seg + q * (p.nblk + 1) + b), s1 = ld_ro(p.seg + q * (p.nblk + 1) + b + 1);
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t base = s0 + lane; base < s1; base += 512) {
+      int c[16];
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int64_t e = base + 32 * u;
+        c[u] = e < s1 ? ld_stream(p.col + e) - (int)c0 : 0;
+        v[u] = e < s1 ? ld_stream(p.val + e) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; u += 2) {
+        a0 = fma(v[u], xs[c[u]], a0);
+        a1 = fma(v[u + 1], xs[c[u + 1]], a1);
+      }
+    }
+    const double t = warp_sum(a0 + a1);
+    if (lane == 0) p.partial[q * p.nblk + b] = t;
+  }
+}
+
+}  // namespace spmv

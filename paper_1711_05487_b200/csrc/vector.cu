@@ -8,6 +8,8 @@
 //                  per-row reduction of the chunk partials (IMB decomposition,
 //                  P:608-621, Fig. 7 semantics per SURVEY 8(c3) #11).
 // All sums are formed in an order fixed by the plan (deterministic).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -118,24 +120,24 @@ __global__ void __launch_bounds__(kNT) fixup_kernel(const int32_t* __restrict__ 
   y[r] = set ? s : y[r] + s;
 }
 
-__global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restrict__ crow,
-                                                          const double* __restrict__ cval, int64_t n,
-                                                          double* __restrict__ y, int set,
-                                                          int32_t* __restrict__ orow, double* __restrict__ oval) {
+// one CTA of a reduce-by-key level: carries [b*1024, min(n, (b+1)*1024))
+__device__ __forceinline__ void fixup_block(const int32_t* __restrict__ crow, const double* __restrict__ cval,
+                                            int64_t n, int64_t blk, double* __restrict__ y, int set,
+                                            int32_t* __restrict__ orow, double* __restrict__ oval) {
   __shared__ double wv[kNT / 32];
   __shared__ int wf[kNT / 32];
-  __shared__ int64_t first_end;
-  const int64_t bs = (int64_t)blockIdx.x * kFixItems;
+  __shared__ unsigned long long first_end;
+  const int64_t bs = blk * kFixItems;
   const int64_t be = (bs + kFixItems) < n ? (bs + kFixItems) : n;
-  const bool head_open = bs > 0 && crow[bs - 1] == crow[bs];
-  const bool tail_open = be < n && crow[be] == crow[be - 1];
+  const bool head_open = bs > 0 && __ldcg(crow + bs - 1) == __ldcg(crow + bs);
+  const bool tail_open = be < n && __ldcg(crow + be) == __ldcg(crow + be - 1);
   if (threadIdx.x == 0) {
-    first_end = be - 1;
+    first_end = (unsigned long long)(be - 1);
     if (orow) {
-      orow[2 * blockIdx.x] = -1;
-      orow[2 * blockIdx.x + 1] = -1;
-      oval[2 * blockIdx.x] = 0.0;
-      oval[2 * blockIdx.x + 1] = 0.0;
+      orow[2 * blk] = -1;
+      orow[2 * blk + 1] = -1;
+      oval[2 * blk] = 0.0;
+      oval[2 * blk + 1] = 0.0;
     }
   }
   __syncthreads();
@@ -147,11 +149,11 @@ __global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restr
   for (int u = 0; u < 4; ++u) {
     const int64_t i = i0 + u;
     const bool ok = i < be;
-    r[u] = ok ? crow[i] : INT32_MIN;
-    v[u] = ok ? cval[i] : 0.0;
-    st[u] = ok && (i == bs || crow[i - 1] != r[u]);
-    en[u] = ok && (i == be - 1 || crow[i + 1] != r[u]);
-    if (en[u] && i < be - 1) atomicMin((unsigned long long*)&first_end, (unsigned long long)i);
+    r[u] = ok ? __ldcg(crow + i) : INT32_MIN;
+    v[u] = ok ? __ldcg(cval + i) : 0.0;
+    st[u] = ok && (i == bs || __ldcg(crow + i - 1) != r[u]);
+    en[u] = ok && (i == be - 1 || __ldcg(crow + i + 1) != r[u]);
+    if (en[u] && i < be - 1) atomicMin(&first_end, (unsigned long long)i);
   }
   // thread-local segmented inclusive sums
   double acc = 0.0;
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restr
     }
     ex = pre + ex;
   }
-  const int64_t e1 = first_end;
+  const int64_t e1 = (int64_t)first_end;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     if (!en[u] || r[u] < 0) continue;
@@ -212,18 +214,42 @@ __global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restr
       // neighbours' pieces
       const bool whole = in_first && head_open;
       if (whole) {
-        orow[2 * blockIdx.x] = r[u];
-        oval[2 * blockIdx.x] = sum;
+        orow[2 * blk] = r[u];
+        oval[2 * blk] = sum;
       }
-      orow[2 * blockIdx.x + 1] = r[u];
-      oval[2 * blockIdx.x + 1] = whole ? 0.0 : sum;
+      orow[2 * blk + 1] = r[u];
+      oval[2 * blk + 1] = whole ? 0.0 : sum;
     } else if (in_first && head_open) {
-      orow[2 * blockIdx.x] = r[u];
-      oval[2 * blockIdx.x] = sum;
+      orow[2 * blk] = r[u];
+      oval[2 * blk] = sum;
     } else {
       y[r[u]] = set ? sum : y[r[u]] + sum;
     }
   }
+  __syncthreads();  // smem reuse by a following fixup_block in the same CTA
+}
+
+// level kernel; the last CTA to finish also runs the next level when it fits
+// in one CTA (the usual case: saves a launch)
+__global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restrict__ crow,
+                                                          const double* __restrict__ cval, int64_t n,
+                                                          double* __restrict__ y, int set,
+                                                          int32_t* __restrict__ orow, double* __restrict__ oval,
+                                                          unsigned int* __restrict__ done) {
+  fixup_block(crow, cval, n, blockIdx.x, y, set, orow, oval);
+  const int64_t n2 = 2 * (int64_t)gridDim.x;
+  if (!orow || !done || n2 > kFixItems) return;
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (last) *done = 0u;  // ready for the next launch
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  fixup_block(orow, oval, n2, 0, y, set, nullptr, nullptr);
 }
 
 int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int64_t max_run, cudaStream_t s) {
@@ -232,6 +258,7 @@ int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int
     fixup_kernel<<<(int)((T + kNT - 1) / kNT), kNT, 0, s>>>(crow, cval, T, y, set);
     return 1;
   }
+  unsigned int* done = reinterpret_cast<unsigned int*>(crow + fixup_capacity(T));
   int launches = 0;
   int64_t n = T;
   int32_t* cr = crow;
@@ -241,9 +268,9 @@ int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int
     const int64_t nb = (n + kFixItems - 1) / kFixItems;
     int32_t* orow = nb > 1 ? crow + off : nullptr;
     double* oval = nb > 1 ? cval + off : nullptr;
-    fixup_level_kernel<<<(int)nb, kNT, 0, s>>>(cr, cv, n, y, set, orow, oval);
+    fixup_level_kernel<<<(int)nb, kNT, 0, s>>>(cr, cv, n, y, set, orow, oval, done);
     ++launches;
-    if (nb == 1) break;
+    if (nb == 1 || 2 * nb <= kFixItems) break;  // the last CTA ran the final level
     cr = orow;
     cv = oval;
     n = 2 * nb;
@@ -331,9 +358,16 @@ __global__ void __launch_bounds__(kNT) long_chunk_kernel(const RP* __restrict__ 
   }
 }
 
+static int diag_skip() {  // diagnostics only (SPMV_DIAG_SKIP=1: no long rows, 2: no bins); y is then wrong
+  static int v = [] { const char* e = getenv("SPMV_DIAG_SKIP"); return e ? atoi(e) : 0; }();
+  return v;
+}
+
 int launch_split(const ExecArgs& a, cudaStream_t s) {
+  if (a.split_fused && a.use_nz && a.long_tiled && a.n_long > 0 && a.nz.T > 0 && diag_skip() == 0)
+    return launch_split_fused(a, s);
   int n = 0;
-  const bool longs = a.n_long > 0 && (a.long_tiled || a.n_chunks > 0);
+  const bool longs = a.n_long > 0 && (a.long_tiled || a.n_chunks > 0) && diag_skip() != 1;
   // 0. rows in no bin must read 0: legacy stream bins (empty rows), or an
   //    nnz_split bin without nonzeros
   if (a.stage != 2 && a.A.m > 0 && ((!a.use_nz && a.zero_y) || (a.use_nz && a.nz.T == 0)))
@@ -371,9 +405,12 @@ int launch_split(const ExecArgs& a, cudaStream_t s) {
   if (conc) cudaEventRecord(a.ev_join, ls);
   // 2. short / medium rows: one nnz_split bin, or cta_stream length bins
   //    (rows mapped back to y through the bin's row map; disjoint rows)
-  if (a.use_nz) n += launch_nz_plan(a.nz, a.x, a.y, a.stage, s);
-  else
+  if (diag_skip() == 2) {
+  } else if (a.use_nz) {
+    n += launch_nz_plan(a.nz, a.x, a.y, a.stage, s);
+  } else {
     for (int b = 0; b < a.n_sp; ++b) n += launch_stream_plan(a.sp[b], a.x, a.y, a.stage, s);
+  }
   if (conc) cudaStreamWaitEvent(s, a.ev_join, 0);
   return n;
 }

@@ -41,7 +41,8 @@ def m_maxlen(m):
 
 VARIANTS = [("vector", 1), ("vector", 2), ("vector", 8), ("vector", 32), ("stream", 1), ("stream", 4),
             ("stream", 8), ("stream", 32), ("stream_seg", 1), ("stream_nnz_tiles", 1), ("merge", 0), ("split", 4),
-    ("split_seg", 32), ("split_chunks", 16), ("split_tiled", 8), ("split_bins", 8), ("nnzsplit", 0)]
+    ("split_seg", 32), ("split_chunks", 16), ("split_tiled", 8), ("split_bins", 8), ("nnzsplit", 0),
+    ("nnzsplit_hot", 0), ("nnzsplit_nohot", 0)]
 ALL = ("vector", "stream", "merge", "split", "nnzsplit")
 
 SUITE = sg.small_suite(seed=21)
@@ -57,6 +58,10 @@ def variant_kw(variant):
         return "split", {"seg": 1, "split_bins": 0}
     if variant == "split_bins":
         return "split", {"split_bins": 0}
+    if variant == "nnzsplit_hot":
+        return "nnzsplit", {"hot_x": 64}
+    if variant == "nnzsplit_nohot":
+        return "nnzsplit", {"hot_x": 0}
     if variant == "split_chunks":
         return "split", {"long_mode": 1}
     if variant == "split_tiled":
@@ -142,6 +147,12 @@ def test_plan_structures_bit_exact(name, m):
     assert np.array_equal(pz.export("nz_rpc"), rpc)
     assert np.array_equal(pz.export("nz_tile_q"), oracle.nz_tiles(rpc) if m.nnz else np.array([0]))
     assert pz.info()["n_nz_rows"] == rowmap.size - 1
+    ph = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="nnzsplit", hot_x=100)
+    hot, cov = oracle.hot_columns(m.colind, m.x.size, 100)
+    assert np.array_equal(ph.export("nz_hot_cols"), hot) and ph.info()["n_hot"] == hot.size
+    if m.nnz:
+        assert abs(ph.info()["hot_cover"] - cov / m.nnz) < 1e-15
+    assert_bound(ph.execute(m.x), m)
     # features: exact integers, identical doubles (same formula, IEEE sqrt)
     f = oracle.features(m.rowptr, m.colind, n_cols=m.x.size)
     g = pm.info()["feat"]
@@ -334,3 +345,16 @@ def test_nzsplit_edges(name, lens, rp_dtype):
         y = p.execute(m.x, np.full(m.n, np.nan))
         assert_bound(y, m)
         assert np.all(y[lens == 0] == 0.0)
+
+
+@pytest.mark.parametrize("K", [2, 1000, 16384])
+def test_nzsplit_hot_sizes(K):
+    m = sg.config(3, small=True)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="nnzsplit", hot_x=K)
+    hot, _ = oracle.hot_columns(m.colind, m.n, min(K, 16384))
+    assert p.info()["n_hot"] == hot.size
+    y = p.execute(m.x)
+    assert_bound(y, m)
+    for _ in range(2):  # x changes between calls: the hot table is refreshed per SpMV
+        x2 = m.x[::-1].copy()
+        assert_bound(p.execute(x2), sg.CSR(m.n, m.rowptr, m.colind, m.vals, x2))

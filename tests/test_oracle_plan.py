@@ -317,3 +317,32 @@ def test_nz_structures_rederived(seed):
         for kk in k[:: max(1, T // 50)]:
             q = tq[kk]
             assert rpc[q] <= kk * W < rpc[q + 1]
+
+
+# ---- nnz_split hot-x set (reading 20) ------------------------------------
+def test_hot_columns_hand_example():
+    # column counts: c0:5, c1:1, c2:3, c3:3, c4:0, c5:2
+    ci = np.array([0, 0, 0, 0, 0, 1, 2, 2, 2, 3, 3, 3, 5, 5], np.int32)
+    hot, cov = oracle.hot_columns(ci, 6, K=4)   # cnt >= 2: columns 0, 2, 3, 5
+    assert hot.tolist() == [0, 2, 3, 5] and cov == 13
+    hot, cov = oracle.hot_columns(ci, 6, K=6)   # cnt >= 1: 5 columns -> 4
+    assert hot.tolist() == [0, 1, 2, 3] and cov == 12
+    hot, cov = oracle.hot_columns(ci, 6, K=2)   # cnt >= 5 only c0 -> 0 columns (even)
+    assert hot.tolist() == [] and cov == 0
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_hot_columns_threshold_maximal(seed):
+    g = np.random.default_rng(seed)
+    n = 5000
+    ci = np.minimum((g.pareto(1.1, 40000) * 10).astype(np.int64), n - 1).astype(np.int32)
+    cnt = np.bincount(ci, minlength=n)
+    for K in (16, 256, 1000):
+        hot, cov = oracle.hot_columns(ci, n, K)
+        assert hot.size <= K and hot.size % 2 == 0 and np.all(np.diff(hot) > 0)
+        assert cov == cnt[hot].sum()
+        # brute force: t = the smallest count >= 1 whose columns (cnt >= t)
+        # number <= K, unless even the top bucket exceeds K
+        t = next((v for v in range(1, 4096) if np.count_nonzero(cnt >= v) <= K), 4095)
+        cand = np.flatnonzero(cnt >= t)
+        assert np.array_equal(hot, cand[:min(cand.size, K) & ~1])
