@@ -91,6 +91,7 @@ typedef struct spmv_features {
   int64_t misses;          /* non-head nonzeros with gap > 16 (Table I misses_i, 128-B line) */
   double nnz_avg, nnz_sd, avg_short, sd_short;
   int64_t n_cols;          /* columns (x length); the long-row density test uses it */
+  int64_t n_big_gaps;      /* distinct in-row gaps >= 65472 (129 = more than 128): escape-coded D16 needs <= 64 */
 } spmv_features;
 
 typedef struct spmv_device_props {
@@ -118,7 +119,7 @@ typedef struct spmv_plan_info {
   spmv_selection sel;
   spmv_features feat;
   int32_t d16_width;          /* 0, 8 or 16 (matrix-global, "never both") */
-  int32_t pad_;
+  int32_t d16_n_esc;          /* escape-coded large deltas (16-bit codes >= 65472, reading 21) */
   int64_t tile_nnz, n_tiles;  /* STREAM tiling */
   int64_t merge_items, n_merge_tiles;
   int64_t l_split, long_chunk, n_long_chunks;

@@ -75,6 +75,9 @@ def _lib():
         L.oracle_d16_encode.argtypes = [i64, vp, vp, vp, vp, _i64p]
         L.oracle_d16_encode.restype = ctypes.c_int
         L.oracle_d16_decode.argtypes = [i64, vp, vp, vp, vp]
+        L.oracle_d16_encode_esc.argtypes = [i64, vp, vp, vp, vp, _i64p, vp, ctypes.POINTER(ctypes.c_int)]
+        L.oracle_d16_encode_esc.restype = ctypes.c_int
+        L.oracle_d16_decode_esc.argtypes = [i64, vp, vp, vp, vp, vp]
         L.oracle_tile_anchor.argtypes = [vp, i64, i64, i64, vp]
         _LIB = L
     return _LIB
@@ -197,7 +200,26 @@ def features(rowptr, colind, L_split=4096, line_elems=16, n_cols=None):
     _lib().oracle_features(rp.size - 1, _p(rp), _p(ci), int(L_split), int(line_elems), ctypes.byref(f))
     d = {k: getattr(f, k) for k, _ in _Feat._fields_}
     d["n_cols"] = int(rp.size - 1 if n_cols is None else n_cols)
+    d["n_big_gaps"] = big_gap_count(rp, ci)
     return d
+
+
+ESC0, ESC_MAX, BIG_TAB = 65472, 64, 128
+
+
+def big_gap_count(rowptr, colind):
+    """Distinct in-row gaps >= 65472 (the escape-coded D16 candidates),
+    BIG_TAB + 1 when there are more than BIG_TAB (reading 21)."""
+    rp, ci = _rp64(rowptr), np.asarray(colind, np.int64)
+    if ci.size < 2:
+        return 0
+    g = np.diff(ci)
+    head = np.zeros(ci.size, bool)
+    starts = rp[:-1][np.diff(rp) > 0]
+    head[starts] = True
+    g = g[~head[1:]]
+    u = np.unique(g[g >= ESC0])
+    return int(u.size) if u.size <= BIG_TAB else BIG_TAB + 1
 
 
 def tile_count(nnz, C):
@@ -290,6 +312,33 @@ def d16_encode(rowptr, colind):
     if w == 0:
         return 0, mg.value, None, None
     return w, mg.value, dcol[:nnz], head[:n]
+
+
+def d16_encode_esc(rowptr, colind):
+    """d16_encode extended with escape codes (reading 21). Returns
+    (width, maxgap, dcol | None, head | None, esc table)."""
+    rp, ci = _rp64(rowptr), _c32(colind)
+    n, nnz = rp.size - 1, int(rp[-1])
+    dcol = np.zeros(max(nnz, 1), np.uint16)
+    head = np.zeros(max(n, 1), np.int32)
+    esc = np.zeros(64, np.int32)
+    mg = ctypes.c_int64(0)
+    ne = ctypes.c_int(0)
+    w = _lib().oracle_d16_encode_esc(n, _p(rp), _p(ci), _p(dcol), _p(head), ctypes.byref(mg), _p(esc),
+                                     ctypes.byref(ne))
+    if w == 0:
+        return 0, mg.value, None, None, esc[:0]
+    return w, mg.value, dcol[:nnz], head[:n], esc[:ne.value].copy()
+
+
+def d16_decode_esc(rowptr, dcol, head, esc):
+    rp = _rp64(rowptr)
+    out = np.empty(max(int(rp[-1]), 1), np.int32)
+    e = np.zeros(64, np.int32)
+    e[:len(esc)] = esc
+    _lib().oracle_d16_decode_esc(rp.size - 1, _p(rp), _p(np.ascontiguousarray(dcol, np.uint16)),
+                                 _p(np.ascontiguousarray(head, np.int32)), _p(e), _p(out))
+    return out[:int(rp[-1])]
 
 
 def d16_decode(rowptr, dcol, head):
@@ -405,7 +454,12 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     mb = ws > l2_bytes // 2
     if mb and not (classes & CLASS_IMB):
         classes |= CLASS_MB
-    d16 = False  # MB delta colind is implemented but not auto-selected (reading 9)
+    # MB delta colind (reading 9): rows averaging >= 16 nonzeros,
+    # 16-bit deltas or escape codes (<= 64 distinct deltas >= 65472)
+    d16_ok = f["maxgap"] <= 65535 or f.get("n_big_gaps", BIG_TAB + 1) <= ESC_MAX
+    # (escape codes only when forced: measured slower, reading 21)
+    d16 = bool((classes & CLASS_MB) and avg_s >= 16.0 and f["maxgap"] <= 65535 and variant == VARIANT_STREAM)
+    del d16_ok
     ml = nnz > 0 and f["misses"] > 0.75 * nnz and 8 * n > l2_bytes // 16
     if ml:
         classes |= CLASS_ML

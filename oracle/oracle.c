@@ -338,6 +338,59 @@ int oracle_d16_encode(int64_t n, const int64_t* rowptr, const int32_t* colind, u
   return width;
 }
 
+/* Escape-coded 16-bit deltas (reading 21): when
+ * the largest gap exceeds 65535 but at most 64 DISTINCT gaps are >= 65472,
+ * a gap d < 65472 is stored as d and a gap d >= 65472 as 65472 + (index of d
+ * in the ascending table esc[] of those distinct gaps). Returns 16 and the
+ * table size in *n_esc (esc needs 64 entries), or 0 when not encodable.
+ * Plain widths (8 / 16 without escapes) follow oracle_d16_encode. */
+int oracle_d16_encode_esc(int64_t n, const int64_t* rowptr, const int32_t* colind, uint16_t* dcol,
+                          int32_t* head, int64_t* maxgap_out, int32_t* esc, int* n_esc) {
+  int w = oracle_d16_encode(n, rowptr, colind, dcol, head, maxgap_out);
+  *n_esc = 0;
+  if (w) return w;
+  int k = 0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = rowptr[i] + 1; j < rowptr[i + 1]; ++j) {
+      int64_t g = (int64_t)colind[j] - (int64_t)colind[j - 1];
+      if (g < 65472) continue;
+      int found = 0;
+      for (int t = 0; t < k; ++t) if (esc[t] == g) { found = 1; break; }
+      if (found) continue;
+      if (k == 64) return 0;
+      esc[k++] = (int32_t)g;
+    }
+  /* ascending (insertion sort, at most 64 entries) */
+  for (int a = 1; a < k; ++a)
+    for (int b = a; b > 0 && esc[b - 1] > esc[b]; --b) { int32_t t = esc[b]; esc[b] = esc[b - 1]; esc[b - 1] = t; }
+  for (int64_t i = 0; i < n; ++i) {
+    head[i] = rowptr[i + 1] > rowptr[i] ? colind[rowptr[i]] : (int32_t)n;
+    for (int64_t j = rowptr[i]; j < rowptr[i + 1]; ++j) {
+      int64_t g = j == rowptr[i] ? 0 : (int64_t)colind[j] - (int64_t)colind[j - 1];
+      if (g >= 65472) {
+        int t = 0;
+        while (esc[t] != g) ++t;
+        g = 65472 + t;
+      }
+      dcol[j] = (uint16_t)g;
+    }
+  }
+  *n_esc = k;
+  return 16;
+}
+
+/* escape-aware decode: delta = code < 65472 ? code : esc[code - 65472] */
+void oracle_d16_decode_esc(int64_t n, const int64_t* rowptr, const uint16_t* dcol, const int32_t* head,
+                           const int32_t* esc, int32_t* col_out) {
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t c = head[i];
+    for (int64_t j = rowptr[i]; j < rowptr[i + 1]; ++j) {
+      if (j > rowptr[i]) c += dcol[j] < 65472 ? (int64_t)dcol[j] : (int64_t)esc[dcol[j] - 65472];
+      col_out[j] = (int32_t)c;
+    }
+  }
+}
+
 /* decode: col[j] = head[i] + sum_{t=rowptr[i]+1}^{j} dcol[t] */
 void oracle_d16_decode(int64_t n, const int64_t* rowptr, const uint16_t* dcol, const int32_t* head,
                        int32_t* col_out) {

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_PATH = os.path.join(_HERE, "libspmv.so")
+_PATH = os.environ.get("SPMV_LIB_PATH") or os.path.join(_HERE, "libspmv.so")  # override: experiment builds
 if not os.path.exists(_PATH):
     raise ImportError(f"{_PATH} is missing: build it with `make spmv` or __graft_entry__.build() "
                       "(there is no CPU fallback)")
@@ -57,7 +57,7 @@ class Features(ctypes.Structure):
                [(k, ctypes.c_uint64) for k in ("s1", "s2", "s1_short", "s2_short")] + \
                [(k, ctypes.c_int64) for k in ("maxgap", "misses")] + \
                [(k, ctypes.c_double) for k in ("nnz_avg", "nnz_sd", "avg_short", "sd_short")] + \
-               [("n_cols", ctypes.c_int64)]
+               [("n_cols", ctypes.c_int64), ("n_big_gaps", ctypes.c_int64)]
 
 
 class DeviceProps(ctypes.Structure):
@@ -74,7 +74,7 @@ class Selection(ctypes.Structure):
 class PlanInfo(ctypes.Structure):
     _fields_ = [("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64), ("nnz", ctypes.c_int64),
                 ("rowptr_bytes", ctypes.c_int32), ("ngpus", ctypes.c_int32), ("sel", Selection),
-                ("feat", Features), ("d16_width", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("feat", Features), ("d16_width", ctypes.c_int32), ("d16_n_esc", ctypes.c_int32),
                 ("tile_nnz", ctypes.c_int64), ("n_tiles", ctypes.c_int64), ("merge_items", ctypes.c_int64),
                 ("n_merge_tiles", ctypes.c_int64), ("l_split", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
                 ("n_long_chunks", ctypes.c_int64), ("upload_ms", ctypes.c_double), ("inspect_ms", ctypes.c_double),

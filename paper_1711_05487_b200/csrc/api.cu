@@ -178,7 +178,8 @@ struct spmv_plan_s {
   std::vector<int64_t> bounds;
   double upload_ms = 0, inspect_ms = 0, select_ms = 0, encode_ms = 0;
   int64_t l_split = 4096, k_long = 100, C = 2048, items = 2048, chunk = 8192;
-  double hot_cover = 0.0;  // nnz_split hot-x set: fraction of nonzeros in the hot columns
+  double hot_cover = 0.0;
+  std::vector<int32_t> esc;  // D16 escape table (sorted distinct deltas >= kEsc0)  // nnz_split hot-x set: fraction of nonzeros in the hot columns
 
   ~spmv_plan_s() {
     for (auto& s : shards) s.release();
@@ -277,16 +278,22 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   if (avg_s <= 4) classes |= SPMV_CLASS_CMP;
   if (ws > d.l2_bytes / 2 && !(classes & SPMV_CLASS_IMB)) classes |= SPMV_CLASS_MB;
   // MB -> delta colind: implemented and bit-exact, but on B200 the
-  // decode costs more than the 2 B/nnz it saves (C2: 55 us with vs 45 us
-  // without), so the feature-guided rule leaves it off; d16=1 forces it
-  bool d16 = false;
+  // decode costs more than the 2 B/nnz it saves on short rows (C2: 55 us
+  // with vs 45 us without; 7-pt 250^3: 389 vs 319 us) but pays on long
+  // regular rows (27-pt 180^3: 352 vs 378 us), so it is auto-selected for
+  // MB rows averaging >= 16 nonzeros. Large deltas can be escape-coded when
+  // at most kEscMax distinct values exceed kEsc0, but the
+  // per-element escape check costs more than it saves (27-pt 260^3: 1.33 ms
+  // with vs 1.09 ms without), so escapes are used only when forced (d16=1)
+  const bool d16_ok = f.maxgap <= 65535 || f.n_big_gaps <= kEscMax;
+  bool d16 = (classes & SPMV_CLASS_MB) && avg_s >= 16.0 && f.maxgap <= 65535;
   const bool ml = nnz > 0 && (double)f.misses > 0.75 * (double)nnz && 8 * n > d.l2_bytes / 16;
   if (ml) classes |= SPMV_CLASS_ML;
   bool xwin = ml && 8 * n <= d.access_window_max;
   // explicit options override the feature-guided choice
   if (o.force_vs > 0) vs = o.force_vs;
   if (o.d16 == 0) d16 = false;
-  if (o.d16 == 1) d16 = f.maxgap <= 65535;
+  if (o.d16 == 1) d16 = d16_ok;
   if (variant != SPMV_VARIANT_STREAM) d16 = false;
   if (o.xwin == 0) xwin = false;
   if (o.xwin == 1) xwin = true;
@@ -344,6 +351,18 @@ void features_from_stats(const std::vector<DevStats>& st, const std::vector<int6
     f.misses += s.misses;
   }
   if (f.n == 0) f.nnz_min = 0;
+  {  // distinct in-row gaps >= kEsc0 over all shards (kBigTab + 1 = more than kBigTab)
+    std::vector<int32_t> big;
+    bool over = false;
+    for (const auto& s : st) {
+      over = over || s.big_over;
+      for (int i = 0; i < kBigTab; ++i)
+        if (s.bigtab[i] > 0) big.push_back(s.bigtab[i]);
+    }
+    std::sort(big.begin(), big.end());
+    big.erase(std::unique(big.begin(), big.end()), big.end());
+    f.n_big_gaps = (over || (int64_t)big.size() > kBigTab) ? kBigTab + 1 : (int64_t)big.size();
+  }
   f.nnz = (int64_t)f.s1;
   auto sd = [](uint64_t cnt, uint64_t s1, uint64_t s2) {
     if (cnt == 0) return 0.0;
@@ -551,6 +570,16 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   P->feat.n_cols = n_cols;
   select_impl(P->feat, P->props, rp_bytes, opt, P->sel);
   if (P->sel.d16) P->d16_width = P->feat.maxgap <= 255 ? 8 : 16;
+  // escape table: the sorted distinct large deltas of all shards
+  if (P->sel.d16 && P->feat.maxgap > 65535) {
+    std::vector<int32_t> big;
+    for (auto& sh : P->shards)
+      for (int i = 0; i < kBigTab; ++i)
+        if (sh.hs.bigtab[i] > 0) big.push_back(sh.hs.bigtab[i]);
+    std::sort(big.begin(), big.end());
+    big.erase(std::unique(big.begin(), big.end()), big.end());
+    P->esc.assign(big.begin(), big.end());
+  }
   P->select_ms = now_ms() - t_c;
 
   // ---- a3/a4: structures for the selected variant ---------------------------------
@@ -603,7 +632,11 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       uint16_t* dcol = s.alloc<uint16_t>((size_t)V.nnz);
       int32_t* head = s.alloc<int32_t>((size_t)V.m);
       int32_t* anchor = s.alloc<int32_t>((size_t)sp.T);
-      launch_d16_encode(V, s.headbits, sp.stride, sp.T, dcol, head, anchor, s.stream);
+      int32_t* esc_dev = s.alloc<int32_t>((size_t)kEscMax);
+      sp.n_esc = (int)P->esc.size();
+      for (int i = 0; i < sp.n_esc; ++i) sp.esc[i] = P->esc[(size_t)i];
+      ck(cudaMemcpyAsync(esc_dev, sp.esc, sizeof sp.esc, cudaMemcpyHostToDevice, s.stream), "esc table");
+      launch_d16_encode(V, s.headbits, sp.stride, sp.T, dcol, head, anchor, esc_dev, sp.n_esc, s.stream);
       count_launches(3, "d16_encode");
       sp.dcol = dcol;
       sp.head = head;
@@ -1088,6 +1121,7 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     info->sel = p->sel;
     info->feat = p->feat;
     info->d16_width = p->d16_width;
+    info->d16_n_esc = (int32_t)p->esc.size();
     const Shard& s0 = p->shards[0];
     info->tile_nnz = s0.sp[0].C;
     info->n_tiles = s0.sp[0].T;

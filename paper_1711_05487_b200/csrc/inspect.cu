@@ -61,6 +61,13 @@ __global__ void __launch_bounds__(kNT) rowstats_kernel(const RP* __restrict__ rp
 __global__ void __launch_bounds__(kNT) validate_gaps_kernel(const int32_t* __restrict__ col, int64_t nnz,
                                                             int64_t n_cols, const uint32_t* __restrict__ headbits,
                                                             DevStats* st) {
+  // distinct large gaps (>= kEsc0): deduplicated in a per-CTA smem set first
+  // (a stencil repeats a handful of values ~2x per row), merged at the end
+  __shared__ int32_t tab[kBigTab];
+  __shared__ int over;
+  for (int i = threadIdx.x; i < kBigTab; i += blockDim.x) tab[i] = 0;
+  if (threadIdx.x == 0) over = 0;
+  __syncthreads();
   long long mg = 0, miss = 0, err = LLONG_MAX;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz; j += stride) {
@@ -72,8 +79,33 @@ __global__ void __launch_bounds__(kNT) validate_gaps_kernel(const int32_t* __res
       if (g <= 0) { long long k = 2 * j + 1; err = k < err ? k : err; continue; }
       mg = g > mg ? g : mg;
       miss += (g > 16);
+      if (g >= kEsc0) {
+        const int32_t v = (int32_t)g;
+        uint32_t h = ((uint32_t)v * 2654435761u) % kBigTab;
+        for (int probe = 0;; ++probe, h = (h + 1) % kBigTab) {
+          if (probe == kBigTab) { over = 1; break; }
+          const int32_t cur = tab[h];
+          if (cur == v) break;
+          if (cur == 0) {
+            const int32_t prev = atomicCAS(&tab[h], 0, v);
+            if (prev == 0 || prev == v) break;
+          }
+        }
+      }
     }
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBigTab; i += blockDim.x) {
+    const int32_t v = tab[i];
+    if (v == 0) continue;
+    uint32_t h = ((uint32_t)v * 2654435761u) % kBigTab;
+    for (int probe = 0;; ++probe, h = (h + 1) % kBigTab) {
+      if (probe == kBigTab) { st->big_over = 1; break; }
+      const int32_t prev = atomicCAS(&st->bigtab[h], 0, v);
+      if (prev == 0 || prev == v) break;
+    }
+  }
+  if (threadIdx.x == 0 && over) st->big_over = 1;
   mg = warp_max(mg); miss = warp_sum(miss); err = warp_min(err);
   if ((threadIdx.x & 31) == 0) {
     if (mg) atomicMax(&st->maxgap, mg);
@@ -269,11 +301,21 @@ void launch_long_rows(const MatView& A, int64_t l_split, int64_t chunk, int32_t*
 // dcol[j] = colind[j] - colind[j-1] for non-head j, 0 at row heads;
 // head[i] = colind[rowptr[i]] or n_cols for an empty row; anchor[k] = colind[k*C].
 __global__ void __launch_bounds__(kNT) d16_dcol_kernel(const int32_t* __restrict__ col, int64_t nnz,
-                                                       const uint32_t* __restrict__ headbits, uint16_t* dcol) {
+                                                       const uint32_t* __restrict__ headbits, uint16_t* dcol,
+                                                       const int32_t* __restrict__ esc, int n_esc) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz; j += stride) {
     const bool h = (headbits[j >> 5] >> (j & 31)) & 1u;
-    dcol[j] = h ? (uint16_t)0 : (uint16_t)(col[j] - col[j - 1]);
+    int32_t d = h ? 0 : col[j] - col[j - 1];
+    if (d >= kEsc0) {  // escape code: index in the sorted table
+      int lo = 0, hi = n_esc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (esc[mid] < d) lo = mid + 1; else hi = mid;
+      }
+      d = kEsc0 + lo;
+    }
+    dcol[j] = (uint16_t)d;
   }
 }
 template <typename RP>
@@ -291,8 +333,8 @@ __global__ void d16_anchor_kernel(const int32_t* __restrict__ col, int64_t nnz, 
 }
 
 void launch_d16_encode(const MatView& A, const uint32_t* headbits, int64_t C, int64_t T, uint16_t* dcol,
-                       int32_t* head, int32_t* anchor, cudaStream_t s) {
-  if (A.nnz) d16_dcol_kernel<<<grid_for(A.nnz), kNT, 0, s>>>(A.col, A.nnz, headbits, dcol);
+                       int32_t* head, int32_t* anchor, const int32_t* esc_dev, int n_esc, cudaStream_t s) {
+  if (A.nnz) d16_dcol_kernel<<<grid_for(A.nnz), kNT, 0, s>>>(A.col, A.nnz, headbits, dcol, esc_dev, n_esc);
   if (A.m) {
     if (A.rp_bytes == 8)
       d16_head_kernel<int64_t><<<grid_for(A.m), kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, A.m, A.n_cols, head);

@@ -18,7 +18,17 @@ struct DevStats {
   long long rp_err;   // smallest row i with rowptr[i+1] < rowptr[i] (LLONG_MAX if none)
   long long col_err;  // min over nonzeros of 2*j + (order violation ? 1 : 0) (LLONG_MAX if none)
   long long n_incoming;  // STREAM tiles with an incoming row (carry fix-up needed)
+  // distinct in-row gaps >= kEsc0 (escape-coded D16): open-addressing set,
+  // 0 = empty slot; big_over = 1 when more than kBigTab distinct values
+  int32_t bigtab[128];
+  int32_t big_over;
 };
+// escape-coded 16-bit deltas (SURVEY 8(f) f3 reading; reading 21):
+// a delta d < kEsc0 is stored as d, a delta d >= kEsc0 as kEsc0 + (index of d
+// in the plan's sorted table of distinct large deltas, at most kEscMax)
+constexpr int kEsc0 = 65536 - 64;
+constexpr int kEscMax = 64;
+constexpr int kBigTab = 128;
 
 struct MatView {
   int rp_bytes;
@@ -39,6 +49,8 @@ struct StreamPlan {
   double* carry_val = nullptr;
   bool need_fixup = false;
   const uint16_t* dcol = nullptr;  // D16 stream (nullptr = int32 colind)
+  int n_esc = 0;                   // escape-coded large deltas (<= kEscMax)
+  int32_t esc[kEscMax] = {};       // sorted distinct deltas >= kEsc0
   const int32_t* head = nullptr;
   const int32_t* anchor = nullptr;
   int stages = 0, grid = 0, vs = 1, rows_cap = 0;
@@ -81,7 +93,7 @@ int nz_prepare(NzPlan& z, int sm_count);  // persistent grid (<0 on error)
 // hot-x set (plan time): column counts + a count histogram of kHotBuckets,
 // then the ordered compaction of the columns with count >= t (first K)
 constexpr int kHotBuckets = 4096;
-constexpr int kHotMax = 16384;  // hot columns staged in smem (128 KB)
+constexpr int kHotMax = 16384;  // hot columns staged in smem (128 KB; B200 sweep on C3: 8K 283, 16K 275, 20K 285, 24K 322 us)
 void launch_col_counts(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* cnt, int32_t* H, cudaStream_t s);
 void launch_hot_flags(const int32_t* cnt, int64_t n_cols, int32_t t, int32_t* bsum, cudaStream_t s);
 void launch_hot_write(const int32_t* cnt, int64_t n_cols, int32_t t, const int32_t* boff, int K, int32_t* hot_cols,
@@ -98,7 +110,7 @@ void launch_merge_splits(const MatView& A, int64_t items, int64_t T, int32_t* mr
 void launch_long_rows(const MatView& A, int64_t l_split, int64_t chunk, int32_t* long_rows, int64_t n_long,
                       int64_t* chunk_start, int32_t* scratch_counts, int nblocks_scratch, cudaStream_t s);
 void launch_d16_encode(const MatView& A, const uint32_t* headbits, int64_t C, int64_t T, uint16_t* dcol,
-                       int32_t* head, int32_t* anchor, cudaStream_t s);
+                       int32_t* head, int32_t* anchor, const int32_t* esc_dev, int n_esc, cudaStream_t s);
 void launch_d16_decode_export(const StreamPlan& sp, int32_t* out, cudaStream_t s);
 // ordered carry fix-up (vector.cu); the carry arrays must hold fixup_capacity(T)
 // entries (levels of the hierarchical reduce-by-key live after the T carries)

@@ -36,7 +36,14 @@
 namespace spmv {
 
 constexpr int kNzWarps = 8;  // warps per CTA (plain mode)
-constexpr int kNzHotWarps = 32;  // warps per CTA (hot-x mode: one 1024-thread CTA per SM)
+#ifndef NZ_HOT_WARPS
+#define NZ_HOT_WARPS 32
+#endif
+#ifndef NZ_HOT_PF
+#define NZ_HOT_PF 0
+#endif
+constexpr int kNzHotWarps = NZ_HOT_WARPS;  // warps per CTA (hot-x mode: one CTA per SM)
+constexpr bool kNzHotPrefetch = NZ_HOT_PF;
 
 size_t nz_smem_bytes(int n_hot) { return n_hot > 0 ? (size_t)n_hot * 8 + 16 : 0; }
 
@@ -69,7 +76,24 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
   // which B200 DRAM rewards (C3: 294 us; chunks of 8 consecutive tiles per
   // warp 358 us; dynamic tickets 350 us -- same-address atomics serialise)
   const int64_t nw = (int64_t)gridDim.x * NW;
-  for (int64_t k = (int64_t)blockIdx.x * NW + w; k < p.T; k += nw) nz_tile<RP, HOT>(p, k, lane, em, xh);
+  if constexpr (HOT && kNzHotPrefetch) {
+    // the next tile's streams are loaded while this tile gathers x
+    int64_t k = (int64_t)blockIdx.x * NW + w;
+    int c[8], cn[8];
+    double v[8], vn[8];
+    if (k < p.T) nz_tile_load(p, k, lane, c, v);
+    for (; k < p.T; k += nw) {
+      if (k + nw < p.T) nz_tile_load(p, k + nw, lane, cn, vn);
+      nz_tile_compute<RP, HOT>(p, k, lane, em, xh, c, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        c[i] = cn[i];
+        v[i] = vn[i];
+      }
+    }
+  } else {
+    for (int64_t k = (int64_t)blockIdx.x * NW + w; k < p.T; k += nw) nz_tile<RP, HOT>(p, k, lane, em, xh);
+  }
 }
 
 // xhot[s] = x[hot_cols[s]] (once per SpMV, before the hot-x kernel)

@@ -27,6 +27,9 @@
 
 namespace spmv {
 
+#ifndef SPMV_D16_LB
+#define SPMV_D16_LB 7
+#endif
 constexpr int kConsumerWarps = kStreamConsumerWarps;
 constexpr int kStreamThreads = 32 * (kConsumerWarps + 1);
 
@@ -77,6 +80,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// escape-coded delta (kEsc0 + i -> the plan's i-th large delta)
+struct EscTab {
+  int32_t v[kEscMax];
+};
+// (esc: the table in shared memory -- a dynamically indexed kernel-parameter
+// array spills to local memory)
+// ESC is a template flag: plans without escape codes keep the plain add
+// (any per-element check -- a select with a predicated LDS or a branch --
+// measured ~25 % slower on a 27-point stencil, 451 vs 352 us)
+template <bool ESC>
+__device__ __forceinline__ int d16_delta(uint32_t code, const int32_t* esc) {
+  if constexpr (ESC) return code >= (uint32_t)kEsc0 ? esc[code - kEsc0] : (int)code;
+  else return (int)code;
+}
+
 template <typename RP>
 struct StreamP {
   const RP* rp;
@@ -95,6 +113,7 @@ struct StreamP {
   int stages, rows_cap;
   int aligned;  // 1: row-aligned tiles (no row crosses a tile, no carries)
   int l2pf;     // 1: the producer prefetches the stage's next tile into L2
+  EscTab esc;   // D16: escape table (sorted large deltas)
 };
 
 template <typename RP>
@@ -104,9 +123,9 @@ __device__ __forceinline__ int64_t out_row(const StreamP<RP>& p, int64_t r) {
 
 // D16 columns of one row's lane piece: calls f(t, col) for t in the lane's
 // contiguous sub-range of [ls, le). Every lane of the VS-group must call it.
-template <int VS, typename F>
+template <int VS, bool ESC, typename F>
 __device__ __forceinline__ void d16_row_cols(const uint16_t* __restrict__ d_s, int ls, int le, int lane, int base,
-                                             F&& f) {
+                                             const int32_t* e, F&& f) {
   const int len = le - ls;
   const int chunk = (len + VS - 1) / VS;
   int a = ls + lane * chunk;
@@ -114,7 +133,7 @@ __device__ __forceinline__ void d16_row_cols(const uint16_t* __restrict__ d_s, i
   int b = a + chunk;
   b = b < le ? b : le;
   uint32_t ps = 0;
-  for (int t = a; t < b; ++t) ps += (t == ls) ? 0u : (uint32_t)d_s[t];
+  for (int t = a; t < b; ++t) ps += (t == ls) ? 0u : (uint32_t)d16_delta<ESC>(d_s[t], e);
   uint32_t inc = ps;
 #pragma unroll
   for (int o = 1; o < VS; o <<= 1) {
@@ -124,7 +143,7 @@ __device__ __forceinline__ void d16_row_cols(const uint16_t* __restrict__ d_s, i
   int c = base + (int)(inc - ps);
 #pragma unroll 4
   for (int t = a; t < b; ++t) {
-    c += (t == ls) ? 0 : (int)d_s[t];
+    c += (t == ls) ? 0 : d16_delta<ESC>(d_s[t], e);
     f(t, c);
   }
 }
@@ -217,12 +236,14 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
 
 // MODE: 0 = row-step over nnz-aligned tiles, 1 = segmented, 2 = row-step over
 // row-aligned tiles (compile-time so the nnz-tile path carries no per-tile
-// offsets: measured ~9% faster on C5 than a runtime switch)
-template <int VS, typename RP, bool D16, int MODE>
-__global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? 7 : 8))
+// offsets: measured ~9% faster on C5 than a runtime switch). D16: 0 = int32
+// colind, 1 = 16-bit deltas, 2 = 16-bit deltas with escape codes.
+template <int VS, typename RP, int D16, int MODE>
+__global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D16_LB : 8))
     stream_kernel(const StreamP<RP> p) {
   constexpr bool SEG = MODE == 1;
   constexpr bool AL = MODE == 2;
+  constexpr bool ESC = D16 == 2;
   extern __shared__ __align__(128) unsigned char smem[];
   const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), p.rows_cap, D16, SEG);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
@@ -232,6 +253,10 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? 7 : 8))
   constexpr int RPB = (int)sizeof(RP);
   const int S = p.stages;
 
+  __shared__ int32_t esc_s[D16 ? kEscMax : 1];
+  if constexpr (D16) {
+    if (threadIdx.x < kEscMax) esc_s[threadIdx.x] = p.esc.v[threadIdx.x];
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -450,7 +475,7 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? 7 : 8))
               for (int u = 0; u < 8; ++u) {
                 const int l = l0 + u;
                 if (l < le) {
-                  c += (l == ls) ? 0 : (int)d_s[l];
+                  c += (l == ls) ? 0 : d16_delta<ESC>(d_s[l], esc_s);
                   cc[u] = c;
                 } else {
                   cc[u] = -1;
@@ -467,7 +492,7 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? 7 : 8))
             }
             a0 += a1;
           } else {
-            d16_row_cols<VS>(d_s, ls, le, lane, base,
+            d16_row_cols<VS, ESC>(d_s, ls, le, lane, base, esc_s,
                              [&](int t, int c) { a0 = fma(vals_s[t], ld_x(p.x + c), a0); });
           }
           acc = a0;
@@ -511,10 +536,11 @@ static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y)
   p.rows_cap = sp.rows_cap;
   p.aligned = sp.aligned ? 1 : 0;
   p.l2pf = sp.l2pf ? 1 : 0;
+  for (int i = 0; i < kEscMax; ++i) p.esc.v[i] = i < sp.n_esc ? sp.esc[i] : 0;
   return p;
 }
 
-template <int VS, typename RP, bool D16, int MODE>
+template <int VS, typename RP, int D16, int MODE>
 static int stream_prepare_t(const StreamPlan& sp, int sm_count) {
   const size_t smem = stream_smem_bytes(sp.C, sp.stages, sizeof(RP), sp.rows_cap, D16, MODE == 1);
   if (cudaFuncSetAttribute(stream_kernel<VS, RP, D16, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -530,20 +556,20 @@ static int stream_prepare_t(const StreamPlan& sp, int sm_count) {
   return (int)grid;
 }
 
-template <int VS, typename RP, bool D16, int MODE>
+template <int VS, typename RP, int D16, int MODE>
 static void stream_launch_t(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
   const size_t smem = stream_smem_bytes(sp.C, sp.stages, sizeof(RP), sp.rows_cap, D16, MODE == 1);
   stream_kernel<VS, RP, D16, MODE><<<sp.grid, kStreamThreads, smem, s>>>(make_params<RP>(sp, x, y));
 }
 
-template <int VS, typename RP, bool D16, int MODE, bool PREP>
+template <int VS, typename RP, int D16, int MODE, bool PREP>
 static int stream_one(const StreamPlan& sp, int sm_count, const double* x, double* y, cudaStream_t s) {
   if (PREP) return stream_prepare_t<VS, RP, D16, MODE>(sp, sm_count);
   stream_launch_t<VS, RP, D16, MODE>(sp, x, y, s);
   return 0;
 }
 
-template <typename RP, bool D16, int MODE, bool PREP>
+template <typename RP, int D16, int MODE, bool PREP>
 static int stream_vs(const StreamPlan& sp, int smc, const double* x, double* y, cudaStream_t s) {
   switch (sp.vs) {
     case 1: return stream_one<1, RP, D16, MODE, PREP>(sp, smc, x, y, s);
@@ -557,11 +583,14 @@ static int stream_vs(const StreamPlan& sp, int smc, const double* x, double* y, 
 
 template <typename RP, bool PREP>
 static int stream_rp(const StreamPlan& sp, int smc, const double* x, double* y, cudaStream_t s) {
-  const bool d16 = sp.dcol != nullptr;
-  if (sp.seg && !d16) return stream_one<1, RP, false, 1, PREP>(sp, smc, x, y, s);
-  if (sp.aligned)
-    return d16 ? stream_vs<RP, true, 2, PREP>(sp, smc, x, y, s) : stream_vs<RP, false, 2, PREP>(sp, smc, x, y, s);
-  return d16 ? stream_vs<RP, true, 0, PREP>(sp, smc, x, y, s) : stream_vs<RP, false, 0, PREP>(sp, smc, x, y, s);
+  const int d16 = sp.dcol == nullptr ? 0 : (sp.n_esc > 0 ? 2 : 1);
+  if (sp.seg && !d16) return stream_one<1, RP, 0, 1, PREP>(sp, smc, x, y, s);
+  if (sp.aligned) {
+    if (d16 == 2) return stream_vs<RP, 2, 2, PREP>(sp, smc, x, y, s);
+    return d16 ? stream_vs<RP, 1, 2, PREP>(sp, smc, x, y, s) : stream_vs<RP, 0, 2, PREP>(sp, smc, x, y, s);
+  }
+  if (d16 == 2) return stream_vs<RP, 2, 0, PREP>(sp, smc, x, y, s);
+  return d16 ? stream_vs<RP, 1, 0, PREP>(sp, smc, x, y, s) : stream_vs<RP, 0, 0, PREP>(sp, smc, x, y, s);
 }
 
 template <bool PREP>
@@ -594,9 +623,11 @@ __global__ void __launch_bounds__(kNT) d16_decode_kernel(const RP* __restrict__ 
                                                          const int32_t* __restrict__ head,
                                                          const int32_t* __restrict__ anchor,
                                                          const int32_t* __restrict__ tile_row, int64_t nnz, int64_t C,
-                                                         int32_t* __restrict__ out) {
+                                                         int32_t* __restrict__ out, const EscTab esc) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint16_t* d_s = reinterpret_cast<uint16_t*>(smem);
+  __shared__ int32_t esc_s[kEscMax];
+  if (threadIdx.x < kEscMax) esc_s[threadIdx.x] = esc.v[threadIdx.x];
   const int64_t k = blockIdx.x;
   const int64_t t0 = k * C, t1 = (t0 + C) < nnz ? (t0 + C) : nnz;
   const int cnt = (int)(t1 - t0);
@@ -618,21 +649,23 @@ __global__ void __launch_bounds__(kNT) d16_decode_kernel(const RP* __restrict__ 
       le = (int)((b < t1 ? b : t1) - t0);
       if (!incoming || q > 0) base = head[r];
     }
-    d16_row_cols<VS>(d_s, ls, le, lane, base, [&](int t, int c) { out[t0 + t] = c; });
+    d16_row_cols<VS, true>(d_s, ls, le, lane, base, esc_s, [&](int t, int c) { out[t0 + t] = c; });
   }
 }
 
 template <int VS>
 static void d16_export_vs(const StreamPlan& sp, int32_t* out, cudaStream_t s) {
   const size_t smem = (size_t)sp.C * 2 + 16;
+  EscTab esc;
+  for (int i = 0; i < kEscMax; ++i) esc.v[i] = i < sp.n_esc ? sp.esc[i] : 0;
   if (sp.V.rp_bytes == 8) {
     cudaFuncSetAttribute(d16_decode_kernel<VS, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     d16_decode_kernel<VS, int64_t><<<(int)sp.T, kNT, smem, s>>>((const int64_t*)sp.V.rowptr, sp.dcol, sp.head,
-                                                                sp.anchor, sp.tile_row, sp.V.nnz, sp.C, out);
+                                                                sp.anchor, sp.tile_row, sp.V.nnz, sp.C, out, esc);
   } else {
     cudaFuncSetAttribute(d16_decode_kernel<VS, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     d16_decode_kernel<VS, int32_t><<<(int)sp.T, kNT, smem, s>>>((const int32_t*)sp.V.rowptr, sp.dcol, sp.head,
-                                                                sp.anchor, sp.tile_row, sp.V.nnz, sp.C, out);
+                                                                sp.anchor, sp.tile_row, sp.V.nnz, sp.C, out, esc);
   }
 }
 

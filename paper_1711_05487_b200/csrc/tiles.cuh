@@ -38,13 +38,12 @@ struct NzP {
 
 // warp tile k = nonzeros [k*256, (k+1)*256); em: the warp's 8-word smem row-end
 // mask; xh: the hot-x smem table (HOT)
-template <typename RP, bool HOT>
-__device__ __forceinline__ void nz_tile(const NzP<RP>& p, int64_t k, int lane, uint32_t* em, const double* xh) {
+// the lane's 8 consecutive nonzeros of tile k (colind, values)
+template <typename RP>
+__device__ __forceinline__ void nz_tile_load(const NzP<RP>& p, int64_t k, int lane, int (&c)[8], double (&v)[8]) {
   const int64_t t0 = k * kNzTile;
   const int cnt = (int)((p.nnz - t0) < kNzTile ? (p.nnz - t0) : kNzTile);
   const int e0 = lane * 8;
-  int c[8];
-  double v[8];
   if (e0 + 8 <= cnt) {
     ld256_s32(p.col + t0 + e0, c);
     ld256_f64(p.val + t0 + e0, v);
@@ -57,6 +56,25 @@ __device__ __forceinline__ void nz_tile(const NzP<RP>& p, int64_t k, int lane, u
       v[i] = ok ? ld_stream(p.val + t0 + e0 + i) : 0.0;
     }
   }
+}
+
+template <typename RP, bool HOT>
+__device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int lane, uint32_t* em, const double* xh,
+                                                const int (&c)[8], const double (&v)[8]);
+
+template <typename RP, bool HOT>
+__device__ __forceinline__ void nz_tile(const NzP<RP>& p, int64_t k, int lane, uint32_t* em, const double* xh) {
+  int c[8];
+  double v[8];
+  nz_tile_load(p, k, lane, c, v);
+  nz_tile_compute<RP, HOT>(p, k, lane, em, xh, c, v);
+}
+
+template <typename RP, bool HOT>
+__device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int lane, uint32_t* em, const double* xh,
+                                                const int (&c)[8], const double (&v)[8]) {
+  const int64_t t0 = k * kNzTile;
+  const int cnt = (int)((p.nnz - t0) < kNzTile ? (p.nnz - t0) : kNzTile);
   double xv[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {

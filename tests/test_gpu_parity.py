@@ -108,7 +108,7 @@ def test_dyadic_bit_exact(name, m, variant, vs):
 @pytest.mark.parametrize("vs", [1, 4])
 @pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
 def test_stream_d16_and_structures(name, m, tile, vs):
-    w, mg, dcol, head = oracle.d16_encode(m.rowptr, m.colind)
+    w, mg, dcol, head, esc = oracle.d16_encode_esc(m.rowptr, m.colind)
     p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", d16=1, tile_nnz=tile,
                   force_vs=vs)
     info = p.info()
@@ -118,7 +118,8 @@ def test_stream_d16_and_structures(name, m, tile, vs):
     if w == 0:
         assert info["sel"]["d16"] == 0
     else:
-        assert info["sel"]["d16"] == 1 and info["d16_width"] == w
+        assert info["sel"]["d16"] == 1 and info["d16_width"] == (8 if mg <= 255 else 16)
+        assert info["d16_n_esc"] == esc.size
         if m.nnz:
             assert np.array_equal(p.export("dcol"), dcol)
             assert np.array_equal(p.export("head"), head)
@@ -358,3 +359,34 @@ def test_nzsplit_hot_sizes(K):
     for _ in range(2):  # x changes between calls: the hot table is refreshed per SpMV
         x2 = m.x[::-1].copy()
         assert_bound(p.execute(x2), sg.CSR(m.n, m.rowptr, m.colind, m.vals, x2))
+
+
+# escape-coded D16 (reading 21): large in-row gaps (a 27-point
+# stencil with n^2 > 65535, rows of a random matrix with a few big jumps)
+@pytest.mark.parametrize("vs", [1, 4])
+def test_d16_escapes_parity(vs):
+    cases = [sg.stencil(260, 27, rp64=True, x_seed=3, rows=(0, 150000))]
+    g = np.random.default_rng(9)
+    n = 3000
+    lens = g.integers(1, 40, n)
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    ci = np.empty(rp[-1], np.int32)
+    for i in range(n):  # columns spaced by small gaps or one of 5 large jumps
+        steps = np.where(g.random(lens[i]) < 0.2, g.choice([70000, 80000, 90001, 123456, 65472], lens[i]),
+                         g.integers(1, 50, lens[i]))
+        steps[0] = g.integers(0, 100)
+        ci[rp[i]:rp[i + 1]] = np.cumsum(steps)
+    cases.append(sg.CSR(n, rp, ci, g.uniform(-1, 1, ci.size), g.uniform(-1, 1, int(ci.max()) + 1)))
+    for m in cases:
+        ncols = m.x.size
+        w, mg, dcol, head, esc = oracle.d16_encode_esc(m.rowptr, m.colind)
+        assert w == 16 and mg > 65535 and esc.size > 0
+        for tile in (512, 1024):
+            p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=ncols, force_variant="stream", d16=1, force_vs=vs,
+                          tile_nnz=tile)
+            info = p.info()
+            assert info["sel"]["d16"] == 1 and info["d16_n_esc"] == esc.size
+            assert info["feat"]["n_big_gaps"] == esc.size
+            assert np.array_equal(p.export("dcol"), dcol)
+            assert np.array_equal(p.export("decoded"), m.colind)
+            assert_bound(p.execute(m.x), m)

@@ -223,16 +223,24 @@ WIN = 128 * 2 ** 20
 
 
 def test_select_rule_table_on_closed_form_features():
-    def feat(n, nnz, avg_s, sd_s, n_empty=0, n_long=0, nnz_max=0, maxgap=0, misses=0, nnz_long=0):
+    def feat(n, nnz, avg_s, sd_s, n_empty=0, n_long=0, nnz_max=0, maxgap=0, misses=0, nnz_long=0, n_big_gaps=129):
         return dict(n=n, nnz=nnz, avg_short=avg_s, sd_short=sd_s, n_empty=n_empty, n_long=n_long,
-                    nnz_max=nnz_max, nnz_avg=nnz / n, maxgap=maxgap, misses=misses, nnz_long=nnz_long, n_cols=n)
+                    nnz_max=nnz_max, nnz_avg=nnz / n, maxgap=maxgap, misses=misses, nnz_long=nnz_long, n_cols=n,
+                    n_big_gaps=n_big_gaps)
     S = oracle
     # C2: 7-pt 128^3 (closed forms above): regular, 217 MB > L2/2, maxgap 16384
     s = S.select(feat(2097152, 14581760, 6.953125, 0.2148, maxgap=16384, misses=8323072), L2, WIN, 4)
     assert (s.variant, s.d16, s.xwin, s.vs) == (S.VARIANT_STREAM, False, False, 1) and s.classes & S.CLASS_MB
-    # C5: 27-pt 384^3: regular, maxgap 147071 -> no D16
-    s = S.select(feat(56623104, 1520875000, 26.86, 0.5, maxgap=147071, misses=10 ** 8), L2, WIN, 8)
+    # C5: 27-pt 384^3: regular, maxgap 147071 (4 distinct gaps >= 65472: escape
+    # codes possible but not auto-selected, reading 21) -> no D16
+    s = S.select(feat(56623104, 1520875000, 26.86, 0.5, maxgap=147071, misses=10 ** 8, n_big_gaps=4), L2, WIN, 8)
     assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, False, 1)  # rows <= 32 nnz: one lane per row
+    # a 27-pt grid with 16-bit gaps (n = 180: maxgap 32219) -> D16 (rows >= 16 nonzeros)
+    s = S.select(feat(5832000, 155235000, 26.6, 0.6, maxgap=32219, misses=10 ** 7, n_big_gaps=0), L2, WIN, 8)
+    assert s.d16 is True
+    # 7-pt rows (avg < 16) keep int32 colind
+    s = S.select(feat(15625000, 109000000, 6.98, 0.2, maxgap=62250, misses=10 ** 7, n_big_gaps=0), L2, WIN, 4)
+    assert s.d16 is False
     # C1: 1.28 MB working set -> no MB, no D16
     s = S.select(feat(10000, 90000, 9.0, 0.0, maxgap=9000, misses=80000), L2, WIN, 4)
     assert (s.variant, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_STREAM, False, 0)
@@ -346,3 +354,30 @@ def test_hot_columns_threshold_maximal(seed):
         t = next((v for v in range(1, 4096) if np.count_nonzero(cnt >= v) <= K), 4095)
         cand = np.flatnonzero(cnt >= t)
         assert np.array_equal(hot, cand[:min(cand.size, K) & ~1])
+
+
+# ---- escape-coded D16 (reading 21) --------------------------------------
+def test_d16_escape_hand_example():
+    rp = np.array([0, 4, 6])
+    ci = np.array([0, 70000, 70001, 140001, 5, 100005], np.int32)  # gaps 70000, 1, 70000 | 100000
+    assert oracle.d16_encode(rp, ci)[0] == 0  # plain 16-bit deltas cannot hold 70000
+    w, mg, dcol, head, esc = oracle.d16_encode_esc(rp, ci)
+    assert (w, mg) == (16, 100000) and esc.tolist() == [70000, 100000]
+    assert dcol.tolist() == [0, 65472, 1, 65472, 0, 65473] and head.tolist() == [0, 5]
+    assert np.array_equal(oracle.d16_decode_esc(rp, dcol, head, esc), ci)
+    assert oracle.big_gap_count(rp, ci) == 2
+
+
+def test_d16_escape_limits_and_stencil():
+    # 65 distinct large gaps -> not encodable; 64 -> encodable
+    for k, ok in ((64, True), (65, False)):
+        ci = np.cumsum(np.concatenate([[0], 65472 + np.arange(k)])).astype(np.int32)
+        rp = np.array([0, ci.size])
+        w = oracle.d16_encode_esc(rp, ci)[0]
+        assert (w == 16) == ok and oracle.big_gap_count(rp, ci) == k
+    # 27-point stencil n = 260: exactly the 4 closed-form large gaps, round trip
+    m = sg.stencil(260, 27, rp64=True, rows=(0, 200000))
+    n = 260
+    w, mg, dcol, head, esc = oracle.d16_encode_esc(m.rowptr, m.colind)
+    assert w == 16 and esc.tolist() == [n * n - 2 * n - 2, n * n - 2 * n - 1, n * n - n - 2, n * n - n - 1]
+    assert np.array_equal(oracle.d16_decode_esc(m.rowptr, dcol, head, esc), m.colind)
