@@ -610,6 +610,8 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     // (B200: removes a ~5 us fix-up launch, worth it below ~256M nonzeros;
     // on C5, 1.5G nonzeros, nnz-aligned tiles measured 7% faster)
     sp.aligned = !seg && maxlen >= 0 && 2 * maxlen <= sp.C && V.nnz < ((int64_t)1 << 28) && opt.reserved[0] == 0;
+    if (const char* e = getenv("SPMV_ALIGNED"))  // experiments: force row-aligned tiles
+      sp.aligned = !seg && maxlen >= 0 && 2 * maxlen <= sp.C && atoi(e) != 0;
     sp.stride = sp.aligned ? sp.C - maxlen : sp.C;
     sp.T = std::max<int64_t>(1, (V.nnz + sp.stride - 1) / sp.stride);
     // staged rowptr entries: 1.5x the expected rows per tile (+32)
@@ -645,6 +647,12 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
     ck(cudaStreamSynchronize(s.stream), "tiles");
     sp.need_fixup = !sp.aligned && s.hs.n_incoming > 0;
+    // (the fix-up costs ~81 us per SpMV on C5, its scattered y lines; three
+    // in-kernel alternatives were measured slower on B200: a tile-to-tile
+    // carry chain that waits (8.0 vs 3.5 ms: a waiting warp holds its stage
+    // and the waits line the CTAs up), done-flags with a release fence per
+    // tile and opportunistic resolution (6.2 ms: the fence stalls the warp),
+    // and keeping the start part out of y (no shorter fix-up))
     // one stage per consumer warp: measured on B200 (tools/sweep.py, C2/C5),
     // more resident warps beat a deeper ring (the x gathers are latency-bound)
     sp.stages = opt.stages > 0 ? opt.stages : kStreamConsumerWarps;

@@ -390,3 +390,4 @@ def test_d16_escapes_parity(vs):
             assert np.array_equal(p.export("dcol"), dcol)
             assert np.array_equal(p.export("decoded"), m.colind)
             assert_bound(p.execute(m.x), m)
+
