@@ -1,0 +1,68 @@
+"""Copy a round's measurements (gpurun_out/prof/, from tools/round_profile.sh)
+into the tracked profiles/ directory: bench JSON lines, ncu summaries of the
+dominant kernels, the C5 launch list, and per-kernel DRAM traffic
+(profiles/traffic.json, read by bench.py's roofline.traffic).
+  python tools/update_profiles.py [tag]   (default tag r01)"""
+import collections, json, os, subprocess, sys
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import launches
+import ncu_summary
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+src = os.path.join(ROOT, "gpurun_out", "prof")
+dst = os.path.join(ROOT, "profiles")
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+
+
+def last_json(path):
+    lines = [l for l in open(path) if l.startswith("{")]
+    return json.loads(lines[-1]) if lines else None
+
+
+for c in (1, 2, 3, 4, 5):
+    p = os.path.join(src, f"bench_c{c}.log")
+    if os.path.exists(p) and last_json(p):
+        json.dump(last_json(p), open(os.path.join(dst, f"{tag}_bench_c{c}.json"), "w"))
+p = os.path.join(src, "bench_ref.log")
+if os.path.exists(p) and last_json(p):
+    json.dump(last_json(p), open(os.path.join(dst, f"{tag}_bench_reference_c5.json"), "w"))
+
+traffic = json.load(open(os.path.join(dst, "traffic.json"))) if os.path.exists(os.path.join(dst, "traffic.json")) else {}
+variant = {5: "stream", 2: "stream", 3: "nnzsplit", 4: "split", 1: "stream"}
+for c in (2, 3, 4, 5):
+    rep = os.path.join(src, f"full_c{c}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
+    res = ncu_summary.summarise(rep)
+    with open(os.path.join(dst, f"{tag}_ncu_full_c{c}_{variant[c]}.txt"), "w") as f:
+        f.write(f"== ncu --set full --clock-control none (cold cache), dominant kernel of C{c}\n")
+        for m in res:
+            for k, v in m.items():
+                f.write(f"  {k}: {v}\n")
+    m = res[0]
+    rd = float(m["dram__bytes_read.sum"].split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3}.get(m["dram__bytes_read.sum"].split()[1], 1)
+    wr = float(m["dram__bytes_write.sum"].split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3}.get(m["dram__bytes_write.sum"].split()[1], 1)
+    traffic[f"C{c}:{variant[c]}"] = rd + wr
+json.dump(traffic, open(os.path.join(dst, "traffic.json"), "w"), indent=1)
+
+lc = os.path.join(src, "launches_c5.csv")
+if os.path.exists(lc):
+    rows = launches.load(lc)
+    import shutil
+    shutil.copy(lc, os.path.join(dst, f"{tag}_launches_c5.csv"))
+    agg = collections.OrderedDict()
+    for _, name, g, b, us in rows:
+        k = name.split("(")[0][:40]
+        a = agg.setdefault(k, [0, 0.0])
+        a[0] += 1
+        a[1] += us
+    step = {k: v for k, v in agg.items() if "stream_kernel" in k or "fixup" in k}
+    tot = sum(v[1] for v in step.values()) or 1
+    with open(os.path.join(dst, f"{tag}_launches_c5_summary.txt"), "w") as f:
+        f.write("# ncu launch list, `python bench.py --steps 3 --warmup 1 --no-cpu --no-e2e --iters 0` (C5), "
+                "--clock-control none, cold-cache serialised\n")
+        f.write(f"# {'kernel':40s} launches   mean_us    total_us\n")
+        for k, (n, t) in agg.items():
+            f.write(f"{k:42s} {n:6d} {t / n:10.1f} {t:11.1f}\n")
+        f.write("# SpMV step share: " + "  ".join(f"{k} {100 * v[1] / tot:.1f}%" for k, v in step.items()) + "\n")
+print("profiles updated")
