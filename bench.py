@@ -349,6 +349,8 @@ def run_native(a):
     gbs = byts / (ms_step * 1e-3) / 1e9
     peak, peak_kind = measured_peak()
     kbytes = algo_bytes(n_rows, blk["N"], nnz_local, blk["rp_bytes"])
+    if info["sel"]["d16"]:  # the kernel's own format: 2-B deltas + 4-B row heads instead of 4-B colind
+        kbytes += -2 * nnz_local + 4 * n_rows
     achieved = kbytes / (ms_main * 1e-3) / 1e9
     traffic = None
     try:
@@ -370,8 +372,8 @@ def run_native(a):
             "config": {
                 "workload": WORKLOADS[a.config], "N": N, "nnz": nnz, "rowptr_bytes": blk["rp_bytes"],
                 "parallelism": f"row-shard{world} (nnz-balanced, x replicated)",
-                "l2": "inputs larger than L2, no flush" if byts > 4 * 126e6 else
-                      "working set comparable to L2 (warm runs; see roofline.traffic)",
+                "l2": (f"inputs {byts / 1e6:.0f} MB > 126 MB L2, no flush" if byts > 126e6 else
+                       f"inputs {byts / 1e6:.1f} MB fit in L2: warm-cache, not an HBM measurement"),
                 "variant": info["variant"], "vs": info["sel"]["vs"], "d16": info["sel"]["d16"],
                 "xwin": info["sel"]["xwin"], "classes": info["classes"],
                 "tile_nnz": info["tile_nnz"], "hbm_gbs_effective": gbs,
