@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
   constexpr int NW = HOT ? kNzHotWarps : kNzWarps;
   extern __shared__ __align__(16) double xh[];
   __shared__ __align__(16) uint32_t emask_s[NW][8];
+  pdl_trigger();
+  pdl_wait();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* em = emask_s[w];
   if constexpr (HOT) {
@@ -99,6 +101,8 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
 // xhot[s] = x[hot_cols[s]] (once per SpMV, before the hot-x kernel)
 __global__ void nz_hot_gather_kernel(const int32_t* __restrict__ hot_cols, int n_hot, const double* __restrict__ x,
                                      double* __restrict__ xhot) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n_hot) xhot[i] = __ldg(x + hot_cols[i]);
 }
@@ -191,16 +195,19 @@ int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaS
   }
   if (stage != 2) {
     if (z.n_hot > 0) {
-      nz_hot_gather_kernel<<<(z.n_hot + kNT - 1) / kNT, kNT, 0, s>>>(z.hot_cols, z.n_hot, x, z.xhot);
+      launch_pdl(nz_hot_gather_kernel, dim3((z.n_hot + kNT - 1) / kNT), dim3(kNT), 0, s, z.hot_cols, z.n_hot, x,
+                 z.xhot);
       ++n;
       const size_t sm = nz_smem_bytes(z.n_hot);
       if (z.V.rp_bytes == 8)
-        nzsplit_kernel<int64_t, true><<<z.grid, 32 * kNzHotWarps, sm, s>>>(nz_params<int64_t>(z, x, y));
+        launch_pdl(nzsplit_kernel<int64_t, true>, dim3(z.grid), dim3(32 * kNzHotWarps), sm, s, nz_params<int64_t>(z, x, y));
       else
-        nzsplit_kernel<int32_t, true><<<z.grid, 32 * kNzHotWarps, sm, s>>>(nz_params<int32_t>(z, x, y));
+        launch_pdl(nzsplit_kernel<int32_t, true>, dim3(z.grid), dim3(32 * kNzHotWarps), sm, s, nz_params<int32_t>(z, x, y));
     } else {
-      if (z.V.rp_bytes == 8) nzsplit_kernel<int64_t, false><<<z.grid, 32 * kNzWarps, 0, s>>>(nz_params<int64_t>(z, x, y));
-      else nzsplit_kernel<int32_t, false><<<z.grid, 32 * kNzWarps, 0, s>>>(nz_params<int32_t>(z, x, y));
+      if (z.V.rp_bytes == 8)
+        launch_pdl(nzsplit_kernel<int64_t, false>, dim3(z.grid), dim3(32 * kNzWarps), 0, s, nz_params<int64_t>(z, x, y));
+      else
+        launch_pdl(nzsplit_kernel<int32_t, false>, dim3(z.grid), dim3(32 * kNzWarps), 0, s, nz_params<int32_t>(z, x, y));
     }
     ++n;
   }

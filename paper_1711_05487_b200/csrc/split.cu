@@ -21,6 +21,8 @@ __global__ void __launch_bounds__(kSplitThreads, 4) split_fused_kernel(const NzP
                                                                          int64_t n_groups) {
   __shared__ double xs[kLongXB];
   __shared__ __align__(16) uint32_t emask_s[kSplitThreads / 32][8];
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = n_items + n_groups;
   const int64_t b = blockIdx.x;
   const int64_t Lb = (b + 1) * n_items / total;  // long items among blocks [0, b]
@@ -40,6 +42,8 @@ __global__ void __launch_bounds__(kNT) split_epilogue_kernel(const int32_t* __re
                                                              const double* __restrict__ partial, int64_t n_long,
                                                              int64_t nblk, const int32_t* __restrict__ long_rows,
                                                              double* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   if ((int)blockIdx.x < nfb) {
     const int64_t k = (int64_t)blockIdx.x * kNT + threadIdx.x;
     if (k >= T) return;
@@ -71,9 +75,11 @@ int launch_split_fused(const ExecArgs& a, cudaStream_t s) {
     const int64_t items = long_items(a), groups = (z.T + kSplitThreads / 32 - 1) / (kSplitThreads / 32);
     const int grid = (int)(items + groups);
     if (z.V.rp_bytes == 8)
-      split_fused_kernel<int64_t><<<grid, kSplitThreads, 0, s>>>(nz_params64(z, a.x, a.y), long_params(a), items, groups);
+      launch_pdl(split_fused_kernel<int64_t>, dim3(grid), dim3(kSplitThreads), 0, s, nz_params64(z, a.x, a.y),
+                 long_params(a), items, groups);
     else
-      split_fused_kernel<int32_t><<<grid, kSplitThreads, 0, s>>>(nz_params32(z, a.x, a.y), long_params(a), items, groups);
+      launch_pdl(split_fused_kernel<int32_t>, dim3(grid), dim3(kSplitThreads), 0, s, nz_params32(z, a.x, a.y),
+                 long_params(a), items, groups);
     ++n;
   }
   if (a.stage != 1) {
@@ -84,8 +90,9 @@ int launch_split_fused(const ExecArgs& a, cudaStream_t s) {
     } else {
       const int nfb = z.T > 1 ? (int)((z.T + kNT - 1) / kNT) : 0;
       const int nrb = (int)((a.n_long * 32 + kNT - 1) / kNT);
-      split_epilogue_kernel<<<nfb + nrb, kNT, 0, s>>>(z.carry_row, z.carry_val, z.T, nfb, a.long_partial, a.n_long,
-                                                       a.nblk, a.long_rows, a.y);
+      launch_pdl(split_epilogue_kernel, dim3(nfb + nrb), dim3(kNT), 0, s, (const int32_t*)z.carry_row,
+                 (const double*)z.carry_val, z.T, nfb, (const double*)a.long_partial, a.n_long, a.nblk, a.long_rows,
+                 a.y);
       ++n;
     }
   }

@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
   constexpr int RPB = (int)sizeof(RP);
   const int S = p.stages;
 
+  pdl_trigger();
   __shared__ int32_t esc_s[D16 ? kEscMax : 1];
   if constexpr (D16) {
     if (threadIdx.x < kEscMax) esc_s[threadIdx.x] = p.esc.v[threadIdx.x];
@@ -380,6 +381,9 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
   }
 
   // ------------------------------- consumers --------------------------------
+  // (the producer streams plan-constant matrix data only; x, y and the
+  // carries wait for the previous kernel in the stream)
+  pdl_wait();
   const int w = (threadIdx.x >> 5) - 1;
   const int lane32 = threadIdx.x & 31;
   constexpr int GPW = 32 / VS;
@@ -559,7 +563,7 @@ static int stream_prepare_t(const StreamPlan& sp, int sm_count) {
 template <int VS, typename RP, int D16, int MODE>
 static void stream_launch_t(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
   const size_t smem = stream_smem_bytes(sp.C, sp.stages, sizeof(RP), sp.rows_cap, D16, MODE == 1);
-  stream_kernel<VS, RP, D16, MODE><<<sp.grid, kStreamThreads, smem, s>>>(make_params<RP>(sp, x, y));
+  launch_pdl(stream_kernel<VS, RP, D16, MODE>, dim3(sp.grid), dim3(kStreamThreads), smem, s, make_params<RP>(sp, x, y));
 }
 
 template <int VS, typename RP, int D16, int MODE, bool PREP>

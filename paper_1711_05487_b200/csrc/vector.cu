@@ -110,6 +110,8 @@ int64_t fixup_capacity(int64_t T) {
 __global__ void __launch_bounds__(kNT) fixup_kernel(const int32_t* __restrict__ crow,
                                                     const double* __restrict__ cval, int64_t T,
                                                     double* __restrict__ y, int set) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t k = (int64_t)blockIdx.x * kNT + threadIdx.x;
   if (k >= T) return;
   const int32_t r = crow[k];
@@ -236,6 +238,8 @@ __global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restr
                                                           double* __restrict__ y, int set,
                                                           int32_t* __restrict__ orow, double* __restrict__ oval,
                                                           unsigned int* __restrict__ done) {
+  pdl_trigger();
+  pdl_wait();
   fixup_block(crow, cval, n, blockIdx.x, y, set, orow, oval);
   const int64_t n2 = 2 * (int64_t)gridDim.x;
   if (!orow || !done || n2 > kFixItems) return;
@@ -255,7 +259,8 @@ __global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restr
 int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int64_t max_run, cudaStream_t s) {
   if (T <= 0) return 0;
   if (max_run <= 16) {
-    fixup_kernel<<<(int)((T + kNT - 1) / kNT), kNT, 0, s>>>(crow, cval, T, y, set);
+    launch_pdl(fixup_kernel, dim3((unsigned)((T + kNT - 1) / kNT)), dim3(kNT), 0, s, (const int32_t*)crow,
+               (const double*)cval, T, y, set);
     return 1;
   }
   unsigned int* done = reinterpret_cast<unsigned int*>(crow + fixup_capacity(T));
@@ -268,7 +273,8 @@ int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int
     const int64_t nb = (n + kFixItems - 1) / kFixItems;
     int32_t* orow = nb > 1 ? crow + off : nullptr;
     double* oval = nb > 1 ? cval + off : nullptr;
-    fixup_level_kernel<<<(int)nb, kNT, 0, s>>>(cr, cv, n, y, set, orow, oval, done);
+    launch_pdl(fixup_level_kernel, dim3((unsigned)nb), dim3(kNT), 0, s, (const int32_t*)cr, (const double*)cv, n, y,
+               set, orow, oval, done);
     ++launches;
     if (nb == 1 || 2 * nb <= kFixItems) break;  // the last CTA ran the final level
     cr = orow;
