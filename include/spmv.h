@@ -79,7 +79,9 @@ typedef struct spmv_options {
   int32_t split_bins;      /* SPLIT non-long rows: -1 auto (one nnz_split bin), 0 cta_stream length bins, 1 nnz_split bin */
   int32_t hot_x;           /* NNZSPLIT hot-x table in smem: -1 auto (top columns cover >= 20 % of nnz), 0 off,
                               K > 0 = force, at most K (<= 16384) columns */
-  int32_t reserved[2];     /* reserved[0] = 1 disables row-aligned tiles (tests) */
+  int32_t select_mode;     /* 0 feature-guided (Table I features, default), 1 profile-guided (Sec. III-B bounds from
+                              three timed micro-benchmarks + Fig. 4 rules; reading 22) */
+  int32_t reserved[1];     /* reserved[0] = 1 disables row-aligned tiles (tests) */
 } spmv_options;
 
 /* Theta(N) features (Table I) + counts used by the selection.
@@ -133,6 +135,12 @@ typedef struct spmv_plan_info {
   int64_t n_nz_tiles;         /* nnz_split: warp tiles of 256 nonzeros */
   int64_t n_hot;              /* nnz_split: hot columns served from shared memory (0 = off) */
   double hot_cover;           /* fraction of nonzeros in the (candidate) hot columns */
+  /* profile-guided mode (select_mode = 1): Sec. III-B bounds in flop/s and B_max in bytes/s; the Fig. 4
+   * classes are sel.classes. p_csr/p_ml/p_cmp measured, p_imb from the median CTA busy time of the
+   * static nnz-balanced baseline, p_mb/p_peak analytic. Zero in feature mode. */
+  double p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak, bmax;
+  int32_t profile_vs, profile_ctas; /* baseline lanes per row, CTAs of its static partition */
+  double profile_ms;          /* micro-benchmark time (part of select_ms: the classifier's t_pre) */
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */

@@ -25,6 +25,7 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``) -- no function is
   nonempty_rows   numpy flatnonzero of the row lengths, coverage
   nz_tiles        binary-search (searchsorted) re-derivation, ownership cover
   hot_columns     hand example, maximality of the count threshold
+  classify_profile SPEC S:469-474 examples, strictness, monotonicity in P_ML
   d16 encode/dec  SPEC S:134-136 widths, round trip, stencil gap closed forms
   features        SPEC S:415 sd example, stencil closed forms
   select          hand-evaluated rule table on the configs' closed-form features
@@ -464,4 +465,52 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     if ml:
         classes |= CLASS_ML
     xwin = bool(ml and 8 * n <= window_max)
+    return Selection(variant, vs, d16, xwin, classes)
+
+
+# ---- profile-guided selection (reading 22) --------------
+T_IMB, T_ML, APPROX_TOL = 1.24, 1.25, 0.10  # Fig. 4 caption
+
+
+def classify_profile(p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak, t_imb=T_IMB, t_ml=T_ML, tol=APPROX_TOL):
+    """Fig. 4, written out: multilabel, strict '>', 'P_CSR ~ P_MB'
+    read as P_CSR >= (1 - tol) P_MB. Returns a CLASS_* bitmask."""
+    c = 0
+    if p_csr <= 0:
+        return 0
+    if p_imb / p_csr > t_imb:
+        c |= CLASS_IMB
+    if p_ml / p_csr > t_ml:
+        c |= CLASS_ML
+    if p_csr >= (1 - tol) * p_mb and p_mb < p_cmp < p_peak:
+        c |= CLASS_MB
+    if p_mb > p_cmp or p_cmp > p_peak:
+        c |= CLASS_CMP
+    return c
+
+
+def profile_select(f, bounds, window_max, K_long=100):
+    """Table II for the GPU variants: IMB -> long_row_split (dense
+    long rows) or nnz_split; ML -> nnz_split with the x window; MB / CMP ->
+    cta_stream (MB adds 16-bit deltas when the gaps fit); no class -> the CSR
+    baseline (csr_vector), "not worth applying any" (P:459-461). Precedence
+    IMB > ML > MB/CMP. bounds: dict with p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak."""
+    classes = classify_profile(*(bounds[k] for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak")))
+    avg_s = f["avg_short"]
+    longr = f["n_long"] > 0 and f["nnz_max"] > K_long * f["nnz_avg"]
+    nblk = -(-int(f.get("n_cols", f["n"])) // 2048)
+    dense_long = f["n_long"] > 0 and f["nnz_long"] >= 64 * f["n_long"] * nblk
+    if classes & CLASS_IMB:
+        variant = VARIANT_SPLIT if (longr and dense_long) else VARIANT_NNZSPLIT
+    elif classes & CLASS_ML:
+        variant = VARIANT_NNZSPLIT
+    elif classes & (CLASS_MB | CLASS_CMP):
+        variant = VARIANT_STREAM
+    else:
+        variant = VARIANT_VECTOR
+    vs = min(32, max(2, _pow2ceil(int(math.ceil(avg_s))))) if avg_s > 0 else 2
+    if variant == VARIANT_STREAM:
+        vs = min(32, _pow2ceil(int(math.ceil(avg_s / 32.0)))) if avg_s > 32 else 1
+    d16 = bool(classes & CLASS_MB) and variant == VARIANT_STREAM and f["maxgap"] <= 65535
+    xwin = bool(classes & CLASS_ML) and 8 * f["n"] <= window_max
     return Selection(variant, vs, d16, xwin, classes)

@@ -35,7 +35,7 @@ class Options(ctypes.Structure):
                 ("merge_items", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
                 ("emulate_devices", ctypes.c_int32), ("stages", ctypes.c_int32), ("seg", ctypes.c_int32),
                 ("long_mode", ctypes.c_int32), ("split_bins", ctypes.c_int32), ("hot_x", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("select_mode", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
     @classmethod
     def make(cls, **kw):
@@ -81,7 +81,9 @@ class PlanInfo(ctypes.Structure):
                 ("select_ms", ctypes.c_double), ("encode_ms", ctypes.c_double), ("device_bytes", ctypes.c_int64),
                 ("shard_bounds", ctypes.c_int64 * 9), ("tile_stride", ctypes.c_int64),
                 ("tiles_row_aligned", ctypes.c_int32), ("pad2_", ctypes.c_int32), ("n_nz_rows", ctypes.c_int64),
-                ("n_nz_tiles", ctypes.c_int64), ("n_hot", ctypes.c_int64), ("hot_cover", ctypes.c_double)]
+                ("n_nz_tiles", ctypes.c_int64), ("n_hot", ctypes.c_int64), ("hot_cover", ctypes.c_double)] + \
+               [(k, ctypes.c_double) for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak", "bmax")] + \
+               [("profile_vs", ctypes.c_int32), ("profile_ctas", ctypes.c_int32), ("profile_ms", ctypes.c_double)]
 
 
 _vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double

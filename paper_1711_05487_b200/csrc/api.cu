@@ -179,7 +179,9 @@ struct spmv_plan_s {
   double upload_ms = 0, inspect_ms = 0, select_ms = 0, encode_ms = 0;
   int64_t l_split = 4096, k_long = 100, C = 2048, items = 2048, chunk = 8192;
   double hot_cover = 0.0;
-  std::vector<int32_t> esc;  // D16 escape table (sorted distinct deltas >= kEsc0)  // nnz_split hot-x set: fraction of nonzeros in the hot columns
+  std::vector<int32_t> esc;  // D16 escape table (sorted distinct deltas >= kEsc0)
+  ProfileBounds pb;          // profile-guided mode: measured / analytic bounds
+  double profile_ms = 0.0;  // nnz_split hot-x set: fraction of nonzeros in the hot columns
 
   ~spmv_plan_s() {
     for (auto& s : shards) s.release();
@@ -312,6 +314,56 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   s.seg = seg ? 1 : 0;
 }
 
+// ---- profile-guided mode -------------------------------------
+// Fig. 4 on the measured bounds, thresholds T_IMB = 1.24,
+// T_ML = 1.25, strict ">", "P_CSR ~ P_MB" read as P_CSR >=
+// (1 - 0.10) P_MB (reading 22).
+int classify_profile(const ProfileBounds& b) {
+  int c = 0;
+  if (b.p_csr <= 0) return 0;
+  if (b.p_imb / b.p_csr > 1.24) c |= SPMV_CLASS_IMB;
+  if (b.p_ml / b.p_csr > 1.25) c |= SPMV_CLASS_ML;
+  if (b.p_csr >= 0.9 * b.p_mb && b.p_mb < b.p_cmp && b.p_cmp < b.p_peak) c |= SPMV_CLASS_MB;
+  if (b.p_mb > b.p_cmp || b.p_cmp > b.p_peak) c |= SPMV_CLASS_CMP;
+  return c;
+}
+
+// Table II for the GPU: IMB -> decomposition (dense long rows:
+// long_row_split) or nnz_split (the "auto" analogue); ML -> nnz_split (L1 x
+// gathers + hot-x table, the prefetch analogue) with the x window; MB ->
+// cta_stream + 16-bit deltas when the gaps fit; CMP -> cta_stream (rows sized
+// to lanes, the unroll/vectorise analogue); no class -> the CSR baseline
+// (csr_vector), "not worth optimising". Precedence IMB > ML > MB/CMP.
+void profile_select_impl(const spmv_features& f, const spmv_device_props& d, const spmv_options& o,
+                         const ProfileBounds& b, spmv_selection& s) {
+  const int classes = classify_profile(b);
+  const int64_t k_long = o.k_long > 0 ? o.k_long : 100;
+  const double avg_s = f.avg_short;
+  const bool longr = f.n_long > 0 && (double)f.nnz_max > (double)k_long * f.nnz_avg;
+  const int64_t nblk = (f.n_cols + 2047) / 2048;
+  const bool dense_long = f.n_long > 0 && f.nnz_long >= 64 * f.n_long * nblk;
+  int variant;
+  if (classes & SPMV_CLASS_IMB) variant = (longr && dense_long) ? SPMV_VARIANT_SPLIT : SPMV_VARIANT_NNZSPLIT;
+  else if (classes & SPMV_CLASS_ML) variant = SPMV_VARIANT_NNZSPLIT;
+  else if (classes & (SPMV_CLASS_MB | SPMV_CLASS_CMP)) variant = SPMV_VARIANT_STREAM;
+  else variant = SPMV_VARIANT_VECTOR;
+  int vs = avg_s > 0 ? std::min(32, std::max(2, pow2ceil((int64_t)std::ceil(avg_s)))) : 2;
+  if (variant == SPMV_VARIANT_STREAM)
+    vs = avg_s > 32 ? std::min(32, pow2ceil((int64_t)std::ceil(avg_s / 32.0))) : 1;
+  bool d16 = (classes & SPMV_CLASS_MB) && variant == SPMV_VARIANT_STREAM && f.maxgap <= 65535;
+  bool xwin = (classes & SPMV_CLASS_ML) && 8 * f.n <= d.access_window_max;
+  if (o.force_vs > 0) vs = o.force_vs;
+  if (o.d16 == 0) d16 = false;
+  if (o.xwin == 0) xwin = false;
+  if (o.xwin == 1) xwin = true;
+  s.variant = variant;
+  s.vs = vs;
+  s.d16 = d16 ? 1 : 0;
+  s.xwin = xwin ? 1 : 0;
+  s.classes = classes;
+  s.seg = 0;
+}
+
 void validate_options(const spmv_options& o) {
   if (o.force_variant < 0 || o.force_variant > 5) fail(SPMV_E_ARG, "force_variant %d out of range", o.force_variant);
   if (o.force_vs != 0 && o.force_vs != 1 && o.force_vs != 2 && o.force_vs != 4 && o.force_vs != 8 &&
@@ -324,6 +376,7 @@ void validate_options(const spmv_options& o) {
     fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
   if (o.l_split < 0 || o.k_long < 0) fail(SPMV_E_ARG, "negative l_split / k_long");
   if (o.long_mode < 0 || o.long_mode > 2) fail(SPMV_E_ARG, "long_mode must be 0, 1 or 2");
+  if (o.select_mode < 0 || o.select_mode > 1) fail(SPMV_E_ARG, "select_mode must be 0 (feature) or 1 (profile)");
   if (o.hot_x < -1) fail(SPMV_E_ARG, "hot_x must be -1 (auto), 0 (off) or a column count");
   if (o.split_bins < -1 || o.split_bins > 1) fail(SPMV_E_ARG, "split_bins must be -1, 0 or 1");
   if (o.stages < 0 || o.stages > 32 || o.stages % kStreamConsumerWarps)
@@ -569,6 +622,29 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   features_from_stats(st, ms, P->feat);
   P->feat.n_cols = n_cols;
   select_impl(P->feat, P->props, rp_bytes, opt, P->sel);
+  if (opt.select_mode == 1) {
+    // profile-guided: three timed micro-benchmarks of the CSR baseline on
+    // shard 0 (Sec. III-B), then Fig. 4 and the Table II mapping; their time
+    // is the classifier's t_pre
+    Shard& s0 = P->shards[0];
+    ck(cudaSetDevice(s0.dev), "cudaSetDevice");
+    const double t_p = now_ms();
+    const int vs0 = P->feat.avg_short > 0
+                        ? std::min(32, std::max(2, pow2ceil((int64_t)std::ceil(P->feat.avg_short))))
+                        : 2;
+    double *px = nullptr, *py = nullptr;
+    ck(cudaMalloc(&px, (size_t)std::max<int64_t>(s0.n_cols, 1) * 8 + 64), "cudaMalloc");
+    if (cudaMalloc(&py, (size_t)std::max<int64_t>(s0.m, 1) * 8 + 64) != cudaSuccess) {
+      cudaFree(px);
+      ck(cudaErrorMemoryAllocation, "cudaMalloc");
+    }
+    const int rc = run_profile_probes(s0.view(), vs0, s0.sm_count, P->props.l2_bytes, px, py, P->pb, s0.stream);
+    cudaFree(px);
+    cudaFree(py);
+    if (rc != 0) ck(cudaGetLastError() != cudaSuccess ? cudaGetLastError() : cudaErrorUnknown, "profile probes");
+    P->profile_ms = now_ms() - t_p;
+    if (opt.force_variant == 0) profile_select_impl(P->feat, P->props, opt, P->pb, P->sel);
+  }
   if (P->sel.d16) P->d16_width = P->feat.maxgap <= 255 ? 8 : 16;
   // escape table: the sorted distinct large deltas of all shards
   if (P->sel.d16 && P->feat.maxgap > 65535) {
@@ -1130,6 +1206,16 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     info->feat = p->feat;
     info->d16_width = p->d16_width;
     info->d16_n_esc = (int32_t)p->esc.size();
+    info->p_csr = p->pb.p_csr;
+    info->p_mb = p->pb.p_mb;
+    info->p_ml = p->pb.p_ml;
+    info->p_imb = p->pb.p_imb;
+    info->p_cmp = p->pb.p_cmp;
+    info->p_peak = p->pb.p_peak;
+    info->bmax = p->pb.bmax;
+    info->profile_vs = p->pb.vs;
+    info->profile_ctas = p->pb.ctas;
+    info->profile_ms = p->profile_ms;
     const Shard& s0 = p->shards[0];
     info->tile_nnz = s0.sp[0].C;
     info->n_tiles = s0.sp[0].T;

@@ -186,6 +186,14 @@ size_t stream_smem_bytes(int64_t C, int stages, int rp_bytes, int rows_cap, bool
 int stream_prepare(const StreamPlan& sp, int sm_count);  // smem attribute + persistent grid (<0 on error)
 void launch_chunk_export(const ExecArgs& a, int64_t* out, cudaStream_t s);  // [row|begin|end] x n_chunks
 
+// ---- profile-guided selection (profile.cu; Sec. III-B bounds, Fig. 4) -----------
+struct ProfileBounds {
+  double p_csr = 0, p_mb = 0, p_ml = 0, p_imb = 0, p_cmp = 0, p_peak = 0, bmax = 0;
+  int ws_fits_l2 = 0, vs = 0, ctas = 0;
+};
+int run_profile_probes(const MatView& A, int vs, int sm_count, int64_t l2_bytes, double* x, double* y,
+                       ProfileBounds& out, cudaStream_t s);
+
 // ---- iterated mode -------------------------------------------------------------
 int launch_norm_partials(const double* y, int64_t m, double* partials, cudaStream_t s);
 int launch_normalize(const double* y, int64_t m, const double* partials, int count, double* x_out,

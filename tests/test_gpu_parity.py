@@ -391,3 +391,27 @@ def test_d16_escapes_parity(vs):
             assert np.array_equal(p.export("decoded"), m.colind)
             assert_bound(p.execute(m.x), m)
 
+
+
+# profile-guided mode: the plan's Fig. 4 classes and Table II
+# choice equal the oracle's pure functions of the bounds the plan measured
+PROFILE_KEYS = ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak")
+
+
+@pytest.mark.parametrize("c,small", [(1, False), (2, True), (3, True), (4, True), (5, True), (2, False), (3, False),
+                                     (4, False)])
+def test_profile_mode_selection(c, small):
+    m = sg.config(c, small=small)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, select_mode=1)
+    info = p.info()
+    b = {k: info[k] for k in PROFILE_KEYS}
+    assert all(v > 0 for v in b.values()) and info["bmax"] > 0
+    assert b["p_peak"] > b["p_mb"]                      # S:303-306 invariant
+    assert b["p_imb"] >= 0.95 * b["p_csr"]              # median <= max busy time (+ noise)
+    assert 0 < info["profile_ms"] <= info["select_ms"]
+    f = oracle.features(m.rowptr, m.colind)
+    o = oracle.profile_select(f, b, spmv.device_query(0)["access_window_max"])
+    s = info["sel"]
+    assert (s["variant"], s["vs"], bool(s["d16"]), bool(s["xwin"]), s["classes"]) == \
+        (o.variant, o.vs, o.d16, o.xwin, o.classes), (b, s)
+    assert_bound(p.execute(m.x), m)

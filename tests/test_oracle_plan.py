@@ -381,3 +381,50 @@ def test_d16_escape_limits_and_stencil():
     w, mg, dcol, head, esc = oracle.d16_encode_esc(m.rowptr, m.colind)
     assert w == 16 and esc.tolist() == [n * n - 2 * n - 2, n * n - 2 * n - 1, n * n - n - 2, n * n - n - 1]
     assert np.array_equal(oracle.d16_decode_esc(m.rowptr, dcol, head, esc), m.colind)
+
+
+# ---- profile-guided classifier (Fig. 4) ------------------
+def test_classify_profile_spec_examples():
+    C = oracle
+    neutral = dict(p_csr=1.0, p_mb=2.0, p_ml=1.0, p_imb=1.0, p_cmp=3.0, p_peak=4.0)
+    assert C.classify_profile(**neutral) == 0                              # no rule fires
+    assert C.classify_profile(**{**neutral, "p_ml": 1.30}) == C.CLASS_ML   # 1.30 > 1.25
+    assert C.classify_profile(**{**neutral, "p_imb": 1.24}) == 0           # strict >
+    assert C.classify_profile(**{**neutral, "p_imb": 1.2401}) == C.CLASS_IMB
+    assert C.classify_profile(**{**neutral, "p_cmp": 5.0}) & C.CLASS_CMP   # P_CMP > P_peak
+    assert C.classify_profile(**{**neutral, "p_cmp": 1.5}) == C.CLASS_CMP  # P_MB > P_CMP
+    # MB: P_CSR within 10 % of P_MB and P_MB < P_CMP < P_peak
+    assert C.classify_profile(**{**neutral, "p_csr": 1.8}) == C.CLASS_MB
+    assert C.classify_profile(**{**neutral, "p_csr": 1.79}) == 0
+    # all four at once is impossible only for MB + (P_MB > P_CMP) CMP; MB + IMB + ML is fine
+    assert C.classify_profile(p_csr=1.8, p_mb=2.0, p_ml=3.0, p_imb=3.0, p_cmp=3.0, p_peak=4.0) == \
+        C.CLASS_MB | C.CLASS_ML | C.CLASS_IMB
+
+
+def test_classify_profile_properties():
+    g = np.random.default_rng(3)
+    for _ in range(2000):
+        b = dict(zip(("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak"), g.uniform(0.5, 3.0, 6)))
+        c = oracle.classify_profile(**b)
+        # monotone in P_ML
+        assert (oracle.classify_profile(**{**b, "p_ml": b["p_ml"] * 2}) & oracle.CLASS_ML) >= (c & oracle.CLASS_ML)
+        # MB and the P_MB > P_CMP branch of CMP exclude each other
+        if b["p_mb"] > b["p_cmp"]:
+            assert not (c & oracle.CLASS_MB)
+
+
+def test_profile_select_table2_mapping():
+    f = dict(n=1000, nnz=20000, avg_short=20.0, n_long=0, nnz_max=30, nnz_avg=20.0, n_cols=1000, nnz_long=0,
+             maxgap=100)
+    b = dict(p_csr=1.0, p_mb=2.0, p_ml=1.0, p_imb=1.0, p_cmp=3.0, p_peak=4.0)
+    S = oracle
+    assert S.profile_select(f, b, 1 << 27).variant == S.VARIANT_VECTOR                     # no class: baseline
+    assert S.profile_select(f, {**b, "p_imb": 2.0}, 1 << 27).variant == S.VARIANT_NNZSPLIT  # IMB, no long rows
+    s = S.profile_select(f, {**b, "p_ml": 2.0}, 1 << 27)
+    assert s.variant == S.VARIANT_NNZSPLIT and s.xwin                                       # ML
+    s = S.profile_select(f, {**b, "p_csr": 1.9}, 1 << 27)
+    assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, True, 1)                          # MB -> stream + D16
+    s = S.profile_select(f, {**b, "p_cmp": 1.0}, 1 << 27)
+    assert (s.variant, s.d16) == (S.VARIANT_STREAM, False)                                  # CMP
+    fl = {**f, "n_long": 10, "nnz_max": 5000, "nnz_long": 50000}
+    assert S.profile_select(fl, {**b, "p_imb": 2.0}, 1 << 27).variant == S.VARIANT_SPLIT    # dense long rows
