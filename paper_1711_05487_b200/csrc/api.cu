@@ -266,10 +266,13 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   // long-row or skewed matrix -> nnz_split (rows cut at warp-tile edges)
   const int64_t nblk = (f.n_cols + 2047) / 2048;
   const bool dense_long = f.n_long > 0 && f.nnz_long >= 64 * f.n_long * nblk;
+  // tiny regular matrices (<= 2^20 nonzeros) are launch-bound: the plain
+  // csr_vector kernel beats the warp-specialised stream kernel's set-up
+  // (C1: 6 vs 10 us on B200, tools/table5.py)
   int variant = longr ? (dense_long ? SPMV_VARIANT_SPLIT : SPMV_VARIANT_NNZSPLIT)
                 : skew ? SPMV_VARIANT_NNZSPLIT
-                : avg_s <= 32 ? SPMV_VARIANT_STREAM
-                              : SPMV_VARIANT_VECTOR;
+                : (avg_s <= 32 && nnz > (1 << 20)) ? SPMV_VARIANT_STREAM
+                                                   : SPMV_VARIANT_VECTOR;
   if (o.force_variant > 0) variant = o.force_variant;
   if (variant == SPMV_VARIANT_STREAM) {
     // cta_stream: one lane per row for rows up to 32 nonzeros (lanes walk
@@ -917,8 +920,13 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       } else {
         ck(cudaMemsetAsync(rpc, 0, rp_bytes, s.stream), "memset");
       }
+      const double th0 = now_ms();
       build_hot(s, s.nz, A, s.col);
+      const double th1 = now_ms();
       build_nz(s, s.nz, A, rpc, rows, mc, P->feat.nnz_max);
+      if (getenv("SPMV_PLAN_TRACE"))
+        fprintf(stderr, "[spmv plan] nz rows %.2f ms, hot set %.2f ms, nz tiles %.2f ms\n", th0 - t_d, th1 - th0,
+                now_ms() - th1);
       s.use_nz = true;
     } else if (P->sel.variant == SPMV_VARIANT_SPLIT) {
       // decomposition by row length (Fig. 6 read through S:120-125):
@@ -1013,6 +1021,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     }
   }
   P->encode_ms = now_ms() - t_d;
+  if (getenv("SPMV_PLAN_TRACE"))
+    fprintf(stderr, "[spmv plan] upload %.2f inspect %.2f select %.2f (profile %.2f) encode %.2f ms\n", P->upload_ms,
+            P->inspect_ms, P->select_ms, P->profile_ms, P->encode_ms);
   ck(cudaSetDevice(cur), "cudaSetDevice");
   return P.release();
 }

@@ -241,9 +241,9 @@ def test_select_rule_table_on_closed_form_features():
     # 7-pt rows (avg < 16) keep int32 colind
     s = S.select(feat(15625000, 109000000, 6.98, 0.2, maxgap=62250, misses=10 ** 7, n_big_gaps=0), L2, WIN, 4)
     assert s.d16 is False
-    # C1: 1.28 MB working set -> no MB, no D16
+    # C1: 1.28 MB working set, 90,000 nonzeros -> launch-bound: csr_vector VS 16, no MB, no D16
     s = S.select(feat(10000, 90000, 9.0, 0.0, maxgap=9000, misses=80000), L2, WIN, 4)
-    assert (s.variant, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_STREAM, False, 0)
+    assert (s.variant, s.vs, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_VECTOR, 16, False, 0)
     # C3-like: half the rows empty, sparse long rows (11.4M nnz over 1794 rows of
     # 4.2M columns: far below 64 per 2048-column block) -> nnz_split, IMB + ML
     s = S.select(feat(4194304, 65244537, 12.8, 78.5, n_empty=2185429, n_long=1794, nnz_max=97958,
