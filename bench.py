@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--d16", type=int, default=-1)
     ap.add_argument("--seg", type=int, default=-1)
     ap.add_argument("--split-bins", type=int, default=-1, help="SPLIT non-long rows: 0 cta_stream bins, 1 nnz_split")
+    ap.add_argument("--xwin", type=int, default=-1, help="L2 persistence window on x: -1 auto, 0 off, 1 on")
     ap.add_argument("--stages", type=int, default=0, help="STREAM smem ring depth (multiple of 4; 0 auto)")
     ap.add_argument("--hot", type=int, default=-1, help="NNZSPLIT hot-x table: -1 auto, 0 off, K columns")
     ap.add_argument("--no-aligned", action="store_true", help="nnz-aligned STREAM tiles (carries + fix-up)")
@@ -254,6 +255,8 @@ def run_native(a):
         opts["hot_x"] = a.hot
     if a.stages:
         opts["stages"] = a.stages
+    if a.xwin >= 0:
+        opts["xwin"] = a.xwin
     t0 = time.time()
     plan = spmv.Plan(blk["rowptr"], blk["colind"], blk["vals"], n_cols=blk["N"], **opts)
     plan_s = time.time() - t0
