@@ -204,6 +204,26 @@ int spmv_normalize(spmv_plan p, const double* y, const double* partials, int cou
 
 spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info);
 
+/* The full Table I feature vector, computed on
+ * demand on the device for a single-shard plan (one Theta(N) + Theta(NNZ)
+ * pass over rowptr/colind and one Theta(N) pass for the deviations; the
+ * feature-guided selection itself only uses the nnz_* subset). Definitions
+ * (reading 23): size = 1 iff the CSR + x + y working set fits in L2;
+ * density = NNZ / (n_rows * n_cols); bw_i = last - first column + 1; scatter_i
+ * = nnz_i / bw_i; clustering_i = ngroups_i / nnz_i (groups of consecutive
+ * columns); misses_i = in-row gaps > 16 doubles (128-B line). nnz_* over all
+ * rows (as spmv_features); bw_*, scatter_*, clustering_avg over the non-empty
+ * rows; misses_avg over all rows; population standard deviations. */
+typedef struct spmv_table1 {
+  int32_t size_fits_l2, pad_;
+  double density;
+  double nnz_min, nnz_max, nnz_avg, nnz_sd;
+  double bw_min, bw_max, bw_avg, bw_sd;
+  double scatter_avg, scatter_sd, clustering_avg, misses_avg;
+  int64_t n_nonempty;
+} spmv_table1;
+spmv_status spmv_plan_table1(spmv_plan p, spmv_table1* out);
+
 /* Plan-resident buffers and stream of shard g (the timed path: no copies
  * when spmv_execute* receives these pointers). */
 double* spmv_plan_x_device(spmv_plan p, int g);

@@ -26,6 +26,7 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``) -- no function is
   nz_tiles        binary-search (searchsorted) re-derivation, ownership cover
   hot_columns     hand example, maximality of the count threshold
   classify_profile SPEC S:469-474 examples, strictness, monotonicity in P_ML
+  table1          SPEC S:415-417 worked rows, diagonal closed form, brute-force per-row loops
   d16 encode/dec  SPEC S:134-136 widths, round trip, stencil gap closed forms
   features        SPEC S:415 sd example, stencil closed forms
   select          hand-evaluated rule table on the configs' closed-form features
@@ -515,3 +516,55 @@ def profile_select(f, bounds, window_max, K_long=100):
     d16 = bool(classes & CLASS_MB) and variant == VARIANT_STREAM and f["maxgap"] <= 65535
     xwin = bool(classes & CLASS_ML) and 8 * f["n"] <= window_max
     return Selection(variant, vs, d16, xwin, classes)
+
+
+# ---- full Table I (reading 23) ------------------
+def table1(rowptr, colind, n_cols=None, l2_bytes=126 * 2 ** 20, rp_bytes=None, line=16):
+    """Every Table I feature, from the definitions (numpy): size (1 iff CSR +
+    x + y fit in L2), density NNZ/(N*M), nnz_{min,max,avg,sd} over all rows,
+    bw_i = last - first + 1 (inclusive, S:426), scatter_i = nnz_i/bw_i,
+    clustering_i = ngroups_i/nnz_i (groups of consecutive columns),
+    bw/scatter/clustering statistics over the non-empty rows,
+    misses_avg = in-row gaps > line elements / N (all rows); population sd."""
+    rp = _rp64(rowptr)
+    ci = np.asarray(colind, np.int64)
+    n = rp.size - 1
+    m = int(n if n_cols is None else n_cols)
+    nnz = int(rp[-1])
+    lens = np.diff(rp)
+    rpb = (np.asarray(rowptr).dtype.itemsize if rp_bytes is None else rp_bytes)
+    ws = 12 * nnz + rpb * (n + 1) + 8 * m + 8 * n
+    out = {"size_fits_l2": int(ws <= l2_bytes), "density": nnz / (n * m) if n and m else 0.0}
+    out["nnz_min"] = float(lens.min()) if n else 0.0
+    out["nnz_max"] = float(lens.max()) if n else 0.0
+    out["nnz_avg"] = float(lens.mean()) if n else 0.0
+    out["nnz_sd"] = float(np.sqrt(((lens - lens.mean()) ** 2).mean())) if n else 0.0
+    ne = lens > 0
+    first = ci[rp[:-1][ne]]
+    last = ci[rp[1:][ne] - 1]
+    bw = (last - first + 1).astype(np.float64)
+    sc = lens[ne] / bw
+    row_of = np.repeat(np.arange(n), lens)
+    head = np.zeros(nnz, bool)
+    head[rp[:-1][ne]] = True
+    g = np.diff(ci)
+    nh = ~head[1:]
+    new_group = np.zeros(nnz, bool)
+    new_group[1:] = nh & (g > 1)
+    groups = 1 + np.bincount(row_of[new_group], minlength=n)
+    cl = groups[ne] / lens[ne]
+    misses = int(np.count_nonzero(nh & (g > line)))
+    k = int(ne.sum())
+    def stat(v):
+        if k == 0:
+            return 0.0, 0.0
+        a = v.sum() / k
+        return float(a), float(np.sqrt(((v - a) ** 2).sum() / k))
+    out["bw_min"] = float(bw.min()) if k else 0.0
+    out["bw_max"] = float(bw.max()) if k else 0.0
+    out["bw_avg"], out["bw_sd"] = stat(bw)
+    out["scatter_avg"], out["scatter_sd"] = stat(sc)
+    out["clustering_avg"] = float(cl.sum() / k) if k else 0.0
+    out["misses_avg"] = misses / n if n else 0.0
+    out["n_nonempty"] = k
+    return out

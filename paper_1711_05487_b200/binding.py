@@ -101,6 +101,16 @@ lib.spmv_norm_partial_count.restype = _i32
 lib.spmv_norm_partials.argtypes = [_vp, _vp, _vp]
 lib.spmv_normalize.argtypes = [_vp, _vp, _vp, ctypes.c_int, _vp, _vp]
 lib.spmv_plan_query.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
+
+
+class Table1(ctypes.Structure):
+    _fields_ = [("size_fits_l2", ctypes.c_int32), ("pad_", ctypes.c_int32)] + \
+               [(k, ctypes.c_double) for k in ("density", "nnz_min", "nnz_max", "nnz_avg", "nnz_sd", "bw_min",
+                                               "bw_max", "bw_avg", "bw_sd", "scatter_avg", "scatter_sd",
+                                               "clustering_avg", "misses_avg")] + [("n_nonempty", ctypes.c_int64)]
+
+
+lib.spmv_plan_table1.argtypes = [_vp, ctypes.POINTER(Table1)]
 lib.spmv_plan_x_device.argtypes = [_vp, ctypes.c_int]
 lib.spmv_plan_x_device.restype = _vp
 lib.spmv_plan_y_device.argtypes = [_vp, ctypes.c_int]
@@ -256,6 +266,11 @@ class Plan:
         d["feat"] = {k: getattr(i.feat, k) for k, _ in Features._fields_}
         d["shard_bounds"] = list(i.shard_bounds)[: i.ngpus + 1]
         return d
+
+    def table1(self) -> dict:
+        t = Table1()
+        _check(lib.spmv_plan_table1(self._h, ctypes.byref(t)))
+        return {k: getattr(t, k) for k, _ in Table1._fields_ if k != "pad_"}
 
     def export(self, which, g=0) -> np.ndarray:
         w = ARR[which] if isinstance(which, str) else which

@@ -1252,6 +1252,37 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
   });
 }
 
+spmv_status spmv_plan_table1(spmv_plan p, spmv_table1* out) {
+  return guard([&] {
+    if (!p || !out) fail(SPMV_E_ARG, "null argument");
+    if (p->shards.size() != 1) fail(SPMV_E_ARG, "spmv_plan_table1 needs a single-shard plan");
+    Shard& s = p->shards[0];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    Table1 t;
+    const int32_t* hot = (s.use_nz && s.nz.n_hot > 0 && s.nz.V.col == s.col) ? s.nz.hot_cols : nullptr;
+    if (compute_table1(s.view(), hot, s.sm_count, t, s.stream) != 0) ck(cudaGetLastError(), "table1");
+    g_launches += s.m ? 2 : 0;
+    memset(out, 0, sizeof *out);
+    const double ws = 12.0 * (double)p->nnz + (double)p->rp_bytes * (double)(p->n_rows + 1) + 8.0 * (double)p->n_cols +
+                      8.0 * (double)p->n_rows;
+    out->size_fits_l2 = ws <= (double)p->props.l2_bytes ? 1 : 0;
+    out->density = (p->n_rows && p->n_cols) ? (double)p->nnz / ((double)p->n_rows * (double)p->n_cols) : 0.0;
+    out->nnz_min = (double)p->feat.nnz_min;
+    out->nnz_max = (double)p->feat.nnz_max;
+    out->nnz_avg = p->feat.nnz_avg;
+    out->nnz_sd = p->feat.nnz_sd;
+    out->bw_min = t.bw_min;
+    out->bw_max = t.bw_max;
+    out->bw_avg = t.bw_avg;
+    out->bw_sd = t.bw_sd;
+    out->scatter_avg = t.scatter_avg;
+    out->scatter_sd = t.scatter_sd;
+    out->clustering_avg = t.clustering_avg;
+    out->misses_avg = p->n_rows ? (double)t.misses_total / (double)p->n_rows : 0.0;
+    out->n_nonempty = t.n_nonempty;
+  });
+}
+
 double* spmv_plan_x_device(spmv_plan p, int g) {
   return (p && g >= 0 && g < (int)p->shards.size()) ? p->shards[g].x : nullptr;
 }

@@ -194,6 +194,14 @@ struct ProfileBounds {
 int run_profile_probes(const MatView& A, int vs, int sm_count, int64_t l2_bytes, double* x, double* y,
                        ProfileBounds& out, cudaStream_t s);
 
+// ---- full Table I features (table1.cu; f4) ------------------------------------
+struct Table1 {
+  double bw_min = 0, bw_max = 0, bw_avg = 0, bw_sd = 0, scatter_avg = 0, scatter_sd = 0, clustering_avg = 0;
+  int64_t n_nonempty = 0, misses_total = 0;
+};
+// hot_cols: the plan's hot-x column list when its colind copy is re-encoded (else null)
+int compute_table1(const MatView& A, const int32_t* hot_cols, int sm_count, Table1& out, cudaStream_t s);
+
 // ---- iterated mode -------------------------------------------------------------
 int launch_norm_partials(const double* y, int64_t m, double* partials, cudaStream_t s);
 int launch_normalize(const double* y, int64_t m, const double* partials, int count, double* x_out,

@@ -415,3 +415,17 @@ def test_profile_mode_selection(c, small):
     assert (s["variant"], s["vs"], bool(s["d16"]), bool(s["xwin"]), s["classes"]) == \
         (o.variant, o.vs, o.d16, o.xwin, o.classes), (b, s)
     assert_bound(p.execute(m.x), m)
+
+
+
+# full Table I on the device (f4) vs the oracle's definitions
+@pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
+def test_table1_device(name, m):
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size)
+    t = p.table1()
+    o = oracle.table1(m.rowptr, m.colind, n_cols=m.x.size, l2_bytes=spmv.device_query(0)["l2_bytes"])
+    for k in ("size_fits_l2", "n_nonempty", "bw_min", "bw_max", "nnz_min", "nnz_max"):
+        assert t[k] == o[k], k
+    for k in ("density", "nnz_avg", "nnz_sd", "bw_avg", "bw_sd", "scatter_avg", "scatter_sd", "clustering_avg",
+              "misses_avg"):
+        assert abs(t[k] - o[k]) <= 1e-12 * max(1.0, abs(o[k])), (k, t[k], o[k])

@@ -428,3 +428,45 @@ def test_profile_select_table2_mapping():
     assert (s.variant, s.d16) == (S.VARIANT_STREAM, False)                                  # CMP
     fl = {**f, "n_long": 10, "nnz_max": 5000, "nnz_long": 50000}
     assert S.profile_select(fl, {**b, "p_imb": 2.0}, 1 << 27).variant == S.VARIANT_SPLIT    # dense long rows
+
+
+# ---- full Table I (reading 23) --------------------------------
+def test_table1_spec_worked_rows():
+    rp = np.array([0, 4])
+    ci = np.array([4, 5, 6, 20], np.int32)
+    t = oracle.table1(rp, ci, n_cols=30, line=8)
+    assert t["bw_avg"] == 17 and abs(t["scatter_avg"] - 4 / 17) < 1e-15 and t["clustering_avg"] == 0.5
+    assert t["misses_avg"] == 1.0  # gap 14 > 8 elements (S:416, 64-B lines)
+    assert oracle.table1(rp, ci, n_cols=30)["misses_avg"] == 0.0  # 128-B lines: 14 <= 16
+    # lengths [1, 2, 3]: nnz_sd = sqrt(2/3)
+    t = oracle.table1(np.array([0, 1, 3, 6]), np.array([0, 0, 1, 0, 1, 2], np.int32), n_cols=3)
+    # consecutive columns: one group per row, clustering_i = 1 / nnz_i
+    assert abs(t["nnz_sd"] - math.sqrt(2 / 3)) < 1e-15 and abs(t["clustering_avg"] - (1 + 1 / 2 + 1 / 3) / 3) < 1e-15
+    # diagonal: bw 1, scatter 1, clustering 1, no misses
+    n = 50
+    t = oracle.table1(np.arange(n + 1), np.arange(n, dtype=np.int32))
+    assert (t["bw_min"], t["bw_max"], t["scatter_avg"], t["scatter_sd"], t["clustering_avg"], t["misses_avg"]) == \
+        (1.0, 1.0, 1.0, 0.0, 1.0, 0.0)
+    assert t["density"] == 1 / n and t["size_fits_l2"] == 1
+
+
+def test_table1_bruteforce_rows():
+    for name, m in sg.small_suite(seed=11)[:6]:
+        t = oracle.table1(m.rowptr, m.colind, n_cols=m.x.size)
+        rp = m.rowptr.astype(np.int64)
+        bws, scs, cls, miss = [], [], [], 0
+        for i in range(rp.size - 1):
+            row = m.colind[rp[i]:rp[i + 1]].astype(np.int64)
+            if row.size == 0:
+                continue
+            bws.append(row[-1] - row[0] + 1)
+            scs.append(row.size / bws[-1])
+            gaps = np.diff(row)
+            cls.append((1 + int(np.sum(gaps > 1))) / row.size)
+            miss += int(np.sum(gaps > 16))
+        if bws:
+            assert t["bw_min"] == min(bws) and t["bw_max"] == max(bws)
+            assert abs(t["bw_avg"] - np.mean(bws)) <= 1e-12 * max(1.0, np.mean(bws))
+            assert abs(t["scatter_sd"] - np.std(scs)) <= 1e-12
+            assert abs(t["clustering_avg"] - np.mean(cls)) <= 1e-12
+        assert t["misses_avg"] == miss / (rp.size - 1), name
