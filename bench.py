@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--seg", type=int, default=-1)
     ap.add_argument("--split-bins", type=int, default=-1, help="SPLIT non-long rows: 0 cta_stream bins, 1 nnz_split")
     ap.add_argument("--xwin", type=int, default=-1, help="L2 persistence window on x: -1 auto, 0 off, 1 on")
+    ap.add_argument("--no-halo", action="store_true", help="iterated mode: full all-gather of x instead of halos")
     ap.add_argument("--stages", type=int, default=0, help="STREAM smem ring depth (multiple of 4; 0 auto)")
     ap.add_argument("--hot", type=int, default=-1, help="NNZSPLIT hot-x table: -1 auto, 0 off, K columns")
     ap.add_argument("--no-aligned", action="store_true", help="nnz-aligned STREAM tiles (carries + fix-up)")
@@ -338,15 +339,27 @@ def run_native(a):
         steps = parallel.native_steps(plan)
         b = [int(v) for v in blk["bounds"]]
         dd = dist if world > 1 else parallel.NoDist
+        halo, recv_bytes = None, 0
+        if world > 1:  # halo exchange (f2): each rank receives only the x range its rows read
+            feat = info["feat"]
+            need = torch.tensor([feat["col_min"], feat["col_max"] + 1], dtype=torch.int64, device="cuda")
+            needs = [torch.empty(2, dtype=torch.int64, device="cuda") for _ in range(world)]
+            dist.all_gather(needs, need)
+            needs = [v.tolist() for v in needs]
+            halo = parallel.halo_plan(b, needs, rank) if not a.no_halo else None
+            recv_bytes = parallel.halo_bytes(b, needs, rank) if halo else 8 * (blk["N"] - n_rows)
         with torch.cuda.stream(stream):
-            parallel.iterate(dd, steps, b, rank, world, xf, yl, pl, pa, nu, 2)
-            ms_it = max_over_ranks(timed(lambda: parallel.iterate(dd, steps, b, rank, world, xf, yl, pl, pa, nu, 1),
-                                         a.iters)) / a.iters
-            exch = lambda: parallel.exchange_only(dd, b, rank, world, xf, pl, pa)  # noqa: E731
+            parallel.iterate(dd, steps, b, rank, world, xf, yl, pl, pa, nu, 2, halo=halo)
+            ms_it = max_over_ranks(timed(lambda: parallel.iterate(dd, steps, b, rank, world, xf, yl, pl, pa, nu, 1,
+                                                                  halo=halo), a.iters)) / a.iters
+            exch = lambda: parallel.exchange_only(dd, b, rank, world, xf, pl, pa, halo=halo)  # noqa: E731
             ms_ex = max_over_ranks(timed(exch, a.iters)) / a.iters
         iterated = {"iters_timed": a.iters, "ms_per_iter": ms_it, "spmv_ms": ms_step, "exchange_ms": ms_ex,
                     "gflops_per_iter": 2.0 * blk["nnz"] / (ms_it * 1e-3) / 1e9,
-                    "exchange": "NCCL all-gather(partials) + per-rank broadcast of x blocks" if world > 1 else "none (1 GPU)"}
+                    "exchange": ("none (1 GPU)" if world == 1 else
+                                 "NCCL all-gather(partials) + " + ("point-to-point halo of the x range each rank reads"
+                                                                   if halo else "per-rank broadcast of x blocks")),
+                    "x_recv_bytes_per_iter_rank0": recv_bytes}
 
     nnz = blk["nnz"]
     N = blk["N"]

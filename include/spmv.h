@@ -94,6 +94,8 @@ typedef struct spmv_features {
   double nnz_avg, nnz_sd, avg_short, sd_short;
   int64_t n_cols;          /* columns (x length); the long-row density test uses it */
   int64_t n_big_gaps;      /* distinct in-row gaps >= 65472 (129 = more than 128): escape-coded D16 needs <= 64 */
+  int64_t col_min, col_max;/* smallest / largest column index (x range the rows read; 0 / -1 when nnz = 0):
+                              the halo of a row block in the distributed iterated mode */
 } spmv_features;
 
 typedef struct spmv_device_props {

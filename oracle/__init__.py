@@ -203,6 +203,8 @@ def features(rowptr, colind, L_split=4096, line_elems=16, n_cols=None):
     d = {k: getattr(f, k) for k, _ in _Feat._fields_}
     d["n_cols"] = int(rp.size - 1 if n_cols is None else n_cols)
     d["n_big_gaps"] = big_gap_count(rp, ci)
+    c = np.asarray(colind)
+    d["col_min"], d["col_max"] = (int(c.min()), int(c.max())) if c.size else (0, -1)
     return d
 
 

@@ -57,7 +57,8 @@ class Features(ctypes.Structure):
                [(k, ctypes.c_uint64) for k in ("s1", "s2", "s1_short", "s2_short")] + \
                [(k, ctypes.c_int64) for k in ("maxgap", "misses")] + \
                [(k, ctypes.c_double) for k in ("nnz_avg", "nnz_sd", "avg_short", "sd_short")] + \
-               [("n_cols", ctypes.c_int64), ("n_big_gaps", ctypes.c_int64)]
+               [("n_cols", ctypes.c_int64), ("n_big_gaps", ctypes.c_int64), ("col_min", ctypes.c_int64),
+                ("col_max", ctypes.c_int64)]
 
 
 class DeviceProps(ctypes.Structure):

@@ -407,6 +407,13 @@ void features_from_stats(const std::vector<DevStats>& st, const std::vector<int6
     f.misses += s.misses;
   }
   if (f.n == 0) f.nnz_min = 0;
+  f.col_min = LLONG_MAX;
+  f.col_max = -1;
+  for (const auto& s : st) {
+    f.col_min = std::min<int64_t>(f.col_min, s.col_min);
+    f.col_max = std::max<int64_t>(f.col_max, s.col_max);
+  }
+  if (f.col_max < 0) f.col_min = 0;  // no nonzeros: the empty range [0, 0)
   {  // distinct in-row gaps >= kEsc0 over all shards (kBigTab + 1 = more than kBigTab)
     std::vector<int32_t> big;
     bool over = false;
@@ -592,6 +599,8 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     init.nnz_min = LLONG_MAX;
     init.rp_err = LLONG_MAX;
     init.col_err = LLONG_MAX;
+    init.col_min = LLONG_MAX;
+    init.col_max = -1;
     ck(cudaMemcpyAsync(s.stats, &init, sizeof init, cudaMemcpyHostToDevice, s.stream), "stats init");
     ck(cudaMemsetAsync(s.headbits, 0, ((size_t)(s.nnz + 31) / 32 + 1) * 4, s.stream), "memset");
     launch_rowstats(s.view(), P->l_split, s.headbits, s.stats, s.stream);
@@ -1180,12 +1189,17 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
         for (int g = 0; g < G; ++g) {
           Shard& s = p->shards[g];
           ck(cudaSetDevice(s.dev), "cudaSetDevice");
+          // halo exchange: shard g only reads x[col_min_g,
+          // col_max_g], so it copies just the part of each other block inside
+          // that range (banded matrices: a few planes, not the whole vector)
+          const int64_t lo = s.hs.col_min, hi = s.hs.col_max + 1;
           for (int h = 0; h < G; ++h) {
             if (h == g) continue;
             Shard& t = p->shards[h];
+            const int64_t a = std::max<int64_t>(lo, t.row0), b = std::min<int64_t>(hi, t.row0 + t.m);
+            if (a >= b) continue;
             ck(cudaStreamWaitEvent(s.stream, t.ev_x, 0), "wait");
-            ck(cudaMemcpyPeerAsync(s.x + t.row0, s.dev, t.x + t.row0, t.dev, (size_t)t.m * 8, s.stream),
-               "x all-gather");
+            ck(cudaMemcpyPeerAsync(s.x + a, s.dev, t.x + a, t.dev, (size_t)(b - a) * 8, s.stream), "x halo");
           }
         }
       }
@@ -1195,7 +1209,14 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
     ck(cudaSetDevice(s0.dev), "cudaSetDevice");
     for (auto& s : p->shards) ck(cudaStreamSynchronize(s.stream), "iterate");
     ck(cudaMemcpy(nu.data(), s0.nu, (size_t)iters * 8, cudaMemcpyDeviceToHost), "nu");
-    ck(cudaMemcpy(x_out, s0.x, (size_t)p->n_cols * 8, cudaMemcpyDefault), "x_out");
+    // (halo exchange: each replica is complete only on the range its shard reads,
+    // so x_out is assembled from every shard's own block)
+    if (G == 1) {
+      ck(cudaMemcpy(x_out, s0.x, (size_t)p->n_cols * 8, cudaMemcpyDefault), "x_out");
+    } else {
+      for (auto& s : p->shards)
+        if (s.m) ck(cudaMemcpy(x_out + s.row0, s.x + s.row0, (size_t)s.m * 8, cudaMemcpyDefault), "x_out");
+    }
     cudaSetDevice(cur);
     if (nu_out) memcpy(nu_out, nu.data(), (size_t)iters * 8);
     if (last_norm) *last_norm = nu[iters - 1];

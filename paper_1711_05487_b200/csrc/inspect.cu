@@ -68,11 +68,13 @@ __global__ void __launch_bounds__(kNT) validate_gaps_kernel(const int32_t* __res
   for (int i = threadIdx.x; i < kBigTab; i += blockDim.x) tab[i] = 0;
   if (threadIdx.x == 0) over = 0;
   __syncthreads();
-  long long mg = 0, miss = 0, err = LLONG_MAX;
+  long long mg = 0, miss = 0, err = LLONG_MAX, cmin = LLONG_MAX, cmax = -1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz; j += stride) {
     const int64_t c = col[j];
     if (c < 0 || c >= n_cols) { long long k = 2 * j; err = k < err ? k : err; continue; }
+    cmin = c < cmin ? c : cmin;
+    cmax = c > cmax ? c : cmax;
     const bool head = (headbits[j >> 5] >> (j & 31)) & 1u;
     if (!head && j > 0) {
       const int64_t g = c - (int64_t)col[j - 1];
@@ -107,7 +109,10 @@ __global__ void __launch_bounds__(kNT) validate_gaps_kernel(const int32_t* __res
   }
   if (threadIdx.x == 0 && over) st->big_over = 1;
   mg = warp_max(mg); miss = warp_sum(miss); err = warp_min(err);
+  cmin = warp_min(cmin); cmax = warp_max(cmax);
   if ((threadIdx.x & 31) == 0) {
+    if (cmin != LLONG_MAX) atomicMin(&st->col_min, cmin);
+    if (cmax >= 0) atomicMax(&st->col_max, cmax);
     if (mg) atomicMax(&st->maxgap, mg);
     if (miss) atomicAdd((unsigned long long*)&st->misses, (unsigned long long)miss);
     if (err != LLONG_MAX) atomicMin(&st->col_err, err);

@@ -18,6 +18,7 @@ struct DevStats {
   long long rp_err;   // smallest row i with rowptr[i+1] < rowptr[i] (LLONG_MAX if none)
   long long col_err;  // min over nonzeros of 2*j + (order violation ? 1 : 0) (LLONG_MAX if none)
   long long n_incoming;  // STREAM tiles with an incoming row (carry fix-up needed)
+  long long col_min, col_max;  // column range touched (LLONG_MAX / -1 if no nonzero)
   // distinct in-row gaps >= kEsc0 (escape-coded D16): open-addressing set,
   // 0 = empty slot; big_over = 1 when more than kBigTab distinct values
   int32_t bigtab[128];

@@ -94,6 +94,7 @@ def test_selection_matches_oracle_on_random_features():
                  n_empty=int(n * g.choice([0, 0.1, 0.3, 0.6])), n_long=int(g.choice([0, 0, 5, 100])),
                  nnz_long=int(g.choice([0, 10 ** 5, 10 ** 7])), n_cols=int(n * g.choice([1, 0.1, 10])),
                  n_big_gaps=int(g.choice([0, 4, 64, 65, 129])),
+                 col_min=0, col_max=n - 1,
                  n_short=n, max_short=0, s1=nnz, s2=0, s1_short=0, s2_short=0,
                  maxgap=int(g.choice([3, 300, 70000, 10 ** 6])), misses=int(nnz * g.choice([0.1, 0.6, 0.9])),
                  nnz_avg=nnz / n, nnz_sd=1.0, avg_short=avg, sd_short=avg * float(g.choice([0.1, 0.9, 1.5])))

@@ -23,14 +23,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, K, out_q):
+def _worker(rank, world, port, K, out_q, use_halo=False, cfg=5):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_1711_05487_b200 as pkg
         from paper_1711_05487_b200 import parallel
-        m = sg.config(5, small=True)
+        m = sg.config(cfg, small=True)
         rp = m.rowptr.astype(np.int64)
         b = pkg.shard_bounds(rp, world)
         b0, b1 = int(b[rank]), int(b[rank + 1])
@@ -50,7 +50,19 @@ def _worker(rank, world, port, K, out_q):
         pl = torch.empty(P, dtype=torch.float64)
         pa = torch.empty(world * P, dtype=torch.float64)
         nu = torch.empty(K, dtype=torch.float64)
-        parallel.iterate(dist, steps, b, rank, world, x, y, pl, pa, nu, K)
+        halo = None
+        if use_halo:
+            need = torch.tensor([int(lci.min()), int(lci.max()) + 1] if lci.size else [0, 0], dtype=torch.int64)
+            needs = [torch.empty(2, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(needs, need)
+            halo = parallel.halo_plan(b, [n.tolist() for n in needs], rank)
+        parallel.iterate(dist, steps, b, rank, world, x, y, pl, pa, nu, K, halo=halo)
+        if use_halo:  # only the range this rank reads is guaranteed: compare that, plus its own block
+            lo, hi = int(lci.min()), int(lci.max()) + 1
+            xs = np.full(x.numel(), np.nan)
+            xs[lo:hi] = x.numpy()[lo:hi]
+            xs[b0:b1] = x.numpy()[b0:b1]
+            x = torch.from_numpy(xs)
         out_q.put((rank, b.tolist(), x.numpy().copy(), nu.numpy().copy()))
     finally:
         dist.destroy_process_group()
@@ -80,3 +92,51 @@ def test_sharded_power_iteration_gloo(world):
     # every rank ends with the identical replica and identical nu (rank-ordered combine)
     for rank, b, x, nu in res[1:]:
         assert np.array_equal(x, res[0][2]) and np.array_equal(nu, res[0][3])
+
+
+
+@pytest.mark.parametrize("world,cfg", [(2, 5), (3, 5), (4, 5), (3, 1)])
+def test_halo_exchange_power_iteration_gloo(world, cfg):
+    """Halo exchange (f2): each rank receives only the x ranges its rows read;
+    the iterated result equals the oracle on every rank's own block and on the
+    range it reads (banded 27-pt: small halos; random C1: whole blocks)."""
+    K = 20
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, K, q, True, cfg)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m = sg.config(cfg, small=True)
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, K)
+    assert rc == 0
+    for rank, b, x, nu in res:
+        ok = ~np.isnan(x)
+        assert ok.sum() >= b[rank + 1] - b[rank]
+        assert np.max(np.abs(x[ok] - xr[ok])) <= 1e-10 * np.max(np.abs(xr))
+        assert np.all(np.abs(nu - nur) <= 1e-12 * nur)
+
+
+def test_halo_plan_pure():
+    from paper_1711_05487_b200 import parallel
+    bounds = [0, 10, 20, 30]
+    needs = [(0, 12), (8, 23), (19, 30)]  # banded: each rank reads a little of its neighbours
+    s0, r0 = parallel.halo_plan(bounds, needs, 0)
+    s1, r1 = parallel.halo_plan(bounds, needs, 1)
+    s2, r2 = parallel.halo_plan(bounds, needs, 2)
+    assert s0 == [(1, 8, 10)] and r0 == [(1, 10, 12)]
+    assert s1 == [(0, 10, 12), (2, 19, 20)] and r1 == [(0, 8, 10), (2, 20, 23)]
+    assert s2 == [(1, 20, 23)] and r2 == [(1, 19, 20)]
+    # every send has the matching receive on the peer
+    plans = [parallel.halo_plan(bounds, needs, g) for g in range(3)]
+    for g, (sends, _) in enumerate(plans):
+        for peer, lo, hi in sends:
+            assert (g, lo, hi) in plans[peer][1]
+    assert parallel.halo_bytes(bounds, needs, 1) == 8 * (2 + 3)
+    # a rank reading everything receives every other block whole
+    s, r = parallel.halo_plan(bounds, [(0, 30)] * 3, 1)
+    assert r == [(0, 0, 10), (2, 20, 30)]
