@@ -771,10 +771,12 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     if (const char* e = getenv("SPMV_NZ_PERSIST")) z.persistent = atoi(e) != 0;
     z.T = (V.nnz + kNzTile - 1) / kNzTile;
     z.tile_q = s.alloc<int32_t>((size_t)z.T + 1);
+    z.emask = s.alloc<uint32_t>((size_t)std::max<int64_t>(z.T, 1) * 8);
+    z.epre = s.alloc<uint64_t>((size_t)std::max<int64_t>(z.T, 1));
     alloc_carries(s, z.T, z.carry_row, z.carry_val);
     z.max_run = maxlen / kNzTile + 2;
     launch_nz_tiles(z, s.stream);
-    count_launches(2, "nz tiles");
+    count_launches(4, "nz tiles");
     z.grid = nz_prepare(z, s.sm_count);
     if (z.grid < 0) fail(SPMV_E_CUDA, "nnz_split: occupancy query failed");
   };

@@ -74,6 +74,8 @@ struct NzPlan {
   const void* rpc = nullptr;
   const int32_t* rowmap = nullptr;
   int32_t* tile_q = nullptr;
+  uint32_t* emask = nullptr;  // [T][8] row-end bits of each 256-nonzero tile
+  uint64_t* epre = nullptr;   // [T] per-word prefix counts of emask (bytes)
   int32_t* carry_row = nullptr;
   double* carry_val = nullptr;
   int64_t mc = 0, T = 0, m_out = 0;

@@ -42,8 +42,18 @@ constexpr int kNzWarps = 8;  // warps per CTA (plain mode)
 #ifndef NZ_HOT_PF
 #define NZ_HOT_PF 0
 #endif
+#ifndef NZ_HOT_MASK
+#define NZ_HOT_MASK 0
+#endif
+#ifndef NZ_MASK
+#define NZ_MASK 1
+#endif
 constexpr int kNzHotWarps = NZ_HOT_WARPS;  // warps per CTA (hot-x mode: one CTA per SM)
 constexpr bool kNzHotPrefetch = NZ_HOT_PF;
+// row ends from the per-tile mask (see nz_tile_compute); B200: C4 134 -> 127 us,
+// C5 as nnz_split 4.47 -> 3.91 ms, C3 hot-x 282 -> 290 us (kept on tile_q + rpc)
+constexpr bool kNzHotMask = NZ_HOT_MASK;
+constexpr bool kNzMask = NZ_MASK;
 
 size_t nz_smem_bytes(int n_hot) { return n_hot > 0 ? (size_t)n_hot * 8 + 16 : 0; }
 
@@ -56,12 +66,13 @@ template <typename RP, bool HOT>
 __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 1 : 4)
     nzsplit_kernel(const NzP<RP> p) {
   constexpr int NW = HOT ? kNzHotWarps : kNzWarps;
+  constexpr bool MASK = HOT ? kNzHotMask : kNzMask;
   extern __shared__ __align__(16) double xh[];
-  __shared__ __align__(16) uint32_t emask_s[NW][8];
+  __shared__ __align__(16) uint32_t emask_s[MASK ? 1 : NW][8];
   pdl_trigger();
   pdl_wait();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* em = emask_s[w];
+  uint32_t* em = emask_s[MASK ? 0 : w];
   if constexpr (HOT) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(xh + p.n_hot);
     if (threadIdx.x == 0) {
@@ -83,18 +94,20 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
     int64_t k = (int64_t)blockIdx.x * NW + w;
     int c[8], cn[8];
     double v[8], vn[8];
-    if (k < p.T) nz_tile_load(p, k, lane, c, v);
+    NzMeta m, mn;
+    if (k < p.T) nz_tile_load<RP, MASK>(p, k, lane, c, v, m);
     for (; k < p.T; k += nw) {
-      if (k + nw < p.T) nz_tile_load(p, k + nw, lane, cn, vn);
-      nz_tile_compute<RP, HOT>(p, k, lane, em, xh, c, v);
+      if (k + nw < p.T) nz_tile_load<RP, MASK>(p, k + nw, lane, cn, vn, mn);
+      nz_tile_compute<RP, HOT, MASK>(p, k, lane, xh, em, c, v, m);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         c[i] = cn[i];
         v[i] = vn[i];
       }
+      m = mn;
     }
   } else {
-    for (int64_t k = (int64_t)blockIdx.x * NW + w; k < p.T; k += nw) nz_tile<RP, HOT>(p, k, lane, em, xh);
+    for (int64_t k = (int64_t)blockIdx.x * NW + w; k < p.T; k += nw) nz_tile<RP, HOT, MASK>(p, k, lane, xh, em);
   }
 }
 
@@ -127,6 +140,28 @@ __global__ void nz_tile_rows_kernel(const RP* __restrict__ rpc, int64_t mc, int6
 
 __global__ void set_i32_kernel(int32_t* p, int32_t v) { *p = v; }
 
+// emask bit e set when a (non-empty, compacted) row ends at nonzero e
+template <typename RP>
+__global__ void nz_emask_kernel(const RP* __restrict__ rpc, int64_t mc, uint32_t* __restrict__ emask) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= mc) return;
+  const int64_t e = (int64_t)rpc[q + 1] - 1;
+  atomicOr(emask + (e >> 5), 1u << (e & 31));
+}
+
+// epre[k] byte w = row ends in mask words [0, w) of tile k
+__global__ void nz_epre_kernel(const uint32_t* __restrict__ emask, int64_t T, uint64_t* __restrict__ epre) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= T) return;
+  uint64_t b = 0;
+  uint32_t acc = 0;
+  for (int w = 0; w < 8; ++w) {
+    b |= (uint64_t)acc << (8 * w);
+    acc += __popc(emask[k * 8 + w]);
+  }
+  epre[k] = b;
+}
+
 void launch_nz_tiles(const NzPlan& z, cudaStream_t s) {
   const int g = (int)((z.T + 1 + kNT - 1) / kNT);
   if (z.V.rp_bytes == 8)
@@ -134,6 +169,13 @@ void launch_nz_tiles(const NzPlan& z, cudaStream_t s) {
   else
     nz_tile_rows_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)z.rpc, z.mc, z.T, z.tile_q);
   set_i32_kernel<<<1, 1, 0, s>>>(const_cast<int32_t*>(z.rowmap) + z.mc, (int32_t)z.m_out);
+  cudaMemsetAsync(z.emask, 0, (size_t)z.T * 8 * sizeof(uint32_t), s);
+  const int ge = (int)std::max<int64_t>(1, (z.mc + kNT - 1) / kNT);
+  if (z.V.rp_bytes == 8)
+    nz_emask_kernel<int64_t><<<ge, kNT, 0, s>>>((const int64_t*)z.rpc, z.mc, z.emask);
+  else
+    nz_emask_kernel<int32_t><<<ge, kNT, 0, s>>>((const int32_t*)z.rpc, z.mc, z.emask);
+  nz_epre_kernel<<<(unsigned)std::max<int64_t>(1, (z.T + kNT - 1) / kNT), kNT, 0, s>>>(z.emask, z.T, z.epre);
 }
 
 template <typename RP>
@@ -146,6 +188,8 @@ static NzP<RP> nz_params(const NzPlan& z, const double* x, double* y) {
   p.y = y;
   p.rowmap = z.rowmap;
   p.tile_q = z.tile_q;
+  p.emask = z.emask;
+  p.epre = z.epre;
   p.carry_row = z.carry_row;
   p.carry_val = z.carry_val;
   p.orp = (const RP*)z.skip_rp;

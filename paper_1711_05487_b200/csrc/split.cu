@@ -20,7 +20,7 @@ template <typename RP>
 __global__ void __launch_bounds__(kSplitThreads, 4) split_fused_kernel(const NzP<RP> z, const LongP l, int64_t n_items,
                                                                          int64_t n_groups) {
   __shared__ double xs[kLongXB];
-  __shared__ __align__(16) uint32_t emask_s[kSplitThreads / 32][8];
+  __shared__ __align__(16) uint32_t emask_s[kSplitThreads / 32][8];  // tile_q + rpc path only
   pdl_trigger();
   pdl_wait();
   const int64_t total = n_items + n_groups;
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kSplitThreads, 4) split_fused_kernel(const NzP
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k = (b - Lb) * (kSplitThreads / 32) + w;  // nz tile: group (b - Lb), warp w
-  if (k < z.T) nz_tile<RP, false>(z, k, lane, emask_s[w], nullptr);
+  if (k < z.T) nz_tile<RP, false, true>(z, k, lane, nullptr, emask_s[w]);
 }
 
 // blocks [0, nfb): ordered carry fix-up of the bin (runs <= 16: one thread

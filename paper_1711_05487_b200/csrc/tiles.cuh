@@ -27,6 +27,8 @@ struct NzP {
   double* y;
   const int32_t* rowmap;
   const int32_t* tile_q;
+  const uint32_t* emask;  // [T][8] row-end bits: bit i of tile k set when a row ends at nonzero k*256+i
+  const uint64_t* epre;   // [T]: byte w = row ends in words [0, w) of the tile's mask
   int32_t* carry_row;
   double* carry_val;
   const RP* orp;        // non-null: zero a gap row only if it is empty in this rowptr (SPLIT: long rows are not ours)
@@ -36,11 +38,30 @@ struct NzP {
   int zero_gaps;
 };
 
-// warp tile k = nonzeros [k*256, (k+1)*256); em: the warp's 8-word smem row-end
-// mask; xh: the hot-x smem table (HOT)
-// the lane's 8 consecutive nonzeros of tile k (colind, values)
+// warp tile k = nonzeros [k*256, (k+1)*256); xh: the hot-x smem table (HOT).
+// Per-tile metadata loaded with the streams (one tile ahead where the kernel
+// prefetches): the lane's row-end mask word and tile_q[k], both indexed by k,
+// so no load of the compute phase waits on another global load except the
+// rowmap lookups of the rows it writes.
+// y = 0 for the empty rows between compacted rows q and q + 1 (SPLIT: only
+// those empty in orp too)
 template <typename RP>
-__device__ __forceinline__ void nz_tile_load(const NzP<RP>& p, int64_t k, int lane, int (&c)[8], double (&v)[8]) {
+__device__ __forceinline__ void nz_zero_gaps(const NzP<RP>& p, int64_t q) {
+  const int32_t ra = ld_ro(p.rowmap + q), rb = ld_ro(p.rowmap + q + 1);
+  for (int32_t r = ra + 1; r < rb; ++r)
+    if (!p.orp || ld_ro(p.orp + r + 1) == ld_ro(p.orp + r)) p.y[r] = 0.0;
+}
+
+struct NzMeta {
+  uint32_t mw;  // emask word lane/4 of the tile
+  uint32_t pw;  // row ends in the words before it (epre byte lane/4)
+  int32_t q0;   // tile_q[k]: first row (compacted) ending in or after the tile
+};
+
+// the lane's 8 consecutive nonzeros of tile k (colind, values) + metadata
+template <typename RP, bool MASK>
+__device__ __forceinline__ void nz_tile_load(const NzP<RP>& p, int64_t k, int lane, int (&c)[8], double (&v)[8],
+                                             NzMeta& m) {
   const int64_t t0 = k * kNzTile;
   const int cnt = (int)((p.nnz - t0) < kNzTile ? (p.nnz - t0) : kNzTile);
   const int e0 = lane * 8;
@@ -56,23 +77,35 @@ __device__ __forceinline__ void nz_tile_load(const NzP<RP>& p, int64_t k, int la
       v[i] = ok ? ld_stream(p.val + t0 + e0 + i) : 0.0;
     }
   }
+  if constexpr (MASK) {
+    m.mw = (uint32_t)ld_stream(reinterpret_cast<const int*>(p.emask) + k * 8 + (lane >> 2));
+    const uint32_t* pre = reinterpret_cast<const uint32_t*>(p.epre + k);
+    m.pw = (uint32_t)ld_stream(reinterpret_cast<const int*>(pre) + (lane >> 4));
+    m.q0 = ld_ro(p.tile_q + k);
+  }
 }
 
-template <typename RP, bool HOT>
-__device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int lane, uint32_t* em, const double* xh,
-                                                const int (&c)[8], const double (&v)[8]);
+template <typename RP, bool HOT, bool MASK>
+__device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int lane, const double* xh,
+                                                uint32_t* em, const int (&c)[8], const double (&v)[8],
+                                                const NzMeta& m);
 
-template <typename RP, bool HOT>
-__device__ __forceinline__ void nz_tile(const NzP<RP>& p, int64_t k, int lane, uint32_t* em, const double* xh) {
+template <typename RP, bool HOT, bool MASK>
+__device__ __forceinline__ void nz_tile(const NzP<RP>& p, int64_t k, int lane, const double* xh, uint32_t* em) {
   int c[8];
   double v[8];
-  nz_tile_load(p, k, lane, c, v);
-  nz_tile_compute<RP, HOT>(p, k, lane, em, xh, c, v);
+  NzMeta m;
+  nz_tile_load<RP, MASK>(p, k, lane, c, v, m);
+  nz_tile_compute<RP, HOT, MASK>(p, k, lane, xh, em, c, v, m);
 }
 
-template <typename RP, bool HOT>
-__device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int lane, uint32_t* em, const double* xh,
-                                                const int (&c)[8], const double (&v)[8]) {
+// MASK: row ends from the plan's per-tile mask (emask/epre, loaded with the
+// streams); else from tile_q[k..k+1] and the compacted rowptr (em: the warp's
+// 8-word smem scratch mask)
+template <typename RP, bool HOT, bool MASK>
+__device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int lane, const double* xh,
+                                                uint32_t* em, const int (&c)[8], const double (&v)[8],
+                                                const NzMeta& m) {
   const int64_t t0 = k * kNzTile;
   const int cnt = (int)((p.nnz - t0) < kNzTile ? (p.nnz - t0) : kNzTile);
   double xv[8];
@@ -82,40 +115,54 @@ __device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int
     else xv[i] = ld_x(p.x + c[i]);
   }
 
-  // rows ending in the tile: q in [q0, q1), end position rpc[q+1]-1
-  const int64_t q0 = ld_ro(p.tile_q + k), q1 = ld_ro(p.tile_q + k + 1);
-  const int n_end = (int)(q1 - q0);
-  if (lane < 8) em[lane] = 0u;
-  __syncwarp();
-  for (int j = lane; j < n_end; j += 32) {
-    const int64_t q = q0 + j;
-    const int e = (int)((int64_t)ld_ro(p.rpc + q + 1) - 1 - t0);
-    atomicOr(&em[e >> 5], 1u << (e & 31));
+  uint32_t my;
+  int before;
+  int64_t q0;
+  if constexpr (MASK) {
+    // the lane's 8 row-end bits; rows ending before them: the word prefix
+    // byte + the lower bits of the word; rows ending in the tile: q in
+    // [q0, q1) (lane 31 holds the count; the gap loop broadcasts it)
+    const int sh = (lane & 3) * 8;
+    my = (m.mw >> sh) & 0xffu;
+    before = (int)((m.pw >> (((lane >> 2) & 3) * 8)) & 0xffu) + __popc(m.mw & ((1u << sh) - 1u));
+    q0 = m.q0;
     if (p.zero_gaps) {
-      const int32_t ra = ld_ro(p.rowmap + q), rb = ld_ro(p.rowmap + q + 1);
-      for (int32_t r = ra + 1; r < rb; ++r)
-        if (!p.orp || ld_ro(p.orp + r + 1) == ld_ro(p.orp + r)) p.y[r] = 0.0;
+      const int n_end = __shfl_sync(0xffffffffu, before + __popc(my), 31);
+      for (int j = lane; j < n_end; j += 32) nz_zero_gaps(p, q0 + j);
     }
+  } else {
+    // rows ending in the tile: q in [q0, q1), end position rpc[q+1]-1
+    q0 = ld_ro(p.tile_q + k);
+    const int64_t q1 = ld_ro(p.tile_q + k + 1);
+    const int n_end = (int)(q1 - q0);
+    if (lane < 8) em[lane] = 0u;
+    __syncwarp();
+    for (int j = lane; j < n_end; j += 32) {
+      const int64_t q = q0 + j;
+      const int e = (int)((int64_t)ld_ro(p.rpc + q + 1) - 1 - t0);
+      atomicOr(&em[e >> 5], 1u << (e & 31));
+      if (p.zero_gaps) nz_zero_gaps(p, q);
+    }
+    __syncwarp();
+    const uint4 m0 = *reinterpret_cast<const uint4*>(em);
+    const uint4 m1 = *reinterpret_cast<const uint4*>(em + 4);
+    const uint32_t words[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+    const int wi = lane >> 2, sh = (lane & 3) * 8;
+    uint32_t word = 0;
+    before = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < wi) before += __popc(words[i]);
+      if (i == wi) word = words[i];
+    }
+    before += __popc(word & ((1u << sh) - 1u));
+    my = (word >> sh) & 0xffu;
   }
   if (k == 0 && p.zero_gaps) {
     const int32_t r0 = ld_ro(p.rowmap);
     for (int32_t r = lane; r < r0; r += 32)
       if (!p.orp || ld_ro(p.orp + r + 1) == ld_ro(p.orp + r)) p.y[r] = 0.0;
   }
-  __syncwarp();
-  const uint4 m0 = *reinterpret_cast<const uint4*>(em);
-  const uint4 m1 = *reinterpret_cast<const uint4*>(em + 4);
-  const uint32_t words[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-  const int wi = lane >> 2, sh = (lane & 3) * 8;
-  uint32_t word = 0;
-  int before = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if (i < wi) before += __popc(words[i]);
-    if (i == wi) word = words[i];
-  }
-  before += __popc(word & ((1u << sh) - 1u));
-  const uint32_t my = (word >> sh) & 0xffu;
 
   // lane-sequential sums; the first row end of the lane is completed after
   // the cross-lane scan, later ones are complete inside the lane
@@ -148,7 +195,7 @@ __device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int
   if (ne > 0) p.y[ld_ro(p.rowmap + qf)] = (lane > 0 ? cin : 0.0) + head;
   if (lane == 31) {
     if (cnt == kNzTile && !(my & 0x80u)) {
-      p.carry_row[k] = ld_ro(p.rowmap + q1);
+      p.carry_row[k] = ld_ro(p.rowmap + qf + ne);  // q1: lane 31 ends the count
       p.carry_val[k] = S;
     } else {
       p.carry_row[k] = -1;

@@ -256,10 +256,70 @@ __global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restr
   fixup_block(orow, oval, n2, 0, y, set, nullptr, nullptr);
 }
 
+// Runs up to kWarpRunMax carries (rows cut into at most that many tiles): one
+// launch. A thread per run start walks a short run (< 16 carries); a longer
+// run is summed by its whole warp, 256 carries per step (8 independent loads
+// per lane), lane partials combined by a fixed xor tree: deterministic.
+constexpr int64_t kWarpRunMax = 2048;
+
+__global__ void __launch_bounds__(kNT) fixup_warp_kernel(const int32_t* __restrict__ crow,
+                                                         const double* __restrict__ cval, int64_t T,
+                                                         double* __restrict__ y, int set) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t k = (int64_t)blockIdx.x * kNT + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int32_t r = k < T ? __ldcg(crow + k) : -1;
+  int32_t prev = __shfl_up_sync(0xffffffffu, r, 1);
+  if (lane == 0) prev = (k > 0 && k < T) ? __ldcg(crow + k - 1) : INT32_MIN;
+  bool longrun = false;
+  if (r >= 0 && prev != r) {
+    double s = __ldcg(cval + k);
+    int64_t q = k + 1;
+    for (; q < T && q < k + 16 && __ldcg(crow + q) == r; ++q) s += __ldcg(cval + q);
+    longrun = q == k + 16 && q < T && __ldcg(crow + q) == r;
+    if (!longrun) y[r] = set ? s : y[r] + s;
+  }
+  unsigned bal = __ballot_sync(0xffffffffu, longrun);
+  while (bal) {
+    const int src = __ffs(bal) - 1;
+    bal &= bal - 1;
+    const int64_t k0 = __shfl_sync(0xffffffffu, k, src);
+    const int32_t rr = __shfl_sync(0xffffffffu, r, src);
+    double acc = 0.0;
+    for (int64_t base = k0;; base += 256) {
+      int32_t cr[8];
+      double cv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t q = base + u * 32 + lane;
+        cr[u] = q < T ? __ldcg(crow + q) : -1;
+        cv[u] = q < T ? __ldcg(cval + q) : 0.0;
+      }
+      bool all = true;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc += cr[u] == rr ? cv[u] : 0.0;
+        all = all && cr[u] == rr;
+      }
+      if (!__all_sync(0xffffffffu, all)) break;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[rr] = set ? acc : y[rr] + acc;
+  }
+}
+
 int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int64_t max_run, cudaStream_t s) {
   if (T <= 0) return 0;
   if (max_run <= 16) {
     launch_pdl(fixup_kernel, dim3((unsigned)((T + kNT - 1) / kNT)), dim3(kNT), 0, s, (const int32_t*)crow,
+               (const double*)cval, T, y, set);
+    return 1;
+  }
+  static const bool hier = getenv("SPMV_FIXUP_HIER") != nullptr;
+  if (max_run <= kWarpRunMax && !hier) {
+    launch_pdl(fixup_warp_kernel, dim3((unsigned)((T + kNT - 1) / kNT)), dim3(kNT), 0, s, (const int32_t*)crow,
                (const double*)cval, T, y, set);
     return 1;
   }
