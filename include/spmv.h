@@ -143,6 +143,9 @@ typedef struct spmv_plan_info {
   double p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak, bmax;
   int32_t profile_vs, profile_ctas; /* baseline lanes per row, CTAs of its static partition */
   double profile_ms;          /* micro-benchmark time (part of select_ms: the classifier's t_pre) */
+  double x_reuse;             /* sampled fraction of nonzeros whose 128-B x line the previous row also reads */
+  int32_t nz_gather_l2;       /* nnz_split / split tiles gather x through L2 only (x_reuse < 0.5, x > 1 MB) */
+  int32_t pad3_;
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */

@@ -38,6 +38,10 @@ class Options(ctypes.Structure):
                 ("select_mode", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
     @classmethod
+    def _names(cls):
+        return {f[0] for f in cls._fields_} - {"struct_size", "reserved"}
+
+    @classmethod
     def make(cls, **kw):
         o = cls()
         lib.spmv_options_default(ctypes.byref(o))
@@ -47,6 +51,8 @@ class Options(ctypes.Structure):
                 continue
             if k == "force_variant" and isinstance(v, str):
                 v = VARIANTS[v]
+            if k not in cls._names():
+                raise TypeError(f"unknown spmv option {k!r}")
             setattr(o, k, v)
         return o
 
@@ -84,7 +90,8 @@ class PlanInfo(ctypes.Structure):
                 ("tiles_row_aligned", ctypes.c_int32), ("pad2_", ctypes.c_int32), ("n_nz_rows", ctypes.c_int64),
                 ("n_nz_tiles", ctypes.c_int64), ("n_hot", ctypes.c_int64), ("hot_cover", ctypes.c_double)] + \
                [(k, ctypes.c_double) for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak", "bmax")] + \
-               [("profile_vs", ctypes.c_int32), ("profile_ctas", ctypes.c_int32), ("profile_ms", ctypes.c_double)]
+               [("profile_vs", ctypes.c_int32), ("profile_ctas", ctypes.c_int32), ("profile_ms", ctypes.c_double),
+               ("x_reuse", ctypes.c_double), ("nz_gather_l2", ctypes.c_int32), ("pad3_", ctypes.c_int32)]
 
 
 _vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double

@@ -615,6 +615,8 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     launch_validate_gaps(s.view(), s.headbits, s.stats, s.stream);
     count_launches(s.nnz ? 1 : 0, "validate_gaps");
+    launch_x_reuse(s.view(), s.stats, s.stream);
+    count_launches(s.m > 1 && s.nnz ? 1 : 0, "x_reuse");
     ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
   }
   for (auto& s : P->shards) {
@@ -775,6 +777,11 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     z.epre = s.alloc<uint64_t>((size_t)std::max<int64_t>(z.T, 1));
     alloc_carries(s, z.T, z.carry_row, z.carry_val);
     z.max_run = maxlen / kNzTile + 2;
+    // x gathers through L2 only when sampled neighbouring rows share under
+    // half of their x lines and x exceeds 1 MB (B200: C3 283 -> 275 us, C4
+    // 126 -> 123 us; stencils as nnz_split lose 3-9 % without L1)
+    z.gather_l2 = s.hs.reuse_tot > 0 && 2 * s.hs.reuse_hit < s.hs.reuse_tot && V.n_cols * 8 > (1 << 20);
+    if (const char* e = getenv("SPMV_NZ_GATHER_L2")) z.gather_l2 = atoi(e) != 0;
     launch_nz_tiles(z, s.stream);
     count_launches(4, "nz tiles");
     z.grid = nz_prepare(z, s.sm_count);
@@ -1033,6 +1040,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   }
   P->encode_ms = now_ms() - t_d;
   if (getenv("SPMV_PLAN_TRACE"))
+    fprintf(stderr, "[spmv plan] x-line reuse %llu / %llu sampled nonzeros, nz gather_l2 %d\n",
+            P->shards[0].hs.reuse_hit, P->shards[0].hs.reuse_tot, (int)P->shards[0].nz.gather_l2);
+  if (getenv("SPMV_PLAN_TRACE"))
     fprintf(stderr, "[spmv plan] upload %.2f inspect %.2f select %.2f (profile %.2f) encode %.2f ms\n", P->upload_ms,
             P->inspect_ms, P->select_ms, P->profile_ms, P->encode_ms);
   ck(cudaSetDevice(cur), "cudaSetDevice");
@@ -1251,6 +1261,10 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     info->profile_ctas = p->pb.ctas;
     info->profile_ms = p->profile_ms;
     const Shard& s0 = p->shards[0];
+    unsigned long long rh = 0, rt = 0;
+    for (const Shard& s : p->shards) { rh += s.hs.reuse_hit; rt += s.hs.reuse_tot; }
+    info->x_reuse = rt ? (double)rh / (double)rt : 0.0;
+    info->nz_gather_l2 = s0.nz.gather_l2 ? 1 : 0;
     info->tile_nnz = s0.sp[0].C;
     info->n_tiles = s0.sp[0].T;
     info->tile_stride = s0.sp[0].stride;

@@ -32,6 +32,14 @@ __device__ __forceinline__ double2 ld_stream2(const double* p) {
 }
 // x gather: read-only path, cached in L1 (neighbouring rows share x entries)
 __device__ __forceinline__ double ld_x(const double* p) { return __ldg(p); }
+// x gather of the nnz tiles: L1-cached, or L2 only (L2G: rows without x-line
+// reuse; B200 measures the same ~270 G gathers/s either way for random
+// columns, and .cg leaves L1 to the streams and the in-flight misses)
+template <bool L2G>
+__device__ __forceinline__ double ld_xg(const double* p) {
+  if constexpr (L2G) return __ldcg(p);
+  else return __ldg(p);
+}
 
 template <typename T>
 __device__ __forceinline__ T ld_ro(const T* p) { return __ldg(p); }

@@ -140,6 +140,60 @@ void launch_validate_gaps(const MatView& A, const uint32_t* headbits, DevStats* 
   validate_gaps_kernel<<<grid_for(A.nnz), kNT, 0, s>>>(A.col, A.nnz, A.n_cols, headbits, st);
 }
 
+// x-line reuse probe (plan-time heuristic for the nnz_split gather cache
+// mode): kReuseRows rows sampled (all rows when fewer), a warp per row r >= 1, up to 256
+// nonzeros of r each; hit when row r-1 holds a column in the same 16-column
+// (128-B) line -- the L1 reuse a row-ordered sweep can expect
+constexpr int64_t kReuseRows = 4096;
+template <typename RP>
+__global__ void x_reuse_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ col, int64_t m,
+                               DevStats* st) {
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t S = (m - 1) < kReuseRows ? (m - 1) : kReuseRows;
+  if (wid >= S) return;
+  // pseudo-random rows (splitmix64 of the warp id): evenly spaced rows alias
+  // with structured matrices (C2: rows 512w all sit on a 16-column line edge)
+  uint64_t z = (uint64_t)wid + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  const int64_t r = S == m - 1 ? 1 + wid : 1 + (int64_t)(z % (uint64_t)(m - 1));
+  const int64_t a0 = rp[r - 1], a1 = rp[r], b0 = a1, b1 = rp[r + 1];
+  const int64_t nb = (b1 - b0) < 256 ? (b1 - b0) : 256;
+  unsigned hit = 0, tot = 0;
+  for (int64_t j = lane; j < nb; j += 32) {
+    const int64_t line0 = ((int64_t)col[b0 + j] >> 4) << 4;
+    int64_t lo = a0, hi = a1;  // first column >= line0 in row r-1
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (col[mid] < line0) lo = mid + 1;
+      else hi = mid;
+    }
+    hit += (lo < a1 && col[lo] < line0 + 16) ? 1u : 0u;
+    ++tot;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    hit += __shfl_xor_sync(0xffffffffu, hit, o);
+    tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  }
+  if (lane == 0 && tot) {
+    atomicAdd(&st->reuse_hit, (unsigned long long)hit);
+    atomicAdd(&st->reuse_tot, (unsigned long long)tot);
+  }
+}
+
+void launch_x_reuse(const MatView& A, DevStats* st, cudaStream_t s) {
+  if (A.m < 2 || A.nnz == 0) return;
+  const int64_t S = (A.m - 1) < kReuseRows ? (A.m - 1) : kReuseRows;
+  const int g = (int)((S * 32 + kNT - 1) / kNT);
+  if (A.rp_bytes == 8)
+    x_reuse_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, A.m, st);
+  else
+    x_reuse_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, A.m, st);
+}
+
 // ---- K2: tiles, merge splits -------------------------------------------------
 template <typename RP>
 __global__ void tile_rows_kernel(const RP* __restrict__ rp, int64_t m, int64_t C, int64_t T,

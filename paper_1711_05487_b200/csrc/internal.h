@@ -23,6 +23,9 @@ struct DevStats {
   // 0 = empty slot; big_over = 1 when more than kBigTab distinct values
   int32_t bigtab[128];
   int32_t big_over;
+  // x-line reuse probe: sampled rows r, nonzeros of r whose 128-B x line row
+  // r-1 also reads (hits) out of the sampled nonzeros (tot)
+  unsigned long long reuse_hit, reuse_tot;
 };
 // escape-coded 16-bit deltas (SURVEY 8(f) f3 reading; reading 21):
 // a delta d < kEsc0 is stored as d, a delta d >= kEsc0 as kEsc0 + (index of d
@@ -76,6 +79,7 @@ struct NzPlan {
   int32_t* tile_q = nullptr;
   uint32_t* emask = nullptr;  // [T][8] row-end bits of each 256-nonzero tile
   uint64_t* epre = nullptr;   // [T] per-word prefix counts of emask (bytes)
+  bool gather_l2 = false;     // x gathers bypass L1 (.cg): rows share no x lines with their neighbours
   int32_t* carry_row = nullptr;
   double* carry_val = nullptr;
   int64_t mc = 0, T = 0, m_out = 0;
@@ -96,7 +100,10 @@ int nz_prepare(NzPlan& z, int sm_count);  // persistent grid (<0 on error)
 // hot-x set (plan time): column counts + a count histogram of kHotBuckets,
 // then the ordered compaction of the columns with count >= t (first K)
 constexpr int kHotBuckets = 4096;
-constexpr int kHotMax = 16384;  // hot columns staged in smem (128 KB; B200 sweep on C3: 8K 283, 16K 275, 20K 285, 24K 322 us)
+#ifndef SPMV_HOT_MAX
+#define SPMV_HOT_MAX 16384
+#endif
+constexpr int kHotMax = SPMV_HOT_MAX;  // hot columns staged in smem (128 KB; B200 sweep on C3: 8K 283, 16K 275, 20K 285, 24K 322 us)
 void launch_col_counts(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* cnt, int32_t* H, cudaStream_t s);
 void launch_hot_flags(const int32_t* cnt, int64_t n_cols, int32_t t, int32_t* bsum, cudaStream_t s);
 void launch_hot_write(const int32_t* cnt, int64_t n_cols, int32_t t, const int32_t* boff, int K, int32_t* hot_cols,
@@ -107,6 +114,7 @@ int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaS
 // ---- inspector ------------------------------------------------------------
 void launch_rowstats(const MatView& A, int64_t l_split, uint32_t* headbits, DevStats* st, cudaStream_t s);
 void launch_validate_gaps(const MatView& A, const uint32_t* headbits, DevStats* st, cudaStream_t s);
+void launch_x_reuse(const MatView& A, DevStats* st, cudaStream_t s);  // DevStats reuse_hit / reuse_tot
 void launch_tile_rows(const MatView& A, int64_t C, int64_t T, int32_t* tile_row, DevStats* st, cudaStream_t s);
 void launch_merge_splits(const MatView& A, int64_t items, int64_t T, int32_t* mrow, int64_t* mnnz, cudaStream_t s);
 // ordered list of rows with len > l_split and exclusive prefix of their chunk counts

@@ -62,7 +62,7 @@ size_t nz_smem_bytes(int n_hot) { return n_hot > 0 ? (size_t)n_hot * 8 + 16 : 0;
 // per CTA and gathered from there. On B200 a divergent global gather costs
 // the L1 data pipe about one wavefront per lane (~1 sector / clk / SM is the
 // C3 ceiling), a shared-memory gather only its bank conflicts.
-template <typename RP, bool HOT>
+template <typename RP, bool HOT, bool L2G>
 __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 1 : 4)
     nzsplit_kernel(const NzP<RP> p) {
   constexpr int NW = HOT ? kNzHotWarps : kNzWarps;
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
     if (k < p.T) nz_tile_load<RP, MASK>(p, k, lane, c, v, m);
     for (; k < p.T; k += nw) {
       if (k + nw < p.T) nz_tile_load<RP, MASK>(p, k + nw, lane, cn, vn, mn);
-      nz_tile_compute<RP, HOT, MASK>(p, k, lane, xh, em, c, v, m);
+      nz_tile_compute<RP, HOT, MASK, L2G>(p, k, lane, xh, em, c, v, m);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         c[i] = cn[i];
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
       m = mn;
     }
   } else {
-    for (int64_t k = (int64_t)blockIdx.x * NW + w; k < p.T; k += nw) nz_tile<RP, HOT, MASK>(p, k, lane, xh, em);
+    for (int64_t k = (int64_t)blockIdx.x * NW + w; k < p.T; k += nw) nz_tile<RP, HOT, MASK, L2G>(p, k, lane, xh, em);
   }
 }
 
@@ -210,13 +210,16 @@ static int nz_grid_t(const NzPlan& z, int sm_count) {
   const int threads = HOT ? 32 * kNzHotWarps : 32 * kNzWarps;
   // (the attribute is per function: always the largest table, so plans of
   // different table sizes can share it)
-  if (HOT && cudaFuncSetAttribute(nzsplit_kernel<RP, HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)nz_smem_bytes(kHotMax)) != cudaSuccess)
+  if (HOT && (cudaFuncSetAttribute(nzsplit_kernel<RP, HOT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)nz_smem_bytes(kHotMax)) != cudaSuccess ||
+              cudaFuncSetAttribute(nzsplit_kernel<RP, HOT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)nz_smem_bytes(kHotMax)) != cudaSuccess))
     return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nzsplit_kernel<RP, HOT>, threads, sm) != cudaSuccess ||
-      per_sm < 1)
-    return -1;
+  const cudaError_t oe =
+      z.gather_l2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nzsplit_kernel<RP, HOT, true>, threads, sm)
+                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nzsplit_kernel<RP, HOT, false>, threads, sm);
+  if (oe != cudaSuccess || per_sm < 1) return -1;
   if (const char* e = getenv("SPMV_NZ_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
   int64_t grid = (int64_t)sm_count * per_sm;
   const int64_t nwarps = HOT ? kNzHotWarps : kNzWarps;
@@ -231,6 +234,19 @@ int nz_prepare(NzPlan& z, int sm_count) {
   return hot ? nz_grid_t<int32_t, true>(z, sm_count) : nz_grid_t<int32_t, false>(z, sm_count);
 }
 
+template <bool HOT>
+static void launch_nz_main(const NzPlan& z, const double* x, double* y, cudaStream_t s) {
+  const size_t sm = nz_smem_bytes(HOT ? z.n_hot : 0);
+  const dim3 blk(32 * (HOT ? kNzHotWarps : kNzWarps));
+  if (z.V.rp_bytes == 8) {
+    if (z.gather_l2) launch_pdl(nzsplit_kernel<int64_t, HOT, true>, dim3(z.grid), blk, sm, s, nz_params<int64_t>(z, x, y));
+    else launch_pdl(nzsplit_kernel<int64_t, HOT, false>, dim3(z.grid), blk, sm, s, nz_params<int64_t>(z, x, y));
+  } else {
+    if (z.gather_l2) launch_pdl(nzsplit_kernel<int32_t, HOT, true>, dim3(z.grid), blk, sm, s, nz_params<int32_t>(z, x, y));
+    else launch_pdl(nzsplit_kernel<int32_t, HOT, false>, dim3(z.grid), blk, sm, s, nz_params<int32_t>(z, x, y));
+  }
+}
+
 int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaStream_t s) {
   int n = 0;
   if (z.T == 0) {
@@ -242,16 +258,9 @@ int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaS
       launch_pdl(nz_hot_gather_kernel, dim3((z.n_hot + kNT - 1) / kNT), dim3(kNT), 0, s, z.hot_cols, z.n_hot, x,
                  z.xhot);
       ++n;
-      const size_t sm = nz_smem_bytes(z.n_hot);
-      if (z.V.rp_bytes == 8)
-        launch_pdl(nzsplit_kernel<int64_t, true>, dim3(z.grid), dim3(32 * kNzHotWarps), sm, s, nz_params<int64_t>(z, x, y));
-      else
-        launch_pdl(nzsplit_kernel<int32_t, true>, dim3(z.grid), dim3(32 * kNzHotWarps), sm, s, nz_params<int32_t>(z, x, y));
+      launch_nz_main<true>(z, x, y, s);
     } else {
-      if (z.V.rp_bytes == 8)
-        launch_pdl(nzsplit_kernel<int64_t, false>, dim3(z.grid), dim3(32 * kNzWarps), 0, s, nz_params<int64_t>(z, x, y));
-      else
-        launch_pdl(nzsplit_kernel<int32_t, false>, dim3(z.grid), dim3(32 * kNzWarps), 0, s, nz_params<int32_t>(z, x, y));
+      launch_nz_main<false>(z, x, y, s);
     }
     ++n;
   }

@@ -16,7 +16,7 @@ namespace spmv {
 
 constexpr int kSplitThreads = 256;
 
-template <typename RP>
+template <typename RP, bool L2G>
 __global__ void __launch_bounds__(kSplitThreads, 4) split_fused_kernel(const NzP<RP> z, const LongP l, int64_t n_items,
                                                                          int64_t n_groups) {
   __shared__ double xs[kLongXB];
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kSplitThreads, 4) split_fused_kernel(const NzP
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k = (b - Lb) * (kSplitThreads / 32) + w;  // nz tile: group (b - Lb), warp w
-  if (k < z.T) nz_tile<RP, false, true>(z, k, lane, nullptr, emask_s[w]);
+  if (k < z.T) nz_tile<RP, false, true, L2G>(z, k, lane, nullptr, emask_s[w]);
 }
 
 // blocks [0, nfb): ordered carry fix-up of the bin (runs <= 16: one thread
@@ -74,12 +74,18 @@ int launch_split_fused(const ExecArgs& a, cudaStream_t s) {
   if (a.stage != 2) {
     const int64_t items = long_items(a), groups = (z.T + kSplitThreads / 32 - 1) / (kSplitThreads / 32);
     const int grid = (int)(items + groups);
-    if (z.V.rp_bytes == 8)
-      launch_pdl(split_fused_kernel<int64_t>, dim3(grid), dim3(kSplitThreads), 0, s, nz_params64(z, a.x, a.y),
-                 long_params(a), items, groups);
-    else
-      launch_pdl(split_fused_kernel<int32_t>, dim3(grid), dim3(kSplitThreads), 0, s, nz_params32(z, a.x, a.y),
-                 long_params(a), items, groups);
+    const dim3 g(grid), b(kSplitThreads);
+    if (z.V.rp_bytes == 8) {
+      if (z.gather_l2)
+        launch_pdl(split_fused_kernel<int64_t, true>, g, b, 0, s, nz_params64(z, a.x, a.y), long_params(a), items, groups);
+      else
+        launch_pdl(split_fused_kernel<int64_t, false>, g, b, 0, s, nz_params64(z, a.x, a.y), long_params(a), items, groups);
+    } else {
+      if (z.gather_l2)
+        launch_pdl(split_fused_kernel<int32_t, true>, g, b, 0, s, nz_params32(z, a.x, a.y), long_params(a), items, groups);
+      else
+        launch_pdl(split_fused_kernel<int32_t, false>, g, b, 0, s, nz_params32(z, a.x, a.y), long_params(a), items, groups);
+    }
     ++n;
   }
   if (a.stage != 1) {

@@ -85,24 +85,24 @@ __device__ __forceinline__ void nz_tile_load(const NzP<RP>& p, int64_t k, int la
   }
 }
 
-template <typename RP, bool HOT, bool MASK>
+template <typename RP, bool HOT, bool MASK, bool L2G>
 __device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int lane, const double* xh,
                                                 uint32_t* em, const int (&c)[8], const double (&v)[8],
                                                 const NzMeta& m);
 
-template <typename RP, bool HOT, bool MASK>
+template <typename RP, bool HOT, bool MASK, bool L2G>
 __device__ __forceinline__ void nz_tile(const NzP<RP>& p, int64_t k, int lane, const double* xh, uint32_t* em) {
   int c[8];
   double v[8];
   NzMeta m;
   nz_tile_load<RP, MASK>(p, k, lane, c, v, m);
-  nz_tile_compute<RP, HOT, MASK>(p, k, lane, xh, em, c, v, m);
+  nz_tile_compute<RP, HOT, MASK, L2G>(p, k, lane, xh, em, c, v, m);
 }
 
 // MASK: row ends from the plan's per-tile mask (emask/epre, loaded with the
 // streams); else from tile_q[k..k+1] and the compacted rowptr (em: the warp's
-// 8-word smem scratch mask)
-template <typename RP, bool HOT, bool MASK>
+// 8-word smem scratch mask); L2G: x gathers bypass L1 (ld_xg)
+template <typename RP, bool HOT, bool MASK, bool L2G>
 __device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int lane, const double* xh,
                                                 uint32_t* em, const int (&c)[8], const double (&v)[8],
                                                 const NzMeta& m) {
@@ -111,8 +111,8 @@ __device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int
   double xv[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    if constexpr (HOT) xv[i] = c[i] < 0 ? xh[~c[i]] : ld_x(p.x + c[i]);
-    else xv[i] = ld_x(p.x + c[i]);
+    if constexpr (HOT) xv[i] = c[i] < 0 ? xh[~c[i]] : ld_xg<L2G>(p.x + c[i]);
+    else xv[i] = ld_xg<L2G>(p.x + c[i]);
   }
 
   uint32_t my;

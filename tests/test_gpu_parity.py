@@ -429,3 +429,48 @@ def test_table1_device(name, m):
     for k in ("density", "nnz_avg", "nnz_sd", "bw_avg", "bw_sd", "scatter_avg", "scatter_sd", "clustering_avg",
               "misses_avg"):
         assert abs(t[k] - o[k]) <= 1e-12 * max(1.0, abs(o[k])), (k, t[k], o[k])
+
+
+# ---- x-line reuse probe (gather cache mode of the nnz tiles) ----------------
+def _splitmix(w):
+    M = (1 << 64) - 1
+    z = (w + 0x9E3779B97F4A7C15) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def _reuse_numpy(rp, ci):
+    """Sampled fraction of nonzeros of row r (first 256) whose 16-column line
+    row r-1 also touches; rows as the plan samples them (all when < 4097)."""
+    rp = rp.astype(np.int64)
+    n = rp.size - 1
+    S = min(n - 1, 4096)
+    hits = tot = 0
+    for w in range(S):
+        r = 1 + w if S == n - 1 else 1 + _splitmix(w) % (n - 1)
+        a = ci[rp[r]:rp[r + 1]][:256] >> 4
+        b = np.unique(ci[rp[r - 1]:rp[r]] >> 4)
+        hits += int(np.isin(a, b).sum())
+        tot += a.size
+    return hits / tot if tot else 0.0
+
+
+@pytest.mark.parametrize("kind", ["stencil", "random", "rmat_small"])
+def test_x_reuse_probe(kind):
+    if kind == "stencil":
+        m = sg.stencil(48, 7)
+    elif kind == "random":
+        m = sg.randrows(300_000, 12, col_seed=5)
+    else:
+        m = sg.config(3, small=True)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="nnzsplit")
+    info = p.info()
+    want = _reuse_numpy(m.rowptr, m.colind)
+    assert info["x_reuse"] == pytest.approx(want, abs=1e-12)
+    if kind == "stencil":
+        assert want > 0.5 and info["nz_gather_l2"] == 0
+    if kind == "random":
+        assert want < 0.1 and info["nz_gather_l2"] == 1  # x = 2.4 MB > 1 MB
+    y = p.execute(m.x)
+    assert_bound(y, m)

@@ -1,8 +1,7 @@
 run() { name=$1; shift; timeout 300 python bench.py --no-cpu --no-e2e --iters 0 "$@" > gpurun_out/x_$name.log 2>&1; }
-for v in def hotmask hotmaskpf nomask; do
-  if [ $v = def ]; then unset SPMV_LIB_PATH; else export SPMV_LIB_PATH=exp/$v/libspmv.so; fi
-  run c3_$v --config 3 --steps 30
-  run c4_$v --config 4 --steps 30
-done
-unset SPMV_LIB_PATH
-run c3_def2 --config 3 --steps 30
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/x_pytest.txt 2>&1
+run c3 --config 3 --steps 30
+run c4 --config 4 --steps 30
+run c2nz --config 2 --steps 30 --variant nnzsplit
+run c5nz --config 5 --steps 10 --variant nnzsplit
+SPMV_PLAN_TRACE=1 python tools/dbg_reuse.py > gpurun_out/x_dbg.txt 2>&1
