@@ -91,8 +91,8 @@ int launch_vector(const ExecArgs& a, bool skip_long, cudaStream_t s) {
 // T carries (row, value) in tile order; a run of equal consecutive rows holds
 // the pieces of one row cut by tile edges. Each run is summed in order and
 // added to (set = 0) or stored in (set = 1) y[row]; rows < 0 are no carry.
-// Short runs (plan-time bound max_run <= 16): one thread per run start walks
-// it. Longer runs (long rows cut into many tiles): a hierarchical
+// Runs up to 2048 carries (plan-time bound max_run): fixup_seg_kernel, one
+// launch. Longer runs (long rows cut into many tiles): a hierarchical
 // reduce-by-key, 1024 carries per CTA (block segmented scan); runs cut by a
 // CTA edge are passed up as (head, tail) pieces to the next level, stored
 // after the T carries (fixup_capacity). Deterministic, no fp atomics.
@@ -105,21 +105,6 @@ int64_t fixup_capacity(int64_t T) {
     tot += n;
   }
   return tot > 1 ? tot : 1;
-}
-
-__global__ void __launch_bounds__(kNT) fixup_kernel(const int32_t* __restrict__ crow,
-                                                    const double* __restrict__ cval, int64_t T,
-                                                    double* __restrict__ y, int set) {
-  pdl_trigger();
-  pdl_wait();
-  const int64_t k = (int64_t)blockIdx.x * kNT + threadIdx.x;
-  if (k >= T) return;
-  const int32_t r = crow[k];
-  if (r < 0) return;
-  if (k > 0 && crow[k - 1] == r) return;
-  double s = cval[k];
-  for (int64_t q = k + 1; q < T && crow[q] == r; ++q) s += cval[q];
-  y[r] = set ? s : y[r] + s;
 }
 
 // one CTA of a reduce-by-key level: carries [b*1024, min(n, (b+1)*1024))
@@ -256,70 +241,72 @@ __global__ void __launch_bounds__(kNT) fixup_level_kernel(const int32_t* __restr
   fixup_block(orow, oval, n2, 0, y, set, nullptr, nullptr);
 }
 
-// Runs up to kWarpRunMax carries (rows cut into at most that many tiles): one
-// launch. A thread per run start walks a short run (< 16 carries); a longer
-// run is summed by its whole warp, 256 carries per step (8 independent loads
-// per lane), lane partials combined by a fixed xor tree: deterministic.
+// Runs up to kWarpRunMax carries (rows cut into at most that many tiles)
 constexpr int64_t kWarpRunMax = 2048;
 
-__global__ void __launch_bounds__(kNT) fixup_warp_kernel(const int32_t* __restrict__ crow,
-                                                         const double* __restrict__ cval, int64_t T,
-                                                         double* __restrict__ y, int set) {
+// Runs up to kWarpRunMax carries, one launch and no serial walk: each warp
+// loads 32 consecutive carries, a segmented warp scan sums every run piece
+// in it; a run that starts in the warp is written by its last lane there, or
+// -- when it continues past the warp -- finished by the whole warp reading
+// 256 carries per step. Pieces of runs that started in an earlier warp are
+// left to that warp. Deterministic (fixed shuffle trees).
+__global__ void __launch_bounds__(kNT) fixup_seg_kernel(const int32_t* __restrict__ crow,
+                                                        const double* __restrict__ cval, int64_t T,
+                                                        double* __restrict__ y, int set) {
   pdl_trigger();
   pdl_wait();
   const int64_t k = (int64_t)blockIdx.x * kNT + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int32_t r = k < T ? __ldcg(crow + k) : -1;
+  const double v = k < T ? __ldcg(cval + k) : 0.0;
   int32_t prev = __shfl_up_sync(0xffffffffu, r, 1);
   if (lane == 0) prev = (k > 0 && k < T) ? __ldcg(crow + k - 1) : INT32_MIN;
-  bool longrun = false;
-  if (r >= 0 && prev != r) {
-    double s = __ldcg(cval + k);
-    int64_t q = k + 1;
-    for (; q < T && q < k + 16 && __ldcg(crow + q) == r; ++q) s += __ldcg(cval + q);
-    longrun = q == k + 16 && q < T && __ldcg(crow + q) == r;
-    if (!longrun) y[r] = set ? s : y[r] + s;
-  }
-  unsigned bal = __ballot_sync(0xffffffffu, longrun);
-  while (bal) {
-    const int src = __ffs(bal) - 1;
-    bal &= bal - 1;
-    const int64_t k0 = __shfl_sync(0xffffffffu, k, src);
-    const int32_t rr = __shfl_sync(0xffffffffu, r, src);
-    double acc = 0.0;
-    for (int64_t base = k0;; base += 256) {
-      int32_t cr[8];
-      double cv[8];
+  int32_t nxt = __shfl_down_sync(0xffffffffu, r, 1);
+  if (lane == 31) nxt = (k + 1 < T) ? __ldcg(crow + k + 1) : INT32_MIN;
+  double S = v;
+  int f = r != prev;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t q = base + u * 32 + lane;
-        cr[u] = q < T ? __ldcg(crow + q) : -1;
-        cv[u] = q < T ? __ldcg(cval + q) : 0.0;
-      }
-      bool all = true;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        acc += cr[u] == rr ? cv[u] : 0.0;
-        all = all && cr[u] == rr;
-      }
-      if (!__all_sync(0xffffffffu, all)) break;
+  for (int o = 1; o < 32; o <<= 1) {
+    const double su = __shfl_up_sync(0xffffffffu, S, o);
+    const int fu = __shfl_up_sync(0xffffffffu, f, o);
+    if (lane >= o) {
+      if (!f) S += su;
+      f |= fu;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) y[rr] = set ? acc : y[rr] + acc;
   }
+  const bool own = r >= 0 && f;  // the run piece started inside this warp
+  if (own && nxt != r) y[r] = set ? S : y[r] + S;
+  const bool open = __shfl_sync(0xffffffffu, own && nxt == r, 31);  // lane 31's run goes on
+  if (!open) return;
+  const int32_t rr = __shfl_sync(0xffffffffu, r, 31);
+  const double s31 = __shfl_sync(0xffffffffu, S, 31);
+  double acc = lane == 0 ? s31 : 0.0;
+  for (int64_t base = k - lane + 32;; base += 256) {
+    int32_t cr[8];
+    double cv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t q = base + u * 32 + lane;
+      cr[u] = q < T ? __ldcg(crow + q) : -1;
+      cv[u] = q < T ? __ldcg(cval + q) : 0.0;
+    }
+    bool all = true;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc += cr[u] == rr ? cv[u] : 0.0;
+      all = all && cr[u] == rr;
+    }
+    if (!__all_sync(0xffffffffu, all)) break;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[rr] = set ? acc : y[rr] + acc;
 }
 
 int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int64_t max_run, cudaStream_t s) {
   if (T <= 0) return 0;
-  if (max_run <= 16) {
-    launch_pdl(fixup_kernel, dim3((unsigned)((T + kNT - 1) / kNT)), dim3(kNT), 0, s, (const int32_t*)crow,
-               (const double*)cval, T, y, set);
-    return 1;
-  }
-  static const bool hier = getenv("SPMV_FIXUP_HIER") != nullptr;
-  if (max_run <= kWarpRunMax && !hier) {
-    launch_pdl(fixup_warp_kernel, dim3((unsigned)((T + kNT - 1) / kNT)), dim3(kNT), 0, s, (const int32_t*)crow,
+  if (max_run <= kWarpRunMax) {
+    launch_pdl(fixup_seg_kernel, dim3((unsigned)((T + kNT - 1) / kNT)), dim3(kNT), 0, s, (const int32_t*)crow,
                (const double*)cval, T, y, set);
     return 1;
   }
