@@ -22,11 +22,17 @@
 //  Rows are written to y[rowmap[r]] (identity without a map). In row-step
 //  mode the row entering a tile is the tile's carry; in segmented mode the
 //  row leaving it is; the ordered fix-up kernel adds carries in tile order.
+#include <cstdlib>
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
 namespace spmv {
 
+#ifndef SPMV_STREAM_LB
+#define SPMV_STREAM_LB 5
+#endif
 #ifndef SPMV_D16_LB
 #define SPMV_D16_LB 7
 #endif
@@ -234,12 +240,17 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
   }
 }
 
+#ifndef STREAM_UNR1
+#define STREAM_UNR1 8
+#endif
+constexpr int kStreamUnroll1 = STREAM_UNR1;  // gathers in flight per lane, one lane per row (VS = 1)
+
 // MODE: 0 = row-step over nnz-aligned tiles, 1 = segmented, 2 = row-step over
 // row-aligned tiles (compile-time so the nnz-tile path carries no per-tile
 // offsets: measured ~9% faster on C5 than a runtime switch). D16: 0 = int32
 // colind, 1 = 16-bit deltas, 2 = 16-bit deltas with escape codes.
 template <int VS, typename RP, int D16, int MODE>
-__global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D16_LB : 8))
+__global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D16_LB : SPMV_STREAM_LB))
     stream_kernel(const StreamP<RP> p) {
   constexpr bool SEG = MODE == 1;
   constexpr bool AL = MODE == 2;
@@ -440,24 +451,23 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
         }
         double acc;
         if constexpr (!D16) {
-          // batches of 8 predicated elements per lane: 8 independent gathers in flight
+          // batches of UN predicated elements per lane: UN independent gathers
+          // in flight (values read from smem after the gathers are issued)
+          constexpr int UN = VS == 1 ? kStreamUnroll1 : 8;
           const int32_t* idx_s = reinterpret_cast<const int32_t*>(idx_b);
           double a0 = 0.0, a1 = 0.0;
-          for (int l0 = ls + lane; l0 < le; l0 += 8 * VS) {
-            int c[8];
-            double v[8], xv[8];
+          for (int l0 = ls + lane; l0 < le; l0 += UN * VS) {
+            double xv[UN];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < UN; ++u) {
               const int l = l0 + u * VS;
-              c[u] = l < le ? idx_s[l] : -1;
-              v[u] = l < le ? vals_s[l] : 0.0;
+              xv[u] = l < le ? ld_x(p.x + idx_s[l]) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_x(p.x + c[u]) : 0.0;
-#pragma unroll
-            for (int u = 0; u < 8; u += 2) {
-              a0 = fma(v[u], xv[u], a0);
-              a1 = fma(v[u + 1], xv[u + 1], a1);
+            for (int u = 0; u < UN; u += 2) {
+              const int l = l0 + u * VS;
+              a0 = fma(l < le ? vals_s[l] : 0.0, xv[u], a0);
+              a1 = fma(l + VS < le ? vals_s[l + VS] : 0.0, xv[u + 1], a1);
             }
           }
           acc = a0 + a1;
@@ -555,6 +565,7 @@ static int stream_prepare_t(const StreamPlan& sp, int sm_count) {
                                                     smem) != cudaSuccess ||
       per_sm < 1)
     return -1;
+  if (const char* e = getenv("SPMV_STREAM_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));  // experiments
   int64_t grid = (int64_t)sm_count * per_sm;
   if (grid > sp.T) grid = sp.T;
   return (int)grid;

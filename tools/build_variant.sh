@@ -16,4 +16,5 @@ for f in $ROOT/paper_1711_05487_b200/csrc/*.cu; do
 done
 wait
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libspmv.so "${objs[@]}" -cudart static -lpthread -ldl -lrt
+rm -f "${objs[@]}"
 echo built $out/libspmv.so

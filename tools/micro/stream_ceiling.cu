@@ -82,18 +82,86 @@ __global__ void __launch_bounds__(160) rd_tma(const char* __restrict__ in, int64
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nout; j += stride) out[j] = acc;
 }
 
+// generic TMA ring: S stages of CH bytes (runtime), 4 consumer warps + 1 producer
+__global__ void __launch_bounds__(160) rd_tma_rt(const char* __restrict__ in, int64_t nch, int S, int CH,
+                                                 double* __restrict__ out) {
+  extern __shared__ __align__(128) char sm[];
+  __shared__ uint64_t full[16], empty[16];
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) { for (int i = 0; i < S; ++i) { bar_init(&full[i], 1); bar_init(&empty[i], 4); } asm volatile("fence.mbarrier_init.release.cluster;"); }
+  __syncthreads();
+  double acc = 0.0;
+  if (w == 4) {
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, ++it) {
+        const int st = it % S;
+        if (it >= S) bar_wait(&empty[st], ((it / S) - 1) & 1);
+        bar_expect(&full[st], CH);
+        g2s(sm + (size_t)st * CH, in + c * CH, CH, &full[st]);
+      }
+    }
+  } else {
+    int it = 0;
+    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, ++it) {
+      const int st = it % S;
+      bar_wait(&full[st], (it / S) & 1);
+      const double* d = (const double*)(sm + (size_t)st * CH);
+      for (int j = threadIdx.x; j < CH / 8; j += 128) acc += d[j];
+      __syncwarp();
+      if (lane == 0) bar_arrive(&empty[st]);
+    }
+  }
+  if (acc == 1234.5) out[0] = acc;
+}
+
 __global__ void flush(double* f, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     f[i] = f[i] * 0.5 + 1.0;
 }
 
-int main() {
+int sweep(double* fl, int64_t fl_n, int sms) {
+  const int64_t bytes = 4096ll << 20;
+  char* in;
+  double* out;
+  cudaMalloc(&in, bytes);
+  cudaMalloc(&out, 64);
+  cudaMemset(in, 0, bytes);
+  cudaFuncSetAttribute(rd_tma_rt, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int CH : {3072, 6144, 9216, 12288, 16384, 32768})
+    for (int S : {2, 4, 8})
+      for (int occ : {1, 2, 4, 6, 8}) {
+        if ((size_t)S * CH * occ > 200 * 1024) continue;
+        const int64_t nch = bytes / CH;
+        float best = 1e30f;
+        for (int t = 0; t < 5; ++t) {
+          flush<<<sms * 4, 512>>>(fl, fl_n);
+          cudaEventRecord(e0);
+          rd_tma_rt<<<sms * occ, 160, (size_t)S * CH>>>(in, nch, S, CH, out);
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (t >= 1) best = std::min(best, ms);
+        }
+        printf("TMA CH %6d S %d ctas/SM %d  inflight/SM %4d KB  %8.1f us  %6.0f GB/s\n", CH, S, occ,
+               S * CH * occ / 1024, best * 1e3, nch * (double)CH / (best * 1e-3) / 1e9);
+      }
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
+
+int main(int argc, char** argv) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int64_t fl_n = 64ll << 20;  // 512 MB flush buffer
   double* fl;
   cudaMalloc(&fl, fl_n * 8);
   cudaMemset(fl, 0, fl_n * 8);
+  if (argc > 1) return sweep(fl, fl_n, sms);
   struct Case { const char* name; double rd_mb, wr_mb; };
   const Case cases[] = {{"C2-like 200MB rd + 17MB wr", 200.5, 16.8},
                         {"C4-like 430MB rd + 8MB wr", 430.0, 8.0},
