@@ -683,13 +683,18 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     sp.vs = vs;
     sp.seg = seg;
     const double avg = V.m ? (double)V.nnz / (double)V.m : 0.0;
-    // tile size: one pass of the consumer warp over its 32/VS rows (row-step
-    // mode; B200 sweeps: 768 for 27-nnz rows, 384 for 15-nnz and shorter
-    // rows), clamp [384, 4096]; 512 in the segmented mode
+    // tile size: P whole passes of the consumer warp over its 32/VS rows
+    // (row-step mode), the fewest passes giving >= 640 nonzeros -- a tile
+    // that ends just short of a pass boundary keeps the lanes busy, and below
+    // ~640 nonzeros the per-tile TMA/mbarrier overhead shows (B200 sweeps:
+    // 27-nnz rows 768 = 1 pass (896 = 1.04 passes: +21 %); 7-nnz rows 640 =
+    // 2.9 passes, 33.1 us vs 36.6 at 512 and 39.3 at 384), clamp [384, 4096];
+    // 512 in the segmented mode
     int64_t C = 512;
     if (!seg) {
       const double rows_per_pass = 32.0 / vs;
-      C = (int64_t)(rows_per_pass * avg / 128.0) * 128;
+      C = 0;
+      for (int P = 1; P <= 64 && C < 640; ++P) C = (int64_t)(P * rows_per_pass * avg / 128.0) * 128;
       C = std::min<int64_t>(4096, std::max<int64_t>(384, C));
     }
     sp.C = opt.tile_nnz > 0 ? opt.tile_nnz : C;
