@@ -422,8 +422,11 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     IMB: long rows (n_long > 0 and nnz_max > K_long*nnz_avg) ->
     long_row_split when they are dense enough for column-tiled x blocks
     (nnz_long >= 64 * n_long * ceil(n_cols/2048)), else nnz_split; skew
-    (sd_s/avg_s > skew_sd or empty/N > empty_frac) -> nnz_split. Regular rows -> cta_stream for avg_s <= 32
-    and more than 2^20 nonzeros (tiny matrices are launch-bound), else
+    (sd_s/avg_s > skew_sd or empty/N > empty_frac) -> nnz_split. Tiny
+    matrices (<= 2^20 nonzeros, launch-bound) -> csr_vector. Scattered
+    columns (misses/nnz > 0.75: most nonzeros open a new x line, the ML access
+    pattern of Table I) -> nnz_split (L1 x gathers, 8 per lane; DESIGN.md
+    reading 24). Other regular rows -> cta_stream for avg_s <= 32, else
     csr_vector (CMP analogue: lane group sized to the row, VS =
     clamp(pow2ceil(avg_s), 2, 32)). MB: working set > L2/2 (the
     D16 colind it maps to is available but not auto-selected: slower on
@@ -447,7 +450,11 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
         variant = VARIANT_SPLIT if dense_long else VARIANT_NNZSPLIT
     elif skew:
         variant = VARIANT_NNZSPLIT
-    elif avg_s <= 32 and nnz > (1 << 20):  # tiny matrices: launch-bound, plain csr_vector
+    elif nnz <= (1 << 20):  # tiny matrices: launch-bound, plain csr_vector
+        variant = VARIANT_VECTOR
+    elif nnz > 0 and f["misses"] > 0.75 * nnz:  # scattered columns (ML access pattern, Table I misses)
+        variant = VARIANT_NNZSPLIT
+    elif avg_s <= 32:
         variant = VARIANT_STREAM
     else:
         variant = VARIANT_VECTOR

@@ -269,10 +269,18 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   // tiny regular matrices (<= 2^20 nonzeros) are launch-bound: the plain
   // csr_vector kernel beats the warp-specialised stream kernel's set-up
   // (C1: 6 vs 10 us on B200, tools/table5.py)
+  // scattered columns (misses/nnz > 0.75, the ML access pattern of Table I)
+  // -> nnz_split: its 8 independent L1 gathers per lane beat the row-walking
+  // stream kernel once the lanes' rows share no x lines (B200, uniform random
+  // rows, tools/exp_random.py: 1M x 30/row 162 vs 274 us, 4M x 8/row 185 vs
+  // 267 us, the C4 short rows 77 vs 156 us; equal at x >> L2)
+  const bool scattered = nnz > 0 && (double)f.misses > 0.75 * (double)nnz;
   int variant = longr ? (dense_long ? SPMV_VARIANT_SPLIT : SPMV_VARIANT_NNZSPLIT)
                 : skew ? SPMV_VARIANT_NNZSPLIT
-                : (avg_s <= 32 && nnz > (1 << 20)) ? SPMV_VARIANT_STREAM
-                                                   : SPMV_VARIANT_VECTOR;
+                : nnz <= (1 << 20) ? SPMV_VARIANT_VECTOR
+                : scattered ? SPMV_VARIANT_NNZSPLIT
+                : avg_s <= 32 ? SPMV_VARIANT_STREAM
+                              : SPMV_VARIANT_VECTOR;
   if (o.force_variant > 0) variant = o.force_variant;
   if (variant == SPMV_VARIANT_STREAM) {
     // cta_stream: one lane per row for rows up to 32 nonzeros (lanes walk
@@ -789,6 +797,19 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     if (const char* e = getenv("SPMV_NZ_GATHER_L2")) z.gather_l2 = atoi(e) != 0;
     launch_nz_tiles(z, s.stream);
     count_launches(4, "nz tiles");
+    // a very long run of empty rows (> kNzGapMax) would be zeroed by one warp
+    // (R-MAT's long rows alone: 2.6 ms instead of ~60 us on B200): clear y
+    // before the pass instead and skip the in-kernel gap zeroing
+    {
+      int32_t* g = s.alloc<int32_t>(1);
+      int32_t gmax = 0;
+      launch_nz_max_gap(z, g, s.stream);
+      count_launches(1, "nz max gap");
+      ck(cudaMemcpyAsync(&gmax, g, 4, cudaMemcpyDeviceToHost, s.stream), "max gap");
+      ck(cudaStreamSynchronize(s.stream), "max gap");
+      z.memset_y = gmax > kNzGapMax;
+      if (z.memset_y) z.zero_gaps = false;
+    }
     z.grid = nz_prepare(z, s.sm_count);
     if (z.grid < 0) fail(SPMV_E_CUDA, "nnz_split: occupancy query failed");
   };

@@ -94,8 +94,11 @@ struct NzPlan {
   bool persistent = true;  // grid = resident CTAs (else one tile per warp: lets a concurrent kernel share the SMs)
   const void* skip_rp = nullptr;  // SPLIT: zero only the gap rows empty in this rowptr (long rows are written
                                   // concurrently by the long-row reduction)
+  bool memset_y = false;  // a gap of more than kNzGapMax empty rows: y cleared before the pass, no gap zeroing
 };
+constexpr int32_t kNzGapMax = 4096;  // longest empty-row run a warp zeroes in-kernel
 void launch_nz_tiles(const NzPlan& z, cudaStream_t s);  // tile_q and rowmap[mc] = m_out
+void launch_nz_max_gap(const NzPlan& z, int32_t* out, cudaStream_t s);  // *out = longest run of rows not in rowmap
 int nz_prepare(NzPlan& z, int sm_count);  // persistent grid (<0 on error)
 // hot-x set (plan time): column counts + a count histogram of kHotBuckets,
 // then the ordered compaction of the columns with count >= t (first K)
@@ -180,7 +183,10 @@ struct ExecArgs {
   bool split_fused;           // SPLIT: nz bin + tiled long rows interleaved in one grid
 };
 
-constexpr int64_t kLongXB = 2048;  // columns per x block staged in smem by the column-tiled long-row kernel
+#ifndef LONG_XB
+#define LONG_XB 2048
+#endif
+constexpr int64_t kLongXB = LONG_XB;  // columns per x block staged in smem by the column-tiled long-row kernel
 void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long, int64_t nblk, int64_t* seg,
                      cudaStream_t s);
 void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s);

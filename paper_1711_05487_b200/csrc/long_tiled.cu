@@ -14,7 +14,10 @@
 
 namespace spmv {
 
-constexpr int kLongRG = 2;  // row groups per x block (CTAs per block)
+#ifndef LONG_RG
+#define LONG_RG 2
+#endif
+constexpr int kLongRG = LONG_RG;  // row groups per x block (CTAs per block)
 
 // seg[q*(nblk+1) + b] = first nonzero of long row q with column >= b*XB
 template <typename RP>

@@ -162,6 +162,20 @@ __global__ void nz_epre_kernel(const uint32_t* __restrict__ emask, int64_t T, ui
   epre[k] = b;
 }
 
+// *out = max over q of the empty run before compacted row q (q <= mc; the
+// run after the last row ends at rowmap[mc] = m_out); *out zeroed by the caller
+__global__ void nz_max_gap_kernel(const int32_t* __restrict__ rowmap, int64_t mc, int32_t* out) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q > mc) return;
+  const int32_t g = rowmap[q] - (q > 0 ? rowmap[q - 1] + 1 : 0);
+  if (g > 0) atomicMax(out, g);
+}
+
+void launch_nz_max_gap(const NzPlan& z, int32_t* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, 4, s);
+  nz_max_gap_kernel<<<(unsigned)((z.mc + 1 + kNT - 1) / kNT), kNT, 0, s>>>(z.rowmap, z.mc, out);
+}
+
 void launch_nz_tiles(const NzPlan& z, cudaStream_t s) {
   const int g = (int)((z.T + 1 + kNT - 1) / kNT);
   if (z.V.rp_bytes == 8)
@@ -254,6 +268,7 @@ int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaS
     return 0;
   }
   if (stage != 2) {
+    if (z.memset_y) cudaMemsetAsync(y, 0, (size_t)z.m_out * 8, s);
     if (z.n_hot > 0) {
       launch_pdl(nz_hot_gather_kernel, dim3((z.n_hot + kNT - 1) / kNT), dim3(kNT), 0, s, z.hot_cols, z.n_hot, x,
                  z.xhot);

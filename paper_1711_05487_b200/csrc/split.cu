@@ -15,9 +15,12 @@
 namespace spmv {
 
 constexpr int kSplitThreads = 256;
+#ifndef SPLIT_LB
+#define SPLIT_LB 4
+#endif
 
 template <typename RP, bool L2G>
-__global__ void __launch_bounds__(kSplitThreads, 4) split_fused_kernel(const NzP<RP> z, const LongP l, int64_t n_items,
+__global__ void __launch_bounds__(kSplitThreads, SPLIT_LB) split_fused_kernel(const NzP<RP> z, const LongP l, int64_t n_items,
                                                                          int64_t n_groups) {
   __shared__ double xs[kLongXB];
   __shared__ __align__(16) uint32_t emask_s[kSplitThreads / 32][8];  // tile_q + rpc path only
@@ -72,6 +75,7 @@ int launch_split_fused(const ExecArgs& a, cudaStream_t s) {
   int n = 0;
   const NzPlan& z = a.nz;
   if (a.stage != 2) {
+    if (z.memset_y) cudaMemsetAsync(a.y, 0, (size_t)z.m_out * 8, s);
     const int64_t items = long_items(a), groups = (z.T + kSplitThreads / 32 - 1) / (kSplitThreads / 32);
     const int grid = (int)(items + groups);
     const dim3 g(grid), b(kSplitThreads);

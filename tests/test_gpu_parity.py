@@ -331,6 +331,11 @@ NZ_EDGE = [
     # runs of > 1024 carries: the hierarchical fix-up (two and three levels)
     ("huge_rows", [3, 600000, 2, 0, 300000, 1]),
     ("huge_adjacent", [270000, 270000, 1, 270000]),
+    # long empty runs between sparse non-empty rows: the warp-cooperative gap
+    # zeroing (gaps > 8 rows), gaps straddling 32-gap chunks, mixed with short gaps
+    ("empty_runs", ([0] * 2300 + [700]) * 40 + [0] * 5000),
+    ("empty_runs_mixed", ([0] * 9 + [1] + [0] * 3 + [2] + [0] * 40 + [1]) * 300 + [0] * 77),
+    ("empty_runs_dense_ends", ([1] * 40 + [0] * 500) * 20),
 ]
 
 

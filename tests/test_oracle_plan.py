@@ -241,6 +241,13 @@ def test_select_rule_table_on_closed_form_features():
     # 7-pt rows (avg < 16) keep int32 colind
     s = S.select(feat(15625000, 109000000, 6.98, 0.2, maxgap=62250, misses=10 ** 7, n_big_gaps=0), L2, WIN, 4)
     assert s.d16 is False
+    # uniform random rows (4M x 8/row: every nonzero opens a new x line) ->
+    # scattered columns -> nnz_split (reading 24), not the row-walking stream
+    s = S.select(feat(4000000, 36000000, 9.0, 0.3, maxgap=3999000, misses=35900000), L2, WIN, 4)
+    assert s.variant == S.VARIANT_NNZSPLIT and s.classes & S.CLASS_ML and not s.classes & S.CLASS_IMB
+    # the same pattern below 2^20 nonzeros stays on the launch-bound csr_vector
+    s = S.select(feat(100000, 900000, 9.0, 0.3, maxgap=99000, misses=899000), L2, WIN, 4)
+    assert s.variant == S.VARIANT_VECTOR
     # C1: 1.28 MB working set, 90,000 nonzeros -> launch-bound: csr_vector VS 16, no MB, no D16
     s = S.select(feat(10000, 90000, 9.0, 0.0, maxgap=9000, misses=80000), L2, WIN, 4)
     assert (s.variant, s.vs, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_VECTOR, 16, False, 0)
