@@ -34,7 +34,7 @@ namespace spmv {
 #define SPMV_STREAM_LB 5
 #endif
 #ifndef SPMV_D16_LB
-#define SPMV_D16_LB 7
+#define SPMV_D16_LB 5
 #endif
 constexpr int kConsumerWarps = kStreamConsumerWarps;
 constexpr int kStreamThreads = 32 * (kConsumerWarps + 1);
@@ -483,20 +483,25 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
             double a1 = 0.0;
             int c = base;
             for (int l0 = ls; l0 < le; l0 += 8) {
+              // branch-free decode: the 8 codes are read unconditionally (the
+              // stage's index area has >= 64 entries of slack past any tile
+              // end; a stale code indexes inside the 64-entry escape table)
+              // and masked by selects -- a per-element `if` compiled to a
+              // branch + reconvergence around every LDS.U16
+              uint32_t dd[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) dd[u] = d_s[l0 + u];
               int cc[8];
               double xv[8];
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
                 const int l = l0 + u;
-                if (l < le) {
-                  c += (l == ls) ? 0 : d16_delta<ESC>(d_s[l], esc_s);
-                  cc[u] = c;
-                } else {
-                  cc[u] = -1;
-                }
+                const int d = d16_delta<ESC>(dd[u], esc_s);
+                c += (l > ls && l < le) ? d : 0;
+                cc[u] = c;
               }
 #pragma unroll
-              for (int u = 0; u < 8; ++u) xv[u] = cc[u] >= 0 ? ld_x(p.x + cc[u]) : 0.0;
+              for (int u = 0; u < 8; ++u) xv[u] = l0 + u < le ? ld_x(p.x + cc[u]) : 0.0;
 #pragma unroll
               for (int u = 0; u < 8; u += 2) {
                 const int l = l0 + u;

@@ -1,6 +1,1 @@
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/x_pytest.txt 2>&1
-timeout 600 python tools/exp_parts.py --config 3 --variants auto,split --parts long > gpurun_out/x_parts_c3.txt 2>&1
-run() { name=$1; shift; timeout 300 python bench.py --no-cpu --no-e2e --iters 0 "$@" > gpurun_out/x_$name.log 2>&1; }
-run c3 --config 3 --steps 30
-run c4 --config 4 --steps 30
-run c2 --config 2 --steps 30
+timeout 1200 python -m pytest tests -m gpu -x -q -k "d16 or stream or dyadic" > gpurun_out/x_pytest.txt 2>&1
