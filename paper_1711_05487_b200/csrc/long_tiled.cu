@@ -48,9 +48,15 @@ void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long,
 }
 
 // CTA item loop (persistent when the grid is smaller than the item count)
-__global__ void __launch_bounds__(kNT) long_tiled_kernel(const LongP p) {
+#ifndef LONG_LB
+#define LONG_LB 4
+#endif
+__global__ void __launch_bounds__(kNT, LONG_LB) long_tiled_kernel(const LongP p) {
   __shared__ double xs[kLongXB];
-  for (int64_t it = blockIdx.x; it < p.nblk * p.rg; it += gridDim.x) long_item<kNT>(p, it, xs);
+  for (int64_t it = blockIdx.x; it < p.nblk * p.rg; it += gridDim.x) {
+    long_item<kNT>(p, it, xs);
+    __syncthreads();  // every warp is done with xs before the next item restages it
+  }
 }
 
 // y[long_rows[q]] = sum_b partial[q][b] (lane-strided, butterfly: fixed order)

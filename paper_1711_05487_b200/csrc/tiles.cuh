@@ -257,36 +257,72 @@ struct LongP {
 // consecutive nonzeros of a sorted row, i.e. nearby columns (~2-way bank
 // conflicts), where lane-contiguous chunks scatter over the whole block
 // (measured ~8 wavefronts per gather on C4).
+// The segment bounds of the warp's first 32 rows (lane j: row j) are loaded
+// with the x block, so a row starts with its stream loads; the caller
+// separates items with a barrier (xs is rewritten by the next item).
+#ifndef LONG_U
+#define LONG_U 16
+#endif
+constexpr int kLongU = LONG_U;  // nonzeros per lane per batch of the long-row stream
 template <int NT>
 __device__ __forceinline__ void long_item(const LongP& p, int64_t it, double* xs) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   constexpr int NW = NT / 32;
+  constexpr int XPT = (int)(kLongXB / NT);
   const int64_t b = it / p.rg, g = it % p.rg;
   const int64_t c0 = b * kLongXB;
   const int cw = (int)((p.n_cols - c0) < kLongXB ? (p.n_cols - c0) : kLongXB);
-  __syncthreads();  // previous readers of xs are done
-  for (int i = threadIdx.x; i < cw; i += NT) xs[i] = ld_x(p.x + c0 + i);
-  __syncthreads();
-  for (int64_t q = g + (int64_t)p.rg * w; q < p.n_long; q += (int64_t)p.rg * NW) {
-    const int64_t s0 = ld_ro(p.seg + q * (p.nblk + 1) + b), s1 = ld_ro(p.seg + q * (p.nblk + 1) + b + 1);
-    double a0 = 0.0, a1 = 0.0;
-    for (int64_t base = s0 + lane; base < s1; base += 512) {
-      int c[16];
-      double v[16];
+  const int64_t qs = (int64_t)p.rg * NW, q0 = g + (int64_t)p.rg * w, ld = p.nblk + 1;
+  const int nq = q0 < p.n_long ? (int)((p.n_long - 1 - q0) / qs) + 1 : 0;
+  long long sa = 0, sb = 0;
+  if (lane < nq) {
+    const int64_t q = q0 + qs * lane;
+    sa = ld_ro(p.seg + q * ld + b);
+    sb = ld_ro(p.seg + q * ld + b + 1);
+  }
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int64_t e = base + 32 * u;
-        c[u] = e < s1 ? ld_stream(p.col + e) - (int)c0 : 0;
-        v[u] = e < s1 ? ld_stream(p.val + e) : 0.0;
+  for (int u = 0; u < XPT; ++u) {
+    const int i = (int)threadIdx.x + NT * u;
+    if (i < cw) xs[i] = ld_x(p.x + c0 + i);
+  }
+  int64_t s0 = 0, s1 = 0;
+  auto bounds = [&](int j) {
+    if (j < 32) {
+      s0 = __shfl_sync(0xffffffffu, sa, j);
+      s1 = __shfl_sync(0xffffffffu, sb, j);
+    } else {
+      const int64_t q = q0 + qs * j;
+      s0 = ld_ro(p.seg + q * ld + b);
+      s1 = ld_ro(p.seg + q * ld + b + 1);
+    }
+  };
+  constexpr int U = kLongU;
+  __syncthreads();
+  for (int j = 0; j < nq; ++j) {
+    bounds(j);
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t bb = s0; bb < s1; bb += 32 * U) {
+      // one base pointer per stream + immediate offsets; slot u valid iff 32u < rem
+      const int32_t* cp = p.col + bb + lane;
+      const double* vp = p.val + bb + lane;
+      const int64_t r64 = s1 - bb - lane;
+      const int rem = r64 > 32 * U ? 32 * U : (int)r64;
+      int c[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = 32 * u < rem;
+        c[u] = ok ? ld_stream(cp + 32 * u) - (int)c0 : 0;
+        v[u] = ok ? ld_stream(vp + 32 * u) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 16; u += 2) {
+      for (int u = 0; u < U; u += 2) {
         a0 = fma(v[u], xs[c[u]], a0);
         a1 = fma(v[u + 1], xs[c[u + 1]], a1);
       }
     }
     const double t = warp_sum(a0 + a1);
-    if (lane == 0) p.partial[q * p.nblk + b] = t;
+    if (lane == 0) p.partial[(q0 + qs * j) * p.nblk + b] = t;
   }
 }
 
