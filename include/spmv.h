@@ -188,7 +188,12 @@ int spmv_execute_stage(spmv_plan p, const double* x, double* y, int stage);
 /* Iterated mode (BJ.configs[5]): x_0 = x0; for k < iters: y = A x_k,
  * nu_k = ||y||_2, x_{k+1} = y / nu_k. Writes x_iters to x_out (host or
  * device), nu_{iters-1} to *last_norm (nullable) and nu_0..nu_{iters-1} to
- * nu_out (nullable, host). Square plans only. Synchronous. */
+ * nu_out (nullable, host). Square plans only. Synchronous. Computed with
+ * deferred normalisation (reading 25): yh_k = A yh_{k-1}
+ * (yh_{-1} = x0), nu_k = ||yh_k|| / ||yh_{k-1}||, x_iters = yh_{iters-1} /
+ * ||yh_{iters-1}||, magnitudes kept in range by exact power-of-two rescales;
+ * equal to the per-step form up to rounding (SURVEY 8(c3) #21 tolerances).
+ * SPMV_E_ZERO_NORM when some ||y|| is 0. */
 spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters, double* last_norm,
                          double* nu_out);
 
@@ -204,6 +209,16 @@ int32_t spmv_norm_partial_count(void);
 int spmv_norm_partials(spmv_plan p, const double* y, double* partials);
 int spmv_normalize(spmv_plan p, const double* y, const double* partials, int count, double* x_out,
                    double* nu_dev);
+/* Deferred-normalisation steps (what spmv_iterate runs per shard):
+ *   spmv_norm_step: n = sqrt(sum_{q ascending} partials[q]) over `count`
+ *     partials; *nu_k = n / nn[0] (n when nn[0] == 0, i.e. the first step);
+ *     nn[0] = n and, when n leaves [2^-256, 2^256], y[0..n_rows) and nn[0]
+ *     are scaled by the same exact power of two (nn[1] = that factor, else
+ *     1). nn: 2 device doubles, zeroed by the caller before the first step.
+ *   spmv_unit: x_out[i] = y[i] / nn[0] for i < n (the final x = yh/||yh||;
+ *     x_out may equal y). */
+int spmv_norm_step(spmv_plan p, const double* partials, int count, double* nn, double* nu_k, double* y);
+int spmv_unit(spmv_plan p, const double* y, int64_t n, const double* nn, double* x_out);
 
 /* ---- inspection ---------------------------------------------------------- */
 

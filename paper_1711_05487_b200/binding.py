@@ -108,6 +108,8 @@ lib.spmv_iterate.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.POINTER(_d), _v
 lib.spmv_norm_partial_count.restype = _i32
 lib.spmv_norm_partials.argtypes = [_vp, _vp, _vp]
 lib.spmv_normalize.argtypes = [_vp, _vp, _vp, ctypes.c_int, _vp, _vp]
+lib.spmv_norm_step.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp, _vp]
+lib.spmv_unit.argtypes = [_vp, _vp, ctypes.c_int64, _vp, _vp]
 lib.spmv_plan_query.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
 
 
@@ -263,6 +265,12 @@ class Plan:
 
     def normalize(self, y, partials, count, x_out, nu_dev):
         _check(lib.spmv_normalize(self._h, _ptr(y), _ptr(partials), int(count), _ptr(x_out), _ptr(nu_dev)))
+
+    def norm_step(self, partials, count, nn, nu_k, y):
+        _check(lib.spmv_norm_step(self._h, _ptr(partials), int(count), _ptr(nn), _ptr(nu_k), _ptr(y)))
+
+    def unit(self, y, nn, x_out):
+        _check(lib.spmv_unit(self._h, _ptr(y), int(_numel(y)), _ptr(nn), _ptr(x_out)))
 
     def info(self) -> dict:
         i = PlanInfo()

@@ -133,6 +133,8 @@ struct Shard {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // iterated mode
   double* allpart = nullptr;  // G * kNormPartials
+  double* x2 = nullptr;       // second x replica (deferred-normalisation ping-pong)
+  double* nn = nullptr;       // running norm + rescale factor (norm.cu)
   double* nu = nullptr;
   int nu_cap = 0;
   cudaEvent_t ev_part = nullptr, ev_x = nullptr;
@@ -1187,28 +1189,77 @@ int spmv_normalize(spmv_plan p, const double* y, const double* partials, int cou
   });
 }
 
+int spmv_norm_step(spmv_plan p, const double* partials, int count, double* nn, double* nu_k, double* y) {
+  return guard([&] {
+    if (!p || !partials || !nn || !nu_k || !y || count < 1 || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    count_launches(launch_norm_step(partials, count, nn, nu_k, y, s.m, s.stream), "norm step");
+  });
+}
+
+int spmv_unit(spmv_plan p, const double* y, int64_t n, const double* nn, double* x_out) {
+  return guard([&] {
+    if (!p || !y || !nn || !x_out || n < 0 || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    count_launches(launch_unit(y, n, nn, x_out, s.stream), "unit");
+  });
+}
+
+namespace {
+// ML x-window on the replica the next SpMV reads (the iterate ping-pongs)
+void set_xwin(const spmv_plan_s* P, Shard& s, const double* base) {
+  if (!P->sel.xwin) return;
+  const size_t xb = (size_t)s.n_cols * 8;
+  const size_t win = std::min<size_t>(xb, (size_t)P->props.access_window_max);
+  const size_t persist = std::min<size_t>(win, (size_t)P->props.persisting_l2_max);
+  cudaStreamAttrValue v;
+  memset(&v, 0, sizeof v);
+  v.accessPolicyWindow.base_ptr = const_cast<double*>(base);
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = win ? std::min(1.0f, (float)persist / (float)win) : 0.f;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  ck(cudaStreamSetAttribute(s.stream, cudaStreamAttributeAccessPolicyWindow, &v), "access policy window");
+}
+}  // namespace
+
+// Deferred normalisation (norm.cu, reading 25): iteration k runs
+// the SpMV on replica `cur` (x_0, then yh_{k-1}) and writes yh_k straight into
+// the shard's block of replica `nxt`; the norm partials, the rank-ordered
+// norm step (nu_k = ||yh_k|| / ||yh_{k-1}||, exact power-of-two rescale when
+// the magnitude drifts) and the halo exchange of `nxt` follow; no x = y/nu
+// pass per iteration. x_iters = yh_{iters-1} / ||yh_{iters-1}|| at the end.
 spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters, double* last_norm,
                          double* nu_out) {
   return guard([&] {
     if (!p || !x0 || !x_out || iters < 1) fail(SPMV_E_ARG, "bad argument");
     if (p->n_rows != p->n_cols) fail(SPMV_E_ARG, "iterated mode needs a square matrix");
     const int G = (int)p->shards.size();
-    int cur = 0;
-    cudaGetDevice(&cur);
-    for (auto& s : p->shards) {
+    int cur_dev = 0;
+    cudaGetDevice(&cur_dev);
+    std::vector<double*> cur(G), nxt(G);
+    for (int g = 0; g < G; ++g) {
+      Shard& s = p->shards[g];
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
       if (s.nu_cap < iters) {
         s.nu = s.alloc<double>((size_t)iters);
         s.nu_cap = iters;
       }
+      if (!s.x2) s.x2 = s.alloc<double>((size_t)p->n_cols);
+      if (!s.nn) s.nn = s.alloc<double>(2);
+      ck(cudaMemsetAsync(s.nn, 0, 16, s.stream), "nn");
       ck(cudaMemcpyAsync(s.x, x0, (size_t)p->n_cols * 8, cudaMemcpyDefault, s.stream), "copy x0");
+      cur[g] = s.x;
+      nxt[g] = s.x2;
     }
     for (int k = 0; k < iters; ++k) {
       for (int g = 0; g < G; ++g) {
         Shard& s = p->shards[g];
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
-        count_launches(p->launch(s, s.x, s.y), "spmv");
-        count_launches(launch_norm_partials(s.y, s.m, s.allpart + (size_t)g * kNormPartials, s.stream), "norm");
+        set_xwin(p, s, cur[g]);
+        count_launches(p->launch(s, cur[g], nxt[g] + s.row0), "spmv");
+        count_launches(launch_norm_partials(nxt[g] + s.row0, s.m, s.allpart + (size_t)g * kNormPartials, s.stream),
+                       "norm");
         ck(cudaEventRecord(s.ev_part, s.stream), "event");
       }
       for (int g = 0; g < G; ++g) {
@@ -1221,8 +1272,8 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
           ck(cudaMemcpyPeerAsync(s.allpart + (size_t)h * kNormPartials, s.dev, t.allpart + (size_t)h * kNormPartials,
                                  t.dev, kNormPartials * 8, s.stream), "partials exchange");
         }
-        count_launches(launch_normalize(s.y, s.m, s.allpart, G * kNormPartials, s.x + s.row0, s.nu + k, s.stream),
-                       "normalize");
+        count_launches(launch_norm_step(s.allpart, G * kNormPartials, s.nn, s.nu + k, nxt[g] + s.row0, s.m, s.stream),
+                       "norm step");
         ck(cudaEventRecord(s.ev_x, s.stream), "event");
       }
       if (G > 1) {
@@ -1239,29 +1290,34 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
             const int64_t a = std::max<int64_t>(lo, t.row0), b = std::min<int64_t>(hi, t.row0 + t.m);
             if (a >= b) continue;
             ck(cudaStreamWaitEvent(s.stream, t.ev_x, 0), "wait");
-            ck(cudaMemcpyPeerAsync(s.x + a, s.dev, t.x + a, t.dev, (size_t)(b - a) * 8, s.stream), "x halo");
+            ck(cudaMemcpyPeerAsync(nxt[g] + a, s.dev, nxt[h] + a, t.dev, (size_t)(b - a) * 8, s.stream), "x halo");
           }
         }
       }
+      std::swap(cur, nxt);
+    }
+    // x_iters = yh_{iters-1} / ||yh_{iters-1}|| on each shard's own block
+    for (int g = 0; g < G; ++g) {
+      Shard& s = p->shards[g];
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      count_launches(launch_unit(cur[g] + s.row0, s.m, s.nn, nxt[g] + s.row0, s.stream), "unit");
+      set_xwin(p, s, s.x);
     }
     Shard& s0 = p->shards[0];
     std::vector<double> nu(iters);
     ck(cudaSetDevice(s0.dev), "cudaSetDevice");
     for (auto& s : p->shards) ck(cudaStreamSynchronize(s.stream), "iterate");
     ck(cudaMemcpy(nu.data(), s0.nu, (size_t)iters * 8, cudaMemcpyDeviceToHost), "nu");
-    // (halo exchange: each replica is complete only on the range its shard reads,
-    // so x_out is assembled from every shard's own block)
-    if (G == 1) {
-      ck(cudaMemcpy(x_out, s0.x, (size_t)p->n_cols * 8, cudaMemcpyDefault), "x_out");
-    } else {
-      for (auto& s : p->shards)
-        if (s.m) ck(cudaMemcpy(x_out + s.row0, s.x + s.row0, (size_t)s.m * 8, cudaMemcpyDefault), "x_out");
+    for (int g = 0; g < G; ++g) {
+      Shard& s = p->shards[g];
+      if (s.m) ck(cudaMemcpy(x_out + s.row0, nxt[g] + s.row0, (size_t)s.m * 8, cudaMemcpyDefault), "x_out");
     }
-    cudaSetDevice(cur);
+    cudaSetDevice(cur_dev);
     if (nu_out) memcpy(nu_out, nu.data(), (size_t)iters * 8);
     if (last_norm) *last_norm = nu[iters - 1];
     for (int k = 0; k < iters; ++k)
-      if (nu[k] == 0.0) fail(SPMV_E_ZERO_NORM, "iterated mode: ||y|| == 0 at iteration %d", k);
+      if (nu[k] == 0.0 || !std::isfinite(nu[k]))
+        fail(SPMV_E_ZERO_NORM, "iterated mode: ||y|| == 0 at iteration %d", k);
   });
 }
 

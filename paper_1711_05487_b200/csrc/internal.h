@@ -221,6 +221,10 @@ int compute_table1(const MatView& A, const int32_t* hot_cols, int sm_count, Tabl
 
 // ---- iterated mode -------------------------------------------------------------
 int launch_norm_partials(const double* y, int64_t m, double* partials, cudaStream_t s);
+// deferred normalisation (norm.cu): nn[0..1] running norm / rescale factor
+int launch_norm_step(const double* partials, int count, double* nn, double* nu_k, double* y, int64_t m,
+                     cudaStream_t s);
+int launch_unit(const double* y, int64_t m, const double* nn, double* x_out, cudaStream_t s);
 int launch_normalize(const double* y, int64_t m, const double* partials, int count, double* x_out,
                      double* nu_dev, cudaStream_t s);
 

@@ -1,6 +1,14 @@
 // norm.cu -- iterated mode epilogue (BJ.configs[5]): nu = ||y||_2 from a fixed
 // chunking of the rows (partials in chunk order, every rank sums the gathered
 // partials in rank order => identical nu everywhere), then x = y / nu.
+//
+// Deferred normalisation (reading 25): the iterate runs on the
+// unnormalised vectors yh_k = A yh_{k-1} (yh_{-1} = x_0), written by the SpMV
+// straight into the other x replica, so no per-iteration x = y / nu pass:
+// x_k = yh_{k-1} / ||yh_{k-1}|| and nu_k = ||A x_k|| = ||yh_k|| / ||yh_{k-1}||.
+// The running norm lives on the device (nn[0]); when it leaves [2^-256,
+// 2^256] the block is rescaled by an exact power of two (nn[1]), so the
+// magnitudes never overflow and no rounding is added.
 #include "common.cuh"
 #include "internal.h"
 
@@ -46,6 +54,55 @@ __global__ void __launch_bounds__(kNT) normalize_kernel(const double* __restrict
   const double nu = nu_s;
   const int64_t stride = (int64_t)gridDim.x * kNT;
   for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = y[i] / nu;
+}
+
+// nn[0] = ||yh_k|| (after an exact power-of-two rescale), nn[1] = that
+// rescale factor (1.0: none), *nu_k = ||yh_k|| / ||yh_{k-1}|| (nn[0] == 0 on
+// entry at k = 0: nu_0 = ||yh_0||). One thread: the partials in order.
+__global__ void norm_step_kernel(const double* __restrict__ partials, int count, double* __restrict__ nn,
+                                 double* __restrict__ nu_k) {
+  double ss = 0.0;
+  for (int q = 0; q < count; ++q) ss += partials[q];
+  const double n = sqrt(ss), prev = nn[0];
+  *nu_k = prev > 0.0 ? n / prev : n;
+  const int e = (n > 0.0 && isfinite(n)) ? ilogb(n) : 0;
+  const bool rs = e > 256 || e < -256;  // squares stay far from overflow (2^1024)
+  nn[0] = rs ? scalbn(n, -e) : n;
+  nn[1] = rs ? scalbn(1.0, -e) : 1.0;
+}
+
+// y *= nn[1] when the step asked for a rescale (exact: a power of two)
+__global__ void __launch_bounds__(kNT) rescale_kernel(double* __restrict__ y, int64_t m, const double* __restrict__ nn) {
+  const double f = nn[1];
+  if (f == 1.0) return;
+  const int64_t stride = (int64_t)gridDim.x * kNT;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) y[i] *= f;
+}
+
+// x_out = yh / nn[0]
+__global__ void __launch_bounds__(kNT) unit_kernel(const double* __restrict__ y, int64_t m,
+                                                   const double* __restrict__ nn, double* __restrict__ x_out) {
+  const double nu = nn[0];
+  const int64_t stride = (int64_t)gridDim.x * kNT;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = y[i] / nu;
+}
+
+static int grid_for(int64_t m) {
+  int64_t g = (m + kNT - 1) / kNT;
+  if (g > 148 * 8) g = 148 * 8;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int launch_norm_step(const double* partials, int count, double* nn, double* nu_k, double* y, int64_t m,
+                     cudaStream_t s) {
+  norm_step_kernel<<<1, 1, 0, s>>>(partials, count, nn, nu_k);
+  rescale_kernel<<<grid_for(m), kNT, 0, s>>>(y, m, nn);
+  return 2;
+}
+
+int launch_unit(const double* y, int64_t m, const double* nn, double* x_out, cudaStream_t s) {
+  unit_kernel<<<grid_for(m), kNT, 0, s>>>(y, m, nn, x_out);
+  return 1;
 }
 
 int launch_norm_partials(const double* y, int64_t m, double* partials, cudaStream_t s) {

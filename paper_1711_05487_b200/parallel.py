@@ -4,13 +4,15 @@ Rank g owns rows [b_g, b_{g+1}) of A (the nnz-balanced lower_bound rule,
 P:708-711, computed by ``spmv_shard_bounds``) and a full replica of x.
 
 * single SpMV: no collective; every rank writes its y block.
-* iterated mode (BJ.configs[5]): per iteration
-    1. y_g = A_g x                      (libspmv kernel, plan stream)
-    2. partials_g = fixed-chunk sums of y_g^2   (libspmv kernel)
-    3. all-gather of the partials (rank order)    -- NCCL
-    4. nu = sqrt(sum of all partials in rank order) on every rank (identical),
-       x[b_g:b_{g+1}] = y_g / nu                  (libspmv kernel)
-    5. the x exchange  -- NCCL
+* iterated mode (BJ.configs[5]), deferred normalisation (DESIGN.md reading
+  25): two x replicas A, B; iteration k reads `cur` (x_0, then yh_{k-1}) and
+    1. yh_k block = A_g cur     (libspmv kernel, written straight into the
+                                 rank's block of `nxt`, plan stream)
+    2. partials_g = fixed-chunk sums of yh_k^2        (libspmv kernel)
+    3. all-gather of the partials (rank order)        -- NCCL
+    4. norm step on every rank (identical): nu_k = ||yh_k|| / ||yh_{k-1}||,
+       exact power-of-two rescale of the block when the magnitude drifts
+    5. the exchange of `nxt` blocks                   -- NCCL
        * all-gather(v): one broadcast per rank into its slice of every
          replica (blocks differ in size), or
        * halo exchange: rank g's rows only read x columns
@@ -18,6 +20,8 @@ P:708-711, computed by ``spmv_shard_bounds``) and a full replica of x.
          g just the part of its block inside that range (point-to-point);
          for banded matrices a few planes instead of the whole vector
          (27-pt 384^3 at G = 8: ~2.4 MB per rank per iteration vs 396 MB).
+  and swaps the replicas; no x = y / nu pass per iteration. At the end
+  x_iters = yh_{iters-1} / ||yh_{iters-1}|| over the replica.
 
 This module only orchestrates (argument marshalling, process-group calls);
 every arithmetic step runs in the native library. The step functions are
@@ -32,9 +36,10 @@ from typing import Callable, Sequence
 @dataclass
 class ShardSteps:
     """Per-rank local steps. Tensors are 1-D float64 on the rank's device."""
-    spmv: Callable[[object, object], None]            # (x_full, y_local)
-    partials: Callable[[object, object], None]        # (y_local, partials_local[P])
-    normalize: Callable[[object, object, int, object, object], None]  # (y, partials_all, count, x_block, nu[1])
+    spmv: Callable[[object, object], None]            # (x_full, y_block): y_block = A_g x_full
+    partials: Callable[[object, object], None]        # (y_block, partials_local[P])
+    norm_step: Callable[[object, int, object, object, object], None]  # (partials_all, count, nn[2], nu[1], y_block)
+    unit: Callable[[object, object, object], None]    # (y, nn[2], x_out): x_out = y / nn[0]
 
 
 def halo_plan(bounds: Sequence[int], needs: Sequence[Sequence[int]], rank: int):
@@ -84,23 +89,29 @@ def exchange_x(dist, bounds, rank, world, x_full, halo=None, group=None):
         w.wait()
 
 
-def iterate(dist, steps: ShardSteps, bounds: Sequence[int], rank: int, world: int, x_full, y_local,
-            partials_local, partials_all, nu_hist, iters: int, group=None, halo=None):
-    """Run `iters` power iterations in place on x_full (the replica).
+def iterate(dist, steps: ShardSteps, bounds: Sequence[int], rank: int, world: int, x_full, x_alt,
+            partials_local, partials_all, nu_hist, nn, iters: int, group=None, halo=None):
+    """Run `iters` power iterations (deferred normalisation) on x_full.
 
-    partials_all: tensor of world * P; nu_hist: tensor of >= iters (nu_k);
+    x_alt: a second replica (len n); partials_all: tensor of world * P;
+    nu_hist: tensor of >= iters (nu_k); nn: 2 doubles of state (zeroed here);
     halo: this rank's halo_plan(...) to exchange only the x ranges the ranks
-    read (else the full all-gather). Returns nothing; x_full holds x_iters on
-    every rank (with a halo plan: at least the range this rank reads).
+    read (else the full all-gather). On return x_full holds x_iters on every
+    rank (with a halo plan: at least the range this rank reads and its own
+    block); x_alt is scratch.
     """
     P = partials_local.numel()
     b0, b1 = int(bounds[rank]), int(bounds[rank + 1])
+    nn.zero_()
+    cur, nxt = x_full, x_alt
     for k in range(iters):
-        steps.spmv(x_full, y_local)
-        steps.partials(y_local, partials_local)
+        steps.spmv(cur, nxt[b0:b1])
+        steps.partials(nxt[b0:b1], partials_local)
         dist.all_gather_into_tensor(partials_all, partials_local, group=group)
-        steps.normalize(y_local, partials_all, world * P, x_full[b0:b1], nu_hist[k:k + 1])
-        exchange_x(dist, bounds, rank, world, x_full, halo, group)
+        steps.norm_step(partials_all, world * P, nn, nu_hist[k:k + 1], nxt[b0:b1])
+        exchange_x(dist, bounds, rank, world, nxt, halo, group)
+        cur, nxt = nxt, cur
+    steps.unit(cur, nn, x_full)
 
 
 def exchange_only(dist, bounds: Sequence[int], rank: int, world: int, x_full, partials_local, partials_all,
@@ -124,5 +135,6 @@ def native_steps(plan) -> ShardSteps:
     return ShardSteps(
         spmv=lambda x, y: plan.execute_async(x, y),
         partials=lambda y, p: plan.norm_partials(y, p),
-        normalize=lambda y, pa, cnt, xb, nu: plan.normalize(y, pa, cnt, xb, nu),
+        norm_step=lambda pa, cnt, nn, nu, y: plan.norm_step(pa, cnt, nn, nu, y),
+        unit=lambda y, nn, x: plan.unit(y, nn, x),
     )

@@ -36,13 +36,14 @@ def test_native_distributed_iteration_world1():
         b = spmv.shard_bounds(m.rowptr, 1)
         P = spmv.norm_partial_count()
         x = torch.from_numpy(m.x.copy()).cuda()
-        y = torch.empty(m.n, dtype=torch.float64, device="cuda")
+        x2 = torch.empty(m.n, dtype=torch.float64, device="cuda")
+        nn = torch.zeros(2, dtype=torch.float64, device="cuda")
         pl = torch.empty(P, dtype=torch.float64, device="cuda")
         pa = torch.empty(P, dtype=torch.float64, device="cuda")
         nu = torch.empty(K, dtype=torch.float64, device="cuda")
         st = torch.cuda.ExternalStream(plan.stream())
         with torch.cuda.stream(st):
-            parallel.iterate(dist, parallel.native_steps(plan), b, 0, 1, x, y, pl, pa, nu, K)
+            parallel.iterate(dist, parallel.native_steps(plan), b, 0, 1, x, x2, pl, pa, nu, nn, K)
         torch.cuda.synchronize()
         rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, K)
         xg, nug = x.cpu().numpy(), nu.cpu().numpy()

@@ -287,6 +287,24 @@ def test_iterated_mode_vs_oracle():
         assert np.all(np.diff(nug[1:]) >= -1e-13 * nug[1:-1])  # monotone for symmetric A
 
 
+@pytest.mark.parametrize("scale", [1e40, 1e-40])
+def test_iterated_mode_rescale(scale):
+    # deferred normalisation (reading 25): the unnormalised iterate
+    # grows (or shrinks) by ~1e40 per step, so the exact power-of-two rescale
+    # must fire every few iterations; results match the per-step oracle
+    m = sg.config(5, small=True)
+    vals = m.vals * scale
+    K = 40
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, vals, m.x, K)
+    assert rc == 0
+    for G in (1, 2):
+        p = spmv.Plan(m.rowptr, m.colind, vals, ngpus=G, emulate_devices=1)
+        xg, nug = p.iterate(m.x, K)
+        assert np.all(np.isfinite(xg)) and np.all(np.isfinite(nug))
+        assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
+        assert np.all(np.abs(nug - nur) <= 1e-12 * nur)
+
+
 def test_iterated_zero_norm():
     rp = np.zeros(11, np.int64)
     p = spmv.Plan(rp, np.zeros(0, np.int32), np.zeros(0))

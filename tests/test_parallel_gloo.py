@@ -2,6 +2,7 @@
 paper_1711_05487_b200/parallel.py: shard bounds, the rank-ordered norm
 combine and the all-gather(v) of x blocks. The local steps are CPU stubs built
 on the oracle (tests may use it; the product never does)."""
+import math
 import os
 import socket
 
@@ -37,16 +38,25 @@ def _worker(rank, world, port, K, out_q, use_halo=False, cfg=5):
         lrp = rp[b0:b1 + 1] - rp[b0]
         lci, lva = m.colind[rp[b0]:rp[b1]], m.vals[rp[b0]:rp[b1]]
         P = 512
+        def norm_step(pa, cnt, nn, nu, y):  # the spmv_norm_step contract (include/spmv.h)
+            n = math.sqrt(math.fsum(pa.numpy()[:cnt]))
+            nu.fill_(n / float(nn[0]) if float(nn[0]) > 0 else n)
+            e = math.frexp(n)[1] - 1 if n > 0 else 0
+            f = math.ldexp(1.0, -e) if abs(e) > 256 else 1.0
+            nn[0], nn[1] = n * f, f
+            y.mul_(f)
+
         steps = parallel.ShardSteps(
             spmv=lambda x, y: y.copy_(torch.from_numpy(oracle.spmv(lrp, lci, lva, x.numpy()))),
             partials=lambda y, p: p.copy_(torch.tensor(
                 [float(np.sum(y.numpy()[q * y.numel() // P:(q + 1) * y.numel() // P] ** 2)) for q in range(P)],
                 dtype=torch.float64)),
-            normalize=lambda y, pa, cnt, xb, nu: (nu.fill_(float(np.sqrt(np.sum(pa.numpy()[:cnt])))),
-                                                  xb.copy_(y / nu[0])),
+            norm_step=norm_step,
+            unit=lambda y, nn, x: x.copy_(y / nn[0]),
         )
         x = torch.from_numpy(m.x.copy())
-        y = torch.empty(b1 - b0, dtype=torch.float64)
+        x2 = torch.full_like(x, float("nan"))
+        nn = torch.zeros(2, dtype=torch.float64)
         pl = torch.empty(P, dtype=torch.float64)
         pa = torch.empty(world * P, dtype=torch.float64)
         nu = torch.empty(K, dtype=torch.float64)
@@ -56,7 +66,7 @@ def _worker(rank, world, port, K, out_q, use_halo=False, cfg=5):
             needs = [torch.empty(2, dtype=torch.int64) for _ in range(world)]
             dist.all_gather(needs, need)
             halo = parallel.halo_plan(b, [n.tolist() for n in needs], rank)
-        parallel.iterate(dist, steps, b, rank, world, x, y, pl, pa, nu, K, halo=halo)
+        parallel.iterate(dist, steps, b, rank, world, x, x2, pl, pa, nu, nn, K, halo=halo)
         if use_halo:  # only the range this rank reads is guaranteed: compare that, plus its own block
             lo, hi = int(lci.min()), int(lci.max()) + 1
             xs = np.full(x.numel(), np.nan)
