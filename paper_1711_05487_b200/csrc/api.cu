@@ -138,6 +138,16 @@ struct Shard {
   double* nu = nullptr;
   int nu_cap = 0;
   cudaEvent_t ev_part = nullptr, ev_x = nullptr;
+  // pipelined host execute (STREAM plans, host x and y): tile blocks with the
+  // x chunk each needs, the first row each block completes, copy streams
+  struct HostPipe {
+    bool ready = false, usable = false;
+    std::vector<int64_t> kb;     // block b = tiles [kb[b], kb[b+1])
+    std::vector<int64_t> srow;   // block b completes rows [srow[b], srow[b+1])
+    std::vector<int64_t> xhi;    // x[0, xhi[b]) is needed by blocks <= b
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev_h, ev_c;
+  } hp;
   std::vector<void*> allocs;
   int64_t bytes = 0;
 
@@ -158,6 +168,13 @@ struct Shard {
     allocs.clear();
     if (ev_part) cudaEventDestroy(ev_part);
     if (ev_x) cudaEventDestroy(ev_x);
+    for (cudaEvent_t e : hp.ev_h) cudaEventDestroy(e);
+    for (cudaEvent_t e : hp.ev_c) cudaEventDestroy(e);
+    hp.ev_h.clear();
+    hp.ev_c.clear();
+    if (hp.h2d) cudaStreamDestroy(hp.h2d);
+    if (hp.d2h) cudaStreamDestroy(hp.d2h);
+    hp.h2d = hp.d2h = nullptr;
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
@@ -1093,6 +1110,122 @@ spmv_status guard(F&& f) {
   }
 }
 
+// ---- pipelined host execute ---------------------------------------------------
+// Host x in, host y out through a STREAM plan: the tiles are cut into NB
+// blocks; block b's kernel waits only for the x chunk its columns need
+// (uploaded in column order on a copy stream), and its finished rows go back
+// on a second copy stream while later blocks compute and upload, so the
+// PCIe transfers in both directions overlap each other and the SpMV
+// (BJ e2e: C5 moves 453 MB each way per step).
+int64_t read_rp(const Shard& s, int64_t r) {
+  int64_t v = 0;
+  if (s.rp_bytes == 8) {
+    ck(cudaMemcpy(&v, (const int64_t*)s.rowptr + r, 8, cudaMemcpyDeviceToHost), "rowptr");
+  } else {
+    int32_t w = 0;
+    ck(cudaMemcpy(&w, (const int32_t*)s.rowptr + r, 4, cudaMemcpyDeviceToHost), "rowptr");
+    v = w;
+  }
+  return v;
+}
+
+void host_pipe_prepare(spmv_plan p, Shard& s) {
+  auto& h = s.hp;
+  if (h.ready) return;
+  h.ready = true;
+  const StreamPlan& sp = s.sp[0];
+  const int64_t xbytes = p->n_cols * 8;
+  // (segmented-mode tiles assign a row where it ENDS and add the carries after:
+  // a later range would overwrite an earlier range's fix-up, so not pipelined)
+  int64_t min_bytes = 16ll << 20;
+  if (const char* e = getenv("SPMV_HOST_PIPE_MIN_BYTES")) min_bytes = atoll(e);  // tests: pipeline small plans
+  if (p->sel.variant != SPMV_VARIANT_STREAM || sp.rowmap || sp.seg || sp.T < 8 || xbytes < min_bytes || s.m == 0)
+    return;
+  // blocks: one per ~4 MB of x, 2..16 (B200 sweeps: C2 16.8 MB -> 4 blocks
+  // 0.655 ms vs 0.677 (2) / 0.773 (8); C5 453 MB -> 16 blocks 11.07 ms vs
+  // 11.37 (8) / 11.25 (24))
+  int64_t nbw = std::min<int64_t>(16, std::max<int64_t>(2, xbytes / (4ll << 20)));
+  if (const char* e = getenv("SPMV_HOST_PIPE_BLOCKS")) nbw = atoll(e);  // tests
+  const int nb = (int)std::max<int64_t>(2, std::min<int64_t>(nbw, sp.T / 4));
+  h.kb.resize(nb + 1);
+  h.srow.resize(nb + 1);
+  h.xhi.resize(nb);
+  for (int b = 0; b <= nb; ++b) h.kb[b] = sp.T * b / nb;
+  std::vector<int64_t> t0(nb + 1);
+  int32_t* cm = nullptr;
+  ck(cudaMalloc(&cm, 4 * (size_t)nb), "cudaMalloc");
+  try {
+    ck(cudaMemsetAsync(cm, 0xff, 4 * (size_t)nb, s.stream), "memset");
+    for (int b = 0; b <= nb; ++b) {
+      const int64_t k = h.kb[b];
+      if (sp.aligned) {
+        ck(cudaMemcpy(&t0[b], sp.tile_nz + k, 8, cudaMemcpyDeviceToHost), "tile_nz");
+      } else {
+        t0[b] = std::min<int64_t>(k * sp.stride, s.nnz);
+      }
+      if (b == 0) { h.srow[b] = 0; continue; }
+      if (b == nb) { h.srow[b] = s.m; continue; }
+      int32_t R = 0;
+      ck(cudaMemcpy(&R, sp.tile_row + k, 4, cudaMemcpyDeviceToHost), "tile_row");
+      const bool incoming = !sp.aligned && R > 0 && read_rp(s, R) > t0[b];
+      h.srow[b] = R - (incoming ? 1 : 0);
+    }
+    for (int b = 0; b < nb; ++b) launch_range_colmax(s.col, t0[b], t0[b + 1], cm + b, s.stream);
+    std::vector<int32_t> mx(nb);
+    ck(cudaMemcpyAsync(mx.data(), cm, 4 * (size_t)nb, cudaMemcpyDeviceToHost, s.stream), "colmax");
+    ck(cudaStreamSynchronize(s.stream), "colmax");
+    int64_t hi = 0;
+    for (int b = 0; b < nb; ++b) {
+      hi = std::max<int64_t>(hi, (int64_t)mx[b] + 1);
+      h.xhi[b] = b == nb - 1 ? p->n_cols : std::min<int64_t>(hi, p->n_cols);
+    }
+    cudaFree(cm);
+  } catch (...) {
+    cudaFree(cm);
+    throw;
+  }
+  ck(cudaStreamCreateWithFlags(&h.h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaStreamCreateWithFlags(&h.d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+  h.ev_h.resize(nb);
+  h.ev_c.resize(nb);
+  for (int b = 0; b < nb; ++b) {
+    ck(cudaEventCreateWithFlags(&h.ev_h[b], cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&h.ev_c[b], cudaEventDisableTiming), "cudaEventCreate");
+  }
+  h.usable = true;
+}
+
+// enqueue the pipelined SpMV of shard s (x, y host); returns launches
+int host_pipe_run(spmv_plan p, Shard& s, const double* x, double* y) {
+  auto& h = s.hp;
+  const int nb = (int)h.xhi.size();
+  int n = 0;
+  ck(cudaEventRecord(h.ev_c[0], s.stream), "event");  // copies start after earlier work on the plan stream
+  ck(cudaStreamWaitEvent(h.h2d, h.ev_c[0], 0), "wait");
+  ck(cudaStreamWaitEvent(h.d2h, h.ev_c[0], 0), "wait");
+  int64_t lo = 0;
+  for (int b = 0; b < nb; ++b) {
+    if (h.xhi[b] > lo)
+      ck(cudaMemcpyAsync(s.x + lo, x + lo, (size_t)(h.xhi[b] - lo) * 8, cudaMemcpyHostToDevice, h.h2d), "copy x");
+    lo = std::max(lo, h.xhi[b]);
+    ck(cudaEventRecord(h.ev_h[b], h.h2d), "event");
+  }
+  for (int b = 0; b < nb; ++b) {
+    ck(cudaStreamWaitEvent(s.stream, h.ev_h[b], 0), "wait");
+    n += launch_stream_range(s.sp[0], s.x, s.y, h.kb[b], h.kb[b + 1], s.stream);
+    ck(cudaEventRecord(h.ev_c[b], s.stream), "event");
+    ck(cudaStreamWaitEvent(h.d2h, h.ev_c[b], 0), "wait");
+    const int64_t r0 = h.srow[b], r1 = h.srow[b + 1];
+    if (r1 > r0)
+      ck(cudaMemcpyAsync(y + s.row0 + r0, s.y + r0, (size_t)(r1 - r0) * 8, cudaMemcpyDeviceToHost, h.d2h), "copy y");
+  }
+  // the plan stream resumes after the last copy
+  ck(cudaEventRecord(h.ev_h[0], h.d2h), "event");
+  ck(cudaStreamWaitEvent(s.stream, h.ev_h[0], 0), "wait");
+  (void)p;
+  return n;
+}
+
 // run the plan on x (device pointer valid on every shard's device or the
 // shards' replicas) into y (per-shard outputs)
 void execute_impl(spmv_plan p, const double* x, double* y, bool sync) {
@@ -1101,6 +1234,24 @@ void execute_impl(spmv_plan p, const double* x, double* y, bool sync) {
   const bool xd = is_device_ptr(x, &xdev), yd = is_device_ptr(y, &ydev);
   int cur = 0;
   cudaGetDevice(&cur);
+  if (!xd && !yd && !getenv("SPMV_NO_HOST_PIPE")) {
+    bool all = true;
+    for (auto& s : p->shards) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      host_pipe_prepare(p, s);
+      all = all && s.hp.usable;
+    }
+    if (all) {
+      for (auto& s : p->shards) {
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        count_launches(host_pipe_run(p, s, x, y), "spmv");
+      }
+      if (sync)
+        for (auto& s : p->shards) ck(cudaStreamSynchronize(s.stream), "spmv sync");
+      cudaSetDevice(cur);
+      return;
+    }
+  }
   for (auto& s : p->shards) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const double* xs = x;

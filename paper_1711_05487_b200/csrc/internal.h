@@ -64,7 +64,13 @@ struct StreamPlan {
   int64_t* tile_nz = nullptr;  // aligned: tile_nz[k] = rowptr[tile_row[k]], k = 0..T
   int64_t max_run = 1;         // longest run of equal carry rows (fix-up choice)
   bool l2pf = false;           // producer L2-prefetches each stage's next tile (measured slower: C2 53.7 vs 47.0 us)
+  int64_t k0 = 0;              // first tile of the launch (tile-range launches: pipelined host execute)
 };
+// tiles [k0, k1) of a STREAM plan (+ the fix-up of their carries); the rows
+// cut at k0 / k1 are completed by the neighbouring ranges' fix-ups
+int launch_stream_range(const StreamPlan& sp, const double* x, double* y, int64_t k0, int64_t k1, cudaStream_t s);
+// out[0] = max colind over nonzeros [a, b) (atomicMax; out zeroed by the caller)
+void launch_range_colmax(const int32_t* col, int64_t a, int64_t b, int32_t* out, cudaStream_t s);
 void launch_tile_nz(const MatView& A, const int32_t* tile_row, int64_t T, int64_t* tile_nz, cudaStream_t s);
 
 // One nnz_split pass (nzsplit.cu) over the CSR view V restricted to its

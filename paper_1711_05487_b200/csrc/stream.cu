@@ -115,7 +115,8 @@ struct StreamP {
   const int64_t* tile_nz;  // row-aligned tiles: first nonzero of tile k (= rowptr[tile_row[k]])
   int32_t* carry_row;
   double* carry_val;
-  int64_t nnz, C, T;
+  int64_t nnz, C, T;  // T: end of the tile range
+  int64_t k0;         // first tile of the range
   int stages, rows_cap;
   int aligned;  // 1: row-aligned tiles (no row crosses a tile, no carries)
   int l2pf;     // 1: the producer prefetches the stage's next tile into L2
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
           }
         }
       };
-      fetch(blockIdx.x);
+      fetch(p.k0 + blockIdx.x);
       // L2 prefetch of the tile that will next reuse this stage (S tiles
       // ahead): its DRAM latency then overlaps the consumer's current tile
       // and the later TMA copy hits L2 (metadata fetched one tile earlier)
@@ -311,9 +312,9 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
           }
         }
       };
-      pfetch(blockIdx.x + (int64_t)S * gridDim.x);
+      pfetch(p.k0 + blockIdx.x + (int64_t)S * gridDim.x);
       int i = 0;
-      for (int64_t k = blockIdx.x; k < p.T; k += gridDim.x, ++i) {
+      for (int64_t k = p.k0 + blockIdx.x; k < p.T; k += gridDim.x, ++i) {
         const int s = i % S;
         const int64_t R0 = nR0, R1 = nR1, aT0 = nT0, aT1 = nT1;
         fetch(k + gridDim.x);
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
   const int lane = lane32 % VS;
   const int gi = lane32 / VS;
   for (int i = w;; i += kConsumerWarps) {
-    const int64_t k = blockIdx.x + (int64_t)i * gridDim.x;
+    const int64_t k = p.k0 + blockIdx.x + (int64_t)i * gridDim.x;
     if (k >= p.T) break;
     const int s = i % S;
     mbar_wait(&full[s], (uint32_t)((i / S) & 1));
@@ -551,6 +552,7 @@ static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y)
   p.nnz = sp.V.nnz;
   p.C = sp.C;
   p.T = sp.T;
+  p.k0 = sp.k0;
   p.stages = sp.stages;
   p.rows_cap = sp.rows_cap;
   p.aligned = sp.aligned ? 1 : 0;
@@ -635,6 +637,42 @@ int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int sta
 }
 
 int launch_stream(const ExecArgs& a, cudaStream_t s) { return launch_stream_plan(a.sp[0], a.x, a.y, a.stage, s); }
+
+int launch_stream_range(const StreamPlan& sp_in, const double* x, double* y, int64_t k0, int64_t k1, cudaStream_t s) {
+  if (k1 <= k0) return 0;
+  StreamPlan sp = sp_in;
+  sp.k0 = k0;
+  sp.T = k1;
+  if (sp.grid > k1 - k0) sp.grid = (int)(k1 - k0);
+  stream_dispatch<false>(sp, 0, x, y, s);
+  int n = 1;
+  // a carry run crossing k0 is split between two ranges' fix-ups: both add
+  // to y in stream order (additive), so the row is complete after the later one
+  if (sp.need_fixup) n += launch_fixup(sp.carry_row + k0, sp.carry_val + k0, k1 - k0, y, 0, sp.max_run, s);
+  return n;
+}
+
+__global__ void __launch_bounds__(kNT) range_colmax_kernel(const int32_t* __restrict__ col, int64_t a, int64_t b,
+                                                           int32_t* out) {
+  int32_t mx = -1;
+  for (int64_t j = a + (int64_t)blockIdx.x * kNT + threadIdx.x; j < b; j += (int64_t)gridDim.x * kNT)
+    mx = max(mx, __ldg(col + j));
+  mx = warp_max(mx);
+  __shared__ int32_t ws[kNT / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kNT / 32; ++w) mx = max(mx, ws[w]);
+    if (mx >= 0) atomicMax(out, mx);
+  }
+}
+
+void launch_range_colmax(const int32_t* col, int64_t a, int64_t b, int32_t* out, cudaStream_t s) {
+  if (b <= a) return;
+  int64_t g = (b - a + kNT * 8 - 1) / (kNT * 8);
+  if (g > 148 * 8) g = 148 * 8;
+  range_colmax_kernel<<<(unsigned)g, kNT, 0, s>>>(col, a, b, out);
+}
 
 // Export: re-decode the delta colind on the device with the STREAM kernel's
 // own per-row decoder (bit-exact round trip).

@@ -244,6 +244,33 @@ def test_device_and_host_buffers_agree():
     assert np.array_equal(yd.cpu().numpy(), y_host)
 
 
+@pytest.mark.parametrize("extra", [{}, {"no_aligned": 1}, {"d16": 1}, {"force_vs": 4}])
+@pytest.mark.parametrize("name,lens", [("uniform", [7] * 40000), ("mixed", ([3, 0, 9, 27, 1, 64] * 8000)),
+                                       ("long_rows", [5] * 20000 + [9000] * 3 + [5] * 20000)])
+def test_pipelined_host_execute(monkeypatch, name, lens, extra):
+    # host x / host y through a STREAM plan: tile blocks overlapped with the
+    # x upload and the y download (api.cu host_pipe_*); rows cut at block
+    # edges are completed by the next block's fix-up
+    monkeypatch.setenv("SPMV_HOST_PIPE_MIN_BYTES", "1")
+    monkeypatch.setenv("SPMV_HOST_PIPE_BLOCKS", "7")
+    g = np.random.default_rng(11)
+    lens = np.asarray(lens, np.int64)
+    m = sg.from_lengths(lens, lens.size, g, sg.MODE_U11, sg.MODE_U11)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="stream", tile_nnz=512, **extra)
+    yh = p.execute(m.x, np.full(m.n, np.nan))  # host buffers: pipelined
+    assert_bound(yh, m)
+    assert np.all(yh[lens == 0] == 0.0)
+    xd = torch.from_numpy(m.x).cuda()
+    yd = torch.full((m.n,), float("nan"), dtype=torch.float64, device="cuda")
+    p.execute(xd, yd)  # device buffers: one launch over all tiles
+    yd = yd.cpu().numpy()
+    if p.info()["tiles_row_aligned"]:
+        assert np.array_equal(yh, yd)  # no carries: identical arithmetic
+    else:
+        assert_bound(yd, m)
+    p.destroy()
+
+
 def test_deterministic_repeat():
     m = sg.config(3, small=True)
     for v in ALL:
