@@ -45,17 +45,22 @@ struct NzP {
 // rowmap lookups of the rows it writes.
 // y = 0 for the empty rows between compacted rows q and q + 1 (SPLIT: only
 // those empty in orp too)
-// The n_end gaps after rows q0 .. q0+n_end-1: a short gap (<= 8 rows) is
-// zeroed by its own lane; long ones by the whole warp -- their lengths
-// scanned across the lanes, the rows dealt out 32 per step (a lane finds its
-// gap by a 5-step search over the scanned lengths). A lane per long gap
-// serialises long empty runs (non-empty rows 0.04 % of the rows: 10 ms
-// instead of ~60 us on B200); all gaps cooperative costs C3 ~3 %.
+// The n_end gaps after rows q0 .. q0+n_end-1 (MASK path): a short gap
+// (<= kGapLane rows) is zeroed by its own lane; long ones by the whole warp --
+// their lengths scanned across the lanes, the rows dealt out 32 per step (a
+// lane finds its gap by a 5-step search over the scanned lengths). A lane
+// per long gap serialises long empty runs (non-empty rows 0.04 % of the
+// rows: 10 ms instead of ~60 us on B200 before runs > kNzGapMax made the
+// plan clear y first).
+template <typename RP>
+__device__ __forceinline__ void nz_zero_row(const NzP<RP>& p, int32_t r) {
+  if (!p.orp || ld_ro(p.orp + r + 1) == ld_ro(p.orp + r)) p.y[r] = 0.0;
+}
+constexpr int32_t kGapLane = 64;  // gaps up to this many rows are zeroed by their own lane
+
 template <typename RP>
 __device__ __forceinline__ void nz_zero_gaps_warp(const NzP<RP>& p, int64_t q0, int n_end, int lane) {
-  auto zero = [&](int32_t r) {
-    if (!p.orp || ld_ro(p.orp + r + 1) == ld_ro(p.orp + r)) p.y[r] = 0.0;
-  };
+  auto zero = [&](int32_t r) { nz_zero_row(p, r); };
   for (int jb = 0; jb < n_end; jb += 32) {
     const int j = jb + lane;
     int32_t ra = 0, g = 0;
@@ -63,7 +68,7 @@ __device__ __forceinline__ void nz_zero_gaps_warp(const NzP<RP>& p, int64_t q0, 
       ra = ld_ro(p.rowmap + q0 + j);
       g = ld_ro(p.rowmap + q0 + j + 1) - ra - 1;
     }
-    const bool lng = g > 8;
+    const bool lng = g > kGapLane;
     if (!lng)
       for (int32_t r = ra + 1; r <= ra + g; ++r) zero(r);
     if (!__any_sync(0xffffffffu, lng)) continue;
@@ -172,12 +177,19 @@ __device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int
     const int n_end = (int)(q1 - q0);
     if (lane < 8) em[lane] = 0u;
     __syncwarp();
+    // rows ending in the tile; the empty rows after each are zeroed by its own
+    // lane (gaps are at most kNzGapMax rows: longer runs make the plan clear y
+    // first). B200, C3: 264 us vs 269 us with the warp-cooperative zeroing of
+    // the MASK path below, 275 us with a per-lane/warp hybrid in this loop.
     for (int j = lane; j < n_end; j += 32) {
       const int64_t q = q0 + j;
       const int e = (int)((int64_t)ld_ro(p.rpc + q + 1) - 1 - t0);
       atomicOr(&em[e >> 5], 1u << (e & 31));
+      if (p.zero_gaps) {
+        const int32_t ra = ld_ro(p.rowmap + q), rb = ld_ro(p.rowmap + q + 1);
+        for (int32_t r = ra + 1; r < rb; ++r) nz_zero_row(p, r);
+      }
     }
-    if (p.zero_gaps) nz_zero_gaps_warp(p, q0, n_end, lane);
     __syncwarp();
     const uint4 m0 = *reinterpret_cast<const uint4*>(em);
     const uint4 m1 = *reinterpret_cast<const uint4*>(em + 4);
