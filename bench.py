@@ -322,8 +322,16 @@ def run_native(a):
         f()
         k = max(3, min(a.steps, 10))
         ms_e2e = max_over_ranks(timed(f, k)) / k
+        # each rank uploads the x range its rows read (the whole x at N = 1,
+        # a halo'd 1/N of it for a banded matrix) and downloads its y block
+        feat = info["feat"]
+        h2d = 8 * max(0, int(feat["col_max"]) - int(feat["col_min"]) + 1)
+        if world > 1:
+            t = torch.tensor([h2d], dtype=torch.int64, device="cuda")
+            dist.all_reduce(t)
+            h2d = int(t.item())
         e2e = {"value": 2.0 * blk["nnz"] / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": 8 * blk["N"] * world, "d2h_bytes_per_step": 8 * blk["N"],
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * blk["N"],
                "ms_per_step": ms_e2e}
 
     # iterated mode x <- Ax/||Ax|| (BJ.configs[5]), deferred normalisation:

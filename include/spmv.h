@@ -245,7 +245,10 @@ typedef struct spmv_table1 {
 spmv_status spmv_plan_table1(spmv_plan p, spmv_table1* out);
 
 /* Plan-resident buffers and stream of shard g (the timed path: no copies
- * when spmv_execute* receives these pointers). */
+ * when spmv_execute* receives these pointers). A host x given to
+ * spmv_execute is copied into the replica only on the column range shard g
+ * reads ([col_min, col_max] of its nonzeros: the halo of a banded row block),
+ * the rest of the replica is left as it was. */
 double* spmv_plan_x_device(spmv_plan p, int g);
 double* spmv_plan_y_device(spmv_plan p, int g);
 void* spmv_plan_stream(spmv_plan p, int g);  /* a cudaStream_t */

@@ -144,7 +144,8 @@ struct Shard {
     bool ready = false, usable = false;
     std::vector<int64_t> kb;     // block b = tiles [kb[b], kb[b+1])
     std::vector<int64_t> srow;   // block b completes rows [srow[b], srow[b+1])
-    std::vector<int64_t> xhi;    // x[0, xhi[b]) is needed by blocks <= b
+    std::vector<int64_t> xhi;    // x[xlo, xhi[b]) is needed by blocks <= b
+    int64_t xlo = 0;             // first column the shard reads
     cudaStream_t h2d = nullptr, d2h = nullptr;
     std::vector<cudaEvent_t> ev_h, ev_c;
   } hp;
@@ -1174,10 +1175,14 @@ void host_pipe_prepare(spmv_plan p, Shard& s) {
     std::vector<int32_t> mx(nb);
     ck(cudaMemcpyAsync(mx.data(), cm, 4 * (size_t)nb, cudaMemcpyDeviceToHost, s.stream), "colmax");
     ck(cudaStreamSynchronize(s.stream), "colmax");
-    int64_t hi = 0;
+    // x is uploaded from the shard's first read column (a row block of a
+    // banded matrix reads only its halo range: 1/G of x at G shards)
+    const int64_t c_lo = std::max<long long>(0, s.hs.col_min), c_hi = s.hs.col_max + 1;
+    h.xlo = std::min<int64_t>(c_lo, c_hi);
+    int64_t hi = h.xlo;
     for (int b = 0; b < nb; ++b) {
       hi = std::max<int64_t>(hi, (int64_t)mx[b] + 1);
-      h.xhi[b] = b == nb - 1 ? p->n_cols : std::min<int64_t>(hi, p->n_cols);
+      h.xhi[b] = b == nb - 1 ? c_hi : std::min<int64_t>(hi, c_hi);
     }
     cudaFree(cm);
   } catch (...) {
@@ -1203,7 +1208,7 @@ int host_pipe_run(spmv_plan p, Shard& s, const double* x, double* y) {
   ck(cudaEventRecord(h.ev_c[0], s.stream), "event");  // copies start after earlier work on the plan stream
   ck(cudaStreamWaitEvent(h.h2d, h.ev_c[0], 0), "wait");
   ck(cudaStreamWaitEvent(h.d2h, h.ev_c[0], 0), "wait");
-  int64_t lo = 0;
+  int64_t lo = h.xlo;
   for (int b = 0; b < nb; ++b) {
     if (h.xhi[b] > lo)
       ck(cudaMemcpyAsync(s.x + lo, x + lo, (size_t)(h.xhi[b] - lo) * 8, cudaMemcpyHostToDevice, h.h2d), "copy x");
@@ -1256,8 +1261,10 @@ void execute_impl(spmv_plan p, const double* x, double* y, bool sync) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const double* xs = x;
     if (!(xd && xdev == s.dev)) {
-      if (x != s.x)
-        ck(cudaMemcpyAsync(s.x, x, (size_t)p->n_cols * 8, cudaMemcpyDefault, s.stream), "copy x");
+      // only the column range the shard reads (include/spmv.h, x_device)
+      const int64_t lo = std::max<long long>(0, s.hs.col_min), hi = s.hs.col_max + 1;
+      if (x != s.x && hi > lo)
+        ck(cudaMemcpyAsync(s.x + lo, x + lo, (size_t)(hi - lo) * 8, cudaMemcpyDefault, s.stream), "copy x");
       xs = s.x;
     }
     double* ys = y + s.row0;
