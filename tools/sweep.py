@@ -75,7 +75,7 @@ def main():
     for vs in vss:
         grid.append(dict(force_variant="vector", force_vs=vs))
     svs = (1, 2, 4) if not a.quick else (1, 4)
-    tiles = (256, 384, 512, 768, 1024) if not a.quick else (384, 512)
+    tiles = (256, 384, 512, 640, 768, 1024) if not a.quick else (512, 640, 768)
     stages = (4, 8) if not a.quick else (4,)
     d16s = (0, 1) if a.config in (1, 2) else (0,)
     for vs, t, sg_, d in itertools.product(svs, tiles, stages, d16s):
@@ -83,6 +83,9 @@ def main():
     for t in tiles:
         grid.append(dict(force_variant="stream", seg=1, tile_nnz=t))
     grid.append(dict(force_variant="merge"))
+    grid.append(dict(force_variant="nnzsplit"))
+    grid.append(dict(force_variant="nnzsplit", hot_x=0))
+    grid.append(dict(force_variant="nnzsplit", hot_x=16384))
     for sg_ in (0, 1):
         for t in tiles:
             grid.append(dict(force_variant="split", seg=sg_, tile_nnz=t))

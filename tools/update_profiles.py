@@ -65,4 +65,12 @@ if os.path.exists(lc):
         for k, (n, t) in agg.items():
             f.write(f"{k:42s} {n:6d} {t / n:10.1f} {t:11.1f}\n")
         f.write("# SpMV step share: " + "  ".join(f"{k} {100 * v[1] / tot:.1f}%" for k, v in step.items()) + "\n")
+import shutil
+for c in (2, 3, 4, 5):
+    sp_ = os.path.join(src, f"sweep_c{c}.json")
+    if os.path.exists(sp_):
+        shutil.copy(sp_, os.path.join(dst, f"{tag}_sweep_c{c}.json"))
+t5 = os.path.join(src, "table5.json")
+if os.path.exists(t5):
+    shutil.copy(t5, os.path.join(dst, f"{tag}_table5.json"))
 print("profiles updated")
