@@ -132,7 +132,7 @@ typedef struct spmv_plan_info {
   int64_t shard_bounds[9];    /* b_0..b_G for G <= 8 (rows) */
   int64_t tile_stride;        /* STREAM tile stride in nonzeros (= tile_nnz, or tile_nnz - longest row) */
   int32_t tiles_row_aligned;  /* 1: tile k = rows starting in [k*stride, (k+1)*stride); no carries */
-  int32_t pad2_;
+  int32_t rows_per_tile;      /* > 0: row-count tiles, tile k = rows [k*rows_per_tile, (k+1)*rows_per_tile) */
   int64_t n_nz_rows;          /* nnz_split: non-empty rows of the pass (mc) */
   int64_t n_nz_tiles;         /* nnz_split: warp tiles of 256 nonzeros */
   int64_t n_hot;              /* nnz_split: hot columns served from shared memory (0 = off) */

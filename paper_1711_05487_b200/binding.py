@@ -87,7 +87,7 @@ class PlanInfo(ctypes.Structure):
                 ("n_long_chunks", ctypes.c_int64), ("upload_ms", ctypes.c_double), ("inspect_ms", ctypes.c_double),
                 ("select_ms", ctypes.c_double), ("encode_ms", ctypes.c_double), ("device_bytes", ctypes.c_int64),
                 ("shard_bounds", ctypes.c_int64 * 9), ("tile_stride", ctypes.c_int64),
-                ("tiles_row_aligned", ctypes.c_int32), ("pad2_", ctypes.c_int32), ("n_nz_rows", ctypes.c_int64),
+                ("tiles_row_aligned", ctypes.c_int32), ("rows_per_tile", ctypes.c_int32), ("n_nz_rows", ctypes.c_int64),
                 ("n_nz_tiles", ctypes.c_int64), ("n_hot", ctypes.c_int64), ("hot_cover", ctypes.c_double)] + \
                [(k, ctypes.c_double) for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak", "bmax")] + \
                [("profile_vs", ctypes.c_int32), ("profile_ctas", ctypes.c_int32), ("profile_ms", ctypes.c_double),
@@ -275,7 +275,7 @@ class Plan:
     def info(self) -> dict:
         i = PlanInfo()
         _check(lib.spmv_plan_query(self._h, ctypes.byref(i)))
-        d = {k: getattr(i, k) for k, _ in PlanInfo._fields_ if k not in ("sel", "feat", "pad_", "pad2_", "shard_bounds")}
+        d = {k: getattr(i, k) for k, _ in PlanInfo._fields_ if k not in ("sel", "feat", "pad_", "shard_bounds")}
         d["sel"] = {k: getattr(i.sel, k) for k, _ in Selection._fields_ if k != "pad_"}
         d["variant"] = VARIANT_NAMES[i.sel.variant]
         d["classes"] = [k for k, v in CLASSES.items() if i.sel.classes & v]

@@ -65,7 +65,9 @@ struct StreamPlan {
   int64_t max_run = 1;         // longest run of equal carry rows (fix-up choice)
   bool l2pf = false;           // producer L2-prefetches each stage's next tile (measured slower: C2 53.7 vs 47.0 us)
   int64_t k0 = 0;              // first tile of the launch (tile-range launches: pipelined host execute)
+  int64_t rows_per_tile = 0;   // > 0: row-count tiles (tile k = rows [k*rpt, (k+1)*rpt), aligned)
 };
+void launch_tile_rows_count(int32_t* tile_row, int64_t T, int64_t rows_per_tile, int64_t m, cudaStream_t s);
 // tiles [k0, k1) of a STREAM plan (+ the fix-up of their carries); the rows
 // cut at k0 / k1 are completed by the neighbouring ranges' fix-ups
 int launch_stream_range(const StreamPlan& sp, const double* x, double* y, int64_t k0, int64_t k1, cudaStream_t s);

@@ -652,6 +652,15 @@ int launch_stream_range(const StreamPlan& sp_in, const double* x, double* y, int
   return n;
 }
 
+__global__ void tile_rows_count_kernel(int32_t* __restrict__ tile_row, int64_t T, int64_t rpt, int64_t m) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k <= T) tile_row[k] = (int32_t)(k * rpt < m ? k * rpt : m);
+}
+
+void launch_tile_rows_count(int32_t* tile_row, int64_t T, int64_t rows_per_tile, int64_t m, cudaStream_t s) {
+  tile_rows_count_kernel<<<(unsigned)((T + 1 + kNT - 1) / kNT), kNT, 0, s>>>(tile_row, T, rows_per_tile, m);
+}
+
 __global__ void __launch_bounds__(kNT) range_colmax_kernel(const int32_t* __restrict__ col, int64_t a, int64_t b,
                                                            int32_t* out) {
   int32_t mx = -1;

@@ -244,6 +244,25 @@ def test_device_and_host_buffers_agree():
     assert np.array_equal(yd.cpu().numpy(), y_host)
 
 
+@pytest.mark.parametrize("lens,vs", [([7] * 5000 + [6, 5] * 700 + [7] * 3, 1), ([3, 4] * 3000 + [5], 1),
+                                     ([30, 31, 29] * 900, 4), ([7] * 95 + [6], 1)])
+def test_row_count_tiles(lens, vs):
+    # regular short rows: tile k = rows [k*Rt, (k+1)*Rt) (Rt = whole warp
+    # passes), ragged last tile; structure exported and checked exactly
+    g = np.random.default_rng(5)
+    lens = np.asarray(lens, np.int64)
+    m = sg.from_lengths(lens, lens.size, g, sg.MODE_U11, sg.MODE_U11)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="stream", force_vs=vs, seg=0)
+    info = p.info()
+    Rt = info["rows_per_tile"]
+    assert Rt > 0 and Rt % (32 // vs) == 0 and info["tiles_row_aligned"] == 1
+    T = -(-m.n // Rt)
+    assert np.array_equal(p.export("tile_rows"), np.minimum(np.arange(T + 1) * Rt, m.n))
+    assert Rt * int(lens.max()) <= info["tile_nnz"]
+    assert_bound(p.execute(m.x, np.full(m.n, np.nan)), m)
+    p.destroy()
+
+
 @pytest.mark.parametrize("extra", [{}, {"no_aligned": 1}, {"d16": 1}, {"force_vs": 4}])
 @pytest.mark.parametrize("name,lens", [("uniform", [7] * 40000), ("mixed", ([3, 0, 9, 27, 1, 64] * 8000)),
                                        ("long_rows", [5] * 20000 + [9000] * 3 + [5] * 20000)])
