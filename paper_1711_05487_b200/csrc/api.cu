@@ -746,7 +746,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     // vs 91 rows in 2.85 passes with nnz-cut tiles)
     sp.rows_per_tile = 0;
     const bool regular = maxlen > 0 && (double)maxlen <= 1.25 * avg + 1.0;
-    bool rowtiles = sp.aligned && !d16 && regular && opt.tile_nnz <= 0;
+    // (also above 2^28 nonzeros, unlike the nnz-cut aligned tiles: C5 27-nnz
+    // rows, 32-row tiles, no fix-up: 2.890 vs 2.940 ms per step)
+    bool rowtiles = !seg && opt.reserved[0] == 0 && !d16 && regular && opt.tile_nnz <= 0;
     if (const char* e = getenv("SPMV_ROW_TILES")) rowtiles = rowtiles && atoi(e) != 0;  // experiments
     if (rowtiles) {
       const int64_t rpp = 32 / vs;
@@ -754,6 +756,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       while ((double)Rt * avg < 576.0 && Rt < 4096) Rt += rpp;
       const int64_t Crt = ((Rt * maxlen + 127) / 128) * 128;
       if (Crt <= 4096) {
+        sp.aligned = true;
         sp.rows_per_tile = Rt;
         sp.C = Crt;
         P->C = sp.C;
