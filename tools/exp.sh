@@ -1,4 +1,7 @@
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/x_pytest.txt 2>&1
-run() { name=$1; shift; timeout 300 python bench.py --no-cpu "$@" > gpurun_out/x_$name.log 2>&1; }
-run c5 --config 5 --steps 10
-run c2 --config 2 --steps 30
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "hot or nzsplit or configs_full or suite" > gpurun_out/x_pytest.txt 2>&1
+run() { name=$1; shift; timeout 300 python bench.py --no-cpu --no-e2e --iters 0 "$@" > gpurun_out/x_$name.log 2>&1; }
+for r in 1 2; do
+run c3_cl2_$r --config 3 --steps 40
+SPMV_HOT_CLUSTER=0 run c3_cl1_$r --config 3 --steps 40
+done
+for h in 20000 24576 28672; do run c3_h$h --config 3 --steps 40 --hot $h; done
