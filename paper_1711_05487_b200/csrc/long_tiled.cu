@@ -66,9 +66,7 @@ __global__ void __launch_bounds__(kNT) long_reduce_kernel(const double* __restri
   const int lane = threadIdx.x & 31;
   const int64_t q = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
   if (q >= n_long) return;
-  double a = 0.0;
-  for (int64_t b = lane; b < nblk; b += 32) a += partial[q * nblk + b];
-  a = warp_sum(a);
+  const double a = long_row_total(partial + q * nblk, nblk, lane);
   if (lane == 0) y[long_rows[q]] = a;
 }
 

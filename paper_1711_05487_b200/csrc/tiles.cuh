@@ -338,4 +338,22 @@ __device__ __forceinline__ void long_item(const LongP& p, int64_t it, double* xs
   }
 }
 
+// sum_b partial[b] over b < nblk for one warp (lane-strided): 8 independent
+// accumulators so 8 loads are in flight per lane (a single running sum waits
+// one L2 round trip per 32 partials: ~4 us for C4's 489 blocks), combined in a
+// fixed order, then the fixed butterfly -- deterministic
+__device__ __forceinline__ double long_row_total(const double* __restrict__ partial, int64_t nblk, int lane) {
+  double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int64_t b = lane;
+  for (; b + 7 * 32 < nblk; b += 8 * 32) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] += partial[b + 32 * u];
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (b + 32 * u < nblk) a[u] += partial[b + 32 * u];
+  const double t = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  return warp_sum(t);
+}
+
 }  // namespace spmv
