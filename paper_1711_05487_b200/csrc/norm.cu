@@ -18,18 +18,24 @@ __global__ void __launch_bounds__(kNT) norm_partials_kernel(const double* __rest
                                                             double* __restrict__ partials) {
   const int64_t b = blockIdx.x;
   const int64_t r0 = b * m / kNormPartials, r1 = (b + 1) * m / kNormPartials;
-  double a0 = 0.0, a1 = 0.0;
+  // 8 independent accumulators per thread (8 loads in flight: with 2 the
+  // 512-chunk pass over a C5 block was latency-bound), fixed combine order
+  double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int64_t i = r0 + threadIdx.x;
-  for (; i + kNT < r1; i += 2 * kNT) {
-    const double v0 = ld_stream(y + i), v1 = ld_stream(y + i + kNT);
-    a0 = fma(v0, v0, a0);
-    a1 = fma(v1, v1, a1);
+  for (; i + 7 * kNT < r1; i += 8 * kNT) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = ld_stream(y + i + u * kNT);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = fma(v[u], v[u], a[u]);
   }
-  if (i < r1) {
-    const double v = ld_stream(y + i);
-    a0 = fma(v, v, a0);
-  }
-  const double t = warp_sum(a0 + a1);
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (i + u * kNT < r1) {
+      const double v = ld_stream(y + i + u * kNT);
+      a[u] = fma(v, v, a[u]);
+    }
+  const double t = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
   __shared__ double ws[kNT / 32];
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;
   __syncthreads();
