@@ -345,7 +345,7 @@ def run_native(a):
         xa = torch.empty_like(xf)
         nn = torch.zeros(2, dtype=torch.float64, device="cuda")
         pl = torch.empty(P, dtype=torch.float64, device="cuda")
-        pa = torch.empty(world * P, dtype=torch.float64, device="cuda")
+        pa = torch.empty(world * P, dtype=torch.float64, device="cuda") if world > 1 else pl  # N=1: no gather
         nu = torch.empty(a.iters + 2, dtype=torch.float64, device="cuda")
         steps = parallel.native_steps(plan)
         b = [int(v) for v in blk["bounds"]]

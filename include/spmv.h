@@ -218,6 +218,11 @@ int spmv_normalize(spmv_plan p, const double* y, const double* partials, int cou
  *   spmv_unit: x_out[i] = y[i] / nn[0] for i < n (the final x = yh/||yh||;
  *     x_out may equal y). */
 int spmv_norm_step(spmv_plan p, const double* partials, int count, double* nn, double* nu_k, double* y);
+/* spmv_execute_async(p, x, y) followed by spmv_norm_partials(p, y, partials),
+ * the partials computed inside the SpMV for row-aligned STREAM plans (each
+ * tile sums the squares of the rows it writes; kNormPartials fixed chunks of
+ * the tile sums), so y is not read again. Same contract as the two calls. */
+int spmv_execute_norm(spmv_plan p, const double* x, double* y, double* partials);
 int spmv_unit(spmv_plan p, const double* y, int64_t n, const double* nn, double* x_out);
 
 /* ---- inspection ---------------------------------------------------------- */

@@ -109,6 +109,7 @@ lib.spmv_norm_partial_count.restype = _i32
 lib.spmv_norm_partials.argtypes = [_vp, _vp, _vp]
 lib.spmv_normalize.argtypes = [_vp, _vp, _vp, ctypes.c_int, _vp, _vp]
 lib.spmv_norm_step.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp, _vp]
+lib.spmv_execute_norm.argtypes = [_vp, _vp, _vp, _vp]
 lib.spmv_unit.argtypes = [_vp, _vp, ctypes.c_int64, _vp, _vp]
 lib.spmv_plan_query.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
 
@@ -265,6 +266,9 @@ class Plan:
 
     def normalize(self, y, partials, count, x_out, nu_dev):
         _check(lib.spmv_normalize(self._h, _ptr(y), _ptr(partials), int(count), _ptr(x_out), _ptr(nu_dev)))
+
+    def execute_norm(self, x, y, partials):
+        _check(lib.spmv_execute_norm(self._h, _ptr(x), _ptr(y), _ptr(partials)))
 
     def norm_step(self, partials, count, nn, nu_k, y):
         _check(lib.spmv_norm_step(self._h, _ptr(partials), int(count), _ptr(nn), _ptr(nu_k), _ptr(y)))

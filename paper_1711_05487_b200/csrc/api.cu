@@ -134,6 +134,7 @@ struct Shard {
   // iterated mode
   double* allpart = nullptr;  // G * kNormPartials
   double* x2 = nullptr;       // second x replica (deferred-normalisation ping-pong)
+  double* sq = nullptr;       // per-tile sums of y^2 (fused norm partials, row-aligned STREAM)
   double* nn = nullptr;       // running norm + rescale factor (norm.cu)
   double* nu = nullptr;
   int nu_cap = 0;
@@ -1393,6 +1394,23 @@ int spmv_unit(spmv_plan p, const double* y, int64_t n, const double* nn, double*
 }
 
 namespace {
+// y = A x on shard s plus the norm partials of y (kNormPartials fixed chunks):
+// a row-aligned STREAM plan sums the squares of each tile's rows inside the
+// SpMV (no second pass over y), otherwise a separate partials pass
+int spmv_with_partials(const spmv_plan_s* P, Shard& s, const double* x, double* y, double* partials) {
+  const StreamPlan& sp = s.sp[0];
+  if (P->sel.variant == SPMV_VARIANT_STREAM && sp.aligned && !sp.seg && !sp.rowmap && !sp.need_fixup &&
+      !getenv("SPMV_NO_FUSED_NORM")) {
+    if (!s.sq) s.sq = s.alloc<double>((size_t)sp.T);
+    int n = launch_stream_sq(sp, x, y, s.sq, s.stream);
+    n += launch_sum_partials(s.sq, sp.T, partials, s.stream);
+    return n;
+  }
+  int n = P->launch(s, x, y);
+  n += launch_norm_partials(y, s.m, partials, s.stream);
+  return n;
+}
+
 // ML x-window on the replica the next SpMV reads (the iterate ping-pongs)
 void set_xwin(const spmv_plan_s* P, Shard& s, const double* base) {
   if (!P->sel.xwin) return;
@@ -1409,6 +1427,14 @@ void set_xwin(const spmv_plan_s* P, Shard& s, const double* base) {
   ck(cudaStreamSetAttribute(s.stream, cudaStreamAttributeAccessPolicyWindow, &v), "access policy window");
 }
 }  // namespace
+
+int spmv_execute_norm(spmv_plan p, const double* x, double* y, double* partials) {
+  return guard([&] {
+    if (!p || !x || !y || !partials || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    count_launches(spmv_with_partials(p, s, x, y, partials), "spmv + norm partials");
+  });
+}
 
 // Deferred normalisation (norm.cu, reading 25): iteration k runs
 // the SpMV on replica `cur` (x_0, then yh_{k-1}) and writes yh_k straight into
@@ -1444,9 +1470,8 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
         Shard& s = p->shards[g];
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
         set_xwin(p, s, cur[g]);
-        count_launches(p->launch(s, cur[g], nxt[g] + s.row0), "spmv");
-        count_launches(launch_norm_partials(nxt[g] + s.row0, s.m, s.allpart + (size_t)g * kNormPartials, s.stream),
-                       "norm");
+        count_launches(spmv_with_partials(p, s, cur[g], nxt[g] + s.row0, s.allpart + (size_t)g * kNormPartials),
+                       "spmv + norm partials");
         ck(cudaEventRecord(s.ev_part, s.stream), "event");
       }
       for (int g = 0; g < G; ++g) {

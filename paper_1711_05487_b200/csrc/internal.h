@@ -66,7 +66,10 @@ struct StreamPlan {
   bool l2pf = false;           // producer L2-prefetches each stage's next tile (measured slower: C2 53.7 vs 47.0 us)
   int64_t k0 = 0;              // first tile of the launch (tile-range launches: pipelined host execute)
   int64_t rows_per_tile = 0;   // > 0: row-count tiles (tile k = rows [k*rpt, (k+1)*rpt), aligned)
+  double* sq = nullptr;        // launch-time: per-tile sums of y^2 (row-aligned tiles, iterated mode)
 };
+// row-aligned STREAM plan (no fix-up) with sq[k] = sum of y_r^2 over tile k's rows
+int launch_stream_sq(const StreamPlan& sp, const double* x, double* y, double* sq, cudaStream_t s);
 void launch_tile_rows_count(int32_t* tile_row, int64_t T, int64_t rows_per_tile, int64_t m, cudaStream_t s);
 // tiles [k0, k1) of a STREAM plan (+ the fix-up of their carries); the rows
 // cut at k0 / k1 are completed by the neighbouring ranges' fix-ups
@@ -229,6 +232,8 @@ int compute_table1(const MatView& A, const int32_t* hot_cols, int sm_count, Tabl
 
 // ---- iterated mode -------------------------------------------------------------
 int launch_norm_partials(const double* y, int64_t m, double* partials, cudaStream_t s);
+// partials[q] = sum of v over the fixed chunk q of v[0..n) (no squares)
+int launch_sum_partials(const double* v, int64_t n, double* partials, cudaStream_t s);
 // deferred normalisation (norm.cu): nn[0..1] running norm / rescale factor
 int launch_norm_step(const double* partials, int count, double* nn, double* nu_k, double* y, int64_t m,
                      cudaStream_t s);

@@ -14,8 +14,11 @@
 
 namespace spmv {
 
+template <bool SQ>
 __global__ void __launch_bounds__(kNT) norm_partials_kernel(const double* __restrict__ y, int64_t m,
                                                             double* __restrict__ partials) {
+  pdl_trigger();  // the next kernel in the stream may launch (it waits before reading)
+  pdl_wait();
   const int64_t b = blockIdx.x;
   const int64_t r0 = b * m / kNormPartials, r1 = (b + 1) * m / kNormPartials;
   // 8 independent accumulators per thread (8 loads in flight: with 2 the
@@ -27,13 +30,13 @@ __global__ void __launch_bounds__(kNT) norm_partials_kernel(const double* __rest
 #pragma unroll
     for (int u = 0; u < 8; ++u) v[u] = ld_stream(y + i + u * kNT);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] = fma(v[u], v[u], a[u]);
+    for (int u = 0; u < 8; ++u) a[u] = SQ ? fma(v[u], v[u], a[u]) : a[u] + v[u];
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u)
     if (i + u * kNT < r1) {
       const double v = ld_stream(y + i + u * kNT);
-      a[u] = fma(v, v, a[u]);
+      a[u] = SQ ? fma(v, v, a[u]) : a[u] + v;
     }
   const double t = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
   __shared__ double ws[kNT / 32];
@@ -46,13 +49,28 @@ __global__ void __launch_bounds__(kNT) norm_partials_kernel(const double* __rest
   }
 }
 
+// sum of partials[0..count) by one CTA in a fixed order (thread t: q = t,
+// t+kNT, ... ascending; butterflies; warps ascending) -- identical on every
+// rank; one thread walking the partials waited one L2 round trip per few
+// partials (~30 us for 512, the iterated mode's largest overhead on C5)
+__device__ __forceinline__ double block_sum_fixed(const double* __restrict__ partials, int count) {
+  double a = 0.0;
+  for (int q = threadIdx.x; q < count; q += kNT) a += partials[q];
+  a = warp_sum(a);
+  __shared__ double ws[kNT / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = a;
+  __syncthreads();
+  double ss = 0.0;
+  for (int w = 0; w < kNT / 32; ++w) ss += ws[w];
+  return ss;
+}
+
 __global__ void __launch_bounds__(kNT) normalize_kernel(const double* __restrict__ y, int64_t m,
                                                         const double* __restrict__ partials, int count,
                                                         double* __restrict__ x_out, double* __restrict__ nu_dev) {
   __shared__ double nu_s;
+  const double ss = block_sum_fixed(partials, count);
   if (threadIdx.x == 0) {
-    double ss = 0.0;
-    for (int q = 0; q < count; ++q) ss += partials[q];
     nu_s = sqrt(ss);
     if (blockIdx.x == 0 && nu_dev) *nu_dev = nu_s;
   }
@@ -64,11 +82,13 @@ __global__ void __launch_bounds__(kNT) normalize_kernel(const double* __restrict
 
 // nn[0] = ||yh_k|| (after an exact power-of-two rescale), nn[1] = that
 // rescale factor (1.0: none), *nu_k = ||yh_k|| / ||yh_{k-1}|| (nn[0] == 0 on
-// entry at k = 0: nu_0 = ||yh_0||). One thread: the partials in order.
-__global__ void norm_step_kernel(const double* __restrict__ partials, int count, double* __restrict__ nn,
-                                 double* __restrict__ nu_k) {
-  double ss = 0.0;
-  for (int q = 0; q < count; ++q) ss += partials[q];
+// entry at k = 0: nu_0 = ||yh_0||). One CTA.
+__global__ void __launch_bounds__(kNT) norm_step_kernel(const double* __restrict__ partials, int count,
+                                                        double* __restrict__ nn, double* __restrict__ nu_k) {
+  pdl_trigger();  // the next kernel in the stream may launch (it waits before reading)
+  pdl_wait();
+  const double ss = block_sum_fixed(partials, count);
+  if (threadIdx.x != 0) return;
   const double n = sqrt(ss), prev = nn[0];
   *nu_k = prev > 0.0 ? n / prev : n;
   const int e = (n > 0.0 && isfinite(n)) ? ilogb(n) : 0;
@@ -79,6 +99,8 @@ __global__ void norm_step_kernel(const double* __restrict__ partials, int count,
 
 // y *= nn[1] when the step asked for a rescale (exact: a power of two)
 __global__ void __launch_bounds__(kNT) rescale_kernel(double* __restrict__ y, int64_t m, const double* __restrict__ nn) {
+  pdl_trigger();  // the next kernel in the stream may launch (it waits before reading)
+  pdl_wait();
   const double f = nn[1];
   if (f == 1.0) return;
   const int64_t stride = (int64_t)gridDim.x * kNT;
@@ -88,6 +110,8 @@ __global__ void __launch_bounds__(kNT) rescale_kernel(double* __restrict__ y, in
 // x_out = yh / nn[0]
 __global__ void __launch_bounds__(kNT) unit_kernel(const double* __restrict__ y, int64_t m,
                                                    const double* __restrict__ nn, double* __restrict__ x_out) {
+  pdl_trigger();  // the next kernel in the stream may launch (it waits before reading)
+  pdl_wait();
   const double nu = nn[0];
   const int64_t stride = (int64_t)gridDim.x * kNT;
   for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = y[i] / nu;
@@ -101,18 +125,23 @@ static int grid_for(int64_t m) {
 
 int launch_norm_step(const double* partials, int count, double* nn, double* nu_k, double* y, int64_t m,
                      cudaStream_t s) {
-  norm_step_kernel<<<1, 1, 0, s>>>(partials, count, nn, nu_k);
-  rescale_kernel<<<grid_for(m), kNT, 0, s>>>(y, m, nn);
+  launch_pdl(norm_step_kernel, dim3(1), dim3(kNT), 0, s, partials, count, nn, nu_k);
+  launch_pdl(rescale_kernel, dim3(grid_for(m)), dim3(kNT), 0, s, y, m, (const double*)nn);
   return 2;
 }
 
 int launch_unit(const double* y, int64_t m, const double* nn, double* x_out, cudaStream_t s) {
-  unit_kernel<<<grid_for(m), kNT, 0, s>>>(y, m, nn, x_out);
+  launch_pdl(unit_kernel, dim3(grid_for(m)), dim3(kNT), 0, s, y, m, nn, x_out);
   return 1;
 }
 
 int launch_norm_partials(const double* y, int64_t m, double* partials, cudaStream_t s) {
-  norm_partials_kernel<<<kNormPartials, kNT, 0, s>>>(y, m, partials);
+  launch_pdl(norm_partials_kernel<true>, dim3(kNormPartials), dim3(kNT), 0, s, y, m, partials);
+  return 1;
+}
+
+int launch_sum_partials(const double* v, int64_t n, double* partials, cudaStream_t s) {
+  launch_pdl(norm_partials_kernel<false>, dim3(kNormPartials), dim3(kNT), 0, s, v, n, partials);
   return 1;
 }
 

@@ -117,6 +117,7 @@ struct StreamP {
   double* carry_val;
   int64_t nnz, C, T;  // T: end of the tile range
   int64_t k0;         // first tile of the range
+  double* sq;         // row-aligned tiles: sq[k] = sum of y_r^2 over tile k's rows (iterated mode), or null
   int stages, rows_cap;
   int aligned;  // 1: row-aligned tiles (no row crosses a tile, no carries)
   int l2pf;     // 1: the producer prefetches the stage's next tile into L2
@@ -439,6 +440,7 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
       seg_tile(p, vals_s, reinterpret_cast<const int32_t*>(idx_b),
                reinterpret_cast<double*>(smem + L.prod) + (size_t)w * p.C, rows, fr, nloc, t0, cnt, k, lane32);
     } else {
+      double sqa = 0.0;  // (AL) squares of the rows this lane group writes
       for (int qb = 0; qb < nloc; qb += GPW) {
         const int q = qb + gi;
         const bool active = q < nloc;
@@ -524,7 +526,14 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
             p.carry_val[k] = acc;
           } else {
             p.y[out_row(p, r)] = acc;
+            if constexpr (AL) sqa = fma(acc, acc, sqa);
           }
+        }
+      }
+      if constexpr (AL) {
+        if (p.sq) {  // fixed butterfly over the lanes: deterministic per tile
+          sqa = warp_sum(sqa);
+          if (lane32 == 0) p.sq[k] = sqa;
         }
       }
       if (!incoming && lane32 == 0) p.carry_row[k] = -1;
@@ -553,6 +562,7 @@ static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y)
   p.C = sp.C;
   p.T = sp.T;
   p.k0 = sp.k0;
+  p.sq = sp.sq;
   p.stages = sp.stages;
   p.rows_cap = sp.rows_cap;
   p.aligned = sp.aligned ? 1 : 0;
@@ -637,6 +647,13 @@ int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int sta
 }
 
 int launch_stream(const ExecArgs& a, cudaStream_t s) { return launch_stream_plan(a.sp[0], a.x, a.y, a.stage, s); }
+
+int launch_stream_sq(const StreamPlan& sp_in, const double* x, double* y, double* sq, cudaStream_t s) {
+  StreamPlan sp = sp_in;
+  sp.sq = sq;
+  stream_dispatch<false>(sp, 0, x, y, s);
+  return 1;
+}
 
 int launch_stream_range(const StreamPlan& sp_in, const double* x, double* y, int64_t k0, int64_t k1, cudaStream_t s) {
   if (k1 <= k0) return 0;

@@ -30,7 +30,7 @@ injectable so the orchestration is tested with the ``gloo`` backend on CPU.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Callable, Sequence
+from typing import Callable, Optional, Sequence
 
 
 @dataclass
@@ -40,6 +40,8 @@ class ShardSteps:
     partials: Callable[[object, object], None]        # (y_block, partials_local[P])
     norm_step: Callable[[object, int, object, object, object], None]  # (partials_all, count, nn[2], nu[1], y_block)
     unit: Callable[[object, object, object], None]    # (y, nn[2], x_out): x_out = y / nn[0]
+    # optional fused spmv + partials (x_full, y_block, partials_local)
+    spmv_partials: Optional[Callable[[object, object, object], None]] = None
 
 
 def halo_plan(bounds: Sequence[int], needs: Sequence[Sequence[int]], rank: int):
@@ -105,8 +107,11 @@ def iterate(dist, steps: ShardSteps, bounds: Sequence[int], rank: int, world: in
     nn.zero_()
     cur, nxt = x_full, x_alt
     for k in range(iters):
-        steps.spmv(cur, nxt[b0:b1])
-        steps.partials(nxt[b0:b1], partials_local)
+        if steps.spmv_partials is not None:
+            steps.spmv_partials(cur, nxt[b0:b1], partials_local)
+        else:
+            steps.spmv(cur, nxt[b0:b1])
+            steps.partials(nxt[b0:b1], partials_local)
         dist.all_gather_into_tensor(partials_all, partials_local, group=group)
         steps.norm_step(partials_all, world * P, nn, nu_hist[k:k + 1], nxt[b0:b1])
         exchange_x(dist, bounds, rank, world, nxt, halo, group)
@@ -127,7 +132,8 @@ class NoDist:
 
     @staticmethod
     def all_gather_into_tensor(out, inp, group=None):
-        out.copy_(inp)
+        if out.data_ptr() != inp.data_ptr():  # (callers may pass one buffer for both: no copy kernel)
+            out.copy_(inp)
 
 
 def native_steps(plan) -> ShardSteps:
@@ -137,4 +143,5 @@ def native_steps(plan) -> ShardSteps:
         partials=lambda y, p: plan.norm_partials(y, p),
         norm_step=lambda pa, cnt, nn, nu, y: plan.norm_step(pa, cnt, nn, nu, y),
         unit=lambda y, nn, x: plan.unit(y, nn, x),
+        spmv_partials=lambda x, y, p: plan.execute_norm(x, y, p),
     )

@@ -351,6 +351,27 @@ def test_iterated_mode_rescale(scale):
         assert np.all(np.abs(nug - nur) <= 1e-12 * nur)
 
 
+@pytest.mark.parametrize("c,variant", [(2, "stream"), (5, "stream"), (3, "nnzsplit"), (2, "merge")])
+def test_execute_norm_fused_partials(c, variant):
+    # spmv_execute_norm: y bit-equal to the plain SpMV; the partials (fused
+    # per-tile squares for row-aligned STREAM plans, else the separate pass)
+    # sum to ||y||^2 up to rounding
+    m = sg.config(c, small=True)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant=variant)
+    P = spmv.norm_partial_count()
+    xd = torch.from_numpy(m.x).cuda()
+    y1 = torch.empty(m.n, dtype=torch.float64, device="cuda")
+    y2 = torch.empty(m.n, dtype=torch.float64, device="cuda")
+    pa = torch.empty(P, dtype=torch.float64, device="cuda")
+    p.execute(xd, y1)
+    p.execute_norm(xd, y2, pa)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    ref = float(np.sum(y1.cpu().numpy() ** 2))
+    assert abs(float(pa.sum()) - ref) <= 1e-13 * ref
+    p.destroy()
+
+
 def test_iterated_zero_norm():
     rp = np.zeros(11, np.int64)
     p = spmv.Plan(rp, np.zeros(0, np.int32), np.zeros(0))
