@@ -755,7 +755,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       const int64_t rpp = 32 / vs;
       int64_t Rt = rpp;
       while ((double)Rt * avg < 576.0 && Rt < 4096) Rt += rpp;
-      const int64_t Crt = ((Rt * maxlen + 127) / 128) * 128;
+      const int64_t Crt = ((Rt * maxlen + 31) / 32) * 32;  // capacity only (C5: 864 -> 5 CTAs/SM fit)
       if (Crt <= 4096) {
         sp.aligned = true;
         sp.rows_per_tile = Rt;
@@ -768,6 +768,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     // staged rowptr entries: 1.5x the expected rows per tile (+32)
     const double rpt = avg > 0 ? (double)sp.C / avg : (double)sp.C;
     sp.rows_cap = (int)std::min<double>((double)sp.C + 32, 1.5 * rpt + 32);
+    if (sp.rows_per_tile > 0) sp.rows_cap = (int)sp.rows_per_tile;  // exact
     if (const char* e = getenv("SPMV_ROWS_CAP")) sp.rows_cap = atoi(e);  // tuning knob
     sp.tile_row = s.alloc<int32_t>((size_t)sp.T + 1);
     alloc_carries(s, sp.T, sp.carry_row, sp.carry_val);

@@ -63,9 +63,13 @@ __host__ __device__ inline StreamLayout stream_layout(int64_t C, int stages, int
   StreamLayout L;
   L.rp_cap = (uint32_t)(((size_t)(rows_cap + 2) * rp_bytes + 32 + 15) & ~(size_t)15);
   L.hd_cap = d16 ? (uint32_t)(((size_t)(rows_cap + 2) * 4 + 32 + 15) & ~(size_t)15) : 0u;
+  // slack past C: a row-aligned tile's copies start at the 128-B line of its
+  // first element (values: <= 15 entries before it, int32 colind: <= 31);
+  // the D16 stream keeps 128 entries (its branch-free decode reads up to 8
+  // codes past a row end)
   L.vals = 0;
-  L.idx = al128((size_t)(C + 32) * 8);  // + line-rounding slack of row-aligned tiles
-  L.rp = al128(L.idx + (size_t)(C + 128) * (d16 ? 2 : 4));
+  L.idx = al128((size_t)(C + 16) * 8);
+  L.rp = al128(L.idx + (size_t)(C + (d16 ? 128 : 32)) * (d16 ? 2 : 4));
   L.hd = al128(L.rp + L.rp_cap);
   L.stage = al128(L.hd + L.hd_cap);
   size_t o = L.stage * stages;
