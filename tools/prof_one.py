@@ -13,7 +13,10 @@ ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 blk = bench.build_block(a.config, 0, 1, spmv)
 p = spmv.Plan(blk["rowptr"], blk["colind"], blk["vals"], n_cols=blk["N"], **json.loads(a.opts))
-y = np.empty(p.n_rows)
+# device buffers: every launch is a whole SpMV (a host x/y would take the
+# pipelined tile-range path and ncu would capture one block)
+xd = torch.from_numpy(blk["x"]).cuda()
+yd = torch.empty(p.n_rows, dtype=torch.float64, device="cuda")
 for _ in range(a.reps):
-    p.execute(blk["x"], y)
+    p.execute(xd, yd)
 print(json.dumps({k: v for k, v in p.info().items() if k in ("variant", "sel", "tile_nnz", "n_tiles")}))
