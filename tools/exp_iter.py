@@ -43,13 +43,25 @@ def timed(f):
 
 
 bufs = (xa, xb)
-res = {
-    "a_plain": timed(lambda k: p.execute_async(xd, yd)),
-    "b_pingpong": timed(lambda k: p.execute_async(bufs[k & 1], bufs[(k + 1) & 1])),
-    "c_fused_partials": timed(lambda k: p.execute_norm(bufs[k & 1], bufs[(k + 1) & 1], pl)),
-    "d_plus_norm_step": timed(lambda k: (p.execute_norm(bufs[k & 1], bufs[(k + 1) & 1], pl),
-                                         p.norm_step(pl, P, nn, nu[k:k + 1], bufs[(k + 1) & 1]))),
-}
+x0 = xa.clone()
+
+
+def reset():
+    xa.copy_(x0)
+    xb.copy_(x0)
+    nn.zero_()
+    torch.cuda.synchronize()
+
+
+res = {"a_plain": timed(lambda k: p.execute_async(xd, yd))}
+reset()
+res["b_pingpong"] = timed(lambda k: p.execute_async(bufs[k & 1], bufs[(k + 1) & 1]))
+reset()
+res["c_fused_partials"] = timed(lambda k: p.execute_norm(bufs[k & 1], bufs[(k + 1) & 1], pl))
+reset()
+res["d_plus_norm_step"] = timed(lambda k: (p.execute_norm(bufs[k & 1], bufs[(k + 1) & 1], pl),
+                                           p.norm_step(pl, P, nn, nu[k:k + 1], bufs[(k + 1) & 1])))
+reset()
 steps = parallel.native_steps(p)
 pa = pl
 b = [0, n]

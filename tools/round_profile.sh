@@ -10,7 +10,7 @@ for c in 5 2 3 4 1; do
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_ref.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_c5.csv \
-  python bench.py --steps 3 --warmup 1 --no-cpu --no-e2e --iters 0 > $out/ncu_launch_c5.log 2>&1
+  python bench.py --steps 3 --warmup 1 --no-cpu --no-e2e --no-cold --iters 0 > $out/ncu_launch_c5.log 2>&1
 declare -A K=([5]="stream_kernel" [2]="stream_kernel" [3]="nzsplit_kernel" [4]="split_fused_kernel" [1]="stream_kernel")
 for c in 5 2 3 4; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:${K[$c]} -s 2 -c 1 \
