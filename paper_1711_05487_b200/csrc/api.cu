@@ -14,6 +14,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "spmv.h"
@@ -81,6 +82,64 @@ bool is_device_ptr(const void* p, int* dev) {
     return true;
   }
   return false;
+}
+
+bool is_pageable_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Host -> device copy of a large pageable array: chunks are copied by host
+// threads into two pinned staging buffers and DMA'd from there, the next
+// chunk's host copy overlapping the previous chunk's DMA (the driver's own
+// pageable path stages single-threaded: C5's 18.7 GB took ~4.2 s). Pinned or
+// device sources and small arrays go straight to cudaMemcpyAsync.
+void upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  constexpr size_t kChunk = 64ull << 20;
+  if (bytes < 2 * kChunk || !is_pageable_host(src) || getenv("SPMV_NO_STAGED_UPLOAD")) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s), "upload");
+    return;
+  }
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  auto cleanup = [&] {
+    for (int i = 0; i < 2; ++i) {
+      if (ev[i]) cudaEventDestroy(ev[i]);
+      if (buf[i]) cudaFreeHost(buf[i]);
+    }
+  };
+  try {
+    for (int i = 0; i < 2; ++i) {
+      ck(cudaHostAlloc(&buf[i], kChunk, cudaHostAllocDefault), "cudaHostAlloc");
+      ck(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const char* sp = static_cast<const char*>(src);
+    char* dp = static_cast<char*>(dst);
+    int i = 0;
+    for (size_t off = 0; off < bytes; off += kChunk, i ^= 1) {
+      const size_t n = std::min(kChunk, bytes - off);
+      ck(cudaEventSynchronize(ev[i]), "staging");  // the DMA that last used buf[i] is done
+      std::vector<std::thread> th;
+      const size_t per = (n + nt - 1) / nt;
+      for (unsigned t = 0; t < nt; ++t) {
+        const size_t a = t * per, b = std::min(n, a + per);
+        if (a < b) th.emplace_back([=] { memcpy(static_cast<char*>(buf[i]) + a, sp + off + a, b - a); });
+      }
+      for (auto& t : th) t.join();
+      ck(cudaMemcpyAsync(dp + off, buf[i], n, cudaMemcpyHostToDevice, s), "upload");
+      ck(cudaEventRecord(ev[i], s), "event");
+    }
+    ck(cudaStreamSynchronize(s), "upload");
+    cleanup();
+  } catch (...) {
+    cleanup();
+    throw;
+  }
 }
 
 int64_t rp_at(const void* rp, int bytes, int64_t i) {
@@ -608,11 +667,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     s.rowptr = s.alloc<char>((size_t)(s.m + 1) * rp_bytes);
     s.col = s.alloc<int32_t>((size_t)s.nnz);
     s.val = s.alloc<double>((size_t)s.nnz);
-    ck(cudaMemcpyAsync(s.rowptr, (const char*)rowptr + s.row0 * rp_bytes, (size_t)(s.m + 1) * rp_bytes,
-                       cudaMemcpyDefault, s.stream), "upload rowptr");
+    upload(s.rowptr, (const char*)rowptr + s.row0 * rp_bytes, (size_t)(s.m + 1) * rp_bytes, s.stream);
     if (s.nnz) {
-      ck(cudaMemcpyAsync(s.col, colind + s.nnz0, (size_t)s.nnz * 4, cudaMemcpyDefault, s.stream), "upload colind");
-      ck(cudaMemcpyAsync(s.val, values + s.nnz0, (size_t)s.nnz * 8, cudaMemcpyDefault, s.stream), "upload values");
+      upload(s.col, colind + s.nnz0, (size_t)s.nnz * 4, s.stream);
+      upload(s.val, values + s.nnz0, (size_t)s.nnz * 8, s.stream);
     }
     launch_rebase(s.rowptr, rp_bytes, s.m + 1, s.nnz0, s.stream);
     count_launches(s.nnz0 ? 1 : 0, "rebase");
