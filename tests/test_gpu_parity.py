@@ -263,7 +263,7 @@ def test_row_count_tiles(lens, vs):
     p.destroy()
 
 
-@pytest.mark.parametrize("extra", [{}, {"no_aligned": 1}, {"d16": 1}, {"force_vs": 4}])
+@pytest.mark.parametrize("extra", [{}, {"no_aligned": 1}, {"d16": 1}, {"force_vs": 4}, {"tile_nnz": 0}])
 @pytest.mark.parametrize("name,lens", [("uniform", [7] * 40000), ("mixed", ([3, 0, 9, 27, 1, 64] * 8000)),
                                        ("long_rows", [5] * 20000 + [9000] * 3 + [5] * 20000)])
 def test_pipelined_host_execute(monkeypatch, name, lens, extra):
@@ -275,7 +275,9 @@ def test_pipelined_host_execute(monkeypatch, name, lens, extra):
     g = np.random.default_rng(11)
     lens = np.asarray(lens, np.int64)
     m = sg.from_lengths(lens, lens.size, g, sg.MODE_U11, sg.MODE_U11)
-    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="stream", tile_nnz=512, **extra)
+    kw = {"tile_nnz": 512, "seg": 0}
+    kw.update(extra)  # tile_nnz 0: the plan's own tile rule (row-count tiles on regular rows)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="stream", **kw)
     yh = p.execute(m.x, np.full(m.n, np.nan))  # host buffers: pipelined
     assert_bound(yh, m)
     assert np.all(yh[lens == 0] == 0.0)
