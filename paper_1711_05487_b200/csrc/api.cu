@@ -202,6 +202,7 @@ struct Shard {
   // x chunk each needs, the first row each block completes, copy streams
   struct HostPipe {
     bool ready = false, usable = false;
+    bool nz = false;             // nnz_split pass (else STREAM)
     std::vector<int64_t> kb;     // block b = tiles [kb[b], kb[b+1])
     std::vector<int64_t> srow;   // block b completes rows [srow[b], srow[b+1])
     std::vector<int64_t> xhi;    // x[xlo, xhi[b]) is needed by blocks <= b
@@ -1229,6 +1230,41 @@ void host_pipe_prepare(spmv_plan p, Shard& s) {
   // a later range would overwrite an earlier range's fix-up, so not pipelined)
   int64_t min_bytes = 16ll << 20;
   if (const char* e = getenv("SPMV_HOST_PIPE_MIN_BYTES")) min_bytes = atoll(e);  // tests: pipeline small plans
+  if (p->sel.variant == SPMV_VARIANT_NNZSPLIT && s.use_nz && !s.nz.skip_rp && xbytes >= min_bytes && s.m > 0) {
+    // nnz_split: the x gather is random, so the whole column range goes up
+    // first; the ranges then overlap the download of y. A row is assigned by
+    // the tile where it ends and range b's carries are added after range
+    // b+1, so a range must be longer than any row (rows span <= 2 ranges).
+    const NzPlan& z = s.nz;
+    int64_t nbw = std::min<int64_t>(8, std::max<int64_t>(2, (int64_t)s.m * 8 / (4ll << 20)));
+    if (const char* e = getenv("SPMV_HOST_PIPE_BLOCKS")) nbw = atoll(e);  // tests
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(nbw, z.T / std::max<int64_t>(2 * z.max_run, 8)));
+    if (nb < 2) return;
+    h.nz = true;
+    h.kb.resize(nb + 1);
+    h.srow.resize(nb + 1);
+    h.xhi.assign(nb, s.hs.col_max + 1);
+    h.xlo = std::min<int64_t>(std::max<long long>(0, s.hs.col_min), s.hs.col_max + 1);
+    for (int b = 0; b <= nb; ++b) h.kb[b] = z.T * b / nb;
+    h.srow[0] = 0;
+    h.srow[nb] = s.m;
+    for (int b = 1; b < nb; ++b) {  // first row ending in range b: rowmap[tile_q[kb]]
+      int32_t q = 0, r = 0;
+      ck(cudaMemcpy(&q, z.tile_q + h.kb[b], 4, cudaMemcpyDeviceToHost), "tile_q");
+      ck(cudaMemcpy(&r, z.rowmap + q, 4, cudaMemcpyDeviceToHost), "rowmap");
+      h.srow[b] = r;
+    }
+    ck(cudaStreamCreateWithFlags(&h.h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&h.d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+    h.ev_h.resize(nb);
+    h.ev_c.resize(nb);
+    for (int b = 0; b < nb; ++b) {
+      ck(cudaEventCreateWithFlags(&h.ev_h[b], cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventCreateWithFlags(&h.ev_c[b], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    h.usable = true;
+    return;
+  }
   if (p->sel.variant != SPMV_VARIANT_STREAM || sp.rowmap || sp.seg || sp.T < 8 || xbytes < min_bytes || s.m == 0)
     return;
   // blocks: one per ~4 MB of x, 2..16 (B200 sweeps: C2 16.8 MB -> 4 blocks
@@ -1289,9 +1325,40 @@ void host_pipe_prepare(spmv_plan p, Shard& s) {
   h.usable = true;
 }
 
+// nnz_split ranges: K(0), then K(b), F(b-1), copy of range b-1's rows, ...
+int host_pipe_run_nz(Shard& s, const double* x, double* y) {
+  auto& h = s.hp;
+  const NzPlan& z = s.nz;
+  const int nb = (int)h.xhi.size();
+  int n = 0;
+  ck(cudaEventRecord(h.ev_c[0], s.stream), "event");
+  ck(cudaStreamWaitEvent(h.h2d, h.ev_c[0], 0), "wait");
+  ck(cudaStreamWaitEvent(h.d2h, h.ev_c[0], 0), "wait");
+  if (h.xhi[0] > h.xlo)
+    ck(cudaMemcpyAsync(s.x + h.xlo, x + h.xlo, (size_t)(h.xhi[0] - h.xlo) * 8, cudaMemcpyHostToDevice, h.h2d),
+       "copy x");
+  ck(cudaEventRecord(h.ev_h[0], h.h2d), "event");
+  ck(cudaStreamWaitEvent(s.stream, h.ev_h[0], 0), "wait");
+  n += launch_nz_prologue(z, s.x, s.y, s.stream);
+  n += launch_nz_range(z, s.x, s.y, h.kb[0], h.kb[1], s.stream);
+  for (int b = 0; b < nb; ++b) {
+    if (b + 1 < nb) n += launch_nz_range(z, s.x, s.y, h.kb[b + 1], h.kb[b + 2], s.stream);
+    n += launch_nz_fixup_range(z, s.y, h.kb[b], h.kb[b + 1], s.stream);
+    ck(cudaEventRecord(h.ev_c[b], s.stream), "event");
+    ck(cudaStreamWaitEvent(h.d2h, h.ev_c[b], 0), "wait");
+    const int64_t r0 = h.srow[b], r1 = h.srow[b + 1];
+    if (r1 > r0)
+      ck(cudaMemcpyAsync(y + s.row0 + r0, s.y + r0, (size_t)(r1 - r0) * 8, cudaMemcpyDeviceToHost, h.d2h), "copy y");
+  }
+  ck(cudaEventRecord(h.ev_h[0], h.d2h), "event");
+  ck(cudaStreamWaitEvent(s.stream, h.ev_h[0], 0), "wait");
+  return n;
+}
+
 // enqueue the pipelined SpMV of shard s (x, y host); returns launches
 int host_pipe_run(spmv_plan p, Shard& s, const double* x, double* y) {
   auto& h = s.hp;
+  if (h.nz) return host_pipe_run_nz(s, x, y);
   const int nb = (int)h.xhi.size();
   int n = 0;
   ck(cudaEventRecord(h.ev_c[0], s.stream), "event");  // copies start after earlier work on the plan stream

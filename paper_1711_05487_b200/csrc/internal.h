@@ -124,6 +124,9 @@ void launch_hot_write(const int32_t* cnt, int64_t n_cols, int32_t t, const int32
                       int32_t* slot, cudaStream_t s);
 void launch_hot_encode(int32_t* col, int64_t nnz, const int32_t* slot, cudaStream_t s);
 int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaStream_t s);
+int launch_nz_prologue(const NzPlan& z, const double* x, double* y, cudaStream_t s);
+int launch_nz_range(const NzPlan& z, const double* x, double* y, int64_t k0, int64_t k1, cudaStream_t s);
+int launch_nz_fixup_range(const NzPlan& z, double* y, int64_t k0, int64_t k1, cudaStream_t s);
 
 // ---- inspector ------------------------------------------------------------
 void launch_rowstats(const MatView& A, int64_t l_split, uint32_t* headbits, DevStats* st, cudaStream_t s);

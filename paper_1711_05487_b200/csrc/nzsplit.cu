@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
   const int64_t nw = (int64_t)gridDim.x * NW;
   if constexpr (HOT && kNzHotPrefetch) {
     // the next tile's streams are loaded while this tile gathers x
-    int64_t k = (int64_t)blockIdx.x * NW + w;
+    int64_t k = p.k0 + (int64_t)blockIdx.x * NW + w;
     int c[8], cn[8];
     double v[8], vn[8];
     NzMeta m, mn;
@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
       m = mn;
     }
   } else {
-    for (int64_t k = (int64_t)blockIdx.x * NW + w; k < p.T; k += nw) nz_tile<RP, HOT, MASK, L2G>(p, k, lane, xh, em);
+    for (int64_t k = p.k0 + (int64_t)blockIdx.x * NW + w; k < p.T; k += nw)
+      nz_tile<RP, HOT, MASK, L2G>(p, k, lane, xh, em);
   }
 }
 
@@ -210,6 +211,7 @@ static NzP<RP> nz_params(const NzPlan& z, const double* x, double* y) {
   p.xhot = z.xhot;
   p.nnz = z.V.nnz;
   p.T = z.T;
+  p.k0 = 0;
   p.n_hot = z.n_hot;
   p.zero_gaps = z.zero_gaps ? 1 : 0;
   return p;
@@ -248,17 +250,53 @@ int nz_prepare(NzPlan& z, int sm_count) {
   return hot ? nz_grid_t<int32_t, true>(z, sm_count) : nz_grid_t<int32_t, false>(z, sm_count);
 }
 
+template <typename RP>
+static NzP<RP> nz_range_params(const NzPlan& z, const double* x, double* y, int64_t k0, int64_t k1) {
+  NzP<RP> p = nz_params<RP>(z, x, y);
+  p.k0 = k0;
+  p.T = k1;
+  return p;
+}
+
+// tiles [k0, k1) (the whole pass: 0, T); grid capped to the range's warps
 template <bool HOT>
-static void launch_nz_main(const NzPlan& z, const double* x, double* y, cudaStream_t s) {
+static void launch_nz_main(const NzPlan& z, const double* x, double* y, cudaStream_t s, int64_t k0 = 0,
+                           int64_t k1 = -1) {
+  if (k1 < 0) k1 = z.T;
   const size_t sm = nz_smem_bytes(HOT ? z.n_hot : 0);
-  const dim3 blk(32 * (HOT ? kNzHotWarps : kNzWarps));
+  const int nw = HOT ? kNzHotWarps : kNzWarps;
+  const dim3 blk(32 * nw);
+  const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(z.grid, (k1 - k0 + nw - 1) / nw)));
   if (z.V.rp_bytes == 8) {
-    if (z.gather_l2) launch_pdl(nzsplit_kernel<int64_t, HOT, true>, dim3(z.grid), blk, sm, s, nz_params<int64_t>(z, x, y));
-    else launch_pdl(nzsplit_kernel<int64_t, HOT, false>, dim3(z.grid), blk, sm, s, nz_params<int64_t>(z, x, y));
+    if (z.gather_l2) launch_pdl(nzsplit_kernel<int64_t, HOT, true>, g, blk, sm, s, nz_range_params<int64_t>(z, x, y, k0, k1));
+    else launch_pdl(nzsplit_kernel<int64_t, HOT, false>, g, blk, sm, s, nz_range_params<int64_t>(z, x, y, k0, k1));
   } else {
-    if (z.gather_l2) launch_pdl(nzsplit_kernel<int32_t, HOT, true>, dim3(z.grid), blk, sm, s, nz_params<int32_t>(z, x, y));
-    else launch_pdl(nzsplit_kernel<int32_t, HOT, false>, dim3(z.grid), blk, sm, s, nz_params<int32_t>(z, x, y));
+    if (z.gather_l2) launch_pdl(nzsplit_kernel<int32_t, HOT, true>, g, blk, sm, s, nz_range_params<int32_t>(z, x, y, k0, k1));
+    else launch_pdl(nzsplit_kernel<int32_t, HOT, false>, g, blk, sm, s, nz_range_params<int32_t>(z, x, y, k0, k1));
   }
+}
+
+// pipelined host execute (api.cu host_pipe_*): the y clear / hot-x gather
+// before the first range, the ranges, and the fix-up of a range's carries
+// (run after the NEXT range: a row is assigned by the tile where it ends)
+int launch_nz_prologue(const NzPlan& z, const double* x, double* y, cudaStream_t s) {
+  if (z.memset_y) cudaMemsetAsync(y, 0, (size_t)z.m_out * 8, s);
+  if (z.n_hot > 0) {
+    launch_pdl(nz_hot_gather_kernel, dim3((z.n_hot + kNT - 1) / kNT), dim3(kNT), 0, s, z.hot_cols, z.n_hot, x,
+               z.xhot);
+    return 1;
+  }
+  return 0;
+}
+int launch_nz_range(const NzPlan& z, const double* x, double* y, int64_t k0, int64_t k1, cudaStream_t s) {
+  if (k1 <= k0) return 0;
+  if (z.n_hot > 0) launch_nz_main<true>(z, x, y, s, k0, k1);
+  else launch_nz_main<false>(z, x, y, s, k0, k1);
+  return 1;
+}
+int launch_nz_fixup_range(const NzPlan& z, double* y, int64_t k0, int64_t k1, cudaStream_t s) {
+  if (k1 <= k0 || z.T <= 1) return 0;
+  return launch_fixup(z.carry_row + k0, z.carry_val + k0, k1 - k0, y, 0, z.max_run, s);
 }
 
 int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaStream_t s) {

@@ -33,7 +33,8 @@ struct NzP {
   double* carry_val;
   const RP* orp;        // non-null: zero a gap row only if it is empty in this rowptr (SPLIT: long rows are not ours)
   const double* xhot;   // hot-x mode: x of the hot columns, [n_hot]
-  int64_t nnz, T;
+  int64_t nnz, T;  // T: end of the tile range
+  int64_t k0;      // first tile of the range (pipelined host execute)
   int n_hot;
   int zero_gaps;
 };

@@ -292,6 +292,27 @@ def test_pipelined_host_execute(monkeypatch, name, lens, extra):
     p.destroy()
 
 
+@pytest.mark.parametrize("hot", [0, 256])
+@pytest.mark.parametrize("name,lens", [("powerlaw", None), ("empty_runs", ([0] * 300 + [700, 3, 0, 5]) * 60),
+                                       ("long_rows", [5] * 20000 + [9000] * 3 + [0] * 500 + [5] * 20000)])
+def test_pipelined_host_execute_nnzsplit(monkeypatch, name, lens, hot):
+    # nnz_split ranges with the y download overlapped: range b's carries are
+    # added after range b+1 (rows are assigned where they end); every row,
+    # empty ones included, must come back complete
+    monkeypatch.setenv("SPMV_HOST_PIPE_MIN_BYTES", "1")
+    monkeypatch.setenv("SPMV_HOST_PIPE_BLOCKS", "5")
+    g = np.random.default_rng(13)
+    if lens is None:
+        lens = np.minimum((g.pareto(1.2, size=60000) * 3).astype(np.int64), 20000)
+    lens = np.asarray(lens, np.int64)
+    m = sg.from_lengths(lens, lens.size, g, sg.MODE_U11, sg.MODE_U11)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="nnzsplit", hot_x=hot)
+    yh = p.execute(m.x, np.full(m.n, np.nan))
+    assert_bound(yh, m)
+    assert np.all(yh[lens == 0] == 0.0)
+    p.destroy()
+
+
 def test_deterministic_repeat():
     m = sg.config(3, small=True)
     for v in ALL:
