@@ -1,3 +1,4 @@
-run() { name=$1; shift; timeout 300 python bench.py --no-cpu --no-cold --iters 0 "$@" > gpurun_out/x_$name.log 2>&1; }
-for r in 1 2 3; do run c4_$r --config 4 --steps 10; done
-run c2 --config 2 --steps 10
+for v in def p8 p8lb3 p12lb3; do
+  if [ $v = def ]; then unset SPMV_LIB_PATH; else export SPMV_LIB_PATH=exp/$v/libspmv.so; fi
+  timeout 600 python tools/exp_parts.py --config 4 --variants auto --parts all,long > gpurun_out/x_parts_$v.txt 2>&1
+done
