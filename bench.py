@@ -440,7 +440,9 @@ def run_native(a):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": f"{info['variant']} main kernel (stage 1), rank 0",
-                         "kernel_ms": ms_main, "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind},
+                         "kernel_ms": ms_main, "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
+                         # ncu DRAM bytes of one launch / this run's kernel time (SURVEY 8(d) "actual DRAM GB/s")
+                         "traffic_gbs": (traffic / (ms_main * 1e-3) / 1e9) if traffic else None},
             "cold_l2": cold,
             "cpu_baseline": cpu,
             "e2e": e2e,
