@@ -1,1 +1,1 @@
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:long_tiled -s 2 -c 1 -o gpurun_out/x_c4long python tools/exp_parts.py --config 4 --variants split --parts long --reps 3 > gpurun_out/x_ncu1.txt 2>&1
+timeout 1200 python -m pytest tests/test_gpu_stress.py -m gpu -q > gpurun_out/x_pytest.txt 2>&1
