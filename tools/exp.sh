@@ -1,6 +1,4 @@
-export SPMV_LIB_PATH=exp/tma/libspmv.so
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "hot or nzsplit_edges or configs_full" > gpurun_out/x_pytest.txt 2>&1
-run() { name=$1; shift; timeout 300 python bench.py --no-cpu --no-e2e --no-cold --iters 0 "$@" > gpurun_out/x_$name.log 2>&1; }
-for r in 1 2; do run c3_tma_$r --config 3 --steps 40; done
-unset SPMV_LIB_PATH
-for r in 1 2; do run c3_def_$r --config 3 --steps 40; done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/x_pytest.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/x_smoke.txt 2>&1
+timeout 600 python bench.py > gpurun_out/x_bench.txt 2>&1
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/x_bench_ref.txt 2>&1
