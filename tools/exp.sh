@@ -1,4 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/x_pytest.txt 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/x_smoke.txt 2>&1
-timeout 600 python bench.py > gpurun_out/x_bench.txt 2>&1
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/x_bench_ref.txt 2>&1
+timeout 1200 python tools/cusparse_context.py --configs 2,3,4,5 --out gpurun_out/x_cusparse.json > gpurun_out/x_cusparse.txt 2>&1

@@ -75,6 +75,9 @@ for c in (2, 3, 4, 5):
     sp_ = os.path.join(src, f"sweep_c{c}.json")
     if os.path.exists(sp_):
         shutil.copy(sp_, os.path.join(dst, f"{tag}_sweep_c{c}.json"))
+cs = os.path.join(src, "cusparse.json")
+if os.path.exists(cs):
+    shutil.copy(cs, os.path.join(dst, f"{tag}_cusparse.json"))
 t5 = os.path.join(src, "table5.json")
 if os.path.exists(t5):
     shutil.copy(t5, os.path.join(dst, f"{tag}_table5.json"))
