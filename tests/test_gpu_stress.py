@@ -30,7 +30,10 @@ def _lengths(g, kind, n):
     return lens
 
 
-CASES = [(seed, kind) for seed in range(3) for kind in ("regular", "powerlaw", "empty_runs", "long")]
+import os
+
+_SEEDS = int(os.environ.get("SPMV_STRESS_SEEDS", "3"))  # more seeds for a longer sweep
+CASES = [(seed, kind) for seed in range(_SEEDS) for kind in ("regular", "powerlaw", "empty_runs", "long")]
 
 
 @pytest.mark.parametrize("seed,kind", CASES)

@@ -1,1 +1,1 @@
-timeout 1200 python tools/cusparse_context.py --configs 2,3,4,5 --out gpurun_out/x_cusparse.json > gpurun_out/x_cusparse.txt 2>&1
+SPMV_STRESS_SEEDS=40 timeout 2400 python -m pytest tests/test_gpu_stress.py -m gpu -q > gpurun_out/x_pytest.txt 2>&1
