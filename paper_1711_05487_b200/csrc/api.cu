@@ -871,6 +871,13 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     // one stage per consumer warp: measured on B200 (tools/sweep.py, C2/C5),
     // more resident warps beat a deeper ring (the x gathers are latency-bound)
     sp.stages = opt.stages > 0 ? opt.stages : kStreamConsumerWarps;
+    // 6 consumer warps (one stage each) when 4 such CTAs fit an SM: more
+    // bytes in flight for small row-aligned stages (C2: 4 x 6 x 8.8 KB,
+    // 31.4 vs 32.5 us; C5's 11.4-KB stages keep 5 CTAs x 4)
+    if (opt.stages == 0 && sp.aligned && vs == 1 && !d16 && !seg && !getenv("SPMV_NO_CW6")) {
+      const size_t sm6 = stream_smem_bytes(sp.C, 6, V.rp_bytes, sp.rows_cap, false, false);
+      if (4 * (sm6 + 1024) <= 228 * 1024) sp.stages = 6;
+    }
     if (const char* e = getenv("SPMV_STREAM_L2PF")) sp.l2pf = atoi(e) != 0;
     // shrink the staged-rowptr capacity until the ring fits (sparser tiles
     // then read rowptr from global memory)

@@ -7,7 +7,10 @@ namespace spmv {
 
 constexpr int kNT = 256;  // threads per CTA for every SpMV kernel
 constexpr int kNormPartials = 512;  // fixed row chunking of the norm reduction
-constexpr int kStreamConsumerWarps = 4;  // cta_stream consumer warps per CTA (stages: multiple of this)
+#ifndef STREAM_CW
+#define STREAM_CW 4
+#endif
+constexpr int kStreamConsumerWarps = STREAM_CW;  // cta_stream consumer warps per CTA (stages: multiple of this)
 constexpr int64_t kShortRowMax = 32;  // SPLIT: rows up to this length form the one-lane-per-row bin
 
 // Device-side inspector accumulators (integers only => order-independent).

@@ -255,8 +255,12 @@ constexpr int kStreamUnroll1 = STREAM_UNR1;  // gathers in flight per lane, one 
 // row-aligned tiles (compile-time so the nnz-tile path carries no per-tile
 // offsets: measured ~9% faster on C5 than a runtime switch). D16: 0 = int32
 // colind, 1 = 16-bit deltas, 2 = 16-bit deltas with escape codes.
-template <int VS, typename RP, int D16, int MODE>
-__global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D16_LB : SPMV_STREAM_LB))
+// CW: consumer warps per CTA (one smem stage each); 6 for small row-aligned
+// stages (C2: 4 CTAs x 6 x 8.8 KB in flight per SM, 31.4 vs 32.5 us with
+// 5 x 4), else 4 (C5's 11.4-KB stages: 5 x 4 fills the 228 KB)
+template <int VS, typename RP, int D16, int MODE, int CW = kConsumerWarps>
+__global__ void __launch_bounds__(32 * (CW + 1),
+                                  MODE == 1 ? 4 : (D16 ? SPMV_D16_LB : (CW == 4 ? SPMV_STREAM_LB : 24 / CW)))
     stream_kernel(const StreamP<RP> p) {
   constexpr bool SEG = MODE == 1;
   constexpr bool AL = MODE == 2;
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(kStreamThreads, MODE == 1 ? 4 : (D16 ? SPMV_D1
   constexpr int GPW = 32 / VS;
   const int lane = lane32 % VS;
   const int gi = lane32 / VS;
-  for (int i = w;; i += kConsumerWarps) {
+  for (int i = w;; i += CW) {
     const int64_t k = p.k0 + blockIdx.x + (int64_t)i * gridDim.x;
     if (k >= p.T) break;
     const int s = i % S;
@@ -575,14 +579,14 @@ static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y)
   return p;
 }
 
-template <int VS, typename RP, int D16, int MODE>
+template <int VS, typename RP, int D16, int MODE, int CW>
 static int stream_prepare_t(const StreamPlan& sp, int sm_count) {
   const size_t smem = stream_smem_bytes(sp.C, sp.stages, sizeof(RP), sp.rows_cap, D16, MODE == 1);
-  if (cudaFuncSetAttribute(stream_kernel<VS, RP, D16, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(stream_kernel<VS, RP, D16, MODE, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_kernel<VS, RP, D16, MODE>, kStreamThreads,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_kernel<VS, RP, D16, MODE, CW>, 32 * (CW + 1),
                                                     smem) != cudaSuccess ||
       per_sm < 1)
     return -1;
@@ -592,16 +596,25 @@ static int stream_prepare_t(const StreamPlan& sp, int sm_count) {
   return (int)grid;
 }
 
-template <int VS, typename RP, int D16, int MODE>
+template <int VS, typename RP, int D16, int MODE, int CW>
 static void stream_launch_t(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
   const size_t smem = stream_smem_bytes(sp.C, sp.stages, sizeof(RP), sp.rows_cap, D16, MODE == 1);
-  launch_pdl(stream_kernel<VS, RP, D16, MODE>, dim3(sp.grid), dim3(kStreamThreads), smem, s, make_params<RP>(sp, x, y));
+  launch_pdl(stream_kernel<VS, RP, D16, MODE, CW>, dim3(sp.grid), dim3(32 * (CW + 1)), smem, s,
+             make_params<RP>(sp, x, y));
 }
 
 template <int VS, typename RP, int D16, int MODE, bool PREP>
 static int stream_one(const StreamPlan& sp, int sm_count, const double* x, double* y, cudaStream_t s) {
-  if (PREP) return stream_prepare_t<VS, RP, D16, MODE>(sp, sm_count);
-  stream_launch_t<VS, RP, D16, MODE>(sp, x, y, s);
+  // 6 consumer warps only for the plain row-aligned one-lane-per-row kernel
+  if constexpr (VS == 1 && D16 == 0 && MODE == 2) {
+    if (sp.stages == 6) {
+      if (PREP) return stream_prepare_t<VS, RP, D16, MODE, 6>(sp, sm_count);
+      stream_launch_t<VS, RP, D16, MODE, 6>(sp, x, y, s);
+      return 0;
+    }
+  }
+  if (PREP) return stream_prepare_t<VS, RP, D16, MODE, kConsumerWarps>(sp, sm_count);
+  stream_launch_t<VS, RP, D16, MODE, kConsumerWarps>(sp, x, y, s);
   return 0;
 }
 
