@@ -813,7 +813,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     if (rowtiles) {
       const int64_t rpp = 32 / vs;
       int64_t Rt = rpp;
-      while ((double)Rt * avg < 576.0 && Rt < 4096) Rt += rpp;
+      double min_nz = 576.0;
+      if (const char* e = getenv("SPMV_ROW_TILE_MIN_NNZ")) min_nz = atof(e);  // experiments
+      while ((double)Rt * avg < min_nz && Rt < 4096) Rt += rpp;
       const int64_t Crt = ((Rt * maxlen + 31) / 32) * 32;  // capacity only (C5: 864 -> 5 CTAs/SM fit)
       if (Crt <= 4096) {
         sp.aligned = true;
