@@ -112,3 +112,24 @@ def test_invalid_options_rejected_without_gpu():
         pkg.select(f, _props(), 4, force_vs=3)
     with pytest.raises(pkg.SpmvError):
         pkg.select(f, _props(), 4, tile_nnz=100)
+
+
+def test_null_plan_arguments_fail_with_status_not_crash():
+    # every plan-taking entry point rejects a NULL plan with SPMV_E_ARG (-1)
+    # and a message, without touching a device (include/spmv.h conventions)
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_1711_05487_b200", "libspmv.so"))
+    vp = ctypes.c_void_p
+    lib.spmv_last_error.restype = ctypes.c_char_p
+    buf = (ctypes.c_double * 16)()
+    calls = {
+        "spmv_execute": (vp(None), buf, buf),
+        "spmv_execute_async": (vp(None), buf, buf),
+        "spmv_execute_norm": (vp(None), buf, buf, buf),
+        "spmv_norm_partials": (vp(None), buf, buf),
+        "spmv_norm_step": (vp(None), buf, ctypes.c_int(4), buf, buf, buf),
+        "spmv_unit": (vp(None), buf, ctypes.c_int64(4), buf, buf),
+    }
+    for name, args in calls.items():
+        rc = getattr(lib, name)(*args)
+        assert rc == -1, name
+        assert lib.spmv_last_error(), name
