@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, K, out_q, use_halo=False, cfg=5):
+def _worker(rank, world, port, K, out_q, use_halo=False, cfg=5, scale=1.0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -36,7 +36,7 @@ def _worker(rank, world, port, K, out_q, use_halo=False, cfg=5):
         b = pkg.shard_bounds(rp, world)
         b0, b1 = int(b[rank]), int(b[rank + 1])
         lrp = rp[b0:b1 + 1] - rp[b0]
-        lci, lva = m.colind[rp[b0]:rp[b1]], m.vals[rp[b0]:rp[b1]]
+        lci, lva = m.colind[rp[b0]:rp[b1]], m.vals[rp[b0]:rp[b1]] * scale
         P = 512
         def norm_step(pa, cnt, nn, nu, y):  # the spmv_norm_step contract (include/spmv.h)
             n = math.sqrt(math.fsum(pa.numpy()[:cnt]))
@@ -150,3 +150,29 @@ def test_halo_plan_pure():
     # a rank reading everything receives every other block whole
     s, r = parallel.halo_plan(bounds, [(0, 30)] * 3, 1)
     assert r == [(0, 0, 10), (2, 20, 30)]
+
+
+@pytest.mark.parametrize("scale", [1e40, 1e-40])
+def test_deferred_normalisation_rescale_gloo(scale):
+    """Deferred normalisation across ranks (reading 25): the
+    unnormalised iterate grows or shrinks by ~1e40 per step, so the exact
+    power-of-two rescale fires every few iterations on every rank alike, and
+    the exchanged blocks stay consistent; x and nu match the per-step oracle."""
+    K, world = 25, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, K, q, False, 5, scale)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m = sg.config(5, small=True)
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals * scale, m.x, K)
+    assert rc == 0
+    for rank, b, x, nu in res:
+        assert np.all(np.isfinite(x)) and np.all(np.isfinite(nu))
+        assert np.max(np.abs(x - xr)) <= 1e-10 * np.max(np.abs(xr))
+        assert np.all(np.abs(nu - nur) <= 1e-12 * nur)
