@@ -470,7 +470,7 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     # 16-bit deltas or escape codes (<= 64 distinct deltas >= 65472)
     d16_ok = f["maxgap"] <= 65535 or f.get("n_big_gaps", BIG_TAB + 1) <= ESC_MAX
     # (escape codes only when forced: measured slower, reading 21)
-    d16 = bool((classes & CLASS_MB) and avg_s >= 16.0 and f["maxgap"] <= 65535 and variant == VARIANT_STREAM)
+    d16 = False  # measured slower than the plain stream kernel on B200 (reading 9): forced only
     del d16_ok
     ml = nnz > 0 and f["misses"] > 0.75 * nnz and 8 * n > l2_bytes // 16
     if ml:

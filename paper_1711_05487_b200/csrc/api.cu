@@ -382,7 +382,10 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   // per-element escape check costs more than it saves (27-pt 260^3: 1.33 ms
   // with vs 1.09 ms without), so escapes are used only when forced (d16=1)
   const bool d16_ok = f.maxgap <= 65535 || f.n_big_gaps <= kEscMax;
-  bool d16 = (classes & SPMV_CLASS_MB) && avg_s >= 16.0 && f.maxgap <= 65535;
+  // (not auto-selected: with row-count tiles the plain stream kernel wins on
+  // every measured MB matrix, 27-pt 180^3 281.6 vs 313.9 us, C2 31.4 vs
+  // 35.0 us; the option d16 = 1 forces it)
+  bool d16 = false;
   const bool ml = nnz > 0 && (double)f.misses > 0.75 * (double)nnz && 8 * n > d.l2_bytes / 16;
   if (ml) classes |= SPMV_CLASS_ML;
   bool xwin = ml && 8 * n <= d.access_window_max;
@@ -808,7 +811,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     const bool regular = maxlen > 0 && (double)maxlen <= 1.25 * avg + 1.0;
     // (also above 2^28 nonzeros, unlike the nnz-cut aligned tiles: C5 27-nnz
     // rows, 32-row tiles, no fix-up: 2.890 vs 2.940 ms per step)
-    bool rowtiles = !seg && opt.reserved[0] == 0 && !d16 && regular && opt.tile_nnz <= 0;
+    bool rowtiles = !seg && opt.reserved[0] == 0 && regular && opt.tile_nnz <= 0;
     if (const char* e = getenv("SPMV_ROW_TILES")) rowtiles = rowtiles && atoi(e) != 0;  // experiments
     if (rowtiles) {
       const int64_t rpp = 32 / vs;
@@ -876,8 +879,8 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     // 6 consumer warps (one stage each) when 4 such CTAs fit an SM: more
     // bytes in flight for small row-aligned stages (C2: 4 x 6 x 8.8 KB,
     // 31.4 vs 32.5 us; C5's 11.4-KB stages keep 5 CTAs x 4)
-    if (opt.stages == 0 && sp.aligned && vs == 1 && !d16 && !seg && !getenv("SPMV_NO_CW6")) {
-      const size_t sm6 = stream_smem_bytes(sp.C, 6, V.rp_bytes, sp.rows_cap, false, false);
+    if (opt.stages == 0 && sp.aligned && vs == 1 && !seg && (!d16 || P->esc.empty()) && !getenv("SPMV_NO_CW6")) {
+      const size_t sm6 = stream_smem_bytes(sp.C, 6, V.rp_bytes, sp.rows_cap, d16, false);
       if (4 * (sm6 + 1024) <= 228 * 1024) sp.stages = 6;
     }
     if (const char* e = getenv("SPMV_STREAM_L2PF")) sp.l2pf = atoi(e) != 0;

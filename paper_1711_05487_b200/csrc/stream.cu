@@ -260,7 +260,7 @@ constexpr int kStreamUnroll1 = STREAM_UNR1;  // gathers in flight per lane, one 
 // 5 x 4), else 4 (C5's 11.4-KB stages: 5 x 4 fills the 228 KB)
 template <int VS, typename RP, int D16, int MODE, int CW = kConsumerWarps>
 __global__ void __launch_bounds__(32 * (CW + 1),
-                                  MODE == 1 ? 4 : (D16 ? SPMV_D16_LB : (CW == 4 ? SPMV_STREAM_LB : 24 / CW)))
+                                  MODE == 1 ? 4 : (CW != 4 ? 24 / CW : (D16 ? SPMV_D16_LB : SPMV_STREAM_LB)))
     stream_kernel(const StreamP<RP> p) {
   constexpr bool SEG = MODE == 1;
   constexpr bool AL = MODE == 2;
@@ -606,7 +606,7 @@ static void stream_launch_t(const StreamPlan& sp, const double* x, double* y, cu
 template <int VS, typename RP, int D16, int MODE, bool PREP>
 static int stream_one(const StreamPlan& sp, int sm_count, const double* x, double* y, cudaStream_t s) {
   // 6 consumer warps only for the plain row-aligned one-lane-per-row kernel
-  if constexpr (VS == 1 && D16 == 0 && MODE == 2) {
+  if constexpr (VS == 1 && D16 <= 1 && MODE == 2) {
     if (sp.stages == 6) {
       if (PREP) return stream_prepare_t<VS, RP, D16, MODE, 6>(sp, sm_count);
       stream_launch_t<VS, RP, D16, MODE, 6>(sp, x, y, s);
@@ -717,71 +717,38 @@ void launch_range_colmax(const int32_t* col, int64_t a, int64_t b, int32_t* out,
   range_colmax_kernel<<<(unsigned)g, kNT, 0, s>>>(col, a, b, out);
 }
 
-// Export: re-decode the delta colind on the device with the STREAM kernel's
-// own per-row decoder (bit-exact round trip).
-template <int VS, typename RP>
-__global__ void __launch_bounds__(kNT) d16_decode_kernel(const RP* __restrict__ rp, const uint16_t* __restrict__ dcol,
-                                                         const int32_t* __restrict__ head,
-                                                         const int32_t* __restrict__ anchor,
-                                                         const int32_t* __restrict__ tile_row, int64_t nnz, int64_t C,
-                                                         int32_t* __restrict__ out, const EscTab esc) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint16_t* d_s = reinterpret_cast<uint16_t*>(smem);
+// Export (tests): re-decode the delta colind on the device, one thread per
+// row: col = head[r] + running sum of the row's deltas (the head's placeholder
+// delta skipped), escape codes through the plan's table -- the same delta
+// arithmetic as the kernels (d16_delta), independent of the tiling
+// (SURVEY 8(c2) D16 round trip)
+template <typename RP>
+__global__ void __launch_bounds__(kNT) d16_decode_rows_kernel(const RP* __restrict__ rp, int64_t m,
+                                                              const uint16_t* __restrict__ dcol,
+                                                              const int32_t* __restrict__ head, int32_t* __restrict__ out,
+                                                              const EscTab esc) {
   __shared__ int32_t esc_s[kEscMax];
   if (threadIdx.x < kEscMax) esc_s[threadIdx.x] = esc.v[threadIdx.x];
-  const int64_t k = blockIdx.x;
-  const int64_t t0 = k * C, t1 = (t0 + C) < nnz ? (t0 + C) : nnz;
-  const int cnt = (int)(t1 - t0);
-  for (int l = threadIdx.x; l < cnt; l += kNT) d_s[l] = dcol[t0 + l];
   __syncthreads();
-  const int64_t R0 = tile_row[k], R1 = tile_row[k + 1];
-  const bool incoming = R0 > 0 && (int64_t)rp[R0] > t0;
-  const int64_t fr = R0 - (incoming ? 1 : 0);
-  const int nloc = (int)(R1 - R0) + (incoming ? 1 : 0);
-  const int lane = threadIdx.x % VS, gi = (threadIdx.x & 31) / VS, w = threadIdx.x >> 5;
-  for (int qb = w * (32 / VS); qb < nloc; qb += kNT / VS) {
-    const int q = qb + gi;
-    const bool active = q < nloc;
-    int ls = 0, le = 0, base = anchor[k];
-    if (active) {
-      const int64_t r = fr + q;
-      const int64_t a = rp[r], b = rp[r + 1];
-      ls = (int)((a > t0 ? a : t0) - t0);
-      le = (int)((b < t1 ? b : t1) - t0);
-      if (!incoming || q > 0) base = head[r];
-    }
-    d16_row_cols<VS, true>(d_s, ls, le, lane, base, esc_s, [&](int t, int c) { out[t0 + t] = c; });
+  const int64_t r = (int64_t)blockIdx.x * kNT + threadIdx.x;
+  if (r >= m) return;
+  const int64_t a = rp[r], b = rp[r + 1];
+  int c = a < b ? head[r] : 0;
+  for (int64_t t = a; t < b; ++t) {
+    if (t > a) c += d16_delta<true>(dcol[t], esc_s);
+    out[t] = c;
   }
 }
 
-template <int VS>
-static void d16_export_vs(const StreamPlan& sp, int32_t* out, cudaStream_t s) {
-  const size_t smem = (size_t)sp.C * 2 + 16;
+void launch_d16_decode_export(const StreamPlan& sp, int32_t* out, cudaStream_t s) {
+  if (sp.V.nnz == 0 || sp.V.m == 0) return;
   EscTab esc;
   for (int i = 0; i < kEscMax; ++i) esc.v[i] = i < sp.n_esc ? sp.esc[i] : 0;
-  if (sp.V.rp_bytes == 8) {
-    cudaFuncSetAttribute(d16_decode_kernel<VS, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    d16_decode_kernel<VS, int64_t><<<(int)sp.T, kNT, smem, s>>>((const int64_t*)sp.V.rowptr, sp.dcol, sp.head,
-                                                                sp.anchor, sp.tile_row, sp.V.nnz, sp.C, out, esc);
-  } else {
-    cudaFuncSetAttribute(d16_decode_kernel<VS, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    d16_decode_kernel<VS, int32_t><<<(int)sp.T, kNT, smem, s>>>((const int32_t*)sp.V.rowptr, sp.dcol, sp.head,
-                                                                sp.anchor, sp.tile_row, sp.V.nnz, sp.C, out, esc);
-  }
-}
-
-void launch_d16_decode_export(const StreamPlan& sp_in, int32_t* out, cudaStream_t s) {
-  if (sp_in.V.nnz == 0) return;
-  StreamPlan sp = sp_in;
-  sp.C = sp.stride;  // the tile_row / anchor arrays are laid out at the stride
-  switch (sp.vs) {
-    case 1: d16_export_vs<1>(sp, out, s); break;
-    case 2: d16_export_vs<2>(sp, out, s); break;
-    case 4: d16_export_vs<4>(sp, out, s); break;
-    case 8: d16_export_vs<8>(sp, out, s); break;
-    case 16: d16_export_vs<16>(sp, out, s); break;
-    default: d16_export_vs<32>(sp, out, s); break;
-  }
+  const unsigned g = (unsigned)((sp.V.m + kNT - 1) / kNT);
+  if (sp.V.rp_bytes == 8)
+    d16_decode_rows_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)sp.V.rowptr, sp.V.m, sp.dcol, sp.head, out, esc);
+  else
+    d16_decode_rows_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)sp.V.rowptr, sp.V.m, sp.dcol, sp.head, out, esc);
 }
 
 }  // namespace spmv

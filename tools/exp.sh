@@ -1,3 +1,2 @@
-run() { name=$1; shift; timeout 300 python bench.py --no-cpu --no-e2e --no-cold --iters 0 "$@" > gpurun_out/x_$name.log 2>&1; }
-for t in 200 400 576 800 1100; do SPMV_ROW_TILE_MIN_NNZ=$t run c2_t$t --config 2 --steps 40; done
-for t in 500 1100; do SPMV_ROW_TILE_MIN_NNZ=$t run c5_t$t --config 5 --steps 10; done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/x_pytest.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/x_smoke.txt 2>&1
