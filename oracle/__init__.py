@@ -466,8 +466,8 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     mb = ws > l2_bytes // 2
     if mb and not (classes & CLASS_IMB):
         classes |= CLASS_MB
-    # MB delta colind (reading 9): rows averaging >= 16 nonzeros,
-    # 16-bit deltas or escape codes (<= 64 distinct deltas >= 65472)
+    # MB delta colind (reading 9): 16-bit deltas or escape codes
+    # (<= 64 distinct deltas >= 65472) are possible, but only when forced
     d16_ok = f["maxgap"] <= 65535 or f.get("n_big_gaps", BIG_TAB + 1) <= ESC_MAX
     # (escape codes only when forced: measured slower, reading 21)
     d16 = False  # measured slower than the plain stream kernel on B200 (reading 9): forced only

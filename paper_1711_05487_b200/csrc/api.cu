@@ -372,12 +372,9 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   if (avg_s <= 4) classes |= SPMV_CLASS_CMP;
   if (ws > d.l2_bytes / 2 && !(classes & SPMV_CLASS_IMB)) classes |= SPMV_CLASS_MB;
   // MB -> delta colind: implemented and bit-exact, but on B200 the
-  // decode costs about what the 2 B/nnz save on short rows (branch-free
-  // decode, launch bound 5: C2 33.0 us at tile 896 vs 33.1 us without; the
-  // stream kernel is bound by the bytes its stages keep in flight, and a
-  // D16 tile carries fewer) but pays on long regular rows (27-pt 180^3:
-  // 352 vs 378 us), so it is auto-selected for MB rows averaging >= 16
-  // nonzeros. Large deltas can be escape-coded when
+  // plain stream kernel is faster on every measured MB matrix (see below;
+  // DESIGN.md reading 9), so deltas are used only when forced. Large deltas
+  // can be escape-coded when
   // at most kEscMax distinct values exceed kEsc0, but the
   // per-element escape check costs more than it saves (27-pt 260^3: 1.33 ms
   // with vs 1.09 ms without), so escapes are used only when forced (d16=1)
