@@ -1,3 +1,5 @@
+"""D16 vs plain stream on a 27-point 180^3 stencil (16-bit gaps: D16-eligible;
+DESIGN.md reading 9). Experiment tool: python tools/exp_d16_27.py"""
 import sys, os, json
 sys.path.insert(0, "/root/repo")
 import numpy as np, torch
