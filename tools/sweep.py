@@ -78,6 +78,9 @@ def main():
     tiles = (256, 384, 512, 640, 768, 1024) if not a.quick else (512, 640, 768)
     stages = (4, 8) if not a.quick else (4,)
     d16s = (0, 1) if a.config in (1, 2) else (0,)
+    # the plan's own tile rule (row-count tiles on regular rows, 4/6 consumer warps)
+    grid.append(dict(force_variant="stream", force_vs=1))
+    grid.append(dict(force_variant="stream", force_vs=1, d16=1))
     for vs, t, sg_, d in itertools.product(svs, tiles, stages, d16s):
         grid.append(dict(force_variant="stream", force_vs=vs, tile_nnz=t, stages=sg_, d16=d))
     for t in tiles:
