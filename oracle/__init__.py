@@ -16,6 +16,8 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``) -- no function is
   spmv            dense brute-force matvec, identity/diagonal exact, A e_j =
                   column j exact, stencil A*1 closed forms, dyadic exactness
                   vs Fraction arithmetic, scipy csr @ x, Neumaier self-check
+  spmv_neumaier   exact Fraction row sums on cancellation rows (the plain sum
+                  fails them), the compensated-summation error bound
   power_iter      monotone nu_k (k>=1) for symmetric A, nu <= lambda_max closed
                   form, nu -> lambda_max vs numpy eigvalsh on a small grid
   shard_bounds    SPEC S:254-255 examples, linear-scan definition, coverage
@@ -28,7 +30,10 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``) -- no function is
   classify_profile SPEC S:469-474 examples, strictness, monotonicity in P_ML
   table1          SPEC S:415-417 worked rows, diagonal closed form, brute-force per-row loops
   d16 encode/dec  SPEC S:134-136 widths, round trip, stencil gap closed forms
-  features        SPEC S:415 sd example, stencil closed forms
+  features        SPEC S:415 sd example, stencil closed forms, short-row
+                  statistics / n_empty / long rows vs numpy incl. L_split edges
+  d8 dict/enc/dec stencil dictionaries from the grid geometry (7-pt: 10, 27-pt:
+                  15 codes), hand example, 256/257 and 255/256 limits, round trip
   select          hand-evaluated rule table on the configs' closed-form features
 """
 from __future__ import annotations
@@ -81,6 +86,11 @@ def _lib():
         L.oracle_d16_encode_esc.restype = ctypes.c_int
         L.oracle_d16_decode_esc.argtypes = [i64, vp, vp, vp, vp, vp]
         L.oracle_tile_anchor.argtypes = [vp, i64, i64, i64, vp]
+        L.oracle_d8_dict.argtypes = [i64, vp, vp, vp]
+        L.oracle_d8_dict.restype = ctypes.c_int
+        L.oracle_d8_encode.argtypes = [i64, vp, vp, vp, vp, vp]
+        L.oracle_d8_encode.restype = ctypes.c_int
+        L.oracle_d8_decode.argtypes = [i64, vp, vp, vp, vp]
         _LIB = L
     return _LIB
 
@@ -352,6 +362,42 @@ def d16_decode(rowptr, dcol, head):
     _lib().oracle_d16_decode(n, _p(rp), _p(np.ascontiguousarray(dcol, np.uint16)),
                              _p(np.ascontiguousarray(head, np.int32)), _p(out))
     return out[:nnz]
+
+
+def d8_dict(rowptr, colind):
+    """Distinct row-relative deltas in ascending order (DESIGN.md reading 26;
+    P:589-597): head delta colind[rowptr[i]] - i, in-row gaps
+    colind[j] - colind[j-1]. Returns (count, dict) with count = 257 (and a
+    partial dict) when more than 256 distinct deltas exist."""
+    rp, ci = _rp64(rowptr), _c32(colind)
+    d = np.zeros(257, np.int64)
+    nd = _lib().oracle_d8_dict(rp.size - 1, _p(rp), _p(ci), _p(d))
+    return nd, d[:min(nd, 256)].copy()
+
+
+def d8_encode(rowptr, colind):
+    """Dictionary-coded 8-bit deltas. Returns (dict int64[nd], codes u8[nnz],
+    rlen u8[n]) or None when not D8-codable (> 256 distinct deltas or a row
+    longer than 255)."""
+    rp, ci = _rp64(rowptr), _c32(colind)
+    n, nnz = rp.size - 1, int(rp[-1])
+    d = np.zeros(256, np.int64)
+    codes = np.zeros(max(nnz, 1), np.uint8)
+    rlen = np.zeros(max(n, 1), np.uint8)
+    nd = _lib().oracle_d8_encode(n, _p(rp), _p(ci), _p(d), _p(codes), _p(rlen))
+    if nd == 0 and nnz > 0:
+        return None
+    return d[:nd].copy(), codes[:nnz], rlen[:n]
+
+
+def d8_decode(dict_, codes, rlen):
+    rl = np.ascontiguousarray(rlen, np.uint8)
+    cd = np.ascontiguousarray(codes, np.uint8)
+    d = np.zeros(256, np.int64)
+    d[:len(dict_)] = dict_
+    out = np.empty(max(cd.size, 1), np.int32)
+    _lib().oracle_d8_decode(rl.size, _p(rl), _p(cd), _p(d), _p(out))
+    return out[:cd.size]
 
 
 def tile_anchor(colind, C):

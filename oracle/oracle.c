@@ -406,3 +406,76 @@ void oracle_d16_decode(int64_t n, const int64_t* rowptr, const uint16_t* dcol, c
 void oracle_tile_anchor(const int32_t* colind, int64_t nnz, int64_t C, int64_t T, int32_t* anchor) {
   for (int64_t k = 0; k < T; ++k) anchor[k] = k * C < nnz ? colind[k * C] : 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * Dictionary-coded 8-bit column deltas ("D8"; the MB-class optimisation of
+ * Sec. III-E: "8- or 16-bit deltas wherever possible, but never
+ * both"; Table II; reading 26).
+ * Row-relative deltas of row i (row id i of the matrix) and its nonzeros
+ * j = rowptr[i] .. rowptr[i+1]-1:
+ *     delta_j = colind[j] - i               (j = rowptr[i], the row head)
+ *     delta_j = colind[j] - colind[j-1]     (j > rowptr[i])
+ * dict = the distinct deltas in ascending order. The matrix is D8-codable iff
+ * |dict| <= 256 (one byte per code) and every row has <= 255 nonzeros (one
+ * byte per row length). code_j = the index of delta_j in dict; rlen[i] =
+ * rowptr[i+1] - rowptr[i]. Decode: c = i; c += dict[code_j]; colind[j] = c.
+ *
+ * oracle_d8_dict: fills dict (>= 256 entries) and returns |dict|, or 257 as
+ * soon as a 257th distinct delta appears. Kept as a sorted array with plain
+ * insertion (at most 257 entries).
+ * ------------------------------------------------------------------------- */
+static int d8_find(const int64_t* dict, int nd, int64_t v) {
+  int lo = 0, hi = nd; /* first index with dict[idx] >= v */
+  while (lo < hi) {
+    int mid = (lo + hi) / 2;
+    if (dict[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+int oracle_d8_dict(int64_t n, const int64_t* rowptr, const int32_t* colind, int64_t* dict) {
+  int nd = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t j = rowptr[i]; j < rowptr[i + 1]; ++j) {
+      int64_t d = j == rowptr[i] ? (int64_t)colind[j] - i : (int64_t)colind[j] - (int64_t)colind[j - 1];
+      int at = d8_find(dict, nd, d);
+      if (at < nd && dict[at] == d) continue;
+      if (nd == 256) return 257;
+      for (int t = nd; t > at; --t) dict[t] = dict[t - 1];
+      dict[at] = d;
+      ++nd;
+    }
+  }
+  return nd;
+}
+
+/* Encode: returns |dict| (codes and rlen written) or 0 when not D8-codable
+ * (|dict| > 256 or a row longer than 255). dict: 256 entries. */
+int oracle_d8_encode(int64_t n, const int64_t* rowptr, const int32_t* colind, int64_t* dict, uint8_t* codes,
+                     uint8_t* rlen) {
+  for (int64_t i = 0; i < n; ++i)
+    if (rowptr[i + 1] - rowptr[i] > 255) return 0;
+  int nd = oracle_d8_dict(n, rowptr, colind, dict);
+  if (nd > 256) return 0;
+  for (int64_t i = 0; i < n; ++i) {
+    rlen[i] = (uint8_t)(rowptr[i + 1] - rowptr[i]);
+    for (int64_t j = rowptr[i]; j < rowptr[i + 1]; ++j) {
+      int64_t d = j == rowptr[i] ? (int64_t)colind[j] - i : (int64_t)colind[j] - (int64_t)colind[j - 1];
+      codes[j] = (uint8_t)d8_find(dict, nd, d);
+    }
+  }
+  return nd;
+}
+
+/* Decode (rowptr from the row lengths: rowptr[i+1] = rowptr[i] + rlen[i]). */
+void oracle_d8_decode(int64_t n, const uint8_t* rlen, const uint8_t* codes, const int64_t* dict,
+                      int32_t* col_out) {
+  int64_t j = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t c = i;
+    for (int t = 0; t < rlen[i]; ++t, ++j) {
+      c += dict[codes[j]];
+      col_out[j] = (int32_t)c;
+    }
+  }
+}

@@ -191,7 +191,7 @@ struct Shard {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // iterated mode
-  double* allpart = nullptr;  // G * kNormPartials
+  double* allpart = nullptr;  // 2 x G * kNormPartials (iteration parity: double-buffered)
   double* x2 = nullptr;       // second x replica (deferred-normalisation ping-pong)
   double* sq = nullptr;       // per-tile sums of y^2 (fused norm partials, row-aligned STREAM)
   double* nn = nullptr;       // running norm + rescale factor (norm.cu)
@@ -638,10 +638,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     rp0 = rp_at(rp_h, rp_bytes, 0);
     rpn = rp_at(rp_h, rp_bytes, n_rows);
   }
-  if (opt.validate || true) {
-    if (rp0 != 0) fail_csr(1, 0);
-    if (rpn != nnz) fail_csr(2, n_rows);
-  }
+  // (always checked, even with validate = 0: the shard bounds and every
+  // size below are derived from rowptr[0] and rowptr[n])
+  if (rp0 != 0) fail_csr(1, 0);
+  if (rpn != nnz) fail_csr(2, n_rows);
   P->bounds.assign(ngpus + 1, 0);
   if (ngpus == 1) { P->bounds[1] = n_rows; }
   else shard_bounds_host(n_rows, rp_h, rp_bytes, ngpus, P->bounds.data());
@@ -1157,7 +1157,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     }
     s.x = s.alloc<double>((size_t)n_cols);
     s.y = s.alloc<double>((size_t)s.m);
-    s.allpart = s.alloc<double>((size_t)kNormPartials * ngpus);
+    s.allpart = s.alloc<double>((size_t)2 * kNormPartials * ngpus);
   }
   for (auto& s : P->shards) {
     ck(cudaStreamSynchronize(s.stream), "structures");
@@ -1396,6 +1396,14 @@ int host_pipe_run(spmv_plan p, Shard& s, const double* x, double* y) {
   return n;
 }
 
+// the async entry points take device pointers of the shard's device only (a
+// host pointer would fault inside the kernel instead of returning an error)
+void require_dev(const Shard& s, const void* p, const char* what) {
+  int dev = -1;
+  if (!is_device_ptr(p, &dev) || dev != s.dev)
+    fail(SPMV_E_ARG, "%s must be a device pointer of device %d on the asynchronous path", what, s.dev);
+}
+
 // run the plan on x (device pointer valid on every shard's device or the
 // shards' replicas) into y (per-shard outputs)
 void execute_impl(spmv_plan p, const double* x, double* y, bool sync) {
@@ -1490,6 +1498,8 @@ int spmv_execute_stage(spmv_plan p, const double* x, double* y, int stage) {
     if (!p || !x || !y || stage < 0 || stage > 2) fail(SPMV_E_ARG, "bad argument");
     if (p->shards.size() != 1) fail(SPMV_E_ARG, "spmv_execute_async/_stage need a single-shard plan");
     Shard& s = p->shards[0];
+    require_dev(s, x, "x");
+    require_dev(s, y, "y");
     count_launches(p->launch(s, x, y, stage), "spmv");
   });
 }
@@ -1567,6 +1577,9 @@ int spmv_execute_norm(spmv_plan p, const double* x, double* y, double* partials)
   return guard([&] {
     if (!p || !x || !y || !partials || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
     Shard& s = p->shards[0];
+    require_dev(s, x, "x");
+    require_dev(s, y, "y");
+    require_dev(s, partials, "partials");
     count_launches(spmv_with_partials(p, s, x, y, partials), "spmv + norm partials");
   });
 }
@@ -1601,12 +1614,19 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
       nxt[g] = s.x2;
     }
     for (int k = 0; k < iters; ++k) {
+      // partials of iteration k live in half (k & 1) of every shard's allpart:
+      // shard h may run ahead of a peer that has not yet copied h's partials
+      // of iteration k (non-neighbour shards never wait on each other's x
+      // halo), but not by two iterations -- its norm step k+1 waits for every
+      // peer's partials of k+1, which follow that peer's copies of k
+      const size_t half = (size_t)(k & 1) * G * kNormPartials;
       for (int g = 0; g < G; ++g) {
         Shard& s = p->shards[g];
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
         set_xwin(p, s, cur[g]);
-        count_launches(spmv_with_partials(p, s, cur[g], nxt[g] + s.row0, s.allpart + (size_t)g * kNormPartials),
-                       "spmv + norm partials");
+        count_launches(
+            spmv_with_partials(p, s, cur[g], nxt[g] + s.row0, s.allpart + half + (size_t)g * kNormPartials),
+            "spmv + norm partials");
         ck(cudaEventRecord(s.ev_part, s.stream), "event");
       }
       for (int g = 0; g < G; ++g) {
@@ -1616,11 +1636,13 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
           if (h == g) continue;
           Shard& t = p->shards[h];
           ck(cudaStreamWaitEvent(s.stream, t.ev_part, 0), "wait");
-          ck(cudaMemcpyPeerAsync(s.allpart + (size_t)h * kNormPartials, s.dev, t.allpart + (size_t)h * kNormPartials,
-                                 t.dev, kNormPartials * 8, s.stream), "partials exchange");
+          ck(cudaMemcpyPeerAsync(s.allpart + half + (size_t)h * kNormPartials, s.dev,
+                                 t.allpart + half + (size_t)h * kNormPartials, t.dev, kNormPartials * 8, s.stream),
+             "partials exchange");
         }
-        count_launches(launch_norm_step(s.allpart, G * kNormPartials, s.nn, s.nu + k, nxt[g] + s.row0, s.m, s.stream),
-                       "norm step");
+        count_launches(
+            launch_norm_step(s.allpart + half, G * kNormPartials, s.nn, s.nu + k, nxt[g] + s.row0, s.m, s.stream),
+            "norm step");
         ck(cudaEventRecord(s.ev_x, s.stream), "event");
       }
       if (G > 1) {

@@ -147,6 +147,9 @@ void launch_d16_decode_export(const StreamPlan& sp, int32_t* out, cudaStream_t s
 // entries (levels of the hierarchical reduce-by-key live after the T carries)
 int64_t fixup_capacity(int64_t T);
 int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int64_t max_run, cudaStream_t s);
+// fix-up of the carries of one tile range (crow/cval offset to the range start,
+// T = its length): adds to y, uses no scratch, any run length
+int launch_fixup_range(const int32_t* crow, const double* cval, int64_t T, double* y, cudaStream_t s);
 void launch_rebase(void* rowptr, int rp_bytes, int64_t count, int64_t base, cudaStream_t s);
 
 // ---- length bins (bins.cu) ----------------------------------------------------

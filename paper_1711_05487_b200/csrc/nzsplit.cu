@@ -296,7 +296,7 @@ int launch_nz_range(const NzPlan& z, const double* x, double* y, int64_t k0, int
 }
 int launch_nz_fixup_range(const NzPlan& z, double* y, int64_t k0, int64_t k1, cudaStream_t s) {
   if (k1 <= k0 || z.T <= 1) return 0;
-  return launch_fixup(z.carry_row + k0, z.carry_val + k0, k1 - k0, y, 0, z.max_run, s);
+  return launch_fixup_range(z.carry_row + k0, z.carry_val + k0, k1 - k0, y, s);
 }
 
 int launch_nz_plan(const NzPlan& z, const double* x, double* y, int stage, cudaStream_t s) {

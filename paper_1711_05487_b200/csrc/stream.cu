@@ -682,7 +682,7 @@ int launch_stream_range(const StreamPlan& sp_in, const double* x, double* y, int
   int n = 1;
   // a carry run crossing k0 is split between two ranges' fix-ups: both add
   // to y in stream order (additive), so the row is complete after the later one
-  if (sp.need_fixup) n += launch_fixup(sp.carry_row + k0, sp.carry_val + k0, k1 - k0, y, 0, sp.max_run, s);
+  if (sp.need_fixup) n += launch_fixup_range(sp.carry_row + k0, sp.carry_val + k0, k1 - k0, y, s);
   return n;
 }
 

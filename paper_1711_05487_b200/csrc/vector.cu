@@ -303,6 +303,17 @@ __global__ void __launch_bounds__(kNT) fixup_seg_kernel(const int32_t* __restric
   if (lane == 0) y[rr] = set ? acc : y[rr] + acc;
 }
 
+// Carries [0, T) of a tile RANGE (pointers offset by the range start): always
+// the single-launch forward walk, which needs no scratch -- the hierarchical
+// path keeps its levels and counter after the plan's T carries, i.e. inside
+// the next range's carries when called with offset pointers. A run of any
+// length is summed by one warp walking it 256 carries per step.
+int launch_fixup_range(const int32_t* crow, const double* cval, int64_t T, double* y, cudaStream_t s) {
+  if (T <= 0) return 0;
+  launch_pdl(fixup_seg_kernel, dim3((unsigned)((T + kNT - 1) / kNT)), dim3(kNT), 0, s, crow, cval, T, y, 0);
+  return 1;
+}
+
 int launch_fixup(int32_t* crow, double* cval, int64_t T, double* y, int set, int64_t max_run, cudaStream_t s) {
   if (T <= 0) return 0;
   if (max_run <= kWarpRunMax) {

@@ -29,6 +29,7 @@ injectable so the orchestration is tested with the ``gloo`` backend on CPU.
 """
 from __future__ import annotations
 
+from contextlib import nullcontext
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
 
@@ -42,6 +43,10 @@ class ShardSteps:
     unit: Callable[[object, object, object], None]    # (y, nn[2], x_out): x_out = y / nn[0]
     # optional fused spmv + partials (x_full, y_block, partials_local)
     spmv_partials: Optional[Callable[[object, object, object], None]] = None
+    # optional context-manager factory making the steps' stream the current
+    # one, so the collectives (issued on the current stream) are ordered with
+    # the native steps (issued on the plan's stream)
+    stream: Optional[Callable[[], object]] = None
 
 
 def halo_plan(bounds: Sequence[int], needs: Sequence[Sequence[int]], rank: int):
@@ -104,19 +109,20 @@ def iterate(dist, steps: ShardSteps, bounds: Sequence[int], rank: int, world: in
     """
     P = partials_local.numel()
     b0, b1 = int(bounds[rank]), int(bounds[rank + 1])
-    nn.zero_()
-    cur, nxt = x_full, x_alt
-    for k in range(iters):
-        if steps.spmv_partials is not None:
-            steps.spmv_partials(cur, nxt[b0:b1], partials_local)
-        else:
-            steps.spmv(cur, nxt[b0:b1])
-            steps.partials(nxt[b0:b1], partials_local)
-        dist.all_gather_into_tensor(partials_all, partials_local, group=group)
-        steps.norm_step(partials_all, world * P, nn, nu_hist[k:k + 1], nxt[b0:b1])
-        exchange_x(dist, bounds, rank, world, nxt, halo, group)
-        cur, nxt = nxt, cur
-    steps.unit(cur, nn, x_full)
+    with steps.stream() if steps.stream is not None else nullcontext():
+        nn.zero_()
+        cur, nxt = x_full, x_alt
+        for k in range(iters):
+            if steps.spmv_partials is not None:
+                steps.spmv_partials(cur, nxt[b0:b1], partials_local)
+            else:
+                steps.spmv(cur, nxt[b0:b1])
+                steps.partials(nxt[b0:b1], partials_local)
+            dist.all_gather_into_tensor(partials_all, partials_local, group=group)
+            steps.norm_step(partials_all, world * P, nn, nu_hist[k:k + 1], nxt[b0:b1])
+            exchange_x(dist, bounds, rank, world, nxt, halo, group)
+            cur, nxt = nxt, cur
+        steps.unit(cur, nn, x_full)
 
 
 def exchange_only(dist, bounds: Sequence[int], rank: int, world: int, x_full, partials_local, partials_all,
@@ -137,8 +143,16 @@ class NoDist:
 
 
 def native_steps(plan) -> ShardSteps:
-    """ShardSteps backed by a libspmv plan (device pointers, plan stream)."""
+    """ShardSteps backed by a libspmv plan (device pointers, plan stream).
+    iterate() runs under torch.cuda.stream(<the plan stream>), so NCCL
+    collectives and torch ops are enqueued in order with the native steps."""
+    import torch
+
+    def stream():
+        return torch.cuda.stream(torch.cuda.ExternalStream(plan.stream(), device=torch.cuda.current_device()))
+
     return ShardSteps(
+        stream=stream,
         spmv=lambda x, y: plan.execute_async(x, y),
         partials=lambda y, p: plan.norm_partials(y, p),
         norm_step=lambda pa, cnt, nn, nu, y: plan.norm_step(pa, cnt, nn, nu, y),

@@ -265,7 +265,9 @@ def test_row_count_tiles(lens, vs):
 
 @pytest.mark.parametrize("extra", [{}, {"no_aligned": 1}, {"d16": 1}, {"force_vs": 4}, {"tile_nnz": 0}])
 @pytest.mark.parametrize("name,lens", [("uniform", [7] * 40000), ("mixed", ([3, 0, 9, 27, 1, 64] * 8000)),
-                                       ("long_rows", [5] * 20000 + [9000] * 3 + [5] * 20000)])
+                                       ("long_rows", [5] * 20000 + [9000] * 3 + [5] * 20000),
+                                       # a row cut into > 2048 tiles: the range fix-ups
+                                       ("huge_row", [5] * 20000 + [1_100_000] + [5] * 20000)])
 def test_pipelined_host_execute(monkeypatch, name, lens, extra):
     # host x / host y through a STREAM plan: tile blocks overlapped with the
     # x upload and the y download (api.cu host_pipe_*); rows cut at block
@@ -274,7 +276,7 @@ def test_pipelined_host_execute(monkeypatch, name, lens, extra):
     monkeypatch.setenv("SPMV_HOST_PIPE_BLOCKS", "7")
     g = np.random.default_rng(11)
     lens = np.asarray(lens, np.int64)
-    m = sg.from_lengths(lens, lens.size, g, sg.MODE_U11, sg.MODE_U11)
+    m = sg.from_lengths(lens, max(lens.size, int(lens.max())), g, sg.MODE_U11, sg.MODE_U11)
     kw = {"tile_nnz": 512, "seg": 0}
     kw.update(extra)  # tile_nnz 0: the plan's own tile rule (row-count tiles on regular rows)
     p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="stream", **kw)
@@ -294,7 +296,10 @@ def test_pipelined_host_execute(monkeypatch, name, lens, extra):
 
 @pytest.mark.parametrize("hot", [0, 256])
 @pytest.mark.parametrize("name,lens", [("powerlaw", None), ("empty_runs", ([0] * 300 + [700, 3, 0, 5]) * 60),
-                                       ("long_rows", [5] * 20000 + [9000] * 3 + [0] * 500 + [5] * 20000)])
+                                       ("long_rows", [5] * 20000 + [9000] * 3 + [0] * 500 + [5] * 20000),
+                                       # rows cut into > 2048 warp tiles, one crossing several pipeline ranges:
+                                       # the range fix-ups must not use the plan-wide hierarchical scratch
+                                       ("huge_rows", [5] * 20000 + [700_000] + [3] * 3000 + [650_000] + [5] * 20000)])
 def test_pipelined_host_execute_nnzsplit(monkeypatch, name, lens, hot):
     # nnz_split ranges with the y download overlapped: range b's carries are
     # added after range b+1 (rows are assigned where they end); every row,
@@ -305,7 +310,7 @@ def test_pipelined_host_execute_nnzsplit(monkeypatch, name, lens, hot):
     if lens is None:
         lens = np.minimum((g.pareto(1.2, size=60000) * 3).astype(np.int64), 20000)
     lens = np.asarray(lens, np.int64)
-    m = sg.from_lengths(lens, lens.size, g, sg.MODE_U11, sg.MODE_U11)
+    m = sg.from_lengths(lens, max(lens.size, int(lens.max())), g, sg.MODE_U11, sg.MODE_U11)
     p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="nnzsplit", hot_x=hot)
     yh = p.execute(m.x, np.full(m.n, np.nan))
     assert_bound(yh, m)

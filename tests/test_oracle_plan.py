@@ -478,3 +478,126 @@ def test_table1_bruteforce_rows():
             assert abs(t["scatter_sd"] - np.std(scs)) <= 1e-12
             assert abs(t["clustering_avg"] - np.mean(cls)) <= 1e-12
         assert t["misses_avg"] == miss / (rp.size - 1), name
+
+
+# ---- D8: dictionary-coded 8-bit deltas (reading 26) ------
+def _d8_stencil_dict(n, pts):
+    """Closed form from the stencil geometry (not the delta formula): heads =
+    -(smallest present neighbour offset) over the boundary cases; in-row gaps
+    between consecutive present offsets (7-pt: sums of adjacent base gaps; 27-pt:
+    1 inside an x-run, n + xmin - xmax on a y step, n^2 + (ymin-ymax) n +
+    (xmin-xmax) on a z step, with xmin-xmax, ymin-ymax in {-2, -1})."""
+    if pts == 7:
+        heads = {-n * n, -n, -1, 0}
+        gaps = {1, n - 1, n, n * n - n, n * n - 1, n * n}
+    else:
+        heads = {-(a * n * n + b * n + c) for a in (0, 1) for b in (0, 1) for c in (0, 1)}
+        gaps = {1, n - 2, n - 1} | {n * n + dy * n + dx for dy in (-2, -1) for dx in (-2, -1)}
+    return sorted(heads | gaps)
+
+
+@pytest.mark.parametrize("n", [3, 4, 7, 16])
+@pytest.mark.parametrize("pts", [7, 27])
+def test_d8_stencil_dictionary_closed_form(n, pts):
+    m = sg.stencil(n, pts)
+    want = _d8_stencil_dict(n, pts)
+    nd, d = oracle.d8_dict(m.rowptr, m.colind)
+    assert nd == len(want) and d.tolist() == want
+    enc = oracle.d8_encode(m.rowptr, m.colind)
+    assert enc is not None and enc[0].tolist() == want
+    assert np.array_equal(enc[2], np.diff(m.rowptr.astype(np.int64)))
+    assert np.array_equal(oracle.d8_decode(*enc), m.colind)  # round trip (S:148)
+
+
+def test_d8_config_dictionaries():
+    # C2 7-pt 128^3: 10 codes; C5 27-pt 384^3: 15 codes (closed forms above)
+    assert _d8_stencil_dict(128, 7) == [-16384, -128, -1, 0, 1, 127, 128, 16256, 16383, 16384]
+    assert len(_d8_stencil_dict(384, 27)) == 15
+    m = sg.stencil(128, 7, rows=(0, 40000))
+    assert oracle.d8_dict(m.rowptr, m.colind)[0] <= 10
+    # C1 (uniform random columns): far more than 256 distinct deltas
+    m1 = sg.config(1)
+    assert oracle.d8_dict(m1.rowptr, m1.colind)[0] == 257 and oracle.d8_encode(m1.rowptr, m1.colind) is None
+
+
+def test_d8_hand_example_and_limits():
+    # rows: [2, 5, 6], [], [0, 3] (row ids 0, 1, 2): deltas 2,3,1 | - | -2,3
+    rp = rp_of([3, 0, 2])
+    ci = np.array([2, 5, 6, 0, 3], np.int32)
+    d, codes, rlen = oracle.d8_encode(rp, ci)
+    assert d.tolist() == [-2, 1, 2, 3]
+    assert codes.tolist() == [2, 3, 1, 0, 3] and rlen.tolist() == [3, 0, 2]
+    assert oracle.d8_decode(d, codes, rlen).tolist() == ci.tolist()
+    # diagonal: one delta (0), every code 0
+    n = 50
+    d, codes, _ = oracle.d8_encode(np.arange(n + 1), np.arange(n, dtype=np.int32))
+    assert d.tolist() == [0] and not codes.any()
+    # exactly 256 distinct head deltas: codable; 257: not
+    for k, ok in ((256, True), (257, False)):
+        ci = (np.arange(k) * 2).astype(np.int32)  # row i -> column 2i: head delta i
+        enc = oracle.d8_encode(np.arange(k + 1), ci)
+        assert (enc is not None) == ok
+        if ok:
+            assert enc[0].tolist() == list(range(k)) and enc[1].tolist() == list(range(k))
+    # row lengths: 255 codable, 256 not (u8 lengths), even with 2 distinct deltas
+    for L_, ok in ((255, True), (256, False)):
+        enc = oracle.d8_encode(rp_of([L_]), np.arange(L_, dtype=np.int32))
+        assert (enc is not None) == ok
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_d8_round_trip_random_banded(seed):
+    # banded rows drawn from a small gap alphabet: codable, decode(encode) == colind
+    g = np.random.default_rng(seed)
+    n = 3000
+    lens = g.integers(0, 30, n)
+    rp = rp_of(lens)
+    ci = np.empty(int(rp[-1]), np.int32)
+    for i in range(n):
+        if lens[i] == 0:
+            continue
+        steps = g.choice([1, 2, 7, 40, 333], lens[i])
+        steps[0] = g.integers(-min(i, 60), 60)
+        ci[rp[i]:rp[i + 1]] = i + np.cumsum(steps)
+    enc = oracle.d8_encode(rp, ci)
+    nd = oracle.d8_dict(rp, ci)[0]
+    if nd > 256:
+        assert enc is None
+        return
+    d, codes, rlen = enc
+    assert np.all(np.diff(d) > 0)  # strictly ascending, distinct
+    assert np.array_equal(oracle.d8_decode(d, codes, rlen), ci)
+
+
+# ---- short-row statistics and empty rows (Table I nnz stats over len <= L_split) ----
+@pytest.mark.parametrize("seed", range(4))
+def test_features_short_row_stats_vs_numpy(seed):
+    g = np.random.default_rng(seed)
+    n = 2000
+    lens = g.choice([0, 0, 1, 3, 9, 40, 700], n).astype(np.int64)
+    # L_split edge rows: exactly 4096 (short) and 4097 (long), plus longer ones
+    lens[g.choice(n, 6, replace=False)] = [4096, 4096, 4097, 4097, 5000, 9000]
+    rp = rp_of(lens)
+    ci = np.concatenate([np.arange(L, dtype=np.int32) for L in lens])
+    f = oracle.features(rp, ci, n_cols=10000)
+    short = lens[lens <= 4096]
+    assert f["n_short"] == short.size and f["max_short"] == short.max()
+    assert f["n_empty"] == int((lens == 0).sum())
+    assert f["n_long"] == int((lens > 4096).sum()) and f["nnz_long"] == int(lens[lens > 4096].sum())
+    assert f["s1_short"] == short.sum() and f["s2_short"] == int((short * short).sum())
+    assert abs(f["avg_short"] - short.mean()) <= 1e-15 * short.mean()
+    assert abs(f["sd_short"] - short.std()) <= 1e-12 * short.std()
+    assert abs(f["nnz_sd"] - lens.std()) <= 1e-12 * lens.std()
+    for L in (4096, 4097, 100):
+        fl = oracle.features(rp, ci, L_split=L, n_cols=10000)
+        sh = lens[lens <= L]
+        assert fl["n_short"] == sh.size and fl["max_short"] == sh.max()
+        assert abs(fl["sd_short"] - sh.std()) <= 1e-12 * max(sh.std(), 1)
+
+
+def test_features_all_empty_and_all_long():
+    f = oracle.features(np.zeros(6, np.int64), np.zeros(0, np.int32))
+    assert f["n_empty"] == 5 and f["n_short"] == 5 and f["avg_short"] == 0.0 and f["sd_short"] == 0.0
+    lens = np.array([5000, 6000])
+    f = oracle.features(rp_of(lens), np.concatenate([np.arange(L, dtype=np.int32) for L in lens]), n_cols=6000)
+    assert f["n_short"] == 0 and f["n_long"] == 2 and f["avg_short"] == 0.0 and f["max_short"] == 0

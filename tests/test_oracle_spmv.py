@@ -183,3 +183,50 @@ def test_power_iteration_zero_norm():
     rp = np.zeros(11, np.int64)
     rc, _, nu = oracle.power_iter(rp, np.zeros(0, np.int32), np.zeros(0), np.ones(10), 5)
     assert rc == -7 and nu[0] == 0.0
+
+
+# ---- Neumaier self-check pinned to exact rational sums ------
+def _exact_row_sums(rp, ci, va, x):
+    return [sum((Fraction(float(va[j])) * Fraction(float(x[ci[j]])) for j in range(rp[i], rp[i + 1])), Fraction(0))
+            for i in range(rp.size - 1)]
+
+
+def test_neumaier_exact_on_cancellation_rows():
+    # products {1e16, 1, -1e16} -> 1; {1, 1e100, 1, -1e100} -> 2 (Neumaier's
+    # example); {3, 1e16, -1e16, -2**-30}: a plain left-to-right sum gives 0 / -2^-30,
+    # the compensated sum the exact value
+    rows = [[1e16, 1.0, -1e16], [1.0, 1e100, 1.0, -1e100], [3.0, 1e16, -1e16, -2.0 ** -30], [0.5, 0.25, -0.125]]
+    rp = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum([len(r) for r in rows], out=rp[1:])
+    va = np.concatenate([np.array(r) for r in rows])
+    ci = np.arange(va.size, dtype=np.int32)
+    x = np.ones(va.size)
+    yc = oracle.spmv_neumaier(rp, ci, va, x)
+    exact = _exact_row_sums(rp, ci, va, x)
+    assert yc.tolist() == [float(e) for e in exact] == [1.0, 2.0, 3.0 - 2.0 ** -30, 0.625]
+    yp = oracle.spmv(rp, ci, va, x)
+    assert yp[0] != 1.0 and yp[1] != 2.0  # the plain sum loses them: the pin is not vacuous
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_neumaier_error_bound_vs_exact(seed):
+    # |y_neu - S| <= u|S| + 2 n u^2 sum|p| (compensated summation bound), on rows
+    # with heavy cancellation where the plain sum's error is far larger
+    g = np.random.default_rng(seed)
+    n, L = 60, 200
+    rp = np.arange(n + 1, dtype=np.int64) * L
+    big = g.uniform(-1, 1, n * L) * 10.0 ** g.integers(0, 16, n * L)
+    va = np.concatenate([np.concatenate([b, -b[::-1]])[: L] + g.uniform(-1, 1, L) for b in big.reshape(n, L)[:, :L // 2]])
+    ci = np.arange(va.size, dtype=np.int32)
+    x = np.ones(va.size)
+    yc = oracle.spmv_neumaier(rp, ci, va, x)
+    exact = _exact_row_sums(rp, ci, va, x)
+    u = 2.0 ** -53
+    worst_plain = 0.0
+    yp = oracle.spmv(rp, ci, va, x)
+    for i in range(n):
+        S = exact[i]
+        a = float(sum(abs(Fraction(float(v))) for v in va[rp[i]:rp[i + 1]]))
+        assert abs(Fraction(float(yc[i])) - S) <= u * abs(S) + Fraction(2 * L * u * u * a)
+        worst_plain = max(worst_plain, float(abs(Fraction(float(yp[i])) - S)) / a)
+    assert worst_plain > 4 * L * u * u  # the plain sum does not meet the compensated bound
