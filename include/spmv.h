@@ -64,7 +64,9 @@ typedef struct spmv_options {
   int32_t struct_size;     /* = sizeof(spmv_options); set by spmv_options_default */
   int32_t force_variant;   /* spmv_variant; 0 = feature-guided selection */
   int32_t force_vs;        /* lanes per row for VECTOR/STREAM/SPLIT reductions: 0 = auto, else 1,2,4,8,16,32 */
-  int32_t d16;             /* delta colind: -1 auto, 0 off, 1 on when encodable (STREAM only) */
+  int32_t d16;             /* delta colind (STREAM only): -1 auto, 0 off, 1 = 16-bit deltas when
+                              encodable, 2 = dictionary-coded 8-bit deltas (D8) when codable (<= 256 distinct
+                              row-relative deltas, rows <= 255 nonzeros; reading 26) */
   int32_t xwin;            /* L2 persistence window on x (ML analogue of P:599-606): -1 auto, 0 off, 1 on */
   int32_t validate;        /* 1 = check CSR invariants on the device (default), 0 = trust the input */
   int64_t l_split;         /* long-row threshold in nnz (0 = 4096) */
@@ -96,6 +98,8 @@ typedef struct spmv_features {
   int64_t n_big_gaps;      /* distinct in-row gaps >= 65472 (129 = more than 128): escape-coded D16 needs <= 64 */
   int64_t col_min, col_max;/* smallest / largest column index (x range the rows read; 0 / -1 when nnz = 0):
                               the halo of a row block in the distributed iterated mode */
+  int64_t n_deltas;        /* distinct row-relative deltas (head: colind[rowptr[i]] - i, else the in-row gap;
+                              257 = more than 256): the D8 dictionary size (reading 26) */
 } spmv_features;
 
 typedef struct spmv_device_props {
@@ -111,7 +115,7 @@ typedef struct spmv_device_props {
 typedef struct spmv_selection {
   int32_t variant;   /* spmv_variant (never AUTO) */
   int32_t vs;        /* lanes per row */
-  int32_t d16;       /* 1 when the delta-encoded colind stream is used */
+  int32_t d16;       /* index stream: 0 int32 colind, 1 16-bit deltas, 2 dictionary-coded 8-bit deltas (D8) */
   int32_t xwin;      /* 1 when the x persistence window is set */
   int32_t classes;   /* SPMV_CLASS_* bitmask */
   int32_t seg;       /* 1: cta_stream runs in segmented mode (random gathers: products first, balanced row walk) */
@@ -145,7 +149,11 @@ typedef struct spmv_plan_info {
   double profile_ms;          /* micro-benchmark time (part of select_ms: the classifier's t_pre) */
   double x_reuse;             /* sampled fraction of nonzeros whose 128-B x line the previous row also reads */
   int32_t nz_gather_l2;       /* nnz_split / split tiles gather x through L2 only (x_reuse < 0.5, x > 1 MB) */
-  int32_t pad3_;
+  int32_t stream_stages;      /* STREAM: smem stages (= consumer warps per CTA) */
+  int32_t d8_n_dict;          /* D8: dictionary entries (0 when D8 is not used) */
+  int32_t stream_grid;        /* STREAM: persistent CTAs of shard 0's main kernel */
+  int64_t kernel_bytes;       /* compulsory DRAM bytes of one SpMV in the plan's own format (all shards):
+                                 values + the index streams the kernel reads + x (n_cols) + y (n_rows) */
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */
@@ -270,12 +278,15 @@ enum {
   SPMV_ARR_DCOL = 7,         /* uint16[nnz] delta colind */
   SPMV_ARR_HEAD = 8,         /* int32[n_rows] */
   SPMV_ARR_ANCHOR = 9,       /* int32[n_tiles] */
-  SPMV_ARR_DECODED = 10,     /* int32[nnz] colind re-decoded on the device from dcol/head/anchor */
+  SPMV_ARR_DECODED = 10,     /* int32[nnz] colind re-decoded on the device from dcol/head (D16) or codes/rlen/dict (D8) */
   SPMV_ARR_SHARD_BOUNDS = 11, /* int64[ngpus+1] */
   SPMV_ARR_NZ_ROWMAP = 12,    /* int64[mc+1]: nnz_split non-empty rows (y row ids), rowmap[mc] = n_rows */
   SPMV_ARR_NZ_RPC = 13,       /* int64[mc+1]: their rowptr (rpc[q] = rowptr[rowmap[q]], rpc[mc] = nnz) */
   SPMV_ARR_NZ_TILE_Q = 14,    /* int64[n_nz_tiles+1]: tile_q[k] = last q with rpc[q] <= 256k; tile_q[T] = mc */
-  SPMV_ARR_NZ_HOT_COLS = 15   /* int64[n_hot]: hot columns in column order (reading 20) */
+  SPMV_ARR_NZ_HOT_COLS = 15,  /* int64[n_hot]: hot columns in column order (reading 20) */
+  SPMV_ARR_D8_CODES = 16,     /* uint8[nnz]: D8 codes (index of each row-relative delta in the dictionary) */
+  SPMV_ARR_D8_RLEN = 17,      /* uint8[n_rows]: D8 row lengths */
+  SPMV_ARR_D8_DICT = 18       /* int64[d8_n_dict]: D8 dictionary (ascending distinct deltas) */
 };
 int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst);
 

@@ -215,6 +215,7 @@ def features(rowptr, colind, L_split=4096, line_elems=16, n_cols=None):
     d["n_big_gaps"] = big_gap_count(rp, ci)
     c = np.asarray(colind)
     d["col_min"], d["col_max"] = (int(c.min()), int(c.max())) if c.size else (0, -1)
+    d["n_deltas"] = d8_dict(rp, ci)[0]
     return d
 
 
@@ -446,11 +447,14 @@ VARIANT_VECTOR, VARIANT_STREAM, VARIANT_MERGE, VARIANT_SPLIT, VARIANT_NNZSPLIT =
 CLASS_MB, CLASS_ML, CLASS_IMB, CLASS_CMP = 1, 2, 4, 8
 
 
+D8_MAX, D8_MAX_ROW = 256, 255  # one byte per code / per row length
+
+
 @dataclass
 class Selection:
     variant: int
     vs: int
-    d16: bool
+    d16: int  # 0 int32 colind, 1 16-bit deltas, 2 dictionary-coded 8-bit deltas (D8)
     xwin: bool
     classes: int
 
@@ -512,12 +516,13 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
     mb = ws > l2_bytes // 2
     if mb and not (classes & CLASS_IMB):
         classes |= CLASS_MB
-    # MB delta colind (reading 9): 16-bit deltas or escape codes
-    # (<= 64 distinct deltas >= 65472) are possible, but only when forced
-    d16_ok = f["maxgap"] <= 65535 or f.get("n_big_gaps", BIG_TAB + 1) <= ESC_MAX
-    # (escape codes only when forced: measured slower, reading 21)
-    d16 = False  # measured slower than the plain stream kernel on B200 (reading 9): forced only
-    del d16_ok
+    # MB delta colind: 16-bit deltas (or escape codes) only when forced
+    # (measured slower on B200, reading 9); dictionary-coded 8-bit
+    # deltas (D8, reading 26) for MB stream plans with regular rows, one lane
+    # per row, <= 256 distinct row-relative deltas and rows <= 255 nonzeros
+    d8_ok = f.get("n_deltas", D8_MAX + 1) <= D8_MAX and f["nnz_max"] <= D8_MAX_ROW and nnz > 0
+    regular = f["nnz_max"] > 0 and f["nnz_max"] <= 1.25 * f["nnz_avg"] + 1.0
+    d16 = 2 if (variant == VARIANT_STREAM and (classes & CLASS_MB) and d8_ok and regular and vs == 1) else 0
     ml = nnz > 0 and f["misses"] > 0.75 * nnz and 8 * n > l2_bytes // 16
     if ml:
         classes |= CLASS_ML
@@ -549,7 +554,8 @@ def classify_profile(p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak, t_imb=T_IMB, t_ml=
 def profile_select(f, bounds, window_max, K_long=100):
     """Table II for the GPU variants: IMB -> long_row_split (dense
     long rows) or nnz_split; ML -> nnz_split with the x window; MB / CMP ->
-    cta_stream (MB adds 16-bit deltas when the gaps fit); no class -> the CSR
+    cta_stream (MB adds D8 codes when codable, else 16-bit deltas when the
+    gaps fit); no class -> the CSR
     baseline (csr_vector), "not worth applying any" (P:459-461). Precedence
     IMB > ML > MB/CMP. bounds: dict with p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak."""
     classes = classify_profile(*(bounds[k] for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak")))
@@ -568,7 +574,10 @@ def profile_select(f, bounds, window_max, K_long=100):
     vs = min(32, max(2, _pow2ceil(int(math.ceil(avg_s))))) if avg_s > 0 else 2
     if variant == VARIANT_STREAM:
         vs = min(32, _pow2ceil(int(math.ceil(avg_s / 32.0)))) if avg_s > 32 else 1
-    d16 = bool(classes & CLASS_MB) and variant == VARIANT_STREAM and f["maxgap"] <= 65535
+    d16 = 0
+    if classes & CLASS_MB and variant == VARIANT_STREAM:  # MB -> deltas: D8 when codable, else 16-bit
+        d8_ok = f.get("n_deltas", D8_MAX + 1) <= D8_MAX and f["nnz_max"] <= D8_MAX_ROW and vs == 1
+        d16 = 2 if d8_ok else (1 if f["maxgap"] <= 65535 else 0)
     xwin = bool(classes & CLASS_ML) and 8 * f["n"] <= window_max
     return Selection(variant, vs, d16, xwin, classes)
 

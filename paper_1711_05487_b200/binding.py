@@ -22,10 +22,10 @@ VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 CLASSES = {"MB": 1, "ML": 2, "IMB": 4, "CMP": 8}
 ARR = {"tile_rows": 1, "merge_rows": 2, "merge_nnz": 3, "chunk_row": 4, "chunk_begin": 5, "chunk_end": 6,
        "dcol": 7, "head": 8, "anchor": 9, "decoded": 10, "shard_bounds": 11, "nz_rowmap": 12, "nz_rpc": 13,
-       "nz_tile_q": 14, "nz_hot_cols": 15}
+       "nz_tile_q": 14, "nz_hot_cols": 15, "d8_codes": 16, "d8_rlen": 17, "d8_dict": 18}
 _ARR_DTYPE = {1: np.int64, 2: np.int64, 3: np.int64, 4: np.int64, 5: np.int64, 6: np.int64, 7: np.uint16,
               8: np.int32, 9: np.int32, 10: np.int32, 11: np.int64, 12: np.int64, 13: np.int64, 14: np.int64,
-              15: np.int64}
+              15: np.int64, 16: np.uint8, 17: np.uint8, 18: np.int64}
 
 
 class Options(ctypes.Structure):
@@ -64,7 +64,7 @@ class Features(ctypes.Structure):
                [(k, ctypes.c_int64) for k in ("maxgap", "misses")] + \
                [(k, ctypes.c_double) for k in ("nnz_avg", "nnz_sd", "avg_short", "sd_short")] + \
                [("n_cols", ctypes.c_int64), ("n_big_gaps", ctypes.c_int64), ("col_min", ctypes.c_int64),
-                ("col_max", ctypes.c_int64)]
+                ("col_max", ctypes.c_int64), ("n_deltas", ctypes.c_int64)]
 
 
 class DeviceProps(ctypes.Structure):
@@ -91,7 +91,8 @@ class PlanInfo(ctypes.Structure):
                 ("n_nz_tiles", ctypes.c_int64), ("n_hot", ctypes.c_int64), ("hot_cover", ctypes.c_double)] + \
                [(k, ctypes.c_double) for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak", "bmax")] + \
                [("profile_vs", ctypes.c_int32), ("profile_ctas", ctypes.c_int32), ("profile_ms", ctypes.c_double),
-               ("x_reuse", ctypes.c_double), ("nz_gather_l2", ctypes.c_int32), ("pad3_", ctypes.c_int32)]
+               ("x_reuse", ctypes.c_double), ("nz_gather_l2", ctypes.c_int32), ("stream_stages", ctypes.c_int32),
+               ("d8_n_dict", ctypes.c_int32), ("stream_grid", ctypes.c_int32), ("kernel_bytes", ctypes.c_int64)]
 
 
 _vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double

@@ -261,6 +261,7 @@ struct spmv_plan_s {
   int64_t l_split = 4096, k_long = 100, C = 2048, items = 2048, chunk = 8192;
   double hot_cover = 0.0;
   std::vector<int32_t> esc;  // D16 escape table (sorted distinct deltas >= kEsc0)
+  std::vector<int32_t> d8dict;  // D8 dictionary (sorted distinct row-relative deltas, <= kD8Max)
   ProfileBounds pb;          // profile-guided mode: measured / analytic bounds
   double profile_ms = 0.0;  // nnz_split hot-x set: fraction of nonzeros in the hot columns
 
@@ -379,18 +380,26 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   // per-element escape check costs more than it saves (27-pt 260^3: 1.33 ms
   // with vs 1.09 ms without), so escapes are used only when forced (d16=1)
   const bool d16_ok = f.maxgap <= 65535 || f.n_big_gaps <= kEscMax;
-  // (not auto-selected: with row-count tiles the plain stream kernel wins on
-  // every measured MB matrix, 27-pt 180^3 281.6 vs 313.9 us, C2 31.4 vs
-  // 35.0 us; the option d16 = 1 forces it)
-  bool d16 = false;
+  // (16-bit deltas are not auto-selected: with row-count tiles the plain
+  // stream kernel wins on every measured MB matrix, 27-pt 180^3 281.6 vs
+  // 313.9 us, C2 31.4 vs 35.0 us; the option d16 = 1 forces them)
+  // MB -> dictionary-coded 8-bit deltas (D8, reading 26) when the
+  // row-relative deltas take at most 256 values and every row fits a byte
+  // length, on regular rows (row-count tiles, one lane per row): 1 B of index
+  // per nonzero and per row instead of 4 B colind + 4/8 B rowptr
+  const bool d8_ok = f.n_deltas <= kD8Max && f.nnz_max <= kD8MaxRow && nnz > 0;
+  const bool regular = f.nnz_max > 0 && (double)f.nnz_max <= 1.25 * f.nnz_avg + 1.0;
+  int d16 = (variant == SPMV_VARIANT_STREAM && (classes & SPMV_CLASS_MB) && d8_ok && regular && vs == 1) ? 2 : 0;
   const bool ml = nnz > 0 && (double)f.misses > 0.75 * (double)nnz && 8 * n > d.l2_bytes / 16;
   if (ml) classes |= SPMV_CLASS_ML;
   bool xwin = ml && 8 * n <= d.access_window_max;
   // explicit options override the feature-guided choice
   if (o.force_vs > 0) vs = o.force_vs;
-  if (o.d16 == 0) d16 = false;
-  if (o.d16 == 1) d16 = d16_ok;
-  if (variant != SPMV_VARIANT_STREAM) d16 = false;
+  if (o.d16 == 0) d16 = 0;
+  if (o.d16 == 1) d16 = d16_ok ? 1 : 0;
+  if (o.d16 == 2) d16 = d8_ok ? 2 : 0;
+  if (variant != SPMV_VARIANT_STREAM) d16 = 0;
+  if (d16 == 2 && vs != 1) d16 = 0;  // D8: one lane per row
   if (o.xwin == 0) xwin = false;
   if (o.xwin == 1) xwin = true;
   // cta_stream consumer mode: segmented (products first, balanced row walk)
@@ -402,7 +411,7 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   if (d16) seg = false;
   s.variant = variant;
   s.vs = vs;
-  s.d16 = d16 ? 1 : 0;
+  s.d16 = d16;
   s.xwin = xwin ? 1 : 0;
   s.classes = classes;
   s.seg = seg ? 1 : 0;
@@ -444,15 +453,18 @@ void profile_select_impl(const spmv_features& f, const spmv_device_props& d, con
   int vs = avg_s > 0 ? std::min(32, std::max(2, pow2ceil((int64_t)std::ceil(avg_s)))) : 2;
   if (variant == SPMV_VARIANT_STREAM)
     vs = avg_s > 32 ? std::min(32, pow2ceil((int64_t)std::ceil(avg_s / 32.0))) : 1;
-  bool d16 = (classes & SPMV_CLASS_MB) && variant == SPMV_VARIANT_STREAM && f.maxgap <= 65535;
+  int d16 = 0;
+  if ((classes & SPMV_CLASS_MB) && variant == SPMV_VARIANT_STREAM)
+    d16 = (f.n_deltas <= kD8Max && f.nnz_max <= kD8MaxRow && vs == 1) ? 2 : (f.maxgap <= 65535 ? 1 : 0);
   bool xwin = (classes & SPMV_CLASS_ML) && 8 * f.n <= d.access_window_max;
   if (o.force_vs > 0) vs = o.force_vs;
-  if (o.d16 == 0) d16 = false;
+  if (o.d16 == 0) d16 = 0;
+  if (d16 == 2 && vs != 1) d16 = 0;
   if (o.xwin == 0) xwin = false;
   if (o.xwin == 1) xwin = true;
   s.variant = variant;
   s.vs = vs;
-  s.d16 = d16 ? 1 : 0;
+  s.d16 = d16;
   s.xwin = xwin ? 1 : 0;
   s.classes = classes;
   s.seg = 0;
@@ -473,6 +485,7 @@ void validate_options(const spmv_options& o) {
   if (o.select_mode < 0 || o.select_mode > 1) fail(SPMV_E_ARG, "select_mode must be 0 (feature) or 1 (profile)");
   if (o.hot_x < -1) fail(SPMV_E_ARG, "hot_x must be -1 (auto), 0 (off) or a column count");
   if (o.split_bins < -1 || o.split_bins > 1) fail(SPMV_E_ARG, "split_bins must be -1, 0 or 1");
+  if (o.d16 < -1 || o.d16 > 2) fail(SPMV_E_ARG, "d16 must be -1 (auto), 0 (off), 1 (16-bit deltas) or 2 (D8)");
   if (o.stages < 0 || o.stages > 32 || o.stages % kStreamConsumerWarps)
     fail(SPMV_E_ARG, "stages must be 0 (auto) or a multiple of %d up to 32", kStreamConsumerWarps);
 }
@@ -516,6 +529,18 @@ void features_from_stats(const std::vector<DevStats>& st, const std::vector<int6
     std::sort(big.begin(), big.end());
     big.erase(std::unique(big.begin(), big.end()), big.end());
     f.n_big_gaps = (over || (int64_t)big.size() > kBigTab) ? kBigTab + 1 : (int64_t)big.size();
+  }
+  {  // distinct row-relative deltas over all shards (kD8Max + 1 = more than kD8Max)
+    std::vector<int32_t> d;
+    bool over = false;
+    for (const auto& s : st) {
+      over = over || s.d_over;
+      for (int i = 0; i < kDTab; ++i)
+        if (s.dtab[i] != INT32_MIN) d.push_back(s.dtab[i]);
+    }
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    f.n_deltas = (over || (int64_t)d.size() > kD8Max) ? kD8Max + 1 : (int64_t)d.size();
   }
   f.nnz = (int64_t)f.s1;
   auto sd = [](uint64_t cnt, uint64_t s1, uint64_t s2) {
@@ -691,9 +716,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     init.col_err = LLONG_MAX;
     init.col_min = LLONG_MAX;
     init.col_max = -1;
+    for (int i = 0; i < kDTab; ++i) init.dtab[i] = INT32_MIN;
     ck(cudaMemcpyAsync(s.stats, &init, sizeof init, cudaMemcpyHostToDevice, s.stream), "stats init");
     ck(cudaMemsetAsync(s.headbits, 0, ((size_t)(s.nnz + 31) / 32 + 1) * 4, s.stream), "memset");
-    launch_rowstats(s.view(), P->l_split, s.headbits, s.stats, s.stream);
+    launch_rowstats(s.view(), P->l_split, s.row0, s.headbits, s.stats, s.stream);
     count_launches(s.m ? 1 : 0, "rowstats");
     ck(cudaMemcpyAsync(&s.hs, s.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s.stream), "stats");
   }
@@ -749,9 +775,21 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     P->profile_ms = now_ms() - t_p;
     if (opt.force_variant == 0) profile_select_impl(P->feat, P->props, opt, P->pb, P->sel);
   }
-  if (P->sel.d16) P->d16_width = P->feat.maxgap <= 255 ? 8 : 16;
+  if (P->sel.d16 == 1) P->d16_width = P->feat.maxgap <= 255 ? 8 : 16;
+  if (P->sel.d16 == 2) {
+    // D8 dictionary: the sorted distinct row-relative deltas of all shards
+    P->d16_width = 8;
+    std::vector<int32_t> d;
+    for (auto& sh : P->shards)
+      for (int i = 0; i < kDTab; ++i)
+        if (sh.hs.dtab[i] != INT32_MIN) d.push_back(sh.hs.dtab[i]);
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    if ((int)d.size() > kD8Max) fail(SPMV_E_CUDA, "D8 dictionary overflow (%d entries)", (int)d.size());
+    P->d8dict = d;
+  }
   // escape table: the sorted distinct large deltas of all shards
-  if (P->sel.d16 && P->feat.maxgap > 65535) {
+  if (P->sel.d16 == 1 && P->feat.maxgap > 65535) {
     std::vector<int32_t> big;
     for (auto& sh : P->shards)
       for (int i = 0; i < kBigTab; ++i)
@@ -766,13 +804,70 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   double t_d = now_ms();
   // cta_stream structures over the CSR view V (the whole shard, or one
   // compacted length bin of long_row_split mapped back through rowmap)
-  auto build_stream = [&](Shard& s, StreamPlan& sp, const MatView& V, const int32_t* rowmap, bool d16, int vs,
+  auto build_stream = [&](Shard& s, StreamPlan& sp, const MatView& V, const int32_t* rowmap, int dmode, int vs,
                           bool seg, int64_t maxlen) {
     sp.V = V;
     sp.rowmap = rowmap;
     sp.vs = vs;
     sp.seg = seg;
+    const bool d16 = dmode == 1;
     const double avg = V.m ? (double)V.nnz / (double)V.m : 0.0;
+    if (dmode == 2) {
+      // ---- D8 (d8.cu): row-count tiles of Rt rows (multiple of 16: the row
+      // lengths are bulk-copied from k*Rt), the fewest giving >= 576 nonzeros
+      // on average (as the int32 path), capacity Rt x longest row
+      int64_t Rt = 32;
+      double min_nz = 576.0;
+      if (const char* e = getenv("SPMV_ROW_TILE_MIN_NNZ")) min_nz = atof(e);  // experiments
+      while ((double)Rt * avg < min_nz && Rt < 4096) Rt += 32;
+      const int64_t ml = std::max<int64_t>(maxlen, 1);
+      int cw = 0;
+      if (const char* e = getenv("SPMV_D8_CW")) cw = atoi(e);  // experiments: 4, 6 or 8
+      // shrink the tile until 4 stages fit (long rows of a forced D8 plan)
+      while (Rt > 16 && d8_smem_bytes(Rt * ml, Rt, 4) > 227 * 1024) Rt -= 16;
+      sp.rows_per_tile = Rt;
+      sp.C = ((Rt * ml + 31) / 32) * 32;
+      P->C = sp.C;
+      sp.aligned = true;
+      sp.stride = sp.C;
+      sp.T = std::max<int64_t>(1, (V.m + Rt - 1) / Rt);
+      sp.rows_cap = (int)Rt;
+      sp.tile_row = s.alloc<int32_t>((size_t)sp.T + 1);
+      alloc_carries(s, sp.T, sp.carry_row, sp.carry_val);
+      launch_tile_rows_count(sp.tile_row, sp.T, Rt, V.m, s.stream);
+      sp.tile_nz = s.alloc<int64_t>((size_t)sp.T + 1);
+      launch_tile_nz(V, sp.tile_row, sp.T, sp.tile_nz, s.stream);
+      count_launches(2, "d8 tiles");
+      sp.n_dict = (int)P->d8dict.size();
+      for (int i = 0; i < sp.n_dict; ++i) sp.dict[i] = P->d8dict[(size_t)i];
+      int32_t* dict_dev = s.alloc<int32_t>(256);
+      ck(cudaMemcpyAsync(dict_dev, sp.dict, sizeof sp.dict, cudaMemcpyHostToDevice, s.stream), "d8 dict");
+      uint8_t* codes = s.alloc<uint8_t>((size_t)V.nnz);
+      uint8_t* rlen = s.alloc<uint8_t>((size_t)V.m);
+      sp.row0 = s.row0;
+      launch_d8_encode(V, sp.row0, dict_dev, sp.n_dict, codes, rlen, s.stream);
+      count_launches(V.m ? 1 : 0, "d8 encode");
+      sp.codes = codes;
+      sp.rlen = rlen;
+      sp.d8_dict_dev = dict_dev;
+      ck(cudaStreamSynchronize(s.stream), "d8 encode");
+      // consumer warps per CTA (one stage each): the most resident consumer
+      // warps per SM (ties: more CTAs), or SPMV_D8_CW
+      int best = -1, best_cw = 4;
+      for (int c : {4, 6, 8}) {
+        if (cw && c != cw) continue;
+        if (d8_smem_bytes(sp.C, Rt, c) > 227 * 1024) continue;
+        sp.stages = c;
+        sp.grid = d8_prepare(sp, s.sm_count);
+        if (sp.grid < 0) { cudaGetLastError(); continue; }
+        const int per_sm = d8_per_sm(sp);
+        if (per_sm * c > best) { best = per_sm * c; best_cw = c; }
+      }
+      sp.stages = best_cw;
+      sp.grid = d8_prepare(sp, s.sm_count);
+      if (sp.grid < 0) fail(SPMV_E_CUDA, "D8: cannot fit %lld-nonzero tiles in shared memory", (long long)sp.C);
+      return;
+    }
     // tile size: P whole passes of the consumer warp over its 32/VS rows
     // (row-step mode), the fewest passes giving >= 640 nonzeros -- a tile
     // that ends just short of a pass boundary keeps the lanes busy, and below
@@ -1047,7 +1142,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       nz->skip_rp = A.rowptr;
       return true;
     }
-    build_stream(s, sp, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, rows, false, vs, seg,
+    build_stream(s, sp, MatView{rp_bytes, brp, bcol, bval, nrows, s.n_cols, bnnz}, rows, 0, vs, seg,
                  std::min<int64_t>(hi, P->feat.nnz_max));
     return true;
   };
@@ -1718,6 +1813,22 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     for (const Shard& s : p->shards) { rh += s.hs.reuse_hit; rt += s.hs.reuse_tot; }
     info->x_reuse = rt ? (double)rh / (double)rt : 0.0;
     info->nz_gather_l2 = s0.nz.gather_l2 ? 1 : 0;
+    info->stream_stages = s0.sp[0].stages;
+    info->stream_grid = s0.sp[0].grid;
+    info->d8_n_dict = s0.sp[0].codes ? s0.sp[0].n_dict : 0;
+    {  // compulsory bytes of one SpMV in the plan's own format
+      int64_t kb = 8 * p->n_cols + 8 * p->n_rows + 8 * p->nnz;
+      for (const Shard& s : p->shards) {
+        const StreamPlan& sp = s.sp[0];
+        if (p->sel.variant == SPMV_VARIANT_STREAM && sp.codes)
+          kb += s.nnz + s.m + 8 * (sp.T + 1);  // codes, row lengths, tile starts
+        else if (p->sel.variant == SPMV_VARIANT_STREAM && sp.dcol)
+          kb += 2 * s.nnz + (int64_t)p->rp_bytes * (s.m + 1) + 4 * s.m;  // deltas, rowptr, heads
+        else
+          kb += 4 * s.nnz + (int64_t)p->rp_bytes * (s.m + 1);
+      }
+      info->kernel_bytes = kb;
+    }
     info->tile_nnz = s0.sp[0].C;
     info->n_tiles = s0.sp[0].T;
     info->tile_stride = s0.sp[0].stride;
@@ -1830,12 +1941,21 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
       case SPMV_ARR_DCOL: raw(s.sp[0].dcol, s.sp[0].dcol ? s.nnz : 0, 2); break;
       case SPMV_ARR_HEAD: raw(s.sp[0].head, s.sp[0].head ? s.m : 0, 4); break;
       case SPMV_ARR_ANCHOR: raw(s.sp[0].anchor, s.sp[0].anchor ? s.sp[0].T : 0, 4); break;
+      case SPMV_ARR_D8_CODES: raw(s.sp[0].codes, s.sp[0].codes ? s.nnz : 0, 1); break;
+      case SPMV_ARR_D8_RLEN: raw(s.sp[0].rlen, s.sp[0].rlen ? s.m : 0, 1); break;
+      case SPMV_ARR_D8_DICT: {
+        count = s.sp[0].codes ? s.sp[0].n_dict : 0;
+        if (dst)
+          for (int64_t i = 0; i < count; ++i) ((int64_t*)dst)[i] = s.sp[0].dict[i];
+        break;
+      }
       case SPMV_ARR_DECODED: {
-        count = s.sp[0].dcol ? s.nnz : 0;
+        count = (s.sp[0].dcol || s.sp[0].codes) ? s.nnz : 0;
         if (!dst || count == 0) break;
         int32_t* tmp = nullptr;
         ck(cudaMalloc(&tmp, (size_t)s.nnz * 4 + 64), "cudaMalloc");
-        launch_d16_decode_export(s.sp[0], tmp, s.stream);
+        if (s.sp[0].codes) launch_d8_decode_export(s.sp[0], s.sp[0].d8_dict_dev, tmp, s.stream);
+        else launch_d16_decode_export(s.sp[0], tmp, s.stream);
         g_launches += 1;
         cudaError_t e = cudaStreamSynchronize(s.stream);
         if (e == cudaSuccess) e = cudaMemcpy(dst, tmp, (size_t)s.nnz * 4, cudaMemcpyDeviceToHost);

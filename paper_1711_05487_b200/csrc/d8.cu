@@ -1,0 +1,353 @@
+// d8.cu -- cta_stream over dictionary-coded 8-bit column deltas ("D8"): the
+// MB-class optimisation of Sec. III-E ("8- or 16-bit deltas
+// wherever possible, but never both"; Table II) re-designed for sm_100a.
+//
+// Format (reading 26):
+//   delta_j = colind[j] - i              for the head j of row i (row id of
+//                                        the matrix: row0 + local row)
+//   delta_j = colind[j] - colind[j-1]    otherwise
+//   dict    = the <= 256 distinct deltas (ascending), codes[j] = index of delta_j
+//   rlen[i] = row length (<= 255)
+// so the kernel reads 1 byte of index per nonzero and 1 byte per row instead
+// of 4 B colind + 4/8 B rowptr: C5 (27-pt 384^3) 19.61 -> 14.66 GB per SpMV.
+// The decode is a running sum per lane: c = row id; c += dict[code].
+//
+// Row-count tiles only (regular rows): tile k = rows [k*Rt, min((k+1)*Rt, m)),
+// nonzeros [tile_nz[k], tile_nz[k+1]); no row crosses a tile, no carries.
+// Persistent warp-specialised CTAs as in stream.cu: one producer lane issues
+// three TMA bulk copies per tile (values, codes, row lengths; L2 evict_first)
+// into the stage of the consumer warp that owns the tile; the consumer's
+// lanes walk consecutive rows in step (one lane per row), 8 predicated x
+// gathers in flight per lane, dictionary in shared memory.
+#include <cstdlib>
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace spmv {
+
+__host__ __device__ __forceinline__ size_t d8_al128(size_t v) { return (v + 127) & ~(size_t)127; }
+
+struct D8Layout {
+  size_t vals, codes, rl, stage, full, empty, meta, total;
+};
+
+// C: nonzero capacity of a tile (Rt x longest row), Rt rows per tile
+__host__ __device__ inline D8Layout d8_layout(int64_t C, int64_t Rt, int stages) {
+  D8Layout L;
+  L.vals = 0;
+  // values: copy starts at the 128-B line of the first value (<= 15 before
+  // t0) and is rounded up to 16 B (<= 1 after)
+  L.codes = d8_al128((size_t)(C + 16) * 8);
+  // codes: copy starts 16-B aligned (<= 15 before t0), rounded up to 16 B,
+  // plus >= 8 readable bytes past any row end (branch-free 8-code batches)
+  L.rl = L.codes + d8_al128((size_t)C + 48);
+  L.stage = d8_al128(L.rl + (size_t)Rt + 16);
+  size_t o = L.stage * stages;
+  L.full = o; o += 8 * (size_t)stages;
+  L.empty = o; o += 8 * (size_t)stages;
+  L.meta = d8_al128(o); o = L.meta + 16 * (size_t)stages;
+  L.total = d8_al128(o);
+  return L;
+}
+
+size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages) { return d8_layout(C, Rt, stages).total; }
+
+struct D8Meta {
+  int64_t t0;
+  int32_t cnt, voff;  // nonzeros; offset of t0 in the staged values (codes: t0 & 15)
+};
+
+struct D8P {
+  const double* val;
+  const uint8_t* codes;
+  const uint8_t* rlen;
+  const int64_t* tile_nz;
+  const double* x;
+  double* y;
+  double* sq;       // iterated mode: sq[k] = sum of y_r^2 over tile k's rows (or null)
+  int64_t m, T, k0; // rows, end of the tile range, first tile
+  int64_t Rt, C;    // rows per tile, nonzero capacity
+  int64_t row0;     // row id of local row 0 (the anchor of the head deltas)
+  int stages;
+  int32_t dict[256];
+};
+
+__device__ __forceinline__ void d8_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int CW>
+__global__ void __launch_bounds__(32 * (CW + 1), CW == 4 ? 5 : (CW == 6 ? 4 : 3)) d8_kernel(const D8P p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int32_t dict_s[256];
+  const D8Layout L = d8_layout(p.C, p.Rt, p.stages);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.empty);
+  D8Meta* meta = reinterpret_cast<D8Meta*>(smem + L.meta);
+  const int S = p.stages;
+
+  pdl_trigger();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) dict_s[i] = p.dict[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (threadIdx.x < 32) {
+    // ------------------------------ producer ------------------------------
+    if (threadIdx.x == 0) {
+      const uint64_t pol = policy_evict_first();
+      int64_t nT0 = 0, nT1 = 0;
+      auto fetch = [&](int64_t kk) {
+        if (kk < p.T) {
+          nT0 = ld_ro(p.tile_nz + kk);
+          nT1 = ld_ro(p.tile_nz + kk + 1);
+        }
+      };
+      fetch(p.k0 + blockIdx.x);
+      int i = 0;
+      for (int64_t k = p.k0 + blockIdx.x; k < p.T; k += gridDim.x, ++i) {
+        const int s = i % S;
+        const int64_t t0 = nT0, t1 = nT1;
+        fetch(k + gridDim.x);
+        if (i >= S) mbar_wait(&empty[s], (uint32_t)(((i / S) - 1) & 1));
+        const int64_t R0 = k * p.Rt;
+        const int64_t R1 = (R0 + p.Rt) < p.m ? (R0 + p.Rt) : p.m;
+        const int64_t v0 = t0 & ~15ll, c0 = t0 & ~15ll;
+        const uint32_t vb = t1 > t0 ? (uint32_t)(((t1 - v0) * 8 + 15) & ~15ll) : 0u;
+        const uint32_t cb = t1 > t0 ? (uint32_t)(((t1 - c0) + 15) & ~15ll) : 0u;
+        const uint32_t rb = (uint32_t)(((R1 - R0) + 15) & ~15ll);
+        D8Meta mt;
+        mt.t0 = t0;
+        mt.cnt = (int32_t)(t1 - t0);
+        mt.voff = (int32_t)(t0 - v0);
+        meta[s] = mt;
+        unsigned char* st = smem + L.stage * s;
+        mbar_arrive_expect_tx(&full[s], vb + cb + rb);
+        if (t1 > t0) {
+          bulk_g2s(st + L.vals, p.val + v0, vb, &full[s], pol);
+          bulk_g2s(st + L.codes, p.codes + c0, cb, &full[s], pol);
+        }
+        bulk_g2s(st + L.rl, p.rlen + R0, rb, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------- consumers --------------------------------
+  pdl_wait();  // x, y, sq may be written by the previous kernel in the stream
+  const int w = (threadIdx.x >> 5) - 1;
+  const int lane = threadIdx.x & 31;
+  for (int i = w;; i += CW) {
+    const int64_t k = p.k0 + blockIdx.x + (int64_t)i * gridDim.x;
+    if (k >= p.T) break;
+    const int s = i % S;
+    mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+    const D8Meta mt = meta[s];
+    const unsigned char* st = smem + L.stage * s;
+    const double* vals_s = reinterpret_cast<const double*>(st + L.vals) + mt.voff;
+    const uint8_t* codes_s = st + L.codes + (mt.t0 & 15);
+    const uint8_t* rl_s = st + L.rl;
+    const int64_t R0 = k * p.Rt;
+    const int nrows = (int)(((R0 + p.Rt) < p.m ? (R0 + p.Rt) : p.m) - R0);
+    double sqa = 0.0;
+    int base = 0;  // first nonzero (tile-relative) of the pass
+    for (int qb = 0; qb < nrows; qb += 32) {
+      const int q = qb + lane;
+      const int len = q < nrows ? (int)rl_s[q] : 0;
+      int inc = len;  // inclusive scan of the row lengths over the pass
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      const int off = base + inc - len;
+      base += __shfl_sync(0xffffffffu, inc, 31);
+      int c = (int)(p.row0 + R0 + q);  // anchor of the head delta
+      double a0 = 0.0, a1 = 0.0;
+      for (int l0 = 0; l0 < len; l0 += 8) {
+        // 8 codes read unconditionally (the stage keeps >= 8 bytes of slack
+        // past the tile; a stale code still indexes the 256-entry dictionary)
+        // and masked by selects: no branch around the shared-memory loads
+        int cc[8];
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int d = dict_s[codes_s[off + l0 + u]];
+          c += (l0 + u < len) ? d : 0;
+          cc[u] = c;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = l0 + u < len ? ld_x(p.x + cc[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          const int l = l0 + u;
+          a0 = fma(l < len ? vals_s[off + l] : 0.0, xv[u], a0);
+          a1 = fma(l + 1 < len ? vals_s[off + l + 1] : 0.0, xv[u + 1], a1);
+        }
+      }
+      const double acc = a0 + a1;
+      if (q < nrows) {
+        p.y[R0 + q] = acc;
+        sqa = fma(acc, acc, sqa);
+      }
+    }
+    if (p.sq) {  // fixed butterfly: deterministic per tile
+      sqa = warp_sum(sqa);
+      if (lane == 0) p.sq[k] = sqa;
+    }
+    __syncwarp();
+    if (lane == 0) d8_arrive(&empty[s]);
+  }
+}
+
+static D8P d8_params(const StreamPlan& sp, const double* x, double* y) {
+  D8P p;
+  p.val = sp.V.val;
+  p.codes = sp.codes;
+  p.rlen = sp.rlen;
+  p.tile_nz = sp.tile_nz;
+  p.x = x;
+  p.y = y;
+  p.sq = sp.sq;
+  p.m = sp.V.m;
+  p.T = sp.T;
+  p.k0 = sp.k0;
+  p.Rt = sp.rows_per_tile;
+  p.C = sp.C;
+  p.row0 = sp.row0;
+  p.stages = sp.stages;
+  for (int i = 0; i < 256; ++i) p.dict[i] = i < sp.n_dict ? sp.dict[i] : 0;
+  return p;
+}
+
+template <int CW>
+static int d8_prepare_t(const StreamPlan& sp, int sm_count) {
+  const size_t smem = d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages);
+  if (cudaFuncSetAttribute(d8_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return -1;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW>, 32 * (CW + 1), smem) != cudaSuccess ||
+      per_sm < 1)
+    return -1;
+  if (const char* e = getenv("SPMV_STREAM_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));  // experiments
+  int64_t grid = (int64_t)sm_count * per_sm;
+  if (grid > sp.T) grid = sp.T;
+  return (int)std::max<int64_t>(grid, 1);
+}
+
+template <int CW>
+static int d8_per_sm_t(const StreamPlan& sp) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW>, 32 * (CW + 1),
+                                                    d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages)) != cudaSuccess)
+    return 0;
+  return per_sm;
+}
+
+int d8_per_sm(const StreamPlan& sp) {
+  switch (sp.stages) {
+    case 4: return d8_per_sm_t<4>(sp);
+    case 6: return d8_per_sm_t<6>(sp);
+    case 8: return d8_per_sm_t<8>(sp);
+    default: return 0;
+  }
+}
+
+int d8_prepare(const StreamPlan& sp, int sm_count) {
+  switch (sp.stages) {
+    case 4: return d8_prepare_t<4>(sp, sm_count);
+    case 6: return d8_prepare_t<6>(sp, sm_count);
+    case 8: return d8_prepare_t<8>(sp, sm_count);
+    default: return -1;
+  }
+}
+
+void launch_d8(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
+  const size_t smem = d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages);
+  const D8P p = d8_params(sp, x, y);
+  switch (sp.stages) {
+    case 4: launch_pdl(d8_kernel<4>, dim3(sp.grid), dim3(32 * 5), smem, s, p); break;
+    case 6: launch_pdl(d8_kernel<6>, dim3(sp.grid), dim3(32 * 7), smem, s, p); break;
+    default: launch_pdl(d8_kernel<8>, dim3(sp.grid), dim3(32 * 9), smem, s, p); break;
+  }
+}
+
+// ---- plan time ----------------------------------------------------------------
+// Encode: one thread per row (rows <= 255 nonzeros): code = index of the
+// row-relative delta in the sorted dictionary (binary search in smem).
+template <typename RP>
+__global__ void __launch_bounds__(kNT) d8_encode_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ col,
+                                                        int64_t m, int64_t row0, const int32_t* __restrict__ dict,
+                                                        int nd, uint8_t* __restrict__ codes,
+                                                        uint8_t* __restrict__ rlen) {
+  __shared__ int32_t d_s[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) d_s[i] = i < nd ? dict[i] : INT32_MAX;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const int64_t a = rp[i], b = rp[i + 1];
+    rlen[i] = (uint8_t)(b - a);
+    int64_t prev = row0 + i;
+    for (int64_t j = a; j < b; ++j) {
+      const int64_t c = col[j];
+      const int32_t d = (int32_t)(c - prev);
+      prev = c;
+      int lo = 0, hi = nd - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (d_s[mid] < d) lo = mid + 1; else hi = mid;
+      }
+      codes[j] = (uint8_t)lo;
+    }
+  }
+}
+
+void launch_d8_encode(const MatView& A, int64_t row0, const int32_t* dict_dev, int nd, uint8_t* codes, uint8_t* rlen,
+                      cudaStream_t s) {
+  if (A.m == 0) return;
+  int64_t g = (A.m + kNT - 1) / kNT;
+  if (g > 148 * 32) g = 148 * 32;
+  if (A.rp_bytes == 8)
+    d8_encode_kernel<int64_t><<<(unsigned)g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, A.m, row0, dict_dev, nd,
+                                                          codes, rlen);
+  else
+    d8_encode_kernel<int32_t><<<(unsigned)g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, A.m, row0, dict_dev, nd,
+                                                          codes, rlen);
+}
+
+// Export (tests): colind re-decoded from codes / rlen / dict, one thread per
+// row (row starts from the plan's rowptr; the SpMV itself never reads it)
+template <typename RP>
+__global__ void __launch_bounds__(kNT) d8_decode_kernel(const RP* __restrict__ rp, int64_t m, int64_t row0,
+                                                        const uint8_t* __restrict__ codes,
+                                                        const uint8_t* __restrict__ rlen,
+                                                        const int32_t* __restrict__ dict, int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x;
+  if (i >= m) return;
+  const int64_t a = rp[i];
+  int64_t c = row0 + i;
+  for (int t = 0; t < rlen[i]; ++t) {
+    c += dict[codes[a + t]];
+    out[a + t] = (int32_t)c;
+  }
+}
+
+void launch_d8_decode_export(const StreamPlan& sp, const int32_t* dict_dev, int32_t* out, cudaStream_t s) {
+  if (sp.V.m == 0) return;
+  const unsigned g = (unsigned)((sp.V.m + kNT - 1) / kNT);
+  if (sp.V.rp_bytes == 8)
+    d8_decode_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)sp.V.rowptr, sp.V.m, sp.row0, sp.codes, sp.rlen,
+                                                dict_dev, out);
+  else
+    d8_decode_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)sp.V.rowptr, sp.V.m, sp.row0, sp.codes, sp.rlen,
+                                                dict_dev, out);
+}
+
+}  // namespace spmv

@@ -19,10 +19,69 @@
 
 namespace spmv {
 
+// ---- distinct row-relative deltas (D8 dictionary, reading 26) ----
+// per-CTA open-addressing set in smem (INT32_MIN = empty), merged into the
+// global table at the end; gives up (over) past kD8Max distinct values
+constexpr int kDSet = 512;
+struct DeltaSet {
+  int32_t tab[kDSet];
+  int count, over;
+};
+__device__ __forceinline__ void dset_init(DeltaSet& ds) {
+  for (int i = threadIdx.x; i < kDSet; i += blockDim.x) ds.tab[i] = INT32_MIN;
+  if (threadIdx.x == 0) ds.count = ds.over = 0;
+}
+__device__ __forceinline__ void dset_insert(DeltaSet& ds, int64_t v64, int32_t& last) {
+  if (v64 <= INT32_MIN || v64 > INT32_MAX) { ds.over = 1; return; }
+  const int32_t v = (int32_t)v64;
+  if (v == last || ds.over) return;
+  last = v;
+  uint32_t h = ((uint32_t)v * 2654435761u) >> 23;  // 9 bits
+  for (int probe = 0; probe < kDSet; ++probe, h = (h + 1) & (kDSet - 1)) {
+    const int32_t cur = ds.tab[h];
+    if (cur == v) return;
+    if (cur == INT32_MIN) {
+      const int32_t prev = atomicCAS(&ds.tab[h], INT32_MIN, v);
+      if (prev == INT32_MIN) {
+        if (atomicAdd(&ds.count, 1) >= kD8Max) ds.over = 1;
+        return;
+      }
+      if (prev == v) return;
+    }
+  }
+  ds.over = 1;
+}
+// after a __syncthreads: the CTA's set into st->dtab
+__device__ __forceinline__ void dset_merge(DeltaSet& ds, DevStats* st) {
+  if (ds.over) {
+    if (threadIdx.x == 0) st->d_over = 1;
+    return;
+  }
+  for (int i = threadIdx.x; i < kDSet; i += blockDim.x) {
+    const int32_t v = ds.tab[i];
+    if (v == INT32_MIN) continue;
+    uint32_t h = ((uint32_t)v * 2654435761u) >> 22;  // 10 bits
+    int probe = 0;
+    for (; probe < kDTab; ++probe, h = (h + 1) & (kDTab - 1)) {
+      const int32_t prev = atomicCAS(&st->dtab[h], INT32_MIN, v);
+      if (prev == INT32_MIN) {
+        if (atomicAdd(&st->d_count, 1) >= kD8Max) st->d_over = 1;
+        break;
+      }
+      if (prev == v) break;
+    }
+    if (probe == kDTab) st->d_over = 1;
+  }
+}
+
 template <typename RP>
-__global__ void __launch_bounds__(kNT) rowstats_kernel(const RP* __restrict__ rp, int64_t m, int64_t nnz,
-                                                       int64_t l_split, uint32_t* __restrict__ headbits,
-                                                       DevStats* st) {
+__global__ void __launch_bounds__(kNT) rowstats_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ col,
+                                                       int64_t m, int64_t nnz, int64_t l_split, int64_t row0,
+                                                       uint32_t* __restrict__ headbits, DevStats* st) {
+  __shared__ DeltaSet ds;
+  dset_init(ds);
+  __syncthreads();
+  int32_t last = INT32_MIN;
   unsigned long long s1 = 0, s2 = 0, s1s = 0, s2s = 0;
   long long mn = LLONG_MAX, mx = 0, ne = 0, nl = 0, nnzl = 0, ns = 0, mxs = 0, err = LLONG_MAX;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -37,8 +96,13 @@ __global__ void __launch_bounds__(kNT) rowstats_kernel(const RP* __restrict__ rp
     ne += (len == 0);
     if (len > l_split) { nl++; nnzl += len; }
     else { ns++; s1s += ul; s2s += ul * ul; mxs = len > mxs ? len : mxs; }
-    if (len > 0 && a >= 0 && a < nnz) atomicOr(&headbits[a >> 5], 1u << (a & 31));
+    if (len > 0 && a >= 0 && a < nnz) {
+      atomicOr(&headbits[a >> 5], 1u << (a & 31));
+      dset_insert(ds, (int64_t)col[a] - (row0 + i), last);  // head delta
+    }
   }
+  __syncthreads();
+  dset_merge(ds, st);
   s1 = warp_sum(s1); s2 = warp_sum(s2); s1s = warp_sum(s1s); s2s = warp_sum(s2s);
   ne = warp_sum(ne); nl = warp_sum(nl); nnzl = warp_sum(nnzl); ns = warp_sum(ns);
   mn = warp_min(mn); mx = warp_max(mx); mxs = warp_max(mxs); err = warp_min(err);
@@ -65,9 +129,12 @@ __global__ void __launch_bounds__(kNT) validate_gaps_kernel(const int32_t* __res
   // (a stencil repeats a handful of values ~2x per row), merged at the end
   __shared__ int32_t tab[kBigTab];
   __shared__ int over;
+  __shared__ DeltaSet ds;
   for (int i = threadIdx.x; i < kBigTab; i += blockDim.x) tab[i] = 0;
   if (threadIdx.x == 0) over = 0;
+  dset_init(ds);
   __syncthreads();
+  int32_t last = INT32_MIN;
   long long mg = 0, miss = 0, err = LLONG_MAX, cmin = LLONG_MAX, cmax = -1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz; j += stride) {
@@ -81,6 +148,7 @@ __global__ void __launch_bounds__(kNT) validate_gaps_kernel(const int32_t* __res
       if (g <= 0) { long long k = 2 * j + 1; err = k < err ? k : err; continue; }
       mg = g > mg ? g : mg;
       miss += (g > 16);
+      dset_insert(ds, g, last);  // in-row gap
       if (g >= kEsc0) {
         const int32_t v = (int32_t)g;
         uint32_t h = ((uint32_t)v * 2654435761u) % kBigTab;
@@ -108,6 +176,7 @@ __global__ void __launch_bounds__(kNT) validate_gaps_kernel(const int32_t* __res
     }
   }
   if (threadIdx.x == 0 && over) st->big_over = 1;
+  dset_merge(ds, st);
   mg = warp_max(mg); miss = warp_sum(miss); err = warp_min(err);
   cmin = warp_min(cmin); cmax = warp_max(cmax);
   if ((threadIdx.x & 31) == 0) {
@@ -126,13 +195,16 @@ static int grid_for(int64_t work, int per_cta_min = kNT) {
   return (int)g;
 }
 
-void launch_rowstats(const MatView& A, int64_t l_split, uint32_t* headbits, DevStats* st, cudaStream_t s) {
+void launch_rowstats(const MatView& A, int64_t l_split, int64_t row0, uint32_t* headbits, DevStats* st,
+                     cudaStream_t s) {
   const int g = grid_for(A.m);
   if (A.m == 0) return;
   if (A.rp_bytes == 8)
-    rowstats_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.m, A.nnz, l_split, headbits, st);
+    rowstats_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, A.m, A.nnz, l_split, row0, headbits,
+                                               st);
   else
-    rowstats_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.m, A.nnz, l_split, headbits, st);
+    rowstats_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, A.m, A.nnz, l_split, row0, headbits,
+                                               st);
 }
 
 void launch_validate_gaps(const MatView& A, const uint32_t* headbits, DevStats* st, cudaStream_t s) {

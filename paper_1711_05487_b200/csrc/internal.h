@@ -29,7 +29,15 @@ struct DevStats {
   // x-line reuse probe: sampled rows r, nonzeros of r whose 128-B x line row
   // r-1 also reads (hits) out of the sampled nonzeros (tot)
   unsigned long long reuse_hit, reuse_tot;
+  // distinct row-relative deltas (D8, reading 26): head deltas
+  // colind[rowptr[i]] - (row0 + i) and in-row gaps; open-addressing set,
+  // INT32_MIN = empty slot; d_over = 1 once more than kD8Max distinct values
+  int32_t dtab[1024];
+  int32_t d_count, d_over;
 };
+constexpr int kDTab = 1024;  // global distinct-delta table slots
+constexpr int kD8Max = 256;  // dictionary entries (one byte per code)
+constexpr int kD8MaxRow = 255;  // row lengths stored in one byte
 // escape-coded 16-bit deltas (SURVEY 8(f) f3 reading; reading 21):
 // a delta d < kEsc0 is stored as d, a delta d >= kEsc0 as kEsc0 + (index of d
 // in the plan's sorted table of distinct large deltas, at most kEscMax)
@@ -70,7 +78,21 @@ struct StreamPlan {
   int64_t k0 = 0;              // first tile of the launch (tile-range launches: pipelined host execute)
   int64_t rows_per_tile = 0;   // > 0: row-count tiles (tile k = rows [k*rpt, (k+1)*rpt), aligned)
   double* sq = nullptr;        // launch-time: per-tile sums of y^2 (row-aligned tiles, iterated mode)
+  // D8 (dictionary-coded 8-bit deltas, d8.cu): codes[nnz], rlen[m], dict; row-count tiles only
+  const uint8_t* codes = nullptr;
+  const uint8_t* rlen = nullptr;
+  int n_dict = 0;
+  int32_t dict[256] = {};
+  int64_t row0 = 0;            // row id of local row 0 (anchor of the head deltas)
+  const int32_t* d8_dict_dev = nullptr;  // the dictionary on the device (export decode)
 };
+size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages);
+int d8_prepare(const StreamPlan& sp, int sm_count);  // stages = consumer warps (4, 6, 8)
+int d8_per_sm(const StreamPlan& sp);                 // resident CTAs per SM (after d8_prepare)
+void launch_d8(const StreamPlan& sp, const double* x, double* y, cudaStream_t s);
+void launch_d8_encode(const MatView& A, int64_t row0, const int32_t* dict_dev, int nd, uint8_t* codes, uint8_t* rlen,
+                      cudaStream_t s);
+void launch_d8_decode_export(const StreamPlan& sp, const int32_t* dict_dev, int32_t* out, cudaStream_t s);
 // row-aligned STREAM plan (no fix-up) with sq[k] = sum of y_r^2 over tile k's rows
 int launch_stream_sq(const StreamPlan& sp, const double* x, double* y, double* sq, cudaStream_t s);
 void launch_tile_rows_count(int32_t* tile_row, int64_t T, int64_t rows_per_tile, int64_t m, cudaStream_t s);
@@ -132,7 +154,8 @@ int launch_nz_range(const NzPlan& z, const double* x, double* y, int64_t k0, int
 int launch_nz_fixup_range(const NzPlan& z, double* y, int64_t k0, int64_t k1, cudaStream_t s);
 
 // ---- inspector ------------------------------------------------------------
-void launch_rowstats(const MatView& A, int64_t l_split, uint32_t* headbits, DevStats* st, cudaStream_t s);
+void launch_rowstats(const MatView& A, int64_t l_split, int64_t row0, uint32_t* headbits, DevStats* st,
+                     cudaStream_t s);
 void launch_validate_gaps(const MatView& A, const uint32_t* headbits, DevStats* st, cudaStream_t s);
 void launch_x_reuse(const MatView& A, DevStats* st, cudaStream_t s);  // DevStats reuse_hit / reuse_tot
 void launch_tile_rows(const MatView& A, int64_t C, int64_t T, int32_t* tile_row, DevStats* st, cudaStream_t s);

@@ -644,6 +644,11 @@ static int stream_rp(const StreamPlan& sp, int smc, const double* x, double* y, 
 
 template <bool PREP>
 static int stream_dispatch(const StreamPlan& sp, int smc, const double* x, double* y, cudaStream_t s) {
+  if (sp.codes) {  // dictionary-coded 8-bit deltas (d8.cu)
+    if (PREP) return d8_prepare(sp, smc);
+    launch_d8(sp, x, y, s);
+    return 0;
+  }
   return sp.V.rp_bytes == 8 ? stream_rp<int64_t, PREP>(sp, smc, x, y, s) : stream_rp<int32_t, PREP>(sp, smc, x, y, s);
 }
 

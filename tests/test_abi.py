@@ -79,7 +79,7 @@ def test_selection_matches_oracle_on_config_features(c):
         p = _props(l2)
         s = pkg.select(f, p, rpb)
         o = oracle.select(f, p["l2_bytes"], p["access_window_max"], rpb)
-        assert (s["variant"], s["vs"], bool(s["d16"]), bool(s["xwin"]), s["classes"]) == \
+        assert (s["variant"], s["vs"], s["d16"], bool(s["xwin"]), s["classes"]) == \
             (o.variant, o.vs, o.d16, o.xwin, o.classes)
 
 
@@ -90,7 +90,8 @@ def test_selection_matches_oracle_on_random_features():
         n = int(g.integers(1, 10 ** 7))
         avg = float(g.choice([0.5, 3, 7, 15, 27, 40, 200]))
         nnz = int(n * avg)
-        f = dict(n=n, nnz=nnz, nnz_min=0, nnz_max=int(g.choice([avg * 2, avg * 500, 10 ** 6])),
+        f = dict(n=n, nnz=nnz, nnz_min=0, nnz_max=int(g.choice([avg, avg + 1, avg * 2, avg * 500, 10 ** 6])),
+                 n_deltas=int(g.choice([1, 15, 256, 257])),
                  n_empty=int(n * g.choice([0, 0.1, 0.3, 0.6])), n_long=int(g.choice([0, 0, 5, 100])),
                  nnz_long=int(g.choice([0, 10 ** 5, 10 ** 7])), n_cols=int(n * g.choice([1, 0.1, 10])),
                  n_big_gaps=int(g.choice([0, 4, 64, 65, 129])),
@@ -101,7 +102,7 @@ def test_selection_matches_oracle_on_random_features():
         p = _props(int(g.choice([2 ** 20, 50 * 2 ** 20, 126 * 2 ** 20])))
         s = pkg.select(f, p, 4)
         o = oracle.select(f, p["l2_bytes"], p["access_window_max"], 4)
-        assert (s["variant"], s["vs"], bool(s["d16"]), bool(s["xwin"]), s["classes"]) == \
+        assert (s["variant"], s["vs"], s["d16"], bool(s["xwin"]), s["classes"]) == \
             (o.variant, o.vs, o.d16, o.xwin, o.classes), f
 
 

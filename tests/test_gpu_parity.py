@@ -279,7 +279,7 @@ def test_pipelined_host_execute(monkeypatch, name, lens, extra):
     m = sg.from_lengths(lens, max(lens.size, int(lens.max())), g, sg.MODE_U11, sg.MODE_U11)
     kw = {"tile_nnz": 512, "seg": 0}
     kw.update(extra)  # tile_nnz 0: the plan's own tile rule (row-count tiles on regular rows)
-    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="stream", **kw)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", **kw)
     yh = p.execute(m.x, np.full(m.n, np.nan))  # host buffers: pipelined
     assert_bound(yh, m)
     assert np.all(yh[lens == 0] == 0.0)
@@ -311,7 +311,7 @@ def test_pipelined_host_execute_nnzsplit(monkeypatch, name, lens, hot):
         lens = np.minimum((g.pareto(1.2, size=60000) * 3).astype(np.int64), 20000)
     lens = np.asarray(lens, np.int64)
     m = sg.from_lengths(lens, max(lens.size, int(lens.max())), g, sg.MODE_U11, sg.MODE_U11)
-    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="nnzsplit", hot_x=hot)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="nnzsplit", hot_x=hot)
     yh = p.execute(m.x, np.full(m.n, np.nan))
     assert_bound(yh, m)
     assert np.all(yh[lens == 0] == 0.0)
@@ -592,3 +592,112 @@ def test_x_reuse_probe(kind):
         assert want < 0.1 and info["nz_gather_l2"] == 1  # x = 2.4 MB > 1 MB
     y = p.execute(m.x)
     assert_bound(y, m)
+
+
+# ---- D8: dictionary-coded 8-bit deltas (d8.cu; reading 26) -----------
+def _d8_cases():
+    g = np.random.default_rng(17)
+    out = [("st7_9", sg.stencil(9, 7)), ("st27_11", sg.stencil(11, 27)), ("st27_20_rp64", sg.stencil(20, 27, rp64=True))]
+    # banded rows from a small gap alphabet, ragged lengths incl. empty rows
+    for name, n, lo, hi in (("banded_ragged", 5003, 0, 30), ("banded_long", 1500, 100, 255), ("tiny", 7, 1, 4)):
+        lens = g.integers(lo, hi + 1, n)
+        rp = np.zeros(n + 1, np.int64)
+        np.cumsum(lens, out=rp[1:])
+        ci = np.empty(int(rp[-1]), np.int32)
+        for i in range(n):
+            if lens[i]:
+                steps = g.choice([1, 2, 5, 40], lens[i])
+                steps[0] = g.integers(-min(i, 20), 20)
+                ci[rp[i]:rp[i + 1]] = i + np.cumsum(steps)
+        ncols = int(ci.max()) + 1 if ci.size else n
+        out.append((name, sg.CSR(n, rp.astype(np.int32), ci, g.uniform(-1, 1, ci.size), g.uniform(-1, 1, ncols))))
+    return out
+
+
+D8_CASES = _d8_cases()
+
+
+@pytest.mark.parametrize("name,m", D8_CASES, ids=[n for n, _ in D8_CASES])
+def test_d8_structures_and_parity(name, m):
+    enc = oracle.d8_encode(m.rowptr, m.colind)
+    assert enc is not None
+    d, codes, rlen = enc
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", d16=2)
+    info = p.info()
+    assert info["sel"]["d16"] == 2 and info["d8_n_dict"] == d.size and info["d16_width"] == 8
+    assert info["feat"]["n_deltas"] == d.size
+    assert np.array_equal(p.export("d8_dict"), d)
+    assert np.array_equal(p.export("d8_codes"), codes)
+    assert np.array_equal(p.export("d8_rlen"), rlen)
+    assert np.array_equal(p.export("decoded"), m.colind)  # device decode, round trip
+    Rt = info["rows_per_tile"]
+    assert Rt % 16 == 0 and np.array_equal(p.export("tile_rows"), np.minimum(np.arange(info["n_tiles"] + 1) * Rt, m.n))
+    y = p.execute(m.x, np.full(m.n, np.nan))
+    assert_bound(y, m)
+    assert np.all(y[np.diff(m.rowptr.astype(np.int64)) == 0] == 0.0)
+    # dyadic inputs: every order exact -> bit-equal (a wrong column shows up)
+    g = np.random.default_rng(3)
+    xv = g.integers(-1024, 1025, m.x.size) / 1024.0
+    vv = g.integers(-1024, 1025, m.vals.size) / 1024.0
+    pd = spmv.Plan(m.rowptr, m.colind, vv, n_cols=m.x.size, force_variant="stream", d16=2)
+    assert np.array_equal(pd.execute(xv), oracle.spmv(m.rowptr, m.colind, vv, xv))
+
+
+@pytest.mark.parametrize("cw", ["4", "6", "8"])
+def test_d8_consumer_warp_counts(monkeypatch, cw):
+    monkeypatch.setenv("SPMV_D8_CW", cw)
+    m = sg.stencil(24, 27, x_seed=5)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="stream", d16=2)
+    assert p.info()["stream_stages"] == int(cw)
+    assert_bound(p.execute(m.x), m)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_d8_emulated_shards(G):
+    m = sg.stencil(16, 27, x_seed=2)
+    d, codes, rlen = oracle.d8_encode(m.rowptr, m.colind)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, ngpus=G, emulate_devices=1, force_variant="stream", d16=2)
+    b = p.info()["shard_bounds"]
+    rp = m.rowptr.astype(np.int64)
+    for g in range(G):  # one global dictionary; shard g's codes are the oracle's slice
+        assert np.array_equal(p.export("d8_dict", g), d)
+        assert np.array_equal(p.export("d8_codes", g), codes[rp[b[g]]:rp[b[g + 1]]])
+        assert np.array_equal(p.export("decoded", g), m.colind[rp[b[g]]:rp[b[g + 1]]])
+    assert_bound(p.execute(m.x), m)
+    # iterated mode through D8 shards (fused per-tile norm partials)
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, 30)
+    xg, nug = p.iterate(m.x, 30)
+    assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
+    assert np.all(np.abs(nug - nur) <= 1e-12 * nur)
+
+
+def test_d8_auto_selected_on_c2_and_host_pipeline(monkeypatch):
+    m = sg.config(2)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals)
+    info = p.info()
+    assert info["variant"] == "stream" and info["sel"]["d16"] == 2 and info["d8_n_dict"] == 10
+    assert info["kernel_bytes"] == 9 * m.nnz + m.n + 8 * (info["n_tiles"] + 1) + 16 * m.n
+    y = p.execute(m.x)
+    assert_bound(y, m)
+    ones = np.ones(m.n)
+    assert np.array_equal(p.execute(ones), oracle.spmv(m.rowptr, m.colind, m.vals, ones))
+    monkeypatch.setenv("SPMV_HOST_PIPE_MIN_BYTES", "1")
+    monkeypatch.setenv("SPMV_HOST_PIPE_BLOCKS", "7")
+    p2 = spmv.Plan(m.rowptr, m.colind, m.vals)
+    assert np.array_equal(p2.execute(m.x, np.full(m.n, np.nan)), y)  # pipelined host path, same arithmetic
+
+
+def test_d16_row_tiles_random_x():
+    # forced 16-bit deltas on row-count tiles (no tile_nnz), one lane
+    # per row and VS > 1, random x so a wrong decoded column cannot hide
+    g = np.random.default_rng(23)
+    for lens, vs in (([7] * 20000, 1), ([40] * 3000, 4)):
+        lens = np.asarray(lens, np.int64)
+        m = sg.from_lengths(lens, 30000, g, sg.MODE_U11, sg.MODE_U11)
+        p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", d16=1, force_vs=vs)
+        info = p.info()
+        assert info["sel"]["d16"] == 1 and info["rows_per_tile"] > 0
+        if vs == 1:
+            assert info["stream_stages"] == 6
+        assert_bound(p.execute(m.x), m)
+        assert np.array_equal(p.export("decoded"), m.colind)

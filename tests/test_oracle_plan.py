@@ -223,25 +223,34 @@ WIN = 128 * 2 ** 20
 
 
 def test_select_rule_table_on_closed_form_features():
-    def feat(n, nnz, avg_s, sd_s, n_empty=0, n_long=0, nnz_max=0, maxgap=0, misses=0, nnz_long=0, n_big_gaps=129):
+    def feat(n, nnz, avg_s, sd_s, n_empty=0, n_long=0, nnz_max=0, maxgap=0, misses=0, nnz_long=0, n_big_gaps=129,
+             n_deltas=257):
         return dict(n=n, nnz=nnz, avg_short=avg_s, sd_short=sd_s, n_empty=n_empty, n_long=n_long,
                     nnz_max=nnz_max, nnz_avg=nnz / n, maxgap=maxgap, misses=misses, nnz_long=nnz_long, n_cols=n,
-                    n_big_gaps=n_big_gaps)
+                    n_big_gaps=n_big_gaps, n_deltas=n_deltas)
     S = oracle
-    # C2: 7-pt 128^3 (closed forms above): regular, 217 MB > L2/2, maxgap 16384
-    s = S.select(feat(2097152, 14581760, 6.953125, 0.2148, maxgap=16384, misses=8323072), L2, WIN, 4)
-    assert (s.variant, s.d16, s.xwin, s.vs) == (S.VARIANT_STREAM, False, False, 1) and s.classes & S.CLASS_MB
-    # C5: 27-pt 384^3: regular, maxgap 147071 (4 distinct gaps >= 65472: escape
-    # codes possible but not auto-selected, reading 21) -> no D16
-    s = S.select(feat(56623104, 1520875000, 26.86, 0.5, maxgap=147071, misses=10 ** 8, n_big_gaps=4), L2, WIN, 8)
-    assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, False, 1)  # rows <= 32 nnz: one lane per row
-    # a 27-pt grid with 16-bit gaps (n = 180: maxgap 32219): D16-eligible but not auto-selected
-    # (reading 9: the plain stream kernel is faster on B200)
-    s = S.select(feat(5832000, 155235000, 26.6, 0.6, maxgap=32219, misses=10 ** 7, n_big_gaps=0), L2, WIN, 8)
-    assert s.d16 is False and s.variant == S.VARIANT_STREAM
-    # 7-pt rows (avg < 16) keep int32 colind
-    s = S.select(feat(15625000, 109000000, 6.98, 0.2, maxgap=62250, misses=10 ** 7, n_big_gaps=0), L2, WIN, 4)
-    assert s.d16 is False
+    # C2: 7-pt 128^3 (closed forms above): regular, 217 MB > L2/2, maxgap 16384,
+    # 10 distinct row-relative deltas (test_d8_config_dictionaries) -> stream + D8
+    s = S.select(feat(2097152, 14581760, 6.953125, 0.2148, nnz_max=7, maxgap=16384, misses=8323072, n_deltas=10),
+                 L2, WIN, 4)
+    assert (s.variant, s.d16, s.xwin, s.vs) == (S.VARIANT_STREAM, 2, False, 1) and s.classes & S.CLASS_MB
+    # C5: 27-pt 384^3: regular, 15 deltas -> D8 (maxgap 147071: no 16-bit deltas;
+    # 4 distinct gaps >= 65472: escape codes possible but forced only, reading 21)
+    s = S.select(feat(56623104, 1520875000, 26.86, 0.5, nnz_max=27, maxgap=147071, misses=10 ** 8, n_big_gaps=4,
+                      n_deltas=15), L2, WIN, 8)
+    assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, 2, 1)  # rows <= 32 nnz: one lane per row
+    # the same without a codable dictionary (> 256 deltas) keeps int32 colind:
+    # 16-bit deltas are never auto-selected (reading 9)
+    s = S.select(feat(5832000, 155235000, 26.6, 0.6, nnz_max=27, maxgap=32219, misses=10 ** 7, n_big_gaps=0), L2,
+                 WIN, 8)
+    assert s.d16 == 0 and s.variant == S.VARIANT_STREAM
+    # irregular rows (longest > 1.25 x average + 1): no D8 even when codable
+    s = S.select(feat(15625000, 109000000, 6.98, 0.2, nnz_max=12, maxgap=62250, misses=10 ** 7, n_big_gaps=0,
+                      n_deltas=40), L2, WIN, 4)
+    assert s.d16 == 0
+    # rows longer than 255: no D8
+    s = S.select(feat(1000000, 300000000, 300.0, 0.0, nnz_max=300, maxgap=100, misses=0, n_deltas=5), L2, WIN, 8)
+    assert s.d16 == 0
     # uniform random rows (4M x 8/row: every nonzero opens a new x line) ->
     # scattered columns -> nnz_split (reading 24), not the row-walking stream
     s = S.select(feat(4000000, 36000000, 9.0, 0.3, maxgap=3999000, misses=35900000), L2, WIN, 4)
@@ -251,7 +260,7 @@ def test_select_rule_table_on_closed_form_features():
     assert s.variant == S.VARIANT_VECTOR
     # C1: 1.28 MB working set, 90,000 nonzeros -> launch-bound: csr_vector VS 16, no MB, no D16
     s = S.select(feat(10000, 90000, 9.0, 0.0, maxgap=9000, misses=80000), L2, WIN, 4)
-    assert (s.variant, s.vs, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_VECTOR, 16, False, 0)
+    assert (s.variant, s.vs, s.d16, s.classes & S.CLASS_MB) == (S.VARIANT_VECTOR, 16, 0, 0)
     # C3-like: half the rows empty, sparse long rows (11.4M nnz over 1794 rows of
     # 4.2M columns: far below 64 per 2048-column block) -> nnz_split, IMB + ML
     s = S.select(feat(4194304, 65244537, 12.8, 78.5, n_empty=2185429, n_long=1794, nnz_max=97958,
@@ -431,9 +440,11 @@ def test_profile_select_table2_mapping():
     s = S.profile_select(f, {**b, "p_ml": 2.0}, 1 << 27)
     assert s.variant == S.VARIANT_NNZSPLIT and s.xwin                                       # ML
     s = S.profile_select(f, {**b, "p_csr": 1.9}, 1 << 27)
-    assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, True, 1)                          # MB -> stream + D16
+    assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, 1, 1)                             # MB -> stream + D16
+    s = S.profile_select({**f, "n_deltas": 12}, {**b, "p_csr": 1.9}, 1 << 27)
+    assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, 2, 1)                             # MB, codable -> D8
     s = S.profile_select(f, {**b, "p_cmp": 1.0}, 1 << 27)
-    assert (s.variant, s.d16) == (S.VARIANT_STREAM, False)                                  # CMP
+    assert (s.variant, s.d16) == (S.VARIANT_STREAM, 0)                                      # CMP
     fl = {**f, "n_long": 10, "nnz_max": 5000, "nnz_long": 50000}
     assert S.profile_select(fl, {**b, "p_imb": 2.0}, 1 << 27).variant == S.VARIANT_SPLIT    # dense long rows
 
