@@ -402,9 +402,9 @@ def run_native(a):
     byts = algo_bytes(N, N, nnz, blk["rp_bytes"]) + 8 * N * (world - 1)  # x replicated: each rank reads it
     gbs = byts / (ms_step * 1e-3) / 1e9
     peak, peak_kind = measured_peak()
-    kbytes = algo_bytes(n_rows, blk["N"], nnz_local, blk["rp_bytes"])
-    if info["sel"]["d16"]:  # the kernel's own format: 2-B deltas + 4-B row heads instead of 4-B colind
-        kbytes += -2 * nnz_local + 4 * n_rows
+    # the dominant kernel's own compulsory bytes (its index format: int32
+    # colind + rowptr, 16-bit deltas + heads, or D8 codes + row lengths)
+    kbytes = int(info["kernel_bytes"])
     achieved = kbytes / (ms_main * 1e-3) / 1e9
     traffic = None
     try:

@@ -217,19 +217,28 @@ int32_t spmv_norm_partial_count(void);
 int spmv_norm_partials(spmv_plan p, const double* y, double* partials);
 int spmv_normalize(spmv_plan p, const double* y, const double* partials, int count, double* x_out,
                    double* nu_dev);
-/* Deferred-normalisation steps (what spmv_iterate runs per shard):
- *   spmv_norm_step: n = sqrt(sum_{q ascending} partials[q]) over `count`
- *     partials; *nu_k = n / nn[0] (n when nn[0] == 0, i.e. the first step);
- *     nn[0] = n and, when n leaves [2^-256, 2^256], y[0..n_rows) and nn[0]
- *     are scaled by the same exact power of two (nn[1] = that factor, else
- *     1). nn: 2 device doubles, zeroed by the caller before the first step.
- *   spmv_unit: x_out[i] = y[i] / nn[0] for i < n (the final x = yh/||yh||;
- *     x_out may equal y). */
-int spmv_norm_step(spmv_plan p, const double* partials, int count, double* nn, double* nu_k, double* y);
-/* spmv_execute_async(p, x, y) followed by spmv_norm_partials(p, y, partials),
- * the partials computed inside the SpMV for row-aligned STREAM plans (each
- * tile sums the squares of the rows it writes; kNormPartials fixed chunks of
- * the tile sums), so y is not read again. Same contract as the two calls. */
+/* Deferred-normalisation steps (what spmv_iterate runs per shard; DESIGN.md
+ * reading 25). nn: 2 device doubles of state, zeroed by the caller before
+ * the first step; nn[0] = the running norm, nn[1] = a PENDING exact
+ * power-of-two rescale factor (0 or 1: none) that the next spmv_iter_step
+ * applies to its output and spmv_unit to the final x -- no pass ever
+ * rescales a block in place.
+ *   spmv_iter_step: y = s * (A x) with s = nn[1] (1 when 0), partials[0..
+ *     spmv_norm_partial_count()) = sums of y_i^2 over fixed chunks (row-
+ *     aligned STREAM / D8 plans: fixed per-CTA sums folded into the chunks by
+ *     the kernel's last CTA), and, when nu_k is non-NULL, the norm step below
+ *     on these partials alone (a single rank: one launch per iteration for
+ *     fused plans). Device pointers of the plan's device, plan stream.
+ *   spmv_norm_step: n = sqrt(sum of `count` partials, fixed order); *nu_k =
+ *     n / nn[0] (n when nn[0] == 0, the first step); nn[0] = n scaled into
+ *     [2^-256, 2^256] by an exact power of two, nn[1] = that factor (else 1).
+ *     Every rank computes identical values from the gathered partials.
+ *   spmv_unit: x_out[i] = y[i] * nn[1] / nn[0] for i < n (the final x =
+ *     yh/||yh||; x_out may equal y). */
+int spmv_iter_step(spmv_plan p, const double* x, double* y, double* partials, double* nn, double* nu_k);
+int spmv_norm_step(spmv_plan p, const double* partials, int count, double* nn, double* nu_k);
+/* spmv_execute_async(p, x, y) followed by the partials of y (as spmv_iter_step
+ * with no pending factor and no norm step). */
 int spmv_execute_norm(spmv_plan p, const double* x, double* y, double* partials);
 int spmv_unit(spmv_plan p, const double* y, int64_t n, const double* nn, double* x_out);
 

@@ -109,7 +109,8 @@ lib.spmv_iterate.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.POINTER(_d), _v
 lib.spmv_norm_partial_count.restype = _i32
 lib.spmv_norm_partials.argtypes = [_vp, _vp, _vp]
 lib.spmv_normalize.argtypes = [_vp, _vp, _vp, ctypes.c_int, _vp, _vp]
-lib.spmv_norm_step.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp, _vp]
+lib.spmv_norm_step.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp]
+lib.spmv_iter_step.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
 lib.spmv_execute_norm.argtypes = [_vp, _vp, _vp, _vp]
 lib.spmv_unit.argtypes = [_vp, _vp, ctypes.c_int64, _vp, _vp]
 lib.spmv_plan_query.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
@@ -271,8 +272,11 @@ class Plan:
     def execute_norm(self, x, y, partials):
         _check(lib.spmv_execute_norm(self._h, _ptr(x), _ptr(y), _ptr(partials)))
 
-    def norm_step(self, partials, count, nn, nu_k, y):
-        _check(lib.spmv_norm_step(self._h, _ptr(partials), int(count), _ptr(nn), _ptr(nu_k), _ptr(y)))
+    def norm_step(self, partials, count, nn, nu_k):
+        _check(lib.spmv_norm_step(self._h, _ptr(partials), int(count), _ptr(nn), _ptr(nu_k)))
+
+    def iter_step(self, x, y, partials, nn, nu_k=None):
+        _check(lib.spmv_iter_step(self._h, _ptr(x), _ptr(y), _ptr(partials), _ptr(nn), _ptr(nu_k)))
 
     def unit(self, y, nn, x_out):
         _check(lib.spmv_unit(self._h, _ptr(y), int(_numel(y)), _ptr(nn), _ptr(x_out)))

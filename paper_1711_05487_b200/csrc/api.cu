@@ -193,7 +193,8 @@ struct Shard {
   // iterated mode
   double* allpart = nullptr;  // 2 x G * kNormPartials (iteration parity: double-buffered)
   double* x2 = nullptr;       // second x replica (deferred-normalisation ping-pong)
-  double* sq = nullptr;       // per-tile sums of y^2 (fused norm partials, row-aligned STREAM)
+  double* cta_part = nullptr; // per-CTA sums of y^2 (fused iteration epilogue, row-aligned STREAM / D8)
+  unsigned int* done = nullptr;  // its last-CTA ticket counter
   double* nn = nullptr;       // running norm + rescale factor (norm.cu)
   double* nu = nullptr;
   int nu_cap = 0;
@@ -399,6 +400,7 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
   if (o.d16 == 1) d16 = d16_ok ? 1 : 0;
   if (o.d16 == 2) d16 = d8_ok ? 2 : 0;
   if (variant != SPMV_VARIANT_STREAM) d16 = 0;
+  if (d16 == 2 && o.d16 == 2 && o.force_vs <= 0) vs = 1;  // forced D8: its kernel runs one lane per row
   if (d16 == 2 && vs != 1) d16 = 0;  // D8: one lane per row
   if (o.xwin == 0) xwin = false;
   if (o.xwin == 1) xwin = true;
@@ -1617,11 +1619,11 @@ int spmv_normalize(spmv_plan p, const double* y, const double* partials, int cou
   });
 }
 
-int spmv_norm_step(spmv_plan p, const double* partials, int count, double* nn, double* nu_k, double* y) {
+int spmv_norm_step(spmv_plan p, const double* partials, int count, double* nn, double* nu_k) {
   return guard([&] {
-    if (!p || !partials || !nn || !nu_k || !y || count < 1 || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    if (!p || !partials || !nn || !nu_k || count < 1 || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
     Shard& s = p->shards[0];
-    count_launches(launch_norm_step(partials, count, nn, nu_k, y, s.m, s.stream), "norm step");
+    count_launches(launch_norm_step(partials, count, nn, nu_k, s.stream), "norm step");
   });
 }
 
@@ -1634,20 +1636,35 @@ int spmv_unit(spmv_plan p, const double* y, int64_t n, const double* nn, double*
 }
 
 namespace {
-// y = A x on shard s plus the norm partials of y (kNormPartials fixed chunks):
-// a row-aligned STREAM plan sums the squares of each tile's rows inside the
-// SpMV (no second pass over y), otherwise a separate partials pass
-int spmv_with_partials(const spmv_plan_s* P, Shard& s, const double* x, double* y, double* partials) {
+// One iteration's SpMV on shard s (iterfuse.cuh): y = f * (A x) with f the
+// pending exact rescale nn[1] of the previous step (nn null: f = 1), the
+// kNormPartials partials of y^2 and, when nu_k is given (single rank: the
+// partials are all of them), the norm step. Row-aligned STREAM / D8 plans do
+// all of it inside the SpMV kernel (its last CTA folds the partials and runs
+// the norm step): one launch per iteration. Other variants: the SpMV, one
+// scale + partials pass over y, the norm-step kernel.
+int spmv_iter(const spmv_plan_s* P, Shard& s, const double* x, double* y, double* partials, double* nn,
+              double* nu_k) {
   const StreamPlan& sp = s.sp[0];
   if (P->sel.variant == SPMV_VARIANT_STREAM && sp.aligned && !sp.seg && !sp.rowmap && !sp.need_fixup &&
       !getenv("SPMV_NO_FUSED_NORM")) {
-    if (!s.sq) s.sq = s.alloc<double>((size_t)sp.T);
-    int n = launch_stream_sq(sp, x, y, s.sq, s.stream);
-    n += launch_sum_partials(s.sq, sp.T, partials, s.stream);
-    return n;
+    if (!s.cta_part) {
+      s.cta_part = s.alloc<double>((size_t)std::max(sp.grid, 1));
+      s.done = s.alloc<unsigned int>(1);
+      ck(cudaMemsetAsync(s.done, 0, sizeof(unsigned int), s.stream), "memset");
+    }
+    IterOut it;
+    it.scale = nn ? nn + 1 : nullptr;
+    it.cta_part = s.cta_part;
+    it.done = s.done;
+    it.partials = partials;
+    it.nn = nu_k ? nn : nullptr;
+    it.nu_k = nu_k;
+    return launch_stream_iter(sp, x, y, it, s.stream);
   }
   int n = P->launch(s, x, y);
-  n += launch_norm_partials(y, s.m, partials, s.stream);
+  n += launch_scale_partials(y, s.m, nn, partials, s.stream);
+  if (nu_k) n += launch_norm_step(partials, kNormPartials, nn, nu_k, s.stream);
   return n;
 }
 
@@ -1675,7 +1692,20 @@ int spmv_execute_norm(spmv_plan p, const double* x, double* y, double* partials)
     require_dev(s, x, "x");
     require_dev(s, y, "y");
     require_dev(s, partials, "partials");
-    count_launches(spmv_with_partials(p, s, x, y, partials), "spmv + norm partials");
+    count_launches(spmv_iter(p, s, x, y, partials, nullptr, nullptr), "spmv + norm partials");
+  });
+}
+
+int spmv_iter_step(spmv_plan p, const double* x, double* y, double* partials, double* nn, double* nu_k) {
+  return guard([&] {
+    if (!p || !x || !y || !partials || !nn || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    require_dev(s, x, "x");
+    require_dev(s, y, "y");
+    require_dev(s, partials, "partials");
+    require_dev(s, nn, "nn");
+    if (nu_k) require_dev(s, nu_k, "nu_k");
+    count_launches(spmv_iter(p, s, x, y, partials, nn, nu_k), "iteration step");
   });
 }
 
@@ -1719,10 +1749,15 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
         Shard& s = p->shards[g];
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
         set_xwin(p, s, cur[g]);
-        count_launches(
-            spmv_with_partials(p, s, cur[g], nxt[g] + s.row0, s.allpart + half + (size_t)g * kNormPartials),
-            "spmv + norm partials");
+        // one shard: the norm step runs inside the SpMV's epilogue (fused plans)
+        count_launches(spmv_iter(p, s, cur[g], nxt[g] + s.row0, s.allpart + half + (size_t)g * kNormPartials, s.nn,
+                                 G == 1 ? s.nu + k : nullptr),
+                       "iteration step");
         ck(cudaEventRecord(s.ev_part, s.stream), "event");
+      }
+      if (G == 1) {
+        std::swap(cur, nxt);
+        continue;
       }
       for (int g = 0; g < G; ++g) {
         Shard& s = p->shards[g];
@@ -1735,9 +1770,7 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
                                  t.allpart + half + (size_t)h * kNormPartials, t.dev, kNormPartials * 8, s.stream),
              "partials exchange");
         }
-        count_launches(
-            launch_norm_step(s.allpart + half, G * kNormPartials, s.nn, s.nu + k, nxt[g] + s.row0, s.m, s.stream),
-            "norm step");
+        count_launches(launch_norm_step(s.allpart + half, G * kNormPartials, s.nn, s.nu + k, s.stream), "norm step");
         ck(cudaEventRecord(s.ev_x, s.stream), "event");
       }
       if (G > 1) {

@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "iterfuse.cuh"
 
 namespace spmv {
 
@@ -66,7 +67,7 @@ struct D8P {
   const int64_t* tile_nz;
   const double* x;
   double* y;
-  double* sq;       // iterated mode: sq[k] = sum of y_r^2 over tile k's rows (or null)
+  IterOut it;       // iterated mode: pending rescale, fused norm partials / step (iterfuse.cuh)
   int64_t m, T, k0; // rows, end of the tile range, first tile
   int64_t Rt, C;    // rows per tile, nonzero capacity
   int64_t row0;     // row id of local row 0 (the anchor of the head deltas)
@@ -141,9 +142,11 @@ __global__ void __launch_bounds__(32 * (CW + 1), CW == 4 ? 5 : (CW == 6 ? 4 : 3)
   }
 
   // ------------------------------- consumers --------------------------------
-  pdl_wait();  // x, y, sq may be written by the previous kernel in the stream
+  pdl_wait();  // x, y, the scale may be written by the previous kernel in the stream
   const int w = (threadIdx.x >> 5) - 1;
   const int lane = threadIdx.x & 31;
+  const double f = iter_scale(p.it);  // exact power of two (1 outside the iterated mode)
+  double wsq = 0.0;                   // squares of the rows this warp writes, its tiles in order
   for (int i = w;; i += CW) {
     const int64_t k = p.k0 + blockIdx.x + (int64_t)i * gridDim.x;
     if (k >= p.T) break;
@@ -192,19 +195,17 @@ __global__ void __launch_bounds__(32 * (CW + 1), CW == 4 ? 5 : (CW == 6 ? 4 : 3)
           a1 = fma(l + 1 < len ? vals_s[off + l + 1] : 0.0, xv[u + 1], a1);
         }
       }
-      const double acc = a0 + a1;
+      const double acc = (a0 + a1) * f;
       if (q < nrows) {
         p.y[R0 + q] = acc;
         sqa = fma(acc, acc, sqa);
       }
     }
-    if (p.sq) {  // fixed butterfly: deterministic per tile
-      sqa = warp_sum(sqa);
-      if (lane == 0) p.sq[k] = sqa;
-    }
+    if (p.it.cta_part) wsq += warp_sum(sqa);  // fixed butterfly: deterministic per tile
     __syncwarp();
     if (lane == 0) d8_arrive(&empty[s]);
   }
+  iter_epilogue<32 * CW>(p.it, wsq);
 }
 
 static D8P d8_params(const StreamPlan& sp, const double* x, double* y) {
@@ -215,7 +216,7 @@ static D8P d8_params(const StreamPlan& sp, const double* x, double* y) {
   p.tile_nz = sp.tile_nz;
   p.x = x;
   p.y = y;
-  p.sq = sp.sq;
+  p.it = sp.it;
   p.m = sp.V.m;
   p.T = sp.T;
   p.k0 = sp.k0;

@@ -45,6 +45,19 @@ constexpr int kEsc0 = 65536 - 64;
 constexpr int kEscMax = 64;
 constexpr int kBigTab = 128;
 
+// iterated-mode epilogue fused into the row-aligned persistent SpMV kernels
+// (iterfuse.cuh): pending exact rescale of the previous step, per-CTA sums of
+// squares folded into kNormPartials rank partials by the last CTA, and for a
+// single rank the norm step itself
+struct IterOut {
+  const double* scale = nullptr;  // pending factor of the previous step (nn + 1; 0 = none), or null
+  double* cta_part = nullptr;     // [grid] per-CTA sums of squares (null: no partials)
+  unsigned int* done = nullptr;   // ticket counter (zero between launches)
+  double* partials = nullptr;     // [kNormPartials] rank partials
+  double* nn = nullptr;           // non-null: fused norm step (single rank), nn[0..1]
+  double* nu_k = nullptr;
+};
+
 struct MatView {
   int rp_bytes;
   const void* rowptr;   // int32 or int64 [m+1]
@@ -77,7 +90,7 @@ struct StreamPlan {
   bool l2pf = false;           // producer L2-prefetches each stage's next tile (measured slower: C2 53.7 vs 47.0 us)
   int64_t k0 = 0;              // first tile of the launch (tile-range launches: pipelined host execute)
   int64_t rows_per_tile = 0;   // > 0: row-count tiles (tile k = rows [k*rpt, (k+1)*rpt), aligned)
-  double* sq = nullptr;        // launch-time: per-tile sums of y^2 (row-aligned tiles, iterated mode)
+  IterOut it{};                // launch-time: iterated-mode epilogue (row-aligned tiles; iterfuse.cuh)
   // D8 (dictionary-coded 8-bit deltas, d8.cu): codes[nnz], rlen[m], dict; row-count tiles only
   const uint8_t* codes = nullptr;
   const uint8_t* rlen = nullptr;
@@ -93,8 +106,8 @@ void launch_d8(const StreamPlan& sp, const double* x, double* y, cudaStream_t s)
 void launch_d8_encode(const MatView& A, int64_t row0, const int32_t* dict_dev, int nd, uint8_t* codes, uint8_t* rlen,
                       cudaStream_t s);
 void launch_d8_decode_export(const StreamPlan& sp, const int32_t* dict_dev, int32_t* out, cudaStream_t s);
-// row-aligned STREAM plan (no fix-up) with sq[k] = sum of y_r^2 over tile k's rows
-int launch_stream_sq(const StreamPlan& sp, const double* x, double* y, double* sq, cudaStream_t s);
+// row-aligned STREAM / D8 plan (no fix-up) with the iterated-mode epilogue
+int launch_stream_iter(const StreamPlan& sp, const double* x, double* y, const IterOut& it, cudaStream_t s);
 void launch_tile_rows_count(int32_t* tile_row, int64_t T, int64_t rows_per_tile, int64_t m, cudaStream_t s);
 // tiles [k0, k1) of a STREAM plan (+ the fix-up of their carries); the rows
 // cut at k0 / k1 are completed by the neighbouring ranges' fix-ups
@@ -266,9 +279,11 @@ int compute_table1(const MatView& A, const int32_t* hot_cols, int sm_count, Tabl
 int launch_norm_partials(const double* y, int64_t m, double* partials, cudaStream_t s);
 // partials[q] = sum of v over the fixed chunk q of v[0..n) (no squares)
 int launch_sum_partials(const double* v, int64_t n, double* partials, cudaStream_t s);
-// deferred normalisation (norm.cu): nn[0..1] running norm / rescale factor
-int launch_norm_step(const double* partials, int count, double* nn, double* nu_k, double* y, int64_t m,
-                     cudaStream_t s);
+// deferred normalisation (norm.cu): nn[0..1] running norm / pending exact
+// rescale factor (applied by the next SpMV or the final unit, never in place)
+int launch_norm_step(const double* partials, int count, double* nn, double* nu_k, cudaStream_t s);
+// non-fused variants: y *= nn[1] (pending factor; nn may be null) + partials of y^2
+int launch_scale_partials(double* y, int64_t m, const double* nn, double* partials, cudaStream_t s);
 int launch_unit(const double* y, int64_t m, const double* nn, double* x_out, cudaStream_t s);
 int launch_normalize(const double* y, int64_t m, const double* partials, int count, double* x_out,
                      double* nu_dev, cudaStream_t s);

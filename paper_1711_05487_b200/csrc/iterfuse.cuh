@@ -1,0 +1,86 @@
+// iterfuse.cuh -- the iterated mode's per-iteration epilogue fused into the
+// persistent SpMV kernels (row-aligned cta_stream and D8): BJ.configs[5]
+// "x <- y/||y||" with deferred normalisation (reading 25).
+//
+//  * pending rescale: y = s * (A x) with s = *scale (the exact power of two the
+//    previous norm step asked for; 0 or null = 1), so no separate pass over
+//    the block ever rescales it
+//  * squares: each consumer warp sums y_r^2 over the rows it writes (its tiles
+//    in launch order), the CTA combines its warps in warp order into
+//    cta_part[blockIdx.x]; the LAST CTA to finish (ticket counter) folds the
+//    CTA partials into the kNormPartials rank partials (slot q = sum over CTAs
+//    b = q (mod kNormPartials), b ascending) and, for a single rank, runs the
+//    norm step itself (nu_k, nn) -- one launch per iteration, deterministic
+//    for a fixed grid
+#pragma once
+#include "common.cuh"
+#include "internal.h"
+
+namespace spmv {
+
+__device__ __forceinline__ double iter_scale(const IterOut& it) {
+  if (!it.scale) return 1.0;
+  const double f = *it.scale;
+  return f != 0.0 ? f : 1.0;
+}
+
+// the norm step (norm.cu norm_step_kernel, same arithmetic): ss = sum of
+// squares of yh_k; nu_k = ||yh_k|| / nn[0] (||yh_k|| at k = 0), nn[0] =
+// ||yh_k|| brought into [2^-256, 2^256] by an exact power of two, nn[1] =
+// that factor (applied to the block by the next SpMV / the final unit)
+__device__ __forceinline__ void norm_step_scalar(double ss, double* nn, double* nu_k) {
+  const double n = sqrt(ss), prev = nn[0];
+  *nu_k = prev > 0.0 ? n / prev : n;
+  const int e = (n > 0.0 && isfinite(n)) ? ilogb(n) : 0;
+  const bool rs = e > 256 || e < -256;  // squares stay far from overflow (2^1024)
+  nn[0] = rs ? scalbn(n, -e) : n;
+  nn[1] = rs ? scalbn(1.0, -e) : 1.0;
+}
+
+// Called by every consumer thread (NC threads, warps 1..NC/32 of the CTA;
+// the producer warp has exited) after its last tile, wsq = the warp's sum of
+// squares (same value in every lane). Named barrier 1 over the consumers.
+template <int NC>
+__device__ __forceinline__ void iter_epilogue(const IterOut& it, double wsq) {
+  if (!it.cta_part) return;
+  __shared__ double ws[NC / 32];
+  __shared__ double fin[NC / 32];
+  __shared__ int last;
+  const int t = threadIdx.x - 32;  // consumer thread index
+  const int w = t >> 5, lane = t & 31;
+  if (lane == 0) ws[w] = wsq;
+  asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+  if (t == 0) {
+    double c = 0.0;
+    for (int q = 0; q < NC / 32; ++q) c += ws[q];
+    it.cta_part[blockIdx.x] = c;
+    __threadfence();
+    const unsigned tk = atomicAdd(it.done, 1u);
+    last = tk == gridDim.x - 1;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+  if (!last) return;
+  __threadfence();
+  const int G = (int)gridDim.x;
+  double mine = 0.0;  // this thread's slots, ascending
+  for (int q = t; q < kNormPartials; q += NC) {
+    double v = 0.0;
+    for (int b = q; b < G; b += kNormPartials) v += __ldcg(it.cta_part + b);
+    it.partials[q] = v;
+    mine += v;
+  }
+  if (it.nn) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0) fin[w] = mine;
+    asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+    if (t == 0) {
+      double ss = 0.0;
+      for (int q = 0; q < NC / 32; ++q) ss += fin[q];
+      norm_step_scalar(ss, it.nn, it.nu_k);
+    }
+  }
+  if (t == 0) *it.done = 0u;  // ready for the next launch (it waits for this grid before its epilogue)
+}
+
+}  // namespace spmv

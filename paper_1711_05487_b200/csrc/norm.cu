@@ -11,6 +11,7 @@
 // magnitudes never overflow and no rounding is added.
 #include "common.cuh"
 #include "internal.h"
+#include "iterfuse.cuh"
 
 namespace spmv {
 
@@ -80,41 +81,60 @@ __global__ void __launch_bounds__(kNT) normalize_kernel(const double* __restrict
   for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = y[i] / nu;
 }
 
-// nn[0] = ||yh_k|| (after an exact power-of-two rescale), nn[1] = that
-// rescale factor (1.0: none), *nu_k = ||yh_k|| / ||yh_{k-1}|| (nn[0] == 0 on
-// entry at k = 0: nu_0 = ||yh_0||). One CTA.
+// the norm step on gathered partials, one CTA (norm_step_scalar in
+// iterfuse.cuh): *nu_k = ||yh_k|| / nn[0] (||yh_k|| at k = 0), nn[0] =
+// ||yh_k|| brought into [2^-256, 2^256] by an exact power of two, nn[1] =
+// that pending factor -- the block itself is not touched: the next SpMV
+// multiplies its output by nn[1] (or spmv_unit the final x)
 __global__ void __launch_bounds__(kNT) norm_step_kernel(const double* __restrict__ partials, int count,
                                                         double* __restrict__ nn, double* __restrict__ nu_k) {
   pdl_trigger();  // the next kernel in the stream may launch (it waits before reading)
   pdl_wait();
   const double ss = block_sum_fixed(partials, count);
-  if (threadIdx.x != 0) return;
-  const double n = sqrt(ss), prev = nn[0];
-  *nu_k = prev > 0.0 ? n / prev : n;
-  const int e = (n > 0.0 && isfinite(n)) ? ilogb(n) : 0;
-  const bool rs = e > 256 || e < -256;  // squares stay far from overflow (2^1024)
-  nn[0] = rs ? scalbn(n, -e) : n;
-  nn[1] = rs ? scalbn(1.0, -e) : 1.0;
+  if (threadIdx.x == 0) norm_step_scalar(ss, nn, nu_k);
 }
 
-// y *= nn[1] when the step asked for a rescale (exact: a power of two)
-__global__ void __launch_bounds__(kNT) rescale_kernel(double* __restrict__ y, int64_t m, const double* __restrict__ nn) {
-  pdl_trigger();  // the next kernel in the stream may launch (it waits before reading)
+// Non-fused variants' iteration epilogue: y *= s (the pending factor nn[1]
+// of the previous step; nothing written when s is 1) and the kNormPartials
+// fixed-chunk partials of y^2 -- one pass over y
+__global__ void __launch_bounds__(kNT) scale_partials_kernel(double* __restrict__ y, int64_t m,
+                                                             const double* __restrict__ nn,
+                                                             double* __restrict__ partials) {
+  pdl_trigger();
   pdl_wait();
-  const double f = nn[1];
-  if (f == 1.0) return;
-  const int64_t stride = (int64_t)gridDim.x * kNT;
-  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) y[i] *= f;
+  const double f0 = nn ? nn[1] : 1.0;
+  const double f = f0 != 0.0 ? f0 : 1.0;
+  const int64_t b = blockIdx.x;
+  const int64_t r0 = b * m / kNormPartials, r1 = (b + 1) * m / kNormPartials;
+  double a = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kNT) {
+    double v = y[i];
+    if (f != 1.0) {
+      v *= f;
+      y[i] = v;
+    }
+    a = fma(v, v, a);
+  }
+  const double t = warp_sum(a);
+  __shared__ double ws[kNT / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kNT / 32; ++w) s += ws[w];
+    partials[b] = s;
+  }
 }
 
-// x_out = yh / nn[0]
+// x_out = yh * nn[1] / nn[0] (the pending factor applied, exact)
 __global__ void __launch_bounds__(kNT) unit_kernel(const double* __restrict__ y, int64_t m,
                                                    const double* __restrict__ nn, double* __restrict__ x_out) {
   pdl_trigger();  // the next kernel in the stream may launch (it waits before reading)
   pdl_wait();
   const double nu = nn[0];
+  const double f = nn[1] != 0.0 ? nn[1] : 1.0;
   const int64_t stride = (int64_t)gridDim.x * kNT;
-  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = y[i] / nu;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = (y[i] * f) / nu;
 }
 
 static int grid_for(int64_t m) {
@@ -123,11 +143,14 @@ static int grid_for(int64_t m) {
   return (int)(g < 1 ? 1 : g);
 }
 
-int launch_norm_step(const double* partials, int count, double* nn, double* nu_k, double* y, int64_t m,
-                     cudaStream_t s) {
+int launch_norm_step(const double* partials, int count, double* nn, double* nu_k, cudaStream_t s) {
   launch_pdl(norm_step_kernel, dim3(1), dim3(kNT), 0, s, partials, count, nn, nu_k);
-  launch_pdl(rescale_kernel, dim3(grid_for(m)), dim3(kNT), 0, s, y, m, (const double*)nn);
-  return 2;
+  return 1;
+}
+
+int launch_scale_partials(double* y, int64_t m, const double* nn, double* partials, cudaStream_t s) {
+  launch_pdl(scale_partials_kernel, dim3(kNormPartials), dim3(kNT), 0, s, y, m, nn, partials);
+  return 1;
 }
 
 int launch_unit(const double* y, int64_t m, const double* nn, double* x_out, cudaStream_t s) {

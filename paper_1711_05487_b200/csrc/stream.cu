@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "iterfuse.cuh"
 
 namespace spmv {
 
@@ -121,7 +122,7 @@ struct StreamP {
   double* carry_val;
   int64_t nnz, C, T;  // T: end of the tile range
   int64_t k0;         // first tile of the range
-  double* sq;         // row-aligned tiles: sq[k] = sum of y_r^2 over tile k's rows (iterated mode), or null
+  IterOut it;         // row-aligned tiles: iterated-mode epilogue (iterfuse.cuh)
   int stages, rows_cap;
   int aligned;  // 1: row-aligned tiles (no row crosses a tile, no carries)
   int l2pf;     // 1: the producer prefetches the stage's next tile into L2
@@ -410,6 +411,8 @@ __global__ void __launch_bounds__(32 * (CW + 1),
   constexpr int GPW = 32 / VS;
   const int lane = lane32 % VS;
   const int gi = lane32 / VS;
+  const double fsc = AL ? iter_scale(p.it) : 1.0;  // pending exact rescale (iterated mode)
+  double wsq = 0.0;                                // (AL) squares of this warp's rows, its tiles in order
   for (int i = w;; i += CW) {
     const int64_t k = p.k0 + blockIdx.x + (int64_t)i * gridDim.x;
     if (k >= p.T) break;
@@ -528,6 +531,7 @@ __global__ void __launch_bounds__(32 * (CW + 1),
           acc = a0;
         }
         acc = group_sum<VS>(acc);
+        if constexpr (AL) acc *= fsc;
         if (active && lane == 0) {
           if (incoming && q == 0) {
             p.carry_row[k] = (int32_t)out_row(p, r);
@@ -539,16 +543,14 @@ __global__ void __launch_bounds__(32 * (CW + 1),
         }
       }
       if constexpr (AL) {
-        if (p.sq) {  // fixed butterfly over the lanes: deterministic per tile
-          sqa = warp_sum(sqa);
-          if (lane32 == 0) p.sq[k] = sqa;
-        }
+        if (p.it.cta_part) wsq += warp_sum(sqa);  // fixed butterfly over the lanes: deterministic per tile
       }
       if (!incoming && lane32 == 0) p.carry_row[k] = -1;
     }
     __syncwarp();
     if (lane32 == 0) mbar_arrive(&empty[s]);
   }
+  if constexpr (AL) iter_epilogue<32 * CW>(p.it, wsq);
 }
 
 template <typename RP>
@@ -570,7 +572,7 @@ static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y)
   p.C = sp.C;
   p.T = sp.T;
   p.k0 = sp.k0;
-  p.sq = sp.sq;
+  p.it = sp.it;
   p.stages = sp.stages;
   p.rows_cap = sp.rows_cap;
   p.aligned = sp.aligned ? 1 : 0;
@@ -670,9 +672,9 @@ int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int sta
 
 int launch_stream(const ExecArgs& a, cudaStream_t s) { return launch_stream_plan(a.sp[0], a.x, a.y, a.stage, s); }
 
-int launch_stream_sq(const StreamPlan& sp_in, const double* x, double* y, double* sq, cudaStream_t s) {
+int launch_stream_iter(const StreamPlan& sp_in, const double* x, double* y, const IterOut& it, cudaStream_t s) {
   StreamPlan sp = sp_in;
-  sp.sq = sq;
+  sp.it = it;
   stream_dispatch<false>(sp, 0, x, y, s);
   return 1;
 }

@@ -6,13 +6,14 @@ P:708-711, computed by ``spmv_shard_bounds``) and a full replica of x.
 * single SpMV: no collective; every rank writes its y block.
 * iterated mode (BJ.configs[5]), deferred normalisation (DESIGN.md reading
   25): two x replicas A, B; iteration k reads `cur` (x_0, then yh_{k-1}) and
-    1. yh_k block = A_g cur     (libspmv kernel, written straight into the
-                                 rank's block of `nxt`, plan stream)
-    2. partials_g = fixed-chunk sums of yh_k^2        (libspmv kernel)
-    3. all-gather of the partials (rank order)        -- NCCL
-    4. norm step on every rank (identical): nu_k = ||yh_k|| / ||yh_{k-1}||,
-       exact power-of-two rescale of the block when the magnitude drifts
-    5. the exchange of `nxt` blocks                   -- NCCL
+    1. yh_k block = s * A_g cur, s = the pending exact power-of-two rescale
+       of the previous step (nn[1]); partials_g = fixed-chunk sums of
+       yh_k^2 -- one libspmv call (spmv_iter_step), written straight into
+       the rank's block of `nxt` on the plan stream
+    2. all-gather of the partials (rank order)        -- NCCL
+    3. norm step on every rank (identical): nu_k = ||yh_k|| / ||yh_{k-1}||,
+       a pending rescale factor when the magnitude drifts (never in place)
+    4. the exchange of `nxt` blocks                   -- NCCL
        * all-gather(v): one broadcast per rank into its slice of every
          replica (blocks differ in size), or
        * halo exchange: rank g's rows only read x columns
@@ -20,8 +21,10 @@ P:708-711, computed by ``spmv_shard_bounds``) and a full replica of x.
          g just the part of its block inside that range (point-to-point);
          for banded matrices a few planes instead of the whole vector
          (27-pt 384^3 at G = 8: ~2.4 MB per rank per iteration vs 396 MB).
-  and swaps the replicas; no x = y / nu pass per iteration. At the end
-  x_iters = yh_{iters-1} / ||yh_{iters-1}|| over the replica.
+  and swaps the replicas; no x = y / nu pass per iteration. With one rank,
+  steps 1-3 are one fused call (the norm step runs in the SpMV kernel's
+  epilogue for row-aligned STREAM / D8 plans). At the end x_iters =
+  yh_{iters-1} * nn[1] / ||yh_{iters-1}|| over the replica.
 
 This module only orchestrates (argument marshalling, process-group calls);
 every arithmetic step runs in the native library. The step functions are
@@ -37,12 +40,11 @@ from typing import Callable, Optional, Sequence
 @dataclass
 class ShardSteps:
     """Per-rank local steps. Tensors are 1-D float64 on the rank's device."""
-    spmv: Callable[[object, object], None]            # (x_full, y_block): y_block = A_g x_full
-    partials: Callable[[object, object], None]        # (y_block, partials_local[P])
-    norm_step: Callable[[object, int, object, object, object], None]  # (partials_all, count, nn[2], nu[1], y_block)
-    unit: Callable[[object, object, object], None]    # (y, nn[2], x_out): x_out = y / nn[0]
-    # optional fused spmv + partials (x_full, y_block, partials_local)
-    spmv_partials: Optional[Callable[[object, object, object], None]] = None
+    # (x_full, y_block, partials_local[P], nn[2], nu[1] or None): y_block = nn[1] * A_g x_full (nn[1] = 0: 1),
+    # the partials of y_block^2, and the norm step on them when nu is given (one rank)
+    iter_step: Callable[[object, object, object, object, Optional[object]], None]
+    norm_step: Callable[[object, int, object, object], None]  # (partials_all, count, nn[2], nu[1])
+    unit: Callable[[object, object, object], None]    # (y, nn[2], x_out): x_out = y * nn[1] / nn[0]
     # optional context-manager factory making the steps' stream the current
     # one, so the collectives (issued on the current stream) are ordered with
     # the native steps (issued on the plan's stream)
@@ -113,14 +115,13 @@ def iterate(dist, steps: ShardSteps, bounds: Sequence[int], rank: int, world: in
         nn.zero_()
         cur, nxt = x_full, x_alt
         for k in range(iters):
-            if steps.spmv_partials is not None:
-                steps.spmv_partials(cur, nxt[b0:b1], partials_local)
+            if world == 1:  # the rank's partials are all of them: norm step fused into the step
+                steps.iter_step(cur, nxt[b0:b1], partials_local, nn, nu_hist[k:k + 1])
             else:
-                steps.spmv(cur, nxt[b0:b1])
-                steps.partials(nxt[b0:b1], partials_local)
-            dist.all_gather_into_tensor(partials_all, partials_local, group=group)
-            steps.norm_step(partials_all, world * P, nn, nu_hist[k:k + 1], nxt[b0:b1])
-            exchange_x(dist, bounds, rank, world, nxt, halo, group)
+                steps.iter_step(cur, nxt[b0:b1], partials_local, nn, None)
+                dist.all_gather_into_tensor(partials_all, partials_local, group=group)
+                steps.norm_step(partials_all, world * P, nn, nu_hist[k:k + 1])
+                exchange_x(dist, bounds, rank, world, nxt, halo, group)
             cur, nxt = nxt, cur
         steps.unit(cur, nn, x_full)
 
@@ -153,9 +154,7 @@ def native_steps(plan) -> ShardSteps:
 
     return ShardSteps(
         stream=stream,
-        spmv=lambda x, y: plan.execute_async(x, y),
-        partials=lambda y, p: plan.norm_partials(y, p),
-        norm_step=lambda pa, cnt, nn, nu, y: plan.norm_step(pa, cnt, nn, nu, y),
+        iter_step=lambda x, y, p, nn, nu: plan.iter_step(x, y, p, nn, nu),
+        norm_step=lambda pa, cnt, nn, nu: plan.norm_step(pa, cnt, nn, nu),
         unit=lambda y, nn, x: plan.unit(y, nn, x),
-        spmv_partials=lambda x, y, p: plan.execute_norm(x, y, p),
     )

@@ -127,7 +127,8 @@ def test_null_plan_arguments_fail_with_status_not_crash():
         "spmv_execute_async": (vp(None), buf, buf),
         "spmv_execute_norm": (vp(None), buf, buf, buf),
         "spmv_norm_partials": (vp(None), buf, buf),
-        "spmv_norm_step": (vp(None), buf, ctypes.c_int(4), buf, buf, buf),
+        "spmv_norm_step": (vp(None), buf, ctypes.c_int(4), buf, buf),
+        "spmv_iter_step": (vp(None), buf, buf, buf, buf, buf),
         "spmv_unit": (vp(None), buf, ctypes.c_int64(4), buf, buf),
     }
     for name, args in calls.items():

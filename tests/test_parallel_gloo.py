@@ -38,21 +38,25 @@ def _worker(rank, world, port, K, out_q, use_halo=False, cfg=5, scale=1.0):
         lrp = rp[b0:b1 + 1] - rp[b0]
         lci, lva = m.colind[rp[b0]:rp[b1]], m.vals[rp[b0]:rp[b1]] * scale
         P = 512
-        def norm_step(pa, cnt, nn, nu, y):  # the spmv_norm_step contract (include/spmv.h)
+        def norm_step(pa, cnt, nn, nu):  # the spmv_norm_step contract (include/spmv.h)
             n = math.sqrt(math.fsum(pa.numpy()[:cnt]))
             nu.fill_(n / float(nn[0]) if float(nn[0]) > 0 else n)
             e = math.frexp(n)[1] - 1 if n > 0 else 0
             f = math.ldexp(1.0, -e) if abs(e) > 256 else 1.0
-            nn[0], nn[1] = n * f, f
-            y.mul_(f)
+            nn[0], nn[1] = n * f, f  # the factor stays pending (applied by the next step / unit)
+
+        def iter_step(x, y, p, nn, nu):  # spmv_iter_step: y = nn[1] * A x, partials, fused norm step
+            f = float(nn[1]) if float(nn[1]) != 0 else 1.0
+            y.copy_(torch.from_numpy(oracle.spmv(lrp, lci, lva, x.numpy()) * f))
+            p.copy_(torch.tensor([float(np.sum(y.numpy()[q * y.numel() // P:(q + 1) * y.numel() // P] ** 2))
+                                  for q in range(P)], dtype=torch.float64))
+            if nu is not None:
+                norm_step(p, P, nn, nu)
 
         steps = parallel.ShardSteps(
-            spmv=lambda x, y: y.copy_(torch.from_numpy(oracle.spmv(lrp, lci, lva, x.numpy()))),
-            partials=lambda y, p: p.copy_(torch.tensor(
-                [float(np.sum(y.numpy()[q * y.numel() // P:(q + 1) * y.numel() // P] ** 2)) for q in range(P)],
-                dtype=torch.float64)),
+            iter_step=iter_step,
             norm_step=norm_step,
-            unit=lambda y, nn, x: x.copy_(y / nn[0]),
+            unit=lambda y, nn, x: x.copy_(y * (float(nn[1]) if float(nn[1]) != 0 else 1.0) / nn[0]),
         )
         x = torch.from_numpy(m.x.copy())
         x2 = torch.full_like(x, float("nan"))

@@ -1,6 +1,7 @@
 """Where the iterated mode's time goes (experiment tool): per-iteration device
 time of (a) the plain SpMV on the plan buffers, (b) the SpMV ping-ponging two
-replicas, (c) + fused norm partials, (d) + the norm step, (e) the full
+replicas, (c) the iteration step + a separate norm-step kernel, (d) the fused step
+(norm step in the SpMV epilogue), (e) the full
 parallel.iterate (world 1).  python tools/exp_iter.py --config 5 --iters 50"""
 import argparse, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -57,10 +58,10 @@ res = {"a_plain": timed(lambda k: p.execute_async(xd, yd))}
 reset()
 res["b_pingpong"] = timed(lambda k: p.execute_async(bufs[k & 1], bufs[(k + 1) & 1]))
 reset()
-res["c_fused_partials"] = timed(lambda k: p.execute_norm(bufs[k & 1], bufs[(k + 1) & 1], pl))
+res["c_step_then_norm"] = timed(lambda k: (p.iter_step(bufs[k & 1], bufs[(k + 1) & 1], pl, nn),
+                                           p.norm_step(pl, P, nn, nu[k:k + 1])))
 reset()
-res["d_plus_norm_step"] = timed(lambda k: (p.execute_norm(bufs[k & 1], bufs[(k + 1) & 1], pl),
-                                           p.norm_step(pl, P, nn, nu[k:k + 1], bufs[(k + 1) & 1])))
+res["d_fused_step"] = timed(lambda k: p.iter_step(bufs[k & 1], bufs[(k + 1) & 1], pl, nn, nu[k:k + 1]))
 reset()
 steps = parallel.native_steps(p)
 pa = pl
