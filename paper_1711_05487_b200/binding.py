@@ -110,7 +110,8 @@ lib.spmv_norm_partial_count.restype = _i32
 lib.spmv_norm_partials.argtypes = [_vp, _vp, _vp]
 lib.spmv_normalize.argtypes = [_vp, _vp, _vp, ctypes.c_int, _vp, _vp]
 lib.spmv_norm_step.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp]
-lib.spmv_iter_step.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+if hasattr(lib, "spmv_iter_step"):  # (experiment builds of older sources lack it)
+    lib.spmv_iter_step.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
 lib.spmv_execute_norm.argtypes = [_vp, _vp, _vp, _vp]
 lib.spmv_unit.argtypes = [_vp, _vp, ctypes.c_int64, _vp, _vp]
 lib.spmv_plan_query.argtypes = [_vp, ctypes.POINTER(PlanInfo)]

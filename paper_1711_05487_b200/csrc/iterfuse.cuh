@@ -18,9 +18,14 @@
 
 namespace spmv {
 
+// Values another kernel of the stream wrote (nn, partials, y) are read with
+// L2-coherent loads (__ldcg): with programmatic dependent launch the kernels
+// overlap, and an L1 line cached by a co-resident CTA of the previous kernel
+// (e.g. nn read at its start) can be stale after griddepcontrol.wait --
+// measured: the final unit read a pre-epilogue nn[1] through L1.
 __device__ __forceinline__ double iter_scale(const IterOut& it) {
   if (!it.scale) return 1.0;
-  const double f = *it.scale;
+  const double f = __ldcg(it.scale);
   return f != 0.0 ? f : 1.0;
 }
 
@@ -29,7 +34,7 @@ __device__ __forceinline__ double iter_scale(const IterOut& it) {
 // ||yh_k|| brought into [2^-256, 2^256] by an exact power of two, nn[1] =
 // that factor (applied to the block by the next SpMV / the final unit)
 __device__ __forceinline__ void norm_step_scalar(double ss, double* nn, double* nu_k) {
-  const double n = sqrt(ss), prev = nn[0];
+  const double n = sqrt(ss), prev = __ldcg(nn);
   *nu_k = prev > 0.0 ? n / prev : n;
   const int e = (n > 0.0 && isfinite(n)) ? ilogb(n) : 0;
   const bool rs = e > 256 || e < -256;  // squares stay far from overflow (2^1024)

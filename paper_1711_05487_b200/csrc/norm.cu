@@ -29,14 +29,14 @@ __global__ void __launch_bounds__(kNT) norm_partials_kernel(const double* __rest
   for (; i + 7 * kNT < r1; i += 8 * kNT) {
     double v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = ld_stream(y + i + u * kNT);
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(y + i + u * kNT);  // written by the previous kernel: L2-coherent
 #pragma unroll
     for (int u = 0; u < 8; ++u) a[u] = SQ ? fma(v[u], v[u], a[u]) : a[u] + v[u];
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u)
     if (i + u * kNT < r1) {
-      const double v = ld_stream(y + i + u * kNT);
+      const double v = __ldcg(y + i + u * kNT);
       a[u] = SQ ? fma(v, v, a[u]) : a[u] + v;
     }
   const double t = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kNT) norm_partials_kernel(const double* __rest
 // partials (~30 us for 512, the iterated mode's largest overhead on C5)
 __device__ __forceinline__ double block_sum_fixed(const double* __restrict__ partials, int count) {
   double a = 0.0;
-  for (int q = threadIdx.x; q < count; q += kNT) a += partials[q];
+  for (int q = threadIdx.x; q < count; q += kNT) a += __ldcg(partials + q);
   a = warp_sum(a);
   __shared__ double ws[kNT / 32];
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = a;
@@ -102,13 +102,13 @@ __global__ void __launch_bounds__(kNT) scale_partials_kernel(double* __restrict_
                                                              double* __restrict__ partials) {
   pdl_trigger();
   pdl_wait();
-  const double f0 = nn ? nn[1] : 1.0;
+  const double f0 = nn ? __ldcg(nn + 1) : 1.0;
   const double f = f0 != 0.0 ? f0 : 1.0;
   const int64_t b = blockIdx.x;
   const int64_t r0 = b * m / kNormPartials, r1 = (b + 1) * m / kNormPartials;
   double a = 0.0;
   for (int64_t i = r0 + threadIdx.x; i < r1; i += kNT) {
-    double v = y[i];
+    double v = __ldcg(y + i);
     if (f != 1.0) {
       v *= f;
       y[i] = v;
@@ -131,10 +131,10 @@ __global__ void __launch_bounds__(kNT) unit_kernel(const double* __restrict__ y,
                                                    const double* __restrict__ nn, double* __restrict__ x_out) {
   pdl_trigger();  // the next kernel in the stream may launch (it waits before reading)
   pdl_wait();
-  const double nu = nn[0];
-  const double f = nn[1] != 0.0 ? nn[1] : 1.0;
+  const double nu = __ldcg(nn), f1 = __ldcg(nn + 1);
+  const double f = f1 != 0.0 ? f1 : 1.0;
   const int64_t stride = (int64_t)gridDim.x * kNT;
-  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = (y[i] * f) / nu;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = (__ldcg(y + i) * f) / nu;
 }
 
 static int grid_for(int64_t m) {

@@ -60,11 +60,12 @@ __global__ void __launch_bounds__(kNT) split_epilogue_kernel(const int32_t* __re
   if ((int)blockIdx.x < nfb) {
     const int64_t k = (int64_t)blockIdx.x * kNT + threadIdx.x;
     if (k >= T) return;
-    const int32_t r = crow[k];
-    if (r < 0 || (k > 0 && crow[k - 1] == r)) return;
-    double s = cval[k];
-    for (int64_t q = k + 1; q < T && crow[q] == r; ++q) s += cval[q];
-    y[r] += s;
+    // (carries / partials / y come from the previous kernel: L2-coherent loads)
+    const int32_t r = __ldcg(crow + k);
+    if (r < 0 || (k > 0 && __ldcg(crow + k - 1) == r)) return;
+    double s = __ldcg(cval + k);
+    for (int64_t q = k + 1; q < T && __ldcg(crow + q) == r; ++q) s += __ldcg(cval + q);
+    y[r] = __ldcg(y + r) + s;
     return;
   }
   const int lane = threadIdx.x & 31;

@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(32 * (CW + 1),
   const int lane = lane32 % VS;
   const int gi = lane32 / VS;
   const double fsc = AL ? iter_scale(p.it) : 1.0;  // pending exact rescale (iterated mode)
-  double wsq = 0.0;                                // (AL) squares of this warp's rows, its tiles in order
+  double sqa = 0.0;  // (AL) this lane's squares over all its rows, its tiles in order (one warp sum at the end)
   for (int i = w;; i += CW) {
     const int64_t k = p.k0 + blockIdx.x + (int64_t)i * gridDim.x;
     if (k >= p.T) break;
@@ -451,7 +451,6 @@ __global__ void __launch_bounds__(32 * (CW + 1),
       seg_tile(p, vals_s, reinterpret_cast<const int32_t*>(idx_b),
                reinterpret_cast<double*>(smem + L.prod) + (size_t)w * p.C, rows, fr, nloc, t0, cnt, k, lane32);
     } else {
-      double sqa = 0.0;  // (AL) squares of the rows this lane group writes
       for (int qb = 0; qb < nloc; qb += GPW) {
         const int q = qb + gi;
         const bool active = q < nloc;
@@ -542,15 +541,12 @@ __global__ void __launch_bounds__(32 * (CW + 1),
           }
         }
       }
-      if constexpr (AL) {
-        if (p.it.cta_part) wsq += warp_sum(sqa);  // fixed butterfly over the lanes: deterministic per tile
-      }
       if (!incoming && lane32 == 0) p.carry_row[k] = -1;
     }
     __syncwarp();
     if (lane32 == 0) mbar_arrive(&empty[s]);
   }
-  if constexpr (AL) iter_epilogue<32 * CW>(p.it, wsq);
+  if constexpr (AL) iter_epilogue<32 * CW>(p.it, p.it.cta_part ? warp_sum(sqa) : 0.0);  // fixed butterfly
 }
 
 template <typename RP>

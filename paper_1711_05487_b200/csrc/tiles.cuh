@@ -348,11 +348,11 @@ __device__ __forceinline__ double long_row_total(const double* __restrict__ part
   int64_t b = lane;
   for (; b + 7 * 32 < nblk; b += 8 * 32) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] += partial[b + 32 * u];
+    for (int u = 0; u < 8; ++u) a[u] += __ldcg(partial + b + 32 * u);  // (previous kernel: L2-coherent)
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u)
-    if (b + 32 * u < nblk) a[u] += partial[b + 32 * u];
+    if (b + 32 * u < nblk) a[u] += __ldcg(partial + b + 32 * u);
   const double t = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   return warp_sum(t);
 }

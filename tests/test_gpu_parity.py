@@ -203,7 +203,7 @@ def test_configs_full_auto_selection(c):
     f = oracle.features(m.rowptr, m.colind)
     props = spmv.device_query(0)
     o = oracle.select(f, props["l2_bytes"], props["access_window_max"], m.rowptr.dtype.itemsize)
-    assert (info["sel"]["variant"], info["sel"]["vs"], bool(info["sel"]["d16"]), bool(info["sel"]["xwin"])) == \
+    assert (info["sel"]["variant"], info["sel"]["vs"], info["sel"]["d16"], bool(info["sel"]["xwin"])) == \
         (o.variant, o.vs, o.d16, o.xwin)
 
 

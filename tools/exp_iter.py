@@ -63,6 +63,10 @@ res["c_step_then_norm"] = timed(lambda k: (p.iter_step(bufs[k & 1], bufs[(k + 1)
 reset()
 res["d_fused_step"] = timed(lambda k: p.iter_step(bufs[k & 1], bufs[(k + 1) & 1], pl, nn, nu[k:k + 1]))
 reset()
+res["f_step_no_norm"] = timed(lambda k: p.iter_step(bufs[k & 1], bufs[(k + 1) & 1], pl, nn))
+reset()
+res["g_execute_norm"] = timed(lambda k: p.execute_norm(bufs[k & 1], bufs[(k + 1) & 1], pl))
+reset()
 steps = parallel.native_steps(p)
 pa = pl
 b = [0, n]
