@@ -339,7 +339,7 @@ def run_native(a):
         kc = max(3, min(a.steps, 10))
         for _ in range(kc):
             with torch.cuda.stream(stream):
-                torch.sum(flush, out=sink)
+                torch.sum(flush, dim=0, out=sink)
             s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
             step()
@@ -423,10 +423,16 @@ def run_native(a):
     # colind + rowptr, 16-bit deltas + heads, or D8 codes + row lengths)
     kbytes = int(info["kernel_bytes"])
     achieved = kbytes / (ms_main * 1e-3) / 1e9
-    traffic = None
+    # ncu DRAM bytes of one launch of this kernel (profiles/traffic.json, from
+    # tools/round2_profile.sh): the warm capture (--cache-control none, a
+    # back-to-back launch: the timed loop's L2 state), the cold one alongside
+    traffic, traffic_cold = None, None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tr.get(f"C{a.config}:{info['variant']}")
+        dmode = {0: "int32", 1: "d16", 2: "d8"}.get(info["sel"]["d16"], "")
+        key = f"C{a.config}:{info['variant']}" + (f":{dmode}" if info["variant"] == "stream" else "")
+        if world == 1 and key in tr:
+            traffic, traffic_cold = tr[key].get("warm"), tr[key].get("cold")
     except Exception:
         pass
 
@@ -459,7 +465,10 @@ def run_native(a):
                          "kernel": f"{info['variant']} main kernel (stage 1), rank 0",
                          "kernel_ms": ms_main, "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
                          # ncu DRAM bytes of one launch / this run's kernel time (SURVEY 8(d) "actual DRAM GB/s")
-                         "traffic_gbs": (traffic / (ms_main * 1e-3) / 1e9) if traffic else None},
+                         "traffic_gbs": (traffic / (ms_main * 1e-3) / 1e9) if traffic else None,
+                         "traffic_cold": traffic_cold,
+                         "traffic_source": "profiles/traffic.json: ncu dram__bytes_{read,write}.sum of one launch, "
+                                           "warm (--cache-control none, back-to-back) / cold (ncu cache flush)"},
             "cold_l2": cold,
             "paper_runs": paper_runs,
             "cpu_baseline": cpu,
