@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -27,6 +28,10 @@ namespace {
 thread_local spmv_status g_status = SPMV_OK;
 thread_local std::string g_msg;
 std::atomic<int64_t> g_launches{0};
+// live plans holding a persisting-L2 carve-out per device (the limit is
+// device-wide: reset only when the last such plan goes)
+std::mutex g_l2_mu;
+int g_l2_plans[64] = {0};
 
 struct Err : std::runtime_error {
   spmv_status st;
@@ -161,7 +166,7 @@ struct Shard {
   uint32_t* headbits = nullptr;
   DevStats* stats = nullptr;
   DevStats hs{};
-  int sm_count = 148;
+  int sm_count = 0;  // the shard device's multiProcessorCount (set at plan creation)
   // STREAM: sp[0] over the whole shard; SPLIT: sp[0] short bin, sp[1] medium bin
   StreamPlan sp[2];
   int n_sp = 0;
@@ -266,8 +271,20 @@ struct spmv_plan_s {
   ProfileBounds pb;          // profile-guided mode: measured / analytic bounds
   double profile_ms = 0.0;  // nnz_split hot-x set: fraction of nonzeros in the hot columns
 
+  bool l2_limit_set = false;  // this plan raised the device's persisting-L2 limit (x window)
   ~spmv_plan_s() {
     for (auto& s : shards) s.release();
+    if (l2_limit_set) {
+      std::lock_guard<std::mutex> lk(g_l2_mu);
+      for (auto& s : shards) {
+        if (s.dev < 0 || s.dev >= 64 || g_l2_plans[s.dev] <= 0) continue;
+        if (--g_l2_plans[s.dev] > 0) continue;
+        cudaSetDevice(s.dev);
+        cudaCtxResetPersistingL2Cache();  // demote persisting lines, then give the carve-out back
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        cudaGetLastError();
+      }
+    }
   }
   ExecArgs args(Shard& s, const double* x, double* y) const {
     ExecArgs a{};
@@ -1271,7 +1288,12 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       const size_t xb = (size_t)n_cols * 8;
       const size_t win = std::min<size_t>(xb, (size_t)P->props.access_window_max);
       const size_t persist = std::min<size_t>(win, (size_t)P->props.persisting_l2_max);
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist);
+      ck(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist), "persisting L2 limit");
+      {
+        std::lock_guard<std::mutex> lk(g_l2_mu);
+        if (s.dev >= 0 && s.dev < 64) ++g_l2_plans[s.dev];
+        P->l2_limit_set = true;
+      }
       cudaStreamAttrValue v;
       memset(&v, 0, sizeof v);
       v.accessPolicyWindow.base_ptr = s.x;

@@ -203,7 +203,7 @@ static void filtered_csr_t(const MatView& A, int64_t lo, int64_t hi, void* out_r
   filt_rowptr_kernel<RP><<<(int)nb, kNT, 0, s>>>(rp, A.m, lo, hi, scratch, (RP*)out_rp);
   if (out_col) {
     int64_t g = (A.m + 32 * 8 - 1) / (32 * 8);
-    if (g > 148 * 16) g = 148 * 16;
+    if (g > dev_sm_count() * 16) g = dev_sm_count() * 16;
     filt_copy_kernel<RP><<<(int)g, kNT, 0, s>>>(rp, A.col, A.val, A.m, lo, hi, (const RP*)out_rp, out_col, out_val);
   }
 }
@@ -261,7 +261,7 @@ __global__ void gather_rowptr_kernel(const RP* __restrict__ frp, const int32_t* 
 void launch_gather_rowptr(const void* frp, int rp_bytes, const int32_t* rows, int64_t n, int64_t m, void* out,
                           cudaStream_t s) {
   int64_t g = (n + 1 + kNT - 1) / kNT;
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > dev_sm_count() * 16) g = dev_sm_count() * 16;
   if (rp_bytes == 8)
     gather_rowptr_kernel<int64_t><<<(int)g, kNT, 0, s>>>((const int64_t*)frp, rows, n, m, (int64_t*)out);
   else

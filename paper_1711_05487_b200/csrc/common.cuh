@@ -149,6 +149,20 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// SM count of the current device (grid sizing of the helper kernels; the
+// persistent hot-path kernels take it from the plan's device properties)
+inline int dev_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
 // ---- warp / subwarp reductions (fixed butterfly order => deterministic) ----
 template <int VS>
 __device__ __forceinline__ double group_sum(double v) {

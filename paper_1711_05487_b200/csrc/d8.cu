@@ -330,7 +330,7 @@ void launch_d8_encode(const MatView& A, int64_t row0, const int32_t* dict_dev, i
                       cudaStream_t s) {
   if (A.m == 0) return;
   int64_t g = (A.m + kNT - 1) / kNT;
-  if (g > 148 * 32) g = 148 * 32;
+  if (g > dev_sm_count() * 32) g = dev_sm_count() * 32;
   if (A.rp_bytes == 8)
     d8_encode_kernel<int64_t><<<(unsigned)g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, A.m, row0, dict_dev, nd,
                                                           codes, rlen);

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kNT) validate_gaps_kernel(const int32_t* __res
 static int grid_for(int64_t work, int per_cta_min = kNT) {
   int64_t g = (work + per_cta_min - 1) / per_cta_min;
   if (g < 1) g = 1;
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > dev_sm_count() * 16) g = dev_sm_count() * 16;
   return (int)g;
 }
 

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kNT) unit_kernel(const double* __restrict__ y,
 
 static int grid_for(int64_t m) {
   int64_t g = (m + kNT - 1) / kNT;
-  if (g > 148 * 8) g = 148 * 8;
+  if (g > dev_sm_count() * 8) g = dev_sm_count() * 8;
   return (int)(g < 1 ? 1 : g);
 }
 
@@ -171,7 +171,7 @@ int launch_sum_partials(const double* v, int64_t n, double* partials, cudaStream
 int launch_normalize(const double* y, int64_t m, const double* partials, int count, double* x_out, double* nu_dev,
                      cudaStream_t s) {
   int64_t grid = (m + kNT - 1) / kNT;
-  if (grid > 148 * 8) grid = 148 * 8;
+  if (grid > dev_sm_count() * 8) grid = dev_sm_count() * 8;
   if (grid < 1) grid = 1;
   normalize_kernel<<<(int)grid, kNT, 0, s>>>(y, m, partials, count, x_out, nu_dev);
   return 1;

@@ -376,8 +376,8 @@ __global__ void hot_encode_kernel(int32_t* __restrict__ col, int64_t nnz, const 
 void launch_col_counts(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* cnt, int32_t* H, cudaStream_t s) {
   cudaMemsetAsync(cnt, 0, (size_t)n_cols * 4, s);
   cudaMemsetAsync(H, 0, (size_t)kHotBuckets * 4, s);
-  if (nnz > 0) col_count_kernel<<<148 * 16, kNT, 0, s>>>(col, nnz, cnt);
-  if (n_cols > 0) count_hist_kernel<<<148 * 8, kNT, 0, s>>>(cnt, n_cols, H);
+  if (nnz > 0) col_count_kernel<<<dev_sm_count() * 16, kNT, 0, s>>>(col, nnz, cnt);
+  if (n_cols > 0) count_hist_kernel<<<dev_sm_count() * 8, kNT, 0, s>>>(cnt, n_cols, H);
 }
 void launch_hot_flags(const int32_t* cnt, int64_t n_cols, int32_t t, int32_t* bsum, cudaStream_t s) {
   hot_flag_count_kernel<<<(int)((n_cols + 1023) / 1024), 1024, 0, s>>>(cnt, n_cols, t, bsum);
@@ -387,7 +387,7 @@ void launch_hot_write(const int32_t* cnt, int64_t n_cols, int32_t t, const int32
   hot_write_kernel<<<(int)((n_cols + 1023) / 1024), 1024, 0, s>>>(cnt, n_cols, t, boff, K, hot_cols, slot);
 }
 void launch_hot_encode(int32_t* col, int64_t nnz, const int32_t* slot, cudaStream_t s) {
-  if (nnz > 0) hot_encode_kernel<<<148 * 16, kNT, 0, s>>>(col, nnz, slot);
+  if (nnz > 0) hot_encode_kernel<<<dev_sm_count() * 16, kNT, 0, s>>>(col, nnz, slot);
 }
 
 }  // namespace spmv

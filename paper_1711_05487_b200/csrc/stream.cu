@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(kNT) range_colmax_kernel(const int32_t* __rest
 void launch_range_colmax(const int32_t* col, int64_t a, int64_t b, int32_t* out, cudaStream_t s) {
   if (b <= a) return;
   int64_t g = (b - a + kNT * 8 - 1) / (kNT * 8);
-  if (g > 148 * 8) g = 148 * 8;
+  if (g > dev_sm_count() * 8) g = dev_sm_count() * 8;
   range_colmax_kernel<<<(unsigned)g, kNT, 0, s>>>(col, a, b, out);
 }
 

@@ -701,3 +701,49 @@ def test_d16_row_tiles_random_x():
             assert info["stream_stages"] == 6
         assert_bound(p.execute(m.x), m)
         assert np.array_equal(p.export("decoded"), m.colind)
+
+
+def test_core_plan_create_signature():
+    # the north_star call exactly: spmv_plan_create(n, nnz, int64 rowptr, int32
+    # colind, fp64 values, ngpus) -> opaque plan (NULL on failure), spmv_execute,
+    # spmv_plan_destroy (include/spmv.h), through ctypes on host arrays
+    import ctypes
+    lib = spmv.binding.lib
+    m = sg.stencil(12, 27, x_seed=4)
+    rp = m.rowptr.astype(np.int64)
+    h = lib.spmv_plan_create(m.n, m.nnz, rp.ctypes.data, m.colind.ctypes.data, m.vals.ctypes.data, 1)
+    assert h
+    y = np.full(m.n, np.nan)
+    assert lib.spmv_execute(ctypes.c_void_p(h), m.x.ctypes.data, y.ctypes.data) == 0
+    assert_bound(y, m)
+    lib.spmv_plan_destroy(ctypes.c_void_p(h))
+    # failure leaves no plan: invalid CSR -> NULL and a located message
+    bad = rp.copy()
+    bad[-1] += 1
+    assert not lib.spmv_plan_create(m.n, m.nnz, bad.ctypes.data, m.colind.ctypes.data, m.vals.ctypes.data, 1)
+    assert lib.spmv_last_status() == -2 and b"rowptr[n] != nnz" in lib.spmv_last_error()
+    assert not lib.spmv_plan_create(m.n, m.nnz, rp.ctypes.data, m.colind.ctypes.data, m.vals.ctypes.data, 0)
+    assert lib.spmv_last_status() == -1
+
+
+def test_x_window_limit_reset_on_destroy():
+    # ML plans set a persisting-L2 carve-out for the x window; the last plan
+    # holding it gives it back on destroy
+    m = sg.config(3, small=True)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="nnzsplit", xwin=1)
+    assert p.info()["sel"]["xwin"] == 1
+    assert_bound(p.execute(m.x), m)
+    assert _persist_limit() > 0
+    p.destroy()
+    assert _persist_limit() == 0
+
+
+def _persist_limit():
+    # the device-wide limit through the CUDA runtime (same primary context)
+    import ctypes
+    import glob
+    libs = sorted(glob.glob("/usr/local/cuda/lib64/libcudart.so*"))
+    rt = ctypes.CDLL(libs[0])
+    v = ctypes.c_size_t(0)
+    assert rt.cudaDeviceGetLimit(ctypes.byref(v), 0x06) == 0  # cudaLimitPersistingL2CacheSize
+    return v.value

@@ -14,6 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 src = os.path.join(ROOT, "gpurun_out", "prof")
 dst = os.path.join(ROOT, "profiles")
 tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
+TUNIT = {"usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "nsecond": 1e-3, "ns": 1e-3, "second": 1e6, "s": 1e6}
 UNIT = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
 
 
@@ -64,7 +65,7 @@ for c in ("5", "2", "3", "4", "5_int32"):
         m = res[0]
         ent["cold"] = nbytes(m["dram__bytes_read.sum"]) + nbytes(m["dram__bytes_write.sum"])
         tv, tu = m["gpu__time_duration.sum"].split()[:2]
-        ent["cold_us"] = float(tv.replace(",", "")) * {"usecond": 1.0, "msecond": 1e3, "nsecond": 1e-3}.get(tu, 1.0)
+        ent["cold_us"] = float(tv.replace(",", "")) * TUNIT.get(tu, 1.0)
     wp = os.path.join(src, f"warm_c{c}.csv")
     if os.path.exists(wp):
         w = warm_metrics(wp)
@@ -72,7 +73,7 @@ for c in ("5", "2", "3", "4", "5_int32"):
             rd = w["dram__bytes_read.sum"][0] * UNIT.get(w["dram__bytes_read.sum"][1], 1.0)
             wr = w["dram__bytes_write.sum"][0] * UNIT.get(w["dram__bytes_write.sum"][1], 1.0)
             t = w["gpu__time_duration.sum"]
-            us = t[0] * {"usecond": 1.0, "msecond": 1e3, "nsecond": 1e-3}.get(t[1], 1.0)
+            us = t[0] * TUNIT.get(t[1], 1.0)
             ent["warm"] = rd + wr
             ent["warm_us"] = us
             with open(os.path.join(dst, f"{tag}_ncu_warm_c{c}.txt"), "w") as f:
