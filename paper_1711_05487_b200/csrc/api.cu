@@ -31,6 +31,7 @@ std::atomic<int64_t> g_launches{0};
 // live plans holding a persisting-L2 carve-out per device (the limit is
 // device-wide: reset only when the last such plan goes)
 std::mutex g_l2_mu;
+constexpr int kIterRegions = 3;  // iterated mode: partials of up to 3 launches per shard (interior + 2 boundary)
 int g_l2_plans[64] = {0};
 
 struct Err : std::runtime_error {
@@ -196,7 +197,13 @@ struct Shard {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // iterated mode
-  double* allpart = nullptr;  // 2 x G * kNormPartials (iteration parity: double-buffered)
+  double* allpart = nullptr;  // [2 parities][G shards][kIterRegions launches][kNormPartials]
+  // interior-first iteration: tiles [kb, ke) read only the
+  // shard's own x block, the others wait for the halo copies
+  bool ovl_ready = false, ovl = false;
+  int64_t kb = 0, ke = 0;
+  cudaStream_t cp = nullptr;     // halo copy stream
+  cudaEvent_t ev_cp = nullptr;   // halo copies of the current iteration done
   double* x2 = nullptr;       // second x replica (deferred-normalisation ping-pong)
   double* cta_part = nullptr; // per-CTA sums of y^2 (fused iteration epilogue, row-aligned STREAM / D8)
   unsigned int* done = nullptr;  // its last-CTA ticket counter
@@ -236,6 +243,10 @@ struct Shard {
     allocs.clear();
     if (ev_part) cudaEventDestroy(ev_part);
     if (ev_x) cudaEventDestroy(ev_x);
+    if (ev_cp) cudaEventDestroy(ev_cp);
+    if (cp) cudaStreamDestroy(cp);
+    ev_cp = nullptr;
+    cp = nullptr;
     for (cudaEvent_t e : hp.ev_h) cudaEventDestroy(e);
     for (cudaEvent_t e : hp.ev_c) cudaEventDestroy(e);
     hp.ev_h.clear();
@@ -842,6 +853,8 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       const int64_t ml = std::max<int64_t>(maxlen, 1);
       int cw = 0;
       if (const char* e = getenv("SPMV_D8_CW")) cw = atoi(e);  // experiments: 4, 6 or 8
+      sp.d8_un = 8;
+      if (const char* e = getenv("SPMV_D8_UN")) sp.d8_un = atoi(e) == 16 ? 16 : 8;  // experiments: 8 or 16
       // shrink the tile until 4 stages fit (long rows of a forced D8 plan)
       while (Rt > 16 && d8_smem_bytes(Rt * ml, Rt, 4) > 227 * 1024) Rt -= 16;
       sp.rows_per_tile = Rt;
@@ -1271,7 +1284,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     }
     s.x = s.alloc<double>((size_t)n_cols);
     s.y = s.alloc<double>((size_t)s.m);
-    s.allpart = s.alloc<double>((size_t)2 * kNormPartials * ngpus);
+    s.allpart = s.alloc<double>((size_t)2 * kIterRegions * kNormPartials * ngpus);
   }
   for (auto& s : P->shards) {
     ck(cudaStreamSynchronize(s.stream), "structures");
@@ -1690,6 +1703,62 @@ int spmv_iter(const spmv_plan_s* P, Shard& s, const double* x, double* y, double
   return n;
 }
 
+// tiles [k0, k1) of a fused-capable plan with the iteration epilogue (partials
+// of this launch only; the pending rescale nn[1] applied; no norm step)
+int spmv_iter_range(const spmv_plan_s* P, Shard& s, const double* x, double* y, double* partials, double* nn,
+                    int64_t k0, int64_t k1) {
+  if (k1 <= k0) {
+    ck(cudaMemsetAsync(partials, 0, kNormPartials * 8, s.stream), "memset");
+    return 0;
+  }
+  (void)P;
+  if (!s.cta_part) {
+    s.cta_part = s.alloc<double>((size_t)std::max(s.sp[0].grid, 1));
+    s.done = s.alloc<unsigned int>(1);
+    ck(cudaMemsetAsync(s.done, 0, sizeof(unsigned int), s.stream), "memset");
+  }
+  IterOut it;
+  it.scale = nn + 1;
+  it.cta_part = s.cta_part;
+  it.done = s.done;
+  it.partials = partials;
+  return launch_stream_iter_range(s.sp[0], x, y, it, k0, k1, s.stream);
+}
+
+// interior tile range of shard s: tiles whose nonzeros read only x[row0,
+// row0 + m) (its own block). Banded row blocks: one contiguous range between
+// the tiles reading the lower and the upper halo. Used when it is at least a
+// quarter of the tiles.
+void prepare_overlap(const spmv_plan_s* P, Shard& s) {
+  if (s.ovl_ready) return;
+  s.ovl_ready = true;
+  const StreamPlan& sp = s.sp[0];
+  const bool fused = P->sel.variant == SPMV_VARIANT_STREAM && sp.aligned && !sp.seg && !sp.rowmap &&
+                     !sp.need_fixup && sp.tile_nz && !getenv("SPMV_NO_FUSED_NORM") && !getenv("SPMV_NO_OVERLAP");
+  ck(cudaSetDevice(s.dev), "cudaSetDevice");
+  ck(cudaStreamCreateWithFlags(&s.cp, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaEventCreateWithFlags(&s.ev_cp, cudaEventDisableTiming), "cudaEventCreate");
+  if (!fused || s.nnz == 0 || sp.T < 8) return;
+  unsigned long long* ext = s.alloc<unsigned long long>(2);
+  unsigned long long h[2] = {0ull, (unsigned long long)s.nnz};
+  ck(cudaMemcpyAsync(ext, h, 16, cudaMemcpyHostToDevice, s.stream), "halo extent");
+  launch_halo_extent(s.col, s.nnz, s.row0, s.row0 + s.m, ext, s.stream);
+  count_launches(1, "halo extent");
+  std::vector<int64_t> tz((size_t)sp.T + 1);
+  ck(cudaMemcpyAsync(h, ext, 16, cudaMemcpyDeviceToHost, s.stream), "halo extent");
+  ck(cudaMemcpyAsync(tz.data(), sp.tile_nz, (size_t)(sp.T + 1) * 8, cudaMemcpyDeviceToHost, s.stream), "tile_nz");
+  ck(cudaStreamSynchronize(s.stream), "halo extent");
+  // tile holding nonzero j: the largest k with tz[k] <= j
+  auto tile_of = [&](int64_t j) { return (int64_t)(std::upper_bound(tz.begin(), tz.end() - 1, j) - tz.begin()) - 1; };
+  const int64_t kb = h[0] == 0 ? 0 : tile_of((int64_t)h[0] - 1) + 1;
+  const int64_t ke = h[1] >= (unsigned long long)s.nnz ? sp.T : tile_of((int64_t)h[1]);
+  if (ke - kb >= sp.T / 4) {
+    s.ovl = true;
+    s.kb = kb;
+    s.ke = ke;
+  }
+}
+
 // ML x-window on the replica the next SpMV reads (the iterate ping-pongs)
 void set_xwin(const spmv_plan_s* P, Shard& s, const double* base) {
   if (!P->sel.xwin) return;
@@ -1760,27 +1829,73 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
       cur[g] = s.x;
       nxt[g] = s.x2;
     }
+    // multi-shard: interior tiles of every shard first (they read only its own
+    // x block), the halo copies of the other blocks concurrently on a copy
+    // stream, then the boundary tiles
+    if (G > 1)
+      for (auto& s : p->shards) prepare_overlap(p, s);
     for (int k = 0; k < iters; ++k) {
       // partials of iteration k live in half (k & 1) of every shard's allpart:
       // shard h may run ahead of a peer that has not yet copied h's partials
       // of iteration k (non-neighbour shards never wait on each other's x
       // halo), but not by two iterations -- its norm step k+1 waits for every
       // peer's partials of k+1, which follow that peer's copies of k
-      const size_t half = (size_t)(k & 1) * G * kNormPartials;
-      for (int g = 0; g < G; ++g) {
-        Shard& s = p->shards[g];
-        ck(cudaSetDevice(s.dev), "cudaSetDevice");
-        set_xwin(p, s, cur[g]);
-        // one shard: the norm step runs inside the SpMV's epilogue (fused plans)
-        count_launches(spmv_iter(p, s, cur[g], nxt[g] + s.row0, s.allpart + half + (size_t)g * kNormPartials, s.nn,
-                                 G == 1 ? s.nu + k : nullptr),
-                       "iteration step");
-        ck(cudaEventRecord(s.ev_part, s.stream), "event");
-      }
+      const size_t RP = (size_t)kIterRegions * kNormPartials;
+      const size_t half = (size_t)(k & 1) * G * RP;
       if (G == 1) {
+        Shard& s = p->shards[0];
+        set_xwin(p, s, cur[0]);
+        // one shard: the norm step runs inside the SpMV's epilogue (fused plans)
+        count_launches(spmv_iter(p, s, cur[0], nxt[0] + s.row0, s.allpart + half, s.nn, s.nu + k), "iteration step");
         std::swap(cur, nxt);
         continue;
       }
+      // A. interior tiles (overlap-capable shards)
+      for (int g = 0; g < G; ++g) {
+        Shard& s = p->shards[g];
+        if (!s.ovl || k == 0) continue;
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        set_xwin(p, s, cur[g]);
+        double* part = s.allpart + half + (size_t)g * RP;
+        count_launches(spmv_iter_range(p, s, cur[g], nxt[g] + s.row0, part, s.nn, s.kb, s.ke), "interior tiles");
+      }
+      // B. halo of yh_{k-1}: the part of each other block inside the x range
+      // shard g reads, copied into g's replica (not needed at k = 0: every
+      // replica holds x_0)
+      if (k > 0)
+        for (int g = 0; g < G; ++g) {
+          Shard& s = p->shards[g];
+          ck(cudaSetDevice(s.dev), "cudaSetDevice");
+          const int64_t lo = s.hs.col_min, hi = s.hs.col_max + 1;
+          for (int h = 0; h < G; ++h) {
+            if (h == g) continue;
+            Shard& t = p->shards[h];
+            const int64_t a = std::max<int64_t>(lo, t.row0), b = std::min<int64_t>(hi, t.row0 + t.m);
+            if (a >= b) continue;
+            ck(cudaStreamWaitEvent(s.cp, t.ev_part, 0), "wait");  // h's yh_{k-1} complete
+            ck(cudaMemcpyPeerAsync(cur[g] + a, s.dev, cur[h] + a, t.dev, (size_t)(b - a) * 8, s.cp), "x halo");
+          }
+          ck(cudaEventRecord(s.ev_cp, s.cp), "event");
+        }
+      // C. boundary tiles (or the whole shard) once the halo is in
+      for (int g = 0; g < G; ++g) {
+        Shard& s = p->shards[g];
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        if (k > 0) ck(cudaStreamWaitEvent(s.stream, s.ev_cp, 0), "wait");
+        double* part = s.allpart + half + (size_t)g * RP;
+        if (s.ovl && k > 0) {
+          count_launches(spmv_iter_range(p, s, cur[g], nxt[g] + s.row0, part + kNormPartials, s.nn, 0, s.kb) +
+                             spmv_iter_range(p, s, cur[g], nxt[g] + s.row0, part + 2 * kNormPartials, s.nn, s.ke,
+                                             s.sp[0].T),
+                         "boundary tiles");
+        } else {
+          set_xwin(p, s, cur[g]);
+          count_launches(spmv_iter(p, s, cur[g], nxt[g] + s.row0, part, s.nn, nullptr), "iteration step");
+          ck(cudaMemsetAsync(part + kNormPartials, 0, 2 * kNormPartials * 8, s.stream), "memset");
+        }
+        ck(cudaEventRecord(s.ev_part, s.stream), "event");
+      }
+      // D. every shard gathers all partials (rank order) and runs the norm step
       for (int g = 0; g < G; ++g) {
         Shard& s = p->shards[g];
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -1788,30 +1903,11 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
           if (h == g) continue;
           Shard& t = p->shards[h];
           ck(cudaStreamWaitEvent(s.stream, t.ev_part, 0), "wait");
-          ck(cudaMemcpyPeerAsync(s.allpart + half + (size_t)h * kNormPartials, s.dev,
-                                 t.allpart + half + (size_t)h * kNormPartials, t.dev, kNormPartials * 8, s.stream),
+          ck(cudaMemcpyPeerAsync(s.allpart + half + (size_t)h * RP, s.dev, t.allpart + half + (size_t)h * RP, t.dev,
+                                 RP * 8, s.stream),
              "partials exchange");
         }
-        count_launches(launch_norm_step(s.allpart + half, G * kNormPartials, s.nn, s.nu + k, s.stream), "norm step");
-        ck(cudaEventRecord(s.ev_x, s.stream), "event");
-      }
-      if (G > 1) {
-        for (int g = 0; g < G; ++g) {
-          Shard& s = p->shards[g];
-          ck(cudaSetDevice(s.dev), "cudaSetDevice");
-          // halo exchange: shard g only reads x[col_min_g,
-          // col_max_g], so it copies just the part of each other block inside
-          // that range (banded matrices: a few planes, not the whole vector)
-          const int64_t lo = s.hs.col_min, hi = s.hs.col_max + 1;
-          for (int h = 0; h < G; ++h) {
-            if (h == g) continue;
-            Shard& t = p->shards[h];
-            const int64_t a = std::max<int64_t>(lo, t.row0), b = std::min<int64_t>(hi, t.row0 + t.m);
-            if (a >= b) continue;
-            ck(cudaStreamWaitEvent(s.stream, t.ev_x, 0), "wait");
-            ck(cudaMemcpyPeerAsync(nxt[g] + a, s.dev, nxt[h] + a, t.dev, (size_t)(b - a) * 8, s.stream), "x halo");
-          }
-        }
+        count_launches(launch_norm_step(s.allpart + half, (int)(G * RP), s.nn, s.nu + k, s.stream), "norm step");
       }
       std::swap(cur, nxt);
     }

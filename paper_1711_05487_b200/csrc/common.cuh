@@ -10,6 +10,16 @@
 #error "libspmv targets sm_100a only"
 #endif
 
+// Checked build (tools/build_variant.sh checks -DSPMV_CHECKS): device-side
+// bounds asserts in the hot kernels (compute-sanitizer is not available on
+// the GPU pool); compiled out of the product build
+#ifdef SPMV_CHECKS
+#include <cassert>
+#define SPMV_CHECK(c) assert(c)
+#else
+#define SPMV_CHECK(c) ((void)0)
+#endif
+
 namespace spmv {
 
 

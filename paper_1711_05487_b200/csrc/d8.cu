@@ -21,6 +21,7 @@
 // gathers in flight per lane, dictionary in shared memory.
 #include <cstdlib>
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -42,8 +43,8 @@ __host__ __device__ inline D8Layout d8_layout(int64_t C, int64_t Rt, int stages)
   // t0) and is rounded up to 16 B (<= 1 after)
   L.codes = d8_al128((size_t)(C + 16) * 8);
   // codes: copy starts 16-B aligned (<= 15 before t0), rounded up to 16 B,
-  // plus >= 8 readable bytes past any row end (branch-free 8-code batches)
-  L.rl = L.codes + d8_al128((size_t)C + 48);
+  // plus >= 16 readable bytes past any row end (branch-free 16-code batches)
+  L.rl = L.codes + d8_al128((size_t)C + 64);
   L.stage = d8_al128(L.rl + (size_t)Rt + 16);
   size_t o = L.stage * stages;
   L.full = o; o += 8 * (size_t)stages;
@@ -71,6 +72,7 @@ struct D8P {
   int64_t m, T, k0; // rows, end of the tile range, first tile
   int64_t Rt, C;    // rows per tile, nonzero capacity
   int64_t row0;     // row id of local row 0 (the anchor of the head deltas)
+  int64_t n_cols;   // (checked build only)
   int stages;
   int32_t dict[256];
 };
@@ -81,7 +83,7 @@ __device__ __forceinline__ void d8_arrive(uint64_t* bar) {
 
 // Consumer warps' tile loop; returns the warp's sum of squares of the rows it
 // wrote (its tiles in launch order; 0 outside the iterated mode).
-template <int CW, bool SCALE>
+template <int CW, bool SCALE, int UN>
 __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, const D8Layout& L, uint64_t* full,
                                              uint64_t* empty, const D8Meta* meta, const int32_t* dict_s, double f) {
   const int S = p.stages;
@@ -94,6 +96,7 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
     const int s = i % S;
     mbar_wait(&full[s], (uint32_t)((i / S) & 1));
     const D8Meta mt = meta[s];
+    SPMV_CHECK(mt.cnt >= 0 && mt.cnt <= p.C && mt.voff >= 0 && mt.voff < 16);
     const unsigned char* st = smem + L.stage * s;
     const double* vals_s = reinterpret_cast<const double*>(st + L.vals) + mt.voff;
     const uint8_t* codes_s = st + L.codes + (mt.t0 & 15);
@@ -112,24 +115,28 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
       }
       const int off = base + inc - len;
       base += __shfl_sync(0xffffffffu, inc, 31);
+      SPMV_CHECK(off + len <= mt.cnt && len <= 255);
       int c = (int)(p.row0 + R0 + q);  // anchor of the head delta
       double a0 = 0.0, a1 = 0.0;
-      for (int l0 = 0; l0 < len; l0 += 8) {
-        // 8 codes read unconditionally (the stage keeps >= 8 bytes of slack
+      for (int l0 = 0; l0 < len; l0 += UN) {
+        // UN codes read unconditionally (the stage keeps >= 16 bytes of slack
         // past the tile; a stale code still indexes the 256-entry dictionary)
-        // and masked by selects: no branch around the shared-memory loads
-        int cc[8];
-        double xv[8];
+        // and masked by selects: no branch around the shared-memory loads;
+        // UN independent x gathers in flight per lane
+        int cc[UN];
+        double xv[UN];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < UN; ++u) {
           const int d = dict_s[codes_s[off + l0 + u]];
           c += (l0 + u < len) ? d : 0;
           cc[u] = c;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) xv[u] = l0 + u < len ? ld_x(p.x + cc[u]) : 0.0;
+        for (int u = 0; u < UN; ++u) SPMV_CHECK(l0 + u >= len || (cc[u] >= 0 && cc[u] < p.n_cols));
 #pragma unroll
-        for (int u = 0; u < 8; u += 2) {
+        for (int u = 0; u < UN; ++u) xv[u] = l0 + u < len ? ld_x(p.x + cc[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < UN; u += 2) {
           const int l = l0 + u;
           a0 = fma(l < len ? vals_s[off + l] : 0.0, xv[u], a0);
           a1 = fma(l + 1 < len ? vals_s[off + l + 1] : 0.0, xv[u + 1], a1);
@@ -138,6 +145,7 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
       double acc = a0 + a1;
       if constexpr (SCALE) acc *= f;
       if (q < nrows) {
+        SPMV_CHECK(R0 + q < p.m);
         p.y[R0 + q] = acc;
         sqa = fma(acc, acc, sqa);
       }
@@ -150,8 +158,12 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
   return p.it.cta_part ? warp_sum(sqa) : 0.0;  // fixed butterfly: deterministic
 }
 
-template <int CW>
-__global__ void __launch_bounds__(32 * (CW + 1), CW == 4 ? 5 : (CW == 6 ? 4 : 3)) d8_kernel(const D8P p) {
+// resident CTAs per SM the registers allow (launch bound): UN = 8 -> ~72
+// registers, UN = 16 -> ~96
+constexpr int d8_lb(int CW, int UN) { return UN == 8 ? (CW == 4 ? 5 : (CW == 6 ? 4 : 3)) : (CW == 4 ? 4 : (CW == 6 ? 3 : 2)); }
+
+template <int CW, int UN>
+__global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const D8P p) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int32_t dict_s[256];
   const D8Layout L = d8_layout(p.C, p.Rt, p.stages);
@@ -219,8 +231,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), CW == 4 ? 5 : (CW == 6 ? 4 : 3)
   // multiply or live f (measured: the scaled loop alone in the kernel cost
   // 7 % on C5, 2.368 vs 2.210 ms, through code generation)
   const double f = iter_scale(p.it);
-  const double wsq = f == 1.0 ? d8_consume<CW, false>(p, smem, L, full, empty, meta, dict_s, 1.0)
-                              : d8_consume<CW, true>(p, smem, L, full, empty, meta, dict_s, f);
+  const double wsq = f == 1.0 ? d8_consume<CW, false, UN>(p, smem, L, full, empty, meta, dict_s, 1.0)
+                              : d8_consume<CW, true, UN>(p, smem, L, full, empty, meta, dict_s, f);
   iter_epilogue<32 * CW>(p.it, wsq);
 }
 
@@ -239,18 +251,19 @@ static D8P d8_params(const StreamPlan& sp, const double* x, double* y) {
   p.Rt = sp.rows_per_tile;
   p.C = sp.C;
   p.row0 = sp.row0;
+  p.n_cols = sp.V.n_cols;
   p.stages = sp.stages;
   for (int i = 0; i < 256; ++i) p.dict[i] = i < sp.n_dict ? sp.dict[i] : 0;
   return p;
 }
 
-template <int CW>
+template <int CW, int UN>
 static int d8_prepare_t(const StreamPlan& sp, int sm_count) {
   const size_t smem = d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages);
-  if (cudaFuncSetAttribute(d8_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (cudaFuncSetAttribute(d8_kernel<CW, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW>, 32 * (CW + 1), smem) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN>, 32 * (CW + 1), smem) != cudaSuccess ||
       per_sm < 1)
     return -1;
   if (const char* e = getenv("SPMV_STREAM_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));  // experiments
@@ -259,41 +272,50 @@ static int d8_prepare_t(const StreamPlan& sp, int sm_count) {
   return (int)std::max<int64_t>(grid, 1);
 }
 
-template <int CW>
+template <int CW, int UN>
 static int d8_per_sm_t(const StreamPlan& sp) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW>, 32 * (CW + 1),
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN>, 32 * (CW + 1),
                                                     d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages)) != cudaSuccess)
     return 0;
   return per_sm;
 }
 
-int d8_per_sm(const StreamPlan& sp) {
-  switch (sp.stages) {
-    case 4: return d8_per_sm_t<4>(sp);
-    case 6: return d8_per_sm_t<6>(sp);
-    case 8: return d8_per_sm_t<8>(sp);
-    default: return 0;
-  }
+template <int CW, int UN>
+static void d8_launch_t(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
+  launch_pdl(d8_kernel<CW, UN>, dim3(sp.grid), dim3(32 * (CW + 1)), d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages),
+             s, d8_params(sp, x, y));
 }
 
-int d8_prepare(const StreamPlan& sp, int sm_count) {
+// (stages = consumer warps CW) x (batch width UN) -> instantiation
+template <int UN, typename F>
+static int d8_cw(const StreamPlan& sp, F&& f) {
   switch (sp.stages) {
-    case 4: return d8_prepare_t<4>(sp, sm_count);
-    case 6: return d8_prepare_t<6>(sp, sm_count);
-    case 8: return d8_prepare_t<8>(sp, sm_count);
+    case 4: return f(std::integral_constant<int, 4>{}, std::integral_constant<int, UN>{});
+    case 6: return f(std::integral_constant<int, 6>{}, std::integral_constant<int, UN>{});
+    case 8: return f(std::integral_constant<int, 8>{}, std::integral_constant<int, UN>{});
     default: return -1;
   }
 }
+template <typename F>
+static int d8_dispatch(const StreamPlan& sp, F&& f) {
+  return sp.d8_un == 16 ? d8_cw<16>(sp, f) : d8_cw<8>(sp, f);
+}
+
+int d8_per_sm(const StreamPlan& sp) {
+  const int r = d8_dispatch(sp, [&](auto cw, auto un) { return d8_per_sm_t<cw.value, un.value>(sp); });
+  return r < 0 ? 0 : r;
+}
+
+int d8_prepare(const StreamPlan& sp, int sm_count) {
+  return d8_dispatch(sp, [&](auto cw, auto un) { return d8_prepare_t<cw.value, un.value>(sp, sm_count); });
+}
 
 void launch_d8(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
-  const size_t smem = d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages);
-  const D8P p = d8_params(sp, x, y);
-  switch (sp.stages) {
-    case 4: launch_pdl(d8_kernel<4>, dim3(sp.grid), dim3(32 * 5), smem, s, p); break;
-    case 6: launch_pdl(d8_kernel<6>, dim3(sp.grid), dim3(32 * 7), smem, s, p); break;
-    default: launch_pdl(d8_kernel<8>, dim3(sp.grid), dim3(32 * 9), smem, s, p); break;
-  }
+  d8_dispatch(sp, [&](auto cw, auto un) {
+    d8_launch_t<cw.value, un.value>(sp, x, y, s);
+    return 0;
+  });
 }
 
 // ---- plan time ----------------------------------------------------------------

@@ -98,6 +98,7 @@ struct StreamPlan {
   int32_t dict[256] = {};
   int64_t row0 = 0;            // row id of local row 0 (anchor of the head deltas)
   const int32_t* d8_dict_dev = nullptr;  // the dictionary on the device (export decode)
+  int d8_un = 8;               // D8 codes decoded + x gathers in flight per lane per batch (8 or 16)
 };
 size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages);
 int d8_prepare(const StreamPlan& sp, int sm_count);  // stages = consumer warps (4, 6, 8)
@@ -108,6 +109,13 @@ void launch_d8_encode(const MatView& A, int64_t row0, const int32_t* dict_dev, i
 void launch_d8_decode_export(const StreamPlan& sp, const int32_t* dict_dev, int32_t* out, cudaStream_t s);
 // row-aligned STREAM / D8 plan (no fix-up) with the iterated-mode epilogue
 int launch_stream_iter(const StreamPlan& sp, const double* x, double* y, const IterOut& it, cudaStream_t s);
+// the same over tiles [k0, k1) (the epilogue folds this launch's CTAs only)
+int launch_stream_iter_range(const StreamPlan& sp, const double* x, double* y, const IterOut& it, int64_t k0,
+                             int64_t k1, cudaStream_t s);
+// out[0] = 1 + largest nonzero index with col < lo (0: none), out[1] = smallest
+// with col >= hi (nnz: none); out preset to {0, nnz} by the caller
+void launch_halo_extent(const int32_t* col, int64_t nnz, int64_t lo, int64_t hi, unsigned long long* out,
+                        cudaStream_t s);
 void launch_tile_rows_count(int32_t* tile_row, int64_t T, int64_t rows_per_tile, int64_t m, cudaStream_t s);
 // tiles [k0, k1) of a STREAM plan (+ the fix-up of their carries); the rows
 // cut at k0 / k1 are completed by the neighbouring ranges' fix-ups

@@ -121,6 +121,7 @@ struct StreamP {
   int32_t* carry_row;
   double* carry_val;
   int64_t nnz, C, T;  // T: end of the tile range
+  int64_t n_cols;     // (checked build only)
   int64_t k0;         // first tile of the range
   IterOut it;         // row-aligned tiles: iterated-mode epilogue (iterfuse.cuh)
   int stages, rows_cap;
@@ -461,6 +462,7 @@ __global__ void __launch_bounds__(32 * (CW + 1),
           const int64_t a = rows(r), b = rows(r + 1);
           ls = (int)((a > t0 ? a : t0) - t0);
           le = (int)((b < t1 ? b : t1) - t0);
+          SPMV_CHECK(ls >= 0 && ls <= le && le <= cnt);
         }
         double acc;
         if constexpr (!D16) {
@@ -474,6 +476,7 @@ __global__ void __launch_bounds__(32 * (CW + 1),
 #pragma unroll
             for (int u = 0; u < UN; ++u) {
               const int l = l0 + u * VS;
+              SPMV_CHECK(l >= le || (idx_s[l] >= 0 && (int64_t)idx_s[l] < p.n_cols));
               xv[u] = l < le ? ld_x(p.x + idx_s[l]) : 0.0;
             }
 #pragma unroll
@@ -565,6 +568,7 @@ static StreamP<RP> make_params(const StreamPlan& sp, const double* x, double* y)
   p.carry_row = sp.carry_row;
   p.carry_val = sp.carry_val;
   p.nnz = sp.V.nnz;
+  p.n_cols = sp.V.n_cols;
   p.C = sp.C;
   p.T = sp.T;
   p.k0 = sp.k0;
@@ -673,6 +677,45 @@ int launch_stream_iter(const StreamPlan& sp_in, const double* x, double* y, cons
   sp.it = it;
   stream_dispatch<false>(sp, 0, x, y, s);
   return 1;
+}
+
+int launch_stream_iter_range(const StreamPlan& sp_in, const double* x, double* y, const IterOut& it, int64_t k0,
+                             int64_t k1, cudaStream_t s) {
+  if (k1 <= k0) return 0;
+  StreamPlan sp = sp_in;
+  sp.it = it;
+  sp.k0 = k0;
+  sp.T = k1;
+  if (sp.grid > k1 - k0) sp.grid = (int)(k1 - k0);
+  stream_dispatch<false>(sp, 0, x, y, s);
+  return 1;
+}
+
+// out[0] = largest j with col[j] < lo (-1 if none), out[1] = smallest j with
+// col[j] >= hi (nnz if none): the nonzeros that read x outside [lo, hi)
+__global__ void __launch_bounds__(kNT) halo_extent_kernel(const int32_t* __restrict__ col, int64_t nnz, int64_t lo,
+                                                          int64_t hi, unsigned long long* out) {
+  long long jl = -1;
+  unsigned long long jh = (unsigned long long)nnz;
+  for (int64_t j = (int64_t)blockIdx.x * kNT + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * kNT) {
+    const int64_t c = __ldg(col + j);
+    if (c < lo) jl = j;
+    if (c >= hi && (unsigned long long)j < jh) jh = (unsigned long long)j;
+  }
+  jl = warp_max(jl);
+  jh = warp_min(jh);
+  if ((threadIdx.x & 31) == 0) {
+    if (jl >= 0) atomicMax(out, (unsigned long long)(jl + 1));  // stored +1 (0 = none)
+    atomicMin(out + 1, jh);
+  }
+}
+
+void launch_halo_extent(const int32_t* col, int64_t nnz, int64_t lo, int64_t hi, unsigned long long* out,
+                        cudaStream_t s) {
+  if (nnz <= 0) return;
+  int64_t g = (nnz + kNT * 8 - 1) / (kNT * 8);
+  if (g > dev_sm_count() * 8) g = dev_sm_count() * 8;
+  halo_extent_kernel<<<(unsigned)g, kNT, 0, s>>>(col, nnz, lo, hi, out);
 }
 
 int launch_stream_range(const StreamPlan& sp_in, const double* x, double* y, int64_t k0, int64_t k1, cudaStream_t s) {

@@ -6,15 +6,38 @@
 
 namespace spmv {
 
+// Streams of the nnz tiles: 256-bit non-coherent loads, L1 no-allocate (every
+// 32-B sector consumed whole by one instruction). NZ_EVICT_FIRST: also an L2
+// evict_first policy, so the once-read matrix streams do not push the
+// gathered x out of L2 (experiment switch)
+#ifndef NZ_EVICT_FIRST
+#define NZ_EVICT_FIRST 0
+#endif
 __device__ __forceinline__ void ld256_s32(const int32_t* p, int (&c)[8]) {
+#if NZ_EVICT_FIRST
+  asm volatile(
+      "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.s32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], pol;\n}"
+      : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7])
+      : "l"(p));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v8.s32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7])
                : "l"(p));
+#endif
 }
 __device__ __forceinline__ void ld256_f64(const double* p, double* v) {
+#if NZ_EVICT_FIRST
+  asm volatile(
+      "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], pol;\n}"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+      : "l"(p));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
                : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
                : "l"(p));
+#endif
 }
 
 // ---- nnz_split warp tile (see nzsplit.cu) -----------------------------------
