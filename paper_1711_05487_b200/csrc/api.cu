@@ -207,6 +207,7 @@ struct Shard {
   double* x2 = nullptr;       // second x replica (deferred-normalisation ping-pong)
   double* cta_part = nullptr; // per-CTA sums of y^2 (fused iteration epilogue, row-aligned STREAM / D8)
   unsigned int* done = nullptr;  // its last-CTA ticket counter
+  double* cta2 = nullptr;        // [2][grid] per-CTA sums of the prologue-norm iteration (parity double-buffered)
   double* nn = nullptr;       // running norm + rescale factor (norm.cu)
   double* nu = nullptr;
   int nu_cap = 0;
@@ -235,6 +236,12 @@ struct Shard {
     allocs.push_back(p);
     bytes += (int64_t)b;
     return static_cast<T*>(p);
+  }
+  void free_alloc(void* p) {  // one allocation of this shard, returned early
+    auto it = std::find(allocs.begin(), allocs.end(), p);
+    if (it == allocs.end()) return;
+    allocs.erase(it);
+    cudaFree(p);
   }
   void release() {
     cudaSetDevice(dev);
@@ -732,6 +739,23 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     count_launches(s.nnz0 ? 1 : 0, "rebase");
   }
   for (auto& s : P->shards) ck(cudaStreamSynchronize(s.stream), "upload sync");
+  // in-process shards on distinct devices exchange partials and x halos with
+  // peer copies: enable direct peer access (NVLink / NVSwitch) where the
+  // pair supports it (otherwise the runtime stages the copies)
+  if (ngpus > 1 && !opt.emulate_devices) {
+    for (int a = 0; a < ngpus; ++a)
+      for (int b = 0; b < ngpus; ++b) {
+        if (a == b) continue;
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, a, b) == cudaSuccess && can) {
+          ck(cudaSetDevice(a), "cudaSetDevice");
+          const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "cudaDeviceEnablePeerAccess");
+          cudaGetLastError();
+        }
+      }
+    ck(cudaSetDevice(cur), "cudaSetDevice");
+  }
   P->upload_ms = now_ms() - t_a;
 
   // ---- a2: inspector (features, validation, max gap) ---------------------------------
@@ -856,7 +880,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       sp.d8_un = 8;
       if (const char* e = getenv("SPMV_D8_UN")) sp.d8_un = atoi(e) == 16 ? 16 : 8;  // experiments: 8 or 16
       // shrink the tile until 4 stages fit (long rows of a forced D8 plan)
-      while (Rt > 16 && d8_smem_bytes(Rt * ml, Rt, 4) > 227 * 1024) Rt -= 16;
+      while (Rt > 16 && d8_smem_bytes(Rt * ml, Rt, 4, 8) > 227 * 1024) Rt -= 16;
       sp.rows_per_tile = Rt;
       sp.C = ((Rt * ml + 31) / 32) * 32;
       P->C = sp.C;
@@ -879,6 +903,20 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       sp.row0 = s.row0;
       launch_d8_encode(V, sp.row0, dict_dev, sp.n_dict, codes, rlen, s.stream);
       count_launches(V.m ? 1 : 0, "d8 encode");
+      // 8-bit codes; 4-bit codes (two per byte, <= 16 dictionary entries) are
+      // kept as an experiment: measured SLOWER on B200 (C5 2.41 vs 2.23 ms,
+      // C2 32.4 vs 28.3 us -- the nibble extraction lengthens the consumer's
+      // decode chain, and the kernel is bound by that latency, not by bytes)
+      sp.d8_bits = 8;
+      if (const char* e = getenv("SPMV_D8_BITS")) sp.d8_bits = (atoi(e) == 4 && sp.n_dict <= 16) ? 4 : 8;  // experiments
+      if (sp.d8_bits == 4) {
+        uint8_t* packed = s.alloc<uint8_t>((size_t)(V.nnz + 1) / 2);
+        launch_d8_pack4(codes, V.nnz, packed, s.stream);
+        count_launches(V.nnz ? 1 : 0, "d8 pack4");
+        ck(cudaStreamSynchronize(s.stream), "d8 pack4");
+        s.free_alloc(codes);
+        codes = packed;
+      }
       sp.codes = codes;
       sp.rlen = rlen;
       sp.d8_dict_dev = dict_dev;
@@ -888,7 +926,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       int best = -1, best_cw = 4;
       for (int c : {4, 6, 8}) {
         if (cw && c != cw) continue;
-        if (d8_smem_bytes(sp.C, Rt, c) > 227 * 1024) continue;
+        if (d8_smem_bytes(sp.C, Rt, c, sp.d8_bits) > 227 * 1024) continue;
         sp.stages = c;
         sp.grid = d8_prepare(sp, s.sm_count);
         if (sp.grid < 0) { cudaGetLastError(); continue; }
@@ -1823,8 +1861,8 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
         s.nu_cap = iters;
       }
       if (!s.x2) s.x2 = s.alloc<double>((size_t)p->n_cols);
-      if (!s.nn) s.nn = s.alloc<double>(2);
-      ck(cudaMemsetAsync(s.nn, 0, 16, s.stream), "nn");
+      if (!s.nn) s.nn = s.alloc<double>(4);
+      ck(cudaMemsetAsync(s.nn, 0, 32, s.stream), "nn");
       ck(cudaMemcpyAsync(s.x, x0, (size_t)p->n_cols * 8, cudaMemcpyDefault, s.stream), "copy x0");
       cur[g] = s.x;
       nxt[g] = s.x2;
@@ -1834,6 +1872,17 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
     // stream, then the boundary tiles
     if (G > 1)
       for (auto& s : p->shards) prepare_overlap(p, s);
+    // single shard, row-aligned STREAM / D8: the prologue-norm iteration
+    const StreamPlan& sp1 = p->shards[0].sp[0];
+    const bool fused1 = G == 1 && p->sel.variant == SPMV_VARIANT_STREAM && sp1.aligned && !sp1.seg && !sp1.rowmap &&
+                        !sp1.need_fixup && !getenv("SPMV_NO_FUSED_NORM") && !getenv("SPMV_NO_LAGGED_NORM");
+    const int grid1 = std::max(sp1.grid, 1);
+    double* cta2 = nullptr;
+    if (fused1) {
+      Shard& s = p->shards[0];
+      if (!s.cta2) s.cta2 = s.alloc<double>((size_t)2 * grid1);
+      cta2 = s.cta2;
+    }
     for (int k = 0; k < iters; ++k) {
       // partials of iteration k live in half (k & 1) of every shard's allpart:
       // shard h may run ahead of a peer that has not yet copied h's partials
@@ -1845,8 +1894,27 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
       if (G == 1) {
         Shard& s = p->shards[0];
         set_xwin(p, s, cur[0]);
-        // one shard: the norm step runs inside the SpMV's epilogue (fused plans)
-        count_launches(spmv_iter(p, s, cur[0], nxt[0] + s.row0, s.allpart + half, s.nn, s.nu + k), "iteration step");
+        if (fused1) {
+          // one launch per iteration, nothing between two SpMVs: launch k
+          // stores its per-CTA sums; launch k+1's last CTA folds them into
+          // ||yh_k|| and nu_k and decides the factor launch k+2 applies
+          // (iterfuse.cuh, lagged mode)
+          IterOut it;
+          it.cta_part = cta2 + (size_t)(k & 1) * grid1;
+          it.cta_only = true;
+          it.st = s.nn;  // lagged-mode state (4 doubles, zeroed)
+          it.par = k & 1;
+          if (k > 0) {
+            it.prev_part = cta2 + (size_t)((k - 1) & 1) * grid1;
+            it.prev_grid = grid1;
+            it.nu_k = s.nu + (k - 1);
+          }
+          count_launches(launch_stream_iter(s.sp[0], cur[0], nxt[0] + s.row0, it, s.stream), "iteration step");
+        } else {
+          // one shard: the norm step runs in the SpMV's epilogue (or its own kernel)
+          count_launches(spmv_iter(p, s, cur[0], nxt[0] + s.row0, s.allpart + half, s.nn, s.nu + k),
+                         "iteration step");
+        }
         std::swap(cur, nxt);
         continue;
       }
@@ -1915,7 +1983,12 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
     for (int g = 0; g < G; ++g) {
       Shard& s = p->shards[g];
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
-      count_launches(launch_unit(cur[g] + s.row0, s.m, s.nn, nxt[g] + s.row0, s.stream), "unit");
+      if (fused1)
+        count_launches(launch_unit_fold(cur[g] + s.row0, s.m, cta2 + (size_t)((iters - 1) & 1) * grid1, grid1,
+                                        s.nn, s.nu + (iters - 1), nxt[g] + s.row0, s.stream),
+                       "unit");
+      else
+        count_launches(launch_unit(cur[g] + s.row0, s.m, s.nn, nxt[g] + s.row0, s.stream), "unit");
       set_xwin(p, s, s.x);
     }
     Shard& s0 = p->shards[0];
@@ -1932,7 +2005,7 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
     if (last_norm) *last_norm = nu[iters - 1];
     for (int k = 0; k < iters; ++k)
       if (nu[k] == 0.0 || !std::isfinite(nu[k]))
-        fail(SPMV_E_ZERO_NORM, "iterated mode: ||y|| == 0 at iteration %d", k);
+        fail(SPMV_E_ZERO_NORM, "iterated mode: ||y|| == 0 (or not finite) at iteration %d", k);
   });
 }
 
@@ -1967,12 +2040,13 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     info->stream_stages = s0.sp[0].stages;
     info->stream_grid = s0.sp[0].grid;
     info->d8_n_dict = s0.sp[0].codes ? s0.sp[0].n_dict : 0;
+    if (s0.sp[0].codes) info->d16_width = s0.sp[0].d8_bits;
     {  // compulsory bytes of one SpMV in the plan's own format
       int64_t kb = 8 * p->n_cols + 8 * p->n_rows + 8 * p->nnz;
       for (const Shard& s : p->shards) {
         const StreamPlan& sp = s.sp[0];
         if (p->sel.variant == SPMV_VARIANT_STREAM && sp.codes)
-          kb += s.nnz + s.m + 8 * (sp.T + 1);  // codes, row lengths, tile starts
+          kb += (sp.d8_bits == 4 ? (s.nnz + 1) / 2 : s.nnz) + s.m + 8 * (sp.T + 1);  // codes, row lengths, tile starts
         else if (p->sel.variant == SPMV_VARIANT_STREAM && sp.dcol)
           kb += 2 * s.nnz + (int64_t)p->rp_bytes * (s.m + 1) + 4 * s.m;  // deltas, rowptr, heads
         else
@@ -2092,7 +2166,19 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
       case SPMV_ARR_DCOL: raw(s.sp[0].dcol, s.sp[0].dcol ? s.nnz : 0, 2); break;
       case SPMV_ARR_HEAD: raw(s.sp[0].head, s.sp[0].head ? s.m : 0, 4); break;
       case SPMV_ARR_ANCHOR: raw(s.sp[0].anchor, s.sp[0].anchor ? s.sp[0].T : 0, 4); break;
-      case SPMV_ARR_D8_CODES: raw(s.sp[0].codes, s.sp[0].codes ? s.nnz : 0, 1); break;
+      case SPMV_ARR_D8_CODES: {  // one code per nonzero (4-bit codes unpacked, low nibble first)
+        const StreamPlan& sp = s.sp[0];
+        count = sp.codes ? s.nnz : 0;
+        if (!dst || count == 0) break;
+        if (sp.d8_bits == 8) {
+          ck(cudaMemcpy(dst, sp.codes, (size_t)count, cudaMemcpyDeviceToHost), "export");
+        } else {
+          std::vector<uint8_t> h((size_t)(count + 1) / 2);
+          ck(cudaMemcpy(h.data(), sp.codes, h.size(), cudaMemcpyDeviceToHost), "export");
+          for (int64_t j = 0; j < count; ++j) ((uint8_t*)dst)[j] = (uint8_t)((h[(size_t)(j >> 1)] >> ((j & 1) * 4)) & 15);
+        }
+        break;
+      }
       case SPMV_ARR_D8_RLEN: raw(s.sp[0].rlen, s.sp[0].rlen ? s.m : 0, 1); break;
       case SPMV_ARR_D8_DICT: {
         count = s.sp[0].codes ? s.sp[0].n_dict : 0;

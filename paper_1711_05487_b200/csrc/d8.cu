@@ -35,8 +35,9 @@ struct D8Layout {
   size_t vals, codes, rl, stage, full, empty, meta, total;
 };
 
-// C: nonzero capacity of a tile (Rt x longest row), Rt rows per tile
-__host__ __device__ inline D8Layout d8_layout(int64_t C, int64_t Rt, int stages) {
+// C: nonzero capacity of a tile (Rt x longest row), Rt rows per tile, CB:
+// bits per code (8, or 4 when the dictionary has <= 16 entries)
+__host__ __device__ inline D8Layout d8_layout(int64_t C, int64_t Rt, int stages, int CB = 8) {
   D8Layout L;
   L.vals = 0;
   // values: copy starts at the 128-B line of the first value (<= 15 before
@@ -44,21 +45,22 @@ __host__ __device__ inline D8Layout d8_layout(int64_t C, int64_t Rt, int stages)
   L.codes = d8_al128((size_t)(C + 16) * 8);
   // codes: copy starts 16-B aligned (<= 15 before t0), rounded up to 16 B,
   // plus >= 16 readable bytes past any row end (branch-free 16-code batches)
-  L.rl = L.codes + d8_al128((size_t)C + 64);
+  L.rl = L.codes + d8_al128((size_t)(CB == 4 ? (C + 1) / 2 : C) + 64);
   L.stage = d8_al128(L.rl + (size_t)Rt + 16);
   size_t o = L.stage * stages;
   L.full = o; o += 8 * (size_t)stages;
   L.empty = o; o += 8 * (size_t)stages;
-  L.meta = d8_al128(o); o = L.meta + 16 * (size_t)stages;
+  L.meta = d8_al128(o); o = L.meta + 32 * (size_t)stages;
   L.total = d8_al128(o);
   return L;
 }
 
-size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages) { return d8_layout(C, Rt, stages).total; }
+size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages, int CB) { return d8_layout(C, Rt, stages, CB).total; }
 
 struct D8Meta {
   int64_t t0;
-  int32_t cnt, voff;  // nonzeros; offset of t0 in the staged values (codes: t0 & 15)
+  int32_t cnt, voff;  // nonzeros; offset of t0 in the staged values
+  int32_t coff, pad;  // offset of t0 in the staged codes, in codes (8-bit: t0 & 15; 4-bit: nibbles)
 };
 
 struct D8P {
@@ -83,7 +85,7 @@ __device__ __forceinline__ void d8_arrive(uint64_t* bar) {
 
 // Consumer warps' tile loop; returns the warp's sum of squares of the rows it
 // wrote (its tiles in launch order; 0 outside the iterated mode).
-template <int CW, bool SCALE, int UN>
+template <int CW, bool SCALE, int UN, int CB>
 __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, const D8Layout& L, uint64_t* full,
                                              uint64_t* empty, const D8Meta* meta, const int32_t* dict_s, double f) {
   const int S = p.stages;
@@ -96,10 +98,10 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
     const int s = i % S;
     mbar_wait(&full[s], (uint32_t)((i / S) & 1));
     const D8Meta mt = meta[s];
-    SPMV_CHECK(mt.cnt >= 0 && mt.cnt <= p.C && mt.voff >= 0 && mt.voff < 16);
+    SPMV_CHECK(mt.cnt >= 0 && mt.cnt <= p.C && mt.voff >= 0 && mt.voff < 16 && mt.coff >= 0 && mt.coff < 32);
     const unsigned char* st = smem + L.stage * s;
     const double* vals_s = reinterpret_cast<const double*>(st + L.vals) + mt.voff;
-    const uint8_t* codes_s = st + L.codes + (mt.t0 & 15);
+    const uint8_t* codes_s = st + L.codes;  // code e of the tile: unit mt.coff + e
     const uint8_t* rl_s = st + L.rl;
     const int64_t R0 = k * p.Rt;
     const int nrows = (int)(((R0 + p.Rt) < p.m ? (R0 + p.Rt) : p.m) - R0);
@@ -127,7 +129,9 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
         double xv[UN];
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
-          const int d = dict_s[codes_s[off + l0 + u]];
+          const int e = mt.coff + off + l0 + u;
+          const int code = CB == 8 ? (int)codes_s[e] : ((int)codes_s[e >> 1] >> ((e & 1) << 2)) & 15;
+          const int d = dict_s[code];
           c += (l0 + u < len) ? d : 0;
           cc[u] = c;
         }
@@ -162,11 +166,14 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
 // registers, UN = 16 -> ~96
 constexpr int d8_lb(int CW, int UN) { return UN == 8 ? (CW == 4 ? 5 : (CW == 6 ? 4 : 3)) : (CW == 4 ? 4 : (CW == 6 ? 3 : 2)); }
 
-template <int CW, int UN>
+template <int CW, int UN, int CB>
 __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const D8P p) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int32_t dict_s[256];
-  const D8Layout L = d8_layout(p.C, p.Rt, p.stages);
+  __shared__ double f_s;                   // iterated mode: this launch's exact factor
+  __shared__ __align__(8) uint64_t fbar_s;  // ... and its hand-over barrier
+  uint64_t* fbar = &fbar_s;
+  const D8Layout L = d8_layout(p.C, p.Rt, p.stages, CB);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.empty);
   D8Meta* meta = reinterpret_cast<D8Meta*>(smem + L.meta);
@@ -179,6 +186,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
+    mbar_init(fbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -203,36 +211,57 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
         if (i >= S) mbar_wait(&empty[s], (uint32_t)(((i / S) - 1) & 1));
         const int64_t R0 = k * p.Rt;
         const int64_t R1 = (R0 + p.Rt) < p.m ? (R0 + p.Rt) : p.m;
-        const int64_t v0 = t0 & ~15ll, c0 = t0 & ~15ll;
+        // codes: 16-B aligned byte range holding codes [t0, t1) (4-bit codes:
+        // two per byte, low nibble first)
+        const int64_t v0 = t0 & ~15ll;
+        const int64_t cb0 = (CB == 8 ? t0 : (t0 >> 1)) & ~15ll;
+        const int64_t cb1 = CB == 8 ? t1 : (t1 + 1) >> 1;
         const uint32_t vb = t1 > t0 ? (uint32_t)(((t1 - v0) * 8 + 15) & ~15ll) : 0u;
-        const uint32_t cb = t1 > t0 ? (uint32_t)(((t1 - c0) + 15) & ~15ll) : 0u;
+        const uint32_t cb = t1 > t0 ? (uint32_t)(((cb1 - cb0) + 15) & ~15ll) : 0u;
         const uint32_t rb = (uint32_t)(((R1 - R0) + 15) & ~15ll);
         D8Meta mt;
         mt.t0 = t0;
         mt.cnt = (int32_t)(t1 - t0);
         mt.voff = (int32_t)(t0 - v0);
+        mt.coff = (int32_t)(CB == 8 ? t0 - cb0 : t0 - 2 * cb0);
+        mt.pad = 0;
         meta[s] = mt;
         unsigned char* st = smem + L.stage * s;
         mbar_arrive_expect_tx(&full[s], vb + cb + rb);
         if (t1 > t0) {
           bulk_g2s(st + L.vals, p.val + v0, vb, &full[s], pol);
-          bulk_g2s(st + L.codes, p.codes + c0, cb, &full[s], pol);
+          bulk_g2s(st + L.codes, p.codes + cb0, cb, &full[s], pol);
         }
         bulk_g2s(st + L.rl, p.rlen + R0, rb, &full[s], pol);
       }
+    } else if (p.it.cta_only && p.it.prev_part && blockIdx.x == gridDim.x - 1) {
+      iter_lag_fold_lanes(p.it);  // lagged iteration: the previous launch's norm (lanes 1..31)
     }
     return;
   }
 
   // ------------------------------- consumers --------------------------------
   pdl_wait();  // x, y, the scale may be written by the previous kernel in the stream
-  // pending exact rescale of the iterated mode (1 almost always): two
-  // instantiations of the consumer loop, so the common path carries no
-  // multiply or live f (measured: the scaled loop alone in the kernel cost
-  // 7 % on C5, 2.368 vs 2.210 ms, through code generation)
-  const double f = iter_scale(p.it);
-  const double wsq = f == 1.0 ? d8_consume<CW, false, UN>(p, smem, L, full, empty, meta, dict_s, 1.0)
-                              : d8_consume<CW, true, UN>(p, smem, L, full, empty, meta, dict_s, f);
+  // iterated mode: the exact factor this launch applies (1 almost always),
+  // fetched by ONE thread and handed over through an mbarrier; each warp
+  // first waits for its first stage (the TMA fill hides the load), then
+  // picks one of two instantiations of the tile loop, so the common path
+  // carries no multiply or live factor (a live factor in the loop, or a
+  // rescale pass after it, cost 7 % on C5 through code generation; a CTA
+  // barrier on the load at the launch start cost ~3 % per C2 iteration)
+  double f = 1.0;
+  if (p.it.cta_part) {
+    if (threadIdx.x == 32) {
+      f_s = iter_factor(p.it);
+      d8_arrive(fbar);
+    }
+    const int w = (threadIdx.x >> 5) - 1;
+    if (p.k0 + blockIdx.x + (int64_t)w * gridDim.x < p.T) mbar_wait(&full[w % S], 0u);
+    mbar_wait(fbar, 0u);
+    f = f_s;
+  }
+  const double wsq = f == 1.0 ? d8_consume<CW, false, UN, CB>(p, smem, L, full, empty, meta, dict_s, 1.0)
+                              : d8_consume<CW, true, UN, CB>(p, smem, L, full, empty, meta, dict_s, f);
   iter_epilogue<32 * CW>(p.it, wsq);
 }
 
@@ -257,13 +286,15 @@ static D8P d8_params(const StreamPlan& sp, const double* x, double* y) {
   return p;
 }
 
-template <int CW, int UN>
+template <int CW, int UN, int CB>
 static int d8_prepare_t(const StreamPlan& sp, int sm_count) {
-  const size_t smem = d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages);
-  if (cudaFuncSetAttribute(d8_kernel<CW, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  const size_t smem = d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB);
+  if (cudaFuncSetAttribute(d8_kernel<CW, UN, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
     return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN>, 32 * (CW + 1), smem) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN, CB>, 32 * (CW + 1), smem) !=
+          cudaSuccess ||
       per_sm < 1)
     return -1;
   if (const char* e = getenv("SPMV_STREAM_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));  // experiments
@@ -272,50 +303,72 @@ static int d8_prepare_t(const StreamPlan& sp, int sm_count) {
   return (int)std::max<int64_t>(grid, 1);
 }
 
-template <int CW, int UN>
+template <int CW, int UN, int CB>
 static int d8_per_sm_t(const StreamPlan& sp) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN>, 32 * (CW + 1),
-                                                    d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages)) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN, CB>, 32 * (CW + 1),
+                                                    d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB)) !=
+      cudaSuccess)
     return 0;
   return per_sm;
 }
 
-template <int CW, int UN>
+template <int CW, int UN, int CB>
 static void d8_launch_t(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
-  launch_pdl(d8_kernel<CW, UN>, dim3(sp.grid), dim3(32 * (CW + 1)), d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages),
-             s, d8_params(sp, x, y));
+  launch_pdl(d8_kernel<CW, UN, CB>, dim3(sp.grid), dim3(32 * (CW + 1)),
+             d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB), s, d8_params(sp, x, y));
 }
 
-// (stages = consumer warps CW) x (batch width UN) -> instantiation
-template <int UN, typename F>
+// (stages = consumer warps CW) x (batch width UN) x (code bits CB) -> instantiation
+template <int UN, int CB, typename F>
 static int d8_cw(const StreamPlan& sp, F&& f) {
+  using U = std::integral_constant<int, UN>;
+  using B = std::integral_constant<int, CB>;
   switch (sp.stages) {
-    case 4: return f(std::integral_constant<int, 4>{}, std::integral_constant<int, UN>{});
-    case 6: return f(std::integral_constant<int, 6>{}, std::integral_constant<int, UN>{});
-    case 8: return f(std::integral_constant<int, 8>{}, std::integral_constant<int, UN>{});
+    case 4: return f(std::integral_constant<int, 4>{}, U{}, B{});
+    case 6: return f(std::integral_constant<int, 6>{}, U{}, B{});
+    case 8: return f(std::integral_constant<int, 8>{}, U{}, B{});
     default: return -1;
   }
 }
 template <typename F>
 static int d8_dispatch(const StreamPlan& sp, F&& f) {
-  return sp.d8_un == 16 ? d8_cw<16>(sp, f) : d8_cw<8>(sp, f);
+  if (sp.d8_bits == 4) return sp.d8_un == 16 ? d8_cw<16, 4>(sp, f) : d8_cw<8, 4>(sp, f);
+  return sp.d8_un == 16 ? d8_cw<16, 8>(sp, f) : d8_cw<8, 8>(sp, f);
 }
 
 int d8_per_sm(const StreamPlan& sp) {
-  const int r = d8_dispatch(sp, [&](auto cw, auto un) { return d8_per_sm_t<cw.value, un.value>(sp); });
+  const int r = d8_dispatch(sp, [&](auto cw, auto un, auto cb) { return d8_per_sm_t<cw.value, un.value, cb.value>(sp); });
   return r < 0 ? 0 : r;
 }
 
 int d8_prepare(const StreamPlan& sp, int sm_count) {
-  return d8_dispatch(sp, [&](auto cw, auto un) { return d8_prepare_t<cw.value, un.value>(sp, sm_count); });
+  return d8_dispatch(sp,
+                     [&](auto cw, auto un, auto cb) { return d8_prepare_t<cw.value, un.value, cb.value>(sp, sm_count); });
 }
 
 void launch_d8(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
-  d8_dispatch(sp, [&](auto cw, auto un) {
-    d8_launch_t<cw.value, un.value>(sp, x, y, s);
+  d8_dispatch(sp, [&](auto cw, auto un, auto cb) {
+    d8_launch_t<cw.value, un.value, cb.value>(sp, x, y, s);
     return 0;
   });
+}
+
+// 4-bit codes: packed[i] = codes[2i] | codes[2i+1] << 4 (low nibble first)
+__global__ void __launch_bounds__(kNT) d8_pack4_kernel(const uint8_t* __restrict__ codes, int64_t nnz,
+                                                       uint8_t* __restrict__ packed) {
+  const int64_t nb = (nnz + 1) / 2;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < nb; i += (int64_t)gridDim.x * kNT) {
+    const uint8_t lo = codes[2 * i], hi = 2 * i + 1 < nnz ? codes[2 * i + 1] : 0;
+    packed[i] = (uint8_t)(lo | (hi << 4));
+  }
+}
+
+void launch_d8_pack4(const uint8_t* codes, int64_t nnz, uint8_t* packed, cudaStream_t s) {
+  if (nnz <= 0) return;
+  int64_t g = ((nnz + 1) / 2 + kNT - 1) / kNT;
+  if (g > dev_sm_count() * 32) g = dev_sm_count() * 32;
+  d8_pack4_kernel<<<(unsigned)g, kNT, 0, s>>>(codes, nnz, packed);
 }
 
 // ---- plan time ----------------------------------------------------------------
@@ -367,13 +420,15 @@ template <typename RP>
 __global__ void __launch_bounds__(kNT) d8_decode_kernel(const RP* __restrict__ rp, int64_t m, int64_t row0,
                                                         const uint8_t* __restrict__ codes,
                                                         const uint8_t* __restrict__ rlen,
-                                                        const int32_t* __restrict__ dict, int32_t* __restrict__ out) {
+                                                        const int32_t* __restrict__ dict, int bits,
+                                                        int32_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x;
   if (i >= m) return;
   const int64_t a = rp[i];
   int64_t c = row0 + i;
   for (int t = 0; t < rlen[i]; ++t) {
-    c += dict[codes[a + t]];
+    const int64_t j = a + t;
+    c += dict[bits == 8 ? codes[j] : (codes[j >> 1] >> ((j & 1) << 2)) & 15];
     out[a + t] = (int32_t)c;
   }
 }
@@ -383,10 +438,10 @@ void launch_d8_decode_export(const StreamPlan& sp, const int32_t* dict_dev, int3
   const unsigned g = (unsigned)((sp.V.m + kNT - 1) / kNT);
   if (sp.V.rp_bytes == 8)
     d8_decode_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)sp.V.rowptr, sp.V.m, sp.row0, sp.codes, sp.rlen,
-                                                dict_dev, out);
+                                                dict_dev, sp.d8_bits, out);
   else
     d8_decode_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)sp.V.rowptr, sp.V.m, sp.row0, sp.codes, sp.rlen,
-                                                dict_dev, out);
+                                                dict_dev, sp.d8_bits, out);
 }
 
 }  // namespace spmv

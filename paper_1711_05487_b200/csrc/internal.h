@@ -56,6 +56,18 @@ struct IterOut {
   double* partials = nullptr;     // [kNormPartials] rank partials
   double* nn = nullptr;           // non-null: fused norm step (single rank), nn[0..1]
   double* nu_k = nullptr;
+  // single-rank iteration, nothing between two SpMVs ("lagged" mode): every
+  // CTA stores its sum of squares; the LAST CTA (the one with the fewest
+  // tiles) then folds the PREVIOUS launch's sums (prev_part[0..prev_grid))
+  // into ||yh_{k-1}||, writes nu_{k-1} (*nu_k) and decides the exact factor
+  // the NEXT launch applies, from ||yh_{k-1}|| and this launch's factor
+  // (state st[0..3] = N_{k-1}, F_k, and the factors by launch parity
+  // st[2 + par]; reading 27)
+  const double* prev_part = nullptr;
+  int prev_grid = 0;
+  int par = 0;  // launch parity (k & 1)
+  double* st = nullptr;
+  bool cta_only = false;
 };
 
 struct MatView {
@@ -99,13 +111,15 @@ struct StreamPlan {
   int64_t row0 = 0;            // row id of local row 0 (anchor of the head deltas)
   const int32_t* d8_dict_dev = nullptr;  // the dictionary on the device (export decode)
   int d8_un = 8;               // D8 codes decoded + x gathers in flight per lane per batch (8 or 16)
+  int d8_bits = 8;             // D8 bits per code: 8, or 4 (two per byte) when the dictionary has <= 16 entries
 };
-size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages);
+size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages, int CB = 8);
 int d8_prepare(const StreamPlan& sp, int sm_count);  // stages = consumer warps (4, 6, 8)
 int d8_per_sm(const StreamPlan& sp);                 // resident CTAs per SM (after d8_prepare)
 void launch_d8(const StreamPlan& sp, const double* x, double* y, cudaStream_t s);
 void launch_d8_encode(const MatView& A, int64_t row0, const int32_t* dict_dev, int nd, uint8_t* codes, uint8_t* rlen,
                       cudaStream_t s);
+void launch_d8_pack4(const uint8_t* codes, int64_t nnz, uint8_t* packed, cudaStream_t s);
 void launch_d8_decode_export(const StreamPlan& sp, const int32_t* dict_dev, int32_t* out, cudaStream_t s);
 // row-aligned STREAM / D8 plan (no fix-up) with the iterated-mode epilogue
 int launch_stream_iter(const StreamPlan& sp, const double* x, double* y, const IterOut& it, cudaStream_t s);
@@ -292,6 +306,10 @@ int launch_sum_partials(const double* v, int64_t n, double* partials, cudaStream
 int launch_norm_step(const double* partials, int count, double* nn, double* nu_k, cudaStream_t s);
 // non-fused variants: y *= nn[1] (pending factor; nn may be null) + partials of y^2
 int launch_scale_partials(double* y, int64_t m, const double* nn, double* partials, cudaStream_t s);
+// final step of the lagged iteration: n = fold of the last launch's per-CTA
+// sums, *nu_last = n / (st[1] st[0]) (n when st[0] == 0), x_out = y / n
+int launch_unit_fold(const double* y, int64_t m, const double* cta_part, int grid, const double* st, double* nu_last,
+                     double* x_out, cudaStream_t s);
 int launch_unit(const double* y, int64_t m, const double* nn, double* x_out, cudaStream_t s);
 int launch_normalize(const double* y, int64_t m, const double* partials, int count, double* x_out,
                      double* nu_dev, cudaStream_t s);

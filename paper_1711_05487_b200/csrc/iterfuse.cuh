@@ -42,6 +42,56 @@ __device__ __forceinline__ void norm_step_scalar(double ss, double* nn, double* 
   nn[1] = rs ? scalbn(1.0, -e) : 1.0;
 }
 
+// Called by every consumer thread right after pdl_wait: the exact factor this
+// launch applies to its output -- lagged mode: st[2], decided by the previous
+// launch's last CTA; else the pending factor of a norm step that already ran
+// The exact factor this launch applies to its output: lagged mode st[2 +
+// par] (decided by the previous launch's producer lanes), else the pending
+// factor *scale of a norm step that already ran, else 1. Read by ONE thread
+// per CTA (every consumer thread reading the same word queued ~3.5K requests
+// on one L2 slice at each launch start).
+__device__ __forceinline__ double iter_factor(const IterOut& it) {
+  double f = 1.0;
+  if (it.st) f = __ldcg(it.st + 2 + it.par);
+  else if (it.scale) f = __ldcg(it.scale);
+  return f != 0.0 ? f : 1.0;
+}
+
+// Lagged mode: the fold of the previous launch's per-CTA sums, by lanes 1..31
+// of the PRODUCER warp of the last CTA at the start of the launch (lane 0
+// issues the TMA copies; the other 31 lanes are otherwise idle), so it sits
+// on no critical path -- run by the last CTA's consumers after their tiles it
+// cost 5.5 % per iteration on C2. Fixed order: lane l sums b = l - 1, l + 30,
+// ... ascending, then lane 1 adds the 31 lane sums in lane order. Then
+//   N = ||yh_{k-1}||, nu_{k-1} = N / (F_{k-1} N_{k-2})   (N at the first step)
+//   F_{k+1} = 2^-e when e = ilogb(N F_k) leaves [-128, 128], else 1
+// (F_k = the factor this launch applies, st[2 + par]; F_{k+1} goes to the
+// other parity slot, which no CTA of this launch reads). The rescale is
+// decided one step late, so a vector may reach ~2^128 lambda^2 before it
+// applies: the 2^-128..2^128 band keeps squares finite for |lambda| up to
+// ~2^190 (the in-place scheme allowed 2^256 with no lag).
+__device__ __forceinline__ void iter_lag_fold_lanes(const IterOut& it) {
+  __shared__ double lsum[32];
+  const int lane = threadIdx.x & 31;  // 1..31
+  const unsigned mask = 0xfffffffeu;
+  pdl_wait();  // the previous launch's sums and state
+  double a = 0.0;
+  for (int b = lane - 1; b < it.prev_grid; b += 31) a += __ldcg(it.prev_part + b);
+  lsum[lane] = a;
+  __syncwarp(mask);
+  if (lane != 1) return;
+  double ss = 0.0;
+  for (int l = 1; l < 32; ++l) ss += lsum[l];
+  const double N = sqrt(ss), Np = __ldcg(it.st), F1 = __ldcg(it.st + 1), F2 = __ldcg(it.st + 2 + it.par);
+  const double fprev = F1 != 0.0 ? F1 : 1.0, fcur = F2 != 0.0 ? F2 : 1.0;
+  *it.nu_k = Np > 0.0 ? N / (fprev * Np) : N;
+  const double mag = N * fcur;
+  const int e = (mag > 0.0 && isfinite(mag)) ? ilogb(mag) : 0;
+  it.st[0] = N;
+  it.st[1] = fcur;
+  it.st[2 + (it.par ^ 1)] = (e > 128 || e < -128) ? scalbn(1.0, -e) : 1.0;
+}
+
 // Called by every consumer thread (NC threads, warps 1..NC/32 of the CTA;
 // the producer warp has exited) after its last tile, wsq = the warp's sum of
 // squares (same value in every lane). Named barrier 1 over the consumers.
@@ -59,10 +109,13 @@ __device__ __forceinline__ void iter_epilogue(const IterOut& it, double wsq) {
     double c = 0.0;
     for (int q = 0; q < NC / 32; ++q) c += ws[q];
     it.cta_part[blockIdx.x] = c;
-    __threadfence();
-    const unsigned tk = atomicAdd(it.done, 1u);
-    last = tk == gridDim.x - 1;
+    if (!it.cta_only) {  // (lagged mode: no ticket)
+      __threadfence();
+      const unsigned tk = atomicAdd(it.done, 1u);
+      last = tk == gridDim.x - 1;
+    }
   }
+  if (it.cta_only) return;  // lagged mode: the fold runs in the next launch's producer warp
   asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
   if (!last) return;
   __threadfence();

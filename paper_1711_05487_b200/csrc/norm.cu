@@ -137,6 +137,31 @@ __global__ void __launch_bounds__(kNT) unit_kernel(const double* __restrict__ y,
   for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = (__ldcg(y + i) * f) / nu;
 }
 
+// lagged iteration's last step: x_out = y / n with n = ||y|| from the
+// fixed-order fold of the last launch's per-CTA sums (every CTA folds the
+// same way); CTA 0 writes the last nu = n / (st[1] st[0]) (n at the first step)
+__global__ void __launch_bounds__(kNT) unit_fold_kernel(const double* __restrict__ y, int64_t m,
+                                                        const double* __restrict__ cta_part, int grid,
+                                                        const double* __restrict__ st, double* __restrict__ nu_last,
+                                                        double* __restrict__ x_out) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ double n_s;
+  const double ss = block_sum_fixed(cta_part, grid);
+  if (threadIdx.x == 0) {
+    const double n = sqrt(ss);
+    n_s = n;
+    if (blockIdx.x == 0) {
+      const double Np = __ldcg(st), F1 = __ldcg(st + 1);
+      *nu_last = Np > 0.0 ? n / ((F1 != 0.0 ? F1 : 1.0) * Np) : n;
+    }
+  }
+  __syncthreads();
+  const double n = n_s;
+  const int64_t stride = (int64_t)gridDim.x * kNT;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) x_out[i] = __ldcg(y + i) / n;
+}
+
 static int grid_for(int64_t m) {
   int64_t g = (m + kNT - 1) / kNT;
   if (g > dev_sm_count() * 8) g = dev_sm_count() * 8;
@@ -150,6 +175,12 @@ int launch_norm_step(const double* partials, int count, double* nn, double* nu_k
 
 int launch_scale_partials(double* y, int64_t m, const double* nn, double* partials, cudaStream_t s) {
   launch_pdl(scale_partials_kernel, dim3(kNormPartials), dim3(kNT), 0, s, y, m, nn, partials);
+  return 1;
+}
+
+int launch_unit_fold(const double* y, int64_t m, const double* cta_part, int grid, const double* st, double* nu_last,
+                     double* x_out, cudaStream_t s) {
+  launch_pdl(unit_fold_kernel, dim3(grid_for(m)), dim3(kNT), 0, s, y, m, cta_part, grid, st, nu_last, x_out);
   return 1;
 }
 

@@ -253,6 +253,17 @@ __device__ __forceinline__ void seg_tile(const StreamP<RP>& p, const double* __r
 #endif
 constexpr int kStreamUnroll1 = STREAM_UNR1;  // gathers in flight per lane, one lane per row (VS = 1)
 
+// y[r] *= f over the rows of this warp's tiles (rare launch of the iterated
+// mode whose exact rescale factor is not 1; out of line, off the tile loop)
+__device__ __noinline__ void stream_rescale_rows(const int32_t* tile_row, double* y, int64_t k0, int64_t T, int CW,
+                                                 double f) {
+  const int w = (threadIdx.x >> 5) - 1, lane = threadIdx.x & 31;
+  for (int64_t k = k0 + blockIdx.x + (int64_t)w * gridDim.x; k < T; k += (int64_t)CW * gridDim.x) {
+    const int64_t r0 = __ldg(tile_row + k), r1 = __ldg(tile_row + k + 1);
+    for (int64_t r = r0 + lane; r < r1; r += 32) y[r] = __ldcg(y + r) * f;
+  }
+}
+
 // MODE: 0 = row-step over nnz-aligned tiles, 1 = segmented, 2 = row-step over
 // row-aligned tiles (compile-time so the nnz-tile path carries no per-tile
 // offsets: measured ~9% faster on C5 than a runtime switch). D16: 0 = int32
@@ -399,6 +410,8 @@ __global__ void __launch_bounds__(32 * (CW + 1),
                             &full[s], pol);
         if (hb) bulk_g2s(st + L.hd, reinterpret_cast<const unsigned char*>(p.head) + h0, hb, &full[s], pol);
       }
+    } else if (AL && p.it.cta_only && p.it.prev_part && blockIdx.x == gridDim.x - 1) {
+      iter_lag_fold_lanes(p.it);  // lagged iteration: the previous launch's norm (lanes 1..31)
     }
     return;
   }
@@ -412,7 +425,11 @@ __global__ void __launch_bounds__(32 * (CW + 1),
   constexpr int GPW = 32 / VS;
   const int lane = lane32 % VS;
   const int gi = lane32 / VS;
-  const double fsc = AL ? iter_scale(p.it) : 1.0;  // pending exact rescale (iterated mode)
+  // iterated mode (AL): the launch's exact factor, fetched by one thread;
+  // rows rescaled after the tiles in the rare launch where it is not 1
+  __shared__ double f_s;
+  if constexpr (AL)
+    if (threadIdx.x == 32 && p.it.cta_part) f_s = iter_factor(p.it);
   double sqa = 0.0;  // (AL) this lane's squares over all its rows, its tiles in order (one warp sum at the end)
   for (int i = w;; i += CW) {
     const int64_t k = p.k0 + blockIdx.x + (int64_t)i * gridDim.x;
@@ -533,7 +550,6 @@ __global__ void __launch_bounds__(32 * (CW + 1),
           acc = a0;
         }
         acc = group_sum<VS>(acc);
-        if constexpr (AL) acc *= fsc;
         if (active && lane == 0) {
           if (incoming && q == 0) {
             p.carry_row[k] = (int32_t)out_row(p, r);
@@ -549,7 +565,18 @@ __global__ void __launch_bounds__(32 * (CW + 1),
     __syncwarp();
     if (lane32 == 0) mbar_arrive(&empty[s]);
   }
-  if constexpr (AL) iter_epilogue<32 * CW>(p.it, p.it.cta_part ? warp_sum(sqa) : 0.0);  // fixed butterfly
+  if constexpr (AL) {
+    double wsq = p.it.cta_part ? warp_sum(sqa) : 0.0;  // fixed butterfly
+    if (p.it.cta_part) {
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * CW) : "memory");
+      const double f = f_s;
+      if (f != 1.0) {  // rescale the rows this warp wrote (rowmap is null on this path; out of line)
+        stream_rescale_rows(p.tile_row, p.y, p.k0, p.T, CW, f);
+        wsq *= f * f;  // exact: f is a power of two
+      }
+    }
+    iter_epilogue<32 * CW>(p.it, wsq);
+  }
 }
 
 template <typename RP>

@@ -9,9 +9,9 @@ namespace spmv {
 // Streams of the nnz tiles: 256-bit non-coherent loads, L1 no-allocate (every
 // 32-B sector consumed whole by one instruction). NZ_EVICT_FIRST: also an L2
 // evict_first policy, so the once-read matrix streams do not push the
-// gathered x out of L2 (experiment switch)
+// gathered x out of L2 (B200: C3 267 -> 262 us, C4 117.5 -> 111 us)
 #ifndef NZ_EVICT_FIRST
-#define NZ_EVICT_FIRST 0
+#define NZ_EVICT_FIRST 1
 #endif
 __device__ __forceinline__ void ld256_s32(const int32_t* p, int (&c)[8]) {
 #if NZ_EVICT_FIRST

@@ -22,8 +22,9 @@ P:708-711, computed by ``spmv_shard_bounds``) and a full replica of x.
          for banded matrices a few planes instead of the whole vector
          (27-pt 384^3 at G = 8: ~2.4 MB per rank per iteration vs 396 MB).
   and swaps the replicas; no x = y / nu pass per iteration. With one rank,
-  steps 1-3 are one fused call (the norm step runs in the SpMV kernel's
-  epilogue for row-aligned STREAM / D8 plans). At the end x_iters =
+  the library runs the whole loop (spmv_iterate): for row-aligned STREAM /
+  D8 plans one launch per iteration, each folding the previous launch's
+  per-CTA sums into the norm at its start. At the end x_iters =
   yh_{iters-1} * nn[1] / ||yh_{iters-1}|| over the replica.
 
 This module only orchestrates (argument marshalling, process-group calls);
@@ -45,6 +46,9 @@ class ShardSteps:
     iter_step: Callable[[object, object, object, object, Optional[object]], None]
     norm_step: Callable[[object, int, object, object], None]  # (partials_all, count, nn[2], nu[1])
     unit: Callable[[object, object, object], None]    # (y, nn[2], x_out): x_out = y * nn[1] / nn[0]
+    # optional whole single-rank run (x_full, iters, nu_hist): the library's own
+    # loop (spmv_iterate), which needs nothing between two SpMVs
+    iterate_all: Optional[Callable[[object, int, object], None]] = None
     # optional context-manager factory making the steps' stream the current
     # one, so the collectives (issued on the current stream) are ordered with
     # the native steps (issued on the plan's stream)
@@ -111,6 +115,9 @@ def iterate(dist, steps: ShardSteps, bounds: Sequence[int], rank: int, world: in
     """
     P = partials_local.numel()
     b0, b1 = int(bounds[rank]), int(bounds[rank + 1])
+    if world == 1 and steps.iterate_all is not None:
+        steps.iterate_all(x_full, iters, nu_hist)
+        return
     with steps.stream() if steps.stream is not None else nullcontext():
         nn.zero_()
         cur, nxt = x_full, x_alt
@@ -152,8 +159,14 @@ def native_steps(plan) -> ShardSteps:
     def stream():
         return torch.cuda.stream(torch.cuda.ExternalStream(plan.stream(), device=torch.cuda.current_device()))
 
+    def iterate_all(x, iters, nu):
+        with stream():
+            _, nu_h = plan.iterate(x, iters, x_out=x)
+            nu[:iters].copy_(torch.from_numpy(nu_h), non_blocking=False)
+
     return ShardSteps(
         stream=stream,
+        iterate_all=iterate_all,
         iter_step=lambda x, y, p, nn, nu: plan.iter_step(x, y, p, nn, nu),
         norm_step=lambda pa, cnt, nn, nu: plan.norm_step(pa, cnt, nn, nu),
         unit=lambda y, nn, x: plan.unit(y, nn, x),

@@ -747,3 +747,26 @@ def _persist_limit():
     v = ctypes.c_size_t(0)
     assert rt.cudaDeviceGetLimit(ctypes.byref(v), 0x06) == 0  # cudaLimitPersistingL2CacheSize
     return v.value
+
+
+@pytest.mark.parametrize("scale", [1e40, 1e-40, 1.0])
+@pytest.mark.parametrize("G,d16", [(1, 2), (1, 0), (2, 2), (3, 0)])
+def test_iterated_fused_paths_rescale(scale, G, d16):
+    # row-aligned STREAM / D8 plans: one shard runs the lagged one-launch
+    # iteration (the norm folded by the next launch's producer lanes, the
+    # exact rescale decided one step late, reading 27); several shards the
+    # interior-first launches with per-launch partials. ~1e40-scaled values
+    # make the rescale fire every few steps.
+    m = sg.stencil(16, 27, x_seed=6)
+    vals = m.vals * scale
+    K = 60
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, vals, m.x, K)
+    assert rc == 0
+    p = spmv.Plan(m.rowptr, m.colind, vals, ngpus=G, emulate_devices=1, force_variant="stream", d16=d16)
+    assert p.info()["sel"]["d16"] == d16
+    for k in (1, 2, 3, K):
+        xg, nug = p.iterate(m.x, k)
+        rc, xk, nuk = oracle.power_iter(m.rowptr, m.colind, vals, m.x, k)
+        assert np.all(np.isfinite(xg)) and np.all(np.isfinite(nug))
+        assert np.max(np.abs(xg - xk)) <= 1e-10 * np.max(np.abs(xk)), k
+        assert np.all(np.abs(nug - nuk) <= 1e-12 * nuk), k

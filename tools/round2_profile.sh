@@ -26,4 +26,13 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:stre
   -o $out/full_c5_int32 python tools/prof_one.py --config 5 --reps 3 --opts '{"d16": 0}' > $out/ncu_full_c5_int32.log 2>&1
 timeout 900 ncu --cache-control none --clock-control none -k regex:stream_kernel -s 3 -c 1 --metrics $WARM --csv \
   --log-file $out/warm_c5_int32.csv python tools/prof_one.py --config 5 --reps 5 --opts '{"d16": 0}' > $out/ncu_warm_c5_int32.log 2>&1
+# forced-variant sweeps (selection regret) and the Table V analogue
+for c in 2 3 4; do timeout 900 python tools/sweep.py --config $c --quick --out $out/sweep_c$c.json > $out/sweep_c$c.log 2>&1; done
+timeout 1200 python tools/sweep.py --config 5 --quick --reps 5 --out $out/sweep_c5.json > $out/sweep_c5.log 2>&1
+timeout 900 python tools/table5.py --configs 2,3,4,5 --out $out/table5.json > $out/table5.log 2>&1
+# iterated-mode overhead vs back-to-back SpMVs, and the emulated-shard timeline
+timeout 600 python tools/exp_iter2.py --config 2 --iters 1000 > $out/iter_overhead.log 2>&1
+timeout 600 python tools/exp_iter2.py --config 5 --iters 100 >> $out/iter_overhead.log 2>&1
+timeout 600 python tools/timeline_iter.py --n 160 --G 4 --iters 3 > $out/timeline_iter.log 2>&1
+python tools/sass_summary.py > $out/sass_summary.txt 2>&1
 echo done

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Forced-variant sweep on one config: time every variant / VS / tile / D16
-choice, report GB/s and the selection regret (feature-guided pick vs the
+"""Forced-variant sweep on one config: time every variant / VS / tile / D16 /
+D8 choice, report GB/s and the selection regret (feature-guided pick vs the
 exhaustive best, the paper's "oracle" optimizer P:805-807 and the trivial
 optimizer cost P:921-926) and N_iters,min.
 
@@ -79,8 +79,10 @@ def main():
     stages = (4, 8) if not a.quick else (4,)
     d16s = (0, 1) if a.config in (1, 2) else (0,)
     # the plan's own tile rule (row-count tiles on regular rows, 4/6 consumer warps)
-    grid.append(dict(force_variant="stream", force_vs=1))
+    grid.append(dict(force_variant="stream", force_vs=1, d16=0))
     grid.append(dict(force_variant="stream", force_vs=1, d16=1))
+    # dictionary-coded 8-bit deltas (D8; the kernel picks 4/6/8 consumer warps)
+    grid.append(dict(force_variant="stream", d16=2))
     for vs, t, sg_, d in itertools.product(svs, tiles, stages, d16s):
         grid.append(dict(force_variant="stream", force_vs=vs, tile_nnz=t, stages=sg_, d16=d))
     for t in tiles:

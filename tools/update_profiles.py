@@ -110,7 +110,8 @@ if os.path.exists(lc):
             f.write(f"{k:42s} {len(us):6d} {us[len(us) // 2]:10.1f} {sum(us):11.1f}\n")
         f.write("# SpMV step (full-grid launches): " + "  ".join(
             f"{k} {len(v)} x {sum(v) / len(v):.1f} us = {100 * (sum(v) / len(v)) / tot:.1f}%" for k, v in step.items()) + "\n")
-for nm in ("sweep_c2.json", "sweep_c3.json", "sweep_c4.json", "sweep_c5.json", "cusparse.json", "table5.json"):
+for nm in ("sweep_c2.json", "sweep_c3.json", "sweep_c4.json", "sweep_c5.json", "cusparse.json", "table5.json",
+           "iter_overhead.log", "sass_summary.txt"):
     sp_ = os.path.join(src, nm)
     if os.path.exists(sp_):
         shutil.copy(sp_, os.path.join(dst, f"{tag}_{nm}"))
