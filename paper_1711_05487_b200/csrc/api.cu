@@ -32,6 +32,7 @@ std::atomic<int64_t> g_launches{0};
 // device-wide: reset only when the last such plan goes)
 std::mutex g_l2_mu;
 constexpr int kIterRegions = 3;  // iterated mode: partials of up to 3 launches per shard (interior + 2 boundary)
+constexpr size_t kStaticSmemMargin = 2048;  // static shared memory of the stream / D8 kernels (< 2 KB)
 int g_l2_plans[64] = {0};
 
 struct Err : std::runtime_error {
@@ -880,7 +881,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       sp.d8_un = 8;
       if (const char* e = getenv("SPMV_D8_UN")) sp.d8_un = atoi(e) == 16 ? 16 : 8;  // experiments: 8 or 16
       // shrink the tile until 4 stages fit (long rows of a forced D8 plan)
-      while (Rt > 16 && d8_smem_bytes(Rt * ml, Rt, 4, 8) > 227 * 1024) Rt -= 16;
+      while (Rt > 16 && d8_smem_bytes(Rt * ml, Rt, 4, 8) > 227 * 1024 - kStaticSmemMargin) Rt -= 16;
       sp.rows_per_tile = Rt;
       sp.C = ((Rt * ml + 31) / 32) * 32;
       P->C = sp.C;
@@ -926,7 +927,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       int best = -1, best_cw = 4;
       for (int c : {4, 6, 8}) {
         if (cw && c != cw) continue;
-        if (d8_smem_bytes(sp.C, Rt, c, sp.d8_bits) > 227 * 1024) continue;
+        if (d8_smem_bytes(sp.C, Rt, c, sp.d8_bits) > 227 * 1024 - kStaticSmemMargin) continue;
         sp.stages = c;
         sp.grid = d8_prepare(sp, s.sm_count);
         if (sp.grid < 0) { cudaGetLastError(); continue; }
@@ -935,7 +936,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       }
       sp.stages = best_cw;
       sp.grid = d8_prepare(sp, s.sm_count);
-      if (sp.grid < 0) fail(SPMV_E_CUDA, "D8: cannot fit %lld-nonzero tiles in shared memory", (long long)sp.C);
+      if (sp.grid < 0) {
+        cudaGetLastError();
+        fail(SPMV_E_CUDA, "D8: cannot fit %lld-nonzero tiles in shared memory", (long long)sp.C);
+      }
       return;
     }
     // tile size: P whole passes of the consumer warp over its 32/VS rows
@@ -1048,7 +1052,9 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     if (const char* e = getenv("SPMV_STREAM_L2PF")) sp.l2pf = atoi(e) != 0;
     // shrink the staged-rowptr capacity until the ring fits (sparser tiles
     // then read rowptr from global memory)
-    while (sp.rows_cap > 64 && stream_smem_bytes(sp.C, sp.stages, V.rp_bytes, sp.rows_cap, d16, seg) > 227 * 1024)
+    // (227 KB per CTA includes the kernel's static shared memory: ~1 KB)
+    while (sp.rows_cap > 64 &&
+           stream_smem_bytes(sp.C, sp.stages, V.rp_bytes, sp.rows_cap, d16, seg) > 227 * 1024 - kStaticSmemMargin)
       sp.rows_cap /= 2;
     sp.grid = stream_prepare(sp, s.sm_count);
     if (sp.grid < 0 && sp.stages > kStreamConsumerWarps) {
@@ -1056,7 +1062,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       sp.stages = kStreamConsumerWarps;
       sp.grid = stream_prepare(sp, s.sm_count);
     }
-    if (sp.grid < 0) fail(SPMV_E_CUDA, "cta_stream: cannot fit tile_nnz=%lld in shared memory", (long long)sp.C);
+    if (sp.grid < 0) {
+      cudaGetLastError();  // (a failed attribute / occupancy query must not poison the next call)
+      fail(SPMV_E_CUDA, "cta_stream: cannot fit tile_nnz=%lld in shared memory", (long long)sp.C);
+    }
   };
   // nnz_split pass over the view V (colind/values) restricted to the
   // non-empty rows rowmap[0..mc) with rowptr rpc; y rows [0, s.m)
@@ -1451,11 +1460,22 @@ void host_pipe_prepare(spmv_plan p, Shard& s) {
   // 11.37 (8) / 11.25 (24))
   int64_t nbw = std::min<int64_t>(16, std::max<int64_t>(2, xbytes / (4ll << 20)));
   if (const char* e = getenv("SPMV_HOST_PIPE_BLOCKS")) nbw = atoll(e);  // tests
-  const int nb = (int)std::max<int64_t>(2, std::min<int64_t>(nbw, sp.T / 4));
+  int nb = (int)std::max<int64_t>(2, std::min<int64_t>(nbw, sp.T / 4));
+  // tapered blocks (experiment, SPMV_HOST_PIPE_TAPER=t): the first t and the
+  // last t blocks a quarter of the others -- measured slower on C5 (11.07 vs
+  // 10.4-10.5 ms per e2e step), so off by default
+  int taper = 0;
+  if (const char* e = getenv("SPMV_HOST_PIPE_TAPER")) taper = std::min(atoi(e), nb / 4);  // experiments
+  if (taper > 0) nb += 2 * taper;
   h.kb.resize(nb + 1);
   h.srow.resize(nb + 1);
   h.xhi.resize(nb);
-  for (int b = 0; b <= nb; ++b) h.kb[b] = sp.T * b / nb;
+  {
+    // block weights: 1 in the middle, 1/4 for the `taper` blocks at each end
+    std::vector<double> cw((size_t)nb + 1, 0.0);
+    for (int b = 0; b < nb; ++b) cw[(size_t)b + 1] = cw[(size_t)b] + ((b < taper || b >= nb - taper) ? 0.25 : 1.0);
+    for (int b = 0; b <= nb; ++b) h.kb[b] = b == nb ? sp.T : (int64_t)((double)sp.T * cw[(size_t)b] / cw[(size_t)nb]);
+  }
   std::vector<int64_t> t0(nb + 1);
   int32_t* cm = nullptr;
   ck(cudaMalloc(&cm, 4 * (size_t)nb), "cudaMalloc");
