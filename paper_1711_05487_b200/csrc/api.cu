@@ -922,6 +922,28 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       sp.rlen = rlen;
       sp.d8_dict_dev = dict_dev;
       ck(cudaStreamSynchronize(s.stream), "d8 encode");
+      // packed tiles (one TMA copy per tile: values | codes | row lengths):
+      // experiment, C2 27.1 vs 28.1 us but C5 2.36 vs 2.21 ms -> off by default
+      bool packed = false;
+      if (const char* e = getenv("SPMV_D8_PACKED")) packed = atoi(e) != 0;  // experiments
+      if (packed && sp.d8_bits == 8 && V.nnz > 0) {
+        std::vector<int64_t> tz((size_t)sp.T + 1), toff((size_t)sp.T + 1);
+        ck(cudaMemcpy(tz.data(), sp.tile_nz, (size_t)(sp.T + 1) * 8, cudaMemcpyDeviceToHost), "tile_nz");
+        toff[0] = 0;
+        for (int64_t k = 0; k < sp.T; ++k) {
+          const int64_t cnt = tz[(size_t)k + 1] - tz[(size_t)k];
+          const int64_t nr = std::min<int64_t>(Rt, V.m - k * Rt);
+          toff[(size_t)k + 1] = toff[(size_t)k] + ((cnt + 1) & ~1ll) * 8 + ((cnt + 15) & ~15ll) + ((nr + 15) & ~15ll);
+        }
+        int64_t* toff_dev = s.alloc<int64_t>((size_t)sp.T + 1);
+        unsigned char* tiles = s.alloc<unsigned char>((size_t)toff[(size_t)sp.T]);
+        ck(cudaMemcpyAsync(toff_dev, toff.data(), (size_t)(sp.T + 1) * 8, cudaMemcpyHostToDevice, s.stream), "toff");
+        launch_d8_pack_tiles(sp, toff_dev, tiles, s.stream);
+        count_launches(1, "d8 pack tiles");
+        ck(cudaStreamSynchronize(s.stream), "d8 pack tiles");
+        sp.d8_tiles = tiles;
+        sp.d8_toff = toff_dev;
+      }
       // consumer warps per CTA (one stage each): the most resident consumer
       // warps per SM (ties: more CTAs), or SPMV_D8_CW
       int best = -1, best_cw = 4;

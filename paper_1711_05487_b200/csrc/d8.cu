@@ -67,6 +67,8 @@ struct D8P {
   const double* val;
   const uint8_t* codes;
   const uint8_t* rlen;
+  const unsigned char* tiles;  // packed tiles (PK): segment k = bytes [toff[k], toff[k+1])
+  const int64_t* toff;
   const int64_t* tile_nz;
   const double* x;
   double* y;
@@ -85,7 +87,7 @@ __device__ __forceinline__ void d8_arrive(uint64_t* bar) {
 
 // Consumer warps' tile loop; returns the warp's sum of squares of the rows it
 // wrote (its tiles in launch order; 0 outside the iterated mode).
-template <int CW, bool SCALE, int UN, int CB>
+template <int CW, bool SCALE, int UN, int CB, bool PK>
 __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, const D8Layout& L, uint64_t* full,
                                              uint64_t* empty, const D8Meta* meta, const int32_t* dict_s, double f) {
   const int S = p.stages;
@@ -100,9 +102,19 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
     const D8Meta mt = meta[s];
     SPMV_CHECK(mt.cnt >= 0 && mt.cnt <= p.C && mt.voff >= 0 && mt.voff < 16 && mt.coff >= 0 && mt.coff < 32);
     const unsigned char* st = smem + L.stage * s;
-    const double* vals_s = reinterpret_cast<const double*>(st + L.vals) + mt.voff;
-    const uint8_t* codes_s = st + L.codes;  // code e of the tile: unit mt.coff + e
-    const uint8_t* rl_s = st + L.rl;
+    const double* vals_s;
+    const uint8_t* codes_s;  // code e of the tile: unit mt.coff + e
+    const uint8_t* rl_s;
+    if constexpr (PK) {  // packed segment: values, codes, row lengths (16-B aligned parts)
+      const int c16 = (mt.cnt + 1) & ~1;  // values padded to 16 B
+      vals_s = reinterpret_cast<const double*>(st);
+      codes_s = st + (size_t)c16 * 8;
+      rl_s = codes_s + ((mt.cnt + 15) & ~15);
+    } else {
+      vals_s = reinterpret_cast<const double*>(st + L.vals) + mt.voff;
+      codes_s = st + L.codes;
+      rl_s = st + L.rl;
+    }
     const int64_t R0 = k * p.Rt;
     const int nrows = (int)(((R0 + p.Rt) < p.m ? (R0 + p.Rt) : p.m) - R0);
     int base = 0;  // first nonzero (tile-relative) of the pass
@@ -138,7 +150,11 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
 #pragma unroll
         for (int u = 0; u < UN; ++u) SPMV_CHECK(l0 + u >= len || (cc[u] >= 0 && cc[u] < p.n_cols));
 #pragma unroll
+#ifdef D8_EXP_XHIT  // timing experiment only: every gather an L1 hit (wrong results)
+        for (int u = 0; u < UN; ++u) xv[u] = l0 + u < len ? ld_x(p.x + (cc[u] & 2047)) : 0.0;
+#else
         for (int u = 0; u < UN; ++u) xv[u] = l0 + u < len ? ld_x(p.x + cc[u]) : 0.0;
+#endif
 #pragma unroll
         for (int u = 0; u < UN; u += 2) {
           const int l = l0 + u;
@@ -166,7 +182,7 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
 // registers, UN = 16 -> ~96
 constexpr int d8_lb(int CW, int UN) { return UN == 8 ? (CW == 4 ? 5 : (CW == 6 ? 4 : 3)) : (CW == 4 ? 4 : (CW == 6 ? 3 : 2)); }
 
-template <int CW, int UN, int CB>
+template <int CW, int UN, int CB, bool PK>
 __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const D8P p) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int32_t dict_s[256];
@@ -222,17 +238,25 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
         D8Meta mt;
         mt.t0 = t0;
         mt.cnt = (int32_t)(t1 - t0);
-        mt.voff = (int32_t)(t0 - v0);
-        mt.coff = (int32_t)(CB == 8 ? t0 - cb0 : t0 - 2 * cb0);
+        mt.voff = PK ? 0 : (int32_t)(t0 - v0);
+        mt.coff = PK ? 0 : (int32_t)(CB == 8 ? t0 - cb0 : t0 - 2 * cb0);
         mt.pad = 0;
         meta[s] = mt;
         unsigned char* st = smem + L.stage * s;
-        mbar_arrive_expect_tx(&full[s], vb + cb + rb);
-        if (t1 > t0) {
-          bulk_g2s(st + L.vals, p.val + v0, vb, &full[s], pol);
-          bulk_g2s(st + L.codes, p.codes + cb0, cb, &full[s], pol);
+        if constexpr (PK) {
+          // packed tiles: [values | codes | row lengths] of tile k contiguous
+          // in one 16-B-aligned segment: ONE bulk copy per tile
+          const int64_t o0 = ld_ro(p.toff + k), o1 = ld_ro(p.toff + k + 1);
+          mbar_arrive_expect_tx(&full[s], (uint32_t)(o1 - o0));
+          bulk_g2s(st, p.tiles + o0, (uint32_t)(o1 - o0), &full[s], pol);
+        } else {
+          mbar_arrive_expect_tx(&full[s], vb + cb + rb);
+          if (t1 > t0) {
+            bulk_g2s(st + L.vals, p.val + v0, vb, &full[s], pol);
+            bulk_g2s(st + L.codes, p.codes + cb0, cb, &full[s], pol);
+          }
+          bulk_g2s(st + L.rl, p.rlen + R0, rb, &full[s], pol);
         }
-        bulk_g2s(st + L.rl, p.rlen + R0, rb, &full[s], pol);
       }
     } else if (p.it.cta_only && p.it.prev_part && blockIdx.x == gridDim.x - 1) {
       iter_lag_fold_lanes(p.it);  // lagged iteration: the previous launch's norm (lanes 1..31)
@@ -260,8 +284,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
     mbar_wait(fbar, 0u);
     f = f_s;
   }
-  const double wsq = f == 1.0 ? d8_consume<CW, false, UN, CB>(p, smem, L, full, empty, meta, dict_s, 1.0)
-                              : d8_consume<CW, true, UN, CB>(p, smem, L, full, empty, meta, dict_s, f);
+  const double wsq = f == 1.0 ? d8_consume<CW, false, UN, CB, PK>(p, smem, L, full, empty, meta, dict_s, 1.0)
+                              : d8_consume<CW, true, UN, CB, PK>(p, smem, L, full, empty, meta, dict_s, f);
   iter_epilogue<32 * CW>(p.it, wsq);
 }
 
@@ -270,6 +294,8 @@ static D8P d8_params(const StreamPlan& sp, const double* x, double* y) {
   p.val = sp.V.val;
   p.codes = sp.codes;
   p.rlen = sp.rlen;
+  p.tiles = sp.d8_tiles;
+  p.toff = sp.d8_toff;
   p.tile_nz = sp.tile_nz;
   p.x = x;
   p.y = y;
@@ -286,14 +312,14 @@ static D8P d8_params(const StreamPlan& sp, const double* x, double* y) {
   return p;
 }
 
-template <int CW, int UN, int CB>
+template <int CW, int UN, int CB, bool PK>
 static int d8_prepare_t(const StreamPlan& sp, int sm_count) {
   const size_t smem = d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB);
-  if (cudaFuncSetAttribute(d8_kernel<CW, UN, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (cudaFuncSetAttribute(d8_kernel<CW, UN, CB, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN, CB>, 32 * (CW + 1), smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN, CB, PK>, 32 * (CW + 1), smem) !=
           cudaSuccess ||
       per_sm < 1)
     return -1;
@@ -303,55 +329,92 @@ static int d8_prepare_t(const StreamPlan& sp, int sm_count) {
   return (int)std::max<int64_t>(grid, 1);
 }
 
-template <int CW, int UN, int CB>
+template <int CW, int UN, int CB, bool PK>
 static int d8_per_sm_t(const StreamPlan& sp) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN, CB>, 32 * (CW + 1),
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN, CB, PK>, 32 * (CW + 1),
                                                     d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB)) !=
       cudaSuccess)
     return 0;
   return per_sm;
 }
 
-template <int CW, int UN, int CB>
+template <int CW, int UN, int CB, bool PK>
 static void d8_launch_t(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
-  launch_pdl(d8_kernel<CW, UN, CB>, dim3(sp.grid), dim3(32 * (CW + 1)),
+  launch_pdl(d8_kernel<CW, UN, CB, PK>, dim3(sp.grid), dim3(32 * (CW + 1)),
              d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB), s, d8_params(sp, x, y));
 }
 
-// (stages = consumer warps CW) x (batch width UN) x (code bits CB) -> instantiation
-template <int UN, int CB, typename F>
+// (stages = consumer warps CW) x (batch width UN) x (code layout) -> instantiation
+template <int UN, int CB, bool PK, typename F>
 static int d8_cw(const StreamPlan& sp, F&& f) {
   using U = std::integral_constant<int, UN>;
   using B = std::integral_constant<int, CB>;
+  using K = std::integral_constant<bool, PK>;
   switch (sp.stages) {
-    case 4: return f(std::integral_constant<int, 4>{}, U{}, B{});
-    case 6: return f(std::integral_constant<int, 6>{}, U{}, B{});
-    case 8: return f(std::integral_constant<int, 8>{}, U{}, B{});
+    case 4: return f(std::integral_constant<int, 4>{}, U{}, B{}, K{});
+    case 6: return f(std::integral_constant<int, 6>{}, U{}, B{}, K{});
+    case 8: return f(std::integral_constant<int, 8>{}, U{}, B{}, K{});
     default: return -1;
   }
 }
 template <typename F>
 static int d8_dispatch(const StreamPlan& sp, F&& f) {
-  if (sp.d8_bits == 4) return sp.d8_un == 16 ? d8_cw<16, 4>(sp, f) : d8_cw<8, 4>(sp, f);
-  return sp.d8_un == 16 ? d8_cw<16, 8>(sp, f) : d8_cw<8, 8>(sp, f);
+  if (sp.d8_bits == 4) return sp.d8_un == 16 ? d8_cw<16, 4, false>(sp, f) : d8_cw<8, 4, false>(sp, f);
+  if (sp.d8_tiles) return d8_cw<8, 8, true>(sp, f);
+  return sp.d8_un == 16 ? d8_cw<16, 8, false>(sp, f) : d8_cw<8, 8, false>(sp, f);
 }
 
 int d8_per_sm(const StreamPlan& sp) {
-  const int r = d8_dispatch(sp, [&](auto cw, auto un, auto cb) { return d8_per_sm_t<cw.value, un.value, cb.value>(sp); });
+  const int r = d8_dispatch(
+      sp, [&](auto cw, auto un, auto cb, auto pk) { return d8_per_sm_t<cw.value, un.value, cb.value, pk.value>(sp); });
   return r < 0 ? 0 : r;
 }
 
 int d8_prepare(const StreamPlan& sp, int sm_count) {
-  return d8_dispatch(sp,
-                     [&](auto cw, auto un, auto cb) { return d8_prepare_t<cw.value, un.value, cb.value>(sp, sm_count); });
+  return d8_dispatch(sp, [&](auto cw, auto un, auto cb, auto pk) {
+    return d8_prepare_t<cw.value, un.value, cb.value, pk.value>(sp, sm_count);
+  });
 }
 
 void launch_d8(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
-  d8_dispatch(sp, [&](auto cw, auto un, auto cb) {
-    d8_launch_t<cw.value, un.value, cb.value>(sp, x, y, s);
+  d8_dispatch(sp, [&](auto cw, auto un, auto cb, auto pk) {
+    d8_launch_t<cw.value, un.value, cb.value, pk.value>(sp, x, y, s);
     return 0;
   });
+}
+
+// packed tiles (plan time): segment k = [values (8 cnt, padded to 16 B) |
+// codes (cnt, padded to 16) | row lengths (nrows, padded to 16)] at toff[k];
+// one warp per tile copies the three parts
+__global__ void __launch_bounds__(kNT) d8_pack_tiles_kernel(const double* __restrict__ val,
+                                                            const uint8_t* __restrict__ codes,
+                                                            const uint8_t* __restrict__ rlen,
+                                                            const int64_t* __restrict__ tile_nz,
+                                                            const int64_t* __restrict__ toff, int64_t T, int64_t Rt,
+                                                            int64_t m, unsigned char* __restrict__ tiles) {
+  const int64_t k = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= T) return;
+  const int64_t t0 = tile_nz[k], cnt = tile_nz[k + 1] - t0;
+  const int64_t R0 = k * Rt, nr = ((R0 + Rt) < m ? (R0 + Rt) : m) - R0;
+  unsigned char* seg = tiles + toff[k];
+  double* v = reinterpret_cast<double*>(seg);
+  const int64_t c16 = (cnt + 1) & ~1ll;
+  for (int64_t j = lane; j < c16; j += 32) v[j] = j < cnt ? val[t0 + j] : 0.0;
+  uint8_t* c = seg + c16 * 8;
+  const int64_t cp = (cnt + 15) & ~15ll;
+  for (int64_t j = lane; j < cp; j += 32) c[j] = j < cnt ? codes[t0 + j] : 0;
+  uint8_t* r = c + cp;
+  const int64_t rp = (nr + 15) & ~15ll;
+  for (int64_t j = lane; j < rp; j += 32) r[j] = j < nr ? rlen[R0 + j] : 0;
+}
+
+void launch_d8_pack_tiles(const StreamPlan& sp, const int64_t* toff, unsigned char* tiles, cudaStream_t s) {
+  if (sp.T <= 0) return;
+  const int64_t g = (sp.T * 32 + kNT - 1) / kNT;
+  d8_pack_tiles_kernel<<<(unsigned)g, kNT, 0, s>>>(sp.V.val, sp.codes, sp.rlen, sp.tile_nz, toff, sp.T,
+                                                   sp.rows_per_tile, sp.V.m, tiles);
 }
 
 // 4-bit codes: packed[i] = codes[2i] | codes[2i+1] << 4 (low nibble first)

@@ -112,6 +112,8 @@ struct StreamPlan {
   const int32_t* d8_dict_dev = nullptr;  // the dictionary on the device (export decode)
   int d8_un = 8;               // D8 codes decoded + x gathers in flight per lane per batch (8 or 16)
   int d8_bits = 8;             // D8 bits per code: 8, or 4 (two per byte) when the dictionary has <= 16 entries
+  const unsigned char* d8_tiles = nullptr;  // packed tiles: [values | codes | row lengths] per tile (one TMA copy)
+  const int64_t* d8_toff = nullptr;         // their byte offsets [T+1]
 };
 size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages, int CB = 8);
 int d8_prepare(const StreamPlan& sp, int sm_count);  // stages = consumer warps (4, 6, 8)
@@ -120,6 +122,7 @@ void launch_d8(const StreamPlan& sp, const double* x, double* y, cudaStream_t s)
 void launch_d8_encode(const MatView& A, int64_t row0, const int32_t* dict_dev, int nd, uint8_t* codes, uint8_t* rlen,
                       cudaStream_t s);
 void launch_d8_pack4(const uint8_t* codes, int64_t nnz, uint8_t* packed, cudaStream_t s);
+void launch_d8_pack_tiles(const StreamPlan& sp, const int64_t* toff, unsigned char* tiles, cudaStream_t s);
 void launch_d8_decode_export(const StreamPlan& sp, const int32_t* dict_dev, int32_t* out, cudaStream_t s);
 // row-aligned STREAM / D8 plan (no fix-up) with the iterated-mode epilogue
 int launch_stream_iter(const StreamPlan& sp, const double* x, double* y, const IterOut& it, cudaStream_t s);

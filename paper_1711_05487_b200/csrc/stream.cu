@@ -494,7 +494,11 @@ __global__ void __launch_bounds__(32 * (CW + 1),
             for (int u = 0; u < UN; ++u) {
               const int l = l0 + u * VS;
               SPMV_CHECK(l >= le || (idx_s[l] >= 0 && (int64_t)idx_s[l] < p.n_cols));
+#ifdef D8_EXP_XHIT  // timing experiment only: every gather an L1 hit (wrong results)
+              xv[u] = l < le ? ld_x(p.x + (idx_s[l] & 2047)) : 0.0;
+#else
               xv[u] = l < le ? ld_x(p.x + idx_s[l]) : 0.0;
+#endif
             }
 #pragma unroll
             for (int u = 0; u < UN; u += 2) {

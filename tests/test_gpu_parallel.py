@@ -54,3 +54,23 @@ def test_native_distributed_iteration_world1():
         assert np.array_equal(xi, xg) and np.array_equal(nui, nug)
     finally:
         dist.destroy_process_group()
+
+
+def test_bench_under_torchrun_world1():
+    # the launch the driver uses for N > 1 (torchrun, one process per GPU,
+    # NCCL), at world size 1 on the one GPU: one JSON line, max-over-ranks
+    # timing, the iterated mode through parallel.iterate
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(root, "bench.py"), "--gpus", "1", "--steps", "3",
+           "--warmup", "3", "--config", "2", "--no-cpu", "--no-paper-runs", "--iters", "20"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["config"]["d16"] == 2 and d["iterated"]["iters_timed"] == 20
