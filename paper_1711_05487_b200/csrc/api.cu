@@ -223,6 +223,10 @@ struct Shard {
     std::vector<int64_t> xhi;    // x[xlo, xhi[b]) is needed by blocks <= b
     int64_t xlo = 0;             // first column the shard reads
     cudaStream_t h2d = nullptr, d2h = nullptr;
+    // optional second copy stream per direction (experiment, off: consecutive
+    // chunks alternating streams starve the other direction)
+    cudaStream_t h2d2 = nullptr, d2h2 = nullptr;
+    cudaEvent_t ev_e2 = nullptr;
     std::vector<cudaEvent_t> ev_h, ev_c;
   } hp;
   std::vector<void*> allocs;
@@ -259,6 +263,11 @@ struct Shard {
     for (cudaEvent_t e : hp.ev_c) cudaEventDestroy(e);
     hp.ev_h.clear();
     hp.ev_c.clear();
+    if (hp.h2d2) cudaStreamDestroy(hp.h2d2);
+    if (hp.d2h2) cudaStreamDestroy(hp.d2h2);
+    if (hp.ev_e2) cudaEventDestroy(hp.ev_e2);
+    hp.h2d2 = hp.d2h2 = nullptr;
+    hp.ev_e2 = nullptr;
     if (hp.h2d) cudaStreamDestroy(hp.h2d);
     if (hp.d2h) cudaStreamDestroy(hp.d2h);
     hp.h2d = hp.d2h = nullptr;
@@ -1537,6 +1546,13 @@ void host_pipe_prepare(spmv_plan p, Shard& s) {
   }
   ck(cudaStreamCreateWithFlags(&h.h2d, cudaStreamNonBlocking), "cudaStreamCreate");
   ck(cudaStreamCreateWithFlags(&h.d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+  // (experiment, SPMV_HOST_PIPE_TWO_STREAMS=1: measured slower on C5, 12.9 vs
+  // 10.4 ms per e2e step -- the two H2D streams starve the D2H direction)
+  if (getenv("SPMV_HOST_PIPE_TWO_STREAMS")) {
+    ck(cudaStreamCreateWithFlags(&h.h2d2, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&h.d2h2, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&h.ev_e2, cudaEventDisableTiming), "cudaEventCreate");
+  }
   h.ev_h.resize(nb);
   h.ev_c.resize(nb);
   for (int b = 0; b < nb; ++b) {
@@ -1582,28 +1598,43 @@ int host_pipe_run(spmv_plan p, Shard& s, const double* x, double* y) {
   if (h.nz) return host_pipe_run_nz(s, x, y);
   const int nb = (int)h.xhi.size();
   int n = 0;
+  const bool two = h.h2d2 != nullptr;
+  auto up = [&](int b) { return (two && (b & 1)) ? h.h2d2 : h.h2d; };
+  auto down = [&](int b) { return (two && (b & 1)) ? h.d2h2 : h.d2h; };
   ck(cudaEventRecord(h.ev_c[0], s.stream), "event");  // copies start after earlier work on the plan stream
   ck(cudaStreamWaitEvent(h.h2d, h.ev_c[0], 0), "wait");
   ck(cudaStreamWaitEvent(h.d2h, h.ev_c[0], 0), "wait");
+  if (two) {
+    ck(cudaStreamWaitEvent(h.h2d2, h.ev_c[0], 0), "wait");
+    ck(cudaStreamWaitEvent(h.d2h2, h.ev_c[0], 0), "wait");
+  }
   int64_t lo = h.xlo;
   for (int b = 0; b < nb; ++b) {
     if (h.xhi[b] > lo)
-      ck(cudaMemcpyAsync(s.x + lo, x + lo, (size_t)(h.xhi[b] - lo) * 8, cudaMemcpyHostToDevice, h.h2d), "copy x");
+      ck(cudaMemcpyAsync(s.x + lo, x + lo, (size_t)(h.xhi[b] - lo) * 8, cudaMemcpyHostToDevice, up(b)), "copy x");
     lo = std::max(lo, h.xhi[b]);
-    ck(cudaEventRecord(h.ev_h[b], h.h2d), "event");
+    ck(cudaEventRecord(h.ev_h[b], up(b)), "event");
   }
   for (int b = 0; b < nb; ++b) {
+    // block b needs every x chunk <= b (column order): chunk b-1 may sit on
+    // the other copy stream
     ck(cudaStreamWaitEvent(s.stream, h.ev_h[b], 0), "wait");
+    if (two && b > 0) ck(cudaStreamWaitEvent(s.stream, h.ev_h[b - 1], 0), "wait");
     n += launch_stream_range(s.sp[0], s.x, s.y, h.kb[b], h.kb[b + 1], s.stream);
     ck(cudaEventRecord(h.ev_c[b], s.stream), "event");
-    ck(cudaStreamWaitEvent(h.d2h, h.ev_c[b], 0), "wait");
+    ck(cudaStreamWaitEvent(down(b), h.ev_c[b], 0), "wait");
     const int64_t r0 = h.srow[b], r1 = h.srow[b + 1];
     if (r1 > r0)
-      ck(cudaMemcpyAsync(y + s.row0 + r0, s.y + r0, (size_t)(r1 - r0) * 8, cudaMemcpyDeviceToHost, h.d2h), "copy y");
+      ck(cudaMemcpyAsync(y + s.row0 + r0, s.y + r0, (size_t)(r1 - r0) * 8, cudaMemcpyDeviceToHost, down(b)),
+         "copy y");
   }
-  // the plan stream resumes after the last copy
+  // the plan stream resumes after the last copies
   ck(cudaEventRecord(h.ev_h[0], h.d2h), "event");
   ck(cudaStreamWaitEvent(s.stream, h.ev_h[0], 0), "wait");
+  if (two) {
+    ck(cudaEventRecord(h.ev_e2, h.d2h2), "event");
+    ck(cudaStreamWaitEvent(s.stream, h.ev_e2, 0), "wait");
+  }
   (void)p;
   return n;
 }
