@@ -1977,6 +1977,7 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
           it.cta_only = true;
           it.st = s.nn;  // lagged-mode state (4 doubles, zeroed)
           it.par = k & 1;
+          it.rev = (k & 1) && !getenv("SPMV_NO_REVERSE");  // D8: odd launches walk the tiles backwards
           if (k > 0) {
             it.prev_part = cta2 + (size_t)((k - 1) & 1) * grid1;
             it.prev_grid = grid1;

@@ -95,8 +95,9 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
   const int lane = threadIdx.x & 31;
   double sqa = 0.0;  // this lane's squares over all its rows (its tiles in order): one warp sum at the end
   for (int i = w;; i += CW) {
-    const int64_t k = p.k0 + blockIdx.x + (int64_t)i * gridDim.x;
-    if (k >= p.T) break;
+    const int64_t kl = p.k0 + blockIdx.x + (int64_t)i * gridDim.x;
+    if (kl >= p.T) break;
+    const int64_t k = p.it.rev ? p.T - 1 + p.k0 - kl : kl;  // reversed launch: tiles from the end
     const int s = i % S;
     mbar_wait(&full[s], (uint32_t)((i / S) & 1));
     const D8Meta mt = meta[s];
@@ -218,12 +219,18 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
           nT1 = ld_ro(p.tile_nz + kk + 1);
         }
       };
-      fetch(p.k0 + blockIdx.x);
+      // reversed launches (iterated mode, every other iteration) walk the
+      // tiles from the end, where the previous launch last wrote its y (the
+      // x read now): those lines are still in L2
+      const int64_t rb = p.it.rev ? p.T - 1 + p.k0 : 0;
+      auto phys = [&](int64_t kl) { return p.it.rev ? rb - kl : kl; };
+      fetch(phys(p.k0 + blockIdx.x));
       int i = 0;
-      for (int64_t k = p.k0 + blockIdx.x; k < p.T; k += gridDim.x, ++i) {
+      for (int64_t kl = p.k0 + blockIdx.x; kl < p.T; kl += gridDim.x, ++i) {
+        const int64_t k = phys(kl);
         const int s = i % S;
         const int64_t t0 = nT0, t1 = nT1;
-        fetch(k + gridDim.x);
+        if (kl + gridDim.x < p.T) fetch(phys(kl + gridDim.x));
         if (i >= S) mbar_wait(&empty[s], (uint32_t)(((i / S) - 1) & 1));
         const int64_t R0 = k * p.Rt;
         const int64_t R1 = (R0 + p.Rt) < p.m ? (R0 + p.Rt) : p.m;

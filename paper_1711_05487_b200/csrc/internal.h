@@ -66,6 +66,7 @@ struct IterOut {
   const double* prev_part = nullptr;
   int prev_grid = 0;
   int par = 0;  // launch parity (k & 1)
+  int rev = 0;  // D8: walk the tiles from the end (every other iteration: x lines still in L2)
   double* st = nullptr;
   bool cta_only = false;
 };

@@ -770,3 +770,20 @@ def test_iterated_fused_paths_rescale(scale, G, d16):
         assert np.all(np.isfinite(xg)) and np.all(np.isfinite(nug))
         assert np.max(np.abs(xg - xk)) <= 1e-10 * np.max(np.abs(xk)), k
         assert np.all(np.abs(nug - nuk) <= 1e-12 * nuk), k
+
+
+@pytest.mark.parametrize("rb,re", [(0, 3000), (2000, 5500), (5000, 8000)])
+def test_d8_row_block_plan(rb, re):
+    # one rank's row block of a 27-pt stencil (the torchrun layout: n_rows <
+    # n_cols, rowptr rebased, global column ids): D8 head deltas are taken
+    # against the block's local row ids -- the oracle encodes the block the same way
+    full = sg.stencil(20, 27, x_seed=9)
+    blk = sg.stencil(20, 27, x_seed=9, rows=(rb, re))
+    enc = oracle.d8_encode(blk.rowptr, blk.colind)
+    assert enc is not None
+    p = spmv.Plan(blk.rowptr, blk.colind, blk.vals, n_cols=full.n, force_variant="stream", d16=2)
+    assert p.info()["sel"]["d16"] == 2
+    assert np.array_equal(p.export("d8_dict"), enc[0]) and np.array_equal(p.export("d8_codes"), enc[1])
+    y = p.execute(full.x)
+    m = sg.CSR(re - rb, blk.rowptr, blk.colind, blk.vals, full.x)
+    assert_bound(y, m)
