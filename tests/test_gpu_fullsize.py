@@ -106,3 +106,22 @@ def test_c5_forced_variants_sampled(c5, variant, extra):
         prod *= 3 - (c == 0).astype(float) - (c == N3 - 1)
     assert np.array_equal(y1, 27.0 - prod)
     p.destroy()
+
+
+def test_c5_emulated_shards(c5):
+    # the in-process multi-shard path at full size (2 shards on one GPU:
+    # nnz-balanced row blocks, x replicated, interior-first iteration with
+    # halo peer copies): every row of y, and 10 iterations vs the oracle
+    m = c5
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, ngpus=2, emulate_devices=1)
+    info = p.info()
+    assert info["shard_bounds"] == oracle.shard_bounds(m.rowptr, 2).tolist()
+    assert info["sel"]["d16"] == 2
+    _all_rows_bound(m, m.x, p.execute(m.x))
+    K = 10
+    xg, nug = p.iterate(m.x, K)
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, K, nthreads=0)
+    assert rc == 0
+    assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
+    assert np.all(np.abs(nug - nur) <= 1e-12 * nur)
+    p.destroy()
