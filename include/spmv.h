@@ -84,6 +84,14 @@ typedef struct spmv_options {
   int32_t select_mode;     /* 0 feature-guided (Table I features, default), 1 profile-guided (Sec. III-B bounds from
                               three timed micro-benchmarks + Fig. 4 rules; reading 22) */
   int32_t reserved[1];     /* reserved[0] = 1 disables row-aligned tiles (tests) */
+  /* Fig. 4 hyperparameters of the profile-guided classifier. The paper tunes T_IMB and T_ML per
+   * platform by grid search (1.24 / 1.25 on KNC); 0 selects the values of this library's
+   * grid search on B200 (tools/tune_profile.py, profiles/r02_profile_tuning.json, reading 29);
+   * pass 1.24 / 1.25 / 0.10 for the paper's. approx_tol: "P_CSR ~ P_MB" read as P_CSR >= (1 - tol) P_MB. */
+  double t_imb, t_ml, approx_tol;
+  int32_t force_classes;   /* profile-guided mode: -1 measure and classify (default); 0..15 = skip the probes and
+                              apply Table II's mapping to this SPMV_CLASS_* set (the grid search times it) */
+  int32_t pad_;
 } spmv_options;
 
 /* Theta(N) features (Table I) + counts used by the selection.

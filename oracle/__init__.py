@@ -532,6 +532,11 @@ def select(f, l2_bytes, window_max, rowptr_bytes, K_long=100, skew_sd=1.0, empty
 
 # ---- profile-guided selection (reading 22) --------------
 T_IMB, T_ML, APPROX_TOL = 1.24, 1.25, 0.10  # Fig. 4 caption
+# The same hyperparameters re-tuned for B200 by the paper's procedure, a grid
+# search maximising the average gain of the selected optimisation,
+# over a synthetic matrix set (tools/tune_profile.py -> profiles/
+# r02_profile_tuning.json; reading 29): the library's defaults.
+T_IMB_B200, T_ML_B200, APPROX_TOL_B200 = 2.71, 1.06, 0.10
 
 
 def classify_profile(p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak, t_imb=T_IMB, t_ml=T_ML, tol=APPROX_TOL):
@@ -551,14 +556,19 @@ def classify_profile(p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak, t_imb=T_IMB, t_ml=
     return c
 
 
-def profile_select(f, bounds, window_max, K_long=100):
+def profile_select(f, bounds, window_max, K_long=100, t_imb=T_IMB_B200, t_ml=T_ML_B200, tol=APPROX_TOL_B200,
+                   classes=None):
     """Table II for the GPU variants: IMB -> long_row_split (dense
     long rows) or nnz_split; ML -> nnz_split with the x window; MB / CMP ->
     cta_stream (MB adds D8 codes when codable, else 16-bit deltas when the
     gaps fit); no class -> the CSR
     baseline (csr_vector), "not worth applying any" (P:459-461). Precedence
-    IMB > ML > MB/CMP. bounds: dict with p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak."""
-    classes = classify_profile(*(bounds[k] for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak")))
+    IMB > ML > MB/CMP. bounds: dict with p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak;
+    t_imb / t_ml / tol: Fig. 4's hyperparameters (default: the B200 grid
+    search); classes: a given CLASS_* set instead of Fig. 4 (bounds unused)."""
+    if classes is None:
+        classes = classify_profile(*(bounds[k] for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak")),
+                                   t_imb=t_imb, t_ml=t_ml, tol=tol)
     avg_s = f["avg_short"]
     longr = f["n_long"] > 0 and f["nnz_max"] > K_long * f["nnz_avg"]
     nblk = -(-int(f.get("n_cols", f["n"])) // 2048)

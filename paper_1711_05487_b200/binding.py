@@ -35,11 +35,13 @@ class Options(ctypes.Structure):
                 ("merge_items", ctypes.c_int64), ("long_chunk", ctypes.c_int64),
                 ("emulate_devices", ctypes.c_int32), ("stages", ctypes.c_int32), ("seg", ctypes.c_int32),
                 ("long_mode", ctypes.c_int32), ("split_bins", ctypes.c_int32), ("hot_x", ctypes.c_int32),
-                ("select_mode", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
+                ("select_mode", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1),
+                ("t_imb", ctypes.c_double), ("t_ml", ctypes.c_double), ("approx_tol", ctypes.c_double),
+                ("force_classes", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
     @classmethod
     def _names(cls):
-        return {f[0] for f in cls._fields_} - {"struct_size", "reserved"}
+        return {f[0] for f in cls._fields_} - {"struct_size", "reserved", "pad_"}
 
     @classmethod
     def make(cls, **kw):

@@ -113,6 +113,12 @@ def test_invalid_options_rejected_without_gpu():
         pkg.select(f, _props(), 4, force_vs=3)
     with pytest.raises(pkg.SpmvError):
         pkg.select(f, _props(), 4, tile_nnz=100)
+    # Fig. 4 hyperparameters and the forced class set (profile mode)
+    for bad in (dict(t_imb=-1.0), dict(t_ml=float("nan")), dict(approx_tol=1.0), dict(force_classes=16),
+                dict(force_classes=-2)):
+        with pytest.raises(pkg.SpmvError):
+            pkg.select(f, _props(), 4, **bad)
+    pkg.select(f, _props(), 4, t_imb=1.24, t_ml=1.25, approx_tol=0.1, force_classes=15)
 
 
 def test_null_plan_arguments_fail_with_status_not_crash():

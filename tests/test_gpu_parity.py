@@ -536,6 +536,43 @@ def test_profile_mode_selection(c, small):
 
 
 
+@pytest.mark.parametrize("c", [2, 4])
+def test_profile_forced_classes_follow_table2(c):
+    """force_classes = set: no probes, Table II's mapping of the set (the grid
+    search's hook, tools/tune_profile.py) equals the oracle's."""
+    m = sg.config(c, small=True)
+    f = oracle.features(m.rowptr, m.colind)
+    w = spmv.device_query(0)["access_window_max"]
+    for mask in range(16):
+        p = spmv.Plan(m.rowptr, m.colind, m.vals, select_mode=1, force_classes=mask)
+        info = p.info()
+        s, o = info["sel"], oracle.profile_select(f, None, w, classes=mask)
+        assert (s["variant"], s["vs"], s["d16"], bool(s["xwin"]), s["classes"]) == \
+            (o.variant, o.vs, o.d16, o.xwin, o.classes), (mask, s)
+        assert info["profile_ms"] == 0.0  # no probes ran
+        if mask in (0, 8, 4, 2):
+            assert_bound(p.execute(m.x), m)
+        p.destroy()
+
+
+def test_profile_mode_paper_thresholds_option():
+    """t_imb / t_ml / approx_tol override the B200 defaults (Fig. 4 with the
+    paper's KNC values)."""
+    m = sg.config(3, small=True)
+    f = oracle.features(m.rowptr, m.colind)
+    w = spmv.device_query(0)["access_window_max"]
+    for t in ((oracle.T_IMB, oracle.T_ML, oracle.APPROX_TOL), (50.0, 50.0, 0.5)):
+        p = spmv.Plan(m.rowptr, m.colind, m.vals, select_mode=1, t_imb=t[0], t_ml=t[1], approx_tol=t[2])
+        info = p.info()
+        b = {k: info[k] for k in PROFILE_KEYS}
+        o = oracle.profile_select(f, b, w, t_imb=t[0], t_ml=t[1], tol=t[2])
+        s = info["sel"]
+        assert (s["variant"], s["vs"], s["d16"], bool(s["xwin"]), s["classes"]) == \
+            (o.variant, o.vs, o.d16, o.xwin, o.classes), (t, b, s)
+        assert_bound(p.execute(m.x), m)
+        p.destroy()
+
+
 # full Table I on the device (f4) vs the oracle's definitions
 @pytest.mark.parametrize("name,m", SUITE, ids=[n for n, _ in SUITE])
 def test_table1_device(name, m):

@@ -435,18 +435,21 @@ def test_profile_select_table2_mapping():
              maxgap=100)
     b = dict(p_csr=1.0, p_mb=2.0, p_ml=1.0, p_imb=1.0, p_cmp=3.0, p_peak=4.0)
     S = oracle
-    assert S.profile_select(f, b, 1 << 27).variant == S.VARIANT_VECTOR                     # no class: baseline
-    assert S.profile_select(f, {**b, "p_imb": 2.0}, 1 << 27).variant == S.VARIANT_NNZSPLIT  # IMB, no long rows
-    s = S.profile_select(f, {**b, "p_ml": 2.0}, 1 << 27)
+
+    def ps(f, b, w):  # the mapping under the paper's Fig. 4 thresholds
+        return oracle.profile_select(f, b, w, t_imb=oracle.T_IMB, t_ml=oracle.T_ML, tol=oracle.APPROX_TOL)
+    assert ps(f, b, 1 << 27).variant == S.VARIANT_VECTOR                     # no class: baseline
+    assert ps(f, {**b, "p_imb": 2.0}, 1 << 27).variant == S.VARIANT_NNZSPLIT  # IMB, no long rows
+    s = ps(f, {**b, "p_ml": 2.0}, 1 << 27)
     assert s.variant == S.VARIANT_NNZSPLIT and s.xwin                                       # ML
-    s = S.profile_select(f, {**b, "p_csr": 1.9}, 1 << 27)
+    s = ps(f, {**b, "p_csr": 1.9}, 1 << 27)
     assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, 1, 1)                             # MB -> stream + D16
-    s = S.profile_select({**f, "n_deltas": 12}, {**b, "p_csr": 1.9}, 1 << 27)
+    s = ps({**f, "n_deltas": 12}, {**b, "p_csr": 1.9}, 1 << 27)
     assert (s.variant, s.d16, s.vs) == (S.VARIANT_STREAM, 2, 1)                             # MB, codable -> D8
-    s = S.profile_select(f, {**b, "p_cmp": 1.0}, 1 << 27)
+    s = ps(f, {**b, "p_cmp": 1.0}, 1 << 27)
     assert (s.variant, s.d16) == (S.VARIANT_STREAM, 0)                                      # CMP
     fl = {**f, "n_long": 10, "nnz_max": 5000, "nnz_long": 50000}
-    assert S.profile_select(fl, {**b, "p_imb": 2.0}, 1 << 27).variant == S.VARIANT_SPLIT    # dense long rows
+    assert ps(fl, {**b, "p_imb": 2.0}, 1 << 27).variant == S.VARIANT_SPLIT    # dense long rows
 
 
 # ---- full Table I (reading 23) --------------------------------
@@ -612,3 +615,47 @@ def test_features_all_empty_and_all_long():
     lens = np.array([5000, 6000])
     f = oracle.features(rp_of(lens), np.concatenate([np.arange(L, dtype=np.int32) for L in lens]), n_cols=6000)
     assert f["n_short"] == 0 and f["n_long"] == 2 and f["avg_short"] == 0.0 and f["max_short"] == 0
+
+
+# ---- B200 grid search of Fig. 4's hyperparameters (reading 29) -------
+def test_tuned_thresholds_reproduce_the_recorded_search():
+    """profiles/r02_profile_tuning.json holds the measured bounds and plan times
+    of the grid search (tools/tune_profile.py); its chosen point is the
+    oracle's (and the library's) B200 default, every matrix's recorded classes
+    follow from Fig. 4 on its bounds, and the tool's Fig. 4 is the oracle's."""
+    import json, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    d = json.load(open(os.path.join(root, "profiles", "r02_profile_tuning.json")))
+    assert (d["chosen"]["t_imb"], d["chosen"]["t_ml"], d["chosen"]["tol"]) == \
+        (oracle.T_IMB_B200, oracle.T_ML_B200, oracle.APPROX_TOL_B200)
+    assert (d["paper_knc"]["t_imb"], d["paper_knc"]["t_ml"], d["paper_knc"]["tol"]) == (oracle.T_IMB, oracle.T_ML, oracle.APPROX_TOL)
+    names = {"MB": oracle.CLASS_MB, "ML": oracle.CLASS_ML, "IMB": oracle.CLASS_IMB, "CMP": oracle.CLASS_CMP}
+    for r in d["matrices"]:
+        b = r["bounds_gflops"]
+        args = [b[k] for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak")]
+        for tag, t in (("b200", (oracle.T_IMB_B200, oracle.T_ML_B200, oracle.APPROX_TOL_B200)), ("paper", (oracle.T_IMB, oracle.T_ML, oracle.APPROX_TOL))):
+            c = oracle.classify_profile(*args, t_imb=t[0], t_ml=t[1], tol=t[2])
+            assert c == sum(names[n] for n in r["classes_" + tag]), (r["name"], tag)
+            assert r["plan_" + tag] == r["plan_of_classes"][str(c)]
+    # the tuned point scores at least the paper's on the recorded set
+    assert d["score_chosen"]["geomean"] >= d["score_paper"]["geomean"]
+    sys.path.insert(0, os.path.join(root, "tools"))
+    import tune_profile as T
+    rng = np.random.default_rng(29)
+    for _ in range(2000):
+        v = rng.uniform(0.2, 5.0, 6)
+        t = (rng.uniform(1, 3), rng.uniform(1, 3), rng.uniform(0.05, 0.9))
+        b = dict(zip(("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak"), v))
+        assert T.classify(b, *t) == oracle.classify_profile(*v, t_imb=t[0], t_ml=t[1], tol=t[2])
+
+
+def test_profile_select_forced_classes_follow_table2():
+    """classes= bypasses Fig. 4: the Table II mapping of a given class set
+    (IMB > ML > MB/CMP precedence)."""
+    f = oracle.features(np.array([0, 2, 4, 6]), np.array([0, 1, 1, 2, 0, 2], np.int32))
+    assert oracle.profile_select(f, None, 1 << 30, classes=0).variant == oracle.VARIANT_VECTOR
+    assert oracle.profile_select(f, None, 1 << 30, classes=oracle.CLASS_CMP).variant == oracle.VARIANT_STREAM
+    assert oracle.profile_select(f, None, 1 << 30, classes=oracle.CLASS_ML | oracle.CLASS_CMP).variant == oracle.VARIANT_NNZSPLIT
+    assert oracle.profile_select(f, None, 1 << 30, classes=oracle.CLASS_IMB | oracle.CLASS_ML).variant == oracle.VARIANT_NNZSPLIT
+    for c in range(16):
+        assert oracle.profile_select(f, None, 1 << 30, classes=c).classes == c
