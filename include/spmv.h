@@ -77,7 +77,9 @@ typedef struct spmv_options {
   int32_t emulate_devices; /* ngpus > 1: 1 = place every shard on the current device (tests) */
   int32_t stages;          /* STREAM smem ring depth: 0 = auto (one stage per consumer warp), else a multiple of 4 <= 32 */
   int32_t seg;             /* STREAM / SPLIT short part, segmented consumer mode: -1 auto, 0 off, 1 on */
-  int32_t long_mode;       /* SPLIT long rows: 0 auto, 1 nonzero chunks, 2 column-tiled (x block in smem) */
+  int32_t long_mode;       /* SPLIT long rows: 0 auto, 1 nonzero chunks, 2 column-tiled (x block in smem),
+                              3 column-tiled with TMA-staged chunks on the side stream (experiment, measured slower;
+                              needs the nnz_split bin, split_bins != 0) */
   int32_t split_bins;      /* SPLIT non-long rows: -1 auto (one nnz_split bin), 0 cta_stream length bins, 1 nnz_split bin */
   int32_t hot_x;           /* NNZSPLIT hot-x table in smem: -1 auto (top columns cover >= 20 % of nnz), 0 off,
                               K > 0 = force, at most K (<= 16384) columns */
@@ -162,6 +164,9 @@ typedef struct spmv_plan_info {
   int32_t stream_grid;        /* STREAM: persistent CTAs of shard 0's main kernel */
   int64_t kernel_bytes;       /* compulsory DRAM bytes of one SpMV in the plan's own format (all shards):
                                  values + the index streams the kernel reads + x (n_cols) + y (n_rows) */
+  int32_t long_mode;          /* SPLIT long rows: 0 none, 1 nonzero chunks, 2 column-tiled (fused grid or side
+                                 stream), 3 column-tiled TMA-staged on the side stream (long_tma.cu) */
+  int32_t long_rg;            /* long_mode 2/3: row groups per x block */
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */

@@ -191,6 +191,8 @@ struct Shard {
   double* long_partial = nullptr;
   int long_grid = 0;
   bool split_fused = true;
+  bool long_tma = false;
+  int long_rg = 0;
   // NNZSPLIT (whole shard) / SPLIT short+medium rows as one nnz_split bin
   NzPlan nz;
   bool use_nz = false;
@@ -346,6 +348,8 @@ struct spmv_plan_s {
     a.long_partial = s.long_partial;
     a.long_grid = s.long_grid;
     a.split_fused = s.split_fused;
+    a.long_tma = s.long_tma;
+    a.long_rg = s.long_rg;
     a.nz = s.nz;
     a.use_nz = s.use_nz;
     a.side = s.side;
@@ -534,7 +538,7 @@ void validate_options(const spmv_options& o) {
   if (o.long_chunk != 0 && (o.long_chunk % 256 || o.long_chunk < 256))
     fail(SPMV_E_ARG, "long_chunk must be a positive multiple of 256");
   if (o.l_split < 0 || o.k_long < 0) fail(SPMV_E_ARG, "negative l_split / k_long");
-  if (o.long_mode < 0 || o.long_mode > 2) fail(SPMV_E_ARG, "long_mode must be 0, 1 or 2");
+  if (o.long_mode < 0 || o.long_mode > 3) fail(SPMV_E_ARG, "long_mode must be 0, 1, 2 or 3");
   if (o.select_mode < 0 || o.select_mode > 1) fail(SPMV_E_ARG, "select_mode must be 0 (feature) or 1 (profile)");
   if (!(o.t_imb >= 0) || !(o.t_ml >= 0) || !(o.approx_tol >= 0) || o.approx_tol >= 1)
     fail(SPMV_E_ARG, "t_imb / t_ml must be >= 0 (0 = default) and approx_tol in [0, 1)");
@@ -1354,7 +1358,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
         // per nonzero); long_mode 1/2 forces chunks / tiled
         const int64_t nblk = (s.n_cols + kLongXB - 1) / kLongXB;
         const bool dense = s.hs.nnz_long >= 64 * s.n_long * nblk;
-        s.long_tiled = opt.long_mode == 2 || (opt.long_mode == 0 && dense);
+        s.long_tiled = opt.long_mode >= 2 || (opt.long_mode == 0 && dense);
         if (s.long_tiled) {
           s.nblk = nblk;
           s.long_seg = s.alloc<int64_t>((size_t)s.n_long * (nblk + 1));
@@ -1365,6 +1369,15 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
           if (const char* e = getenv("SPMV_LONG_CTAS")) per_sm = atoi(e);
           s.long_grid = long_tiled_grid(nblk, s.sm_count, per_sm);
           if (const char* e = getenv("SPMV_SPLIT_FUSED")) s.split_fused = atoi(e) != 0;
+          // long_mode 3: TMA-staged long rows, one persistent CTA per SM on the
+          // side stream next to the short rows' bin (long_tma.cu)
+          if (opt.long_mode == 3 && opt.split_bins != 0 &&
+              ((uintptr_t)A.col & 15) == 0 && ((uintptr_t)A.val & 15) == 0) {
+            if (long_tma_prepare() != 0) ck(cudaGetLastError(), "long_tma smem attribute");
+            s.long_tma = true;
+            s.long_rg = long_tma_rg(s.n_long, nblk, s.sm_count);
+            s.split_fused = false;
+          }
         }
         // the long rows run on a side stream, concurrently with the bins
         ck(cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -2140,6 +2153,10 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
           kb += 4 * s.nnz + (int64_t)p->rp_bytes * (s.m + 1);
       }
       info->kernel_bytes = kb;
+    }
+    if (s0.n_long > 0) {
+      info->long_mode = s0.long_tma ? 3 : s0.long_tiled ? 2 : 1;
+      info->long_rg = s0.long_tma ? s0.long_rg : s0.long_tiled ? 2 : 0;
     }
     info->tile_nnz = s0.sp[0].C;
     info->n_tiles = s0.sp[0].T;

@@ -263,6 +263,8 @@ struct ExecArgs {
   double* long_partial;       // [n_long][nblk]
   int long_grid;              // persistent grid of the column-tiled kernel
   bool split_fused;           // SPLIT: nz bin + tiled long rows interleaved in one grid
+  bool long_tma;              // SPLIT long_mode 3: TMA-staged tiled long rows (long_tma.cu) on the side stream
+  int long_rg;                // its row groups per x block
 };
 
 #ifndef LONG_XB
@@ -273,6 +275,10 @@ void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long,
                      cudaStream_t s);
 void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s);
 int long_tiled_grid(int64_t nblk, int sm_count, int per_sm);
+size_t long_tma_smem_bytes();
+int long_tma_prepare();                                        // smem attribute (< 0 on error)
+int long_tma_rg(int64_t n_long, int64_t nblk, int sm_count);   // row groups per x block (<= 32 rows per warp)
+void launch_long_tma(const ExecArgs& a, int sm_count, cudaStream_t s);
 
 int launch_vector(const ExecArgs& a, bool skip_long, cudaStream_t s);  // returns #launches
 int launch_stream_plan(const StreamPlan& sp, const double* x, double* y, int stage, cudaStream_t s);

@@ -448,7 +448,8 @@ int launch_split(const ExecArgs& a, cudaStream_t s) {
   }
   if (longs && a.stage != 2) {
     ++n;
-    if (a.long_tiled) launch_long_tiled(a, 1, ls);
+    if (a.long_tma && ((uintptr_t)a.x & 15) == 0) launch_long_tma(a, a.sm_count, ls);
+    else if (a.long_tiled) launch_long_tiled(a, 1, ls);
     else if (a.A.rp_bytes == 8)
       long_chunk_kernel<int64_t><<<(int)a.n_chunks, kNT, 0, ls>>>((const int64_t*)a.A.rowptr, a.A.col, a.A.val,
                                                                   a.x, a.long_rows, a.chunk_start, a.n_long, a.chunk,

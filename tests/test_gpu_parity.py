@@ -41,7 +41,7 @@ def m_maxlen(m):
 
 VARIANTS = [("vector", 1), ("vector", 2), ("vector", 8), ("vector", 32), ("stream", 1), ("stream", 4),
             ("stream", 8), ("stream", 32), ("stream_seg", 1), ("stream_nnz_tiles", 1), ("merge", 0), ("split", 4),
-    ("split_seg", 32), ("split_chunks", 16), ("split_tiled", 8), ("split_bins", 8), ("nnzsplit", 0),
+    ("split_seg", 32), ("split_chunks", 16), ("split_tiled", 8), ("split_tma", 8), ("split_bins", 8), ("nnzsplit", 0),
     ("nnzsplit_hot", 0), ("nnzsplit_nohot", 0)]
 ALL = ("vector", "stream", "merge", "split", "nnzsplit")
 
@@ -66,6 +66,8 @@ def variant_kw(variant):
         return "split", {"long_mode": 1}
     if variant == "split_tiled":
         return "split", {"long_mode": 2}
+    if variant == "split_tma":
+        return "split", {"long_mode": 3}
     if variant == "stream_nnz_tiles":
         return "stream", {"no_aligned": 1}
     return variant, {}
@@ -80,6 +82,51 @@ def test_small_suite_all_variants(name, m, variant, vs):
     y = p.execute(m.x)
     assert_bound(y, m)
     assert p.info()["variant"] == fv
+
+
+LONG_TMA_CASES = [  # (n, k per short row, long rows, nonzeros per long row, l_split)
+    (5001, 6, 300, 1500, 64),     # 300 long rows: > 32 rows per warp at rg = 1, so rg > 1; odd n: odd last x block
+    (20000, 15, 10, 4500, 64),    # C4 small
+    (3000, 4, 3, 2990, 64),       # nearly dense long rows
+    (70001, 3, 5, 60000, 4096),   # long segments: several chunks per (row, x block)
+    (9000, 5, 40, 300, 64),       # sparse long rows: many empty (row, x block) segments
+]
+
+
+@pytest.mark.parametrize("case", LONG_TMA_CASES)
+@pytest.mark.parametrize("dyadic", [False, True])
+def test_split_long_tma(case, dyadic):
+    """long_mode 3: TMA-staged column-tiled long rows on the side stream
+    (long_tma.cu) next to the nnz_split bin; every row within the per-row
+    bound, dyadic inputs bit-equal to the oracle, and x at an address that is
+    not 16-B aligned takes the register-staged kernel."""
+    import torch
+    n, k, nl, kl, ls = case
+    mode = sg.MODE_DYADIC if dyadic else sg.MODE_U11
+    m = sg.randrows(n, k, diag=False, long_rows=sg.pick_rows(n, nl, 77 + n), k_long=kl, col_seed=5 + n,
+                    val_mode=mode, val_seed=6, x_seed=7, x_mode=mode)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=n, force_variant="split", long_mode=3, l_split=ls)
+    info = p.info()
+    assert info["variant"] == "split" and info["long_mode"] == 3 and info["long_rg"] >= 1
+    assert -(-nl // (info["long_rg"] * 8)) <= 32  # rows of a warp inside an item fit the lanes
+    y = p.execute(m.x)
+    if dyadic:
+        assert np.array_equal(y, oracle.spmv(m.rowptr, m.colind, m.vals, m.x))
+    else:
+        assert_bound(y, m)
+    xb = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    xb[1:] = torch.from_numpy(m.x)
+    yd = torch.empty(n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        p.execute(xb[1:], yd)  # 8-B offset: the fallback kernel (its own summation order)
+        if dyadic:
+            assert np.array_equal(yd.cpu().numpy(), y)
+        else:
+            assert_bound(yd.cpu().numpy(), m)
+    xa = torch.from_numpy(m.x).cuda()
+    for _ in range(3):  # back-to-back launches on the plan's streams
+        p.execute(xa, yd)
+    assert np.array_equal(yd.cpu().numpy(), y)
 
 
 @pytest.mark.parametrize("tile", [128, 384, 1024])

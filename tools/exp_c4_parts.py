@@ -41,6 +41,14 @@ def run(name, m, variants):
 
 
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "--tma":  # long_mode 2 vs 3 only
+        s = sg.seeds(4)
+        lr = sg.pick_rows(1000000, 100, s["pick"])
+        longm = sg.randrows(1000000, 0, diag=False, long_rows=lr, k_long=200000, col_seed=s["matrix"],
+                            val_seed=s["value"], x_seed=s["x"])
+        run("long", longm, [dict(force_variant="split", long_mode=2), dict(force_variant="split", long_mode=3)])
+        run("full", sg.config(4), [dict(force_variant="split", long_mode=2), dict(force_variant="split", long_mode=3)])
+        return
     s = sg.seeds(4)
     n, nl, kl = 1000000, 100, 200000
     lr = sg.pick_rows(n, nl, s["pick"])
@@ -48,11 +56,13 @@ def main():
     short = sg.randrows(n, 15, diag=False, col_seed=s["matrix"], val_seed=s["value"], x_seed=s["x"])
     longm = sg.randrows(n, 0, diag=False, long_rows=lr, k_long=kl, col_seed=s["matrix"], val_seed=s["value"],
                         x_seed=s["x"])
-    run("full", full, [{}, dict(force_variant="nnzsplit"), dict(force_variant="split", split_bins=0)])
+    run("full", full, [{}, dict(force_variant="split", long_mode=3), dict(force_variant="nnzsplit"),
+                       dict(force_variant="split", split_bins=0)])
     run("short", short, [{}, dict(force_variant="nnzsplit"), dict(force_variant="nnzsplit", hot_x=0),
                          dict(force_variant="stream"), dict(force_variant="stream", seg=1),
                          dict(force_variant="vector", force_vs=16), dict(force_variant="merge")])
-    run("long", longm, [{}, dict(force_variant="split", long_mode=2), dict(force_variant="split", long_mode=1),
+    run("long", longm, [{}, dict(force_variant="split", long_mode=2), dict(force_variant="split", long_mode=3),
+                        dict(force_variant="split", long_mode=1),
                         dict(force_variant="nnzsplit")])
 
 
