@@ -167,6 +167,9 @@ typedef struct spmv_plan_info {
   int32_t long_mode;          /* SPLIT long rows: 0 none, 1 nonzero chunks, 2 column-tiled (fused grid or side
                                  stream), 3 column-tiled TMA-staged on the side stream (long_tma.cu) */
   int32_t long_rg;            /* long_mode 2/3: row groups per x block */
+  int32_t iter_push;          /* 1: the multi-shard iterated mode pushes each shard's halo rows into its
+                                 neighbours' replicas from the SpMV kernel (banded row blocks; 0 = halo copies) */
+  int32_t pad2_;
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */

@@ -95,7 +95,8 @@ class PlanInfo(ctypes.Structure):
                [("profile_vs", ctypes.c_int32), ("profile_ctas", ctypes.c_int32), ("profile_ms", ctypes.c_double),
                ("x_reuse", ctypes.c_double), ("nz_gather_l2", ctypes.c_int32), ("stream_stages", ctypes.c_int32),
                ("d8_n_dict", ctypes.c_int32), ("stream_grid", ctypes.c_int32), ("kernel_bytes", ctypes.c_int64),
-               ("long_mode", ctypes.c_int32), ("long_rg", ctypes.c_int32)]
+               ("long_mode", ctypes.c_int32), ("long_rg", ctypes.c_int32), ("iter_push", ctypes.c_int32),
+               ("pad2_", ctypes.c_int32)]
 
 
 _vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double

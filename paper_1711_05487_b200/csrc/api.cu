@@ -205,6 +205,10 @@ struct Shard {
   // shard's own x block, the others wait for the halo copies
   bool ovl_ready = false, ovl = false;
   int64_t kb = 0, ke = 0;
+  // halo push (IterOut::push_*): the lower / upper neighbour that reads this
+  // block's first rows [0, push_lo_end) / last rows [push_hi_begin, m) (local)
+  int push_lo_peer = -1, push_hi_peer = -1;
+  int64_t push_lo_end = 0, push_hi_begin = 0;
   cudaStream_t cp = nullptr;     // halo copy stream
   cudaEvent_t ev_cp = nullptr;   // halo copies of the current iteration done
   double* x2 = nullptr;       // second x replica (deferred-normalisation ping-pong)
@@ -302,6 +306,7 @@ struct spmv_plan_s {
   double profile_ms = 0.0;  // nnz_split hot-x set: fraction of nonzeros in the hot columns
 
   bool l2_limit_set = false;  // this plan raised the device's persisting-L2 limit (x window)
+  bool push_ready = false, push_ok = false;  // multi-shard iteration: halo push (prepare_push)
   ~spmv_plan_s() {
     for (auto& s : shards) s.release();
     if (l2_limit_set) {
@@ -1816,7 +1821,7 @@ namespace {
 // the norm step): one launch per iteration. Other variants: the SpMV, one
 // scale + partials pass over y, the norm-step kernel.
 int spmv_iter(const spmv_plan_s* P, Shard& s, const double* x, double* y, double* partials, double* nn,
-              double* nu_k) {
+              double* nu_k, const IterOut* push = nullptr) {
   const StreamPlan& sp = s.sp[0];
   if (P->sel.variant == SPMV_VARIANT_STREAM && sp.aligned && !sp.seg && !sp.rowmap && !sp.need_fixup &&
       !getenv("SPMV_NO_FUSED_NORM")) {
@@ -1832,6 +1837,12 @@ int spmv_iter(const spmv_plan_s* P, Shard& s, const double* x, double* y, double
     it.partials = partials;
     it.nn = nu_k ? nn : nullptr;
     it.nu_k = nu_k;
+    if (push) {
+      it.push_lo = push->push_lo;
+      it.push_lo_end = push->push_lo_end;
+      it.push_hi = push->push_hi;
+      it.push_hi_begin = push->push_hi_begin;
+    }
     return launch_stream_iter(sp, x, y, it, s.stream);
   }
   int n = P->launch(s, x, y);
@@ -1894,6 +1905,54 @@ void prepare_overlap(const spmv_plan_s* P, Shard& s) {
     s.kb = kb;
     s.ke = ke;
   }
+}
+
+// Halo push (the exchange fused into the SpMV): usable when
+// every shard runs the fused-capable kernel and the rows each peer reads from
+// a shard form a prefix of its block (one lower neighbour) and/or a suffix
+// (one upper neighbour) -- banded row blocks -- and, across devices, the
+// writer has peer access to the reader. Then shard g's kernel stores those
+// rows of yh_k into the neighbours' next replicas as it writes them and the
+// separate halo copies disappear.
+bool prepare_push(spmv_plan_s* P) {
+  if (P->push_ready) return P->push_ok;
+  P->push_ready = true;
+  P->push_ok = false;
+  const int G = (int)P->shards.size();
+  if (G < 2 || getenv("SPMV_NO_PUSH")) return false;
+  for (auto& s : P->shards) {
+    const StreamPlan& sp = s.sp[0];
+    if (!(P->sel.variant == SPMV_VARIANT_STREAM && sp.aligned && !sp.seg && !sp.rowmap && !sp.need_fixup &&
+          stream_push_capable(sp)))
+      return false;
+    s.push_lo_peer = s.push_hi_peer = -1;
+  }
+  for (int g = 0; g < G; ++g) {
+    Shard& s = P->shards[g];
+    for (int h = 0; h < G; ++h) {
+      if (h == g) continue;
+      const Shard& t = P->shards[h];
+      if (t.hs.col_min > t.hs.col_max) continue;  // reads nothing
+      const int64_t a = std::max<int64_t>(t.hs.col_min, s.row0), b = std::min<int64_t>(t.hs.col_max + 1, s.row0 + s.m);
+      if (a >= b) continue;
+      if (s.dev != t.dev) {
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, s.dev, t.dev) != cudaSuccess || !can) return false;
+      }
+      if (h < g) {
+        if (s.push_lo_peer >= 0 || a != s.row0) return false;
+        s.push_lo_peer = h;
+        s.push_lo_end = b - s.row0;
+      } else {
+        if (s.push_hi_peer >= 0 || b != s.row0 + s.m) return false;
+        s.push_hi_peer = h;
+        s.push_hi_begin = a - s.row0;
+      }
+    }
+  }
+  cudaGetLastError();
+  P->push_ok = true;
+  return true;
 }
 
 // ML x-window on the replica the next SpMV reads (the iterate ping-pongs)
@@ -1969,7 +2028,8 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
     // multi-shard: interior tiles of every shard first (they read only its own
     // x block), the halo copies of the other blocks concurrently on a copy
     // stream, then the boundary tiles
-    if (G > 1)
+    const bool push = G > 1 && prepare_push(p);
+    if (G > 1 && !push)
       for (auto& s : p->shards) prepare_overlap(p, s);
     // single shard, row-aligned STREAM / D8: the prologue-norm iteration
     const StreamPlan& sp1 = p->shards[0].sp[0];
@@ -2018,8 +2078,34 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
         std::swap(cur, nxt);
         continue;
       }
+      if (push) {
+        // the SpMV of every shard writes yh_k into its own block of nxt and
+        // the rows its neighbours read straight into THEIR nxt replicas; the
+        // neighbour reads them at k + 1, after its norm step k waited for
+        // this shard's SpMV (step D), and this shard writes into a replica
+        // only after every peer's SpMV k - 1 finished reading it (its own
+        // step D of k - 1)
+        for (int g = 0; g < G; ++g) {
+          Shard& s = p->shards[g];
+          ck(cudaSetDevice(s.dev), "cudaSetDevice");
+          set_xwin(p, s, cur[g]);
+          IterOut po;
+          if (s.push_lo_peer >= 0) {
+            po.push_lo = nxt[s.push_lo_peer] + s.row0;
+            po.push_lo_end = s.push_lo_end;
+          }
+          if (s.push_hi_peer >= 0) {
+            po.push_hi = nxt[s.push_hi_peer] + s.row0;
+            po.push_hi_begin = s.push_hi_begin;
+          }
+          double* part = s.allpart + half + (size_t)g * RP;
+          count_launches(spmv_iter(p, s, cur[g], nxt[g] + s.row0, part, s.nn, nullptr, &po), "iteration step (push)");
+          ck(cudaMemsetAsync(part + kNormPartials, 0, 2 * kNormPartials * 8, s.stream), "memset");
+          ck(cudaEventRecord(s.ev_part, s.stream), "event");
+        }
+      }
       // A. interior tiles (overlap-capable shards)
-      for (int g = 0; g < G; ++g) {
+      for (int g = 0; g < G && !push; ++g) {
         Shard& s = p->shards[g];
         if (!s.ovl || k == 0) continue;
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -2030,7 +2116,7 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
       // B. halo of yh_{k-1}: the part of each other block inside the x range
       // shard g reads, copied into g's replica (not needed at k = 0: every
       // replica holds x_0)
-      if (k > 0)
+      if (k > 0 && !push)
         for (int g = 0; g < G; ++g) {
           Shard& s = p->shards[g];
           ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -2046,7 +2132,7 @@ spmv_status spmv_iterate(spmv_plan p, const double* x0, double* x_out, int iters
           ck(cudaEventRecord(s.ev_cp, s.cp), "event");
         }
       // C. boundary tiles (or the whole shard) once the halo is in
-      for (int g = 0; g < G; ++g) {
+      for (int g = 0; g < G && !push; ++g) {
         Shard& s = p->shards[g];
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
         if (k > 0) ck(cudaStreamWaitEvent(s.stream, s.ev_cp, 0), "wait");
@@ -2154,6 +2240,7 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
       }
       info->kernel_bytes = kb;
     }
+    info->iter_push = p->push_ready && p->push_ok ? 1 : 0;
     if (s0.n_long > 0) {
       info->long_mode = s0.long_tma ? 3 : s0.long_tiled ? 2 : 1;
       info->long_rg = s0.long_tma ? s0.long_rg : s0.long_tiled ? 2 : 0;

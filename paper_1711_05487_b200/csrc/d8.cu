@@ -87,7 +87,7 @@ __device__ __forceinline__ void d8_arrive(uint64_t* bar) {
 
 // Consumer warps' tile loop; returns the warp's sum of squares of the rows it
 // wrote (its tiles in launch order; 0 outside the iterated mode).
-template <int CW, bool SCALE, int UN, int CB, bool PK>
+template <int CW, bool SCALE, int UN, int CB, bool PK, bool PU>
 __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, const D8Layout& L, uint64_t* full,
                                              uint64_t* empty, const D8Meta* meta, const int32_t* dict_s, double f) {
   const int S = p.stages;
@@ -167,7 +167,8 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
       if constexpr (SCALE) acc *= f;
       if (q < nrows) {
         SPMV_CHECK(R0 + q < p.m);
-        p.y[R0 + q] = acc;
+        if constexpr (PU) iter_store(p.it, p.y, R0 + q, acc);  // + the neighbours' replicas
+        else p.y[R0 + q] = acc;
         sqa = fma(acc, acc, sqa);
       }
     }
@@ -183,7 +184,9 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
 // registers, UN = 16 -> ~96
 constexpr int d8_lb(int CW, int UN) { return UN == 8 ? (CW == 4 ? 5 : (CW == 6 ? 4 : 3)) : (CW == 4 ? 4 : (CW == 6 ? 3 : 2)); }
 
-template <int CW, int UN, int CB, bool PK>
+// PU: the multi-shard halo push instantiation (IterOut::push_*; 8-bit codes,
+// unpacked tiles only -- d8_push_capable)
+template <int CW, int UN, int CB, bool PK, bool PU = false>
 __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const D8P p) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int32_t dict_s[256];
@@ -291,8 +294,11 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
     mbar_wait(fbar, 0u);
     f = f_s;
   }
-  const double wsq = f == 1.0 ? d8_consume<CW, false, UN, CB, PK>(p, smem, L, full, empty, meta, dict_s, 1.0)
-                              : d8_consume<CW, true, UN, CB, PK>(p, smem, L, full, empty, meta, dict_s, f);
+  double wsq;
+  if constexpr (PU) wsq = d8_consume<CW, true, UN, CB, PK, true>(p, smem, L, full, empty, meta, dict_s, f);
+  else
+    wsq = f == 1.0 ? d8_consume<CW, false, UN, CB, PK, false>(p, smem, L, full, empty, meta, dict_s, 1.0)
+                   : d8_consume<CW, true, UN, CB, PK, false>(p, smem, L, full, empty, meta, dict_s, f);
   iter_epilogue<32 * CW>(p.it, wsq);
 }
 
@@ -325,6 +331,11 @@ static int d8_prepare_t(const StreamPlan& sp, int sm_count) {
   if (cudaFuncSetAttribute(d8_kernel<CW, UN, CB, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return -1;
+  if constexpr (CB == 8 && !PK) {
+    if (cudaFuncSetAttribute(d8_kernel<CW, UN, CB, PK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return -1;
+  }
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN, CB, PK>, 32 * (CW + 1), smem) !=
           cudaSuccess ||
@@ -348,9 +359,18 @@ static int d8_per_sm_t(const StreamPlan& sp) {
 
 template <int CW, int UN, int CB, bool PK>
 static void d8_launch_t(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
+  if constexpr (CB == 8 && !PK) {
+    if (sp.it.push_lo || sp.it.push_hi) {
+      launch_pdl(d8_kernel<CW, UN, CB, PK, true>, dim3(sp.grid), dim3(32 * (CW + 1)),
+                 d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB), s, d8_params(sp, x, y));
+      return;
+    }
+  }
   launch_pdl(d8_kernel<CW, UN, CB, PK>, dim3(sp.grid), dim3(32 * (CW + 1)),
              d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB), s, d8_params(sp, x, y));
 }
+
+bool d8_push_capable(const StreamPlan& sp) { return sp.d8_bits == 8 && !sp.d8_tiles; }
 
 // (stages = consumer warps CW) x (batch width UN) x (code layout) -> instantiation
 template <int UN, int CB, bool PK, typename F>

@@ -69,7 +69,22 @@ struct IterOut {
   int rev = 0;  // D8: walk the tiles from the end (every other iteration: x lines still in L2)
   double* st = nullptr;
   bool cta_only = false;
+  // multi-shard iteration, halo push: the kernel also stores
+  // its rows [0, push_lo_end) into push_lo and [push_hi_begin, m) into
+  // push_hi -- a neighbour shard's next replica (peer memory over NVLink, or
+  // the same device when emulated), pre-offset so index r is local row r
+  double* push_lo = nullptr;
+  int64_t push_lo_end = 0;
+  double* push_hi = nullptr;
+  int64_t push_hi_begin = 0;
 };
+
+// the y store of the iterated kernels: own block + the neighbours' replicas
+__device__ __forceinline__ void iter_store(const IterOut& it, double* y, int64_t r, double v) {
+  y[r] = v;
+  if (it.push_lo && r < it.push_lo_end) it.push_lo[r] = v;
+  if (it.push_hi && r >= it.push_hi_begin) it.push_hi[r] = v;
+}
 
 struct MatView {
   int rp_bytes;
@@ -118,6 +133,8 @@ struct StreamPlan {
 };
 size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages, int CB = 8);
 int d8_prepare(const StreamPlan& sp, int sm_count);  // stages = consumer warps (4, 6, 8)
+bool d8_push_capable(const StreamPlan& sp);           // has the halo-push instantiation
+bool stream_push_capable(const StreamPlan& sp);       // STREAM / D8 iterated kernel with the halo push
 int d8_per_sm(const StreamPlan& sp);                 // resident CTAs per SM (after d8_prepare)
 void launch_d8(const StreamPlan& sp, const double* x, double* y, cudaStream_t s);
 void launch_d8_encode(const MatView& A, int64_t row0, const int32_t* dict_dev, int nd, uint8_t* codes, uint8_t* rlen,

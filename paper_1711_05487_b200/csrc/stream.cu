@@ -263,6 +263,21 @@ __device__ __noinline__ void stream_rescale_rows(const int32_t* tile_row, double
     for (int64_t r = r0 + lane; r < r1; r += 32) y[r] = __ldcg(y + r) * f;
   }
 }
+// ... and again in the neighbours' replicas the rows were pushed to (MODE 3)
+__device__ __noinline__ void stream_rescale_rows_push(const int32_t* tile_row, double* y, int64_t k0, int64_t T,
+                                                      int CW, double f, double* plo, int64_t lo_end, double* phi,
+                                                      int64_t hi_begin) {
+  const int w = (threadIdx.x >> 5) - 1, lane = threadIdx.x & 31;
+  for (int64_t k = k0 + blockIdx.x + (int64_t)w * gridDim.x; k < T; k += (int64_t)CW * gridDim.x) {
+    const int64_t r0 = __ldg(tile_row + k), r1 = __ldg(tile_row + k + 1);
+    for (int64_t r = r0 + lane; r < r1; r += 32) {
+      const double v = __ldcg(y + r) * f;
+      y[r] = v;
+      if (plo && r < lo_end) plo[r] = v;
+      if (phi && r >= hi_begin) phi[r] = v;
+    }
+  }
+}
 
 // MODE: 0 = row-step over nnz-aligned tiles, 1 = segmented, 2 = row-step over
 // row-aligned tiles (compile-time so the nnz-tile path carries no per-tile
@@ -276,7 +291,8 @@ __global__ void __launch_bounds__(32 * (CW + 1),
                                   MODE == 1 ? 4 : (CW != 4 ? 24 / CW : (D16 ? SPMV_D16_LB : SPMV_STREAM_LB)))
     stream_kernel(const StreamP<RP> p) {
   constexpr bool SEG = MODE == 1;
-  constexpr bool AL = MODE == 2;
+  constexpr bool AL = MODE >= 2;
+  constexpr bool PUSH = MODE == 3;  // row-aligned + the multi-shard halo push (IterOut::push_*)
   constexpr bool ESC = D16 == 2;
   extern __shared__ __align__(128) unsigned char smem[];
   const StreamLayout L = stream_layout(p.C, p.stages, (int)sizeof(RP), p.rows_cap, D16, SEG);
@@ -559,7 +575,8 @@ __global__ void __launch_bounds__(32 * (CW + 1),
             p.carry_row[k] = (int32_t)out_row(p, r);
             p.carry_val[k] = acc;
           } else {
-            p.y[out_row(p, r)] = acc;
+            if constexpr (PUSH) iter_store(p.it, p.y, out_row(p, r), acc);
+            else p.y[out_row(p, r)] = acc;
             if constexpr (AL) sqa = fma(acc, acc, sqa);
           }
         }
@@ -575,7 +592,11 @@ __global__ void __launch_bounds__(32 * (CW + 1),
       asm volatile("bar.sync 1, %0;" ::"r"(32 * CW) : "memory");
       const double f = f_s;
       if (f != 1.0) {  // rescale the rows this warp wrote (rowmap is null on this path; out of line)
-        stream_rescale_rows(p.tile_row, p.y, p.k0, p.T, CW, f);
+        if constexpr (PUSH)
+          stream_rescale_rows_push(p.tile_row, p.y, p.k0, p.T, CW, f, p.it.push_lo, p.it.push_lo_end, p.it.push_hi,
+                                   p.it.push_hi_begin);
+        else
+          stream_rescale_rows(p.tile_row, p.y, p.k0, p.T, CW, f);
         wsq *= f * f;  // exact: f is a power of two
       }
     }
@@ -639,7 +660,7 @@ static void stream_launch_t(const StreamPlan& sp, const double* x, double* y, cu
 template <int VS, typename RP, int D16, int MODE, bool PREP>
 static int stream_one(const StreamPlan& sp, int sm_count, const double* x, double* y, cudaStream_t s) {
   // 6 consumer warps only for the plain row-aligned one-lane-per-row kernel
-  if constexpr (VS == 1 && D16 <= 1 && MODE == 2) {
+  if constexpr (VS == 1 && D16 <= 1 && MODE >= 2) {
     if (sp.stages == 6) {
       if (PREP) return stream_prepare_t<VS, RP, D16, MODE, 6>(sp, sm_count);
       stream_launch_t<VS, RP, D16, MODE, 6>(sp, x, y, s);
@@ -668,6 +689,16 @@ static int stream_rp(const StreamPlan& sp, int smc, const double* x, double* y, 
   const int d16 = sp.dcol == nullptr ? 0 : (sp.n_esc > 0 ? 2 : 1);
   if (sp.seg && !d16) return stream_one<1, RP, 0, 1, PREP>(sp, smc, x, y, s);
   if (sp.aligned) {
+    // the halo-push instantiation (multi-shard iterated mode): int32 colind,
+    // one lane per row only (prepare_push checks stream_push_capable)
+    if (sp.vs == 1 && !d16) {
+      if (PREP) {
+        const int g = stream_one<1, RP, 0, 3, true>(sp, smc, x, y, s);
+        if (g < 0) return g;
+      } else if (sp.it.push_lo || sp.it.push_hi) {
+        return stream_one<1, RP, 0, 3, false>(sp, smc, x, y, s);
+      }
+    }
     if (d16 == 2) return stream_vs<RP, 2, 2, PREP>(sp, smc, x, y, s);
     return d16 ? stream_vs<RP, 1, 2, PREP>(sp, smc, x, y, s) : stream_vs<RP, 0, 2, PREP>(sp, smc, x, y, s);
   }
@@ -683,6 +714,12 @@ static int stream_dispatch(const StreamPlan& sp, int smc, const double* x, doubl
     return 0;
   }
   return sp.V.rp_bytes == 8 ? stream_rp<int64_t, PREP>(sp, smc, x, y, s) : stream_rp<int32_t, PREP>(sp, smc, x, y, s);
+}
+
+// the plan's iterated kernel has a halo-push instantiation
+bool stream_push_capable(const StreamPlan& sp) {
+  if (sp.codes) return d8_push_capable(sp);
+  return sp.aligned && !sp.seg && !sp.rowmap && sp.vs == 1 && sp.dcol == nullptr;
 }
 
 int stream_prepare(const StreamPlan& sp, int sm_count) {

@@ -856,6 +856,48 @@ def test_iterated_fused_paths_rescale(scale, G, d16):
         assert np.all(np.abs(nug - nuk) <= 1e-12 * nuk), k
 
 
+@pytest.mark.parametrize("G,d16", [(2, 0), (3, 2), (4, 2), (8, 0)])
+def test_iterated_halo_push(G, d16, monkeypatch):
+    """Multi-shard iteration with the halo exchange fused into the SpMV
+    (each shard's kernel stores the rows its neighbours read into their next
+    replicas): banded row blocks take it; the result matches
+    the per-step oracle and the halo-copy path (SPMV_NO_PUSH)."""
+    m = sg.stencil(12, 27, x_seed=8)  # 1728 rows, band 157: every shard reads only its neighbours at G <= 8
+    K = 40
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, K)
+    assert rc == 0
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, ngpus=G, emulate_devices=1, force_variant="stream", d16=d16)
+    xg, nug = p.iterate(m.x, K)
+    assert p.info()["iter_push"] == 1
+    assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
+    assert np.all(np.abs(nug - nur) <= 1e-12 * nur)
+    for k in (1, 2, 7):  # the exchange of the first steps
+        xk, _ = p.iterate(m.x, k)
+        rc, xo, _ = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, k)
+        assert np.max(np.abs(xk - xo)) <= 1e-10 * np.max(np.abs(xo)), k
+    monkeypatch.setenv("SPMV_NO_PUSH", "1")
+    q = spmv.Plan(m.rowptr, m.colind, m.vals, ngpus=G, emulate_devices=1, force_variant="stream", d16=d16)
+    xc, nuc = q.iterate(m.x, K)
+    assert q.info()["iter_push"] == 0
+    assert np.max(np.abs(xg - xc)) <= 1e-13 * np.max(np.abs(xc))  # same SpMVs; the norm partials group differently
+    assert np.all(np.abs(nug - nuc) <= 1e-13 * nuc)
+
+
+def test_iterated_push_not_for_scattered_blocks():
+    # every shard of a random square matrix reads every block: no prefix /
+    # suffix halo, the halo copies run instead (still matching the oracle)
+    m = sg.randrows(3000, 6, diag=True, col_seed=11, val_seed=12, x_seed=13, val_mode=sg.MODE_U01)
+    K = 20
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, K)
+    assert rc == 0
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, ngpus=3, emulate_devices=1, force_variant="stream", seg=0)
+    assert p.info()["tiles_row_aligned"] == 1 and p.info()["sel"]["seg"] == 0  # the fused-capable kernel
+    xg, nug = p.iterate(m.x, K)
+    assert p.info()["iter_push"] == 0
+    assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
+    assert np.all(np.abs(nug - nur) <= 1e-12 * nur)
+
+
 @pytest.mark.parametrize("rb,re", [(0, 3000), (2000, 5500), (5000, 8000)])
 def test_d8_row_block_plan(rb, re):
     # one rank's row block of a 27-pt stencil (the torchrun layout: n_rows <
