@@ -170,6 +170,9 @@ typedef struct spmv_plan_info {
   int32_t iter_push;          /* 1: the multi-shard iterated mode pushes each shard's halo rows into its
                                  neighbours' replicas from the SpMV kernel (banded row blocks; 0 = halo copies) */
   int32_t pad2_;
+  double p_stream;            /* profile mode, second stage: flop/s of the plain cta_stream kernel when Fig. 4
+                                 mapped the matrix to it and its indices are D8-codable; >= (1 - tol) P_MB adds
+                                 MB and D8 (reading 30); 0 when not run */
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */

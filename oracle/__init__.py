@@ -557,7 +557,7 @@ def classify_profile(p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak, t_imb=T_IMB, t_ml=
 
 
 def profile_select(f, bounds, window_max, K_long=100, t_imb=T_IMB_B200, t_ml=T_ML_B200, tol=APPROX_TOL_B200,
-                   classes=None):
+                   classes=None, p_stream=None):
     """Table II for the GPU variants: IMB -> long_row_split (dense
     long rows) or nnz_split; ML -> nnz_split with the x window; MB / CMP ->
     cta_stream (MB adds D8 codes when codable, else 16-bit deltas when the
@@ -565,7 +565,12 @@ def profile_select(f, bounds, window_max, K_long=100, t_imb=T_IMB_B200, t_ml=T_M
     baseline (csr_vector), "not worth applying any" (P:459-461). Precedence
     IMB > ML > MB/CMP. bounds: dict with p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak;
     t_imb / t_ml / tol: Fig. 4's hyperparameters (default: the B200 grid
-    search); classes: a given CLASS_* set instead of Fig. 4 (bounds unused)."""
+    search); classes: a given CLASS_* set instead of Fig. 4 (bounds unused);
+    p_stream: the second stage (reading 30) -- the measured rate of
+    the plain cta_stream kernel a CMP matrix was mapped to: if its indices
+    are D8-codable and it reaches (1 - tol) P_MB, Fig. 4's MB test holds for
+    the optimised kernel and MB (D8) is applied jointly."""
+    forced = classes is not None
     if classes is None:
         classes = classify_profile(*(bounds[k] for k in ("p_csr", "p_mb", "p_ml", "p_imb", "p_cmp", "p_peak")),
                                    t_imb=t_imb, t_ml=t_ml, tol=tol)
@@ -588,6 +593,11 @@ def profile_select(f, bounds, window_max, K_long=100, t_imb=T_IMB_B200, t_ml=T_M
     if classes & CLASS_MB and variant == VARIANT_STREAM:  # MB -> deltas: D8 when codable, else 16-bit
         d8_ok = f.get("n_deltas", D8_MAX + 1) <= D8_MAX and f["nnz_max"] <= D8_MAX_ROW and vs == 1
         d16 = 2 if d8_ok else (1 if f["maxgap"] <= 65535 else 0)
+    if (p_stream and not forced and variant == VARIANT_STREAM and d16 == 0 and vs == 1
+            and f.get("n_deltas", D8_MAX + 1) <= D8_MAX and 0 < f["nnz_max"] <= D8_MAX_ROW
+            and f["nnz_max"] <= 1.25 * f["nnz_avg"] + 1.0 and p_stream >= (1 - tol) * bounds["p_mb"]):
+        classes |= CLASS_MB
+        d16 = 2
     xwin = bool(classes & CLASS_ML) and 8 * f["n"] <= window_max
     return Selection(variant, vs, d16, xwin, classes)
 

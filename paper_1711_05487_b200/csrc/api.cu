@@ -532,6 +532,14 @@ void profile_select_impl(const spmv_features& f, const spmv_device_props& d, con
   s.seg = 0;
 }
 
+// profile mode, second stage (reading 30): the D8 conditions of the feature
+// rules -- at most 256 distinct row-relative deltas, rows <= 255 nonzeros,
+// regular rows, one lane per row
+bool profile_stage2_ok(const spmv_features& f, const spmv_selection& s) {
+  const bool regular = f.nnz_max > 0 && (double)f.nnz_max <= 1.25 * f.nnz_avg + 1.0;
+  return f.n_deltas <= kD8Max && f.nnz_max <= kD8MaxRow && f.nnz > 0 && regular && s.vs == 1;
+}
+
 void validate_options(const spmv_options& o) {
   if (o.force_variant < 0 || o.force_variant > 5) fail(SPMV_E_ARG, "force_variant %d out of range", o.force_variant);
   if (o.force_vs != 0 && o.force_vs != 1 && o.force_vs != 2 && o.force_vs != 4 && o.force_vs != 8 &&
@@ -861,7 +869,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     if (opt.force_variant == 0) profile_select_impl(P->feat, P->props, opt, P->pb, P->sel);
   }
   if (P->sel.d16 == 1) P->d16_width = P->feat.maxgap <= 255 ? 8 : 16;
-  if (P->sel.d16 == 2) {
+  auto make_d8dict = [&]() {
     // D8 dictionary: the sorted distinct row-relative deltas of all shards
     P->d16_width = 8;
     std::vector<int32_t> d;
@@ -872,7 +880,8 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     d.erase(std::unique(d.begin(), d.end()), d.end());
     if ((int)d.size() > kD8Max) fail(SPMV_E_CUDA, "D8 dictionary overflow (%d entries)", (int)d.size());
     P->d8dict = d;
-  }
+  };
+  if (P->sel.d16 == 2) make_d8dict();
   // escape table: the sorted distinct large deltas of all shards
   if (P->sel.d16 == 1 && P->feat.maxgap > 65535) {
     std::vector<int32_t> big;
@@ -1393,6 +1402,49 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     s.x = s.alloc<double>((size_t)n_cols);
     s.y = s.alloc<double>((size_t)s.m);
     s.allpart = s.alloc<double>((size_t)2 * kIterRegions * kNormPartials * ngpus);
+  }
+  // profile-guided mode, second stage (reading 30): when Fig. 4
+  // mapped the matrix to the plain cta_stream kernel (CMP: the CSR baseline
+  // is latency-bound on a GPU, far from P_MB) and its indices are D8-codable,
+  // Fig. 4's MB test is applied to that CMP-optimised kernel: if it reaches
+  // (1 - tol) P_MB, the matrix is now bandwidth-bound and Table II's MB
+  // optimisation (index compression, D8) is applied jointly
+  if (opt.select_mode == 1 && opt.force_classes < 0 && opt.force_variant == 0 && opt.d16 != 0 &&
+      P->sel.variant == SPMV_VARIANT_STREAM && P->sel.d16 == 0 && profile_stage2_ok(P->feat, P->sel) &&
+      P->pb.p_mb > 0) {
+    Shard& s0 = P->shards[0];
+    ck(cudaSetDevice(s0.dev), "cudaSetDevice");
+    const double t_p = now_ms();
+    ck(cudaMemsetAsync(s0.x, 0, (size_t)s0.n_cols * 8, s0.stream), "memset");
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "cudaEventCreate");
+    ck(cudaEventCreate(&e1), "cudaEventCreate");
+    constexpr int kReps = 5;
+    for (int r = 0; r < 2; ++r) P->launch(s0, s0.x, s0.y);
+    ck(cudaEventRecord(e0, s0.stream), "event");
+    for (int r = 0; r < kReps; ++r) P->launch(s0, s0.x, s0.y);
+    ck(cudaEventRecord(e1, s0.stream), "event");
+    ck(cudaEventSynchronize(e1), "stage-2 probe");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, e0, e1), "event");
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    count_launches(2 + kReps, "stage-2 probe");
+    P->pb.p_stream = ms > 0 ? 2.0 * (double)s0.nnz / ((double)ms / kReps * 1e-3) : 0.0;
+    const double tol = opt.approx_tol > 0 ? opt.approx_tol : kTolB200;
+    if (P->pb.p_stream >= (1.0 - tol) * P->pb.p_mb) {
+      P->sel.classes |= SPMV_CLASS_MB;
+      P->sel.d16 = 2;
+      make_d8dict();
+      for (auto& s : P->shards) {  // rebuild the stream structures with D8 codes
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        ck(cudaStreamSynchronize(s.stream), "stage-2 rebuild");
+        s.sp[0] = StreamPlan{};
+        build_stream(s, s.sp[0], s.view(), nullptr, 2, 1, false, P->feat.nnz_max);
+      }
+    }
+    P->profile_ms += now_ms() - t_p;
+    P->select_ms += now_ms() - t_p;
   }
   for (auto& s : P->shards) {
     ck(cudaStreamSynchronize(s.stream), "structures");
@@ -2214,6 +2266,7 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     info->p_imb = p->pb.p_imb;
     info->p_cmp = p->pb.p_cmp;
     info->p_peak = p->pb.p_peak;
+    info->p_stream = p->pb.p_stream;
     info->bmax = p->pb.bmax;
     info->profile_vs = p->pb.vs;
     info->profile_ctas = p->pb.ctas;

@@ -311,6 +311,7 @@ void launch_chunk_export(const ExecArgs& a, int64_t* out, cudaStream_t s);  // [
 // ---- profile-guided selection (profile.cu; Sec. III-B bounds, Fig. 4) -----------
 struct ProfileBounds {
   double p_csr = 0, p_mb = 0, p_ml = 0, p_imb = 0, p_cmp = 0, p_peak = 0, bmax = 0;
+  double p_stream = 0;  // second stage: the plain cta_stream kernel's rate (reading 30; 0 = not run)
   int ws_fits_l2 = 0, vs = 0, ctas = 0;
 };
 int run_profile_probes(const MatView& A, int vs, int sm_count, int64_t l2_bytes, double* x, double* y,

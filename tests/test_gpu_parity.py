@@ -575,10 +575,10 @@ def test_profile_mode_selection(c, small):
     assert b["p_imb"] >= 0.95 * b["p_csr"]              # median <= max busy time (+ noise)
     assert 0 < info["profile_ms"] <= info["select_ms"]
     f = oracle.features(m.rowptr, m.colind)
-    o = oracle.profile_select(f, b, spmv.device_query(0)["access_window_max"])
+    o = oracle.profile_select(f, b, spmv.device_query(0)["access_window_max"], p_stream=info["p_stream"] or None)
     s = info["sel"]
-    assert (s["variant"], s["vs"], bool(s["d16"]), bool(s["xwin"]), s["classes"]) == \
-        (o.variant, o.vs, o.d16, o.xwin, o.classes), (b, s)
+    assert (s["variant"], s["vs"], s["d16"], bool(s["xwin"]), s["classes"]) == \
+        (o.variant, o.vs, o.d16, o.xwin, o.classes), (b, info["p_stream"], s)
     assert_bound(p.execute(m.x), m)
 
 
@@ -600,6 +600,31 @@ def test_profile_forced_classes_follow_table2(c):
         if mask in (0, 8, 4, 2):
             assert_bound(p.execute(m.x), m)
         p.destroy()
+
+
+@pytest.mark.parametrize("which", ["C2", "st27_96"])
+def test_profile_mode_second_stage_d8(which):
+    """Stencils (CMP on the CSR baseline, D8-codable): the second stage times
+    the plain stream kernel, which reaches P_MB, so MB and D8 are applied
+    (reading 30); the D8 plan's results are within the per-row bound.
+    (Tiny stencils such as C5's 20^3 test size are launch-bound: their CTA
+    spread calls them IMB, reading 29.)"""
+    m = sg.config(2) if which == "C2" else sg.stencil(96, 27, x_seed=5)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, select_mode=1)
+    info = p.info()
+    assert info["variant"] == "stream" and info["p_stream"] > 0
+    b = {k: info[k] for k in PROFILE_KEYS}
+    o = oracle.profile_select(oracle.features(m.rowptr, m.colind), b, spmv.device_query(0)["access_window_max"],
+                              p_stream=info["p_stream"])
+    assert (info["sel"]["d16"], info["sel"]["classes"]) == (o.d16, o.classes)
+    if info["p_stream"] >= 0.9 * info["p_mb"]:
+        assert info["sel"]["d16"] == 2 and "MB" in info["classes"] and info["d8_n_dict"] > 0
+    assert_bound(p.execute(m.x), m)
+    xg, _ = p.iterate(m.x, 3)
+    rc, xr, _ = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, 3)
+    assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
+    q = spmv.Plan(m.rowptr, m.colind, m.vals, select_mode=1, d16=0)  # d16 = 0: no second stage
+    assert q.info()["p_stream"] == 0.0 and q.info()["sel"]["d16"] == 0
 
 
 def test_profile_mode_paper_thresholds_option():

@@ -659,3 +659,20 @@ def test_profile_select_forced_classes_follow_table2():
     assert oracle.profile_select(f, None, 1 << 30, classes=oracle.CLASS_IMB | oracle.CLASS_ML).variant == oracle.VARIANT_NNZSPLIT
     for c in range(16):
         assert oracle.profile_select(f, None, 1 << 30, classes=c).classes == c
+
+
+def test_profile_select_second_stage():
+    """Reading 30: a CMP matrix mapped to the plain stream kernel gets MB and
+    D8 when that kernel reaches (1 - tol) P_MB and its indices are codable."""
+    f = dict(n=1000, nnz=7000, avg_short=7.0, n_long=0, nnz_max=7, nnz_avg=7.0, n_cols=1000, nnz_long=0,
+             maxgap=100, n_deltas=7)
+    b = dict(p_csr=1.0, p_mb=3.0, p_ml=1.0, p_imb=1.0, p_cmp=1.3, p_peak=4.0)  # P_MB > P_CMP: CMP
+    w = 1 << 27
+    base = oracle.profile_select(f, b, w)
+    assert (base.variant, base.d16, base.classes) == (oracle.VARIANT_STREAM, 0, oracle.CLASS_CMP)
+    s = oracle.profile_select(f, b, w, p_stream=2.7)  # 2.7 >= 0.9 * 3.0
+    assert (s.variant, s.d16, s.classes) == (oracle.VARIANT_STREAM, 2, oracle.CLASS_CMP | oracle.CLASS_MB)
+    assert oracle.profile_select(f, b, w, p_stream=2.69).d16 == 0          # below (1 - tol) P_MB
+    assert oracle.profile_select({**f, "n_deltas": 257}, b, w, p_stream=3.5).d16 == 0   # not codable
+    assert oracle.profile_select({**f, "nnz_max": 20}, b, w, p_stream=3.5).d16 == 0     # irregular rows
+    assert oracle.profile_select(f, b, w, p_stream=3.5, classes=oracle.CLASS_CMP).d16 == 0  # forced classes
