@@ -90,11 +90,14 @@ def exchange_x(dist, bounds, rank, world, x_full, halo=None, group=None):
     if world == 1:
         return
     if halo is not None:
+        # one coalesced batch (NCCL group): every rank sends and receives at
+        # once, so no send waits on a peer's later receive whatever the sizes
         sends, recvs = halo
-        ops = [dist.isend(x_full[lo:hi], dst=g, group=group) for g, lo, hi in sends]
-        ops += [dist.irecv(x_full[lo:hi], src=g, group=group) for g, lo, hi in recvs]
-        for w in ops:
-            w.wait()
+        ops = [dist.P2POp(dist.isend, x_full[lo:hi], g, group) for g, lo, hi in sends]
+        ops += [dist.P2POp(dist.irecv, x_full[lo:hi], g, group) for g, lo, hi in recvs]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
         return
     works = [dist.broadcast(x_full[int(bounds[g]):int(bounds[g + 1])], src=g, group=group, async_op=True)
              for g in range(world) if bounds[g + 1] > bounds[g]]
