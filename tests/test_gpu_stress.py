@@ -47,7 +47,8 @@ def test_random_matrices_all_variants(monkeypatch, seed, kind):
     s = oracle.absrow(m.rowptr, m.colind, m.vals, m.x)
     xd = torch.from_numpy(m.x).cuda()
     for v, extra in (("auto", {}), ("vector", {}), ("stream", {"seg": 0}), ("stream", {"seg": 1}), ("merge", {}),
-                     ("split", {"l_split": 256}), ("nnzsplit", {}), ("nnzsplit", {"hot_x": 512})):
+                     ("split", {"l_split": 256}), ("split", {"l_split": 256, "long_mode": 3}), ("nnzsplit", {}),
+                     ("nnzsplit", {"hot_x": 512})):
         kw = dict(extra)
         if v != "auto":
             kw["force_variant"] = v
@@ -59,4 +60,38 @@ def test_random_matrices_all_variants(monkeypatch, seed, kind):
             bad = np.nonzero(~(np.abs(y - yr) <= 1e-12 * s))[0]
             assert bad.size == 0, (v, extra, bad[:5])
             assert np.all(y[lens == 0] == 0.0), (v, extra)
+        p.destroy()
+
+
+@pytest.mark.parametrize("seed", range(_SEEDS))
+def test_random_banded_iteration_push(seed):
+    """Random banded symmetric-pattern matrices (variable row lengths inside a
+    band), 2-8 emulated shards: the iterated mode with the halo push (or the
+    copies when a block's halo is not a prefix / suffix) vs the oracle."""
+    g = np.random.default_rng(7000 + seed)
+    n = int(g.integers(3000, 9000))
+    bw = int(g.integers(5, 200))
+    G = int(g.integers(2, 9))
+    rows, cols = [], []
+    for i in range(n):
+        lo, hi = max(0, i - bw), min(n, i + bw + 1)
+        k = int(g.integers(1, min(12, hi - lo) + 1))
+        c = np.unique(np.concatenate([[i], g.choice(np.arange(lo, hi), k, replace=False)]))
+        rows.append(np.full(c.size, i))
+        cols.append(c)
+    lens = np.array([r.size for r in rows], np.int64)
+    cols = np.concatenate(cols).astype(np.int32)
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    vals = g.uniform(0.1, 1.0, cols.size)
+    x0 = g.uniform(-1, 1, n)
+    K = 25
+    rc, xr, nur = oracle.power_iter(rp.astype(np.int32), cols, vals, x0, K)
+    assert rc == 0
+    for d16 in (0, 2):
+        p = spmv.Plan(rp.astype(np.int32), cols, vals, ngpus=G, emulate_devices=1, force_variant="stream", d16=d16,
+                      seg=0)
+        xg, nug = p.iterate(x0, K)
+        assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr)), (seed, d16, p.info()["iter_push"])
+        assert np.all(np.abs(nug - nur) <= 1e-12 * nur), (seed, d16)
         p.destroy()

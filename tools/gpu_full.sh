@@ -1,3 +1,4 @@
+# Round-end style GPU check on the box: build, pytest -m gpu, smoke(), default bench (results under gpurun_out/)
 set -x
 make -j32 > gpurun_out/make.log 2>&1 || tail -20 gpurun_out/make.log
 ( time timeout 2400 python -m pytest tests -x -q -m gpu --durations=25 ) > gpurun_out/gputest.log 2>&1; echo "pytest rc=$?"
