@@ -1409,7 +1409,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
   // Fig. 4's MB test is applied to that CMP-optimised kernel: if it reaches
   // (1 - tol) P_MB, the matrix is now bandwidth-bound and Table II's MB
   // optimisation (index compression, D8) is applied jointly
-  if (opt.select_mode == 1 && opt.force_classes < 0 && opt.force_variant == 0 && opt.d16 != 0 &&
+  if (opt.select_mode == 1 && opt.force_classes < 0 && opt.force_variant == 0 && (opt.d16 < 0 || opt.d16 == 2) &&
       P->sel.variant == SPMV_VARIANT_STREAM && P->sel.d16 == 0 && profile_stage2_ok(P->feat, P->sel) &&
       P->pb.p_mb > 0) {
     Shard& s0 = P->shards[0];

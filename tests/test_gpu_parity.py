@@ -623,8 +623,9 @@ def test_profile_mode_second_stage_d8(which):
     xg, _ = p.iterate(m.x, 3)
     rc, xr, _ = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, 3)
     assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
-    q = spmv.Plan(m.rowptr, m.colind, m.vals, select_mode=1, d16=0)  # d16 = 0: no second stage
-    assert q.info()["p_stream"] == 0.0 and q.info()["sel"]["d16"] == 0
+    for d in (0, 1):  # d16 = 0 (off) or 1 (16-bit deltas asked for): no second stage
+        q = spmv.Plan(m.rowptr, m.colind, m.vals, select_mode=1, d16=d)
+        assert q.info()["p_stream"] == 0.0 and q.info()["sel"]["d16"] != 2
 
 
 def test_profile_mode_paper_thresholds_option():
