@@ -1,7 +1,9 @@
-"""Timeline of the multi-shard iterated mode (emulated shards on one GPU):
-interior-tile kernels, halo copies and boundary-tile kernels per stream, via
-torch.profiler (CUPTI) -- the overlap evidence of SURVEY 8(f) f2.
-  python tools/timeline_iter.py [--n 160] [--G 4] [--iters 3]"""
+"""Timeline of the multi-shard iterated mode (emulated shards on one GPU), via
+torch.profiler (CUPTI) -- SURVEY 8(f) f2: by default the halo push (one
+kernel per shard and iteration, storing its halo rows into the neighbours'
+replicas); with --no-push the interior-tile kernels, halo copies and
+boundary-tile kernels per stream.
+  python tools/timeline_iter.py [--n 160] [--G 4] [--iters 3] [--no-push]"""
 import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -14,7 +16,10 @@ ap.add_argument("--n", type=int, default=160)
 ap.add_argument("--G", type=int, default=4)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--out", default="")
+ap.add_argument("--no-push", action="store_true", help="halo copies + interior-first tiles instead of the halo push")
 a = ap.parse_args()
+if a.no_push:
+    os.environ["SPMV_NO_PUSH"] = "1"  # read when the plan first iterates
 m = sg.stencil(a.n, 27, x_seed=3)
 p = spmv.Plan(m.rowptr, m.colind, m.vals, ngpus=a.G, emulate_devices=1)
 p.iterate(m.x, 2)  # warm-up (plans the interior ranges)
