@@ -187,6 +187,7 @@ struct NzPlan {
   const void* skip_rp = nullptr;  // SPLIT: zero only the gap rows empty in this rowptr (long rows are written
                                   // concurrently by the long-row reduction)
   bool memset_y = false;  // a gap of more than kNzGapMax empty rows: y cleared before the pass, no gap zeroing
+  bool skip_wait = false; // launched with PDL behind the long-row kernel, which waited for the previous SpMV
 };
 constexpr int32_t kNzGapMax = 4096;  // longest empty-row run a warp zeroes in-kernel
 void launch_nz_tiles(const NzPlan& z, cudaStream_t s);  // tile_q and rowmap[mc] = m_out

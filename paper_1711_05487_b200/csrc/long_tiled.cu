@@ -53,6 +53,11 @@ void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long,
 #endif
 __global__ void __launch_bounds__(kNT, LONG_LB) long_tiled_kernel(const LongP p) {
   __shared__ double xs[kLongXB];
+  // PDL-launched (SPLIT concurrent mode): wait for the previous SpMV, THEN let
+  // the short-row bin launch -- it skips its own wait, since every CTA of
+  // this grid has seen the previous kernels complete (no-ops otherwise)
+  pdl_wait();
+  pdl_trigger();
   for (int64_t it = blockIdx.x; it < p.nblk * p.rg; it += gridDim.x) {
     long_item<kNT>(p, it, xs);
     __syncthreads();  // every warp is done with xs before the next item restages it
@@ -97,7 +102,9 @@ int long_tiled_grid(int64_t nblk, int sm_count, int per_sm) {
 
 void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s) {
   if (a.n_long == 0) return;
-  if (part == 1)
+  if (part == 3)  // programmatic launch (SPLIT concurrent mode)
+    launch_pdl(long_tiled_kernel, dim3(a.long_grid), dim3(kNT), 0, s, long_params(a));
+  else if (part == 1)
     long_tiled_kernel<<<a.long_grid, kNT, 0, s>>>(long_params(a));
   else
     long_reduce_kernel<<<(int)((a.n_long * 32 + kNT - 1) / kNT), kNT, 0, s>>>(a.long_partial, a.n_long, a.nblk,

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
   extern __shared__ __align__(16) double xh[];
   __shared__ __align__(16) uint32_t emask_s[MASK ? 1 : NW][8];
   pdl_trigger();
-  pdl_wait();
+  if (!p.skip_wait) pdl_wait();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* em = emask_s[MASK ? 0 : w];
   if constexpr (HOT) {
@@ -214,6 +214,7 @@ static NzP<RP> nz_params(const NzPlan& z, const double* x, double* y) {
   p.k0 = 0;
   p.n_hot = z.n_hot;
   p.zero_gaps = z.zero_gaps ? 1 : 0;
+  p.skip_wait = z.skip_wait ? 1 : 0;
   return p;
 }
 

@@ -60,6 +60,7 @@ struct NzP {
   int64_t k0;      // first tile of the range (pipelined host execute)
   int n_hot;
   int zero_gaps;
+  int skip_wait;  // 1: no griddepcontrol.wait (launched behind a kernel whose CTAs all waited, then triggered)
 };
 
 // warp tile k = nonzeros [k*256, (k+1)*256); xh: the hot-x smem table (HOT).

@@ -428,6 +428,29 @@ static int diag_skip() {  // diagnostics only (SPMV_DIAG_SKIP=1: no long rows, 2
 }
 
 int launch_split(const ExecArgs& a, cudaStream_t s) {
+  static const bool pdlconc = getenv("SPMV_SPLIT_PDLCONC") && atoi(getenv("SPMV_SPLIT_PDLCONC")) != 0;  // experiment
+  if (pdlconc && a.use_nz && a.long_tiled && !a.long_tma && a.n_long > 0 && a.nz.T > 0 && !a.nz.memset_y &&
+      a.nz.n_hot == 0 && diag_skip() == 0) {
+    // one stream, no fork: the long rows' persistent grid first (PDL; it
+    // waits for the previous SpMV, then triggers), the short-row bin behind
+    // it with PDL and no wait of its own, so both grids share the SMs; the
+    // bin's fix-up (PDL, waits for the bin), then the long-row reduction as
+    // a plain launch (waits for everything before it)
+    int n = 0;
+    if (a.stage != 2) {
+      launch_long_tiled(a, 3, s);
+      ++n;
+      NzPlan z = a.nz;
+      z.skip_wait = true;
+      n += launch_nz_plan(z, a.x, a.y, 1, s);
+    }
+    if (a.stage != 1) {
+      n += launch_nz_plan(a.nz, a.x, a.y, 2, s);
+      launch_long_tiled(a, 2, s);
+      ++n;
+    }
+    return n;
+  }
   if (a.split_fused && a.use_nz && a.long_tiled && a.n_long > 0 && a.nz.T > 0 && diag_skip() == 0)
     return launch_split_fused(a, s);
   int n = 0;
