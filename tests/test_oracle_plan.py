@@ -676,3 +676,32 @@ def test_profile_select_second_stage():
     assert oracle.profile_select({**f, "n_deltas": 257}, b, w, p_stream=3.5).d16 == 0   # not codable
     assert oracle.profile_select({**f, "nnz_max": 20}, b, w, p_stream=3.5).d16 == 0     # irregular rows
     assert oracle.profile_select(f, b, w, p_stream=3.5, classes=oracle.CLASS_CMP).d16 == 0  # forced classes
+
+
+def test_tune_profile_search_picks_the_widest_margin():
+    """tools/tune_profile.search on synthetic records: a stencil-like matrix
+    (IMB ratio 1.5: IMB would pick a 2x slower plan) and an R-MAT-like one
+    (ratio 6: IMB gains 4x) leave T_IMB optimal in [1.5, 6); the chosen point
+    sits at the geometric middle of that gap (widest log-margin), and T_ML /
+    tol, which no record's decision depends on, keep the paper's values."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "tools"))
+    import tune_profile as T
+
+    def rec(name, ratio_imb, gains):
+        b = dict(p_csr=1.0, p_mb=5.0, p_ml=0.97, p_imb=ratio_imb, p_cmp=1.3, p_peak=8.0)
+        us, poc = {}, {}
+        for c in range(16):
+            key = f"plan{c & T.IMB}"
+            poc[str(c)] = key
+            us[key] = 100.0 / gains.get(c & T.IMB, 1.0)
+        return dict(name=name, us=us, plan_of_classes=poc), b
+    r1, b1 = rec("stencil", 1.5, {0: 1.0, T.IMB: 0.5})
+    r2, b2 = rec("rmat", 6.0, {0: 1.0, T.IMB: 4.0})
+    res, chosen = T.search([r1, r2], [b1, b2])
+    lo, hi = res["optimal_region_bbox"]["t_imb"]
+    assert 1.5 <= lo <= 1.51 and 5.98 <= hi < 6.0
+    assert abs(chosen[0] - 3.0) <= 0.02            # sqrt(1.5 * 6) = 3: equal log-margins
+    assert (chosen[1], chosen[2]) == (T.PAPER[1], T.PAPER[2])
+    assert T.score([r1, r2], [b1, b2], chosen)[1] > T.score([r1, r2], [b1, b2], T.PAPER)[1]
