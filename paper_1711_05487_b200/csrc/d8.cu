@@ -167,7 +167,11 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
       if constexpr (SCALE) acc *= f;
       if (q < nrows) {
         SPMV_CHECK(R0 + q < p.m);
-        if constexpr (PU) iter_store(p.it, p.y, R0 + q, acc);  // + the neighbours' replicas
+        if constexpr (PU) {  // + the neighbours' replicas
+          SPMV_CHECK(!p.it.push_lo || p.it.push_lo_end <= p.m);
+          SPMV_CHECK(!p.it.push_hi || (p.it.push_hi_begin >= 0 && p.it.push_hi_begin <= p.m));
+          iter_store(p.it, p.y, R0 + q, acc);
+        }
         else p.y[R0 + q] = acc;
         sqa = fma(acc, acc, sqa);
       }

@@ -236,6 +236,10 @@ __global__ void __launch_bounds__(kLtNW * 32, LT_MINB) long_tma_kernel(const Lon
     const unsigned char* st = ring + (size_t)head * kLtStageB;
     const int32_t* cs = reinterpret_cast<const int32_t*>(st) + (m.e0 & 3);
     const double* vs = reinterpret_cast<const double*>(st + kLtColB) + (m.e0 & 1);
+    SPMV_CHECK(m.len > 0 && m.len <= kLtCH && m.q >= 0 && m.q < p.n_long && b < p.nblk);
+#ifdef SPMV_CHECKS
+    for (int i = lane; i < m.len; i += 32) SPMV_CHECK(cs[i] - c0 >= 0 && cs[i] - c0 < kLongXB);
+#endif
     int i = lane;
     for (; i + 32 < m.len; i += 64) {
       a0 = fma(vs[i], xs[cs[i] - c0], a0);

@@ -45,17 +45,23 @@ check("nnz_split hot-x", pl, force_variant="nnzsplit", hot_x=512)
 check("nnz_split long rows (fix-up)", huge, force_variant="nnzsplit")
 check("split fused (tiled long rows)", c4, force_variant="split")
 check("split chunks", c4, force_variant="split", long_mode=1)
+check("split TMA long rows (long_mode 3)", c4, force_variant="split", long_mode=3)
+check("profile mode + second stage (27-pt)", sg.stencil(48, 27, x_seed=4), select_mode=1)
 check("merge path", mixed, force_variant="merge")
 check("csr_vector VS=4", mixed, force_variant="vector", force_vs=4)
 # hierarchical fix-up: a row cut into > 2048 tiles
 big = sg.from_lengths(np.asarray([3, 300000, 2], np.int64), 300000, g)
 check("merge hierarchical fix-up", big, force_variant="merge")
 # iterated mode: fused epilogue (one shard) and emulated shards
-for G in (1, 2):
-    p = spmv.Plan(st.rowptr, st.colind, st.vals, ngpus=G, emulate_devices=1, force_variant="stream", d16=2)
-    x, nu = p.iterate(st.x, 5)
-    rc, xr, nur = oracle.power_iter(st.rowptr, st.colind, st.vals, st.x, 5)
+# (G > 1: the halo push -- each shard's kernel stores its halo rows into the
+# neighbours' replicas -- for both the D8 and the int32 stream kernels; the
+# 1e40-scaled values make the exact rescale (and its pushed copies) fire)
+for G, d16, scale in ((1, 2, 1.0), (2, 2, 1.0), (3, 2, 1e40), (3, 0, 1e40), (4, 0, 1.0)):
+    vals = st.vals * scale
+    p = spmv.Plan(st.rowptr, st.colind, vals, ngpus=G, emulate_devices=1, force_variant="stream", d16=d16)
+    x, nu = p.iterate(st.x, 8)
+    rc, xr, nur = oracle.power_iter(st.rowptr, st.colind, vals, st.x, 8)
     ok = bool(np.max(np.abs(x - xr)) <= 1e-10 * np.max(np.abs(xr)))
-    print(f"iterate D8 G={G:<34d} ok={ok}", flush=True)
+    print(f"iterate G={G} d16={d16} scale={scale:g} push={p.info()['iter_push']:<14d} ok={ok}", flush=True)
     assert ok
 print("sanitize suite done")
