@@ -168,7 +168,8 @@ typedef struct spmv_plan_info {
                                  stream), 3 column-tiled TMA-staged on the side stream (long_tma.cu) */
   int32_t long_rg;            /* long_mode 2/3: row groups per x block */
   int32_t iter_push;          /* 1: the multi-shard iterated mode pushes each shard's halo rows into its
-                                 neighbours' replicas from the SpMV kernel (banded row blocks; 0 = halo copies) */
+                                 neighbours' replicas from the SpMV kernel (banded row blocks; 0 = halo copies,
+                                 or no spmv_iterate yet: decided at the first one) */
   int32_t pad2_;
   double p_stream;            /* profile mode, second stage: flop/s of the plain cta_stream kernel when Fig. 4
                                  mapped the matrix to it and its indices are D8-codable; >= (1 - tol) P_MB adds
