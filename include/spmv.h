@@ -338,6 +338,11 @@ const char* spmv_last_error(void);
 /* Kernels launched by this library since load (all shards, all calls). */
 int64_t spmv_kernel_launches(void);
 
+/* ABI self-description (no GPU needed): out[0..5] = sizeof spmv_options, spmv_features,
+ * spmv_device_props, spmv_selection, spmv_plan_info, spmv_table1; returns the count written
+ * (min(n, 6)). Bindings compare their struct layouts against it. */
+int spmv_abi_sizes(int64_t* out, int n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2500,4 +2500,14 @@ spmv_status spmv_last_status(void) { return g_status; }
 const char* spmv_last_error(void) { return g_msg.c_str(); }
 int64_t spmv_kernel_launches(void) { return g_launches.load(); }
 
+int spmv_abi_sizes(int64_t* out, int n) {
+  const int64_t v[6] = {(int64_t)sizeof(spmv_options), (int64_t)sizeof(spmv_features),
+                        (int64_t)sizeof(spmv_device_props), (int64_t)sizeof(spmv_selection),
+                        (int64_t)sizeof(spmv_plan_info), (int64_t)sizeof(spmv_table1)};
+  if (!out || n <= 0) return 0;
+  const int m = n < 6 ? n : 6;
+  for (int i = 0; i < m; ++i) out[i] = v[i];
+  return m;
+}
+
 }  // extern "C"

@@ -141,3 +141,15 @@ def test_null_plan_arguments_fail_with_status_not_crash():
         rc = getattr(lib, name)(*args)
         assert rc == -1, name
         assert lib.spmv_last_error(), name
+
+
+def test_binding_struct_layouts_match_the_library():
+    """Every ctypes struct of the binding has the size of its C twin
+    (spmv_abi_sizes): a field added on one side only would make the library
+    write past the binding's buffer (spmv_plan_query) or read garbage."""
+    import paper_1711_05487_b200 as pkg
+    B = pkg.binding
+    out = (ctypes.c_int64 * 6)()
+    assert B.lib.spmv_abi_sizes(out, 6) == 6
+    mine = [ctypes.sizeof(c) for c in (B.Options, B.Features, B.DeviceProps, B.Selection, B.PlanInfo, B.Table1)]
+    assert list(out) == mine, (list(out), mine)
