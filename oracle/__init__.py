@@ -536,7 +536,7 @@ T_IMB, T_ML, APPROX_TOL = 1.24, 1.25, 0.10  # Fig. 4 caption; SPEC S
 # search maximising the average gain of the selected optimisation,
 # over a synthetic matrix set (tools/tune_profile.py -> profiles/
 # r02_profile_tuning.json; reading 29): the library's defaults.
-T_IMB_B200, T_ML_B200, APPROX_TOL_B200 = 2.71, 1.06, 0.10
+T_IMB_B200, T_ML_B200, APPROX_TOL_B200 = 2.54, 1.08, 0.10
 
 
 def classify_profile(p_csr, p_mb, p_ml, p_imb, p_cmp, p_peak, t_imb=T_IMB, t_ml=T_ML, tol=APPROX_TOL):

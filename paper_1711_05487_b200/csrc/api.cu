@@ -479,7 +479,7 @@ void select_impl(const spmv_features& f, const spmv_device_props& d, int rp_byte
 // are the classifier's hyperparameters, tuned per platform by grid search
 // (the paper's KNC values T_IMB = 1.24, T_ML = 1.25);
 // the defaults are this library's grid search on B200 (reading 29).
-constexpr double kTImbB200 = 2.71, kTMlB200 = 1.06, kTolB200 = 0.10;  // profiles/r02_profile_tuning.json
+constexpr double kTImbB200 = 2.54, kTMlB200 = 1.08, kTolB200 = 0.10;  // profiles/r02_profile_tuning.json
 int classify_profile(const ProfileBounds& b, const spmv_options& o) {
   const double t_imb = o.t_imb > 0 ? o.t_imb : kTImbB200;
   const double t_ml = o.t_ml > 0 ? o.t_ml : kTMlB200;

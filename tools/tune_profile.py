@@ -66,6 +66,21 @@ def matrices(quick):
         ("long_2M_8_20x500k", lambda: sg.randrows(2000000, 8, diag=False,
                                                  long_rows=sg.pick_rows(2000000, 20, S + 26), k_long=500000,
                                                  col_seed=S + 27, val_seed=S + 28, x_seed=S + 29)),
+        # round 2, second half: more matrices near the decision boundaries
+        ("st7_200", lambda: sg.stencil(200, 7)),
+        ("st27_160", lambda: sg.stencil(160, 27)),
+        ("rmat_21_16_a050", lambda: sg.rmat(21, 16, a=0.50, b=0.20, c=0.20, seed=S + 30, val_seed=S + 31,
+                                            x_seed=S + 32)),
+        ("rmat_22_8_a052", lambda: sg.rmat(22, 8, a=0.52, b=0.21, c=0.21, seed=S + 33, val_seed=S + 34,
+                                           x_seed=S + 35)),
+        ("long_2M_10_2000x4000", lambda: sg.randrows(2000000, 10, diag=False,
+                                                    long_rows=sg.pick_rows(2000000, 2000, S + 36), k_long=4000,
+                                                    col_seed=S + 37, val_seed=S + 38, x_seed=S + 39)),
+        ("long_4M_6_200x40000", lambda: sg.randrows(4000000, 6, diag=False,
+                                                   long_rows=sg.pick_rows(4000000, 200, S + 40), k_long=40000,
+                                                   col_seed=S + 41, val_seed=S + 42, x_seed=S + 43)),
+        ("rand_32M_3", lambda: sg.randrows(32 << 20, 3, col_seed=S + 44, val_seed=S + 45, x_seed=S + 46)),
+        ("rand_2M_32", lambda: sg.randrows(1 << 21, 32, col_seed=S + 47, val_seed=S + 48, x_seed=S + 49)),
     ]
     return out[::3] if quick else out
 
@@ -127,8 +142,9 @@ def search(recs, bnds, tie=0.005):
     parameter). Objective: the geometric-mean speedup over the baseline of the
     plans Fig. 4 selects; points within `tie` (relative) of the best count as
     optimal (plan times differ by ~1 % run to run, and a threshold fitted to
-    that noise is not a decision); the chosen point is the optimal point with
-    the widest margin to the decisions that matter (ties: nearest the median)."""
+    that noise is not a decision); the chosen point is the geometric centre of
+    the optimal region's bounding box when that point is optimal, else the
+    optimal point with the widest margins to the decisions that matter."""
     grid_imb = np.round(np.arange(1.0, 12.0001, 0.01), 2)
     grid_ml = np.round(np.arange(1.0, 4.0001, 0.01), 2)
     grid_tol = np.round(np.arange(0.05, 0.951, 0.05), 2)
@@ -149,11 +165,13 @@ def search(recs, bnds, tie=0.005):
     idx = np.argwhere(L >= best + np.log(1 - tie))
     P = np.array([(grid_imb[i], grid_ml[j], grid_tol[k]) for i, j, k in idx])
     # among the optimal points, the one farthest from every decision that
-    # matters: margin = min over (matrix, parameter) of |log(ratio / T)|,
-    # counting a matrix's boundary only where flipping that class bit
-    # changes its plan's time by more than the tie
-    def margin(t):
-        m = np.inf
+    # matters: the log-margins |log(ratio / T)| of each (matrix, parameter)
+    # whose class bit, flipped, changes the plan's time by more than the tie,
+    # sorted ascending and compared lexicographically (the smallest margin
+    # first, then the next: a parameter the smallest one does not involve is
+    # still centred in its own gap)
+    def margins(t):
+        ms = []
         for r, b in zip(recs, bnds):
             c = classify(b, *t)
             for bit, ratio, T in ((IMB, b["p_imb"] / b["p_csr"], t[0]), (ML, b["p_ml"] / b["p_csr"], t[1]),
@@ -163,13 +181,22 @@ def search(recs, bnds, tie=0.005):
                 t0 = r["us"][r["plan_of_classes"][str(c)]]
                 t1 = r["us"][r["plan_of_classes"][str(c ^ bit)]]
                 if abs(t1 / t0 - 1) > tie:
-                    m = min(m, abs(np.log(ratio / T)))
-        return m
-    mg = np.array([margin(tuple(t)) for t in P])
-    cand = P[mg >= mg.max() - 1e-9]
+                    ms.append(round(abs(float(np.log(ratio / T))), 6))
+        return tuple(sorted(ms))
+    keyed = [(margins(tuple(t)), i) for i, t in enumerate(P)]
+    best_m = max(k for k, _ in keyed)
+    mg = np.array([k[0] if k else np.inf for k, _ in keyed])
+    cand = P[[i for k, i in keyed if k == best_m]]
     med = np.median(cand, axis=0)
     scale = np.array([np.ptp(grid_imb), np.ptp(grid_ml), np.ptp(grid_tol)])
     chosen = [float(v) for v in cand[np.argmin((((cand - med) / scale) ** 2).sum(1))]]
+    # preferred: the geometric centre of the optimal box, when it is optimal
+    # itself (each threshold in the middle of its optimal interval)
+    centre = [float(np.round(np.sqrt(P[:, i].min() * P[:, i].max()) / st) * st)
+              for i, st in ((0, 0.01), (1, 0.01), (2, 0.05))]
+    opt_set = {tuple(np.round(t, 2)) for t in P}
+    if tuple(np.round(centre, 2)) in opt_set:
+        chosen = centre
     # a parameter every grid value of which is optimal is not informed by the
     # matrix set: keep the paper's value for it
     for i, g in enumerate((grid_imb, grid_ml, grid_tol)):
