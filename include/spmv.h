@@ -198,6 +198,13 @@ spmv_status spmv_plan_create_ex(spmv_plan* out, int64_t n_rows, int64_t n_cols, 
 /* NULL-safe; frees device memory and streams of every shard. */
 void spmv_plan_destroy(spmv_plan p);
 
+/* New values for the plan's matrix, same sparsity pattern (iterative solvers re-assemble values without
+ * re-planning): values[nnz] in the CSR order given at creation, host or device memory, not retained.
+ * Every value-derived copy the plan made (SPLIT bins, packed D8 tiles) is refreshed; the selection,
+ * partitions and index encodings depend on the pattern only and are kept. Synchronous: waits for the
+ * plan's earlier work. SPMV_E_ARG on a NULL plan or values. */
+spmv_status spmv_plan_update_values(spmv_plan p, const double* values);
+
 /* ---- execution ----------------------------------------------------------- */
 
 /* y = A x (overwrite, Fig. 2 read as accumulation).

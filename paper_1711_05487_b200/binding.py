@@ -106,6 +106,8 @@ lib.spmv_plan_create.restype = _vp
 lib.spmv_plan_create_ex.argtypes = [ctypes.POINTER(_vp), _i64, _i64, _i64, _vp, ctypes.c_int, _vp, _vp, ctypes.c_int,
                                     ctypes.POINTER(Options)]
 lib.spmv_plan_destroy.argtypes = [_vp]
+lib.spmv_plan_update_values.argtypes = [_vp, _vp]
+lib.spmv_abi_sizes.argtypes = [ctypes.POINTER(_i64), ctypes.c_int]
 lib.spmv_execute.argtypes = [_vp, _vp, _vp]
 lib.spmv_execute_async.argtypes = [_vp, _vp, _vp]
 lib.spmv_execute_stage.argtypes = [_vp, _vp, _vp, ctypes.c_int]
@@ -245,6 +247,12 @@ class Plan:
             self.destroy()
         except Exception:
             pass
+
+    def update_values(self, values):
+        """spmv_plan_update_values: same pattern, new values (CSR order, host or device)."""
+        if _numel(values) != self.nnz:
+            raise ValueError(f"values must have nnz = {self.nnz} entries")
+        _check(lib.spmv_plan_update_values(self._h, _ptr(values)))
 
     def execute(self, x, y=None):
         if y is None:

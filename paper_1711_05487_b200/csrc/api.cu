@@ -4,6 +4,7 @@
 // C++ exceptions are used internally and never cross the ABI: every entry
 // point catches and converts to a spmv_status + thread-local message.
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <chrono>
 #include <climits>
@@ -193,6 +194,9 @@ struct Shard {
   bool split_fused = true;
   bool long_tma = false;
   int long_rg = 0;
+  // values copied into other layouts at plan time (SPLIT bins, packed D8
+  // tiles): refreshed from val by spmv_plan_update_values
+  std::vector<std::function<void(cudaStream_t)>> val_refresh;
   // NNZSPLIT (whole shard) / SPLIT short+medium rows as one nnz_split bin
   NzPlan nz;
   bool use_nz = false;
@@ -979,6 +983,13 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
         ck(cudaMemcpyAsync(toff_dev, toff.data(), (size_t)(sp.T + 1) * 8, cudaMemcpyHostToDevice, s.stream), "toff");
         launch_d8_pack_tiles(sp, toff_dev, tiles, s.stream);
         count_launches(1, "d8 pack tiles");
+        {
+          StreamPlan spc = sp;
+          s.val_refresh.push_back([spc, toff_dev, tiles](cudaStream_t st) {
+            launch_d8_pack_tiles(spc, toff_dev, tiles, st);
+            count_launches(1, "d8 pack tiles");
+          });
+        }
         ck(cudaStreamSynchronize(s.stream), "d8 pack tiles");
         sp.d8_tiles = tiles;
         sp.d8_toff = toff_dev;
@@ -1270,6 +1281,10 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
     double* bval = s.alloc<double>((size_t)bnnz);
     launch_filtered_csr(A, lo, hi, frp, bcol, bval, scan, s.stream);
     count_launches(4, "bin csr");
+    s.val_refresh.push_back([A, lo, hi, frp, bval](cudaStream_t st) {
+      launch_filtered_vals(A, lo, hi, frp, bval, st);
+      count_launches(A.m ? 1 : 0, "bin values");
+    });
     void* brp = s.alloc<char>((size_t)(nrows + 1) * rp_bytes);
     launch_gather_rowptr(frp, rp_bytes, rows, nrows, s.m, brp, s.stream);
     count_launches(1, "bin gather");
@@ -2498,6 +2513,25 @@ spmv_status spmv_device_query(int dev, spmv_device_props* out) {
 
 spmv_status spmv_last_status(void) { return g_status; }
 const char* spmv_last_error(void) { return g_msg.c_str(); }
+spmv_status spmv_plan_update_values(spmv_plan p, const double* values) {
+  return guard([&] {
+    if (!p || (!values && p->nnz > 0)) fail(SPMV_E_ARG, "null argument");
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& s : p->shards) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaStreamSynchronize(s.stream), "update values");  // no SpMV of the plan still reads them
+      if (s.nnz) upload(s.val, values + s.nnz0, (size_t)s.nnz * 8, s.stream);
+      for (auto& f : s.val_refresh) f(s.stream);
+    }
+    for (auto& s : p->shards) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaStreamSynchronize(s.stream), "update values");
+    }
+    cudaSetDevice(cur);
+  });
+}
+
 int64_t spmv_kernel_launches(void) { return g_launches.load(); }
 
 int spmv_abi_sizes(int64_t* out, int n) {

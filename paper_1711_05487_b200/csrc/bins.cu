@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kNT) filt_copy_kernel(const RP* __restrict__ r
       if (l < lo || l > hi) continue;
       const int64_t d = rps[r];
       for (int64_t t = lane; t < l; t += 32) {
-        cols[d + t] = col[a + t];
+        if (cols) cols[d + t] = col[a + t];  // (null: a values refresh, spmv_plan_update_values)
         vals[d + t] = val[a + t];
       }
     }
@@ -206,6 +206,21 @@ static void filtered_csr_t(const MatView& A, int64_t lo, int64_t hi, void* out_r
     if (g > dev_sm_count() * 16) g = dev_sm_count() * 16;
     filt_copy_kernel<RP><<<(int)g, kNT, 0, s>>>(rp, A.col, A.val, A.m, lo, hi, (const RP*)out_rp, out_col, out_val);
   }
+}
+
+// values of the filtered sub-matrix again (its rowptr out_rp from
+// launch_filtered_csr): the bin's colind, possibly re-encoded since, is kept
+void launch_filtered_vals(const MatView& A, int64_t lo, int64_t hi, const void* out_rp, double* out_val,
+                          cudaStream_t s) {
+  if (A.m == 0) return;
+  int64_t g = (A.m + 32 * 8 - 1) / (32 * 8);
+  if (g > dev_sm_count() * 16) g = dev_sm_count() * 16;
+  if (A.rp_bytes == 8)
+    filt_copy_kernel<int64_t><<<(int)g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, A.val, A.m, lo, hi,
+                                                     (const int64_t*)out_rp, nullptr, out_val);
+  else
+    filt_copy_kernel<int32_t><<<(int)g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, A.val, A.m, lo, hi,
+                                                     (const int32_t*)out_rp, nullptr, out_val);
 }
 
 // rowptr (and, when out_col != null, colind/values) of the sub-matrix made of

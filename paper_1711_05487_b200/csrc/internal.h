@@ -239,6 +239,8 @@ int64_t scan_blocks(int64_t m);
 void launch_filtered_csr(const MatView& A, int64_t lo, int64_t hi, void* out_rp, int32_t* out_col, double* out_val,
                          int64_t* scratch, cudaStream_t s);
 // ordered list of the rows with lo <= len <= hi (count in scratch[scan_blocks(m)]; out may be null)
+void launch_filtered_vals(const MatView& A, int64_t lo, int64_t hi, const void* out_rp, double* out_val,
+                          cudaStream_t s);
 void launch_row_list(const MatView& A, int64_t lo, int64_t hi, int32_t* out, int64_t* scratch, cudaStream_t s);
 // compacted rowptr: out[q] = frp[rows[q]] (q < n), out[n] = frp[m]
 void launch_gather_rowptr(const void* frp, int rp_bytes, const int32_t* rows, int64_t n, int64_t m, void* out,

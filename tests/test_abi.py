@@ -136,6 +136,7 @@ def test_null_plan_arguments_fail_with_status_not_crash():
         "spmv_norm_step": (vp(None), buf, ctypes.c_int(4), buf, buf),
         "spmv_iter_step": (vp(None), buf, buf, buf, buf, buf),
         "spmv_unit": (vp(None), buf, ctypes.c_int64(4), buf, buf),
+        "spmv_plan_update_values": (vp(None), buf),
     }
     for name, args in calls.items():
         rc = getattr(lib, name)(*args)

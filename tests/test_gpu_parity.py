@@ -939,3 +939,43 @@ def test_d8_row_block_plan(rb, re):
     y = p.execute(full.x)
     m = sg.CSR(re - rb, blk.rowptr, blk.colind, blk.vals, full.x)
     assert_bound(y, m)
+
+
+UPDATE_CASES = [  # (config builder, plan options)
+    ("C2 D8", lambda: sg.config(2, small=True), dict()),
+    ("C2 D8 packed", lambda: sg.config(2, small=True), dict(force_variant="stream", d16=2)),
+    ("C3 nnz_split hot-x", lambda: sg.config(3, small=True), dict(force_variant="nnzsplit", hot_x=512)),
+    ("C4 split (bin)", lambda: sg.config(4, small=True), dict(force_variant="split")),
+    ("C4 split bins", lambda: sg.config(4, small=True), dict(force_variant="split", split_bins=0)),
+    ("C4 split TMA long rows", lambda: sg.config(4, small=True), dict(force_variant="split", long_mode=3)),
+    ("C3 merge", lambda: sg.config(3, small=True), dict(force_variant="merge")),
+    ("C3 vector", lambda: sg.config(3, small=True), dict(force_variant="vector")),
+    ("C5 3 shards", lambda: sg.config(5, small=True), dict(ngpus=3, emulate_devices=1)),
+]
+
+
+@pytest.mark.parametrize("name,mk,opts", UPDATE_CASES, ids=[c[0] for c in UPDATE_CASES])
+def test_plan_update_values(name, mk, opts, monkeypatch):
+    """spmv_plan_update_values: new values on the same pattern give the
+    oracle's result for the new values (every value-derived copy refreshed),
+    from host and from device memory; the iterated mode sees them too."""
+    if "packed" in name:
+        monkeypatch.setenv("SPMV_D8_PACKED", "1")
+    m = mk()
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, **opts)
+    g = np.random.default_rng(17)
+    for src in ("host", "device"):
+        v2 = g.uniform(-1, 1, m.vals.size)
+        if src == "host":
+            p.update_values(v2)
+        else:
+            p.update_values(torch.from_numpy(v2).cuda())
+        m2 = sg.CSR(m.n, m.rowptr, m.colind, v2, m.x)
+        assert_bound(p.execute(m.x), m2)
+    if m.n == m.x.size and "C5" in name:
+        v3 = np.abs(v2) + 0.1
+        p.update_values(v3)
+        xg, _ = p.iterate(m.x, 5)
+        rc, xr, _ = oracle.power_iter(m.rowptr, m.colind, v3, m.x, 5)
+        assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
+    p.destroy()
