@@ -335,10 +335,13 @@ def run_native(a):
     if not a.no_cold:
         flush = torch.ones(2 * 126 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
         sink = torch.empty((), dtype=torch.float32, device="cuda")
-        tot = 0.0
+        tot, ts = 0.0, []
         kc = max(3, min(a.steps, 10))
         for _ in range(kc):
             with torch.cuda.stream(stream):
+                # the GPU sleeps first, so the host has enqueued the SpMV
+                # before the flush ends: the events see device time only
+                torch.cuda._sleep(200_000)
                 torch.sum(flush, dim=0, out=sink)
             s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
@@ -346,12 +349,14 @@ def run_native(a):
             e0.record(stream)
             e0.synchronize()
             tot += s0.elapsed_time(e0)
+            ts.append(s0.elapsed_time(e0))
         ms_cold = max_over_ranks(tot / kc)
-        cold = {"ms_per_step": ms_cold, "gflops": 2.0 * blk["nnz"] / (ms_cold * 1e-3) / 1e9,
+        cold = {"ms_per_step": ms_cold, "ms_median": max_over_ranks(float(np.median(ts))),
+                "gflops": 2.0 * blk["nnz"] / (ms_cold * 1e-3) / 1e9,
                 "pct_of_8tbs": 100.0 * (algo_bytes(blk["N"], blk["N"], blk["nnz"], blk["rp_bytes"])
                                         + 8 * blk["N"] * (world - 1)) / (ms_cold * 1e-3) / 1e9 / (NOMINAL_HBM_GBS * world),
-                "how": "L2 flushed by reading a 252-MB buffer (clean lines) before each SpMV; CUDA events around the "
-                       "SpMV alone"}
+                "how": "L2 flushed by reading a 252-MB buffer (clean lines) before each SpMV, behind a ~0.1-ms "
+                       "device sleep (the SpMV is enqueued before the flush ends); CUDA events around the SpMV alone"}
         del flush
 
     # end to end through the public API: host (pinned) x in, host y out
