@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--split-bins", type=int, default=-1, help="SPLIT non-long rows: 0 cta_stream bins, 1 nnz_split")
     ap.add_argument("--xwin", type=int, default=-1, help="L2 persistence window on x: -1 auto, 0 off, 1 on")
     ap.add_argument("--no-halo", action="store_true", help="iterated mode: full all-gather of x instead of halos")
+    ap.add_argument("--no-push", action="store_true",
+                    help="iterated mode, N > 1: NCCL halo exchange instead of the halo push (peer stores in the SpMV)")
     ap.add_argument("--stages", type=int, default=0, help="STREAM smem ring depth (multiple of 4; 0 auto)")
     ap.add_argument("--hot", type=int, default=-1, help="NNZSPLIT hot-x table: -1 auto, 0 off, K columns")
     ap.add_argument("--no-aligned", action="store_true", help="nnz-aligned STREAM tiles (carries + fix-up)")
@@ -396,7 +398,7 @@ def run_native(a):
         steps = parallel.native_steps(plan)
         b = [int(v) for v in blk["bounds"]]
         dd = dist if world > 1 else parallel.NoDist
-        halo, recv_bytes = None, 0
+        halo, push, recv_bytes = None, None, 0
         if world > 1:  # halo exchange (f2): each rank receives only the x range its rows read
             feat = info["feat"]
             need = torch.tensor([feat["col_min"], feat["col_max"] + 1], dtype=torch.int64, device="cuda")
@@ -405,17 +407,31 @@ def run_native(a):
             needs = [v.tolist() for v in needs]
             halo = parallel.halo_plan(b, needs, rank) if not a.no_halo else None
             recv_bytes = parallel.halo_bytes(b, needs, rank) if halo else 8 * (blk["N"] - n_rows)
+            # halo push (the exchange fused into the SpMV kernel): banded row
+            # blocks, every rank's kernel push-capable (a collective decision)
+            layout = parallel.push_plan(b, needs, world) if halo else None
+            cap = torch.tensor([int(plan.push_capable() and layout is not None and not a.no_push)], device="cuda")
+            dist.all_reduce(cap, op=dist.ReduceOp.MIN)
+            if int(cap.item()):
+                ra, rb = plan.replicas()
+                xf, xa = parallel.device_view(ra, blk["N"], "cuda"), parallel.device_view(rb, blk["N"], "cuda")
+                xf.copy_(torch.from_numpy(blk["x"]))
+                push = parallel.open_push(dist, plan, layout, rank, world)
         with torch.cuda.stream(stream):
-            parallel.iterate(dd, steps, b, rank, world, xf, xa, pl, pa, nu, nn, 2, halo=halo)
+            parallel.iterate(dd, steps, b, rank, world, xf, xa, pl, pa, nu, nn, 2, halo=halo, push=push)
             ms_it = max_over_ranks(timed(lambda: parallel.iterate(dd, steps, b, rank, world, xf, xa, pl, pa, nu, nn,
-                                                                  a.iters, halo=halo), 1)) / a.iters
-            exch = lambda: parallel.exchange_only(dd, b, rank, world, xf, pl, pa, halo=halo)  # noqa: E731
+                                                                  a.iters, halo=halo, push=push), 1)) / a.iters
+            exch = lambda: parallel.exchange_only(dd, b, rank, world, xf, pl, pa,  # noqa: E731
+                                                  halo=None if push else halo, x_exchange=push is None)
             ms_ex = max_over_ranks(timed(exch, a.iters)) / a.iters
         iterated = {"iters_timed": a.iters, "ms_per_iter": ms_it, "spmv_ms": ms_step, "exchange_ms": ms_ex,
                     "gflops_per_iter": 2.0 * blk["nnz"] / (ms_it * 1e-3) / 1e9,
                     "exchange": ("none (1 GPU)" if world == 1 else
-                                 "NCCL all-gather(partials) + " + ("point-to-point halo of the x range each rank reads"
-                                                                   if halo else "per-rank broadcast of x blocks")),
+                                 "NCCL all-gather(partials) + " + (
+                                     "halo push (the SpMV kernel stores the rows each neighbour reads into its "
+                                     "replica: CUDA IPC, NVLink peer stores)" if push else
+                                     "point-to-point halo of the x range each rank reads" if halo else
+                                     "per-rank broadcast of x blocks")),
                     "x_recv_bytes_per_iter_rank0": recv_bytes}
 
     nnz = blk["nnz"]

@@ -269,6 +269,45 @@ int spmv_norm_step(spmv_plan p, const double* partials, int count, double* nn, d
 int spmv_execute_norm(spmv_plan p, const double* x, double* y, double* partials);
 int spmv_unit(spmv_plan p, const double* y, int64_t n, const double* nn, double* x_out);
 
+/* Halo push across processes: the
+ * one-process-per-GPU form of the exchange fused into the SpMV. For banded
+ * row blocks the rows a neighbour rank reads from this rank's block are a
+ * prefix (lower neighbour) and/or a suffix (upper neighbour) of it; the
+ * iterated kernel stores those rows straight into the neighbours' next x
+ * replicas (NVLink peer stores, CUDA IPC mappings) while it computes them,
+ * so no separate exchange runs. Single-shard plans only.
+ *   spmv_plan_replicas: the plan's two x replicas (n_cols doubles each,
+ *     plan-owned, freed by spmv_plan_destroy; the second is allocated on the
+ *     first call). The iterated mode ping-pongs between them; only these two
+ *     buffers can be exported.
+ *   spmv_iter_push_capable: 1 when the plan's iterated kernel (row-aligned
+ *     STREAM / D8) has the halo-push instantiation, else 0 (NULL plan: 0).
+ *   spmv_ipc_export: writes the SPMV_IPC_HANDLE_BYTES-byte CUDA IPC handle
+ *     of `replica` (one of the two pointers above; else SPMV_E_ARG) to
+ *     `handle` (host memory). The handle is sent to the peers by the caller.
+ *   spmv_ipc_open: maps a peer's exported replica into this process on the
+ *     plan's device (*ptr: its base, device memory of the peer's GPU;
+ *     another process only: CUDA refuses a handle of the same process,
+ *     SPMV_E_CUDA); unmapped by spmv_plan_destroy.
+ *   spmv_iter_step_push: spmv_iter_step (no norm step) whose kernel also
+ *     stores local rows [0, push_lo_end) into push_lo[r] and rows
+ *     [push_hi_begin, m) into push_hi[r] (r = local row; the caller passes
+ *     the peer replica's base + this block's first row). NULL push_lo /
+ *     push_hi: no store on that side. SPMV_E_ARG when a range leaves
+ *     [0, m]; SPMV_E_UNSUPPORTED when the plan is not push-capable.
+ *     Ordering is the caller's: a peer's replica may be written only after
+ *     the peer's previous SpMV finished reading it and read only after this
+ *     launch completed (parallel.iterate: the per-iteration all-gather of the
+ *     norm partials orders both). The kernel fences its peer stores at
+ *     system scope before it completes. */
+#define SPMV_IPC_HANDLE_BYTES 64
+int spmv_plan_replicas(spmv_plan p, double** x_a, double** x_b);
+int spmv_iter_push_capable(spmv_plan p);
+int spmv_ipc_export(spmv_plan p, const double* replica, void* handle);
+int spmv_ipc_open(spmv_plan p, const void* handle, double** ptr);
+int spmv_iter_step_push(spmv_plan p, const double* x, double* y, double* partials, double* nn, double* push_lo,
+                        int64_t push_lo_end, double* push_hi, int64_t push_hi_begin);
+
 /* ---- inspection ---------------------------------------------------------- */
 
 spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info);

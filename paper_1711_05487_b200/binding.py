@@ -121,6 +121,12 @@ if hasattr(lib, "spmv_iter_step"):  # (experiment builds of older sources lack i
 lib.spmv_execute_norm.argtypes = [_vp, _vp, _vp, _vp]
 lib.spmv_unit.argtypes = [_vp, _vp, ctypes.c_int64, _vp, _vp]
 lib.spmv_plan_query.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
+IPC_HANDLE_BYTES = 64  # SPMV_IPC_HANDLE_BYTES
+lib.spmv_plan_replicas.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+lib.spmv_iter_push_capable.argtypes = [_vp]
+lib.spmv_ipc_export.argtypes = [_vp, _vp, _vp]
+lib.spmv_ipc_open.argtypes = [_vp, _vp, ctypes.POINTER(_vp)]
+lib.spmv_iter_step_push.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64]
 
 
 class Table1(ctypes.Structure):
@@ -290,6 +296,32 @@ class Plan:
 
     def iter_step(self, x, y, partials, nn, nu_k=None):
         _check(lib.spmv_iter_step(self._h, _ptr(x), _ptr(y), _ptr(partials), _ptr(nn), _ptr(nu_k)))
+
+    def iter_step_push(self, x, y, partials, nn, push_lo, push_lo_end, push_hi, push_hi_begin):
+        _check(lib.spmv_iter_step_push(self._h, _ptr(x), _ptr(y), _ptr(partials), _ptr(nn), _ptr(push_lo),
+                                       int(push_lo_end), _ptr(push_hi), int(push_hi_begin)))
+
+    def replicas(self):
+        """spmv_plan_replicas: device pointers (ints) of the plan's two x replicas."""
+        a, b = _vp(), _vp()
+        _check(lib.spmv_plan_replicas(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def push_capable(self) -> bool:
+        return bool(lib.spmv_iter_push_capable(self._h))
+
+    def ipc_export(self, replica) -> bytes:
+        h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(lib.spmv_ipc_export(self._h, _ptr(replica), h))
+        return h.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        if len(handle) != IPC_HANDLE_BYTES:
+            raise ValueError("IPC handle must be %d bytes" % IPC_HANDLE_BYTES)
+        d = _vp()
+        _check(lib.spmv_ipc_open(self._h, ctypes.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES),
+                                 ctypes.byref(d)))
+        return d.value
 
     def unit(self, y, nn, x_out):
         _check(lib.spmv_unit(self._h, _ptr(y), int(_numel(y)), _ptr(nn), _ptr(x_out)))

@@ -216,6 +216,7 @@ struct Shard {
   cudaStream_t cp = nullptr;     // halo copy stream
   cudaEvent_t ev_cp = nullptr;   // halo copies of the current iteration done
   double* x2 = nullptr;       // second x replica (deferred-normalisation ping-pong)
+  std::vector<void*> ipc_open;  // peers' replicas mapped by spmv_ipc_open (closed on release)
   double* cta_part = nullptr; // per-CTA sums of y^2 (fused iteration epilogue, row-aligned STREAM / D8)
   unsigned int* done = nullptr;  // its last-CTA ticket counter
   double* cta2 = nullptr;        // [2][grid] per-CTA sums of the prologue-norm iteration (parity double-buffered)
@@ -261,6 +262,8 @@ struct Shard {
   void release() {
     cudaSetDevice(dev);
     if (stream) cudaStreamSynchronize(stream);
+    for (void* p : ipc_open) cudaIpcCloseMemHandle(p);
+    ipc_open.clear();
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
     if (ev_part) cudaEventDestroy(ev_part);
@@ -2060,6 +2063,77 @@ int spmv_iter_step(spmv_plan p, const double* x, double* y, double* partials, do
     require_dev(s, nn, "nn");
     if (nu_k) require_dev(s, nu_k, "nu_k");
     count_launches(spmv_iter(p, s, x, y, partials, nn, nu_k), "iteration step");
+  });
+}
+
+// ---- halo push across processes (one process per GPU; include/spmv.h) ----
+
+int spmv_plan_replicas(spmv_plan p, double** x_a, double** x_b) {
+  return guard([&] {
+    if (!p || !x_a || !x_b || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    if (!s.x2) s.x2 = s.alloc<double>((size_t)p->n_cols);
+    *x_a = s.x;
+    *x_b = s.x2;
+  });
+}
+
+int spmv_iter_push_capable(spmv_plan p) {
+  if (!p || p->shards.size() != 1) return 0;
+  const StreamPlan& sp = p->shards[0].sp[0];
+  return (p->sel.variant == SPMV_VARIANT_STREAM && sp.aligned && !sp.seg && !sp.rowmap && !sp.need_fixup &&
+          stream_push_capable(sp) && !getenv("SPMV_NO_FUSED_NORM"))
+             ? 1
+             : 0;
+}
+
+int spmv_ipc_export(spmv_plan p, const double* replica, void* handle) {
+  return guard([&] {
+    if (!p || !replica || !handle || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    if (replica != s.x && replica != s.x2) fail(SPMV_E_ARG, "not a replica of this plan (spmv_plan_replicas)");
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, const_cast<double*>(replica)), "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == SPMV_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle, &h, sizeof h);
+  });
+}
+
+int spmv_ipc_open(spmv_plan p, const void* handle, double** ptr) {
+  return guard([&] {
+    if (!p || !handle || !ptr || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    void* d = nullptr;
+    ck(cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    s.ipc_open.push_back(d);
+    *ptr = static_cast<double*>(d);
+  });
+}
+
+int spmv_iter_step_push(spmv_plan p, const double* x, double* y, double* partials, double* nn, double* push_lo,
+                        int64_t push_lo_end, double* push_hi, int64_t push_hi_begin) {
+  return guard([&] {
+    if (!p || !x || !y || !partials || !nn || p->shards.size() != 1) fail(SPMV_E_ARG, "bad argument");
+    Shard& s = p->shards[0];
+    if (push_lo_end < 0 || push_lo_end > s.m || push_hi_begin < 0 || push_hi_begin > s.m ||
+        (push_lo && push_lo_end == 0) || (push_hi && push_hi_begin == s.m))
+      fail(SPMV_E_ARG, "push row ranges outside the block");
+    if (!spmv_iter_push_capable(p)) fail(SPMV_E_UNSUPPORTED, "the plan's kernel has no halo-push instantiation");
+    require_dev(s, x, "x");
+    require_dev(s, y, "y");
+    require_dev(s, partials, "partials");
+    require_dev(s, nn, "nn");
+    IterOut po;
+    po.push_lo = push_lo;
+    po.push_lo_end = push_lo ? push_lo_end : 0;
+    po.push_hi = push_hi;
+    po.push_hi_begin = push_hi ? push_hi_begin : s.m;
+    count_launches(spmv_iter(p, s, x, y, partials, nn, nullptr, &po), "iteration step (push)");
   });
 }
 

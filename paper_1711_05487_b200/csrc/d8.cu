@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
   else
     wsq = f == 1.0 ? d8_consume<CW, false, UN, CB, PK, false>(p, smem, L, full, empty, meta, dict_s, 1.0)
                    : d8_consume<CW, true, UN, CB, PK, false>(p, smem, L, full, empty, meta, dict_s, f);
+  if constexpr (PU) __threadfence_system();  // the peer stores, before the partials / kernel end
   iter_epilogue<32 * CW>(p.it, wsq);
 }
 

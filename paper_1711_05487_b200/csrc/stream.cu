@@ -600,6 +600,7 @@ __global__ void __launch_bounds__(32 * (CW + 1),
         wsq *= f * f;  // exact: f is a power of two
       }
     }
+    if constexpr (PUSH) __threadfence_system();  // the peer stores, before the partials / kernel end
     iter_epilogue<32 * CW>(p.it, wsq);
   }
 }

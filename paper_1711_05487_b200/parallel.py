@@ -13,7 +13,13 @@ P:708-711, computed by ``spmv_shard_bounds``) and a full replica of x.
     2. all-gather of the partials (rank order)        -- NCCL
     3. norm step on every rank (identical): nu_k = ||yh_k|| / ||yh_{k-1}||,
        a pending rescale factor when the magnitude drifts (never in place)
-    4. the exchange of `nxt` blocks                   -- NCCL
+    4. the exchange of `nxt` blocks                   -- NCCL, or none:
+       * halo push (the exchange fused into step 1): for
+         banded row blocks the kernel of step 1 also stores the rows each
+         neighbour reads straight into that neighbour's `nxt` replica (CUDA
+         IPC mapping, NVLink peer stores); the all-gather of step 2 is what
+         orders those stores with the neighbour's reads and its previous
+         reads of that replica (push_plan, open_push)
        * all-gather(v): one broadcast per rank into its slice of every
          replica (blocks differ in size), or
        * halo exchange: rank g's rows only read x columns
@@ -49,6 +55,11 @@ class ShardSteps:
     # optional whole single-rank run (x_full, iters, nu_hist): the library's own
     # loop (spmv_iterate), which needs nothing between two SpMVs
     iterate_all: Optional[Callable[[object, int, object], None]] = None
+    # optional halo-push form of iter_step (x_full, y_block, partials_local, nn,
+    # push_lo, push_lo_end, push_hi, push_hi_begin): also stores local rows
+    # [0, push_lo_end) at push_lo and [push_hi_begin, m) at push_hi (device
+    # pointers of the neighbours' replicas + this block's first row, or None)
+    iter_step_push: Optional[Callable[..., None]] = None
     # optional context-manager factory making the steps' stream the current
     # one, so the collectives (issued on the current stream) are ordered with
     # the native steps (issued on the plan's stream)
@@ -84,6 +95,58 @@ def halo_bytes(bounds: Sequence[int], needs: Sequence[Sequence[int]], rank: int)
     return 8 * sum(hi - lo for _, lo, hi in halo_plan(bounds, needs, rank)[1])
 
 
+def push_plan(bounds: Sequence[int], needs: Sequence[Sequence[int]], world: int):
+    """Halo-push layout of every rank (pure function; the rule
+    of the in-process shards, api.cu prepare_push).
+
+    None unless, for every rank g, the rows the other ranks read from g's
+    block form a prefix read by one lower rank and/or a suffix read by one
+    upper rank (banded row blocks). Else, per rank g, (lo_peer, lo_end,
+    hi_peer, hi_begin): g's kernel stores its local rows [0, lo_end) into rank
+    lo_peer's replica and [hi_begin, m_g) into hi_peer's (-1, 0 and -1, m_g
+    when there is no such peer) -- the same rows halo_plan sends."""
+    out = []
+    for g in range(world):
+        b0, b1 = int(bounds[g]), int(bounds[g + 1])
+        lo_peer, lo_end, hi_peer, hi_begin = -1, 0, -1, b1 - b0
+        for h in range(world):
+            if h == g:
+                continue
+            lo, hi = int(needs[h][0]), int(needs[h][1])
+            a, b = max(lo, b0), min(hi, b1)  # h reads x[a:b) of g's block
+            if a >= b:
+                continue
+            if h < g:
+                if lo_peer >= 0 or a != b0:
+                    return None
+                lo_peer, lo_end = h, b - b0
+            else:
+                if hi_peer >= 0 or b != b1:
+                    return None
+                hi_peer, hi_begin = h, a - b0
+        out.append((lo_peer, lo_end, hi_peer, hi_begin))
+    return out
+
+
+def open_push(dist, plan, layout, rank: int, world: int, group=None):
+    """Collective (every rank calls it): exchange the CUDA IPC handles of the
+    plan replicas (spmv_plan_replicas / spmv_ipc_export) and map this rank's
+    push peers' (spmv_ipc_open). Returns this rank's `push` argument of
+    iterate: ((lo_A, lo_B) or None, lo_end, (hi_A, hi_B) or None, hi_begin),
+    the peers' replica base pointers in replica order. iterate() must then run
+    on the plan replicas (x_full = replica A, x_alt = replica B) on every
+    rank."""
+    a, b = plan.replicas()
+    handles = [None] * world
+    dist.all_gather_object(handles, plan.ipc_export(a) + plan.ipc_export(b), group=group)
+    lo_peer, lo_end, hi_peer, hi_begin = layout[rank]
+    n = len(handles[rank]) // 2
+
+    def peer(h):
+        return (plan.ipc_open(handles[h][:n]), plan.ipc_open(handles[h][n:])) if h >= 0 else None
+    return peer(lo_peer), lo_end, peer(hi_peer), hi_begin
+
+
 def exchange_x(dist, bounds, rank, world, x_full, halo=None, group=None):
     """One x exchange: the halo plan (sends, recvs) when given, else the
     all-gather(v) of the blocks."""
@@ -106,15 +169,17 @@ def exchange_x(dist, bounds, rank, world, x_full, halo=None, group=None):
 
 
 def iterate(dist, steps: ShardSteps, bounds: Sequence[int], rank: int, world: int, x_full, x_alt,
-            partials_local, partials_all, nu_hist, nn, iters: int, group=None, halo=None):
+            partials_local, partials_all, nu_hist, nn, iters: int, group=None, halo=None, push=None):
     """Run `iters` power iterations (deferred normalisation) on x_full.
 
     x_alt: a second replica (len n); partials_all: tensor of world * P;
     nu_hist: tensor of >= iters (nu_k); nn: 2 doubles of state (zeroed here);
     halo: this rank's halo_plan(...) to exchange only the x ranges the ranks
-    read (else the full all-gather). On return x_full holds x_iters on every
-    rank (with a halo plan: at least the range this rank reads and its own
-    block); x_alt is scratch.
+    read (else the full all-gather); push: this rank's open_push(...) result
+    (every rank passes one, or none does): the halo rows are stored by the
+    SpMV kernels into the neighbours' replicas and no exchange runs. On return
+    x_full holds x_iters on every rank (with a halo plan or push: at least the
+    range this rank reads and its own block); x_alt is scratch.
     """
     P = partials_local.numel()
     b0, b1 = int(bounds[rank]), int(bounds[rank + 1])
@@ -124,9 +189,25 @@ def iterate(dist, steps: ShardSteps, bounds: Sequence[int], rank: int, world: in
     with steps.stream() if steps.stream is not None else nullcontext():
         nn.zero_()
         cur, nxt = x_full, x_alt
+        if push is not None and world > 1:
+            # the first pushes write the peers' x_alt: wait until every peer
+            # is done with it (its unit() of a previous call reads it)
+            dist.all_gather_into_tensor(partials_all, partials_local, group=group)
         for k in range(iters):
             if world == 1:  # the rank's partials are all of them: norm step fused into the step
                 steps.iter_step(cur, nxt[b0:b1], partials_local, nn, nu_hist[k:k + 1])
+            elif push is not None:
+                # nxt is replica (k + 1) % 2 on every rank; the kernel stores the
+                # neighbours' halo rows into their replica of that parity
+                lo, lo_end, hi, hi_begin = push
+                par = (k + 1) & 1
+                steps.iter_step_push(cur, nxt[b0:b1], partials_local, nn,
+                                     lo[par] + 8 * b0 if lo else None, lo_end,
+                                     hi[par] + 8 * b0 if hi else None, hi_begin)
+                # orders every peer's pushes into nxt before the next SpMV here
+                # reads it, and this rank's reads of cur before peers write it
+                dist.all_gather_into_tensor(partials_all, partials_local, group=group)
+                steps.norm_step(partials_all, world * P, nn, nu_hist[k:k + 1])
             else:
                 steps.iter_step(cur, nxt[b0:b1], partials_local, nn, None)
                 dist.all_gather_into_tensor(partials_all, partials_local, group=group)
@@ -137,10 +218,12 @@ def iterate(dist, steps: ShardSteps, bounds: Sequence[int], rank: int, world: in
 
 
 def exchange_only(dist, bounds: Sequence[int], rank: int, world: int, x_full, partials_local, partials_all,
-                  group=None, halo=None):
-    """The two collectives of one iteration alone (for the exchange-time report)."""
+                  group=None, halo=None, x_exchange=True):
+    """The collectives of one iteration alone (for the exchange-time report;
+    x_exchange=False: the halo push, whose x transfer runs inside the SpMV)."""
     dist.all_gather_into_tensor(partials_all, partials_local, group=group)
-    exchange_x(dist, bounds, rank, world, x_full, halo, group)
+    if x_exchange:
+        exchange_x(dist, bounds, rank, world, x_full, halo, group)
 
 
 class NoDist:
@@ -171,6 +254,18 @@ def native_steps(plan) -> ShardSteps:
         stream=stream,
         iterate_all=iterate_all,
         iter_step=lambda x, y, p, nn, nu: plan.iter_step(x, y, p, nn, nu),
+        iter_step_push=lambda x, y, p, nn, lo, le, hi, hb: plan.iter_step_push(x, y, p, nn, lo, le, hi, hb),
         norm_step=lambda pa, cnt, nn, nu: plan.norm_step(pa, cnt, nn, nu),
         unit=lambda y, nn, x: plan.unit(y, nn, x),
     )
+
+
+def device_view(ptr: int, n: int, device):
+    """A float64 torch tensor over n doubles at device pointer ptr (no copy;
+    the memory stays owned by whoever allocated it, e.g. the plan's replicas)."""
+    import torch
+
+    class _View:
+        __cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_View(), device=device)
