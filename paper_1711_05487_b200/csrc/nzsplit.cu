@@ -49,13 +49,39 @@ constexpr int kNzWarps = 8;  // warps per CTA (plain mode)
 #define NZ_MASK 1
 #endif
 constexpr int kNzHotWarps = NZ_HOT_WARPS;  // warps per CTA (hot-x mode: one CTA per SM)
-constexpr bool kNzHotPrefetch = NZ_HOT_PF;
+constexpr int kNzHotPrefetch = NZ_HOT_PF;  // 1: next tile's streams, 2: next tile's colind only
 // row ends from the per-tile mask (see nz_tile_compute); B200: C4 134 -> 127 us,
 // C5 as nnz_split 4.47 -> 3.91 ms, C3 hot-x 282 -> 290 us (kept on tile_q + rpc)
 constexpr bool kNzHotMask = NZ_HOT_MASK;
 constexpr bool kNzMask = NZ_MASK;
 
 size_t nz_smem_bytes(int n_hot) { return n_hot > 0 ? (size_t)n_hot * 8 + 16 : 0; }
+
+template <typename RP>
+__device__ __forceinline__ void nz_col_load(const NzP<RP>& p, int64_t k, int lane, int (&c)[8]) {
+  const int64_t t0 = k * kNzTile;
+  const int cnt = (int)((p.nnz - t0) < kNzTile ? (p.nnz - t0) : kNzTile);
+  const int e0 = lane * 8;
+  if (e0 + 8 <= cnt) {
+    ld256_s32(p.col + t0 + e0, c);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = e0 + i < cnt ? ld_stream(p.col + t0 + e0 + i) : 0;
+  }
+}
+template <typename RP>
+__device__ __forceinline__ void nz_val_load(const NzP<RP>& p, int64_t k, int lane, double (&v)[8]) {
+  const int64_t t0 = k * kNzTile;
+  const int cnt = (int)((p.nnz - t0) < kNzTile ? (p.nnz - t0) : kNzTile);
+  const int e0 = lane * 8;
+  if (e0 + 8 <= cnt) {
+    ld256_f64(p.val + t0 + e0, v);
+    ld256_f64(p.val + t0 + e0 + 4, v + 4);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = e0 + i < cnt ? ld_stream(p.val + t0 + e0 + i) : 0.0;
+  }
+}
 
 // HOT: the plan re-encoded colind of the n_hot most frequent columns as
 // ~slot (negative); their x values are bulk-copied into shared memory once
@@ -89,7 +115,22 @@ __global__ void __launch_bounds__(HOT ? 32 * kNzHotWarps : 32 * kNzWarps, HOT ? 
   // which B200 DRAM rewards (C3: 294 us; chunks of 8 consecutive tiles per
   // warp 358 us; dynamic tickets 350 us -- same-address atomics serialise)
   const int64_t nw = (int64_t)gridDim.x * NW;
-  if constexpr (HOT && kNzHotPrefetch) {
+  if constexpr (HOT && kNzHotPrefetch == 2) {
+    // the next tile's colind is loaded with this tile's values and gathers:
+    // one round trip per tile instead of colind, then gathers
+    int64_t k = p.k0 + (int64_t)blockIdx.x * NW + w;
+    int c[8], cn[8];
+    if (k < p.T) nz_col_load(p, k, lane, c);
+    for (; k < p.T; k += nw) {
+      double v[8];
+      nz_val_load(p, k, lane, v);
+      if (k + nw < p.T) nz_col_load(p, k + nw, lane, cn);
+      NzMeta m{};
+      nz_tile_compute<RP, HOT, MASK, L2G>(p, k, lane, xh, em, c, v, m);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c[i] = cn[i];
+    }
+  } else if constexpr (HOT && kNzHotPrefetch == 1) {
     // the next tile's streams are loaded while this tile gathers x
     int64_t k = p.k0 + (int64_t)blockIdx.x * NW + w;
     int c[8], cn[8];
