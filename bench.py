@@ -416,7 +416,15 @@ def run_native(a):
                 ra, rb = plan.replicas()
                 xf, xa = parallel.device_view(ra, blk["N"], "cuda"), parallel.device_view(rb, blk["N"], "cuda")
                 xf.copy_(torch.from_numpy(blk["x"]))
-                push = parallel.open_push(dist, plan, layout, rank, world)
+                try:  # (mapping a peer's replica needs peer access between the GPUs)
+                    push = parallel.open_push(dist, plan, layout, rank, world)
+                except Exception as e:  # noqa: BLE001
+                    print(f"rank {rank}: halo push unavailable ({e}); NCCL halo exchange", file=sys.stderr)
+                    push = None
+                ok = torch.tensor([int(push is not None)], device="cuda")
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank pushes, or none does
+                if not int(ok.item()):
+                    push = None
         with torch.cuda.stream(stream):
             parallel.iterate(dd, steps, b, rank, world, xf, xa, pl, pa, nu, nn, 2, halo=halo, push=push)
             ms_it = max_over_ranks(timed(lambda: parallel.iterate(dd, steps, b, rank, world, xf, xa, pl, pa, nu, nn,
