@@ -170,7 +170,8 @@ typedef struct spmv_plan_info {
   int32_t iter_push;          /* 1: the multi-shard iterated mode pushes each shard's halo rows into its
                                  neighbours' replicas from the SpMV kernel (banded row blocks; 0 = halo copies,
                                  or no spmv_iterate yet: decided at the first one) */
-  int32_t pad2_;
+  int32_t long_c16;           /* 1: SPLIT's column-tiled long rows read 16-bit in-block columns (colind mod the
+                                 2048-column x block) instead of int32 colind: 10 instead of 12 B per nonzero */
   double p_stream;            /* profile mode, second stage: flop/s of the plain cta_stream kernel when Fig. 4
                                  mapped the matrix to it and its indices are D8-codable; >= (1 - tol) P_MB adds
                                  MB and D8 (reading 30); 0 when not run */

@@ -96,7 +96,7 @@ class PlanInfo(ctypes.Structure):
                ("x_reuse", ctypes.c_double), ("nz_gather_l2", ctypes.c_int32), ("stream_stages", ctypes.c_int32),
                ("d8_n_dict", ctypes.c_int32), ("stream_grid", ctypes.c_int32), ("kernel_bytes", ctypes.c_int64),
                ("long_mode", ctypes.c_int32), ("long_rg", ctypes.c_int32), ("iter_push", ctypes.c_int32),
-               ("pad2_", ctypes.c_int32), ("p_stream", ctypes.c_double)]
+               ("long_c16", ctypes.c_int32), ("p_stream", ctypes.c_double)]
 
 
 _vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double

@@ -280,6 +280,7 @@ struct ExecArgs {
   bool long_tiled;
   int64_t nblk;               // x blocks of kLongXB columns
   const int64_t* long_seg;    // [n_long][nblk+1] segment starts
+  const uint16_t* long_c16;   // [nnz] (long rows' entries only): colind & (kLongXB - 1), or null
   double* long_partial;       // [n_long][nblk]
   int long_grid;              // persistent grid of the column-tiled kernel
   bool split_fused;           // SPLIT: nz bin + tiled long rows interleaved in one grid
@@ -294,6 +295,7 @@ constexpr int64_t kLongXB = LONG_XB;  // columns per x block staged in smem by t
 void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long, int64_t nblk, int64_t* seg,
                      cudaStream_t s);
 void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s);
+void launch_long_c16(const MatView& A, const int32_t* long_rows, int64_t n_long, uint16_t* c16, cudaStream_t s);
 int long_tiled_grid(int64_t nblk, int sm_count, int per_sm);
 size_t long_tma_smem_bytes();
 int long_tma_prepare();                                        // smem attribute (< 0 on error)

@@ -47,10 +47,33 @@ void launch_long_seg(const MatView& A, const int32_t* long_rows, int64_t n_long,
     long_seg_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, long_rows, n_long, nblk, seg);
 }
 
+// c16[j] = colind[j] & (kLongXB - 1) for the nonzeros of the long rows (one
+// warp per row)
+template <typename RP>
+__global__ void long_c16_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ col,
+                                const int32_t* __restrict__ long_rows, int64_t n_long, uint16_t* __restrict__ c16) {
+  static_assert((kLongXB & (kLongXB - 1)) == 0 && kLongXB <= 65536, "x block: a power of two <= 2^16");
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (q >= n_long) return;
+  const int64_t r = long_rows[q];
+  for (int64_t j = (int64_t)rp[r] + (threadIdx.x & 31); j < (int64_t)rp[r + 1]; j += 32)
+    c16[j] = (uint16_t)(col[j] & (int32_t)(kLongXB - 1));
+}
+
+void launch_long_c16(const MatView& A, const int32_t* long_rows, int64_t n_long, uint16_t* c16, cudaStream_t s) {
+  if (n_long == 0) return;
+  const int g = (int)((n_long * 32 + kNT - 1) / kNT);
+  if (A.rp_bytes == 8)
+    long_c16_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, long_rows, n_long, c16);
+  else
+    long_c16_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, long_rows, n_long, c16);
+}
+
 // CTA item loop (persistent when the grid is smaller than the item count)
 #ifndef LONG_LB
 #define LONG_LB 4
 #endif
+template <bool C16>
 __global__ void __launch_bounds__(kNT, LONG_LB) long_tiled_kernel(const LongP p) {
   __shared__ double xs[kLongXB];
   // PDL-launched (SPLIT concurrent mode): wait for the previous SpMV, THEN let
@@ -59,7 +82,7 @@ __global__ void __launch_bounds__(kNT, LONG_LB) long_tiled_kernel(const LongP p)
   pdl_wait();
   pdl_trigger();
   for (int64_t it = blockIdx.x; it < p.nblk * p.rg; it += gridDim.x) {
-    long_item<kNT>(p, it, xs);
+    long_item<kNT, C16>(p, it, xs);
     __syncthreads();  // every warp is done with xs before the next item restages it
   }
 }
@@ -81,6 +104,7 @@ LongP long_params(const ExecArgs& a) {
   p.val = a.A.val;
   p.x = a.x;
   p.seg = a.long_seg;
+  p.col16 = a.long_c16;
   p.partial = a.long_partial;
   p.n_long = a.n_long;
   p.n_cols = a.A.n_cols;
@@ -102,10 +126,13 @@ int long_tiled_grid(int64_t nblk, int sm_count, int per_sm) {
 
 void launch_long_tiled(const ExecArgs& a, int part, cudaStream_t s) {
   if (a.n_long == 0) return;
-  if (part == 3)  // programmatic launch (SPLIT concurrent mode)
-    launch_pdl(long_tiled_kernel, dim3(a.long_grid), dim3(kNT), 0, s, long_params(a));
-  else if (part == 1)
-    long_tiled_kernel<<<a.long_grid, kNT, 0, s>>>(long_params(a));
+  if (part == 3) {  // programmatic launch (SPLIT concurrent mode)
+    if (a.long_c16) launch_pdl(long_tiled_kernel<true>, dim3(a.long_grid), dim3(kNT), 0, s, long_params(a));
+    else launch_pdl(long_tiled_kernel<false>, dim3(a.long_grid), dim3(kNT), 0, s, long_params(a));
+  } else if (part == 1) {
+    if (a.long_c16) long_tiled_kernel<true><<<a.long_grid, kNT, 0, s>>>(long_params(a));
+    else long_tiled_kernel<false><<<a.long_grid, kNT, 0, s>>>(long_params(a));
+  }
   else
     long_reduce_kernel<<<(int)((a.n_long * 32 + kNT - 1) / kNT), kNT, 0, s>>>(a.long_partial, a.n_long, a.nblk,
                                                                              a.long_rows, a.y);

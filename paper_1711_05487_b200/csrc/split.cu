@@ -10,6 +10,8 @@
 // CTAs with gather-bound short-row CTAs for the whole pass. The epilogue
 // (ordered carry fix-up of the bin + per-row reduction of the long-row
 // partials, disjoint rows) is one launch as well.
+#include <type_traits>
+
 #include "tiles.cuh"
 
 namespace spmv {
@@ -25,7 +27,7 @@ constexpr int kSplitThreads = 256;
 // 1 tile 117.7 us, 2 113.4, 3 112.4, 4 111.2, 5 111.7, 6 113.6)
 constexpr int kSplitTPW = SPLIT_TPW;
 
-template <typename RP, bool L2G>
+template <typename RP, bool L2G, bool C16>
 __global__ void __launch_bounds__(kSplitThreads, SPLIT_LB) split_fused_kernel(const NzP<RP> z, const LongP l, int64_t n_items,
                                                                          int64_t n_groups) {
   __shared__ double xs[kLongXB];
@@ -36,7 +38,7 @@ __global__ void __launch_bounds__(kSplitThreads, SPLIT_LB) split_fused_kernel(co
   const int64_t b = blockIdx.x;
   const int64_t Lb = (b + 1) * n_items / total;  // long items among blocks [0, b]
   if (Lb > b * n_items / total) {
-    long_item<kSplitThreads>(l, Lb - 1, xs);
+    long_item<kSplitThreads, C16>(l, Lb - 1, xs);
     return;
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -89,17 +91,28 @@ int launch_split_fused(const ExecArgs& a, cudaStream_t s) {
                   groups = (z.T + per - 1) / per;
     const int grid = (int)(items + groups);
     const dim3 g(grid), b(kSplitThreads);
-    if (z.V.rp_bytes == 8) {
-      if (z.gather_l2)
-        launch_pdl(split_fused_kernel<int64_t, true>, g, b, 0, s, nz_params64(z, a.x, a.y), long_params(a), items, groups);
+    // one instantiation per (rowptr width, gather path, long-row column
+    // format): a kernel holding both long-row paths spills at 64 registers
+    auto go = [&](auto rp, auto l2g, auto c16) {
+      using RP = decltype(rp);
+      constexpr bool L2G = decltype(l2g)::value, C16 = decltype(c16)::value;
+      if constexpr (sizeof(RP) == 8)
+        launch_pdl(split_fused_kernel<RP, L2G, C16>, g, b, 0, s, nz_params64(z, a.x, a.y), long_params(a), items,
+                   groups);
       else
-        launch_pdl(split_fused_kernel<int64_t, false>, g, b, 0, s, nz_params64(z, a.x, a.y), long_params(a), items, groups);
-    } else {
-      if (z.gather_l2)
-        launch_pdl(split_fused_kernel<int32_t, true>, g, b, 0, s, nz_params32(z, a.x, a.y), long_params(a), items, groups);
-      else
-        launch_pdl(split_fused_kernel<int32_t, false>, g, b, 0, s, nz_params32(z, a.x, a.y), long_params(a), items, groups);
-    }
+        launch_pdl(split_fused_kernel<RP, L2G, C16>, g, b, 0, s, nz_params32(z, a.x, a.y), long_params(a), items,
+                   groups);
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    auto go2 = [&](auto rp) {
+      if (z.gather_l2) {
+        if (a.long_c16) go(rp, T_{}, T_{}); else go(rp, T_{}, F_{});
+      } else {
+        if (a.long_c16) go(rp, F_{}, T_{}); else go(rp, F_{}, F_{});
+      }
+    };
+    if (z.V.rp_bytes == 8) go2(int64_t{}); else go2(int32_t{});
     ++n;
   }
   if (a.stage != 1) {

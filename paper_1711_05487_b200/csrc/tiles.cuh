@@ -278,6 +278,7 @@ __device__ __forceinline__ void nz_tile_compute(const NzP<RP>& p, int64_t k, int
 // ---- column-tiled long rows (see long_tiled.cu) -----------------------------
 struct LongP {
   const int32_t* col;
+  const uint16_t* col16;  // non-null: the long rows' in-block columns (colind & (kLongXB - 1))
   const double* val;
   const double* x;
   const int64_t* seg;   // [n_long][nblk+1]
@@ -301,7 +302,7 @@ struct LongP {
 #define LONG_U 16
 #endif
 constexpr int kLongU = LONG_U;  // nonzeros per lane per batch of the long-row stream
-template <int NT>
+template <int NT, bool C16>
 __device__ __forceinline__ void long_item(const LongP& p, int64_t it, double* xs) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   constexpr int NW = NT / 32;
@@ -341,6 +342,7 @@ __device__ __forceinline__ void long_item(const LongP& p, int64_t it, double* xs
     for (int64_t bb = s0; bb < s1; bb += 32 * U) {
       // one base pointer per stream + immediate offsets; slot u valid iff 32u < rem
       const int32_t* cp = p.col + bb + lane;
+      const uint16_t* cp16 = p.col16 + bb + lane;
       const double* vp = p.val + bb + lane;
       const int64_t r64 = s1 - bb - lane;
       const int rem = r64 > 32 * U ? 32 * U : (int)r64;
@@ -349,7 +351,8 @@ __device__ __forceinline__ void long_item(const LongP& p, int64_t it, double* xs
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool ok = 32 * u < rem;
-        c[u] = ok ? ld_stream(cp + 32 * u) - (int)c0 : 0;
+        if constexpr (C16) c[u] = ok ? ld_stream_u16(cp16 + 32 * u) : 0;
+        else c[u] = ok ? ld_stream(cp + 32 * u) - (int)c0 : 0;
         v[u] = ok ? ld_stream(vp + 32 * u) : 0.0;
       }
 #pragma unroll

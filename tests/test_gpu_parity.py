@@ -263,6 +263,28 @@ def test_configs_full_forced_variants(c, variant):
     assert_bound(p.execute(m.x), m)
 
 
+def test_split_long_rows_16bit_columns(monkeypatch):
+    """SPLIT's column-tiled long rows read 16-bit in-block columns (colind mod
+    the 2048-column x block) on full C4: the plan reports it, its compulsory
+    bytes drop by 2 B per long-row nonzero, and y is bit-identical to the
+    int32-colind long rows (same arithmetic, same order) and within the bound."""
+    m = sg.config(4)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals)
+    info = p.info()
+    assert info["variant"] == "split" and info["long_c16"] == 1
+    monkeypatch.setenv("SPMV_LONG_C16", "0")
+    q = spmv.Plan(m.rowptr, m.colind, m.vals)
+    monkeypatch.delenv("SPMV_LONG_C16")
+    iq = q.info()
+    assert iq["long_c16"] == 0
+    assert iq["kernel_bytes"] - info["kernel_bytes"] == 2 * info["feat"]["nnz_long"]
+    y = p.execute(m.x)
+    assert np.array_equal(y, q.execute(m.x))
+    assert_bound(y, m)
+    p.destroy()
+    q.destroy()
+
+
 def test_stencil_ones_bit_exact():
     # SURVEY 8(c4): 7-pt A*1 counts missing neighbours exactly -> bit-equal
     m = sg.config(2)
