@@ -34,6 +34,10 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``) -- no function is
                   statistics / n_empty / long rows vs numpy incl. L_split edges
   d8 dict/enc/dec stencil dictionaries from the grid geometry (7-pt: 10, 27-pt:
                   15 codes), hand example, 256/257 and 255/256 limits, round trip
+  pat enc/dec     stencil patterns from the grid geometry (27 boundary classes,
+                  interior offsets dz n^2 + dy n + dx), hand example, first-
+                  occurrence order vs a dict-based re-derivation, 256/257 and
+                  offset limits, round trip
   select          hand-evaluated rule table on the configs' closed-form features
 """
 from __future__ import annotations
@@ -91,6 +95,9 @@ def _lib():
         L.oracle_d8_encode.argtypes = [i64, vp, vp, vp, vp, vp]
         L.oracle_d8_encode.restype = ctypes.c_int
         L.oracle_d8_decode.argtypes = [i64, vp, vp, vp, vp]
+        L.oracle_pat_encode.argtypes = [i64, vp, vp, i64, i64, vp, vp, vp]
+        L.oracle_pat_encode.restype = i64
+        L.oracle_pat_decode.argtypes = [i64, vp, i64, vp, vp, vp]
         _LIB = L
     return _LIB
 
@@ -399,6 +406,36 @@ def d8_decode(dict_, codes, rlen):
     out = np.empty(max(cd.size, 1), np.int32)
     _lib().oracle_d8_decode(rl.size, _p(rl), _p(cd), _p(d), _p(out))
     return out[:cd.size]
+
+
+PAT_MAX = 256       # DESIGN.md reading 31: at most 256 row patterns (one byte per row) ...
+PAT_MAX_OFS = 4096  # ... holding at most 4096 column offsets in total
+
+
+def pat_encode(rowptr, colind, maxp=PAT_MAX, maxofs=PAT_MAX_OFS):
+    """Row-pattern codes (DESIGN.md reading 31): pattern of row i = (len_i;
+    colind[j] - i for j in row i), numbered by first occurrence. Returns
+    (ids u8[n], lens int64[np], ofs int64[sum lens]) or None when not codable
+    (a row longer than 255, > maxp patterns or > maxofs offsets)."""
+    rp, ci = _rp64(rowptr), _c32(colind)
+    n = rp.size - 1
+    ids = np.zeros(max(n, 1), np.uint8)
+    lens = np.zeros(max(maxp, 1), np.int64)
+    ofs = np.zeros(max(maxofs, 1), np.int64)
+    npat = _lib().oracle_pat_encode(n, _p(rp), _p(ci), int(maxp), int(maxofs), _p(ids), _p(lens), _p(ofs))
+    if npat < 0:
+        return None
+    return ids[:n], lens[:npat].copy(), ofs[:int(lens[:npat].sum())].copy()
+
+
+def pat_decode(ids, lens, ofs):
+    ids_ = np.ascontiguousarray(ids, np.uint8)
+    ln = np.ascontiguousarray(lens, np.int64)
+    of = np.ascontiguousarray(ofs, np.int64)
+    nnz = int(ln[ids_].sum()) if ids_.size else 0
+    out = np.empty(max(nnz, 1), np.int32)
+    _lib().oracle_pat_decode(ids_.size, _p(ids_), ln.size, _p(ln), _p(of), _p(out))
+    return out[:nnz]
 
 
 def tile_anchor(colind, C):

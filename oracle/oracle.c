@@ -479,3 +479,62 @@ void oracle_d8_decode(int64_t n, const uint8_t* rlen, const uint8_t* codes, cons
     }
   }
 }
+
+/* ---------------------------------------------------------------------------
+ * Row-pattern codes (reading 31; the MB answer of Sec. III-E,
+ * P:589-597, carried to the P_peak limit of P:341-344 -- indexing eliminated
+ * down to one byte per row): the pattern of row i is its length and the
+ * column offsets colind[j] - i, j in row i, in order. Patterns are numbered
+ * in the order of their first row. Returns the number of patterns and writes
+ * ids[n] (the row's pattern), lens[np], ofs[sum of lens] (pattern p's offsets
+ * at position sum_{q<p} lens[q]); returns -1 when the matrix is not codable:
+ * a row longer than 255, more than maxp patterns, or more than maxofs
+ * offsets in total. Each row is compared with the previous row's pattern,
+ * then with every pattern in id order.
+ * ------------------------------------------------------------------------- */
+static int pat_eq(const int64_t* lens, const int64_t* start, const int64_t* ofs, int64_t p, int64_t i,
+                  const int64_t* rowptr, const int32_t* colind) {
+  const int64_t len = rowptr[i + 1] - rowptr[i];
+  if (lens[p] != len) return 0;
+  for (int64_t t = 0; t < len; ++t)
+    if (ofs[start[p] + t] != (int64_t)colind[rowptr[i] + t] - i) return 0;
+  return 1;
+}
+
+int64_t oracle_pat_encode(int64_t n, const int64_t* rowptr, const int32_t* colind, int64_t maxp, int64_t maxofs,
+                          uint8_t* ids, int64_t* lens, int64_t* ofs) {
+  int64_t np = 0, nofs = 0, prev = -1;
+  int64_t* start = (int64_t*)malloc(sizeof(int64_t) * (size_t)(maxp > 0 ? maxp : 1));
+  if (!start) return -1;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t len = rowptr[i + 1] - rowptr[i];
+    if (len > 255) { free(start); return -1; }
+    int64_t found = -1;
+    if (prev >= 0 && pat_eq(lens, start, ofs, prev, i, rowptr, colind)) found = prev;
+    for (int64_t p = 0; found < 0 && p < np; ++p)
+      if (pat_eq(lens, start, ofs, p, i, rowptr, colind)) found = p;
+    if (found < 0) {
+      if (np == maxp || nofs + len > maxofs) { free(start); return -1; }
+      start[np] = nofs;
+      lens[np] = len;
+      for (int64_t t = 0; t < len; ++t) ofs[nofs + t] = (int64_t)colind[rowptr[i] + t] - i;
+      nofs += len;
+      found = np++;
+    }
+    ids[i] = (uint8_t)found;
+    prev = found;
+  }
+  free(start);
+  return np;
+}
+
+/* Decode: colind of row i = i + the offsets of pattern ids[i] (rows in order). */
+void oracle_pat_decode(int64_t n, const uint8_t* ids, int64_t np, const int64_t* lens, const int64_t* ofs,
+                       int32_t* col_out) {
+  int64_t j = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t st = 0;
+    for (int64_t q = 0; q < ids[i] && q < np; ++q) st += lens[q];
+    for (int64_t t = 0; t < lens[ids[i]]; ++t) col_out[j++] = (int32_t)(i + ofs[st + t]);
+  }
+}

@@ -705,3 +705,83 @@ def test_tune_profile_search_picks_the_widest_margin():
     assert abs(chosen[0] - 3.0) <= 0.02            # sqrt(1.5 * 6) = 3: equal log-margins
     assert (chosen[1], chosen[2]) == (T.PAPER[1], T.PAPER[2])
     assert T.score([r1, r2], [b1, b2], chosen)[1] > T.score([r1, r2], [b1, b2], T.PAPER)[1]
+
+
+# ---- row-pattern codes (reading 31) ------------------------------
+def _pat_stencil_closed_form(n, pts):
+    """Patterns of a pts-point stencil on n^3 (n >= 3) from the grid geometry:
+    one per boundary class (low / interior / high in each dimension), offsets
+    dz n^2 + dy n + dx over the neighbours that exist, ascending."""
+    out = {}
+    for cz in (0, 1, 2):
+        for cy in (0, 1, 2):
+            for cx in (0, 1, 2):
+                def rng(c):
+                    return [d for d in (-1, 0, 1) if not (c == 0 and d == -1) and not (c == 2 and d == 1)]
+                if pts == 27:
+                    o = [dz * n * n + dy * n + dx for dz in rng(cz) for dy in rng(cy) for dx in rng(cx)]
+                else:
+                    o = [0] + [dz * n * n for dz in rng(cz) if dz] + [dy * n for dy in rng(cy) if dy] + \
+                        [dx for dx in rng(cx) if dx]
+                out[(cz, cy, cx)] = sorted(o)
+    return out
+
+
+@pytest.mark.parametrize("n", [3, 4, 7, 12])
+@pytest.mark.parametrize("pts", [7, 27])
+def test_pat_stencil_closed_form(n, pts):
+    m = sg.stencil(n, pts)
+    ids, lens, ofs = oracle.pat_encode(m.rowptr, m.colind)
+    want = _pat_stencil_closed_form(n, pts)
+    assert len(lens) == 27  # one pattern per boundary class
+    starts = np.concatenate([[0], np.cumsum(lens)])
+    got = {tuple(ofs[starts[p]:starts[p + 1]].tolist()) for p in range(len(lens))}
+    assert got == {tuple(v) for v in want.values()}
+    # every row carries the pattern of its class
+    i = np.arange(m.n)
+    cls = lambda c: np.where(c == 0, 0, np.where(c == n - 1, 2, 1))  # noqa: E731
+    for r in np.random.default_rng(n).integers(0, m.n, 200):
+        key = (int(cls(i[r] // (n * n))), int(cls((i[r] // n) % n)), int(cls(i[r] % n)))
+        p = ids[r]
+        assert ofs[starts[p]:starts[p + 1]].tolist() == want[key]
+    assert int(lens.sum()) == (343 if pts == 27 else 135)  # (2+3+2)^3; 8*4 + 12*5 + 6*6 + 7
+    assert np.array_equal(oracle.pat_decode(ids, lens, ofs), m.colind)
+
+
+def test_pat_hand_example_and_limits():
+    # rows: [0, 1], [1, 2], [0]: offsets (0, 1), (0, 1), (-2) -> ids 0, 0, 1
+    ids, lens, ofs = oracle.pat_encode(rp_of([2, 2, 1]), np.array([0, 1, 1, 2, 0], np.int32))
+    assert ids.tolist() == [0, 0, 1] and lens.tolist() == [2, 1] and ofs.tolist() == [0, 1, -2]
+    # empty rows are the length-0 pattern; ids by first occurrence
+    ids, lens, ofs = oracle.pat_encode(rp_of([0, 1, 0, 1]), np.array([3, 0], np.int32))
+    assert ids.tolist() == [0, 1, 0, 2] and lens.tolist() == [0, 1, 1] and ofs.tolist() == [2, -3]
+    # 256 patterns codable, 257 not: row i -> column 0 (offset -i)
+    for k, ok in ((256, True), (257, False)):
+        enc = oracle.pat_encode(np.arange(k + 1), np.zeros(k, np.int32))
+        assert (enc is not None) == ok
+        if ok:
+            assert enc[0].tolist() == list(range(k)) and enc[2].tolist() == [-i for i in range(k)]
+    # offsets limit (total over the patterns) and the 255 row-length limit
+    rp, ci = rp_of([3, 3]), np.array([0, 1, 2, 0, 2, 3], np.int32)  # offsets (0,1,2), (-1,1,2): 6
+    assert oracle.pat_encode(rp, ci, maxofs=6) is not None and oracle.pat_encode(rp, ci, maxofs=5) is None
+    for L_, ok in ((255, True), (256, False)):
+        assert (oracle.pat_encode(rp_of([L_]), np.arange(L_, dtype=np.int32)) is not None) == ok
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_pat_first_occurrence_vs_dict(seed):
+    # banded rows from a few templates: ids equal a dict-based re-derivation
+    # (first occurrence of each (length, offsets) tuple), round trip exact
+    g = np.random.default_rng(seed)
+    n = 2000
+    tmpl = [np.array(sorted(set(g.integers(-40, 40, g.integers(1, 12)).tolist()))) for _ in range(9)]
+    rows = [tmpl[t] for t in g.integers(0, 9, n)]
+    rows = [r[(r + i >= 0) & (r + i < n)] + i for i, r in enumerate(rows)]
+    rp = rp_of([len(r) for r in rows])
+    ci = np.concatenate(rows).astype(np.int32)
+    ids, lens, ofs = oracle.pat_encode(rp, ci)
+    seen, want = {}, []
+    for i, r in enumerate(rows):
+        want.append(seen.setdefault(tuple((r - i).tolist()), len(seen)))
+    assert ids.tolist() == want and len(lens) == len(seen)
+    assert np.array_equal(oracle.pat_decode(ids, lens, ofs), ci)
