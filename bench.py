@@ -483,6 +483,7 @@ def run_native(a):
                        f"inputs {byts / 1e6:.1f} MB fit in L2: warm-cache, not an HBM measurement"),
                 "variant": info["variant"], "vs": info["sel"]["vs"], "d16": info["sel"]["d16"],
                 "xwin": info["sel"]["xwin"], "classes": info["classes"],
+                "d8_patterns": info["d8_patterns"], "long_c16": info["long_c16"],
                 "tile_nnz": info["tile_nnz"], "hbm_gbs_effective": gbs,
                 "pct_of_8tbs": 100.0 * gbs / (NOMINAL_HBM_GBS * world),
                 "pct_of_measured_copy_bw": 100.0 * gbs / (peak * world),

@@ -175,6 +175,9 @@ typedef struct spmv_plan_info {
   double p_stream;            /* profile mode, second stage: flop/s of the plain cta_stream kernel when Fig. 4
                                  mapped the matrix to it and its indices are D8-codable; >= (1 - tol) P_MB adds
                                  MB and D8 (reading 30); 0 when not run */
+  int32_t d8_patterns;        /* D8 row-pattern mode (reading 31): the rows' patterns (<= 256; one byte
+                                 per row names its pattern, no per-nonzero index is read); 0 when not used */
+  int32_t pad3_;
 } spmv_plan_info;
 
 /* ---- plan lifecycle ---------------------------------------------------- */
@@ -362,7 +365,10 @@ enum {
   SPMV_ARR_NZ_HOT_COLS = 15,  /* int64[n_hot]: hot columns in column order (reading 20) */
   SPMV_ARR_D8_CODES = 16,     /* uint8[nnz]: D8 codes (index of each row-relative delta in the dictionary) */
   SPMV_ARR_D8_RLEN = 17,      /* uint8[n_rows]: D8 row lengths */
-  SPMV_ARR_D8_DICT = 18       /* int64[d8_n_dict]: D8 dictionary (ascending distinct deltas) */
+  SPMV_ARR_D8_DICT = 18,      /* int64[d8_n_dict]: D8 dictionary (ascending distinct deltas) */
+  SPMV_ARR_PAT_IDS = 19,      /* uint8[n_rows]: row-pattern mode, each row's pattern (reading 31) */
+  SPMV_ARR_PAT_LEN = 20,      /* int64[d8_patterns]: the patterns' lengths, numbered by first row */
+  SPMV_ARR_PAT_OFS = 21       /* int64[sum of lengths]: their column offsets from the row id, pattern by pattern */
 };
 int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst);
 

@@ -22,10 +22,11 @@ VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 CLASSES = {"MB": 1, "ML": 2, "IMB": 4, "CMP": 8}
 ARR = {"tile_rows": 1, "merge_rows": 2, "merge_nnz": 3, "chunk_row": 4, "chunk_begin": 5, "chunk_end": 6,
        "dcol": 7, "head": 8, "anchor": 9, "decoded": 10, "shard_bounds": 11, "nz_rowmap": 12, "nz_rpc": 13,
-       "nz_tile_q": 14, "nz_hot_cols": 15, "d8_codes": 16, "d8_rlen": 17, "d8_dict": 18}
+       "nz_tile_q": 14, "nz_hot_cols": 15, "d8_codes": 16, "d8_rlen": 17, "d8_dict": 18, "pat_ids": 19,
+       "pat_len": 20, "pat_ofs": 21}
 _ARR_DTYPE = {1: np.int64, 2: np.int64, 3: np.int64, 4: np.int64, 5: np.int64, 6: np.int64, 7: np.uint16,
               8: np.int32, 9: np.int32, 10: np.int32, 11: np.int64, 12: np.int64, 13: np.int64, 14: np.int64,
-              15: np.int64, 16: np.uint8, 17: np.uint8, 18: np.int64}
+              15: np.int64, 16: np.uint8, 17: np.uint8, 18: np.int64, 19: np.uint8, 20: np.int64, 21: np.int64}
 
 
 class Options(ctypes.Structure):
@@ -96,7 +97,8 @@ class PlanInfo(ctypes.Structure):
                ("x_reuse", ctypes.c_double), ("nz_gather_l2", ctypes.c_int32), ("stream_stages", ctypes.c_int32),
                ("d8_n_dict", ctypes.c_int32), ("stream_grid", ctypes.c_int32), ("kernel_bytes", ctypes.c_int64),
                ("long_mode", ctypes.c_int32), ("long_rg", ctypes.c_int32), ("iter_push", ctypes.c_int32),
-               ("long_c16", ctypes.c_int32), ("p_stream", ctypes.c_double)]
+               ("long_c16", ctypes.c_int32), ("p_stream", ctypes.c_double),
+               ("d8_patterns", ctypes.c_int32), ("pad3_", ctypes.c_int32)]
 
 
 _vp, _i64, _i32, _d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
@@ -329,7 +331,7 @@ class Plan:
     def info(self) -> dict:
         i = PlanInfo()
         _check(lib.spmv_plan_query(self._h, ctypes.byref(i)))
-        d = {k: getattr(i, k) for k, _ in PlanInfo._fields_ if k not in ("sel", "feat", "pad_", "shard_bounds")}
+        d = {k: getattr(i, k) for k, _ in PlanInfo._fields_ if k not in ("sel", "feat", "pad_", "pad3_", "shard_bounds")}
         d["sel"] = {k: getattr(i.sel, k) for k, _ in Selection._fields_ if k != "pad_"}
         d["variant"] = VARIANT_NAMES[i.sel.variant]
         d["classes"] = [k for k, v in CLASSES.items() if i.sel.classes & v]

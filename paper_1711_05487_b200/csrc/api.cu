@@ -905,6 +905,101 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
 
   // ---- a3/a4: structures for the selected variant ---------------------------------
   double t_d = now_ms();
+  // Row-pattern mode of D8 (reading 31): when the shard's rows
+  // follow <= 256 patterns (length + column offsets from the row id) holding
+  // <= kPatMaxOfs offsets, the per-row byte names the row's pattern and no
+  // per-nonzero index is stored at all -- the P_peak limit of P:341-344 up
+  // to one byte per row. Patterns are numbered by their first row (the
+  // oracle's order); every row is verified against its pattern.
+  auto build_patterns = [&](Shard& s, StreamPlan& sp, const MatView& V) -> bool {
+    if (V.m == 0) return false;
+    if (const char* e = getenv("SPMV_D8_PATTERNS"))
+      if (atoi(e) == 0) return false;  // experiments / tests: the 8-bit codes
+    unsigned long long* gk = s.alloc<unsigned long long>(2 * kPatGlobal);
+    int* flag = s.alloc<int>(1);
+    std::vector<void*> tmp = {gk, flag};
+    auto done = [&](bool ok) {
+      for (void* q : tmp) s.free_alloc(q);
+      return ok;
+    };
+    ck(cudaMemsetAsync(gk, 0, kPatGlobal * 8, s.stream), "memset");
+    ck(cudaMemsetAsync(gk + kPatGlobal, 0xff, kPatGlobal * 8, s.stream), "memset");
+    ck(cudaMemsetAsync(flag, 0, 4, s.stream), "memset");
+    launch_pat_collect(V, sp.row0, gk, gk + kPatGlobal, flag, s.stream);
+    count_launches(1, "pattern collect");
+    std::vector<unsigned long long> hk(2 * kPatGlobal);
+    int hf = 0;
+    ck(cudaMemcpyAsync(hk.data(), gk, 16 * kPatGlobal, cudaMemcpyDeviceToHost, s.stream), "patterns");
+    ck(cudaMemcpyAsync(&hf, flag, 4, cudaMemcpyDeviceToHost, s.stream), "patterns");
+    ck(cudaStreamSynchronize(s.stream), "patterns");
+    if (hf) return done(false);
+    std::vector<std::pair<unsigned long long, unsigned long long>> pat;  // (first row, hash)
+    for (int t = 0; t < kPatGlobal; ++t)
+      if (hk[(size_t)t]) pat.push_back({hk[(size_t)(kPatGlobal + t)], hk[(size_t)t]});
+    if (pat.empty() || pat.size() > 256) return done(false);
+    std::sort(pat.begin(), pat.end());
+    // each pattern's offsets, read from its first row
+    std::vector<int32_t> desc(256, 0), ofs;
+    for (size_t q = 0; q < pat.size(); ++q) {
+      const int64_t r = (int64_t)pat[q].first;
+      int64_t ab[2] = {0, 0};
+      if (V.rp_bytes == 8) {
+        ck(cudaMemcpy(ab, (const int64_t*)V.rowptr + r, 16, cudaMemcpyDeviceToHost), "pattern row");
+      } else {
+        int32_t w[2];
+        ck(cudaMemcpy(w, (const int32_t*)V.rowptr + r, 8, cudaMemcpyDeviceToHost), "pattern row");
+        ab[0] = w[0];
+        ab[1] = w[1];
+      }
+      const int64_t len = ab[1] - ab[0];
+      if (len > 255 || (int64_t)ofs.size() + len > kPatMaxOfs) return done(false);
+      std::vector<int32_t> c((size_t)len);
+      if (len) ck(cudaMemcpy(c.data(), V.col + ab[0], (size_t)len * 4, cudaMemcpyDeviceToHost), "pattern row");
+      desc[q] = (int32_t)((len << 16) | (int64_t)ofs.size());
+      for (int64_t t = 0; t < len; ++t) ofs.push_back((int32_t)((int64_t)c[(size_t)t] - (sp.row0 + r)));
+    }
+    const int np = (int)pat.size(), nofs = (int)ofs.size();
+    std::vector<std::pair<unsigned long long, int32_t>> byk;
+    for (int q = 0; q < np; ++q) byk.push_back({pat[(size_t)q].second, q});
+    std::sort(byk.begin(), byk.end());
+    std::vector<unsigned long long> skey;
+    std::vector<int32_t> sid;
+    for (auto& e : byk) {
+      skey.push_back(e.first);
+      sid.push_back(e.second);
+    }
+    unsigned long long* skey_d = s.alloc<unsigned long long>(256);
+    int32_t* sid_d = s.alloc<int32_t>(256);
+    tmp.push_back(skey_d);
+    tmp.push_back(sid_d);
+    int32_t* desc_d = s.alloc<int32_t>(256);
+    int32_t* ofs_d = s.alloc<int32_t>((size_t)nofs + 16);
+    uint8_t* ids = s.alloc<uint8_t>((size_t)V.m);
+    ck(cudaMemcpyAsync(skey_d, skey.data(), (size_t)np * 8, cudaMemcpyHostToDevice, s.stream), "patterns");
+    ck(cudaMemcpyAsync(sid_d, sid.data(), (size_t)np * 4, cudaMemcpyHostToDevice, s.stream), "patterns");
+    ck(cudaMemcpyAsync(desc_d, desc.data(), 256 * 4, cudaMemcpyHostToDevice, s.stream), "patterns");
+    if (nofs) ck(cudaMemcpyAsync(ofs_d, ofs.data(), (size_t)nofs * 4, cudaMemcpyHostToDevice, s.stream), "patterns");
+    launch_pat_assign(V, sp.row0, skey_d, sid_d, np, desc_d, ofs_d, nofs, ids, flag, s.stream);
+    count_launches(1, "pattern assign");
+    ck(cudaMemcpyAsync(&hf, flag, 4, cudaMemcpyDeviceToHost, s.stream), "patterns");
+    ck(cudaStreamSynchronize(s.stream), "patterns");
+    if (hf) {
+      tmp.push_back(desc_d);
+      tmp.push_back(ofs_d);
+      tmp.push_back(ids);
+      return done(false);
+    }
+    sp.d8_bits = 0;
+    sp.n_dict = np;
+    for (int q = 0; q < 256; ++q) sp.dict[q] = desc[(size_t)q];
+    sp.d8_dict_dev = desc_d;
+    sp.pat_ofs = ofs_d;
+    sp.n_pat_ofs = nofs;
+    sp.codes = ids;  // (marks the plan as D8; the kernel stages the ids as its per-row byte)
+    sp.rlen = ids;
+    return done(true);
+  };
+
   // cta_stream structures over the CSR view V (the whole shard, or one
   // compacted length bin of long_row_split mapped back through rowmap)
   auto build_stream = [&](Shard& s, StreamPlan& sp, const MatView& V, const int32_t* rowmap, int dmode, int vs,
@@ -943,6 +1038,8 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       sp.tile_nz = s.alloc<int64_t>((size_t)sp.T + 1);
       launch_tile_nz(V, sp.tile_row, sp.T, sp.tile_nz, s.stream);
       count_launches(2, "d8 tiles");
+      sp.row0 = s.row0;
+      if (!build_patterns(s, sp, V)) {
       sp.n_dict = (int)P->d8dict.size();
       for (int i = 0; i < sp.n_dict; ++i) sp.dict[i] = P->d8dict[(size_t)i];
       int32_t* dict_dev = s.alloc<int32_t>(256);
@@ -970,6 +1067,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       sp.rlen = rlen;
       sp.d8_dict_dev = dict_dev;
       ck(cudaStreamSynchronize(s.stream), "d8 encode");
+      }
       // packed tiles (one TMA copy per tile: values | codes | row lengths):
       // experiment, C2 27.1 vs 28.1 us but C5 2.36 vs 2.21 ms -> off by default
       bool packed = false;
@@ -1004,7 +1102,7 @@ spmv_plan create_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const void* r
       int best = -1, best_cw = 4;
       for (int c : {4, 6, 8}) {
         if (cw && c != cw) continue;
-        if (d8_smem_bytes(sp.C, Rt, c, sp.d8_bits) > 227 * 1024 - kStaticSmemMargin) continue;
+        if (d8_smem_bytes(sp.C, Rt, c, sp.d8_bits, sp.n_pat_ofs) > 227 * 1024 - kStaticSmemMargin) continue;
         sp.stages = c;
         sp.grid = d8_prepare(sp, s.sm_count);
         if (sp.grid < 0) { cudaGetLastError(); continue; }
@@ -2383,14 +2481,16 @@ spmv_status spmv_plan_query(spmv_plan p, spmv_plan_info* info) {
     info->nz_gather_l2 = s0.nz.gather_l2 ? 1 : 0;
     info->stream_stages = s0.sp[0].stages;
     info->stream_grid = s0.sp[0].grid;
-    info->d8_n_dict = s0.sp[0].codes ? s0.sp[0].n_dict : 0;
-    if (s0.sp[0].codes) info->d16_width = s0.sp[0].d8_bits;
+    info->d8_n_dict = s0.sp[0].codes && s0.sp[0].d8_bits ? s0.sp[0].n_dict : 0;
+    info->d8_patterns = s0.sp[0].codes && !s0.sp[0].d8_bits ? s0.sp[0].n_dict : 0;
+    if (s0.sp[0].codes) info->d16_width = s0.sp[0].d8_bits ? s0.sp[0].d8_bits : 8;
     {  // compulsory bytes of one SpMV in the plan's own format
       int64_t kb = 8 * p->n_cols + 8 * p->n_rows + 8 * p->nnz;
       for (const Shard& s : p->shards) {
         const StreamPlan& sp = s.sp[0];
         if (p->sel.variant == SPMV_VARIANT_STREAM && sp.codes)
-          kb += (sp.d8_bits == 4 ? (s.nnz + 1) / 2 : s.nnz) + s.m + 8 * (sp.T + 1);  // codes, row lengths, tile starts
+          kb += (sp.d8_bits == 0 ? 0 : sp.d8_bits == 4 ? (s.nnz + 1) / 2 : s.nnz) + s.m + 8 * (sp.T + 1);  // codes,
+                                                                   // row lengths (or pattern ids), tile starts
         else if (p->sel.variant == SPMV_VARIANT_STREAM && sp.dcol)
           kb += 2 * s.nnz + (int64_t)p->rp_bytes * (s.m + 1) + 4 * s.m;  // deltas, rowptr, heads
         else if (s.long_c16)
@@ -2520,7 +2620,7 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
       case SPMV_ARR_ANCHOR: raw(s.sp[0].anchor, s.sp[0].anchor ? s.sp[0].T : 0, 4); break;
       case SPMV_ARR_D8_CODES: {  // one code per nonzero (4-bit codes unpacked, low nibble first)
         const StreamPlan& sp = s.sp[0];
-        count = sp.codes ? s.nnz : 0;
+        count = sp.codes && sp.d8_bits ? s.nnz : 0;
         if (!dst || count == 0) break;
         if (sp.d8_bits == 8) {
           ck(cudaMemcpy(dst, sp.codes, (size_t)count, cudaMemcpyDeviceToHost), "export");
@@ -2531,9 +2631,25 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
         }
         break;
       }
-      case SPMV_ARR_D8_RLEN: raw(s.sp[0].rlen, s.sp[0].rlen ? s.m : 0, 1); break;
+      case SPMV_ARR_D8_RLEN: raw(s.sp[0].rlen, s.sp[0].rlen && s.sp[0].d8_bits ? s.m : 0, 1); break;
+      case SPMV_ARR_PAT_IDS: raw(s.sp[0].rlen, s.sp[0].rlen && !s.sp[0].d8_bits ? s.m : 0, 1); break;
+      case SPMV_ARR_PAT_LEN:
+      case SPMV_ARR_PAT_OFS: {
+        const StreamPlan& sp = s.sp[0];
+        const bool on = sp.codes && !sp.d8_bits;
+        count = !on ? 0 : which == SPMV_ARR_PAT_LEN ? sp.n_dict : sp.n_pat_ofs;
+        if (!dst || count == 0) break;
+        if (which == SPMV_ARR_PAT_LEN) {
+          for (int64_t q = 0; q < count; ++q) ((int64_t*)dst)[q] = (sp.dict[q] >> 16) & 0xff;
+        } else {
+          std::vector<int32_t> h((size_t)count);
+          ck(cudaMemcpy(h.data(), sp.pat_ofs, (size_t)count * 4, cudaMemcpyDeviceToHost), "export");
+          for (int64_t q = 0; q < count; ++q) ((int64_t*)dst)[q] = h[(size_t)q];
+        }
+        break;
+      }
       case SPMV_ARR_D8_DICT: {
-        count = s.sp[0].codes ? s.sp[0].n_dict : 0;
+        count = s.sp[0].codes && s.sp[0].d8_bits ? s.sp[0].n_dict : 0;
         if (dst)
           for (int64_t i = 0; i < count; ++i) ((int64_t*)dst)[i] = s.sp[0].dict[i];
         break;
@@ -2543,7 +2659,8 @@ int64_t spmv_plan_export(spmv_plan p, int g, int which, void* dst) {
         if (!dst || count == 0) break;
         int32_t* tmp = nullptr;
         ck(cudaMalloc(&tmp, (size_t)s.nnz * 4 + 64), "cudaMalloc");
-        if (s.sp[0].codes) launch_d8_decode_export(s.sp[0], s.sp[0].d8_dict_dev, tmp, s.stream);
+        if (s.sp[0].codes && !s.sp[0].d8_bits) launch_pat_decode_export(s.sp[0], tmp, s.stream);
+        else if (s.sp[0].codes) launch_d8_decode_export(s.sp[0], s.sp[0].d8_dict_dev, tmp, s.stream);
         else launch_d16_decode_export(s.sp[0], tmp, s.stream);
         g_launches += 1;
         cudaError_t e = cudaStreamSynchronize(s.stream);

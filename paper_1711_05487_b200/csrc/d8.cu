@@ -32,12 +32,14 @@ namespace spmv {
 __host__ __device__ __forceinline__ size_t d8_al128(size_t v) { return (v + 127) & ~(size_t)127; }
 
 struct D8Layout {
-  size_t vals, codes, rl, stage, full, empty, meta, total;
+  size_t vals, codes, rl, stage, full, empty, meta, pat, total;
 };
 
 // C: nonzero capacity of a tile (Rt x longest row), Rt rows per tile, CB:
-// bits per code (8, or 4 when the dictionary has <= 16 entries)
-__host__ __device__ inline D8Layout d8_layout(int64_t C, int64_t Rt, int stages, int CB = 8) {
+// bits per code (8, or 4 when the dictionary has <= 16 entries; 0: row-pattern
+// mode -- no code stream, the per-row byte is the row's pattern, whose npofs
+// column offsets live in shared memory after the barriers)
+__host__ __device__ inline D8Layout d8_layout(int64_t C, int64_t Rt, int stages, int CB = 8, int64_t npofs = 0) {
   D8Layout L;
   L.vals = 0;
   // values: copy starts at the 128-B line of the first value (<= 15 before
@@ -45,17 +47,22 @@ __host__ __device__ inline D8Layout d8_layout(int64_t C, int64_t Rt, int stages,
   L.codes = d8_al128((size_t)(C + 16) * 8);
   // codes: copy starts 16-B aligned (<= 15 before t0), rounded up to 16 B,
   // plus >= 16 readable bytes past any row end (branch-free 16-code batches)
-  L.rl = L.codes + d8_al128((size_t)(CB == 4 ? (C + 1) / 2 : C) + 64);
+  L.rl = L.codes + (CB == 0 ? 0 : d8_al128((size_t)(CB == 4 ? (C + 1) / 2 : C) + 64));
   L.stage = d8_al128(L.rl + (size_t)Rt + 16);
   size_t o = L.stage * stages;
   L.full = o; o += 8 * (size_t)stages;
   L.empty = o; o += 8 * (size_t)stages;
   L.meta = d8_al128(o); o = L.meta + 32 * (size_t)stages;
+  // pattern offsets (+ 16 readable entries past the last: a batch past a
+  // row end reads stale offsets, masked like stale codes)
+  L.pat = d8_al128(o); o = L.pat + (CB == 0 ? (size_t)(npofs + 16) * 4 : 0);
   L.total = d8_al128(o);
   return L;
 }
 
-size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages, int CB) { return d8_layout(C, Rt, stages, CB).total; }
+size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages, int CB, int64_t npofs) {
+  return d8_layout(C, Rt, stages, CB, npofs).total;
+}
 
 struct D8Meta {
   int64_t t0;
@@ -78,7 +85,9 @@ struct D8P {
   int64_t row0;     // row id of local row 0 (the anchor of the head deltas)
   int64_t n_cols;   // (checked build only)
   int stages;
-  int32_t dict[256];
+  const int32_t* pofs;  // row-pattern mode: the patterns' column offsets [n_pofs]
+  int n_pofs;
+  int32_t dict[256];    // dictionary; row-pattern mode: pattern p = offsets [d & 0xffff, + (d >> 16)) of pofs
 };
 
 __device__ __forceinline__ void d8_arrive(uint64_t* bar) {
@@ -90,6 +99,7 @@ __device__ __forceinline__ void d8_arrive(uint64_t* bar) {
 template <int CW, bool SCALE, int UN, int CB, bool PK, bool PU>
 __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, const D8Layout& L, uint64_t* full,
                                              uint64_t* empty, const D8Meta* meta, const int32_t* dict_s, double f) {
+  const int32_t* pat_s = reinterpret_cast<const int32_t*>(smem + L.pat);  // (row-pattern mode)
   const int S = p.stages;
   const int w = (threadIdx.x >> 5) - 1;
   const int lane = threadIdx.x & 31;
@@ -121,7 +131,10 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
     int base = 0;  // first nonzero (tile-relative) of the pass
     for (int qb = 0; qb < nrows; qb += 32) {
       const int q = qb + lane;
-      const int len = q < nrows ? (int)rl_s[q] : 0;
+      // row-pattern mode: the staged byte is the row's pattern, its
+      // descriptor gives the length and where its offsets start
+      const int dsc = CB == 0 ? dict_s[q < nrows ? (int)rl_s[q] : 0] : 0;
+      const int len = q < nrows ? (CB == 0 ? (dsc >> 16) & 0xff : (int)rl_s[q]) : 0;
       int inc = len;  // inclusive scan of the row lengths over the pass
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -140,13 +153,22 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
         // UN independent x gathers in flight per lane
         int cc[UN];
         double xv[UN];
+        if constexpr (CB == 0) {
+          // row-pattern mode: column = row id + the pattern's offset -- no
+          // running sum, every offset an independent smem read (lanes of
+          // one pattern read the same word: a broadcast)
+          const int32_t* po = pat_s + (dsc & 0xffff) + l0;
 #pragma unroll
-        for (int u = 0; u < UN; ++u) {
-          const int e = mt.coff + off + l0 + u;
-          const int code = CB == 8 ? (int)codes_s[e] : ((int)codes_s[e >> 1] >> ((e & 1) << 2)) & 15;
-          const int d = dict_s[code];
-          c += (l0 + u < len) ? d : 0;
-          cc[u] = c;
+          for (int u = 0; u < UN; ++u) cc[u] = c + po[u];
+        } else {
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            const int e = mt.coff + off + l0 + u;
+            const int code = CB == 8 ? (int)codes_s[e] : ((int)codes_s[e >> 1] >> ((e & 1) << 2)) & 15;
+            const int d = dict_s[code];
+            c += (l0 + u < len) ? d : 0;
+            cc[u] = c;
+          }
         }
 #pragma unroll
         for (int u = 0; u < UN; ++u) SPMV_CHECK(l0 + u >= len || (cc[u] >= 0 && cc[u] < p.n_cols));
@@ -188,8 +210,8 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
 // registers, UN = 16 -> ~96
 constexpr int d8_lb(int CW, int UN) { return UN == 8 ? (CW == 4 ? 5 : (CW == 6 ? 4 : 3)) : (CW == 4 ? 4 : (CW == 6 ? 3 : 2)); }
 
-// PU: the multi-shard halo push instantiation (IterOut::push_*; 8-bit codes,
-// unpacked tiles only -- d8_push_capable)
+// PU: the multi-shard halo push instantiation (IterOut::push_*; 8-bit codes or
+// row patterns, unpacked tiles only -- d8_push_capable)
 template <int CW, int UN, int CB, bool PK, bool PU = false>
 __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const D8P p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -197,7 +219,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
   __shared__ double f_s;                   // iterated mode: this launch's exact factor
   __shared__ __align__(8) uint64_t fbar_s;  // ... and its hand-over barrier
   uint64_t* fbar = &fbar_s;
-  const D8Layout L = d8_layout(p.C, p.Rt, p.stages, CB);
+  const D8Layout L = d8_layout(p.C, p.Rt, p.stages, CB, p.n_pofs);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.empty);
   D8Meta* meta = reinterpret_cast<D8Meta*>(smem + L.meta);
@@ -205,6 +227,10 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
 
   pdl_trigger();
   for (int i = threadIdx.x; i < 256; i += blockDim.x) dict_s[i] = p.dict[i];
+  if constexpr (CB == 0) {
+    int32_t* pat_s = reinterpret_cast<int32_t*>(smem + L.pat);
+    for (int i = threadIdx.x; i < p.n_pofs + 16; i += blockDim.x) pat_s[i] = i < p.n_pofs ? p.pofs[i] : 0;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -247,7 +273,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
         const int64_t cb0 = (CB == 8 ? t0 : (t0 >> 1)) & ~15ll;
         const int64_t cb1 = CB == 8 ? t1 : (t1 + 1) >> 1;
         const uint32_t vb = t1 > t0 ? (uint32_t)(((t1 - v0) * 8 + 15) & ~15ll) : 0u;
-        const uint32_t cb = t1 > t0 ? (uint32_t)(((cb1 - cb0) + 15) & ~15ll) : 0u;
+        const uint32_t cb = (CB != 0 && t1 > t0) ? (uint32_t)(((cb1 - cb0) + 15) & ~15ll) : 0u;
         const uint32_t rb = (uint32_t)(((R1 - R0) + 15) & ~15ll);
         D8Meta mt;
         mt.t0 = t0;
@@ -267,7 +293,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), d8_lb(CW, UN)) d8_kernel(const 
           mbar_arrive_expect_tx(&full[s], vb + cb + rb);
           if (t1 > t0) {
             bulk_g2s(st + L.vals, p.val + v0, vb, &full[s], pol);
-            bulk_g2s(st + L.codes, p.codes + cb0, cb, &full[s], pol);
+            if constexpr (CB != 0) bulk_g2s(st + L.codes, p.codes + cb0, cb, &full[s], pol);
           }
           bulk_g2s(st + L.rl, p.rlen + R0, rb, &full[s], pol);
         }
@@ -326,17 +352,19 @@ static D8P d8_params(const StreamPlan& sp, const double* x, double* y) {
   p.row0 = sp.row0;
   p.n_cols = sp.V.n_cols;
   p.stages = sp.stages;
+  p.pofs = sp.pat_ofs;
+  p.n_pofs = sp.n_pat_ofs;
   for (int i = 0; i < 256; ++i) p.dict[i] = i < sp.n_dict ? sp.dict[i] : 0;
   return p;
 }
 
 template <int CW, int UN, int CB, bool PK>
 static int d8_prepare_t(const StreamPlan& sp, int sm_count) {
-  const size_t smem = d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB);
+  const size_t smem = d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB, sp.n_pat_ofs);
   if (cudaFuncSetAttribute(d8_kernel<CW, UN, CB, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return -1;
-  if constexpr (CB == 8 && !PK) {
+  if constexpr ((CB == 8 || CB == 0) && !PK) {
     if (cudaFuncSetAttribute(d8_kernel<CW, UN, CB, PK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
       return -1;
@@ -356,7 +384,7 @@ template <int CW, int UN, int CB, bool PK>
 static int d8_per_sm_t(const StreamPlan& sp) {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d8_kernel<CW, UN, CB, PK>, 32 * (CW + 1),
-                                                    d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB)) !=
+                                                    d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB, sp.n_pat_ofs)) !=
       cudaSuccess)
     return 0;
   return per_sm;
@@ -364,18 +392,18 @@ static int d8_per_sm_t(const StreamPlan& sp) {
 
 template <int CW, int UN, int CB, bool PK>
 static void d8_launch_t(const StreamPlan& sp, const double* x, double* y, cudaStream_t s) {
-  if constexpr (CB == 8 && !PK) {
+  if constexpr ((CB == 8 || CB == 0) && !PK) {
     if (sp.it.push_lo || sp.it.push_hi) {
       launch_pdl(d8_kernel<CW, UN, CB, PK, true>, dim3(sp.grid), dim3(32 * (CW + 1)),
-                 d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB), s, d8_params(sp, x, y));
+                 d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB, sp.n_pat_ofs), s, d8_params(sp, x, y));
       return;
     }
   }
   launch_pdl(d8_kernel<CW, UN, CB, PK>, dim3(sp.grid), dim3(32 * (CW + 1)),
-             d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB), s, d8_params(sp, x, y));
+             d8_smem_bytes(sp.C, sp.rows_per_tile, sp.stages, CB, sp.n_pat_ofs), s, d8_params(sp, x, y));
 }
 
-bool d8_push_capable(const StreamPlan& sp) { return sp.d8_bits == 8 && !sp.d8_tiles; }
+bool d8_push_capable(const StreamPlan& sp) { return (sp.d8_bits == 8 || sp.d8_bits == 0) && !sp.d8_tiles; }
 
 // (stages = consumer warps CW) x (batch width UN) x (code layout) -> instantiation
 template <int UN, int CB, bool PK, typename F>
@@ -392,6 +420,7 @@ static int d8_cw(const StreamPlan& sp, F&& f) {
 }
 template <typename F>
 static int d8_dispatch(const StreamPlan& sp, F&& f) {
+  if (sp.d8_bits == 0) return sp.d8_un == 16 ? d8_cw<16, 0, false>(sp, f) : d8_cw<8, 0, false>(sp, f);  // patterns
   if (sp.d8_bits == 4) return sp.d8_un == 16 ? d8_cw<16, 4, false>(sp, f) : d8_cw<8, 4, false>(sp, f);
   if (sp.d8_tiles) return d8_cw<8, 8, true>(sp, f);
   return sp.d8_un == 16 ? d8_cw<16, 8, false>(sp, f) : d8_cw<8, 8, false>(sp, f);
@@ -537,6 +566,176 @@ void launch_d8_decode_export(const StreamPlan& sp, const int32_t* dict_dev, int3
   else
     d8_decode_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)sp.V.rowptr, sp.V.m, sp.row0, sp.codes, sp.rlen,
                                                 dict_dev, sp.d8_bits, out);
+}
+
+
+// ---- row patterns (plan time; reading 31) --------------------------
+// Pattern of row i = its length and the offsets colind[j] - i. Pass 1 hashes
+// every row and collects the distinct hashes with their first row (per-CTA
+// shared-memory table, then a 1024-slot global table); the host numbers the
+// patterns by first row and reads their offsets from those rows; pass 2 maps
+// each row's hash to its pattern and VERIFIES the row against the pattern's
+// offsets (a hash collision fails the plan over to the 8-bit codes).
+constexpr int kPatLocal = 512;
+
+__device__ __forceinline__ unsigned long long pat_hash(const int32_t* __restrict__ col, int64_t a, int64_t b,
+                                                       int64_t rowid) {
+  unsigned long long h = 0x9E3779B97F4A7C15ull ^ (unsigned long long)(b - a);
+  for (int64_t j = a; j < b; ++j) {
+    const unsigned long long o = (unsigned long long)(uint32_t)(int32_t)((int64_t)col[j] - rowid);
+    h = (h ^ o) * 0x100000001B3ull;
+    h ^= h >> 29;
+  }
+  h ^= h >> 32;
+  h *= 0xD6E8FEB86659FD93ull;
+  h ^= h >> 32;
+  return h | 1ull;  // 0 marks an empty slot
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(kNT) pat_collect_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ col,
+                                                          int64_t m, int64_t row0, unsigned long long* __restrict__ gkey,
+                                                          unsigned long long* __restrict__ gfirst, int* __restrict__ flag) {
+  __shared__ unsigned long long key[kPatLocal], first[kPatLocal];
+  __shared__ int cnt;
+  for (int i = threadIdx.x; i < kPatLocal; i += kNT) {
+    key[i] = 0ull;
+    first[i] = ~0ull;
+  }
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kNT;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) {
+    const int64_t a = rp[i], b = rp[i + 1];
+    if (b - a > 255) {
+      atomicOr(flag, 1);
+      break;
+    }
+    const unsigned long long h = pat_hash(col, a, b, row0 + i);
+    unsigned sl = (unsigned)(h >> 40) & (kPatLocal - 1);
+    for (int probe = 0; probe < kPatLocal; ++probe, sl = (sl + 1) & (kPatLocal - 1)) {
+      unsigned long long k = key[sl];
+      if (k == 0ull) {
+        k = atomicCAS(&key[sl], 0ull, h);
+        if (k == 0ull) {
+          atomicAdd(&cnt, 1);
+          k = h;
+        }
+      }
+      if (k == h) {
+        if ((unsigned long long)i < first[sl]) atomicMin(&first[sl], (unsigned long long)i);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (cnt > 256) {
+    if (threadIdx.x == 0) atomicOr(flag, 2);
+    return;
+  }
+  for (int t = threadIdx.x; t < kPatLocal; t += kNT) {
+    const unsigned long long h = key[t];
+    if (!h) continue;
+    unsigned sl = (unsigned)(h >> 40) & (kPatGlobal - 1);
+    for (int probe = 0; probe < kPatGlobal; ++probe, sl = (sl + 1) & (kPatGlobal - 1)) {
+      const unsigned long long k = atomicCAS(&gkey[sl], 0ull, h);
+      if (k == 0ull || k == h) {
+        atomicMin(&gfirst[sl], first[t]);
+        break;
+      }
+    }
+  }
+}
+
+// pass 2: ids[i] = the pattern of row i (skey: the patterns' hashes sorted,
+// sid: their ids); flag |= 4 when a hash is not found, 8 when a row differs
+// from its pattern (collision)
+template <typename RP>
+__global__ void __launch_bounds__(kNT) pat_assign_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ col,
+                                                         int64_t m, int64_t row0,
+                                                         const unsigned long long* __restrict__ skey,
+                                                         const int32_t* __restrict__ sid, int np,
+                                                         const int32_t* __restrict__ desc,
+                                                         const int32_t* __restrict__ pofs, int npofs,
+                                                         uint8_t* __restrict__ ids, int* __restrict__ flag) {
+  __shared__ unsigned long long k_s[256];
+  __shared__ int32_t id_s[256], d_s[256];
+  __shared__ int32_t o_s[kPatMaxOfs];
+  for (int i = threadIdx.x; i < 256; i += kNT) {
+    k_s[i] = i < np ? skey[i] : ~0ull;
+    id_s[i] = i < np ? sid[i] : 0;
+    d_s[i] = i < np ? desc[i] : 0;
+  }
+  for (int i = threadIdx.x; i < npofs; i += kNT) o_s[i] = pofs[i];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kNT;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < m; i += stride) {
+    const int64_t a = rp[i], b = rp[i + 1];
+    const unsigned long long h = pat_hash(col, a, b, row0 + i);
+    int lo = 0, hi = np - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (k_s[mid] < h) lo = mid + 1; else hi = mid;
+    }
+    if (np == 0 || k_s[lo] != h) {
+      atomicOr(flag, 4);
+      continue;
+    }
+    const int pid = id_s[lo], d = d_s[pid];
+    bool same = ((d >> 16) & 0xff) == (int)(b - a);
+    for (int64_t j = a; same && j < b; ++j) same = o_s[(d & 0xffff) + (j - a)] == (int32_t)((int64_t)col[j] - (row0 + i));
+    if (!same) atomicOr(flag, 8);
+    ids[i] = (uint8_t)pid;
+  }
+}
+
+void launch_pat_collect(const MatView& A, int64_t row0, unsigned long long* gkey, unsigned long long* gfirst,
+                        int* flag, cudaStream_t s) {
+  if (A.m == 0) return;
+  int64_t g = (A.m + kNT - 1) / kNT;
+  if (g > dev_sm_count() * 8) g = dev_sm_count() * 8;
+  if (A.rp_bytes == 8)
+    pat_collect_kernel<int64_t><<<(unsigned)g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, A.m, row0, gkey,
+                                                            gfirst, flag);
+  else
+    pat_collect_kernel<int32_t><<<(unsigned)g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, A.m, row0, gkey,
+                                                            gfirst, flag);
+}
+
+void launch_pat_assign(const MatView& A, int64_t row0, const unsigned long long* skey, const int32_t* sid, int np,
+                       const int32_t* desc, const int32_t* pofs, int npofs, uint8_t* ids, int* flag, cudaStream_t s) {
+  if (A.m == 0) return;
+  int64_t g = (A.m + kNT - 1) / kNT;
+  if (g > dev_sm_count() * 8) g = dev_sm_count() * 8;
+  if (A.rp_bytes == 8)
+    pat_assign_kernel<int64_t><<<(unsigned)g, kNT, 0, s>>>((const int64_t*)A.rowptr, A.col, A.m, row0, skey, sid,
+                                                           np, desc, pofs, npofs, ids, flag);
+  else
+    pat_assign_kernel<int32_t><<<(unsigned)g, kNT, 0, s>>>((const int32_t*)A.rowptr, A.col, A.m, row0, skey, sid,
+                                                           np, desc, pofs, npofs, ids, flag);
+}
+
+// Export (tests): colind re-decoded from the row patterns (one thread per row)
+template <typename RP>
+__global__ void __launch_bounds__(kNT) pat_decode_kernel(const RP* __restrict__ rp, int64_t m, int64_t row0,
+                                                         const uint8_t* __restrict__ ids,
+                                                         const int32_t* __restrict__ desc,
+                                                         const int32_t* __restrict__ pofs, int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x;
+  if (i >= m) return;
+  const int d = desc[ids[i]];
+  for (int t = 0; t < ((d >> 16) & 0xff); ++t) out[(int64_t)rp[i] + t] = (int32_t)(row0 + i + pofs[(d & 0xffff) + t]);
+}
+
+void launch_pat_decode_export(const StreamPlan& sp, int32_t* out, cudaStream_t s) {
+  if (sp.V.m == 0) return;
+  const unsigned g = (unsigned)((sp.V.m + kNT - 1) / kNT);
+  if (sp.V.rp_bytes == 8)
+    pat_decode_kernel<int64_t><<<g, kNT, 0, s>>>((const int64_t*)sp.V.rowptr, sp.V.m, sp.row0, sp.rlen,
+                                                 sp.d8_dict_dev, sp.pat_ofs, out);
+  else
+    pat_decode_kernel<int32_t><<<g, kNT, 0, s>>>((const int32_t*)sp.V.rowptr, sp.V.m, sp.row0, sp.rlen,
+                                                 sp.d8_dict_dev, sp.pat_ofs, out);
 }
 
 }  // namespace spmv

@@ -127,11 +127,23 @@ struct StreamPlan {
   int64_t row0 = 0;            // row id of local row 0 (anchor of the head deltas)
   const int32_t* d8_dict_dev = nullptr;  // the dictionary on the device (export decode)
   int d8_un = 8;               // D8 codes decoded + x gathers in flight per lane per batch (8 or 16)
-  int d8_bits = 8;             // D8 bits per code: 8, or 4 (two per byte) when the dictionary has <= 16 entries
+  int d8_bits = 8;             // D8 bits per code: 8, or 4 (two per byte) when the dictionary has <= 16 entries;
+                               // 0: row-pattern mode (rlen holds each row's pattern id; dict = pattern descriptors
+                               // len << 16 | first offset; pat_ofs = the patterns' column offsets from the row id)
+  const int32_t* pat_ofs = nullptr;
+  int n_pat_ofs = 0;
   const unsigned char* d8_tiles = nullptr;  // packed tiles: [values | codes | row lengths] per tile (one TMA copy)
   const int64_t* d8_toff = nullptr;         // their byte offsets [T+1]
 };
-size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages, int CB = 8);
+size_t d8_smem_bytes(int64_t C, int64_t Rt, int stages, int CB = 8, int64_t npofs = 0);
+// row patterns (reading 31): <= 256 patterns, <= kPatMaxOfs offsets in total
+constexpr int kPatGlobal = 1024;   // slots of the plan-time hash table
+constexpr int kPatMaxOfs = 4096;
+void launch_pat_collect(const MatView& A, int64_t row0, unsigned long long* gkey, unsigned long long* gfirst,
+                        int* flag, cudaStream_t s);
+void launch_pat_assign(const MatView& A, int64_t row0, const unsigned long long* skey, const int32_t* sid, int np,
+                       const int32_t* desc, const int32_t* pofs, int npofs, uint8_t* ids, int* flag, cudaStream_t s);
+void launch_pat_decode_export(const StreamPlan& sp, int32_t* out, cudaStream_t s);
 int d8_prepare(const StreamPlan& sp, int sm_count);  // stages = consumer warps (4, 6, 8)
 bool d8_push_capable(const StreamPlan& sp);           // has the halo-push instantiation
 bool stream_push_capable(const StreamPlan& sp);       // STREAM / D8 iterated kernel with the halo push

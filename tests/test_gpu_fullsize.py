@@ -43,6 +43,7 @@ def test_c5_every_row_and_dyadic(c5):
     p = spmv.Plan(m.rowptr, m.colind, m.vals)
     info = p.info()
     assert info["feat"]["nnz"] == 1520875000 and info["feat"]["n_deltas"] == 15
+    assert info["kernel_bytes"] == 8 * m.nnz + m.n + 8 * (info["n_tiles"] + 1) + 16 * m.n
     assert info["variant"] == "stream" and info["sel"]["d16"] == 2  # the benchmarked configuration
     xd = torch.from_numpy(m.x).cuda()
     yd = torch.empty(m.n, dtype=torch.float64, device="cuda")
@@ -55,15 +56,14 @@ def test_c5_every_row_and_dyadic(c5):
     torch.cuda.synchronize()
     yq, _ = oracle.spmv_omp(m.rowptr, m.colind, m.vals, xq, 0)
     assert np.array_equal(yd.cpu().numpy(), yq)
-    # plan structures at full size: the dictionary equals the oracle's; the
-    # device's codes and row lengths, decoded by the oracle's decoder, give
-    # colind back exactly (codes are unique under a sorted dictionary, so
-    # they equal the oracle's encoding)
-    nd, dict_full = oracle.d8_dict(m.rowptr, m.colind)
-    assert nd == 15 and np.array_equal(p.export("d8_dict"), dict_full)
-    rl = p.export("d8_rlen")
-    assert np.array_equal(rl, np.diff(m.rowptr))
-    assert np.array_equal(oracle.d8_decode(dict_full, p.export("d8_codes"), rl), m.colind)
+    # plan structures at full size: the 27 row patterns (DESIGN.md reading
+    # 31) and every row's pattern equal the oracle's encoding, and the
+    # oracle's decoder gives colind back from the device's patterns
+    assert info["d8_patterns"] == 27
+    ids, lens, ofs = oracle.pat_encode(m.rowptr, m.colind)
+    pid, pl, po = p.export("pat_ids"), p.export("pat_len"), p.export("pat_ofs")
+    assert np.array_equal(pid, ids) and np.array_equal(pl, lens) and np.array_equal(po, ofs)
+    assert np.array_equal(oracle.pat_decode(pid, pl, po), m.colind)
     p.destroy()
 
 

@@ -5,6 +5,8 @@ every row; bit-exact for integer work (plan structures, D16 round trip,
 features, validation codes) and for dyadic inputs where every summation
 order is exact.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -640,7 +642,7 @@ def test_profile_mode_second_stage_d8(which):
                               p_stream=info["p_stream"])
     assert (info["sel"]["d16"], info["sel"]["classes"]) == (o.d16, o.classes)
     if info["p_stream"] >= 0.9 * info["p_mb"]:
-        assert info["sel"]["d16"] == 2 and "MB" in info["classes"] and info["d8_n_dict"] > 0
+        assert info["sel"]["d16"] == 2 and "MB" in info["classes"] and info["d8_n_dict"] + info["d8_patterns"] > 0
     assert_bound(p.execute(m.x), m)
     xg, _ = p.iterate(m.x, 3)
     rc, xr, _ = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, 3)
@@ -749,19 +751,42 @@ def _d8_cases():
 D8_CASES = _d8_cases()
 
 
+def _check_d8_structures(p, m, row_shift=0, g=0):
+    """The plan's D8 structures equal the oracle's: row patterns (DESIGN.md
+    reading 31) when the rows follow <= 256 of them, else dictionary codes;
+    the device's own decode gives colind back (round trip). row_shift:
+    global row id of the block's first row (emulated shards)."""
+    rp = m.rowptr.astype(np.int64)
+    pat = oracle.pat_encode(rp, m.colind.astype(np.int64) - row_shift)
+    info = p.info()
+    assert info["d16_width"] == 8
+    if pat is not None and os.environ.get("SPMV_D8_PATTERNS", "1") != "0":
+        ids, lens, ofs = pat
+        assert info["d8_patterns"] == lens.size and info["d8_n_dict"] == 0
+        assert np.array_equal(p.export("pat_ids", g), ids)
+        assert np.array_equal(p.export("pat_len", g), lens) and np.array_equal(p.export("pat_ofs", g), ofs)
+        assert p.export("d8_codes", g).size == 0
+    else:
+        d, codes, rlen = oracle.d8_encode(m.rowptr, m.colind)
+        assert info["d8_patterns"] == 0 and info["d8_n_dict"] == d.size
+        assert np.array_equal(p.export("d8_dict", g), d)
+        assert np.array_equal(p.export("d8_codes", g), codes)
+        assert np.array_equal(p.export("d8_rlen", g), rlen)
+    assert np.array_equal(p.export("decoded", g), m.colind)  # device decode, round trip (S:148)
+
+
+@pytest.mark.parametrize("mode", ["patterns", "codes"])
 @pytest.mark.parametrize("name,m", D8_CASES, ids=[n for n, _ in D8_CASES])
-def test_d8_structures_and_parity(name, m):
+def test_d8_structures_and_parity(name, m, mode, monkeypatch):
+    if mode == "codes":
+        monkeypatch.setenv("SPMV_D8_PATTERNS", "0")
     enc = oracle.d8_encode(m.rowptr, m.colind)
     assert enc is not None
     d, codes, rlen = enc
     p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", d16=2)
     info = p.info()
-    assert info["sel"]["d16"] == 2 and info["d8_n_dict"] == d.size and info["d16_width"] == 8
-    assert info["feat"]["n_deltas"] == d.size
-    assert np.array_equal(p.export("d8_dict"), d)
-    assert np.array_equal(p.export("d8_codes"), codes)
-    assert np.array_equal(p.export("d8_rlen"), rlen)
-    assert np.array_equal(p.export("decoded"), m.colind)  # device decode, round trip
+    assert info["sel"]["d16"] == 2 and info["feat"]["n_deltas"] == d.size
+    _check_d8_structures(p, m)
     Rt = info["rows_per_tile"]
     assert Rt % 16 == 0 and np.array_equal(p.export("tile_rows"), np.minimum(np.arange(info["n_tiles"] + 1) * Rt, m.n))
     y = p.execute(m.x, np.full(m.n, np.nan))
@@ -784,17 +809,26 @@ def test_d8_consumer_warp_counts(monkeypatch, cw):
     assert_bound(p.execute(m.x), m)
 
 
+@pytest.mark.parametrize("mode", ["patterns", "codes"])
 @pytest.mark.parametrize("G", [2, 3])
-def test_d8_emulated_shards(G):
+def test_d8_emulated_shards(G, mode, monkeypatch):
+    if mode == "codes":
+        monkeypatch.setenv("SPMV_D8_PATTERNS", "0")
     m = sg.stencil(16, 27, x_seed=2)
     d, codes, rlen = oracle.d8_encode(m.rowptr, m.colind)
     p = spmv.Plan(m.rowptr, m.colind, m.vals, ngpus=G, emulate_devices=1, force_variant="stream", d16=2)
     b = p.info()["shard_bounds"]
     rp = m.rowptr.astype(np.int64)
-    for g in range(G):  # one global dictionary; shard g's codes are the oracle's slice
-        assert np.array_equal(p.export("d8_dict", g), d)
-        assert np.array_equal(p.export("d8_codes", g), codes[rp[b[g]]:rp[b[g + 1]]])
-        assert np.array_equal(p.export("decoded", g), m.colind[rp[b[g]]:rp[b[g + 1]]])
+    for g in range(G):
+        sl = slice(rp[b[g]], rp[b[g + 1]])
+        if mode == "codes":  # one global dictionary; shard g's codes are the oracle's slice
+            assert np.array_equal(p.export("d8_dict", g), d)
+            assert np.array_equal(p.export("d8_codes", g), codes[sl])
+        else:  # shard g's patterns: the oracle's on its rows, offsets from the global row id
+            ids, lens, ofs = oracle.pat_encode(rp[b[g]:b[g + 1] + 1] - rp[b[g]], m.colind[sl].astype(np.int64) - b[g])
+            assert np.array_equal(p.export("pat_ids", g), ids) and np.array_equal(p.export("pat_ofs", g), ofs)
+            assert np.array_equal(p.export("pat_len", g), lens)
+        assert np.array_equal(p.export("decoded", g), m.colind[sl])
     assert_bound(p.execute(m.x), m)
     # iterated mode through D8 shards (fused per-tile norm partials)
     rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, 30)
@@ -807,8 +841,16 @@ def test_d8_auto_selected_on_c2_and_host_pipeline(monkeypatch):
     m = sg.config(2)
     p = spmv.Plan(m.rowptr, m.colind, m.vals)
     info = p.info()
-    assert info["variant"] == "stream" and info["sel"]["d16"] == 2 and info["d8_n_dict"] == 10
-    assert info["kernel_bytes"] == 9 * m.nnz + m.n + 8 * (info["n_tiles"] + 1) + 16 * m.n
+    # 27 row patterns (one per boundary class): one byte per row, no per-nonzero index
+    assert info["variant"] == "stream" and info["sel"]["d16"] == 2 and info["d8_patterns"] == 27
+    assert info["kernel_bytes"] == 8 * m.nnz + m.n + 8 * (info["n_tiles"] + 1) + 16 * m.n
+    _check_d8_structures(p, m)
+    monkeypatch.setenv("SPMV_D8_PATTERNS", "0")  # the 8-bit codes
+    q = spmv.Plan(m.rowptr, m.colind, m.vals)
+    iq = q.info()
+    monkeypatch.delenv("SPMV_D8_PATTERNS")
+    assert iq["d8_n_dict"] == 10 and iq["d8_patterns"] == 0
+    assert iq["kernel_bytes"] == 9 * m.nnz + m.n + 8 * (iq["n_tiles"] + 1) + 16 * m.n
     y = p.execute(m.x)
     assert_bound(y, m)
     ones = np.ones(m.n)
@@ -946,8 +988,11 @@ def test_iterated_push_not_for_scattered_blocks():
     assert np.all(np.abs(nug - nur) <= 1e-12 * nur)
 
 
+@pytest.mark.parametrize("mode", ["patterns", "codes"])
 @pytest.mark.parametrize("rb,re", [(0, 3000), (2000, 5500), (5000, 8000)])
-def test_d8_row_block_plan(rb, re):
+def test_d8_row_block_plan(rb, re, mode, monkeypatch):
+    if mode == "codes":
+        monkeypatch.setenv("SPMV_D8_PATTERNS", "0")
     # one rank's row block of a 27-pt stencil (the torchrun layout: n_rows <
     # n_cols, rowptr rebased, global column ids): D8 head deltas are taken
     # against the block's local row ids -- the oracle encodes the block the same way
@@ -957,7 +1002,7 @@ def test_d8_row_block_plan(rb, re):
     assert enc is not None
     p = spmv.Plan(blk.rowptr, blk.colind, blk.vals, n_cols=full.n, force_variant="stream", d16=2)
     assert p.info()["sel"]["d16"] == 2
-    assert np.array_equal(p.export("d8_dict"), enc[0]) and np.array_equal(p.export("d8_codes"), enc[1])
+    _check_d8_structures(p, blk)
     y = p.execute(full.x)
     m = sg.CSR(re - rb, blk.rowptr, blk.colind, blk.vals, full.x)
     assert_bound(y, m)
