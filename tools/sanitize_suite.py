@@ -33,8 +33,12 @@ mixed = sg.from_lengths(lens, 3000, g)
 huge = sg.from_lengths(np.asarray([5] * 2000 + [3000] + [5] * 2000, np.int64), 4001, g)
 check("stream row tiles (27-pt)", st, force_variant="stream", d16=0)
 check("stream row tiles CW6 (7-pt)", st7, force_variant="stream", d16=0)
-check("stream D8 (27-pt)", st, force_variant="stream", d16=2)
-check("stream D8 (7-pt)", st7, force_variant="stream", d16=2)
+check("stream D8 row patterns (27-pt)", st, force_variant="stream", d16=2)
+check("stream D8 row patterns (7-pt)", st7, force_variant="stream", d16=2)
+os.environ["SPMV_D8_PATTERNS"] = "0"  # the dictionary codes (row patterns are the default D8 path)
+check("stream D8 codes (27-pt)", st, force_variant="stream", d16=2)
+check("stream D8 codes (7-pt)", st7, force_variant="stream", d16=2)
+del os.environ["SPMV_D8_PATTERNS"]
 check("stream D16 row tiles", st7, force_variant="stream", d16=1)
 check("stream D16 escapes nnz tiles", st, force_variant="stream", d16=1, tile_nnz=512)
 check("stream nnz tiles + fix-up", mixed, force_variant="stream", tile_nnz=512, no_aligned=1)
