@@ -178,11 +178,20 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
 #else
         for (int u = 0; u < UN; ++u) xv[u] = l0 + u < len ? ld_x(p.x + cc[u]) : 0.0;
 #endif
+        if constexpr (UN % 2 == 0) {
 #pragma unroll
-        for (int u = 0; u < UN; u += 2) {
-          const int l = l0 + u;
-          a0 = fma(l < len ? vals_s[off + l] : 0.0, xv[u], a0);
-          a1 = fma(l + 1 < len ? vals_s[off + l + 1] : 0.0, xv[u + 1], a1);
+          for (int u = 0; u < UN; u += 2) {
+            const int l = l0 + u;
+            a0 = fma(l < len ? vals_s[off + l] : 0.0, xv[u], a0);
+            a1 = fma(l + 1 < len ? vals_s[off + l + 1] : 0.0, xv[u + 1], a1);
+          }
+        } else {  // odd batch (row patterns whose length it divides, e.g. 27 = 3 x 9)
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            const double v = l0 + u < len ? vals_s[off + l0 + u] : 0.0;
+            if (u & 1) a1 = fma(v, xv[u], a1);
+            else a0 = fma(v, xv[u], a0);
+          }
         }
       }
       double acc = a0 + a1;
@@ -208,7 +217,7 @@ __device__ __forceinline__ double d8_consume(const D8P& p, unsigned char* smem, 
 
 // resident CTAs per SM the registers allow (launch bound): UN = 8 -> ~72
 // registers, UN = 16 -> ~96
-constexpr int d8_lb(int CW, int UN) { return UN == 8 ? (CW == 4 ? 5 : (CW == 6 ? 4 : 3)) : (CW == 4 ? 4 : (CW == 6 ? 3 : 2)); }
+constexpr int d8_lb(int CW, int UN) { return UN <= 9 ? (CW == 4 ? 5 : (CW == 6 ? 4 : 3)) : (CW == 4 ? 4 : (CW == 6 ? 3 : 2)); }
 
 // PU: the multi-shard halo push instantiation (IterOut::push_*; 8-bit codes or
 // row patterns, unpacked tiles only -- d8_push_capable)
@@ -420,7 +429,11 @@ static int d8_cw(const StreamPlan& sp, F&& f) {
 }
 template <typename F>
 static int d8_dispatch(const StreamPlan& sp, F&& f) {
-  if (sp.d8_bits == 0) return sp.d8_un == 16 ? d8_cw<16, 0, false>(sp, f) : d8_cw<8, 0, false>(sp, f);  // patterns
+  if (sp.d8_bits == 0)  // row patterns
+    return sp.d8_un == 16  ? d8_cw<16, 0, false>(sp, f)
+           : sp.d8_un == 9 ? d8_cw<9, 0, false>(sp, f)
+           : sp.d8_un == 7 ? d8_cw<7, 0, false>(sp, f)
+                           : d8_cw<8, 0, false>(sp, f);
   if (sp.d8_bits == 4) return sp.d8_un == 16 ? d8_cw<16, 4, false>(sp, f) : d8_cw<8, 4, false>(sp, f);
   if (sp.d8_tiles) return d8_cw<8, 8, true>(sp, f);
   return sp.d8_un == 16 ? d8_cw<16, 8, false>(sp, f) : d8_cw<8, 8, false>(sp, f);
