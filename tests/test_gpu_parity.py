@@ -800,6 +800,25 @@ def test_d8_structures_and_parity(name, m, mode, monkeypatch):
     assert np.array_equal(pd.execute(xv), oracle.spmv(m.rowptr, m.colind, vv, xv))
 
 
+@pytest.mark.parametrize("un", ["7", "8", "9", "16"])
+@pytest.mark.parametrize("pts", [7, 27])
+def test_d8_pattern_batch_widths(monkeypatch, un, pts):
+    """Row-pattern D8 at every batch width (the plan picks 9 for 27-pt rows,
+    7 for 7-pt rows): y within the bound, dyadic inputs bit-exact, and the
+    iterated mode vs the oracle."""
+    monkeypatch.setenv("SPMV_D8_UN", un)
+    m = sg.stencil(20, pts, x_seed=6)
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, force_variant="stream", d16=2)
+    assert p.info()["d8_patterns"] == 27
+    assert_bound(p.execute(m.x), m)
+    g = np.random.default_rng(5)
+    xv = g.integers(-1024, 1025, m.n) / 1024.0
+    assert np.array_equal(p.execute(xv), oracle.spmv(m.rowptr, m.colind, m.vals, xv))
+    xg, nug = p.iterate(m.x, 12)
+    rc, xr, nur = oracle.power_iter(m.rowptr, m.colind, m.vals, m.x, 12)
+    assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr)) and np.all(np.abs(nug - nur) <= 1e-12 * nur)
+
+
 @pytest.mark.parametrize("cw", ["4", "6", "8"])
 def test_d8_consumer_warp_counts(monkeypatch, cw):
     monkeypatch.setenv("SPMV_D8_CW", cw)
