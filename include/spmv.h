@@ -66,7 +66,9 @@ typedef struct spmv_options {
   int32_t force_vs;        /* lanes per row for VECTOR/STREAM/SPLIT reductions: 0 = auto, else 1,2,4,8,16,32 */
   int32_t d16;             /* delta colind (STREAM only): -1 auto, 0 off, 1 = 16-bit deltas when
                               encodable, 2 = dictionary-coded 8-bit deltas (D8) when codable (<= 256 distinct
-                              row-relative deltas, rows <= 255 nonzeros; reading 26) */
+                              row-relative deltas, rows <= 255 nonzeros; reading 26); a D8 plan whose
+                              rows follow <= 256 (length, column offsets) patterns with <= 4096 offsets stores
+                              one pattern byte per row instead (row-pattern mode, reading 31) */
   int32_t xwin;            /* L2 persistence window on x (ML analogue of P:599-606): -1 auto, 0 off, 1 on */
   int32_t validate;        /* 1 = check CSR invariants on the device (default), 0 = trust the input */
   int64_t l_split;         /* long-row threshold in nnz (0 = 4096) */
@@ -357,7 +359,8 @@ enum {
   SPMV_ARR_DCOL = 7,         /* uint16[nnz] delta colind */
   SPMV_ARR_HEAD = 8,         /* int32[n_rows] */
   SPMV_ARR_ANCHOR = 9,       /* int32[n_tiles] */
-  SPMV_ARR_DECODED = 10,     /* int32[nnz] colind re-decoded on the device from dcol/head (D16) or codes/rlen/dict (D8) */
+  SPMV_ARR_DECODED = 10,     /* int32[nnz] colind re-decoded on the device from dcol/head (D16), codes/rlen/dict (D8)
+                                or the row patterns (D8 row-pattern mode) */
   SPMV_ARR_SHARD_BOUNDS = 11, /* int64[ngpus+1] */
   SPMV_ARR_NZ_ROWMAP = 12,    /* int64[mc+1]: nnz_split non-empty rows (y row ids), rowmap[mc] = n_rows */
   SPMV_ARR_NZ_RPC = 13,       /* int64[mc+1]: their rowptr (rpc[q] = rowptr[rowmap[q]], rpc[mc] = nnz) */
