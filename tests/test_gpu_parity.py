@@ -1065,3 +1065,43 @@ def test_plan_update_values(name, mk, opts, monkeypatch):
         rc, xr, _ = oracle.power_iter(m.rowptr, m.colind, v3, m.x, 5)
         assert np.max(np.abs(xg - xr)) <= 1e-10 * np.max(np.abs(xr))
     p.destroy()
+
+
+def _rows_matrix(rows, n_cols, seed):
+    """CSR from explicit per-row column lists (ascending), random values / x."""
+    g = np.random.default_rng(seed)
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int32)
+    ci = np.concatenate([np.asarray(r, np.int32) for r in rows]) if rp[-1] else np.zeros(0, np.int32)
+    return sg.CSR(len(rows), rp, ci, g.uniform(-1, 1, ci.size), g.uniform(-1, 1, n_cols))
+
+
+@pytest.mark.parametrize("case", ["256_patterns", "257_patterns", "4096_offsets", "4186_offsets"])
+def test_d8_pattern_limits(case):
+    """Row-pattern mode at its limits (reading 31): 256 patterns / 4096
+    offsets use it, 257 patterns / more offsets fall back to the dictionary
+    codes -- the same decision as oracle.pat_encode; structures, bound and
+    dyadic bit-exactness either way."""
+    if case.endswith("patterns"):
+        # row i: the single column i + i (offset i: 256 patterns, 256 deltas), plus (257) one row {i, i+1}
+        rows = [[2 * i] for i in range(256)]
+        if case == "257_patterns":
+            rows.append([len(rows), len(rows) + 1])
+    else:
+        top = 90 if case == "4096_offsets" else 91  # sum 1..90 = 4095, 1..91 = 4186
+        rows = [list(range(i, i + L)) for i, L in enumerate(range(1, top + 1))]
+    rows = rows * 3  # repeat: rows reuse their first occurrence
+    rows = [[c + i - (i % (len(rows) // 3)) for c in r] for i, r in enumerate(rows)]
+    m = _rows_matrix(rows, 3 * len(rows) + 300, 7)
+    want = oracle.pat_encode(m.rowptr, m.colind)
+    assert (want is not None) == (case in ("256_patterns", "4096_offsets"))
+    p = spmv.Plan(m.rowptr, m.colind, m.vals, n_cols=m.x.size, force_variant="stream", d16=2)
+    info = p.info()
+    assert info["sel"]["d16"] == 2
+    assert (info["d8_patterns"] > 0) == (want is not None)
+    _check_d8_structures(p, m)
+    assert_bound(p.execute(m.x), m)
+    g = np.random.default_rng(2)
+    xv = g.integers(-1024, 1025, m.x.size) / 1024.0
+    vv = g.integers(-1024, 1025, m.vals.size) / 1024.0
+    pd = spmv.Plan(m.rowptr, m.colind, vv, n_cols=m.x.size, force_variant="stream", d16=2)
+    assert np.array_equal(pd.execute(xv), oracle.spmv(m.rowptr, m.colind, vv, xv))
